@@ -1,0 +1,197 @@
+/*
+ * ll.h -- C ABI of the B200-native Linear Layouts library (libll_b200.so).
+ *
+ * Linear Layouts (arXiv 2505.23819): a layout is a linear map over F2 from
+ * hardware index bits (reg / lane / warp / block, or a memory "offset") to the
+ * bits of logical tensor coordinates (Definition "Linear Layouts", PAPER.md
+ * P:316-318).  This library builds layouts from per-dimension bases, composes,
+ * inverts and applies them on the host, and converts / gathers device buffers
+ * between layouts with hand-written sm_100a kernels.
+ *
+ * Conventions (readings A1/A2):
+ *   - bit vectors are LSB-first (P:305 footnote);
+ *   - input dims are listed minor -> major; the flattened input index puts the
+ *     first-listed dim at the lowest bits ("reg" lowest);
+ *   - output dims are tensor dims dim0..dimN-1 flattened row-major, last dim
+ *     fastest;
+ *   - a device buffer for layout L holds 2^(sum of L's input bits) elements;
+ *     the element at flattened input index h holds tensor element L(h).
+ *
+ * Errors: every call returns ll_status; LL_OK = 0.  On failure a message is
+ * available from ll_last_error() (thread-local, valid until the next call on
+ * the same thread).  No call aborts the process.
+ *
+ * Ownership: layouts are immutable host objects owned by the caller (destroy
+ * with ll_layout_destroy).  All device memory is owned by the caller.  The
+ * library owns a thread-safe host plan cache and the device constants of each
+ * plan; it never allocates device memory on the conversion path.
+ *
+ * Streams: device work is enqueued on the given stream (a cudaStream_t; NULL
+ * = legacy default stream) with no implicit synchronisation.
+ */
+#ifndef LL_B200_H
+#define LL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ll_layout_s* ll_layout;
+struct CUstream_st;
+typedef struct CUstream_st* ll_stream; /* == cudaStream_t */
+
+typedef enum {
+  LL_OK = 0,
+  LL_ERR_ARG = 1,             /* bad argument (NULL, size, alignment, range)      */
+  LL_ERR_SHAPE = 2,           /* layouts map to different tensors                  */
+  LL_ERR_LABEL = 3,           /* dimension names do not match (compose)            */
+  LL_ERR_NOT_SURJECTIVE = 4,  /* a layout that must be surjective is not           */
+  LL_ERR_NOT_INVERTIBLE = 5,  /* reserved                                           */
+  LL_ERR_RANGE = 6,           /* coordinate out of range                            */
+  LL_ERR_UNSUPPORTED = 7,     /* valid request the library cannot execute           */
+  LL_ERR_CUDA = 8,            /* a CUDA runtime call or launch failed               */
+  LL_ERR_OOM = 9              /* host allocation failed                             */
+} ll_status;
+
+/* ---------------------------------------------------------------- layouts -- */
+
+/* Create a layout from per-dimension bases (Definition "Linear Layouts",
+ * P:316-321; the columns of the matrix as displayed for layout A).
+ *   n_in, in_names[n_in], in_bits[n_in]   input dims, minor -> major (e.g.
+ *                                          "reg","lane","warp","block", or
+ *                                          "offset"); names unique.
+ *   n_out, out_names[n_out], out_bits[n_out]  tensor dims dim0..dimN-1.
+ *   bases  int64 array of shape [sum(in_bits)][n_out]: row k (k-th input bit,
+ *          LSB-first within each input dim, dims in listed order) holds the
+ *          output coordinates of that basis vector; an all-zero row is a zero
+ *          column (broadcast).  Coordinates must be < 2^out_bits[d].
+ *   *out   receives the new layout (caller owns).
+ * Limits: sum(in_bits) <= 62, sum(out_bits) <= 62, n_in, n_out <= 16.
+ * Errors: LL_ERR_ARG (NULL, duplicate names, bits < 0), LL_ERR_RANGE. */
+ll_status ll_layout_create(int n_in, const char* const* in_names, const int* in_bits,
+                           int n_out, const char* const* out_names, const int* out_bits,
+                           const int64_t* bases, ll_layout* out);
+
+ll_status ll_layout_destroy(ll_layout l);
+
+/* Query sizes: numbers of dims and total bits.  Any pointer may be NULL. */
+ll_status ll_layout_info(ll_layout l, int* n_in, int* n_out, int* in_bits_total,
+                         int* out_bits_total);
+
+/* Copy out dim names/bits and bases (same formats as ll_layout_create).
+ * name buffers: names[i] must have room for 32 chars.  bases: capacity
+ * `cap` int64 entries, needs sum(in_bits) * n_out. */
+ll_status ll_layout_get(ll_layout l, char (*in_names)[32], int* in_bits, char (*out_names)[32],
+                        int* out_bits, int64_t* bases, size_t cap);
+
+/* outer o inner (Definition "Composition"): the matrix is the
+ * label-wise product M_outer M_inner.  inner's output dims must equal outer's
+ * input dims as a set of (name, bits) (matched by name).  LL_ERR_LABEL
+ * otherwise. */
+ll_status ll_compose(ll_layout outer, ll_layout inner, ll_layout* out);
+
+/* Right inverse (Definition "Right Inverse"): Gauss-Jordan over
+ * F2, pivots in column order, free (slack) variables zero.  The
+ * result maps the tensor (input dims = l's output dims listed fastest first,
+ * so the flat index is unchanged) to l's input dims (listed major first).
+ * LL_ERR_NOT_SURJECTIVE if l is not surjective. */
+ll_status ll_invert(ll_layout l, ll_layout* out);
+
+/* Label-wise product (Definition "Product"): block-diagonal;
+ * for a shared label a's bits are low, b's high. */
+ll_status ll_product(ll_layout a, ll_layout b, ll_layout* out);
+
+/* Apply to one point ("w = Av"): in_coords[n_in] -> out_coords[n_out].
+ * LL_ERR_RANGE if a coordinate does not fit its dim. */
+ll_status ll_apply(ll_layout l, const int64_t* in_coords, int64_t* out_coords);
+
+/* Predicates: distributed, memory, surjective. */
+ll_status ll_layout_props(ll_layout l, int* surjective, int* distributed, int* memory);
+
+/* ------------------------------------------------------------ conversion -- */
+
+/* Convert a device buffer from layout src_layout (A) to dst_layout (B): the
+ * conversion B^{-1} o A of P:599-611, executed as a pull (A6):
+ *     dst[h] = src[X h],  X = A^{-1} o B  (A^{-1} as in ll_invert),
+ * for every h < 2^(input bits of B).  For distributed / memory layouts X h is
+ * the lowest preimage of B(h) under A.
+ *   src, dst   device pointers (caller-owned, must not overlap), 16-byte aligned
+ *   elem_bits  8, 16, 32 or 64 (elements are moved as raw bits)
+ *   stream     cudaStream_t
+ * Errors: LL_ERR_SHAPE (different tensors), LL_ERR_NOT_SURJECTIVE (A),
+ * LL_ERR_ARG (NULL / misaligned / elem_bits), LL_ERR_CUDA (launch failed). */
+ll_status ll_convert(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
+                     int elem_bits, ll_stream stream);
+
+/* Gather along `axis` (tl.gather): one layout L for src, idx and
+ * out (each a buffer of 2^(input bits of L) elements):
+ *     out[h] = src[h*],  h* = L^{-1}( L(h) with coordinate `axis` := idx[h] ).
+ * idx values must lie in [0, 2^out_bits[axis]); they are not checked on the
+ * device unless the environment variable LL_GATHER_CHECK=1 is set, in which
+ * case out-of-range indices raise LL_ERR_RANGE after a synchronisation. */
+ll_status ll_gather(const void* src, const int32_t* idx, void* out, ll_layout layout, int axis,
+                    int elem_bits, ll_stream stream);
+
+/* ------------------------------------------------------ extended control -- */
+
+typedef enum {
+  LL_PATH_AUTO = 0,      /* planner's choice (cost model)                          */
+  LL_PATH_COPY = 1,      /* identity quotient: plain copy                          */
+  LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle    */
+  LL_PATH_SHUFFLE = 3,   /* warp-local exchange with warp shuffles                 */
+  LL_PATH_GENERIC = 4,   /* element-wise pull (any layouts; the slow baseline)     */
+  LL_PATH_SMEM_NOSWIZZLE = 5 /* smem path with an unswizzled staging buffer (ablation) */
+} ll_path;
+
+typedef struct {
+  int path;          /* ll_path                                                   */
+  int64_t batch;     /* >= 1: buffers hold `batch` consecutive copies of the layout */
+  int max_ctas;      /* 0 = auto; else cap on the persistent grid                  */
+  int reserved[8];
+} ll_convert_options;
+
+/* ll_convert with options (NULL = defaults). */
+ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
+                        int elem_bits, const ll_convert_options* opts, ll_stream stream);
+
+/* Same with gather options (path: AUTO, SHUFFLE, SMEM or GENERIC; batch). */
+ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout layout, int axis,
+                       int elem_bits, const ll_convert_options* opts, ll_stream stream);
+
+/* End-to-end conversion of HOST buffers: src_host/dst_host are host pointers
+ * (pinned for full speed); the library pipelines host->device copies, the
+ * conversion and device->host copies in chunks of whole tiles over two
+ * streams, using the caller's device scratch buffers dev_src/dev_dst of
+ * scratch_bytes each (>= one chunk).  Synchronous: returns when dst_host is
+ * complete. */
+ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_host,
+                          ll_layout dst_layout, int elem_bits, int64_t batch, void* dev_src,
+                          void* dev_dst, size_t scratch_bytes, ll_stream stream);
+
+/* JSON description of the plan the planner builds for (src, dst, elem_bits)
+ * with the given path request: path, tile bits, thread mapping, granule,
+ * swizzle bases, predicted wavefronts, shuffle sets.  Writes at most cap bytes
+ * (NUL-terminated); *needed receives the full length. */
+ll_status ll_plan_describe(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
+                           char* json, size_t cap, size_t* needed);
+
+/* Gather-plan description (same conventions). */
+ll_status ll_gather_describe(ll_layout layout, int axis, int elem_bits, int path, char* json,
+                             size_t cap, size_t* needed);
+
+/* Number of kernel launches issued by this library since load (for the
+ * benchmark's gpu_launches claim). */
+int64_t ll_launch_count(void);
+
+const char* ll_last_error(void);
+
+/* Library version string. */
+const char* ll_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LL_B200_H */

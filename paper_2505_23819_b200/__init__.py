@@ -1,0 +1,17 @@
+"""B200-native Linear Layouts (arXiv 2505.23819): Python binding of libll_b200.so.
+
+A thin ctypes layer over the C ABI declared in ``include/ll.h``: argument
+marshalling only.  Every step of a conversion or gather runs in the library
+(host planner in C++, data movement in sm_100a kernels).  There is no CPU or
+PyTorch fallback: if the shared library is missing the import fails loudly.
+
+    import paper_2505_23819_b200 as ll
+    A = ll.Layout(in_dims, out_dims, bases)       # per-dimension bases
+    ll.convert(src, A, dst, B, elem_bits=16)      # device tensors (torch)
+"""
+
+from ._lib import (LLError, Layout, compose, convert, convert_host, gather, gather_describe,
+                   invert, launch_count, lib_path, plan_describe, product, version, PATHS)
+
+__all__ = ["LLError", "Layout", "compose", "convert", "convert_host", "gather", "gather_describe",
+           "invert", "launch_count", "lib_path", "plan_describe", "product", "version", "PATHS"]

@@ -1,0 +1,258 @@
+"""ctypes binding of libll_b200.so (include/ll.h).  Marshalling only."""
+
+import ctypes
+import json
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libll_b200.so")
+
+if not os.path.exists(lib_path):
+    raise ImportError(
+        "libll_b200.so is not built (%s); run `python -m paper_2505_23819_b200.build` "
+        "or __graft_entry__.build() -- there is no fallback path" % lib_path)
+
+_lib = ctypes.CDLL(lib_path)
+
+_c_int64_p = ctypes.POINTER(ctypes.c_int64)
+_lib.ll_last_error.restype = ctypes.c_char_p
+_lib.ll_version.restype = ctypes.c_char_p
+_lib.ll_launch_count.restype = ctypes.c_int64
+_lib.ll_layout_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                                  ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                  ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_int),
+                                  _c_int64_p, ctypes.POINTER(ctypes.c_void_p)]
+_lib.ll_layout_destroy.argtypes = [ctypes.c_void_p]
+_lib.ll_layout_info.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int)] * 4
+_lib.ll_layout_get.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
+                               ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), _c_int64_p,
+                               ctypes.c_size_t]
+_lib.ll_compose.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+_lib.ll_invert.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+_lib.ll_product.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+_lib.ll_apply.argtypes = [ctypes.c_void_p, _c_int64_p, _c_int64_p]
+_lib.ll_layout_props.argtypes = [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int)] * 3
+_lib.ll_convert.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_int, ctypes.c_void_p]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int), ("batch", ctypes.c_int64), ("max_ctas", ctypes.c_int),
+                ("reserved", ctypes.c_int * 8)]
+
+
+_lib.ll_convert_ex.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(_Opts),
+                               ctypes.c_void_p]
+_lib.ll_gather.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+_lib.ll_gather_ex.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Opts), ctypes.c_void_p]
+_lib.ll_convert_host.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+_lib.ll_plan_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_char_p, ctypes.c_size_t,
+                                  ctypes.POINTER(ctypes.c_size_t)]
+_lib.ll_gather_describe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_char_p, ctypes.c_size_t,
+                                    ctypes.POINTER(ctypes.c_size_t)]
+for _f in ("ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
+           "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
+           "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
+           "ll_gather_describe"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+STATUS = {0: "LL_OK", 1: "LL_ERR_ARG", 2: "LL_ERR_SHAPE", 3: "LL_ERR_LABEL",
+          4: "LL_ERR_NOT_SURJECTIVE", 5: "LL_ERR_NOT_INVERTIBLE", 6: "LL_ERR_RANGE",
+          7: "LL_ERR_UNSUPPORTED", 8: "LL_ERR_CUDA", 9: "LL_ERR_OOM"}
+PATHS = {"auto": 0, "copy": 1, "smem": 2, "shuffle": 3, "generic": 4, "smem_noswizzle": 5}
+
+
+class LLError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+def _check(st):
+    if st != 0:
+        raise LLError(st, _lib.ll_last_error().decode())
+
+
+def version():
+    return _lib.ll_version().decode()
+
+
+def launch_count():
+    return int(_lib.ll_launch_count())
+
+
+class Layout:
+    """Owning handle of an ``ll_layout`` (ll_layout_create / ll_layout_destroy)."""
+
+    def __init__(self, in_dims, out_dims, bases, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+            return
+        in_dims = [(str(n), int(b)) for n, b in in_dims]
+        out_dims = [(str(n), int(b)) for n, b in out_dims]
+        n_in, n_out = len(in_dims), len(out_dims)
+        in_names = (ctypes.c_char_p * max(1, n_in))(*[n.encode() for n, _ in in_dims])
+        in_bits = (ctypes.c_int * max(1, n_in))(*[b for _, b in in_dims])
+        out_names = (ctypes.c_char_p * max(1, n_out))(*[n.encode() for n, _ in out_dims])
+        out_bits = (ctypes.c_int * max(1, n_out))(*[b for _, b in out_dims])
+        flat = []
+        for n, b in in_dims:
+            vecs = bases.get(n, [])
+            if len(vecs) != b:
+                raise LLError(1, "dim %s: %d bases given, %d expected" % (n, len(vecs), b))
+            for v in vecs:
+                if len(v) != n_out:
+                    raise LLError(1, "basis arity mismatch")
+                flat.extend(int(c) for c in v)
+        arr = (ctypes.c_int64 * max(1, len(flat)))(*flat)
+        h = ctypes.c_void_p()
+        _check(_lib.ll_layout_create(n_in, in_names, in_bits, n_out, out_names, out_bits, arr,
+                                     ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_spec(cls, spec):
+        return cls(spec["in_dims"], spec["out_dims"], spec["bases"])
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.ll_layout_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        a, b, c, d = (ctypes.c_int() for _ in range(4))
+        _check(_lib.ll_layout_info(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                   ctypes.byref(d)))
+        return a.value, b.value, c.value, d.value
+
+    @property
+    def in_bits(self):
+        return self.info()[2]
+
+    @property
+    def out_bits(self):
+        return self.info()[3]
+
+    def spec(self):
+        n_in, n_out, tin, _ = self.info()
+        in_names = ((ctypes.c_char * 32) * max(1, n_in))()
+        out_names = ((ctypes.c_char * 32) * max(1, n_out))()
+        in_bits = (ctypes.c_int * max(1, n_in))()
+        out_bits = (ctypes.c_int * max(1, n_out))()
+        bases = (ctypes.c_int64 * max(1, tin * n_out))()
+        _check(_lib.ll_layout_get(self._h, in_names, in_bits, out_names, out_bits, bases,
+                                  max(1, tin * n_out)))
+        ind = [(in_names[i].value.decode(), in_bits[i]) for i in range(n_in)]
+        outd = [(out_names[i].value.decode(), out_bits[i]) for i in range(n_out)]
+        res, k = {}, 0
+        for n, b in ind:
+            res[n] = [tuple(bases[(k + j) * n_out + d] for d in range(n_out)) for j in range(b)]
+            k += b
+        return {"in_dims": ind, "out_dims": outd, "bases": res}
+
+    def apply(self, coords):
+        n_in, n_out, _, _ = self.info()
+        ic = (ctypes.c_int64 * max(1, n_in))(*[int(c) for c in coords])
+        oc = (ctypes.c_int64 * max(1, n_out))()
+        _check(_lib.ll_apply(self._h, ic, oc))
+        return tuple(oc[i] for i in range(n_out))
+
+    def props(self):
+        a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(_lib.ll_layout_props(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return {"surjective": bool(a.value), "distributed": bool(b.value), "memory": bool(c.value)}
+
+
+def _wrap(h):
+    return Layout(None, None, None, _handle=h)
+
+
+def compose(outer, inner):
+    h = ctypes.c_void_p()
+    _check(_lib.ll_compose(outer.handle, inner.handle, ctypes.byref(h)))
+    return _wrap(h)
+
+
+def invert(layout):
+    h = ctypes.c_void_p()
+    _check(_lib.ll_invert(layout.handle, ctypes.byref(h)))
+    return _wrap(h)
+
+
+def product(a, b):
+    h = ctypes.c_void_p()
+    _check(_lib.ll_product(a.handle, b.handle, ctypes.byref(h)))
+    return _wrap(h)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ptr(t):
+    return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+
+
+def _opts(path, batch, max_ctas):
+    o = _Opts()
+    o.path = PATHS[path] if isinstance(path, str) else int(path)
+    o.batch = int(batch)
+    o.max_ctas = int(max_ctas)
+    return o
+
+
+def convert(src, A, dst, B, elem_bits, path="auto", batch=1, max_ctas=0, stream=None):
+    """ll_convert_ex on device tensors (or raw device pointers as ints)."""
+    o = _opts(path, batch, max_ctas)
+    _check(_lib.ll_convert_ex(_ptr(src), A.handle, _ptr(dst), B.handle, int(elem_bits),
+                              ctypes.byref(o), _stream_handle(stream)))
+
+
+def gather(src, idx, out, L, axis, elem_bits, path="auto", batch=1, max_ctas=0, stream=None):
+    o = _opts(path, batch, max_ctas)
+    _check(_lib.ll_gather_ex(_ptr(src), _ptr(idx), _ptr(out), L.handle, int(axis),
+                             int(elem_bits), ctypes.byref(o), _stream_handle(stream)))
+
+
+def convert_host(src_host, A, dst_host, B, elem_bits, batch, dev_src, dev_dst, scratch_bytes,
+                 stream=None):
+    """ll_convert_host: host buffers in, host buffers out (pipelined copies)."""
+    _check(_lib.ll_convert_host(_ptr(src_host), A.handle, _ptr(dst_host), B.handle,
+                                int(elem_bits), int(batch), _ptr(dev_src), _ptr(dev_dst),
+                                int(scratch_bytes), _stream_handle(stream)))
+
+
+def _describe(fn, *args):
+    need = ctypes.c_size_t()
+    _check(fn(*args, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value + 1)
+    _check(fn(*args, buf, need.value + 1, ctypes.byref(need)))
+    return json.loads(buf.value.decode())
+
+
+def plan_describe(A, B, elem_bits, path="auto"):
+    return _describe(_lib.ll_plan_describe, A.handle, B.handle, int(elem_bits),
+                     PATHS[path] if isinstance(path, str) else int(path))
+
+
+def gather_describe(L, axis, elem_bits, path="auto"):
+    return _describe(_lib.ll_gather_describe, L.handle, int(axis), int(elem_bits),
+                     PATHS[path] if isinstance(path, str) else int(path))

@@ -1,0 +1,76 @@
+"""Build libll_b200.so in-tree: nvcc for sm_100a (kernels) + g++ (host core).
+
+    python -m paper_2505_23819_b200.build [--force]
+
+The shared library lands next to this file so that it travels with the repo
+snapshot to the GPU box.  Compilation is incremental on source mtimes.
+"""
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+OUT = os.path.join(HERE, "libll_b200.so")
+BUILD = os.path.join(HERE, "build")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+CU_SOURCES = ["kernels.cu"]
+CPP_SOURCES = ["core.cpp", "planner.cpp", "capi.cpp"]
+HEADERS = ["core.hpp", "plan.hpp", "planner.hpp", "kernels.hpp"]
+
+
+def _mtime(p):
+    return os.path.getmtime(p) if os.path.exists(p) else 0.0
+
+
+def _hdr_mtime():
+    hs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "ll.h")]
+    return max(_mtime(h) for h in hs)
+
+
+def _compile(src, force):
+    s = os.path.join(CSRC, src)
+    o = os.path.join(BUILD, src + ".o")
+    if not force and _mtime(o) > max(_mtime(s), _hdr_mtime()):
+        return o, None
+    if src.endswith(".cu"):
+        cmd = [NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
+               "-Xptxas", "-v", "-c", s, "-o", o]
+    else:
+        cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-I", os.path.join(CUDA, "include"),
+               "-c", s, "-o", o]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("compile failed: %s\n%s\n%s" % (" ".join(cmd), r.stdout, r.stderr))
+    return o, r.stderr
+
+
+def build(force=False, verbose=False):
+    os.makedirs(BUILD, exist_ok=True)
+    srcs = CU_SOURCES + CPP_SOURCES
+    with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        results = list(ex.map(lambda s: _compile(s, force), srcs))
+    objs = [o for o, _ in results]
+    if verbose:
+        for _, log in results:
+            if log:
+                sys.stderr.write(log)
+    if force or not os.path.exists(OUT) or _mtime(OUT) < max(_mtime(o) for o in objs):
+        tmp = OUT + ".tmp"
+        cmd = [NVCC, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs,
+               "-Xlinker", "-soname,libll_b200.so"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("link failed: %s\n%s" % (r.stdout, r.stderr))
+        os.replace(tmp, OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,392 @@
+// capi.cpp -- the extern "C" boundary of libll_b200.so (include/ll.h).
+//
+// Every entry point converts internal ll::Error / std::bad_alloc into an
+// ll_status and a thread-local message; nothing throws across the ABI.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <set>
+#include <string>
+
+#include "core.hpp"
+#include "kernels.hpp"
+#include "planner.hpp"
+
+struct ll_layout_s {
+  ll::Layout L;
+};
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+ll_status fail(ll_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+template <class F>
+ll_status guarded(F&& f) {
+  try {
+    g_err.clear();
+    return f();
+  } catch (const ll::Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(LL_ERR_OOM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(LL_ERR_ARG, e.what());
+  }
+}
+
+ll_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return LL_OK;
+  return fail(LL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int elem_bytes(int elem_bits) {
+  switch (elem_bits) {
+    case 8: return 1;
+    case 16: return 2;
+    case 32: return 4;
+    case 64: return 8;
+  }
+  throw ll::Error(LL_ERR_ARG, "elem_bits must be 8, 16, 32 or 64 (got " + std::to_string(elem_bits) + ")");
+}
+
+ll_layout wrap(ll::Layout&& L) {
+  auto* p = new ll_layout_s;
+  p->L = std::move(L);
+  return p;
+}
+
+void check_layout(ll_layout l, const char* what) {
+  if (!l) throw ll::Error(LL_ERR_ARG, std::string(what) + ": NULL layout");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ll_last_error(void) { return g_err.c_str(); }
+const char* ll_version(void) { return "ll_b200 0.1 (sm_100a)"; }
+int64_t ll_launch_count(void) { return g_launches.load(); }
+
+ll_status ll_layout_create(int n_in, const char* const* in_names, const int* in_bits, int n_out,
+                           const char* const* out_names, const int* out_bits,
+                           const int64_t* bases, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    if (!out) return fail(LL_ERR_ARG, "ll_layout_create: out is NULL");
+    *out = nullptr;
+    if (n_in < 0 || n_out < 0 || n_in > 16 || n_out > 16)
+      return fail(LL_ERR_ARG, "ll_layout_create: n_in / n_out out of range [0, 16]");
+    if ((n_in && (!in_names || !in_bits)) || (n_out && (!out_names || !out_bits)))
+      return fail(LL_ERR_ARG, "ll_layout_create: NULL name or size array");
+    ll::Layout L;
+    std::set<std::string> seen;
+    int tin = 0, tout = 0;
+    for (int i = 0; i < n_in; ++i) {
+      if (!in_names[i] || in_bits[i] < 0) return fail(LL_ERR_ARG, "ll_layout_create: bad input dim");
+      if (!seen.insert(in_names[i]).second)
+        return fail(LL_ERR_ARG, std::string("ll_layout_create: duplicate input dim '") + in_names[i] + "'");
+      L.in.push_back({in_names[i], in_bits[i]});
+      tin += in_bits[i];
+    }
+    seen.clear();
+    for (int i = 0; i < n_out; ++i) {
+      if (!out_names[i] || out_bits[i] < 0) return fail(LL_ERR_ARG, "ll_layout_create: bad output dim");
+      if (!seen.insert(out_names[i]).second)
+        return fail(LL_ERR_ARG, std::string("ll_layout_create: duplicate output dim '") + out_names[i] + "'");
+      L.out.push_back({out_names[i], out_bits[i]});
+      tout += out_bits[i];
+    }
+    if (tin > 62 || tout > 62) return fail(LL_ERR_ARG, "ll_layout_create: more than 62 bits");
+    if (tin && !bases) return fail(LL_ERR_ARG, "ll_layout_create: bases is NULL");
+    std::vector<int64_t> coords(n_out);
+    for (int k = 0; k < tin; ++k) {
+      for (int d = 0; d < n_out; ++d) {
+        int64_t c = bases[(size_t)k * n_out + d];
+        if (c < 0 || (out_bits[d] < 63 && c >= (int64_t(1) << out_bits[d])))
+          return fail(LL_ERR_RANGE, "ll_layout_create: basis " + std::to_string(k) +
+                                        " coordinate " + std::to_string(d) + " out of range");
+        coords[d] = c;
+      }
+      L.cols.push_back(L.flatten(coords));
+    }
+    *out = wrap(std::move(L));
+    return LL_OK;
+  });
+}
+
+ll_status ll_layout_destroy(ll_layout l) {
+  delete l;
+  return LL_OK;
+}
+
+ll_status ll_layout_info(ll_layout l, int* n_in, int* n_out, int* in_bits_total,
+                         int* out_bits_total) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_layout_info");
+    if (n_in) *n_in = (int)l->L.in.size();
+    if (n_out) *n_out = (int)l->L.out.size();
+    if (in_bits_total) *in_bits_total = l->L.in_bits();
+    if (out_bits_total) *out_bits_total = l->L.out_bits();
+    return LL_OK;
+  });
+}
+
+ll_status ll_layout_get(ll_layout l, char (*in_names)[32], int* in_bits, char (*out_names)[32],
+                        int* out_bits, int64_t* bases, size_t cap) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_layout_get");
+    const auto& L = l->L;
+    for (size_t i = 0; i < L.in.size(); ++i) {
+      if (in_names) { std::strncpy(in_names[i], L.in[i].name.c_str(), 31); in_names[i][31] = 0; }
+      if (in_bits) in_bits[i] = L.in[i].bits;
+    }
+    for (size_t i = 0; i < L.out.size(); ++i) {
+      if (out_names) { std::strncpy(out_names[i], L.out[i].name.c_str(), 31); out_names[i][31] = 0; }
+      if (out_bits) out_bits[i] = L.out[i].bits;
+    }
+    if (bases) {
+      if (cap < L.cols.size() * L.out.size()) return fail(LL_ERR_ARG, "ll_layout_get: bases too small");
+      for (size_t k = 0; k < L.cols.size(); ++k) {
+        auto c = L.unflatten(L.cols[k]);
+        for (size_t d = 0; d < L.out.size(); ++d) bases[k * L.out.size() + d] = c[d];
+      }
+    }
+    return LL_OK;
+  });
+}
+
+ll_status ll_compose(ll_layout outer, ll_layout inner, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(outer, "ll_compose");
+    check_layout(inner, "ll_compose");
+    if (!out) return fail(LL_ERR_ARG, "ll_compose: out is NULL");
+    *out = wrap(ll::compose(outer->L, inner->L));
+    return LL_OK;
+  });
+}
+
+ll_status ll_invert(ll_layout l, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_invert");
+    if (!out) return fail(LL_ERR_ARG, "ll_invert: out is NULL");
+    *out = wrap(ll::right_inverse(l->L));
+    return LL_OK;
+  });
+}
+
+ll_status ll_product(ll_layout a, ll_layout b, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(a, "ll_product");
+    check_layout(b, "ll_product");
+    if (!out) return fail(LL_ERR_ARG, "ll_product: out is NULL");
+    *out = wrap(ll::product(a->L, b->L));
+    return LL_OK;
+  });
+}
+
+ll_status ll_apply(ll_layout l, const int64_t* in_coords, int64_t* out_coords) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_apply");
+    const auto& L = l->L;
+    if ((!in_coords && !L.in.empty()) || (!out_coords && !L.out.empty()))
+      return fail(LL_ERR_ARG, "ll_apply: NULL coordinates");
+    ll::u64 h = 0;
+    int off = 0;
+    for (size_t i = 0; i < L.in.size(); ++i) {
+      int64_t c = in_coords[i];
+      if (c < 0 || c >= (int64_t(1) << L.in[i].bits))
+        return fail(LL_ERR_RANGE, "ll_apply: coordinate of '" + L.in[i].name + "' out of range");
+      h |= ll::u64(c) << off;
+      off += L.in[i].bits;
+    }
+    auto o = L.unflatten(ll::f2_apply(L.cols, h));
+    for (size_t d = 0; d < L.out.size(); ++d) out_coords[d] = o[d];
+    return LL_OK;
+  });
+}
+
+ll_status ll_layout_props(ll_layout l, int* surjective, int* distributed, int* memory) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_layout_props");
+    if (surjective) *surjective = l->L.surjective();
+    if (distributed) *distributed = l->L.distributed();
+    if (memory) *memory = l->L.memory();
+    return LL_OK;
+  });
+}
+
+ll_status ll_plan_describe(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
+                           char* json, size_t cap, size_t* needed) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_plan_describe");
+    check_layout(dst_layout, "ll_plan_describe");
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, elem_bytes(elem_bits), path, 1);
+    if (needed) *needed = P->json.size() + 1;
+    if (json && cap) {
+      std::strncpy(json, P->json.c_str(), cap - 1);
+      json[cap - 1] = 0;
+    }
+    return LL_OK;
+  });
+}
+
+ll_status ll_gather_describe(ll_layout layout, int axis, int elem_bits, int path, char* json,
+                             size_t cap, size_t* needed) {
+  return guarded([&]() -> ll_status {
+    check_layout(layout, "ll_gather_describe");
+    auto P = ll::get_gather_plan(layout->L, axis, elem_bytes(elem_bits), path, 1);
+    if (needed) *needed = P->json.size() + 1;
+    if (json && cap) {
+      std::strncpy(json, P->json.c_str(), cap - 1);
+      json[cap - 1] = 0;
+    }
+    return LL_OK;
+  });
+}
+
+ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
+                        int elem_bits, const ll_convert_options* opts, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_convert");
+    check_layout(dst_layout, "ll_convert");
+    const int w = elem_bytes(elem_bits);
+    const int path_req = opts ? opts->path : LL_PATH_AUTO;
+    const int64_t batch = opts && opts->batch > 0 ? opts->batch : 1;
+    const int max_ctas = opts ? opts->max_ctas : 0;
+    if (!src || !dst) return fail(LL_ERR_ARG, "ll_convert: NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+      return fail(LL_ERR_ARG, "ll_convert: buffers must be 16-byte aligned");
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, path_req, batch);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t dst_bytes = (size_t)w << P->nB;
+    switch (P->path) {
+      case LL_PATH_COPY:
+        ++g_launches;
+        return cuda_status(cudaMemcpyAsync(dst, src, dst_bytes * batch, cudaMemcpyDeviceToDevice, st),
+                           "ll_convert (copy)");
+      case LL_PATH_SMEM:
+      case LL_PATH_SMEM_NOSWIZZLE:
+        ++g_launches;
+        return cuda_status(ll::launch_convert_smem(P->sp, w, P->nv, P->g, src, dst, max_ctas, st),
+                           "ll_convert (smem kernel)");
+      default:
+        ++g_launches;
+        return cuda_status(ll::launch_convert_generic(P->gp, w, src, dst, max_ctas, st),
+                           "ll_convert (generic kernel)");
+    }
+  });
+}
+
+ll_status ll_convert(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
+                     int elem_bits, ll_stream stream) {
+  return ll_convert_ex(src, src_layout, dst, dst_layout, elem_bits, nullptr, stream);
+}
+
+ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout layout, int axis,
+                       int elem_bits, const ll_convert_options* opts, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(layout, "ll_gather");
+    const int w = elem_bytes(elem_bits);
+    if (!src || !idx || !out) return fail(LL_ERR_ARG, "ll_gather: NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(idx) |
+         reinterpret_cast<uintptr_t>(out)) & 15)
+      return fail(LL_ERR_ARG, "ll_gather: buffers must be 16-byte aligned");
+    const int path_req = opts ? opts->path : LL_PATH_AUTO;
+    const int64_t batch = opts && opts->batch > 0 ? opts->batch : 1;
+    const int max_ctas = opts ? opts->max_ctas : 0;
+    auto P = ll::get_gather_plan(layout->L, axis, w, path_req, batch);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const char* chk = std::getenv("LL_GATHER_CHECK");
+    const bool check = chk && chk[0] == '1';
+    int* derr = nullptr;
+    ll::GatherPlan gp = P->gp;
+    if (check) {
+      if (cudaMalloc(&derr, sizeof(int)) != cudaSuccess) return fail(LL_ERR_CUDA, "ll_gather: cudaMalloc");
+      cudaMemsetAsync(derr, 0, sizeof(int), st);
+      gp.check = 1;
+    }
+    ++g_launches;
+    ll_status s = cuda_status(
+        ll::launch_gather(gp, w, P->path == LL_PATH_SHUFFLE, src, idx, out, derr, max_ctas, st),
+        "ll_gather");
+    if (check) {
+      int h = 0;
+      cudaMemcpyAsync(&h, derr, sizeof(int), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFree(derr);
+      if (s == LL_OK && h) return fail(LL_ERR_RANGE, "ll_gather: index out of range");
+    }
+    return s;
+  });
+}
+
+ll_status ll_gather(const void* src, const int32_t* idx, void* out, ll_layout layout, int axis,
+                    int elem_bits, ll_stream stream) {
+  return ll_gather_ex(src, idx, out, layout, axis, elem_bits, nullptr, stream);
+}
+
+ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_host,
+                          ll_layout dst_layout, int elem_bits, int64_t batch, void* dev_src,
+                          void* dev_dst, size_t scratch_bytes, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_convert_host");
+    check_layout(dst_layout, "ll_convert_host");
+    const int w = elem_bytes(elem_bits);
+    if (!src_host || !dst_host || !dev_src || !dev_dst)
+      return fail(LL_ERR_ARG, "ll_convert_host: NULL buffer");
+    if (batch < 1) batch = 1;
+    const size_t sb = (size_t)w << src_layout->L.in_bits();
+    const size_t db = (size_t)w << dst_layout->L.in_bits();
+    const size_t unit = sb > db ? sb : db;
+    if (scratch_bytes < unit)
+      return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one layout instance");
+    // chunk = whole layout instances (batch elements); two halves of the
+    // scratch alternate so that copies of chunk i+1 overlap the kernel of i.
+    int64_t per_chunk = (int64_t)((scratch_bytes / 2) / unit);
+    if (per_chunk < 1) per_chunk = 1;
+    const bool dbl = (size_t)per_chunk * unit * 2 <= scratch_bytes;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaStream_t cs[2];
+    cudaEvent_t done[2];
+    for (int i = 0; i < 2; ++i) {
+      cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+    }
+    ll_status s = LL_OK;
+    int64_t chunk = 0;
+    for (int64_t b0 = 0; b0 < batch && s == LL_OK; b0 += per_chunk, ++chunk) {
+      const int64_t nb = std::min<int64_t>(per_chunk, batch - b0);
+      const int slot = dbl ? (int)(chunk & 1) : 0;
+      cudaStream_t c = cs[slot];
+      char* ds = (char*)dev_src + (size_t)slot * per_chunk * sb;
+      char* dd = (char*)dev_dst + (size_t)slot * per_chunk * db;
+      cudaMemcpyAsync(ds, (const char*)src_host + b0 * sb, nb * sb, cudaMemcpyHostToDevice, c);
+      ll_convert_options o{};
+      o.path = LL_PATH_AUTO;
+      o.batch = nb;
+      s = ll_convert_ex(ds, src_layout, dd, dst_layout, elem_bits, &o, (ll_stream)c);
+      cudaMemcpyAsync((char*)dst_host + b0 * db, dd, nb * db, cudaMemcpyDeviceToHost, c);
+    }
+    for (int i = 0; i < 2; ++i) {
+      cudaEventRecord(done[i], cs[i]);
+      cudaStreamWaitEvent(st, done[i], 0);
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(done[i]);
+      cudaStreamDestroy(cs[i]);
+    }
+    if (s != LL_OK) return s;
+    return cuda_status(e, "ll_convert_host");
+  });
+}
+
+}  // extern "C"

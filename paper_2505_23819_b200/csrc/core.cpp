@@ -1,0 +1,222 @@
+// core.cpp -- F2 algebra and labeled layouts (host).  See core.hpp.
+#include "core.hpp"
+
+#include <algorithm>
+#include <map>
+
+namespace ll {
+
+std::vector<u64> f2_right_inverse(const std::vector<u64>& cols, int m) {
+  const int n = (int)cols.size();
+  if (m > 63 || n > 63) throw Error(LL_ERR_ARG, "right inverse: more than 63 bits");
+  // rows of M as n-bit ints, augmented with I_m
+  std::vector<u64> rows(m, 0), aug(m, 0);
+  for (int r = 0; r < m; ++r) {
+    aug[r] = u64(1) << r;
+    for (int j = 0; j < n; ++j)
+      if ((cols[j] >> r) & 1) rows[r] |= u64(1) << j;
+  }
+  std::vector<int> pivcol;
+  int p = 0;
+  for (int j = 0; j < n && p < m; ++j) {
+    int sel = -1;
+    for (int r = p; r < m; ++r)
+      if ((rows[r] >> j) & 1) { sel = r; break; }
+    if (sel < 0) continue;
+    std::swap(rows[p], rows[sel]);
+    std::swap(aug[p], aug[sel]);
+    for (int q = 0; q < m; ++q)
+      if (q != p && ((rows[q] >> j) & 1)) { rows[q] ^= rows[p]; aug[q] ^= aug[p]; }
+    pivcol.push_back(j);
+    ++p;
+  }
+  if (p < m)
+    throw Error(LL_ERR_NOT_SURJECTIVE, "layout is not surjective (rank " + std::to_string(p) +
+                                           " < " + std::to_string(m) + " output bits)");
+  std::vector<u64> x(m, 0);
+  for (int c = 0; c < m; ++c)
+    for (int i = 0; i < (int)pivcol.size(); ++i)
+      if ((aug[i] >> c) & 1) x[c] |= u64(1) << pivcol[i];
+  return x;
+}
+
+std::vector<u64> f2_complete(const std::vector<u64>& vecs, int d) {
+  F2Basis b;
+  for (u64 v : vecs)
+    if (!b.add(v)) throw Error(LL_ERR_ARG, "basis completion: dependent input");
+  std::vector<u64> out;
+  for (int k = 0; k < d && b.n < d; ++k)
+    if (b.add(u64(1) << k)) out.push_back(u64(1) << k);
+  return out;
+}
+
+int Layout::in_bits() const {
+  int s = 0;
+  for (auto& d : in) s += d.bits;
+  return s;
+}
+int Layout::out_bits() const {
+  int s = 0;
+  for (auto& d : out) s += d.bits;
+  return s;
+}
+int Layout::in_offset(const std::string& name) const {
+  int off = 0;
+  for (auto& d : in) {
+    if (d.name == name) return off;
+    off += d.bits;
+  }
+  return -1;
+}
+int Layout::in_size(const std::string& name) const {
+  for (auto& d : in)
+    if (d.name == name) return d.bits;
+  return 0;
+}
+int Layout::out_index(const std::string& name) const {
+  for (size_t i = 0; i < out.size(); ++i)
+    if (out[i].name == name) return (int)i;
+  return -1;
+}
+int Layout::out_shift(int d) const {
+  int s = 0;
+  for (size_t i = d + 1; i < out.size(); ++i) s += out[i].bits;
+  return s;
+}
+std::vector<u64> Layout::sub(const std::string& name) const {
+  int off = in_offset(name);
+  if (off < 0) return {};
+  return std::vector<u64>(cols.begin() + off, cols.begin() + off + in_size(name));
+}
+u64 Layout::flatten(const std::vector<int64_t>& c) const {
+  u64 x = 0;
+  for (size_t d = 0; d < out.size(); ++d) x |= u64(c[d]) << out_shift((int)d);
+  return x;
+}
+std::vector<int64_t> Layout::unflatten(u64 x) const {
+  std::vector<int64_t> c(out.size());
+  for (size_t d = 0; d < out.size(); ++d)
+    c[d] = (int64_t)((x >> out_shift((int)d)) & ((u64(1) << out[d].bits) - 1));
+  return c;
+}
+bool Layout::surjective() const { return f2_rank(cols) == out_bits(); }
+bool Layout::distributed() const {
+  // Definition "Distributed Layout"
+  for (auto& d : in)
+    if (d.name != "reg" && d.name != "lane" && d.name != "thread" && d.name != "warp" &&
+        d.name != "block")
+      return false;
+  std::vector<u64> nz;
+  for (u64 c : cols) {
+    if (popcount64(c) > 1) return false;
+    if (c) nz.push_back(c);
+  }
+  std::sort(nz.begin(), nz.end());
+  if (std::adjacent_find(nz.begin(), nz.end()) != nz.end()) return false;
+  return surjective();
+}
+bool Layout::memory() const {
+  // Definition "Memory Layout"
+  if (in.size() != 1 || in[0].name != "offset") return false;
+  if ((int)cols.size() != out_bits() || f2_rank(cols) != out_bits()) return false;
+  for (u64 c : cols)
+    if (popcount64(c) < 1 || popcount64(c) > 2) return false;
+  return true;
+}
+u64 Layout::hash() const {
+  u64 h = 0xcbf29ce484222325ull;
+  auto mix = [&](u64 v) {
+    h ^= v;
+    h *= 0x100000001b3ull;
+    h ^= h >> 29;
+  };
+  for (auto& d : in) {
+    for (char ch : d.name) mix((u64)(unsigned char)ch);
+    mix(0x100 + d.bits);
+  }
+  mix(0xabcdef);
+  for (auto& d : out) {
+    for (char ch : d.name) mix((u64)(unsigned char)ch);
+    mix(0x200 + d.bits);
+  }
+  for (u64 c : cols) mix(c);
+  return h;
+}
+bool Layout::same_tensor(const Layout& o) const {
+  if (out.size() != o.out.size()) return false;
+  for (size_t i = 0; i < out.size(); ++i)
+    if (out[i].name != o.out[i].name || out[i].bits != o.out[i].bits) return false;
+  return true;
+}
+
+Layout compose(const Layout& outer, const Layout& inner) {
+  // Definition "Composition": label-wise product, matched by name.
+  if (outer.in.size() != inner.out.size())
+    throw Error(LL_ERR_LABEL, "compose: inner has " + std::to_string(inner.out.size()) +
+                                  " output dims, outer has " + std::to_string(outer.in.size()) +
+                                  " input dims");
+  for (auto& d : inner.out)
+    if (outer.in_size(d.name) != d.bits || outer.in_offset(d.name) < 0)
+      throw Error(LL_ERR_LABEL, "compose: inner output dim '" + d.name +
+                                    "' does not match an outer input dim of the same size");
+  Layout r;
+  r.in = inner.in;
+  r.out = outer.out;
+  for (u64 c : inner.cols) {
+    auto coords = inner.unflatten(c);
+    u64 h = 0;
+    for (size_t d = 0; d < inner.out.size(); ++d)
+      h |= u64(coords[d]) << outer.in_offset(inner.out[d].name);
+    r.cols.push_back(f2_apply(outer.cols, h));
+  }
+  return r;
+}
+
+Layout right_inverse(const Layout& l) {
+  Layout r;
+  r.cols = f2_right_inverse(l.cols, l.out_bits());
+  r.in.assign(l.out.rbegin(), l.out.rend());
+  r.out.assign(l.in.rbegin(), l.in.rend());
+  return r;
+}
+
+Layout product(const Layout& a, const Layout& b) {
+  // Definition "Product": label-wise block diagonal, a low / b high.
+  Layout r;
+  r.in = a.in;
+  for (auto& d : b.in) {
+    bool found = false;
+    for (auto& e : r.in)
+      if (e.name == d.name) { e.bits += d.bits; found = true; }
+    if (!found) r.in.push_back(d);
+  }
+  r.out = a.out;
+  for (auto& d : b.out) {
+    bool found = false;
+    for (auto& e : r.out)
+      if (e.name == d.name) { e.bits += d.bits; found = true; }
+    if (!found) r.out.push_back(d);
+  }
+  if (r.in_bits() > 62 || r.out_bits() > 62) throw Error(LL_ERR_ARG, "product: too many bits");
+  auto embed = [&](const Layout& src, u64 c, bool high) {
+    auto coords = src.unflatten(c);
+    std::vector<int64_t> rc(r.out.size(), 0);
+    for (size_t d = 0; d < src.out.size(); ++d) {
+      int idx = r.out_index(src.out[d].name);
+      int shift = high ? std::max(0, a.out_index(src.out[d].name) >= 0
+                                         ? a.out[a.out_index(src.out[d].name)].bits
+                                         : 0)
+                       : 0;
+      rc[idx] = coords[d] << shift;
+    }
+    return r.flatten(rc);
+  };
+  for (auto& d : r.in) {
+    auto av = a.sub(d.name), bv = b.sub(d.name);
+    for (u64 c : av) r.cols.push_back(embed(a, c, false));
+    for (u64 c : bv) r.cols.push_back(embed(b, c, true));
+  }
+  return r;
+}
+
+}  // namespace ll

@@ -1,0 +1,529 @@
+// kernels.cu -- sm_100a kernels for layout conversion and gather.
+//
+// Pure data movement: no tensor cores (no dense contraction on this path).
+// Every kernel is persistent-style (grid sized from the SM count, loop over
+// work items) and moves HBM data with 128-bit coalesced loads / stores.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace ll {
+
+// ------------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void stg_stream(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+template <int G>
+__device__ __forceinline__ void sts(uint32_t addr, const uint32_t* r) {
+  if constexpr (G == 16)
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3])
+                 : "memory");
+  else if constexpr (G == 8)
+    asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(addr), "r"(r[0]), "r"(r[1]) : "memory");
+  else
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(r[0]) : "memory");
+}
+
+template <int G>
+__device__ __forceinline__ void lds(uint32_t addr, uint32_t* r) {
+  if constexpr (G == 16)
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr)
+                 : "memory");
+  else if constexpr (G == 8)
+    asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr) : "memory");
+  else
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r[0]) : "r"(addr) : "memory");
+}
+
+__device__ __forceinline__ void group_sync(int gw, int group) {
+  if (gw == 0) {
+    __syncwarp();
+  } else {
+    // named barrier per tile group (id 0 is __syncthreads)
+    asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(32 << gw) : "memory");
+  }
+}
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+// ----------------------------------------------------------- register-bit swaps
+//
+// The thread's register file R[] holds 2^r elements of W bytes in element
+// order rho.  swap(a, b) exchanges element-index bits a < b.  Word-level
+// bits are register renames; a sub-word bit against a word bit is a 2x2
+// transpose with prmt (byte permute, the FlashAttention-3 trick of P:62).
+// (a, b) are warp-uniform plan data; every case below is unrolled with
+// compile-time register indices so R[] stays in registers.
+
+template <int NW>
+__device__ __forceinline__ void swap_word_bits(uint32_t (&R)[NW], int a, int b) {
+  constexpr int LB = ilog2(NW);
+#pragma unroll
+  for (int A = 0; A < LB; ++A) {
+#pragma unroll
+    for (int B = A + 1; B < LB; ++B) {
+      if (a == A && b == B) {
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          if (((i >> A) & 1) == 0 && ((i >> B) & 1) == 1) {
+            const int j = i ^ ((1 << A) | (1 << B));
+            uint32_t t = R[i];
+            R[i] = R[j];
+            R[j] = t;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int NW>
+__device__ __forceinline__ void swap_sub_word(uint32_t (&R)[NW], int wb, uint32_t sel_lo,
+                                              uint32_t sel_hi) {
+  constexpr int LB = ilog2(NW);
+#pragma unroll
+  for (int B = 0; B < LB; ++B) {
+    if (wb == B) {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        if (((i >> B) & 1) == 0) {
+          const int j = i | (1 << B);
+          uint32_t lo = prmt(R[i], R[j], sel_lo);
+          uint32_t hi = prmt(R[i], R[j], sel_hi);
+          R[i] = lo;
+          R[j] = hi;
+        }
+      }
+    }
+  }
+}
+
+template <int W, int NW>
+__device__ __forceinline__ void apply_swap(uint32_t (&R)[NW], int a, int b) {
+  if constexpr (W == 8) {
+    swap_word_bits<NW>(R, a + 1, b + 1);
+  } else if constexpr (W == 4) {
+    swap_word_bits<NW>(R, a, b);
+  } else if constexpr (W == 2) {
+    if (a == 0)
+      swap_sub_word<NW>(R, b - 1, 0x5410u, 0x7632u);
+    else
+      swap_word_bits<NW>(R, a - 1, b - 1);
+  } else {  // W == 1
+    if (a == 0 && b == 1) {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) R[i] = prmt(R[i], 0u, 0x3120u);
+    } else if (a == 0) {
+      swap_sub_word<NW>(R, b - 2, 0x6240u, 0x7351u);
+    } else if (a == 1) {
+      swap_sub_word<NW>(R, b - 2, 0x5410u, 0x7632u);
+    } else {
+      swap_word_bits<NW>(R, a - 2, b - 2);
+    }
+  }
+}
+
+// ------------------------------------------------------------- smem kernel
+
+// W: element bytes; NV: 16-byte vectors per thread per side; G: granule bytes.
+template <int W, int NV, int G>
+__global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
+                                                           const uint8_t* __restrict__ src,
+                                                           uint8_t* __restrict__ dst) {
+  constexpr int NW = NV * 4;          // 32-bit words per thread
+  constexpr int NG = NV * 16 / G;     // granules per thread
+  constexpr int GW = G / 4;           // words per granule
+  extern __shared__ __align__(16) uint8_t smem[];
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gw = p.gw;
+  const int group = warp >> gw;
+  const int tb = lane | ((warp & ((1 << gw) - 1)) << 5);
+  const int groups_per_cta = (blockDim.x >> 5) >> gw;
+  const int tbits = 5 + gw;
+
+  int64_t ld_off = 0, st_off = 0;
+  uint32_t swx = 0, srx = 0;
+#pragma unroll
+  for (int b = 0; b < LL_MAX_TBITS; ++b) {
+    if (b < tbits && ((tb >> b) & 1)) {
+      ld_off += p.ld_thr[b];
+      st_off += p.st_thr[b];
+      swx ^= (uint32_t)p.sw_thr[b];
+      srx ^= (uint32_t)p.sr_thr[b];
+    }
+  }
+  const uint32_t tile_bytes = (uint32_t)p.tile_elems * W;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * tile_bytes;
+  uint32_t waddr[NG], raddr[NG];
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    waddr[j] = sbase + (swx ^ (uint32_t)p.sw_gran[j]) * W;
+    raddr[j] = sbase + (srx ^ (uint32_t)p.sr_gran[j]) * W;
+  }
+
+  const int64_t stride = (int64_t)gridDim.x * groups_per_cta;
+  uint32_t buf = 0;
+  for (int64_t t = (int64_t)blockIdx.x * groups_per_cta + group; t < p.tile.n_tiles; t += stride) {
+    int64_t sb, db;
+    tile_bases(p.tile, t, sb, db);
+    uint32_t R[NW];
+    const uint8_t* sp = src + (sb + ld_off) * W;
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      uint4 v = ldg_stream(sp + p.ld_vec[u] * W);
+      R[4 * u + 0] = v.x;
+      R[4 * u + 1] = v.y;
+      R[4 * u + 2] = v.z;
+      R[4 * u + 3] = v.w;
+    }
+    for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
+#pragma unroll
+    for (int j = 0; j < NG; ++j) sts<G>(waddr[j] + buf, &R[j * GW]);
+    group_sync(gw, group);
+#pragma unroll
+    for (int j = 0; j < NG; ++j) lds<G>(raddr[j] + buf, &R[j * GW]);
+    uint8_t* dp = dst + (db + st_off) * W;
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+      stg_stream(dp + p.st_vec[u] * W,
+                 make_uint4(R[4 * u + 0], R[4 * u + 1], R[4 * u + 2], R[4 * u + 3]));
+    buf ^= tile_bytes;
+  }
+}
+
+// ------------------------------------------------------------ generic kernel
+
+// dst[h] = src[X h]: each thread writes one 16-byte destination vector; the
+// source elements are fetched one by one (the slow, always-applicable path).
+template <int W>
+__global__ void __launch_bounds__(256) convert_generic_kernel(const __grid_constant__ GenericPlan p,
+                                                              const uint8_t* __restrict__ src,
+                                                              uint8_t* __restrict__ dst) {
+  constexpr int NE = 16 / W;
+  constexpr int VB = ilog2(NE);
+  using T = typename std::conditional<W == 1, uint8_t,
+            typename std::conditional<W == 2, uint16_t,
+            typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
+  const int64_t per_batch = (p.nB >= VB) ? (int64_t(1) << (p.nB - VB)) : 1;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n_vec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = v / per_batch;
+    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    uint64_t x0 = 0;
+    for (int k = VB; k < p.nB; ++k)
+      if ((h0 >> k) & 1) x0 ^= (uint64_t)p.x[k];
+    const T* s = reinterpret_cast<const T*>(src) + b * p.batch_stride_src;
+    T* d = reinterpret_cast<T*>(dst) + b * p.batch_stride_dst + h0;
+    union {
+      uint4 v4;
+      T e[NE];
+    } out;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      uint64_t x = x0;
+#pragma unroll
+      for (int k = 0; k < VB; ++k)
+        if ((e >> k) & 1) x ^= (uint64_t)p.x[k];
+      out.e[e] = (e < (1 << (p.nB < VB ? p.nB : VB))) ? __ldg(s + x) : T(0);
+    }
+    if (p.nB >= VB) {
+      *reinterpret_cast<uint4*>(d) = out.v4;
+    } else {
+      for (int e = 0; e < (1 << p.nB); ++e) d[e] = out.e[e];
+    }
+  }
+}
+
+// ------------------------------------------------------------ gather kernels
+
+// Direct gather: each thread produces one 16-byte output vector; source
+// elements are read through L1 (the rows a warp gathers from are the rows it
+// covers, so L1 absorbs the reuse).  Works for any axis placement.
+template <int W>
+__global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constant__ GatherPlan p,
+                                                            const uint8_t* __restrict__ src,
+                                                            const int32_t* __restrict__ idx,
+                                                            uint8_t* __restrict__ out,
+                                                            int* __restrict__ err) {
+  constexpr int NE = 16 / W;
+  constexpr int VB = ilog2(NE);
+  using T = typename std::conditional<W == 1, uint8_t,
+            typename std::conditional<W == 2, uint16_t,
+            typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
+  const int64_t per_batch = int64_t(1) << (p.nbits - VB);
+  const uint32_t amask = (1u << p.ax_bits) - 1;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n_vec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = v / per_batch;
+    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    const T* s = reinterpret_cast<const T*>(src) + b * p.batch_stride;
+    const int32_t* ip = idx + b * p.batch_stride + h0;
+    int32_t iv[NE];
+    if constexpr (NE >= 4) {
+#pragma unroll
+      for (int q = 0; q < NE / 4; ++q) {
+        int4 t = __ldg(reinterpret_cast<const int4*>(ip) + q);
+        iv[4 * q] = t.x; iv[4 * q + 1] = t.y; iv[4 * q + 2] = t.z; iv[4 * q + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NE; ++q) iv[q] = __ldg(ip + q);
+    }
+    union {
+      uint4 v4;
+      T e[NE];
+    } o;
+    // axis coordinate of h0's elements and the "cleared" base
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const uint64_t h = h0 | (uint64_t)e;
+      uint64_t hs;
+      uint32_t i = (uint32_t)iv[e];
+      if (p.check && i > amask) atomicExch(err, 1);
+      i &= amask;
+      if (p.y_contig) {
+        hs = (h & ~(uint64_t)p.axis_mask_buf) | ((uint64_t)i << p.y_base);
+      } else {
+        // h* = h ^ Y(axis(h) ^ idx)
+        uint64_t t = 0;
+        for (int k = 0; k < p.nbits; ++k)
+          if ((h >> k) & 1) t ^= (uint64_t)p.L[k];
+        uint32_t a = (uint32_t)(t >> p.ax_shift) & amask;
+        uint32_t dlt = a ^ i;
+        hs = h;
+        for (int k = 0; k < p.ax_bits; ++k)
+          if ((dlt >> k) & 1) hs ^= (uint64_t)p.Y[k];
+      }
+      o.e[e] = __ldg(s + hs);
+    }
+    *reinterpret_cast<uint4*>(reinterpret_cast<T*>(out) + b * p.batch_stride + h0) = o.v4;
+  }
+}
+
+// Warp-shuffle gather (reading A19): each lane holds one 16-byte
+// vector of src (registers = the vector's elements, lanes = the next five
+// buffer bits).  For each output element the source (register, lane) comes
+// from h* = (h with axis replaced); one shuffle per candidate register
+// (2^|L_reg^axis|, mask `cand_mask`), keeping the value whose register
+// matches.  Requires the axis to live in the warp's buffer bits (vb + 5).
+template <int W>
+__global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_constant__ GatherPlan p,
+                                                             const uint8_t* __restrict__ src,
+                                                             const int32_t* __restrict__ idx,
+                                                             uint8_t* __restrict__ out,
+                                                             int* __restrict__ err) {
+  constexpr int NE = 16 / W;
+  constexpr int VB = ilog2(NE);
+  using T = typename std::conditional<W == 1, uint8_t,
+            typename std::conditional<W == 2, uint16_t,
+            typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t per_batch = int64_t(1) << (p.nbits - VB);
+  const uint32_t amask = (1u << p.ax_bits) - 1;
+  const int64_t nwarps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_wvec = p.n_vec >> 5;  // warps' worth of vectors
+  for (int64_t wv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wv < n_wvec;
+       wv += nwarps_total) {
+    const int64_t v = (wv << 5) | lane;
+    const int64_t b = v / per_batch;
+    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    const uint8_t* sbase = src + (b * p.batch_stride) * W;
+    union {
+      uint4 v4;
+      T e[NE];
+      uint32_t w[4];
+    } sv, o;
+    sv.v4 = ldg_stream(sbase + h0 * W);
+    const int32_t* ip = idx + b * p.batch_stride + h0;
+    int32_t iv[NE];
+    if constexpr (NE >= 4) {
+#pragma unroll
+      for (int q = 0; q < NE / 4; ++q) {
+        int4 t = __ldg(reinterpret_cast<const int4*>(ip) + q);
+        iv[4 * q] = t.x; iv[4 * q + 1] = t.y; iv[4 * q + 2] = t.z; iv[4 * q + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NE; ++q) iv[q] = __ldg(ip + q);
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const uint64_t h = h0 | (uint64_t)e;
+      uint32_t i = (uint32_t)iv[e];
+      if (p.check && i > amask) atomicExch(err, 1);
+      i &= amask;
+      uint64_t hs = (h & ~(uint64_t)p.axis_mask_buf) | ((uint64_t)i << p.y_base);
+      const int src_lane = (int)((hs >> VB) & 31);
+      const int src_reg = (int)(hs & (NE - 1));
+      T val = 0;
+      // candidate rounds: every register index the axis can select, i.e. the
+      // registers that agree with e outside cand_mask (2^|L_reg^axis| shuffles)
+#pragma unroll
+      for (int c = 0; c < NE; ++c) {
+        if (((c ^ e) & ~p.cand_mask) == 0) {
+          T got;
+          if constexpr (W == 8) {
+            uint32_t lo = __shfl_sync(0xffffffffu, sv.w[2 * c], src_lane);
+            uint32_t hi = __shfl_sync(0xffffffffu, sv.w[2 * c + 1], src_lane);
+            got = (T)(((uint64_t)hi << 32) | lo);
+          } else if constexpr (W == 4) {
+            got = (T)__shfl_sync(0xffffffffu, sv.w[c], src_lane);
+          } else {
+            // sub-word elements: shuffle the containing word, then extract
+            uint32_t wd = __shfl_sync(0xffffffffu, sv.w[(c * W) >> 2], src_lane);
+            got = (T)(wd >> (((c * W) & 3) * 8));
+          }
+          if (src_reg == c) val = got;
+        }
+      }
+      o.e[e] = val;
+    }
+    stg_stream(out + (b * p.batch_stride + h0) * W, o.v4);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int W, int NV, int G>
+static cudaError_t launch_smem_t(const SmemPlan& p, const void* src, void* dst, int max_ctas,
+                                 cudaStream_t st) {
+  auto k = convert_smem_kernel<W, NV, G>;
+  const int threads = 256;
+  const int groups = (threads / 32) >> p.gw;
+  const size_t smem = (size_t)groups * 2 * p.tile_elems * W;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
+  if (occ <= 0) return cudaErrorInvalidConfiguration;
+  int64_t want = (p.tile.n_tiles + groups - 1) / groups;
+  int64_t cap = (int64_t)occ * num_sms();
+  if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
+  int grid = (int)(want < cap ? want : cap);
+  if (grid < 1) grid = 1;
+  k<<<grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst);
+  return cudaGetLastError();
+}
+
+template <int W>
+static cudaError_t launch_smem_w(const SmemPlan& p, int nv, int g, const void* src, void* dst,
+                                 int max_ctas, cudaStream_t st) {
+#define LL_CASE(NV_, G_) \
+  if (nv == NV_ && g == G_) return launch_smem_t<W, NV_, G_>(p, src, dst, max_ctas, st);
+  LL_CASE(1, 4) LL_CASE(1, 8) LL_CASE(1, 16)
+  LL_CASE(2, 4) LL_CASE(2, 8) LL_CASE(2, 16)
+  LL_CASE(4, 4) LL_CASE(4, 8) LL_CASE(4, 16)
+  LL_CASE(8, 4) LL_CASE(8, 8) LL_CASE(8, 16)
+#undef LL_CASE
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_convert_smem(const SmemPlan& p, int w, int nv, int g, const void* src, void* dst,
+                                int max_ctas, cudaStream_t st) {
+  switch (w) {
+    case 1: return launch_smem_w<1>(p, nv, g, src, dst, max_ctas, st);
+    case 2: return launch_smem_w<2>(p, nv, g, src, dst, max_ctas, st);
+    case 4: return launch_smem_w<4>(p, nv, g, src, dst, max_ctas, st);
+    case 8: return launch_smem_w<8>(p, nv, g, src, dst, max_ctas, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int W>
+static cudaError_t launch_generic_t(const GenericPlan& p, const void* src, void* dst, int max_ctas,
+                                    cudaStream_t st) {
+  const int threads = 256;
+  int64_t want = (p.n_vec + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
+  int grid = (int)(want < cap ? want : cap);
+  if (grid < 1) grid = 1;
+  convert_generic_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, (uint8_t*)dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src, void* dst,
+                                   int max_ctas, cudaStream_t st) {
+  switch (w) {
+    case 1: return launch_generic_t<1>(p, src, dst, max_ctas, st);
+    case 2: return launch_generic_t<2>(p, src, dst, max_ctas, st);
+    case 4: return launch_generic_t<4>(p, src, dst, max_ctas, st);
+    case 8: return launch_generic_t<8>(p, src, dst, max_ctas, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int W>
+static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void* src,
+                                   const int32_t* idx, void* out, int* err, int max_ctas,
+                                   cudaStream_t st) {
+  const int threads = 256;
+  int64_t want = (p.n_vec + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
+  int grid = (int)(want < cap ? want : cap);
+  if (grid < 1) grid = 1;
+  if (shuffle)
+    gather_shuffle_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
+                                                      err);
+  else
+    gather_direct_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
+                                                     err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* src,
+                          const int32_t* idx, void* out, int* err, int max_ctas, cudaStream_t st) {
+  switch (w) {
+    case 1: return launch_gather_t<1>(p, shuffle, src, idx, out, err, max_ctas, st);
+    case 2: return launch_gather_t<2>(p, shuffle, src, idx, out, err, max_ctas, st);
+    case 4: return launch_gather_t<4>(p, shuffle, src, idx, out, err, max_ctas, st);
+    case 8: return launch_gather_t<8>(p, shuffle, src, idx, out, err, max_ctas, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+int device_sm_count() { return num_sms(); }
+
+}  // namespace ll

@@ -1,0 +1,19 @@
+// kernels.hpp -- host launchers of the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "plan.hpp"
+
+namespace ll {
+
+// w = element bytes, nv = 16-byte vectors per thread per side, g = granule bytes.
+cudaError_t launch_convert_smem(const SmemPlan& p, int w, int nv, int g, const void* src,
+                                void* dst, int max_ctas, cudaStream_t st);
+cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src, void* dst,
+                                   int max_ctas, cudaStream_t st);
+cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* src,
+                          const int32_t* idx, void* out, int* err, int max_ctas, cudaStream_t st);
+int device_sm_count();
+
+}  // namespace ll

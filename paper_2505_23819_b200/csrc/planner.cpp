@@ -1,0 +1,509 @@
+// planner.cpp -- conversion / gather planning on the host.
+//
+// The conversion B^{-1} o A is executed as a pull:
+// dst[h] = src[X h] with X = A^{-1} o B (reading A6).  When X is a
+// permutation of index bits the tensor splits into independent tiles; the
+// planner picks a coalesced load layout and a coalesced store layout for one
+// tile (the "free mapping" of DESIGN.md), and the exchange between them goes
+// through shared memory laid out by the paper's optimal swizzle.
+#include "planner.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <tuple>
+
+namespace ll {
+
+namespace {
+
+int ilog2i(int x) {
+  int r = 0;
+  while ((1 << (r + 1)) <= x) ++r;
+  return r;
+}
+
+std::string vec_json(const std::vector<u64>& v) {
+  std::ostringstream o;
+  o << "[";
+  for (size_t i = 0; i < v.size(); ++i) o << (i ? "," : "") << v[i];
+  o << "]";
+  return o.str();
+}
+std::string ivec_json(const std::vector<int>& v) {
+  std::ostringstream o;
+  o << "[";
+  for (size_t i = 0; i < v.size(); ++i) o << (i ? "," : "") << v[i];
+  o << "]";
+  return o.str();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ optimal swizzle
+SwizzleResult optimal_swizzle(const std::vector<u64>& A_lane, const std::vector<u64>& B_lane,
+                              const std::vector<u64>& V, int d, int elem_bytes) {
+  SwizzleResult s;
+  s.v = (int)V.size();
+  const int gbytes = (1 << s.v) * elem_bytes;
+  // b = log2(128 / (2^v w))
+  s.b = gbytes <= 128 ? ilog2i(128 / gbytes) : 0;
+  s.b = std::min(s.b, d - s.v);
+  s.ell = d - s.v - s.b;
+  // A_bank, B_bank: drop the last log2 max(1, 2^v w / 4) thread vectors (reading A13)
+  const int drop = ilog2i(std::max(1, gbytes / 4));
+  std::vector<u64> At, Bt;
+  for (u64 x : A_lane) if (x) At.push_back(x);
+  for (u64 x : B_lane) if (x) Bt.push_back(x);
+  s.A_bank.assign(At.begin(), At.end() - std::min<int>(drop, (int)At.size()));
+  s.B_bank.assign(Bt.begin(), Bt.end() - std::min<int>(drop, (int)Bt.size()));
+  // E = A_bank \ B_bank, F = B_bank \ A_bank, ascending; |E| <= |F|
+  for (u64 x : s.A_bank)
+    if (std::find(s.B_bank.begin(), s.B_bank.end(), x) == s.B_bank.end()) s.E.push_back(x);
+  for (u64 x : s.B_bank)
+    if (std::find(s.A_bank.begin(), s.A_bank.end(), x) == s.A_bank.end()) s.F.push_back(x);
+  std::sort(s.E.begin(), s.E.end());
+  std::sort(s.F.begin(), s.F.end());
+  if (s.E.size() > s.F.size()) std::swap(s.E, s.F);
+  for (size_t i = 0; i < s.E.size(); ++i) s.H.push_back(s.E[i] ^ s.F[i]);
+  // C: complement of span(S_vect u A_bank u B_bank)
+  {
+    F2Basis bs;
+    for (u64 x : V) bs.add(x);
+    for (u64 x : s.A_bank) bs.add(x);
+    for (u64 x : s.B_bank) bs.add(x);
+    for (int k = 0; k < d && bs.n < d; ++k)
+      if (bs.add(u64(1) << k)) s.C.push_back(u64(1) << k);
+  }
+  // S_idx: ell vectors from H then C (reading A15); pad from A_bank (A16)
+  std::vector<u64> hc = s.H;
+  hc.insert(hc.end(), s.C.begin(), s.C.end());
+  if ((int)hc.size() >= s.ell) {
+    s.idx.assign(hc.begin(), hc.begin() + s.ell);
+  } else {
+    s.idx = hc;
+    s.unavoidable = true;
+    F2Basis bs;
+    for (u64 x : V) bs.add(x);
+    for (u64 x : s.idx) bs.add(x);
+    for (u64 x : s.A_bank) {
+      if ((int)s.idx.size() == s.ell) break;
+      if (bs.add(x)) s.idx.push_back(x);
+    }
+  }
+  s.vect = V;
+  // S_bank completes S_vect u S_idx to a basis of F2^d
+  {
+    F2Basis bs;
+    for (u64 x : V) bs.add(x);
+    for (u64 x : s.idx) bs.add(x);
+    for (int k = 0; k < d && bs.n < d; ++k)
+      if (bs.add(u64(1) << k)) s.bank.push_back(u64(1) << k);
+  }
+  return s;
+}
+
+int lemma_wavefronts(const SwizzleResult& s, const std::vector<u64>& lanes, int elem_bytes) {
+  const int gbytes = (1 << s.v) * elem_bytes;
+  const int n = std::max(1, gbytes / 4);
+  const int drop = ilog2i(n);
+  std::vector<u64> bank(lanes.begin(), lanes.end() - std::min<int>(drop, (int)lanes.size()));
+  std::vector<u64> vi = s.vect;
+  vi.insert(vi.end(), s.idx.begin(), s.idx.end());
+  std::vector<u64> all = vi;
+  all.insert(all.end(), bank.begin(), bank.end());
+  int inter = f2_rank(vi) + f2_rank(bank) - f2_rank(all);
+  return n * (1 << inter);
+}
+
+// ------------------------------------------------------------- conversion plan
+namespace {
+
+// X = A^{-1} o B as columns (one per dst index bit): the src index of each
+// dst basis bit.
+std::vector<u64> quotient(const Layout& A, const Layout& B) {
+  auto Ainv = f2_right_inverse(A.cols, A.out_bits());
+  std::vector<u64> X;
+  X.reserve(B.cols.size());
+  for (u64 c : B.cols) X.push_back(f2_apply(Ainv, c));
+  return X;
+}
+
+void fill_generic(ConvertPlan& P, const std::vector<u64>& X) {
+  GenericPlan& g = P.gp;
+  g = GenericPlan{};
+  const int vb = ilog2i(16 / P.w);
+  g.nB = P.nB;
+  g.n_x = P.nB;
+  for (int k = 0; k < P.nB; ++k) g.x[k] = (int64_t)X[k];
+  g.batch_stride_src = int64_t(1) << P.nA;
+  g.batch_stride_dst = int64_t(1) << P.nB;
+  const int64_t per = P.nB >= vb ? (int64_t(1) << (P.nB - vb)) : 1;
+  g.n_vec = per * P.batch;
+}
+
+// Try to build the shared-memory tile plan; returns false if X is not a bit
+// permutation or the tile does not fit.
+bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ostringstream& js) {
+  const int n = P.nB, w = P.w;
+  if (P.nA != P.nB || n > 62) return false;
+  std::vector<int> sigma(n), sinv(n, -1);
+  for (int k = 0; k < n; ++k) {
+    if (popcount64(X[k]) != 1) return false;
+    sigma[k] = ctz64(X[k]);
+    if (sinv[sigma[k]] >= 0) return false;
+    sinv[sigma[k]] = k;
+  }
+  const int vb = ilog2i(16 / w);
+  if (n < vb + 5) return false;
+  std::vector<int> VD, VS, CD, CS;
+  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
+  for (int k = vb; k < std::min(n, vb + 3); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
+  auto contains = [](const std::vector<int>& v, int x) {
+    return std::find(v.begin(), v.end(), x) != v.end();
+  };
+  const int r_max = ilog2i(128 / w);
+  const int r_pref = ilog2i(64 / w);
+  int G = 0, gbits = 0, r = 0;
+  std::vector<int> V, need;
+  // Granule choice: the largest prefix of the destination vector that the
+  // load side can also hold in registers; prefer choices that keep the
+  // source coalescing bits out of the registers.
+  for (int pass = 0; pass < 2 && !G; ++pass) {
+    for (int Gc : {16, 8, 4}) {
+      if (Gc < w || Gc < 4) continue;
+      int gb = ilog2i(Gc / w);
+      std::vector<int> Vc(VD.begin(), VD.begin() + gb);
+      std::vector<int> nd = VS;
+      for (int x : Vc) if (!contains(nd, x)) nd.push_back(x);
+      int rn = (int)nd.size();
+      if (rn > r_max || rn + 5 > n) continue;
+      bool clash = false;
+      for (int x : nd) if (contains(CS, x)) clash = true;
+      if (clash && pass == 0) continue;
+      G = Gc; gbits = gb; V = Vc; need = nd;
+      r = std::min(std::max(rn, r_pref), std::min(r_max, n - 5));
+      break;
+    }
+  }
+  if (!G) return false;
+  // tile bits T (dst bit ids)
+  std::vector<int> T = VD;
+  for (auto* s : {&VS, &CD, &CS, &need})
+    for (int x : *s) if (!contains(T, x)) T.push_back(x);
+  for (int k = 0; (int)T.size() < r + 5 && k < n; ++k)
+    if (!contains(T, k)) T.push_back(k);
+  int g = (int)T.size() - r - 5;
+  if (g > 3) {
+    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
+    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
+  }
+  if (g < 0 || g > 3) return false;
+  std::sort(T.begin(), T.end());
+  // ---- load layout: rho order = VS, need \ VS (src order), extra (highest src)
+  std::vector<int> ld_reg = VS;
+  {
+    std::vector<int> rest;
+    for (int x : need) if (!contains(ld_reg, x)) rest.push_back(x);
+    std::sort(rest.begin(), rest.end(), [&](int a, int b) { return sigma[a] < sigma[b]; });
+    ld_reg.insert(ld_reg.end(), rest.begin(), rest.end());
+    std::vector<int> cand;
+    for (int x : T) if (!contains(ld_reg, x) && !contains(CS, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) { return sigma[a] > sigma[b]; });
+    for (int x : cand) { if ((int)ld_reg.size() == r) break; ld_reg.push_back(x); }
+    if ((int)ld_reg.size() != r) return false;
+  }
+  std::vector<int> ld_lane, ld_warp;
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(ld_reg, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) { return sigma[a] < sigma[b]; });
+    for (int x : cand) (ld_lane.size() < 5 ? ld_lane : ld_warp).push_back(x);
+  }
+  // ---- store layout: rho order = VD, extra (highest dst)
+  std::vector<int> st_reg = VD;
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(st_reg, x) && !contains(CD, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [](int a, int b) { return a > b; });
+    for (int x : cand) { if ((int)st_reg.size() == r) break; st_reg.push_back(x); }
+    if ((int)st_reg.size() != r) return false;
+  }
+  std::vector<int> st_lane = CD, st_warp;
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(st_reg, x) && !contains(st_lane, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end());
+    for (int x : cand) (st_lane.size() < 5 ? st_lane : st_warp).push_back(x);
+  }
+  if (ld_lane.size() != 5 || st_lane.size() != 5 || (int)ld_warp.size() != g ||
+      (int)st_warp.size() != g)
+    return false;
+  // ---- register-bit swaps on the load side: bring V to rho positions 0..gbits-1
+  std::vector<int> order = ld_reg;
+  std::vector<std::pair<int, int>> swaps;
+  for (int t = 0; t < gbits; ++t) {
+    int s = (int)(std::find(order.begin(), order.end(), V[t]) - order.begin());
+    if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
+  }
+  if ((int)swaps.size() > LL_MAX_SWAPS) return false;
+  // ---- tile-local space
+  const int d = (int)T.size();
+  auto loc = [&](int k) -> u64 {
+    return u64(1) << (std::find(T.begin(), T.end(), k) - T.begin());
+  };
+  std::vector<u64> Al, Bl, Vl;
+  for (int x : ld_lane) Al.push_back(loc(x));
+  for (int x : st_lane) Bl.push_back(loc(x));
+  for (int x : V) Vl.push_back(loc(x));
+  SwizzleResult sw;
+  std::vector<u64> Scols;
+  if (swizzle) {
+    sw = optimal_swizzle(Al, Bl, Vl, d, w);
+    Scols = sw.vect;
+    Scols.insert(Scols.end(), sw.bank.begin(), sw.bank.end());
+    Scols.insert(Scols.end(), sw.idx.begin(), sw.idx.end());
+  } else {
+    // unswizzled staging (ablation): offsets = store order (rho, lane, warp)
+    sw.v = (int)Vl.size();
+    for (int k : st_reg) Scols.push_back(loc(k));
+    for (int k : st_lane) Scols.push_back(loc(k));
+    for (int k : st_warp) Scols.push_back(loc(k));
+    sw.vect = Vl;
+    sw.bank.assign(Scols.begin() + Vl.size(), Scols.end());
+  }
+  auto Sinv = f2_right_inverse(Scols, d);  // square, invertible
+  auto off = [&](int k) -> int32_t { return (int32_t)f2_apply(Sinv, loc(k)); };
+  // ---- fill the device plan
+  SmemPlan& sp = P.sp;
+  sp = SmemPlan{};
+  sp.gw = g;
+  sp.tile_elems = 1 << d;
+  sp.n_swaps = (int)swaps.size();
+  for (size_t i = 0; i < swaps.size(); ++i) {
+    sp.swap_a[i] = (int8_t)swaps[i].first;
+    sp.swap_b[i] = (int8_t)swaps[i].second;
+  }
+  for (int b = 0; b < 5; ++b) {
+    sp.ld_thr[b] = int64_t(1) << sigma[ld_lane[b]];
+    sp.st_thr[b] = int64_t(1) << st_lane[b];
+    sp.sw_thr[b] = off(ld_lane[b]);
+    sp.sr_thr[b] = off(st_lane[b]);
+  }
+  for (int b = 0; b < g; ++b) {
+    sp.ld_thr[5 + b] = int64_t(1) << sigma[ld_warp[b]];
+    sp.st_thr[5 + b] = int64_t(1) << st_warp[b];
+    sp.sw_thr[5 + b] = off(ld_warp[b]);
+    sp.sr_thr[5 + b] = off(st_warp[b]);
+  }
+  const int nvec = 1 << (r - vb);
+  if (nvec > LL_MAX_VEC) return false;
+  for (int u = 0; u < nvec; ++u) {
+    int64_t lo = 0, so = 0;
+    for (int q = 0; q < r - vb; ++q)
+      if ((u >> q) & 1) { lo += int64_t(1) << sigma[ld_reg[vb + q]]; so += int64_t(1) << st_reg[vb + q]; }
+    sp.ld_vec[u] = lo;
+    sp.st_vec[u] = so;
+  }
+  const int ngran = 1 << (r - gbits);
+  if (ngran > LL_MAX_GRAN) return false;
+  for (int j = 0; j < ngran; ++j) {
+    int32_t wo = 0, ro = 0;
+    for (int q = 0; q < r - gbits; ++q)
+      if ((j >> q) & 1) { wo ^= off(order[gbits + q]); ro ^= off(st_reg[gbits + q]); }
+    sp.sw_gran[j] = wo;
+    sp.sr_gran[j] = ro;
+  }
+  // ---- tile map: outer dst bits, identity run at the top
+  std::vector<int> O;
+  for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
+  int m = 0;
+  if (!O.empty()) {
+    m = 1;
+    while (m < (int)O.size()) {
+      int a = O[O.size() - m - 1], b = O[O.size() - m];
+      if (b == a + 1 && sigma[b] == sigma[a] + 1) ++m; else break;
+    }
+  }
+  const int n_scat = (int)O.size() - m;
+  if (n_scat > LL_MAX_SCAT) return false;
+  TileMap& tm = sp.tile;
+  tm.n_scat = n_scat;
+  tm.n_run = m;
+  tm.run_shift_dst = m ? O[n_scat] : 0;
+  tm.run_shift_src = m ? sigma[O[n_scat]] : 0;
+  for (int q = 0; q < n_scat; ++q) {
+    tm.scat_src[q] = int64_t(1) << sigma[O[q]];
+    tm.scat_dst[q] = int64_t(1) << O[q];
+  }
+  tm.batch_stride_src = int64_t(1) << P.nA;
+  tm.batch_stride_dst = int64_t(1) << P.nB;
+  tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
+  P.nv = nvec;
+  P.g = G;
+  P.tile_bits = d;
+  P.r = r;
+  P.gw = g;
+  std::vector<u64> Bw;
+  for (int k : st_lane) Bw.push_back(loc(k));
+  P.pred_wf_ld = lemma_wavefronts(sw, Al, w);
+  P.pred_wf_st = lemma_wavefronts(sw, Bw, w);
+  if (!swizzle) { P.pred_wf_ld = -1; P.pred_wf_st = -1; }
+  // ---- description
+  auto srcpos = [&](const std::vector<int>& v) {
+    std::vector<int> o;
+    for (int x : v) o.push_back(sigma[x]);
+    return o;
+  };
+  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
+     << ",\"granule_bytes\":" << G << ",\"granule_dst_bits\":" << ivec_json(V)
+     << ",\"vectors_per_thread\":" << nvec << ",\"swaps\":[";
+  for (size_t i = 0; i < swaps.size(); ++i)
+    js << (i ? "," : "") << "[" << swaps[i].first << "," << swaps[i].second << "]";
+  js << "],\"ld_reg_dst\":" << ivec_json(ld_reg) << ",\"ld_reg_src\":" << ivec_json(srcpos(ld_reg))
+     << ",\"ld_lane_dst\":" << ivec_json(ld_lane) << ",\"ld_lane_src\":" << ivec_json(srcpos(ld_lane))
+     << ",\"ld_warp_dst\":" << ivec_json(ld_warp) << ",\"ld_rho_after_swaps\":" << ivec_json(order)
+     << ",\"st_reg\":" << ivec_json(st_reg) << ",\"st_lane\":" << ivec_json(st_lane)
+     << ",\"st_warp\":" << ivec_json(st_warp) << ",\"swizzled\":" << (swizzle ? "true" : "false")
+     << ",\"S_vect\":" << vec_json(sw.vect) << ",\"S_bank\":" << vec_json(sw.bank)
+     << ",\"S_idx\":" << vec_json(sw.idx) << ",\"H\":" << vec_json(sw.H)
+     << ",\"C\":" << vec_json(sw.C) << ",\"E\":" << vec_json(sw.E) << ",\"F\":" << vec_json(sw.F)
+     << ",\"unavoidable\":" << (sw.unavoidable ? "true" : "false")
+     << ",\"pred_wavefronts_per_sts\":" << P.pred_wf_ld
+     << ",\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"n_tiles\":" << tm.n_tiles
+     << ",\"outer_scattered\":" << n_scat << ",\"outer_run\":" << m;
+  return true;
+}
+
+std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B, int w,
+                                                int path_req, int64_t batch) {
+  if (!A.same_tensor(B)) throw Error(LL_ERR_SHAPE, "convert: source and destination layouts map to different tensors");
+  if (!A.surjective()) throw Error(LL_ERR_NOT_SURJECTIVE, "convert: the source layout is not surjective");
+  auto P = std::make_shared<ConvertPlan>();
+  P->w = w;
+  P->nA = A.in_bits();
+  P->nB = B.in_bits();
+  P->batch = batch;
+  auto X = quotient(A, B);
+  bool ident = P->nA == P->nB;
+  for (int k = 0; ident && k < P->nB; ++k) ident = X[k] == (u64(1) << k);
+  P->identity = ident;
+  std::ostringstream js;
+  js << "{\"nA\":" << P->nA << ",\"nB\":" << P->nB << ",\"elem_bytes\":" << w
+     << ",\"batch\":" << batch << ",\"X\":" << vec_json(X) << ",\"identity\":"
+     << (ident ? "true" : "false");
+  int path = path_req;
+  if (path == LL_PATH_AUTO) path = ident ? LL_PATH_COPY : LL_PATH_SMEM;
+  if (path == LL_PATH_SHUFFLE) path = LL_PATH_SMEM;  // shuffle exchange: not yet built (falls back)
+  if (path == LL_PATH_COPY && !ident)
+    throw Error(LL_ERR_UNSUPPORTED, "copy path requested but the quotient is not the identity");
+  if (path == LL_PATH_SMEM || path == LL_PATH_SMEM_NOSWIZZLE) {
+    std::ostringstream js2;
+    if (plan_smem(*P, X, path == LL_PATH_SMEM, js2)) {
+      js << js2.str();
+    } else {
+      if (path_req == LL_PATH_SMEM || path_req == LL_PATH_SMEM_NOSWIZZLE)
+        throw Error(LL_ERR_UNSUPPORTED, "smem path requested but the quotient is not a tileable bit permutation");
+      path = LL_PATH_GENERIC;
+    }
+  }
+  if (path == LL_PATH_GENERIC) fill_generic(*P, X);
+  P->path = path;
+  static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle"};
+  js << ",\"path\":\"" << names[path] << "\"}";
+  P->json = js.str();
+  return P;
+}
+
+struct Key {
+  u64 a, b;
+  int w, path;
+  int64_t batch;
+  bool operator<(const Key& o) const {
+    return std::tie(a, b, w, path, batch) < std::tie(o.a, o.b, o.w, o.path, o.batch);
+  }
+};
+
+std::mutex g_mu;
+std::map<Key, std::shared_ptr<const ConvertPlan>> g_cache;
+std::map<Key, std::shared_ptr<const GatherPlanHost>> g_gcache;
+
+}  // namespace
+
+std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
+                                                    int path_req, int64_t batch) {
+  Key k{A.hash(), B.hash(), w, path_req, batch};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(k);
+    if (it != g_cache.end()) return it->second;
+  }
+  auto P = build_convert_plan(A, B, w, path_req, batch);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_cache[k] = P;
+  return P;
+}
+
+// ------------------------------------------------------------------ gather
+std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
+                                                      int path_req, int64_t batch) {
+  Key k{L.hash(), (u64)axis, w, path_req, batch};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_gcache.find(k);
+    if (it != g_gcache.end()) return it->second;
+  }
+  if (axis < 0 || axis >= (int)L.out.size()) throw Error(LL_ERR_ARG, "gather: axis out of range");
+  const int n = L.in_bits();
+  if (n != L.out_bits() || !L.surjective())
+    throw Error(LL_ERR_UNSUPPORTED, "gather: the layout must be a bijection (no broadcasting)");
+  auto P = std::make_shared<GatherPlanHost>();
+  P->w = w;
+  GatherPlan& g = P->gp;
+  g = GatherPlan{};
+  const int vb = ilog2i(16 / w);
+  if (n < vb) throw Error(LL_ERR_UNSUPPORTED, "gather: tensor smaller than one 16-byte vector");
+  g.nbits = n;
+  g.batch_stride = int64_t(1) << n;
+  g.ax_shift = L.out_shift(axis);
+  g.ax_bits = L.out[axis].bits;
+  if (g.ax_bits > 31) throw Error(LL_ERR_UNSUPPORTED, "gather: axis too long");
+  for (int k = 0; k < n; ++k) g.L[k] = (int64_t)L.cols[k];
+  auto Linv = f2_right_inverse(L.cols, L.out_bits());
+  bool contig = true;
+  int64_t amask = 0;
+  for (int k = 0; k < g.ax_bits; ++k) {
+    g.Y[k] = (int64_t)Linv[g.ax_shift + k];
+    amask |= g.Y[k];
+    if (g.Y[k] != (int64_t(1) << (ctz64(Linv[g.ax_shift]) + k))) contig = false;
+  }
+  g.y_contig = contig ? 1 : 0;
+  g.y_base = g.ax_bits ? ctz64(Linv[g.ax_shift]) : 0;
+  g.axis_mask_buf = amask;
+  g.vb = vb;
+  g.cand_mask = (int32_t)(amask & ((1 << vb) - 1));
+  g.n_vec = (int64_t(1) << (n - vb)) * batch;
+  const bool shuffle_ok = contig && n >= vb + 5 && (g.y_base + g.ax_bits) <= vb + 5;
+  int path = path_req;
+  if (path == LL_PATH_AUTO) path = shuffle_ok ? LL_PATH_SHUFFLE : LL_PATH_GENERIC;
+  if (path == LL_PATH_SHUFFLE && !shuffle_ok)
+    throw Error(LL_ERR_UNSUPPORTED, "gather: shuffle path needs the axis inside one warp's registers and lanes (L_warp^axis = 0, P:722)");
+  if (path != LL_PATH_SHUFFLE && path != LL_PATH_GENERIC)
+    throw Error(LL_ERR_UNSUPPORTED, "gather: path must be auto, shuffle or generic");
+  P->path = path;
+  std::ostringstream js;
+  js << "{\"path\":\"" << (path == LL_PATH_SHUFFLE ? "shuffle" : "direct") << "\",\"nbits\":" << n
+     << ",\"elem_bytes\":" << w << ",\"axis_bits\":" << g.ax_bits << ",\"Y\":[";
+  for (int k = 0; k < g.ax_bits; ++k) js << (k ? "," : "") << g.Y[k];
+  js << "],\"y_contig\":" << g.y_contig << ",\"cand_mask\":" << g.cand_mask
+     << ",\"candidate_shuffles\":" << (1 << popcount64((u64)g.cand_mask)) << ",\"batch\":" << batch
+     << "}";
+  P->json = js.str();
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_gcache[k] = P;
+  return P;
+}
+
+}  // namespace ll

@@ -1,0 +1,59 @@
+// planner.hpp -- host planner: conversion quotient, tiling, thread mappings,
+// optimal swizzle (paper Sec. 5.4 / Appendix), gather plans, plan cache.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "core.hpp"
+#include "plan.hpp"
+
+namespace ll {
+
+// Result of the paper's optimal-swizzling construction (P:685-713,
+// P:1104-1130) on a tile-local space of d bits.
+struct SwizzleResult {
+  std::vector<u64> vect, bank, idx;     // columns of S: offset bits -> tile-local vectors
+  std::vector<u64> A_bank, B_bank, E, F, H, C;
+  int v = 0, b = 0, ell = 0;
+  bool unavoidable = false;
+};
+
+// A and B are given by their reg / lane / warp columns (tile-local vectors).
+SwizzleResult optimal_swizzle(const std::vector<u64>& A_lane, const std::vector<u64>& B_lane,
+                              const std::vector<u64>& V, int d, int elem_bytes);
+
+// Lemma: wavefronts per instruction n * c, c from L_bank (A13).
+int lemma_wavefronts(const SwizzleResult& s, const std::vector<u64>& lanes, int elem_bytes);
+
+struct ConvertPlan {
+  int path = LL_PATH_GENERIC;
+  int w = 0;
+  int nA = 0, nB = 0;
+  int64_t batch = 1;
+  bool identity = false;
+  // smem path
+  SmemPlan sp{};
+  int nv = 0, g = 0;
+  int tile_bits = 0, r = 0, gw = 0;
+  int pred_wf_ld = 0, pred_wf_st = 0;   // wavefronts per STS / LDS instruction
+  // generic path
+  GenericPlan gp{};
+  std::string json;
+};
+
+struct GatherPlanHost {
+  int path = LL_PATH_GENERIC;  // LL_PATH_SHUFFLE or LL_PATH_GENERIC (direct)
+  int w = 0;
+  GatherPlan gp{};
+  std::string json;
+};
+
+// path_req: ll_path value (AUTO lets the planner choose).  Throws ll::Error.
+std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
+                                                    int path_req, int64_t batch);
+std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
+                                                      int path_req, int64_t batch);
+
+}  // namespace ll

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, byte-exact.
+
+Inputs are seeded splitmix64 patterns (workloads.values) generated on the
+device; expected outputs come only from ``oracle`` (plain definition of the
+conversion / gather).  Buffers are compared as raw
+bytes.  Small sizes: every element; full BASELINE sizes: sampled outputs
+computed one by one by the oracle + a permutation property on the whole
+buffer.
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import convert as oconv
+from oracle import f2
+from oracle.layout import Layout as OLayout
+from workloads import configs
+from workloads.values import indices_torch, values_torch
+
+if torch.cuda.is_available():
+    import paper_2505_23819_b200 as ll
+
+_NP = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}
+
+
+def _olayout(spec):
+    return OLayout(spec["in_dims"], spec["out_dims"], spec["bases"])
+
+
+def _np(t, w):
+    return t.cpu().numpy().view(_NP[w])
+
+
+def run_convert(c, path="auto", batch=1, seed=7):
+    w = c["elem_bytes"]
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    nA, nB = A.in_bits, B.in_bits
+    src = values_torch((1 << nA) * batch, seed, w, "cuda")
+    dst = torch.full(((1 << nB) * batch,), 0x55 if w == 1 else 0x5555, dtype=src.dtype, device="cuda") \
+        if w <= 2 else torch.zeros((1 << nB) * batch, dtype=src.dtype, device="cuda")
+    ll.convert(src, A, dst, B, 8 * w, path=path, batch=batch)
+    torch.cuda.synchronize()
+    return _np(src, w), _np(dst, w)
+
+
+def expect_convert(c, src_np, batch=1):
+    Ao, Bo = _olayout(c["A"]), _olayout(c["B"])
+    nA, nB = Ao.in_bits, Bo.in_bits
+    out = []
+    for b in range(batch):
+        out.append(oconv.convert_np(src_np[b << nA:(b + 1) << nA], Ao, Bo))
+    return np.concatenate(out)
+
+
+CASES = [
+    ("cfg1a", lambda: configs.cfg1("mma")),
+    ("cfg1b", lambda: configs.cfg1("T")),
+    ("cfg2_b0", lambda: configs.cfg2(batch_bits=0)),
+    ("cfg2_b3", lambda: configs.cfg2(batch_bits=3)),
+    ("cfg3_64", lambda: configs.cfg3(n_bits=6)),
+    ("cfg3_512", lambda: configs.cfg3(n_bits=9)),
+    ("cfg3_rect", lambda: configs.cfg3(n_bits=9, m_bits=7)),
+    ("cfg5_small", lambda: configs.cfg5(m_bits=8, kb_bits=7)),
+    ("cfg5_mid", lambda: configs.cfg5(m_bits=9, kb_bits=9)),
+]
+
+
+@pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "generic"])
+@pytest.mark.parametrize("name,mk", CASES)
+def test_convert_configs_small(name, mk, path):
+    c = mk()
+    src, dst = run_convert(c, path=path)
+    exp = expect_convert(c, src)
+    assert dst.tobytes() == exp.tobytes()
+
+
+@pytest.mark.parametrize("batch", [1, 5, 37])
+def test_convert_ragged_batch(batch):
+    """Batch of independent layout instances not a multiple of anything (the
+    tail of the persistent grid)."""
+    c = configs.cfg2(batch_bits=0)
+    src, dst = run_convert(c, batch=batch, seed=11)
+    assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
+
+
+def rand_pair(rng, d, w):
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    names = [("reg", rng.randint(vb, vb + 2)), ("lane", 5)]
+    rest = d - names[0][1] - 5
+    nw = min(rest, rng.randint(0, 3))
+    names += [("warp", nw), ("block", rest - nw)]
+    out = [("i", d // 2), ("j", d - d // 2)]
+    tmp = OLayout([], out, {})
+    specs = []
+    for _ in range(2):
+        cols = [1 << k for k in range(d)]
+        rng.shuffle(cols)
+        bases, k = {}, 0
+        for n, b in names:
+            bases[n] = [tmp.unflatten(x) for x in cols[k:k + b]]
+            k += b
+        specs.append({"in_dims": names, "out_dims": out, "bases": bases})
+    return {"A": specs[0], "B": specs[1], "elem_bytes": w}
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_random_pairs(w):
+    rng = random.Random(300 + w)
+    for _ in range(15):
+        d = rng.randint(12, 16)
+        c = rand_pair(rng, d, w)
+        src, dst = run_convert(c, seed=rng.randint(0, 1000))
+        assert dst.tobytes() == expect_convert(c, src).tobytes()
+
+
+def test_convert_identity_is_copy():
+    c = configs.cfg2(batch_bits=1)
+    c = {"A": c["A"], "B": c["A"], "elem_bytes": 2}
+    src, dst = run_convert(c)
+    assert dst.tobytes() == src.tobytes()
+
+
+def test_convert_roundtrip_on_device():
+    c = configs.cfg5(m_bits=9, kb_bits=8)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    src = values_torch(1 << A.in_bits, 3, 1, "cuda")
+    mid = torch.empty_like(src)
+    back = torch.empty_like(src)
+    ll.convert(src, A, mid, B, 8)
+    ll.convert(mid, B, back, A, 8)
+    torch.cuda.synchronize()
+    assert torch.equal(src, back)
+
+
+# ----------------------------------------------------------- full BASELINE sizes
+
+def sampled_expected(c, src_np, h):
+    """Oracle one element at a time: dst[h] = src[A^{-1}(B(h))]."""
+    Ao, Bo = _olayout(c["A"]), _olayout(c["B"])
+    Ainv = f2.right_inverse(Ao.cols, Ao.out_bits)
+    x = oconv.apply_np(Bo.cols, h)
+    s = oconv.apply_np(Ainv, x)
+    return src_np[s]
+
+
+@pytest.mark.parametrize("name,mk", [("cfg2", lambda: configs.cfg2()),
+                                     ("cfg3", lambda: configs.cfg3()),
+                                     ("cfg5", lambda: configs.cfg5(m_bits=15, kb_bits=14))])
+def test_convert_full_size_sampled(name, mk):
+    c = mk()
+    w = c["elem_bytes"]
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src = values_torch(n, 17, w, "cuda")
+    dst = torch.empty_like(src)
+    ll.convert(src, A, dst, B, 8 * w)
+    torch.cuda.synchronize()
+    # property at any size: dst is a permutation of src
+    key = (lambda t: t.view(torch.int16).to(torch.int32)) if w == 2 else \
+        (lambda t: t.to(torch.int32)) if w == 1 else (lambda t: t)
+    assert torch.equal(torch.sort(key(src))[0], torch.sort(key(dst))[0])
+    # sampled outputs, computed one by one by the oracle
+    rng = np.random.default_rng(5)
+    h = np.concatenate([rng.integers(0, n, 200000), np.arange(4096), np.arange(n - 4096, n)])
+    exp = sampled_expected(c, _np(src, w), h.astype(np.int64))
+    got = _np(dst, w)[h]
+    assert (got == exp).all()
+
+
+# ------------------------------------------------------------------------ gather
+
+def run_gather(c, path, seed=4, batch=1):
+    w = c["elem_bytes"]
+    L = ll.Layout.from_spec(c["L"])
+    n = (1 << L.in_bits) * batch
+    src = values_torch(n, seed, w, "cuda")
+    idx = indices_torch(n, seed + 1, c["idx_limit"], "cuda")
+    out = torch.zeros_like(src)
+    ll.gather(src, idx, out, L, c["axis"], 8 * w, path=path, batch=batch)
+    torch.cuda.synchronize()
+    return _np(src, w), idx.cpu().numpy(), _np(out, w)
+
+
+@pytest.mark.parametrize("path", ["auto", "shuffle", "generic"])
+@pytest.mark.parametrize("r_bits", [0, 3])
+def test_gather_tile_axis(path, r_bits):
+    c = configs.cfg4(r_bits=r_bits)
+    src, idx, out = run_gather(c, path)
+    exp = oconv.gather_np(src, idx, _olayout(c["L"]), c["axis"])
+    assert out.tobytes() == exp.tobytes()
+
+
+def test_gather_full_axis_direct():
+    c = configs.cfg4(r_bits=2, variant="full")
+    src, idx, out = run_gather(c, "auto")
+    exp = oconv.gather_np(src, idx, _olayout(c["L"]), c["axis"])
+    assert out.tobytes() == exp.tobytes()
+
+
+@pytest.mark.parametrize("w", [1, 2, 8])
+def test_gather_other_widths(w):
+    c = configs.cfg4(r_bits=1)
+    c = dict(c, elem_bytes=w)
+    for path in ("shuffle", "generic"):
+        src, idx, out = run_gather(c, path)
+        exp = oconv.gather_np(src, idx, _olayout(c["L"]), c["axis"])
+        assert out.tobytes() == exp.tobytes(), (w, path)
+
+
+def test_gather_full_size_sampled():
+    c = configs.cfg4()
+    w = 4
+    L = ll.Layout.from_spec(c["L"])
+    n = 1 << L.in_bits
+    src = values_torch(n, 4, w, "cuda")
+    idx = indices_torch(n, 5, 32, "cuda")
+    out = torch.empty_like(src)
+    ll.gather(src, idx, out, L, 2, 32)
+    torch.cuda.synchronize()
+    ref = torch.gather(src.view(-1, 32), 1, idx.view(-1, 32).long()).view(-1)
+    assert torch.equal(ref, out)
+    rng = np.random.default_rng(6)
+    h = rng.integers(0, n, 100000).astype(np.int64)
+    src_np, idx_np = _np(src, w), idx.cpu().numpy()
+    exp = oconv.gather_np(src_np, idx_np, _olayout(c["L"]), c["axis"], h=h)
+    assert (_np(out, w)[h] == exp).all()
+
+
+def test_gather_out_of_range_check(monkeypatch):
+    monkeypatch.setenv("LL_GATHER_CHECK", "1")
+    c = configs.cfg4(r_bits=0)
+    L = ll.Layout.from_spec(c["L"])
+    n = 1 << L.in_bits
+    src = values_torch(n, 1, 4, "cuda")
+    idx = torch.zeros(n, dtype=torch.int32, device="cuda")
+    idx[100] = 40
+    out = torch.empty_like(src)
+    with pytest.raises(ll.LLError) as e:
+        ll.gather(src, idx, out, L, 2, 32)
+    assert e.value.name == "LL_ERR_RANGE"
+
+
+def test_convert_host_e2e():
+    c = configs.cfg2(batch_bits=0)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    batch = 9
+    n = (1 << 14) * batch
+    src_h = values_torch(n, 21, 2, "cpu").pin_memory()
+    dst_h = torch.empty_like(src_h).pin_memory()
+    scratch = 4 * (1 << 15)
+    ds = torch.empty(scratch // 2, dtype=torch.int16, device="cuda")
+    dd = torch.empty(scratch // 2, dtype=torch.int16, device="cuda")
+    ll.convert_host(src_h, A, dst_h, B, 16, batch, ds, dd, scratch)
+    exp = expect_convert(c, src_h.numpy().view(np.uint16), batch)
+    assert dst_h.numpy().view(np.uint16).tobytes() == exp.tobytes()
+
+
+def test_misaligned_pointer_rejected():
+    c = configs.cfg2(batch_bits=0)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    buf = torch.zeros((1 << 14) + 8, dtype=torch.int16, device="cuda")
+    with pytest.raises(ll.LLError) as e:
+        ll.convert(buf[1:], A, buf, B, 16)
+    assert e.value.name == "LL_ERR_ARG"

@@ -1,0 +1,226 @@
+"""Host-side tests of libll_b200.so through its C ABI (CPU only).
+
+* the library loads and exports every symbol declared in include/ll.h;
+* layout create / apply / compose / invert / product agree with the oracle on
+  random layouts;
+* the planner's shared-memory plans are checked against the oracle: the
+  swizzle it builds equals the oracle's construction of the paper's
+  algorithm on the same load/store layouts, and the oracle's brute-force bank
+  counter confirms the predicted (ideal) wavefronts.
+"""
+
+import os
+import random
+import re
+
+import pytest
+
+import paper_2505_23819_b200 as ll
+from oracle import banks, f2, swizzle
+from oracle.layout import Layout as OLayout
+from oracle.layout import compose as ocompose
+from oracle.layout import product as oproduct
+from oracle.layout import right_inverse as oinverse
+from workloads import configs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "ll.h")).read()
+    return sorted(set(re.findall(r"\b(ll_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    lib = ctypes.CDLL(ll.lib_path)
+    syms = header_symbols()
+    assert len(syms) >= 19
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert "sm_100a" in ll.version()
+
+
+def rand_spec(rng, dims_in, out_dims, zeros=0):
+    d = sum(b for _, b in out_dims)
+    cols = [1 << k for k in range(d)] + [0] * zeros
+    rng.shuffle(cols)
+    tmp = OLayout([], out_dims, {})
+    bases, k = {}, 0
+    for n, b in dims_in:
+        bases[n] = [tmp.unflatten(c) for c in cols[k:k + b]]
+        k += b
+    return {"in_dims": dims_in, "out_dims": out_dims, "bases": bases}
+
+
+def rand_general_spec(rng, dims_in, out_dims):
+    d = sum(b for _, b in out_dims)
+    tmp = OLayout([], out_dims, {})
+    bases = {n: [tmp.unflatten(rng.getrandbits(d)) for _ in range(b)] for n, b in dims_in}
+    return {"in_dims": dims_in, "out_dims": out_dims, "bases": bases}
+
+
+def both(spec):
+    return ll.Layout.from_spec(spec), OLayout(spec["in_dims"], spec["out_dims"], spec["bases"])
+
+
+def test_apply_matches_oracle_random():
+    rng = random.Random(100)
+    for _ in range(50):
+        spec = rand_general_spec(rng, [("reg", 3), ("lane", 4), ("warp", 2)], [("i", 4), ("j", 5)])
+        P, O = both(spec)
+        assert P.spec()["bases"] == {n: [tuple(v) for v in vs] for n, vs in O.bases.items()}
+        for _ in range(20):
+            pt = (rng.randrange(8), rng.randrange(16), rng.randrange(4))
+            assert P.apply(pt) == O.apply({"reg": pt[0], "lane": pt[1], "warp": pt[2]})
+
+
+def test_apply_paper_worked_example():
+    P, _ = both(configs.cfg1()["A"])
+    assert P.apply((1, 9, 0)) == (2, 3)
+    with pytest.raises(ll.LLError) as e:
+        P.apply((4, 0, 0))
+    assert e.value.name == "LL_ERR_RANGE"
+
+
+def test_invert_compose_product_match_oracle():
+    rng = random.Random(101)
+    for _ in range(40):
+        spec = rand_spec(rng, [("reg", 2), ("lane", 5), ("warp", 2)], [("i", 4), ("j", 5)])
+        P, O = both(spec)
+        Pi, Oi = ll.invert(P), oinverse(O)
+        assert Pi.spec()["bases"] == {n: [tuple(v) for v in vs] for n, vs in Oi.bases.items()}
+        assert Pi.spec()["in_dims"] == Oi.in_dims and Pi.spec()["out_dims"] == Oi.out_dims
+        C = ll.compose(Pi, P)            # L^{-1} o L = identity
+        assert [c for c in OLayout(**{k: C.spec()[k] for k in ("in_dims", "out_dims", "bases")}).cols] \
+            == [1 << k for k in range(9)]
+        spec2 = rand_spec(rng, [("reg", 1), ("lane", 2)], [("i", 2), ("j", 1)])
+        P2, O2 = both(spec2)
+        Pp, Op = ll.product(P, P2), oproduct(O, O2)
+        assert Pp.spec()["bases"] == {n: [tuple(v) for v in vs] for n, vs in Op.bases.items()}
+
+
+def test_invert_general_matrix_matches_oracle_gauss_jordan():
+    rng = random.Random(102)
+    done = 0
+    while done < 60:
+        spec = rand_general_spec(rng, [("reg", 4), ("lane", 5)], [("t", 6)])
+        O = OLayout(spec["in_dims"], spec["out_dims"], spec["bases"])
+        P = ll.Layout.from_spec(spec)
+        if not O.is_surjective():
+            with pytest.raises(ll.LLError) as e:
+                ll.invert(P)
+            assert e.value.name == "LL_ERR_NOT_SURJECTIVE"
+            continue
+        Pi = ll.invert(P)
+        assert OLayout(**Pi.spec()).cols == f2.right_inverse(O.cols, 6)
+        done += 1
+
+
+def test_compose_label_mismatch():
+    P, _ = both(configs.cfg1()["A"])
+    with pytest.raises(ll.LLError) as e:
+        ll.compose(P, P)
+    assert e.value.name == "LL_ERR_LABEL"
+
+
+def test_create_errors():
+    with pytest.raises(ll.LLError) as e:
+        ll.Layout([("reg", 1), ("reg", 1)], [("x", 2)], {"reg": [(1,)]})
+    with pytest.raises(ll.LLError) as e:
+        ll.Layout([("reg", 1)], [("x", 2)], {"reg": [(4,)]})
+    assert e.value.name == "LL_ERR_RANGE"
+
+
+def test_props():
+    P, O = both(configs.cfg1()["A"])
+    assert P.props() == {"surjective": True, "distributed": True, "memory": False}
+    P3, _ = both(configs.cfg3(n_bits=3)["A"])
+    assert P3.props()["memory"]
+
+
+def test_plan_errors():
+    A, _ = both(configs.cfg1()["A"])
+    B, _ = both(configs.cfg3(n_bits=3)["B"])
+    with pytest.raises(ll.LLError) as e:
+        ll.plan_describe(A, B, 16)
+    assert e.value.name == "LL_ERR_SHAPE"
+    with pytest.raises(ll.LLError) as e:
+        ll.plan_describe(A, A, 12)
+    assert e.value.name == "LL_ERR_ARG"
+
+
+# ------------------------------------------------------------------ planner vs oracle
+
+def _tile_layouts(d):
+    """Load / store layouts of a smem plan as oracle layouts on the tile-local
+    space (d = plan description)."""
+    T = d["tile_dst_bits"]
+    loc = {k: 1 << i for i, k in enumerate(T)}
+    n = len(T)
+    def mk(reg, lane, warp):
+        return OLayout([("reg", len(reg)), ("lane", len(lane)), ("warp", len(warp))], [("t", n)],
+                       {"reg": [(loc[k],) for k in reg], "lane": [(loc[k],) for k in lane],
+                        "warp": [(loc[k],) for k in warp]})
+    A = mk(d["ld_rho_after_swaps"], d["ld_lane_dst"], d["ld_warp_dst"])
+    B = mk(d["st_reg"], d["st_lane"], d["st_warp"])
+    V = [loc[k] for k in d["granule_dst_bits"]]
+    S = OLayout([("offset", n)], [("t", n)], {"offset": [(c,) for c in d["S_vect"] + d["S_bank"] + d["S_idx"]]})
+    return A, B, V, S
+
+
+PLAN_CASES = [("cfg1a", configs.cfg1("mma")), ("cfg1b", configs.cfg1("T")),
+              ("cfg2", configs.cfg2(batch_bits=2)), ("cfg3", configs.cfg3(n_bits=7)),
+              ("cfg3r", configs.cfg3(n_bits=8, m_bits=6)), ("cfg5", configs.cfg5(m_bits=8, kb_bits=7))]
+
+
+@pytest.mark.parametrize("name,c", PLAN_CASES)
+def test_planner_swizzle_equals_oracle_and_is_conflict_free(name, c):
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    w = c["elem_bytes"]
+    d = ll.plan_describe(A, B, 8 * w, "smem")
+    assert d["path"] == "smem"
+    Ao, Bo, V, S = _tile_layouts(d)
+    # same construction as the oracle's step-by-step implementation of the paper
+    So, info = swizzle.optimal_swizzle(Ao, Bo, w, V=V)
+    assert So.cols == S.cols
+    assert info["H"] == d["H"] and info["C"] == d["C"]
+    # brute-force bank counter on the plan's actual accesses: ideal wavefronts
+    vbits = list(range(len(V)))
+    wa = banks.count_wavefronts(S, Ao, w, vbits)
+    wb = banks.count_wavefronts(S, Bo, w, vbits)
+    n_instr = (1 << (Ao.in_bits - 5)) // (1 << len(V))
+    ideal = max(1, ((1 << len(V)) * w) // 4)
+    assert wa == n_instr * ideal and wb == n_instr * ideal
+    assert d["pred_wavefronts_per_sts"] == ideal and d["pred_wavefronts_per_lds"] == ideal
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_planner_random_pairs_conflict_free(w):
+    rng = random.Random(200 + w)
+    for _ in range(12):
+        dims = [("reg", 3), ("lane", 5), ("warp", 2), ("block", 3)]
+        out = [("i", 6), ("j", 7)]
+        sa, sb = rand_spec(rng, dims, out), rand_spec(rng, dims, out)
+        A, B = ll.Layout.from_spec(sa), ll.Layout.from_spec(sb)
+        d = ll.plan_describe(A, B, 8 * w)
+        if d["path"] != "smem":
+            continue
+        Ao, Bo, V, S = _tile_layouts(d)
+        vbits = list(range(len(V)))
+        n_instr = (1 << (Ao.in_bits - 5)) // (1 << len(V))
+        ideal = max(1, ((1 << len(V)) * w) // 4)
+        assert banks.count_wavefronts(S, Ao, w, vbits) == n_instr * ideal
+        assert banks.count_wavefronts(S, Bo, w, vbits) == n_instr * ideal
+
+
+def test_gather_plan_config4():
+    c = configs.cfg4()
+    L = ll.Layout.from_spec(c["L"])
+    d = ll.gather_describe(L, c["axis"], 32)
+    assert d["path"] == "shuffle" and d["candidate_shuffles"] == 4      # reading A19: 2^|L_reg^axis|
+    cf = configs.cfg4(variant="full")
+    Lf = ll.Layout.from_spec(cf["L"])
+    assert ll.gather_describe(Lf, cf["axis"], 32)["path"] == "direct"
+    with pytest.raises(ll.LLError):
+        ll.gather_describe(Lf, cf["axis"], 32, "shuffle")
