@@ -186,6 +186,15 @@ ll_status ll_gather_describe(ll_layout layout, int axis, int elem_bits, int path
  * benchmark's gpu_launches claim). */
 int64_t ll_launch_count(void);
 
+/* Launch-configuration knobs (process-wide; defaults from the environment):
+ *   "tpg"        target tiles per tile group of the smem kernel (0 = persistent
+ *                grid at full occupancy; env LL_TPG, default 2)
+ *   "pipe"       1 = software-pipelined smem kernel (env LL_PIPE, default 0)
+ *   "gather_vpt" 16-byte output vectors per thread of the gather kernels
+ *                (env LL_GATHER_VPT, default 2)
+ * LL_ERR_ARG for an unknown name.  Used by the tuning sweeps. */
+ll_status ll_tune(const char* name, int value);
+
 const char* ll_last_error(void);
 
 /* Library version string. */

@@ -11,7 +11,8 @@ PyTorch fallback: if the shared library is missing the import fails loudly.
 """
 
 from ._lib import (LLError, Layout, compose, convert, convert_host, gather, gather_describe,
-                   invert, launch_count, lib_path, plan_describe, product, version, PATHS)
+                   invert, launch_count, lib_path, plan_describe, product, tune, version, PATHS)
 
 __all__ = ["LLError", "Layout", "compose", "convert", "convert_host", "gather", "gather_describe",
-           "invert", "launch_count", "lib_path", "plan_describe", "product", "version", "PATHS"]
+           "invert", "launch_count", "lib_path", "plan_describe", "product", "tune", "version",
+           "PATHS"]

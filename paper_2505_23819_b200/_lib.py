@@ -57,7 +57,8 @@ _lib.ll_plan_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int
 _lib.ll_gather_describe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_char_p, ctypes.c_size_t,
                                     ctypes.POINTER(ctypes.c_size_t)]
-for _f in ("ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
+_lib.ll_tune.argtypes = [ctypes.c_char_p, ctypes.c_int]
+for _f in ("ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
            "ll_gather_describe"):
@@ -83,6 +84,11 @@ def _check(st):
 
 def version():
     return _lib.ll_version().decode()
+
+
+def tune(name, value):
+    """ll_tune: set a launch-configuration knob (tpg, pipe, gather_vpt)."""
+    _check(_lib.ll_tune(name.encode(), int(value)))
 
 
 def launch_count():

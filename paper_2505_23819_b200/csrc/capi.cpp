@@ -76,6 +76,12 @@ const char* ll_last_error(void) { return g_err.c_str(); }
 const char* ll_version(void) { return "ll_b200 0.1 (sm_100a)"; }
 int64_t ll_launch_count(void) { return g_launches.load(); }
 
+ll_status ll_tune(const char* name, int value) {
+  if (ll::set_knob(name, value) != 0)
+    return fail(LL_ERR_ARG, std::string("ll_tune: unknown knob '") + (name ? name : "") + "'");
+  return LL_OK;
+}
+
 ll_status ll_layout_create(int n_in, const char* const* in_names, const int* in_bits, int n_out,
                            const char* const* out_names, const int* out_bits,
                            const int64_t* bases, ll_layout* out) {

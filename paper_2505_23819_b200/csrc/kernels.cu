@@ -7,6 +7,8 @@
 
 #include <cstdint>
 #include <type_traits>
+#include <cstdlib>
+#include <string>
 
 #include "kernels.hpp"
 #include "plan.hpp"
@@ -151,7 +153,22 @@ __device__ __forceinline__ void apply_swap(uint32_t (&R)[NW], int a, int b) {
 // ------------------------------------------------------------- smem kernel
 
 // W: element bytes; NV: 16-byte vectors per thread per side; G: granule bytes.
-template <int W, int NV, int G>
+// PIPE: software-pipelined variant -- the loads of the group's next tile are
+// issued before the shared-memory exchange of the current one.
+template <int W, int NV>
+__device__ __forceinline__ void load_tile(uint32_t (&R)[NV * 4], const uint8_t* sp,
+                                          const int64_t* ld_vec) {
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    uint4 v = ldg_stream(sp + ld_vec[u] * W);
+    R[4 * u + 0] = v.x;
+    R[4 * u + 1] = v.y;
+    R[4 * u + 2] = v.z;
+    R[4 * u + 3] = v.w;
+  }
+}
+
+template <int W, int NV, int G, bool PIPE>
 __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst) {
@@ -181,39 +198,44 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   }
   const uint32_t tile_bytes = (uint32_t)p.tile_elems * W;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * tile_bytes;
-  uint32_t waddr[NG], raddr[NG];
-#pragma unroll
-  for (int j = 0; j < NG; ++j) {
-    waddr[j] = sbase + (swx ^ (uint32_t)p.sw_gran[j]) * W;
-    raddr[j] = sbase + (srx ^ (uint32_t)p.sr_gran[j]) * W;
-  }
+  const uint32_t wbase = sbase + swx * W, rbase = sbase + srx * W;
 
   const int64_t stride = (int64_t)gridDim.x * groups_per_cta;
   uint32_t buf = 0;
-  for (int64_t t = (int64_t)blockIdx.x * groups_per_cta + group; t < p.tile.n_tiles; t += stride) {
-    int64_t sb, db;
+  int64_t t = (int64_t)blockIdx.x * groups_per_cta + group;
+  uint32_t R[NW];
+  int64_t sb, db;
+  if (PIPE && t < p.tile.n_tiles) {
     tile_bases(p.tile, t, sb, db);
-    uint32_t R[NW];
-    const uint8_t* sp = src + (sb + ld_off) * W;
-#pragma unroll
-    for (int u = 0; u < NV; ++u) {
-      uint4 v = ldg_stream(sp + p.ld_vec[u] * W);
-      R[4 * u + 0] = v.x;
-      R[4 * u + 1] = v.y;
-      R[4 * u + 2] = v.z;
-      R[4 * u + 3] = v.w;
+    load_tile<W, NV>(R, src + (sb + ld_off) * W, p.ld_vec);
+  }
+  for (; t < p.tile.n_tiles; t += stride) {
+    if (!PIPE) {
+      tile_bases(p.tile, t, sb, db);
+      load_tile<W, NV>(R, src + (sb + ld_off) * W, p.ld_vec);
     }
+    const int64_t dcur = db;
     for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
 #pragma unroll
-    for (int j = 0; j < NG; ++j) sts<G>(waddr[j] + buf, &R[j * GW]);
+    for (int j = 0; j < NG; ++j)
+      sts<G>((wbase ^ ((uint32_t)p.sw_gran[j] * W)) + buf, &R[j * GW]);
+    if (PIPE) {
+      const int64_t tn = t + stride;
+      if (tn < p.tile.n_tiles) {
+        tile_bases(p.tile, tn, sb, db);
+        load_tile<W, NV>(R, src + (sb + ld_off) * W, p.ld_vec);
+      }
+    }
     group_sync(gw, group);
+    uint32_t Q[NW];
 #pragma unroll
-    for (int j = 0; j < NG; ++j) lds<G>(raddr[j] + buf, &R[j * GW]);
-    uint8_t* dp = dst + (db + st_off) * W;
+    for (int j = 0; j < NG; ++j)
+      lds<G>((rbase ^ ((uint32_t)p.sr_gran[j] * W)) + buf, &Q[j * GW]);
+    uint8_t* dp = dst + (dcur + st_off) * W;
 #pragma unroll
     for (int u = 0; u < NV; ++u)
       stg_stream(dp + p.st_vec[u] * W,
-                 make_uint4(R[4 * u + 0], R[4 * u + 1], R[4 * u + 2], R[4 * u + 3]));
+                 make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
     buf ^= tile_bytes;
   }
 }
@@ -422,28 +444,69 @@ static int num_sms() {
   return g_num_sms;
 }
 
-template <int W, int NV, int G>
-static cudaError_t launch_smem_t(const SmemPlan& p, const void* src, void* dst, int max_ctas,
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Launch configuration knobs (env, read once): LL_TPG = target tiles per tile
+// group (0 = persistent grid at full occupancy), LL_PIPE = 1 for the
+// software-pipelined kernel.
+struct LaunchKnobs {
+  int tpg, pipe, gather_tpt;
+  LaunchKnobs()
+      : tpg(env_int("LL_TPG", 2)), pipe(env_int("LL_PIPE", 0)),
+        gather_tpt(env_int("LL_GATHER_VPT", 2)) {}
+};
+static LaunchKnobs& knobs() {
+  static LaunchKnobs k;
+  return k;
+}
+
+int set_knob(const char* name, int value) {
+  std::string n(name ? name : "");
+  if (n == "tpg") { knobs().tpg = value; return 0; }
+  if (n == "pipe") { knobs().pipe = value; return 0; }
+  if (n == "gather_vpt") { knobs().gather_tpt = value; return 0; }
+  return -1;
+}
+
+template <int W, int NV, int G, bool PIPE>
+static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, int max_ctas,
                                  cudaStream_t st) {
-  auto k = convert_smem_kernel<W, NV, G>;
+  auto k = convert_smem_kernel<W, NV, G, PIPE>;
   const int threads = 256;
   const int groups = (threads / 32) >> p.gw;
   const size_t smem = (size_t)groups * 2 * p.tile_elems * W;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static int occ_cache = -1;
+  static size_t occ_smem = 0;
+  if (occ_cache < 0 || occ_smem != smem) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
+    occ_smem = smem;
   }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
-  if (occ <= 0) return cudaErrorInvalidConfiguration;
-  int64_t want = (p.tile.n_tiles + groups - 1) / groups;
-  int64_t cap = (int64_t)occ * num_sms();
-  if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
-  int grid = (int)(want < cap ? want : cap);
+  if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
+  const int64_t n_groups = (p.tile.n_tiles + groups - 1) / groups;  // CTAs if one tile per group
+  int64_t grid;
+  const int tpg = knobs().tpg;
+  if (tpg > 0) {
+    grid = (n_groups + tpg - 1) / tpg;
+  } else {
+    grid = (int64_t)occ_cache * num_sms();
+  }
+  if (grid > n_groups) grid = n_groups;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (grid > 0x7fffffff) grid = 0x7fffffff;
   if (grid < 1) grid = 1;
-  k<<<grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst);
+  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst);
   return cudaGetLastError();
+}
+
+template <int W, int NV, int G>
+static cudaError_t launch_smem_t(const SmemPlan& p, const void* src, void* dst, int max_ctas,
+                                 cudaStream_t st) {
+  if (knobs().pipe) return launch_smem_p<W, NV, G, true>(p, src, dst, max_ctas, st);
+  return launch_smem_p<W, NV, G, false>(p, src, dst, max_ctas, st);
 }
 
 template <int W>
@@ -499,10 +562,10 @@ static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void
                                    const int32_t* idx, void* out, int* err, int max_ctas,
                                    cudaStream_t st) {
   const int threads = 256;
-  int64_t want = (p.n_vec + threads - 1) / threads;
-  int64_t cap = (int64_t)num_sms() * 8;
-  if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
-  int grid = (int)(want < cap ? want : cap);
+  const int vpt = knobs().gather_tpt > 0 ? knobs().gather_tpt : 1;
+  int64_t want = (p.n_vec + (int64_t)threads * vpt - 1) / ((int64_t)threads * vpt);
+  if (max_ctas > 0 && want > max_ctas) want = max_ctas;
+  int grid = (int)(want < 0x7fffffff ? want : 0x7fffffff);
   if (grid < 1) grid = 1;
   if (shuffle)
     gather_shuffle_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,

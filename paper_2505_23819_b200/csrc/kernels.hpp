@@ -15,5 +15,6 @@ cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src,
 cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* src,
                           const int32_t* idx, void* out, int* err, int max_ctas, cudaStream_t st);
 int device_sm_count();
+int set_knob(const char* name, int value);
 
 }  // namespace ll
