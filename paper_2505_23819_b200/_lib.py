@@ -9,7 +9,7 @@ lib_path = os.path.join(_HERE, "libll_b200.so")
 
 if not os.path.exists(lib_path):
     raise ImportError(
-        "libll_b200.so is not built (%s); run `python -m paper_2505_23819_b200.build` "
+        "libll_b200.so is not built (%s); run `python paper_2505_23819_b200/build.py` "
         "or __graft_entry__.build() -- there is no fallback path" % lib_path)
 
 _lib = ctypes.CDLL(lib_path)

@@ -1,6 +1,6 @@
 """Build libll_b200.so in-tree: nvcc for sm_100a (kernels) + g++ (host core).
 
-    python -m paper_2505_23819_b200.build [--force]
+    python paper_2505_23819_b200/build.py [--force]      (or __graft_entry__.build())
 
 The shared library lands next to this file so that it travels with the repo
 snapshot to the GPU box.  Compilation is incremental on source mtimes.
