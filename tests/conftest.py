@@ -9,6 +9,20 @@ if ROOT not in sys.path:
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
+def _ensure_library():
+    """Build libll_b200.so in-tree if it is missing or older than its sources
+    (nvcc cross-compiles for sm_100a without a GPU)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "ll_b200_build", os.path.join(ROOT, "paper_2505_23819_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()
+
+
+_ensure_library()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
