@@ -9,6 +9,7 @@
 #include <type_traits>
 #include <cstdlib>
 #include <string>
+#include <algorithm>
 
 #include "kernels.hpp"
 #include "plan.hpp"
@@ -152,15 +153,103 @@ __device__ __forceinline__ void apply_swap(uint32_t (&R)[NW], int a, int b) {
 
 // ------------------------------------------------------------- smem kernel
 
-// W: element bytes; NV: 16-byte vectors per thread per side; G: granule bytes.
-// PIPE: software-pipelined variant -- the loads of the group's next tile are
-// issued before the shared-memory exchange of the current one.
-template <int W, int NV>
+// ------------------------------------------------ compile-time granule selection
+//
+// A write granule is GW consecutive 32-bit words of shared memory.  Its words
+// come from the register file R[NW] at word indices that deposit the
+// granule-internal index k into word bits (A, B) and the granule number j
+// into the remaining word bits (ascending).  (A, B) are plan data; every
+// case is instantiated so the STS operands are compile-time registers.
+
+__host__ __device__ constexpr int deposit_word(int j, int k, int LB, int A, int B) {
+  int idx = 0, q = 0;
+  for (int bit = 0; bit < LB; ++bit) {
+    if (bit == A) {
+      idx |= (k & 1) << bit;
+    } else if (bit == B) {
+      idx |= ((k >> 1) & 1) << bit;
+    } else {
+      idx |= ((j >> q) & 1) << bit;
+      ++q;
+    }
+  }
+  return idx;
+}
+
+template <int NW, int GW, int A, int B>
+__device__ __forceinline__ void sts_granules(const uint32_t (&R)[NW], uint32_t wbase,
+                                             const uint32_t* gran) {
+  constexpr int LB = ilog2(NW);
+  constexpr int NG = NW / GW;
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    uint32_t v[GW];
+#pragma unroll
+    for (int k = 0; k < GW; ++k) v[k] = R[deposit_word(j, k, LB, A, B)];
+    sts<GW * 4>(wbase ^ gran[j], v);
+  }
+}
+
+template <int NW, int GW, int A, int B>
+__device__ __forceinline__ bool sts_try_b(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
+                                          const uint32_t* gran) {
+  constexpr int LB = ilog2(NW);
+  if constexpr (B >= LB) {
+    return false;
+  } else {
+    if constexpr (A != B) {
+      if (a == A && b == B) {
+        sts_granules<NW, GW, A, B>(R, wbase, gran);
+        return true;
+      }
+    }
+    return sts_try_b<NW, GW, A, B + 1>(a, b, R, wbase, gran);
+  }
+}
+
+template <int NW, int GW, int A>
+__device__ __forceinline__ bool sts_try_a(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
+                                          const uint32_t* gran) {
+  constexpr int LB = ilog2(NW);
+  if constexpr (A >= LB) {
+    return false;
+  } else {
+    bool done;
+    if constexpr (GW == 2) {
+      done = false;
+      if (a == A) {
+        sts_granules<NW, 2, A, -1>(R, wbase, gran);
+        done = true;
+      }
+    } else {
+      done = sts_try_b<NW, GW, A, 0>(a, b, R, wbase, gran);
+    }
+    if (done) return true;
+    return sts_try_a<NW, GW, A + 1>(a, b, R, wbase, gran);
+  }
+}
+
+template <int NW, int GW>
+__device__ __forceinline__ void sts_dispatch(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
+                                             const uint32_t* gran) {
+  if constexpr (GW == 1) {
+    sts_granules<NW, 1, -1, -1>(R, wbase, gran);
+  } else {
+    sts_try_a<NW, GW, 0>(a, b, R, wbase, gran);
+  }
+}
+
+// ------------------------------------------------------------- smem kernel
+//
+// W: element bytes; NV: 16-byte vectors per thread per side; G: granule
+// bytes; PIPE: the loads of the group's next tile are issued right after the
+// current tile's STS (before the exchange completes).
+template <int NV>
 __device__ __forceinline__ void load_tile(uint32_t (&R)[NV * 4], const uint8_t* sp,
-                                          const int64_t* ld_vec) {
+                                          const uint32_t* ld_vec) {
 #pragma unroll
   for (int u = 0; u < NV; ++u) {
-    uint4 v = ldg_stream(sp + ld_vec[u] * W);
+    uint4 v = ldg_stream(sp + ld_vec[u]);
     R[4 * u + 0] = v.x;
     R[4 * u + 1] = v.y;
     R[4 * u + 2] = v.z;
@@ -171,7 +260,8 @@ __device__ __forceinline__ void load_tile(uint32_t (&R)[NV * 4], const uint8_t* 
 template <int W, int NV, int G, bool PIPE>
 __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
-                                                           uint8_t* __restrict__ dst) {
+                                                           uint8_t* __restrict__ dst,
+                                                           int64_t hi_step) {
   constexpr int NW = NV * 4;          // 32-bit words per thread
   constexpr int NG = NV * 16 / G;     // granules per thread
   constexpr int GW = G / 4;           // words per granule
@@ -182,61 +272,63 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const int gw = p.gw;
   const int group = warp >> gw;
   const int tb = lane | ((warp & ((1 << gw) - 1)) << 5);
-  const int groups_per_cta = (blockDim.x >> 5) >> gw;
+  const int gpc = (blockDim.x >> 5) >> gw;
   const int tbits = 5 + gw;
 
-  int64_t ld_off = 0, st_off = 0;
-  uint32_t swx = 0, srx = 0;
+  // tile schedule: lo fixed per group, hi strided
+  const int64_t gid = (int64_t)blockIdx.x * gpc + group;
+  const int lo_bits = p.tile.n_scat;
+  const int64_t lo = gid & ((int64_t(1) << lo_bits) - 1);
+  int64_t hi = gid >> lo_bits;
+  if (hi >= hi_step) return;  // idle group (whole warps: barriers stay consistent)
+
+  uint32_t ld_off = 0, st_off = 0, swx = 0, srx = 0;
 #pragma unroll
   for (int b = 0; b < LL_MAX_TBITS; ++b) {
     if (b < tbits && ((tb >> b) & 1)) {
       ld_off += p.ld_thr[b];
       st_off += p.st_thr[b];
-      swx ^= (uint32_t)p.sw_thr[b];
-      srx ^= (uint32_t)p.sr_thr[b];
+      swx ^= p.sw_thr[b];
+      srx ^= p.sr_thr[b];
     }
   }
-  const uint32_t tile_bytes = (uint32_t)p.tile_elems * W;
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * tile_bytes;
-  const uint32_t wbase = sbase + swx * W, rbase = sbase + srx * W;
+  int64_t slo = 0, dlo = 0;
+  for (int q = 0; q < lo_bits; ++q)
+    if ((lo >> q) & 1) { slo += p.tile.scat_src[q]; dlo += p.tile.scat_dst[q]; }
+  const uint8_t* sthr = src + slo + ld_off;
+  uint8_t* dthr = dst + dlo + st_off;
+  const int64_t run_mask = (int64_t(1) << p.tile.n_run) - 1;
 
-  const int64_t stride = (int64_t)gridDim.x * groups_per_cta;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * p.tile_bytes;
+  const uint32_t wbase0 = sbase + swx, rbase0 = sbase + srx;
   uint32_t buf = 0;
-  int64_t t = (int64_t)blockIdx.x * groups_per_cta + group;
+  const int ga = p.gsel_a, gb = p.gsel_b;
+
   uint32_t R[NW];
-  int64_t sb, db;
-  if (PIPE && t < p.tile.n_tiles) {
-    tile_bases(p.tile, t, sb, db);
-    load_tile<W, NV>(R, src + (sb + ld_off) * W, p.ld_vec);
-  }
-  for (; t < p.tile.n_tiles; t += stride) {
-    if (!PIPE) {
-      tile_bases(p.tile, t, sb, db);
-      load_tile<W, NV>(R, src + (sb + ld_off) * W, p.ld_vec);
-    }
-    const int64_t dcur = db;
+  auto src_off = [&](int64_t h) -> int64_t {
+    return ((h & run_mask) << p.tile.run_shift_src) + (h >> p.tile.n_run) * p.tile.batch_stride_src;
+  };
+  auto dst_off = [&](int64_t h) -> int64_t {
+    return ((h & run_mask) << p.tile.run_shift_dst) + (h >> p.tile.n_run) * p.tile.batch_stride_dst;
+  };
+  if (PIPE && hi < p.n_hi) load_tile<NV>(R, sthr + src_off(hi), p.ld_vec);
+  for (; hi < p.n_hi; hi += hi_step) {
+    if (!PIPE) load_tile<NV>(R, sthr + src_off(hi), p.ld_vec);
     for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
-#pragma unroll
-    for (int j = 0; j < NG; ++j)
-      sts<G>((wbase ^ ((uint32_t)p.sw_gran[j] * W)) + buf, &R[j * GW]);
+    sts_dispatch<NW, GW>(ga, gb, R, wbase0 + buf, p.sw_gran);
     if (PIPE) {
-      const int64_t tn = t + stride;
-      if (tn < p.tile.n_tiles) {
-        tile_bases(p.tile, tn, sb, db);
-        load_tile<W, NV>(R, src + (sb + ld_off) * W, p.ld_vec);
-      }
+      const int64_t hn = hi + hi_step;
+      if (hn < p.n_hi) load_tile<NV>(R, sthr + src_off(hn), p.ld_vec);
     }
     group_sync(gw, group);
     uint32_t Q[NW];
 #pragma unroll
-    for (int j = 0; j < NG; ++j)
-      lds<G>((rbase ^ ((uint32_t)p.sr_gran[j] * W)) + buf, &Q[j * GW]);
-    uint8_t* dp = dst + (dcur + st_off) * W;
+    for (int j = 0; j < NG; ++j) lds<G>((rbase0 + buf) ^ p.sr_gran[j], &Q[j * GW]);
+    uint8_t* dp = dthr + dst_off(hi);
 #pragma unroll
     for (int u = 0; u < NV; ++u)
-      stg_stream(dp + p.st_vec[u] * W,
-                 make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
-    buf ^= tile_bytes;
+      stg_stream(dp + p.st_vec[u], make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
+    buf ^= p.tile_bytes;
   }
 }
 
@@ -455,7 +547,7 @@ static int env_int(const char* name, int dflt) {
 struct LaunchKnobs {
   int tpg, pipe, gather_tpt;
   LaunchKnobs()
-      : tpg(env_int("LL_TPG", 2)), pipe(env_int("LL_PIPE", 0)),
+      : tpg(env_int("LL_TPG", 0)), pipe(env_int("LL_PIPE", 1)),
         gather_tpt(env_int("LL_GATHER_VPT", 2)) {}
 };
 static LaunchKnobs& knobs() {
@@ -476,29 +568,38 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
                                  cudaStream_t st) {
   auto k = convert_smem_kernel<W, NV, G, PIPE>;
   const int threads = 256;
-  const int groups = (threads / 32) >> p.gw;
-  const size_t smem = (size_t)groups * 2 * p.tile_elems * W;
+  const int gpc = (threads / 32) >> p.gw;
+  const size_t smem = (size_t)gpc * 2 * p.tile_bytes;
   static int occ_cache = -1;
   static size_t occ_smem = 0;
   if (occ_cache < 0 || occ_smem != smem) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
     occ_smem = smem;
   }
   if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
-  const int64_t n_groups = (p.tile.n_tiles + groups - 1) / groups;  // CTAs if one tile per group
-  int64_t grid;
+  const int64_t lo = int64_t(1) << p.tile.n_scat;
+  const int64_t n_hi = p.n_hi;
+  if (n_hi <= 0) return cudaSuccess;
+  // groups per lo class: a power of two (balanced when n_hi is one) filling the
+  // resident capacity, or n_hi / tpg when the tpg knob is set
+  int64_t cap_groups = (int64_t)occ_cache * num_sms() * gpc;
+  if (max_ctas > 0) cap_groups = std::min<int64_t>(cap_groups, (int64_t)max_ctas * gpc);
+  int64_t hi_step;
   const int tpg = knobs().tpg;
   if (tpg > 0) {
-    grid = (n_groups + tpg - 1) / tpg;
+    hi_step = (n_hi + tpg - 1) / tpg;
   } else {
-    grid = (int64_t)occ_cache * num_sms();
+    hi_step = 1;
+    while (hi_step * 2 * lo <= cap_groups) hi_step *= 2;
   }
-  if (grid > n_groups) grid = n_groups;
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (grid > 0x7fffffff) grid = 0x7fffffff;
-  if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst);
+  if (hi_step > n_hi) hi_step = n_hi;
+  if (hi_step < 1) hi_step = 1;
+  const int64_t groups = hi_step * lo;
+  int64_t grid = (groups + gpc - 1) / gpc;
+  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, hi_step);
   return cudaGetLastError();
 }
 

@@ -44,24 +44,31 @@ LL_HD inline void tile_bases(const TileMap& m, int64_t t, int64_t& sb, int64_t& 
 
 // Shared-memory conversion plan (LL_PATH_SMEM): a tile group of 2^gw warps
 // loads a tile with coalesced 16-byte vectors in the planner's load layout,
-// permutes register bits so that the granule bits come first, stores
-// granules to shared memory through the swizzled layout S (paper's optimal
-// swizzling), synchronises, loads granules in the store layout and writes
-// coalesced 16-byte vectors.
+// fixes the sub-word order with prmt where needed, stores granules to shared
+// memory through the swizzled layout S (paper's optimal swizzling) -- the
+// granule's words are picked at compile time from the word bits gsel_a/b --
+// synchronises, loads granules in the store layout and writes coalesced
+// 16-byte vectors.  All in-tile offsets are in BYTES (32-bit).
+//
+// Scheduling: tile index t = (hi << n_scat) | lo.  A group keeps lo fixed (so
+// the scattered part of its offsets is computed once) and walks hi with a
+// stride passed at launch.
 struct SmemPlan {
-  TileMap tile;
+  TileMap tile;         // scat_* in bytes; run shifts in byte-shift; batch strides in bytes
+  int64_t n_hi;         // n_tiles >> n_scat
   int32_t gw;           // log2 warps per tile group
-  int32_t tile_elems;   // elements per tile (smem per buffer)
-  int32_t n_swaps;
-  int8_t swap_a[LL_MAX_SWAPS], swap_b[LL_MAX_SWAPS];  // register-bit swaps (a < b)
-  int64_t ld_thr[LL_MAX_TBITS];   // src element offset per thread bit (lane 0-4, warp-in-group)
-  int64_t st_thr[LL_MAX_TBITS];   // dst element offset per thread bit
-  int64_t ld_vec[LL_MAX_VEC];     // src element offset of 16-B load u
-  int64_t st_vec[LL_MAX_VEC];     // dst element offset of 16-B store u
-  int32_t sw_thr[LL_MAX_TBITS];   // smem element offset (xor) per thread bit, write side
-  int32_t sr_thr[LL_MAX_TBITS];   // read side
-  int32_t sw_gran[LL_MAX_GRAN];   // smem element offset (xor) of write granule j
-  int32_t sr_gran[LL_MAX_GRAN];   // read granule j
+  int32_t tile_bytes;   // bytes per tile (smem per buffer)
+  int32_t n_swaps;      // sub-word register-bit swaps (prmt), swap_a < sub-word bits
+  int8_t swap_a[LL_MAX_SWAPS], swap_b[LL_MAX_SWAPS];
+  int8_t gsel_a, gsel_b;          // register word bits forming a write granule (-1: unused)
+  uint32_t ld_thr[LL_MAX_TBITS];  // src byte offset per thread bit (lane 0-4, warp-in-group)
+  uint32_t st_thr[LL_MAX_TBITS];  // dst byte offset per thread bit
+  uint32_t ld_vec[LL_MAX_VEC];    // src byte offset of 16-B load u
+  uint32_t st_vec[LL_MAX_VEC];    // dst byte offset of 16-B store u
+  uint32_t sw_thr[LL_MAX_TBITS];  // smem byte offset (xor) per thread bit, write side
+  uint32_t sr_thr[LL_MAX_TBITS];  // read side
+  uint32_t sw_gran[LL_MAX_GRAN];  // smem byte offset (xor) of write granule j
+  uint32_t sr_gran[LL_MAX_GRAN];  // read granule j
 };
 
 // Warp-shuffle conversion plan (LL_PATH_SHUFFLE), warp-local tiles.  Word-

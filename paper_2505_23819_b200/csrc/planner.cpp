@@ -241,14 +241,32 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   if (ld_lane.size() != 5 || st_lane.size() != 5 || (int)ld_warp.size() != g ||
       (int)st_warp.size() != g)
     return false;
-  // ---- register-bit swaps on the load side: bring V to rho positions 0..gbits-1
+  // ---- sub-word register-bit swaps on the load side (prmt): the first sw
+  // positions of rho must hold V's sub-word bits; V's word-level bits are
+  // then picked at compile time by the STS operand selection (gsel).
+  const int nsub = w >= 4 ? 0 : ilog2i(4 / w);
   std::vector<int> order = ld_reg;
   std::vector<std::pair<int, int>> swaps;
-  for (int t = 0; t < gbits; ++t) {
+  for (int t = 0; t < std::min(nsub, gbits); ++t) {
     int s = (int)(std::find(order.begin(), order.end(), V[t]) - order.begin());
     if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
   }
   if ((int)swaps.size() > LL_MAX_SWAPS) return false;
+  // register word bit of each rho position (w = 8: word bit 0 = element half)
+  auto wordbit = [&](int rho) { return w == 8 ? rho + 1 : rho - nsub; };
+  const int LB = w == 8 ? r + 1 : r - nsub;   // word-index bits
+  std::vector<int> gsel;                    // word bits forming a granule
+  if (w == 8) gsel.push_back(0);
+  for (int t = (w == 8 ? 0 : nsub); t < gbits; ++t) {
+    int pos = (int)(std::find(order.begin(), order.end(), V[t]) - order.begin());
+    gsel.push_back(wordbit(pos));
+  }
+  if ((int)gsel.size() > 2) return false;
+  std::vector<int> rest_rho;                // rho positions of the remaining word bits (ascending word bit)
+  for (int wb = 0; wb < LB; ++wb) {
+    if (std::find(gsel.begin(), gsel.end(), wb) != gsel.end()) continue;
+    rest_rho.push_back(w == 8 ? wb - 1 : wb + nsub);
+  }
   // ---- tile-local space
   const int d = (int)T.size();
   auto loc = [&](int k) -> u64 {
@@ -276,43 +294,49 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   }
   auto Sinv = f2_right_inverse(Scols, d);  // square, invertible
   auto off = [&](int k) -> int32_t { return (int32_t)f2_apply(Sinv, loc(k)); };
-  // ---- fill the device plan
+  // ---- fill the device plan (all offsets in bytes)
   SmemPlan& sp = P.sp;
   sp = SmemPlan{};
+  const int lw = ilog2i(w);
+  for (int k : T)
+    if (sigma[k] + lw >= 31 || k + lw >= 31) return false;  // 32-bit in-tile byte offsets
   sp.gw = g;
-  sp.tile_elems = 1 << d;
+  sp.tile_bytes = w << d;
   sp.n_swaps = (int)swaps.size();
   for (size_t i = 0; i < swaps.size(); ++i) {
     sp.swap_a[i] = (int8_t)swaps[i].first;
     sp.swap_b[i] = (int8_t)swaps[i].second;
   }
+  sp.gsel_a = gsel.size() > 0 ? (int8_t)gsel[0] : (int8_t)-1;
+  sp.gsel_b = gsel.size() > 1 ? (int8_t)gsel[1] : (int8_t)-1;
+  auto boff = [&](int k) -> uint32_t { return (uint32_t)off(k) << lw; };
   for (int b = 0; b < 5; ++b) {
-    sp.ld_thr[b] = int64_t(1) << sigma[ld_lane[b]];
-    sp.st_thr[b] = int64_t(1) << st_lane[b];
-    sp.sw_thr[b] = off(ld_lane[b]);
-    sp.sr_thr[b] = off(st_lane[b]);
+    sp.ld_thr[b] = uint32_t(w) << sigma[ld_lane[b]];
+    sp.st_thr[b] = uint32_t(w) << st_lane[b];
+    sp.sw_thr[b] = boff(ld_lane[b]);
+    sp.sr_thr[b] = boff(st_lane[b]);
   }
   for (int b = 0; b < g; ++b) {
-    sp.ld_thr[5 + b] = int64_t(1) << sigma[ld_warp[b]];
-    sp.st_thr[5 + b] = int64_t(1) << st_warp[b];
-    sp.sw_thr[5 + b] = off(ld_warp[b]);
-    sp.sr_thr[5 + b] = off(st_warp[b]);
+    sp.ld_thr[5 + b] = uint32_t(w) << sigma[ld_warp[b]];
+    sp.st_thr[5 + b] = uint32_t(w) << st_warp[b];
+    sp.sw_thr[5 + b] = boff(ld_warp[b]);
+    sp.sr_thr[5 + b] = boff(st_warp[b]);
   }
   const int nvec = 1 << (r - vb);
   if (nvec > LL_MAX_VEC) return false;
   for (int u = 0; u < nvec; ++u) {
-    int64_t lo = 0, so = 0;
+    uint32_t lo = 0, so = 0;
     for (int q = 0; q < r - vb; ++q)
-      if ((u >> q) & 1) { lo += int64_t(1) << sigma[ld_reg[vb + q]]; so += int64_t(1) << st_reg[vb + q]; }
+      if ((u >> q) & 1) { lo += uint32_t(w) << sigma[ld_reg[vb + q]]; so += uint32_t(w) << st_reg[vb + q]; }
     sp.ld_vec[u] = lo;
     sp.st_vec[u] = so;
   }
   const int ngran = 1 << (r - gbits);
-  if (ngran > LL_MAX_GRAN) return false;
+  if (ngran > LL_MAX_GRAN || (int)rest_rho.size() != r - gbits) return false;
   for (int j = 0; j < ngran; ++j) {
-    int32_t wo = 0, ro = 0;
+    uint32_t wo = 0, ro = 0;
     for (int q = 0; q < r - gbits; ++q)
-      if ((j >> q) & 1) { wo ^= off(order[gbits + q]); ro ^= off(st_reg[gbits + q]); }
+      if ((j >> q) & 1) { wo ^= boff(order[rest_rho[q]]); ro ^= boff(st_reg[gbits + q]); }
     sp.sw_gran[j] = wo;
     sp.sr_gran[j] = ro;
   }
@@ -328,19 +352,20 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     }
   }
   const int n_scat = (int)O.size() - m;
-  if (n_scat > LL_MAX_SCAT) return false;
+  if (n_scat > LL_MAX_SCAT || n_scat > 20) return false;
   TileMap& tm = sp.tile;
   tm.n_scat = n_scat;
   tm.n_run = m;
-  tm.run_shift_dst = m ? O[n_scat] : 0;
-  tm.run_shift_src = m ? sigma[O[n_scat]] : 0;
+  tm.run_shift_dst = (m ? O[n_scat] : 0) + lw;
+  tm.run_shift_src = (m ? sigma[O[n_scat]] : 0) + lw;
   for (int q = 0; q < n_scat; ++q) {
-    tm.scat_src[q] = int64_t(1) << sigma[O[q]];
-    tm.scat_dst[q] = int64_t(1) << O[q];
+    tm.scat_src[q] = int64_t(w) << sigma[O[q]];
+    tm.scat_dst[q] = int64_t(w) << O[q];
   }
-  tm.batch_stride_src = int64_t(1) << P.nA;
-  tm.batch_stride_dst = int64_t(1) << P.nB;
+  tm.batch_stride_src = int64_t(w) << P.nA;
+  tm.batch_stride_dst = int64_t(w) << P.nB;
   tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
+  sp.n_hi = tm.n_tiles >> n_scat;
   P.nv = nvec;
   P.g = G;
   P.tile_bits = d;
@@ -357,7 +382,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     for (int x : v) o.push_back(sigma[x]);
     return o;
   };
-  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
+  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"gsel\":" << ivec_json(gsel) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
      << ",\"granule_bytes\":" << G << ",\"granule_dst_bits\":" << ivec_json(V)
      << ",\"vectors_per_thread\":" << nvec << ",\"swaps\":[";
   for (size_t i = 0; i < swaps.size(); ++i)

@@ -166,7 +166,10 @@ def _tile_layouts(d):
     B = mk(d["st_reg"], d["st_lane"], d["st_warp"])
     V = [loc[k] for k in d["granule_dst_bits"]]
     S = OLayout([("offset", n)], [("t", n)], {"offset": [(c,) for c in d["S_vect"] + d["S_bank"] + d["S_idx"]]})
-    return A, B, V, S
+    # register bits of one vectorised access: where V sits in each side's register order
+    vA = [d["ld_rho_after_swaps"].index(k) for k in d["granule_dst_bits"]]
+    vB = [d["st_reg"].index(k) for k in d["granule_dst_bits"]]
+    return A, B, V, S, vA, vB
 
 
 PLAN_CASES = [("cfg1a", configs.cfg1("mma")), ("cfg1b", configs.cfg1("T")),
@@ -180,15 +183,14 @@ def test_planner_swizzle_equals_oracle_and_is_conflict_free(name, c):
     w = c["elem_bytes"]
     d = ll.plan_describe(A, B, 8 * w, "smem")
     assert d["path"] == "smem"
-    Ao, Bo, V, S = _tile_layouts(d)
+    Ao, Bo, V, S, vA, vB = _tile_layouts(d)
     # same construction as the oracle's step-by-step implementation of the paper
     So, info = swizzle.optimal_swizzle(Ao, Bo, w, V=V)
     assert So.cols == S.cols
     assert info["H"] == d["H"] and info["C"] == d["C"]
     # brute-force bank counter on the plan's actual accesses: ideal wavefronts
-    vbits = list(range(len(V)))
-    wa = banks.count_wavefronts(S, Ao, w, vbits)
-    wb = banks.count_wavefronts(S, Bo, w, vbits)
+    wa = banks.count_wavefronts(S, Ao, w, vA)
+    wb = banks.count_wavefronts(S, Bo, w, vB)
     n_instr = (1 << (Ao.in_bits - 5)) // (1 << len(V))
     ideal = max(1, ((1 << len(V)) * w) // 4)
     assert wa == n_instr * ideal and wb == n_instr * ideal
@@ -206,12 +208,11 @@ def test_planner_random_pairs_conflict_free(w):
         d = ll.plan_describe(A, B, 8 * w)
         if d["path"] != "smem":
             continue
-        Ao, Bo, V, S = _tile_layouts(d)
-        vbits = list(range(len(V)))
+        Ao, Bo, V, S, vA, vB = _tile_layouts(d)
         n_instr = (1 << (Ao.in_bits - 5)) // (1 << len(V))
         ideal = max(1, ((1 << len(V)) * w) // 4)
-        assert banks.count_wavefronts(S, Ao, w, vbits) == n_instr * ideal
-        assert banks.count_wavefronts(S, Bo, w, vbits) == n_instr * ideal
+        assert banks.count_wavefronts(S, Ao, w, vA) == n_instr * ideal
+        assert banks.count_wavefronts(S, Bo, w, vB) == n_instr * ideal
 
 
 def test_gather_plan_config4():
