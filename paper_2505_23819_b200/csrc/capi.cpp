@@ -77,6 +77,7 @@ const char* ll_version(void) { return "ll_b200 0.1 (sm_100a)"; }
 int64_t ll_launch_count(void) { return g_launches.load(); }
 
 ll_status ll_tune(const char* name, int value) {
+  if (name && ll::set_planner_knob(name, value)) return LL_OK;
   if (ll::set_knob(name, value) != 0)
     return fail(LL_ERR_ARG, std::string("ll_tune: unknown knob '") + (name ? name : "") + "'");
   return LL_OK;

@@ -176,8 +176,11 @@ __host__ __device__ constexpr int deposit_word(int j, int k, int LB, int A, int 
   return idx;
 }
 
+// wbase: (region base + buffer); wx: the thread's xor offset; the swizzled
+// offsets are combined by XOR *within* the region, then added to the base
+// (the dynamic shared window need not be aligned to the tile size).
 template <int NW, int GW, int A, int B>
-__device__ __forceinline__ void sts_granules(const uint32_t (&R)[NW], uint32_t wbase,
+__device__ __forceinline__ void sts_granules(const uint32_t (&R)[NW], uint32_t wbase, uint32_t wx,
                                              const uint32_t* gran) {
   constexpr int LB = ilog2(NW);
   constexpr int NG = NW / GW;
@@ -186,30 +189,30 @@ __device__ __forceinline__ void sts_granules(const uint32_t (&R)[NW], uint32_t w
     uint32_t v[GW];
 #pragma unroll
     for (int k = 0; k < GW; ++k) v[k] = R[deposit_word(j, k, LB, A, B)];
-    sts<GW * 4>(wbase ^ gran[j], v);
+    sts<GW * 4>(wbase + (wx ^ gran[j]), v);
   }
 }
 
 template <int NW, int GW, int A, int B>
 __device__ __forceinline__ bool sts_try_b(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
-                                          const uint32_t* gran) {
+                                          uint32_t wx, const uint32_t* gran) {
   constexpr int LB = ilog2(NW);
   if constexpr (B >= LB) {
     return false;
   } else {
     if constexpr (A != B) {
       if (a == A && b == B) {
-        sts_granules<NW, GW, A, B>(R, wbase, gran);
+        sts_granules<NW, GW, A, B>(R, wbase, wx, gran);
         return true;
       }
     }
-    return sts_try_b<NW, GW, A, B + 1>(a, b, R, wbase, gran);
+    return sts_try_b<NW, GW, A, B + 1>(a, b, R, wbase, wx, gran);
   }
 }
 
 template <int NW, int GW, int A>
 __device__ __forceinline__ bool sts_try_a(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
-                                          const uint32_t* gran) {
+                                          uint32_t wx, const uint32_t* gran) {
   constexpr int LB = ilog2(NW);
   if constexpr (A >= LB) {
     return false;
@@ -218,24 +221,24 @@ __device__ __forceinline__ bool sts_try_a(int a, int b, const uint32_t (&R)[NW],
     if constexpr (GW == 2) {
       done = false;
       if (a == A) {
-        sts_granules<NW, 2, A, -1>(R, wbase, gran);
+        sts_granules<NW, 2, A, -1>(R, wbase, wx, gran);
         done = true;
       }
     } else {
-      done = sts_try_b<NW, GW, A, 0>(a, b, R, wbase, gran);
+      done = sts_try_b<NW, GW, A, 0>(a, b, R, wbase, wx, gran);
     }
     if (done) return true;
-    return sts_try_a<NW, GW, A + 1>(a, b, R, wbase, gran);
+    return sts_try_a<NW, GW, A + 1>(a, b, R, wbase, wx, gran);
   }
 }
 
 template <int NW, int GW>
 __device__ __forceinline__ void sts_dispatch(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
-                                             const uint32_t* gran) {
+                                             uint32_t wx, const uint32_t* gran) {
   if constexpr (GW == 1) {
-    sts_granules<NW, 1, -1, -1>(R, wbase, gran);
+    sts_granules<NW, 1, -1, -1>(R, wbase, wx, gran);
   } else {
-    sts_try_a<NW, GW, 0>(a, b, R, wbase, gran);
+    sts_try_a<NW, GW, 0>(a, b, R, wbase, wx, gran);
   }
 }
 
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const int64_t run_mask = (int64_t(1) << p.tile.n_run) - 1;
 
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * p.tile_bytes;
-  const uint32_t wbase0 = sbase + swx, rbase0 = sbase + srx;
+
   uint32_t buf = 0;
   const int ga = p.gsel_a, gb = p.gsel_b;
 
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   for (; hi < p.n_hi; hi += hi_step) {
     if (!PIPE) load_tile<NV>(R, sthr + src_off(hi), p.ld_vec);
     for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
-    sts_dispatch<NW, GW>(ga, gb, R, wbase0 + buf, p.sw_gran);
+    sts_dispatch<NW, GW>(ga, gb, R, sbase + buf, swx, p.sw_gran);
     if (PIPE) {
       const int64_t hn = hi + hi_step;
       if (hn < p.n_hi) load_tile<NV>(R, sthr + src_off(hn), p.ld_vec);
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
     group_sync(gw, group);
     uint32_t Q[NW];
 #pragma unroll
-    for (int j = 0; j < NG; ++j) lds<G>((rbase0 + buf) ^ p.sr_gran[j], &Q[j * GW]);
+    for (int j = 0; j < NG; ++j) lds<G>(sbase + buf + (srx ^ p.sr_gran[j]), &Q[j * GW]);
     uint8_t* dp = dthr + dst_off(hi);
 #pragma unroll
     for (int u = 0; u < NV; ++u)
@@ -545,10 +548,11 @@ static int env_int(const char* name, int dflt) {
 // group (0 = persistent grid at full occupancy), LL_PIPE = 1 for the
 // software-pipelined kernel.
 struct LaunchKnobs {
-  int tpg, pipe, gather_tpt;
+  int tpg, pipe, gather_tpt, carveout, pow2;
   LaunchKnobs()
       : tpg(env_int("LL_TPG", 0)), pipe(env_int("LL_PIPE", 1)),
-        gather_tpt(env_int("LL_GATHER_VPT", 2)) {}
+        gather_tpt(env_int("LL_GATHER_VPT", 2)), carveout(env_int("LL_CARVEOUT", -1)),
+        pow2(env_int("LL_POW2", 1)) {}
 };
 static LaunchKnobs& knobs() {
   static LaunchKnobs k;
@@ -560,6 +564,8 @@ int set_knob(const char* name, int value) {
   if (n == "tpg") { knobs().tpg = value; return 0; }
   if (n == "pipe") { knobs().pipe = value; return 0; }
   if (n == "gather_vpt") { knobs().gather_tpt = value; return 0; }
+  if (n == "carveout") { knobs().carveout = value; return 0; }
+  if (n == "pow2") { knobs().pow2 = value; return 0; }
   return -1;
 }
 
@@ -572,11 +578,13 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   const size_t smem = (size_t)gpc * 2 * p.tile_bytes;
   static int occ_cache = -1;
   static size_t occ_smem = 0;
-  if (occ_cache < 0 || occ_smem != smem) {
+  static int occ_carve = -2;
+  if (occ_cache < 0 || occ_smem != smem || occ_carve != knobs().carveout) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, knobs().carveout);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
     occ_smem = smem;
+    occ_carve = knobs().carveout;
   }
   if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
   const int64_t lo = int64_t(1) << p.tile.n_scat;
@@ -590,9 +598,11 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   const int tpg = knobs().tpg;
   if (tpg > 0) {
     hi_step = (n_hi + tpg - 1) / tpg;
-  } else {
+  } else if (knobs().pow2) {
     hi_step = 1;
     while (hi_step * 2 * lo <= cap_groups) hi_step *= 2;
+  } else {
+    hi_step = std::max<int64_t>(1, cap_groups / lo);
   }
   if (hi_step > n_hi) hi_step = n_hi;
   if (hi_step < 1) hi_step = 1;

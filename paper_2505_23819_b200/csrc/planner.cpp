@@ -118,6 +118,30 @@ int lemma_wavefronts(const SwizzleResult& s, const std::vector<u64>& lanes, int 
   return n * (1 << inter);
 }
 
+// ------------------------------------------------------------- planner knobs
+namespace {
+std::mutex g_knob_mu;
+std::map<std::string, int> g_knobs;
+int g_knob_version = 0;
+}  // namespace
+
+int planner_knob(const char* name, int dflt) {
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  auto it = g_knobs.find(name);
+  return it == g_knobs.end() ? dflt : it->second;
+}
+int planner_knob_version() {
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  return g_knob_version;
+}
+bool set_planner_knob(const std::string& name, int value) {
+  if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule") return false;
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  g_knobs[name] = value;
+  ++g_knob_version;
+  return true;
+}
+
 // ------------------------------------------------------------- conversion plan
 namespace {
 
@@ -164,8 +188,8 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   auto contains = [](const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
   };
-  const int r_max = ilog2i(128 / w);
-  const int r_pref = ilog2i(64 / w);
+  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
+  const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("thread_bytes", 64)) / w));
   int G = 0, gbits = 0, r = 0;
   std::vector<int> V, need;
   // Granule choice: the largest prefix of the destination vector that the
@@ -173,7 +197,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   // source coalescing bits out of the registers.
   for (int pass = 0; pass < 2 && !G; ++pass) {
     for (int Gc : {16, 8, 4}) {
-      if (Gc < w || Gc < 4) continue;
+      if (Gc < w || Gc < 4 || Gc > planner_knob("max_granule", 16)) continue;
       int gb = ilog2i(Gc / w);
       std::vector<int> Vc(VD.begin(), VD.begin() + gb);
       std::vector<int> nd = VS;
@@ -446,8 +470,9 @@ struct Key {
   u64 a, b;
   int w, path;
   int64_t batch;
+  int knobs;
   bool operator<(const Key& o) const {
-    return std::tie(a, b, w, path, batch) < std::tie(o.a, o.b, o.w, o.path, o.batch);
+    return std::tie(a, b, w, path, batch, knobs) < std::tie(o.a, o.b, o.w, o.path, o.batch, o.knobs);
   }
 };
 
@@ -459,7 +484,7 @@ std::map<Key, std::shared_ptr<const GatherPlanHost>> g_gcache;
 
 std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
                                                     int path_req, int64_t batch) {
-  Key k{A.hash(), B.hash(), w, path_req, batch};
+  Key k{A.hash(), B.hash(), w, path_req, batch, planner_knob_version()};
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_cache.find(k);
@@ -474,7 +499,7 @@ std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layou
 // ------------------------------------------------------------------ gather
 std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
                                                       int path_req, int64_t batch) {
-  Key k{L.hash(), (u64)axis, w, path_req, batch};
+  Key k{L.hash(), (u64)axis, w, path_req, batch, planner_knob_version()};
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_gcache.find(k);

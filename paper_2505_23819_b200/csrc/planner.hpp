@@ -50,6 +50,10 @@ struct GatherPlanHost {
   std::string json;
 };
 
+int planner_knob(const char* name, int dflt);
+int planner_knob_version();
+bool set_planner_knob(const std::string& name, int value);
+
 // path_req: ll_path value (AUTO lets the planner choose).  Throws ll::Error.
 std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
                                                     int path_req, int64_t batch);

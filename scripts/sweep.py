@@ -19,6 +19,10 @@ from workloads import configs  # noqa: E402
 from workloads.values import indices_torch, values_torch  # noqa: E402
 
 
+DEFAULTS = {"tpg": 0, "pipe": 1, "carveout": -1, "pow2": 1, "thread_bytes": 64,
+            "thread_bytes_max": 128, "max_granule": 16}
+
+
 def timeit(step, steps, warm=5):
     for i in range(warm):
         step(i)
@@ -91,8 +95,8 @@ def main():
                                   **ks))
                     except ll.LLError as e:
                         emit({"cfg": cfg, "path": path, "error": str(e)})
-                    ll.tune("tpg", 2)
-                    ll.tune("pipe", 0)
+                    for k, v in DEFAULTS.items():
+                        ll.tune(k, v)
             a = [torch.empty(nbytes // 2, dtype=torch.uint8, device=dev) for _ in range(nsets)]
             b = [torch.empty(nbytes // 2, dtype=torch.uint8, device=dev) for _ in range(nsets)]
         ms = timeit(lambda i: b[i % len(b)].copy_(a[i % len(a)]), args.steps)
