@@ -450,7 +450,9 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constan
 // from h* = (h with axis replaced); one shuffle per candidate register
 // (2^|L_reg^axis|, mask `cand_mask`), keeping the value whose register
 // matches.  Requires the axis to live in the warp's buffer bits (vb + 5).
-template <int W>
+// ALLC: the axis covers every register bit (cand_mask = NE-1): all NE words
+// are shuffled from the source lane and a select tree picks the element.
+template <int W, bool ALLC>
 __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_constant__ GatherPlan p,
                                                              const uint8_t* __restrict__ src,
                                                              const int32_t* __restrict__ idx,
@@ -466,6 +468,8 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
   const uint32_t amask = (1u << p.ax_bits) - 1;
   const int64_t nwarps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_wvec = p.n_vec >> 5;  // warps' worth of vectors
+  const uint64_t clear = ~(uint64_t)p.axis_mask_buf;
+  const int ybase = p.y_base;
   for (int64_t wv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wv < n_wvec;
        wv += nwarps_total) {
     const int64_t v = (wv << 5) | lane;
@@ -496,31 +500,42 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
       uint32_t i = (uint32_t)iv[e];
       if (p.check && i > amask) atomicExch(err, 1);
       i &= amask;
-      uint64_t hs = (h & ~(uint64_t)p.axis_mask_buf) | ((uint64_t)i << p.y_base);
+      const uint64_t hs = (h & clear) | ((uint64_t)i << ybase);
       const int src_lane = (int)((hs >> VB) & 31);
       const int src_reg = (int)(hs & (NE - 1));
-      T val = 0;
-      // candidate rounds: every register index the axis can select, i.e. the
-      // registers that agree with e outside cand_mask (2^|L_reg^axis| shuffles)
+      if constexpr (ALLC && W == 4) {
+        // four shuffles, then a 2-level select on the register index
+        const uint32_t g0 = __shfl_sync(0xffffffffu, sv.w[0], src_lane);
+        const uint32_t g1 = __shfl_sync(0xffffffffu, sv.w[1], src_lane);
+        const uint32_t g2 = __shfl_sync(0xffffffffu, sv.w[2], src_lane);
+        const uint32_t g3 = __shfl_sync(0xffffffffu, sv.w[3], src_lane);
+        const uint32_t lo = (src_reg & 1) ? g1 : g0;
+        const uint32_t hi = (src_reg & 1) ? g3 : g2;
+        o.e[e] = (T)((src_reg & 2) ? hi : lo);
+      } else {
+        T val = 0;
+        // candidate rounds: every register index the axis can select, i.e. the
+        // registers that agree with e outside cand_mask (2^|L_reg^axis| shuffles)
 #pragma unroll
-      for (int c = 0; c < NE; ++c) {
-        if (((c ^ e) & ~p.cand_mask) == 0) {
-          T got;
-          if constexpr (W == 8) {
-            uint32_t lo = __shfl_sync(0xffffffffu, sv.w[2 * c], src_lane);
-            uint32_t hi = __shfl_sync(0xffffffffu, sv.w[2 * c + 1], src_lane);
-            got = (T)(((uint64_t)hi << 32) | lo);
-          } else if constexpr (W == 4) {
-            got = (T)__shfl_sync(0xffffffffu, sv.w[c], src_lane);
-          } else {
-            // sub-word elements: shuffle the containing word, then extract
-            uint32_t wd = __shfl_sync(0xffffffffu, sv.w[(c * W) >> 2], src_lane);
-            got = (T)(wd >> (((c * W) & 3) * 8));
+        for (int c = 0; c < NE; ++c) {
+          if (ALLC || ((c ^ e) & ~p.cand_mask) == 0) {
+            T got;
+            if constexpr (W == 8) {
+              uint32_t lo = __shfl_sync(0xffffffffu, sv.w[2 * c], src_lane);
+              uint32_t hi = __shfl_sync(0xffffffffu, sv.w[2 * c + 1], src_lane);
+              got = (T)(((uint64_t)hi << 32) | lo);
+            } else if constexpr (W == 4) {
+              got = (T)__shfl_sync(0xffffffffu, sv.w[c], src_lane);
+            } else {
+              // sub-word elements: shuffle the containing word, then extract
+              uint32_t wd = __shfl_sync(0xffffffffu, sv.w[(c * W) >> 2], src_lane);
+              got = (T)(wd >> (((c * W) & 3) * 8));
+            }
+            if (src_reg == c) val = got;
           }
-          if (src_reg == c) val = got;
         }
+        o.e[e] = val;
       }
-      o.e[e] = val;
     }
     stg_stream(out + (b * p.batch_stride + h0) * W, o.v4);
   }
@@ -550,7 +565,7 @@ static int env_int(const char* name, int dflt) {
 struct LaunchKnobs {
   int tpg, pipe, gather_tpt, carveout, pow2;
   LaunchKnobs()
-      : tpg(env_int("LL_TPG", 0)), pipe(env_int("LL_PIPE", 1)),
+      : tpg(env_int("LL_TPG", 2)), pipe(env_int("LL_PIPE", 1)),
         gather_tpt(env_int("LL_GATHER_VPT", 2)), carveout(env_int("LL_CARVEOUT", -1)),
         pow2(env_int("LL_POW2", 1)) {}
 };
@@ -678,9 +693,12 @@ static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void
   if (max_ctas > 0 && want > max_ctas) want = max_ctas;
   int grid = (int)(want < 0x7fffffff ? want : 0x7fffffff);
   if (grid < 1) grid = 1;
-  if (shuffle)
-    gather_shuffle_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
-                                                      err);
+  if (shuffle && p.cand_mask == (16 / W) - 1)
+    gather_shuffle_kernel<W, true><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx,
+                                                            (uint8_t*)out, err);
+  else if (shuffle)
+    gather_shuffle_kernel<W, false><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx,
+                                                             (uint8_t*)out, err);
   else
     gather_direct_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
                                                      err);

@@ -135,7 +135,9 @@ int planner_knob_version() {
   return g_knob_version;
 }
 bool set_planner_knob(const std::string& name, int value) {
-  if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule") return false;
+  if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule" &&
+      name != "run_bytes")
+    return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
   ++g_knob_version;
@@ -184,7 +186,9 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   if (n < vb + 5) return false;
   std::vector<int> VD, VS, CD, CS;
   for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
-  for (int k = vb; k < std::min(n, vb + 3); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
+  // coalescing run: run_bytes contiguous bytes on both sides (default one 128-B line)
+  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 128)) / 16));
+  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
   auto contains = [](const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
   };
@@ -255,7 +259,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     for (int x : cand) { if ((int)st_reg.size() == r) break; st_reg.push_back(x); }
     if ((int)st_reg.size() != r) return false;
   }
-  std::vector<int> st_lane = CD, st_warp;
+  std::vector<int> st_lane(CD.begin(), CD.begin() + std::min<size_t>(5, CD.size())), st_warp;
   {
     std::vector<int> cand;
     for (int x : T) if (!contains(st_reg, x) && !contains(st_lane, x)) cand.push_back(x);
