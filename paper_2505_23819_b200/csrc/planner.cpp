@@ -187,7 +187,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   std::vector<int> VD, VS, CD, CS;
   for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
   // coalescing run: run_bytes contiguous bytes on both sides (default one 128-B line)
-  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 128)) / 16));
+  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
   for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
   auto contains = [](const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
