@@ -32,6 +32,13 @@ std::string vec_json(const std::vector<u64>& v) {
   o << "]";
   return o.str();
 }
+std::string u32_json(const uint32_t* v, int n) {
+  std::ostringstream o;
+  o << "[";
+  for (int i = 0; i < n; ++i) o << (i ? "," : "") << v[i];
+  o << "]";
+  return o.str();
+}
 std::string ivec_json(const std::vector<int>& v) {
   std::ostringstream o;
   o << "[";
@@ -426,6 +433,9 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
      << ",\"unavoidable\":" << (sw.unavoidable ? "true" : "false")
      << ",\"pred_wavefronts_per_sts\":" << P.pred_wf_ld
      << ",\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"n_tiles\":" << tm.n_tiles
+     << ",\"smem_bytes\":{\"sw_thr\":" << u32_json(sp.sw_thr, 5 + g) << ",\"sr_thr\":"
+     << u32_json(sp.sr_thr, 5 + g) << ",\"sw_gran\":" << u32_json(sp.sw_gran, ngran)
+     << ",\"sr_gran\":" << u32_json(sp.sr_gran, ngran) << "}"
      << ",\"outer_scattered\":" << n_scat << ",\"outer_run\":" << m;
   return true;
 }
