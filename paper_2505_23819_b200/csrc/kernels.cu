@@ -264,7 +264,7 @@ template <int W, int NV, int G, bool PIPE>
 __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
-                                                           int64_t hi_step) {
+                                                           int64_t n_groups) {
   constexpr int NW = NV * 4;          // 32-bit words per thread
   constexpr int NG = NV * 16 / G;     // granules per thread
   constexpr int GW = G / 4;           // words per granule
@@ -278,12 +278,21 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const int gpc = (blockDim.x >> 5) >> gw;
   const int tbits = 5 + gw;
 
-  // tile schedule: lo fixed per group, hi strided
+  // tile-offset tables: n_tab chunks of LL_TAB_BITS tile-index bits
+  longlong2* tab = reinterpret_cast<longlong2*>(smem);
+  const int n_tab = p.tile.n_tab;
+  for (int e = threadIdx.x; e < (n_tab << LL_TAB_BITS); e += blockDim.x) {
+    const int k = e >> LL_TAB_BITS, v = e & ((1 << LL_TAB_BITS) - 1);
+    long long so = 0, dof = 0;
+    for (int q = 0; q < LL_TAB_BITS; ++q) {
+      const int bit = k * LL_TAB_BITS + q;
+      if (((v >> q) & 1) && bit < p.tile.n_bits) { so += p.tile.bit_src[bit]; dof += p.tile.bit_dst[bit]; }
+    }
+    tab[e] = make_longlong2(so, dof);
+  }
+  __syncthreads();
   const int64_t gid = (int64_t)blockIdx.x * gpc + group;
-  const int lo_bits = p.tile.n_scat;
-  const int64_t lo = gid & ((int64_t(1) << lo_bits) - 1);
-  int64_t hi = gid >> lo_bits;
-  if (hi >= hi_step) return;  // idle group (whole warps: barriers stay consistent)
+  if (gid >= n_groups) return;  // idle group (whole warps: barriers stay consistent)
 
   uint32_t ld_off = 0, st_off = 0, swx = 0, srx = 0;
 #pragma unroll
@@ -295,39 +304,53 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       srx ^= p.sr_thr[b];
     }
   }
-  int64_t slo = 0, dlo = 0;
-  for (int q = 0; q < lo_bits; ++q)
-    if ((lo >> q) & 1) { slo += p.tile.scat_src[q]; dlo += p.tile.scat_dst[q]; }
-  const uint8_t* sthr = src + slo + ld_off;
-  uint8_t* dthr = dst + dlo + st_off;
-  const int64_t run_mask = (int64_t(1) << p.tile.n_run) - 1;
+  const uint8_t* sthr = src + ld_off;
+  uint8_t* dthr = dst + st_off;
+  const int n_bits = p.tile.n_bits;
+  const int64_t rmask = (int64_t(1) << n_bits) - 1;
+  auto tile_off = [&](int64_t t, int64_t& so, int64_t& dof) {
+    const int64_t inst = t >> n_bits;
+    const int64_t r = t & rmask;
+    so = inst * p.tile.batch_stride_src;
+    dof = inst * p.tile.batch_stride_dst;
+    for (int k = 0; k < n_tab; ++k) {
+      const longlong2 e = tab[(k << LL_TAB_BITS) | (int)((r >> (k * LL_TAB_BITS)) & ((1 << LL_TAB_BITS) - 1))];
+      so += e.x;
+      dof += e.y;
+    }
+  };
 
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * p.tile_bytes;
-
+  const uint32_t tiles_base = (uint32_t)__cvta_generic_to_shared(smem) + (n_tab << LL_TAB_BITS) * 16;
+  const uint32_t sbase = tiles_base + group * 2 * p.tile_bytes;
   uint32_t buf = 0;
   const int ga = p.gsel_a, gb = p.gsel_b;
+  const int64_t n_tiles = p.tile.n_tiles;
 
   uint32_t R[NW];
-  auto src_off = [&](int64_t h) -> int64_t {
-    return ((h & run_mask) << p.tile.run_shift_src) + (h >> p.tile.n_run) * p.tile.batch_stride_src;
-  };
-  auto dst_off = [&](int64_t h) -> int64_t {
-    return ((h & run_mask) << p.tile.run_shift_dst) + (h >> p.tile.n_run) * p.tile.batch_stride_dst;
-  };
-  if (PIPE && hi < p.n_hi) load_tile<NV>(R, sthr + src_off(hi), p.ld_vec);
-  for (; hi < p.n_hi; hi += hi_step) {
-    if (!PIPE) load_tile<NV>(R, sthr + src_off(hi), p.ld_vec);
+  int64_t so, dof;
+  int64_t t = gid;
+  if (PIPE && t < n_tiles) {
+    tile_off(t, so, dof);
+    load_tile<NV>(R, sthr + so, p.ld_vec);
+  }
+  for (; t < n_tiles; t += n_groups) {
+    if (!PIPE) tile_off(t, so, dof);
+    if (!PIPE) load_tile<NV>(R, sthr + so, p.ld_vec);
+    const int64_t dcur = dof;
     for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
     sts_dispatch<NW, GW>(ga, gb, R, sbase + buf, swx, p.sw_gran);
     if (PIPE) {
-      const int64_t hn = hi + hi_step;
-      if (hn < p.n_hi) load_tile<NV>(R, sthr + src_off(hn), p.ld_vec);
+      const int64_t tn = t + n_groups;
+      if (tn < n_tiles) {
+        tile_off(tn, so, dof);
+        load_tile<NV>(R, sthr + so, p.ld_vec);
+      }
     }
     group_sync(gw, group);
     uint32_t Q[NW];
 #pragma unroll
     for (int j = 0; j < NG; ++j) lds<G>(sbase + buf + (srx ^ p.sr_gran[j]), &Q[j * GW]);
-    uint8_t* dp = dthr + dst_off(hi);
+    uint8_t* dp = dthr + dcur;
 #pragma unroll
     for (int u = 0; u < NV; ++u)
       stg_stream(dp + p.st_vec[u], make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
@@ -567,7 +590,7 @@ struct LaunchKnobs {
   LaunchKnobs()
       : tpg(env_int("LL_TPG", 2)), pipe(env_int("LL_PIPE", 1)),
         gather_tpt(env_int("LL_GATHER_VPT", 2)), carveout(env_int("LL_CARVEOUT", -1)),
-        pow2(env_int("LL_POW2", 1)) {}
+        pow2(env_int("LL_POW2", 0)) {}
 };
 static LaunchKnobs& knobs() {
   static LaunchKnobs k;
@@ -590,7 +613,7 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   auto k = convert_smem_kernel<W, NV, G, PIPE>;
   const int threads = 256;
   const int gpc = (threads / 32) >> p.gw;
-  const size_t smem = (size_t)gpc * 2 * p.tile_bytes;
+  const size_t smem = (size_t)gpc * 2 * p.tile_bytes + ((size_t)p.tile.n_tab << LL_TAB_BITS) * 16;
   static int occ_cache = -1;
   static size_t occ_smem = 0;
   static int occ_carve = -2;
@@ -602,29 +625,17 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
     occ_carve = knobs().carveout;
   }
   if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
-  const int64_t lo = int64_t(1) << p.tile.n_scat;
-  const int64_t n_hi = p.n_hi;
-  if (n_hi <= 0) return cudaSuccess;
-  // groups per lo class: a power of two (balanced when n_hi is one) filling the
-  // resident capacity, or n_hi / tpg when the tpg knob is set
-  int64_t cap_groups = (int64_t)occ_cache * num_sms() * gpc;
-  if (max_ctas > 0) cap_groups = std::min<int64_t>(cap_groups, (int64_t)max_ctas * gpc);
-  int64_t hi_step;
+  const int64_t n_tiles = p.tile.n_tiles;
+  if (n_tiles <= 0) return cudaSuccess;
+  // tile groups: n_tiles / tpg (the hardware block scheduler balances the
+  // tail), or the resident capacity when tpg = 0 (persistent)
   const int tpg = knobs().tpg;
-  if (tpg > 0) {
-    hi_step = (n_hi + tpg - 1) / tpg;
-  } else if (knobs().pow2) {
-    hi_step = 1;
-    while (hi_step * 2 * lo <= cap_groups) hi_step *= 2;
-  } else {
-    hi_step = std::max<int64_t>(1, cap_groups / lo);
-  }
-  if (hi_step > n_hi) hi_step = n_hi;
-  if (hi_step < 1) hi_step = 1;
-  const int64_t groups = hi_step * lo;
-  int64_t grid = (groups + gpc - 1) / gpc;
+  int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)occ_cache * num_sms() * gpc;
+  if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
+  groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
+  const int64_t grid = (groups + gpc - 1) / gpc;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, hi_step);
+  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,6 @@
 #define LL_HD __host__ __device__
 #endif
 
-#define LL_MAX_SCAT 40   // scattered outer (tile-index) bits
 #define LL_MAX_VEC 16    // 16-byte global vectors per thread per side
 #define LL_MAX_GRAN 64   // shared-memory granules per thread per side
 #define LL_MAX_TBITS 8   // thread bits inside a tile group: 5 lane + <= 3 warp
@@ -19,28 +18,20 @@
 
 namespace ll {
 
-// Tile index t -> element offset of the tile in src and dst.  The low n_scat
-// bits of t are "scattered" outer bits (each adds a fixed offset); the next
-// n_run bits are an identity run (shifted); bits above are the batch index.
+// Tile index t -> byte offsets of the tile in src and dst.  t = inst * 2^n_bits
+// + r; the bits of r (in the planner's tile order) each add a fixed offset.
+// The smem kernel tabulates r's bits in chunks of LL_TAB_BITS in shared
+// memory, so one tile costs n_tab table reads and adds.
+#define LL_MAX_OUTER 32
+#define LL_TAB_BITS 8
 struct TileMap {
-  int64_t n_tiles;
-  int32_t n_scat, n_run;
-  int32_t run_shift_src, run_shift_dst;
-  int64_t batch_stride_src, batch_stride_dst;  // elements
-  int64_t scat_src[LL_MAX_SCAT];
-  int64_t scat_dst[LL_MAX_SCAT];
+  int64_t n_tiles;                               // tiles incl. batch
+  int32_t n_bits;                                // outer bits per layout instance
+  int32_t n_tab;                                 // ceil(n_bits / LL_TAB_BITS)
+  int64_t batch_stride_src, batch_stride_dst;    // bytes per layout instance
+  int64_t bit_src[LL_MAX_OUTER];                 // bytes, in tile-index order
+  int64_t bit_dst[LL_MAX_OUTER];
 };
-
-LL_HD inline void tile_bases(const TileMap& m, int64_t t, int64_t& sb, int64_t& db) {
-  int64_t s = 0, d = 0;
-  for (int q = 0; q < m.n_scat; ++q)
-    if ((t >> q) & 1) { s += m.scat_src[q]; d += m.scat_dst[q]; }
-  int64_t hi = t >> m.n_scat;
-  int64_t run = hi & ((int64_t(1) << m.n_run) - 1);
-  int64_t b = hi >> m.n_run;
-  sb = s + (run << m.run_shift_src) + b * m.batch_stride_src;
-  db = d + (run << m.run_shift_dst) + b * m.batch_stride_dst;
-}
 
 // Shared-memory conversion plan (LL_PATH_SMEM): a tile group of 2^gw warps
 // loads a tile with coalesced 16-byte vectors in the planner's load layout,
@@ -50,12 +41,9 @@ LL_HD inline void tile_bases(const TileMap& m, int64_t t, int64_t& sb, int64_t& 
 // synchronises, loads granules in the store layout and writes coalesced
 // 16-byte vectors.  All in-tile offsets are in BYTES (32-bit).
 //
-// Scheduling: tile index t = (hi << n_scat) | lo.  A group keeps lo fixed (so
-// the scattered part of its offsets is computed once) and walks hi with a
-// stride passed at launch.
+// Scheduling: grid-stride loop over tile indices (planner's tile order).
 struct SmemPlan {
-  TileMap tile;         // scat_* in bytes; run shifts in byte-shift; batch strides in bytes
-  int64_t n_hi;         // n_tiles >> n_scat
+  TileMap tile;
   int32_t gw;           // log2 warps per tile group
   int32_t tile_bytes;   // bytes per tile (smem per buffer)
   int32_t n_swaps;      // sub-word register-bit swaps (prmt), swap_a < sub-word bits

@@ -143,7 +143,7 @@ int planner_knob_version() {
 }
 bool set_planner_knob(const std::string& name, int value) {
   if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule" &&
-      name != "run_bytes")
+      name != "run_bytes" && name != "tile_order")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -375,32 +375,40 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     sp.sw_gran[j] = wo;
     sp.sr_gran[j] = ro;
   }
-  // ---- tile map: outer dst bits, identity run at the top
+  // ---- tile map: outer dst bits in the planner's tile order.  Order 2
+  // (default) interleaves "next lowest destination bit" and "next lowest
+  // source bit", so the tiles in flight at the same time form a 2-D block
+  // that is contiguous in both buffers (DRAM locality for transposes).
   std::vector<int> O;
   for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
-  int m = 0;
-  if (!O.empty()) {
-    m = 1;
-    while (m < (int)O.size()) {
-      int a = O[O.size() - m - 1], b = O[O.size() - m];
-      if (b == a + 1 && sigma[b] == sigma[a] + 1) ++m; else break;
+  if ((int)O.size() > LL_MAX_OUTER) return false;
+  std::vector<int> by_dst = O, by_src = O;
+  std::sort(by_src.begin(), by_src.end(), [&](int a, int b) { return sigma[a] < sigma[b]; });
+  const int order_knob = planner_knob("tile_order", 2);
+  std::vector<int> torder;
+  if (order_knob == 0) {
+    torder = by_dst;
+  } else if (order_knob == 1) {
+    torder = by_src;
+  } else {
+    size_t i = 0, j = 0;
+    while (torder.size() < O.size()) {
+      while (i < by_dst.size() && contains(torder, by_dst[i])) ++i;
+      if (i < by_dst.size()) torder.push_back(by_dst[i]);
+      while (j < by_src.size() && contains(torder, by_src[j])) ++j;
+      if (j < by_src.size() && torder.size() < O.size()) torder.push_back(by_src[j]);
     }
   }
-  const int n_scat = (int)O.size() - m;
-  if (n_scat > LL_MAX_SCAT || n_scat > 20) return false;
   TileMap& tm = sp.tile;
-  tm.n_scat = n_scat;
-  tm.n_run = m;
-  tm.run_shift_dst = (m ? O[n_scat] : 0) + lw;
-  tm.run_shift_src = (m ? sigma[O[n_scat]] : 0) + lw;
-  for (int q = 0; q < n_scat; ++q) {
-    tm.scat_src[q] = int64_t(w) << sigma[O[q]];
-    tm.scat_dst[q] = int64_t(w) << O[q];
+  tm.n_bits = (int)torder.size();
+  tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
+  for (int q = 0; q < tm.n_bits; ++q) {
+    tm.bit_src[q] = int64_t(w) << sigma[torder[q]];
+    tm.bit_dst[q] = int64_t(w) << torder[q];
   }
   tm.batch_stride_src = int64_t(w) << P.nA;
   tm.batch_stride_dst = int64_t(w) << P.nB;
   tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
-  sp.n_hi = tm.n_tiles >> n_scat;
   P.nv = nvec;
   P.g = G;
   P.tile_bits = d;
@@ -436,7 +444,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
      << ",\"smem_bytes\":{\"sw_thr\":" << u32_json(sp.sw_thr, 5 + g) << ",\"sr_thr\":"
      << u32_json(sp.sr_thr, 5 + g) << ",\"sw_gran\":" << u32_json(sp.sw_gran, ngran)
      << ",\"sr_gran\":" << u32_json(sp.sr_gran, ngran) << "}"
-     << ",\"outer_scattered\":" << n_scat << ",\"outer_run\":" << m;
+     << ",\"tile_order_dst_bits\":" << ivec_json(torder);
   return true;
 }
 
