@@ -278,19 +278,6 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const int gpc = (blockDim.x >> 5) >> gw;
   const int tbits = 5 + gw;
 
-  // tile-offset tables: n_tab chunks of LL_TAB_BITS tile-index bits
-  longlong2* tab = reinterpret_cast<longlong2*>(smem);
-  const int n_tab = p.tile.n_tab;
-  for (int e = threadIdx.x; e < (n_tab << LL_TAB_BITS); e += blockDim.x) {
-    const int k = e >> LL_TAB_BITS, v = e & ((1 << LL_TAB_BITS) - 1);
-    long long so = 0, dof = 0;
-    for (int q = 0; q < LL_TAB_BITS; ++q) {
-      const int bit = k * LL_TAB_BITS + q;
-      if (((v >> q) & 1) && bit < p.tile.n_bits) { so += p.tile.bit_src[bit]; dof += p.tile.bit_dst[bit]; }
-    }
-    tab[e] = make_longlong2(so, dof);
-  }
-  __syncthreads();
   const int64_t gid = (int64_t)blockIdx.x * gpc + group;
   if (gid >= n_groups) return;  // idle group (whole warps: barriers stay consistent)
 
@@ -307,21 +294,24 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const uint8_t* sthr = src + ld_off;
   uint8_t* dthr = dst + st_off;
   const int n_bits = p.tile.n_bits;
+  const int n_tab = p.tile.n_tab;
   const int64_t rmask = (int64_t(1) << n_bits) - 1;
   auto tile_off = [&](int64_t t, int64_t& so, int64_t& dof) {
     const int64_t inst = t >> n_bits;
     const int64_t r = t & rmask;
     so = inst * p.tile.batch_stride_src;
     dof = inst * p.tile.batch_stride_dst;
-    for (int k = 0; k < n_tab; ++k) {
-      const longlong2 e = tab[(k << LL_TAB_BITS) | (int)((r >> (k * LL_TAB_BITS)) & ((1 << LL_TAB_BITS) - 1))];
-      so += e.x;
-      dof += e.y;
+#pragma unroll
+    for (int k = 0; k < LL_MAX_TAB; ++k) {
+      if (k < n_tab) {
+        const TileTab& e = p.tile.tab[k][(int)((r >> (k * LL_TAB_BITS)) & ((1 << LL_TAB_BITS) - 1))];
+        so += e.src;
+        dof += e.dst;
+      }
     }
   };
 
-  const uint32_t tiles_base = (uint32_t)__cvta_generic_to_shared(smem) + (n_tab << LL_TAB_BITS) * 16;
-  const uint32_t sbase = tiles_base + group * 2 * p.tile_bytes;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * p.tile_bytes;
   uint32_t buf = 0;
   const int ga = p.gsel_a, gb = p.gsel_b;
   const int64_t n_tiles = p.tile.n_tiles;
@@ -613,7 +603,7 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   auto k = convert_smem_kernel<W, NV, G, PIPE>;
   const int threads = 256;
   const int gpc = (threads / 32) >> p.gw;
-  const size_t smem = (size_t)gpc * 2 * p.tile_bytes + ((size_t)p.tile.n_tab << LL_TAB_BITS) * 16;
+  const size_t smem = (size_t)gpc * 2 * p.tile_bytes;
   static int occ_cache = -1;
   static size_t occ_smem = 0;
   static int occ_carve = -2;

@@ -20,17 +20,22 @@ namespace ll {
 
 // Tile index t -> byte offsets of the tile in src and dst.  t = inst * 2^n_bits
 // + r; the bits of r (in the planner's tile order) each add a fixed offset.
-// The smem kernel tabulates r's bits in chunks of LL_TAB_BITS in shared
-// memory, so one tile costs n_tab table reads and adds.
-#define LL_MAX_OUTER 32
+// The planner tabulates r in chunks of LL_TAB_BITS bits (tab[k][v] = offsets
+// of chunk k having value v); the tables live in the kernel parameters
+// (constant bank) and are indexed warp-uniformly, so a tile costs n_tab
+// constant loads and adds.
+#define LL_MAX_OUTER 24
 #define LL_TAB_BITS 8
+#define LL_MAX_TAB 3
+struct TileTab {
+  int64_t src, dst;
+};
 struct TileMap {
   int64_t n_tiles;                               // tiles incl. batch
   int32_t n_bits;                                // outer bits per layout instance
   int32_t n_tab;                                 // ceil(n_bits / LL_TAB_BITS)
   int64_t batch_stride_src, batch_stride_dst;    // bytes per layout instance
-  int64_t bit_src[LL_MAX_OUTER];                 // bytes, in tile-index order
-  int64_t bit_dst[LL_MAX_OUTER];
+  TileTab tab[LL_MAX_TAB][1 << LL_TAB_BITS];     // bytes
 };
 
 // Shared-memory conversion plan (LL_PATH_SMEM): a tile group of 2^gw warps

@@ -402,9 +402,19 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   TileMap& tm = sp.tile;
   tm.n_bits = (int)torder.size();
   tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
-  for (int q = 0; q < tm.n_bits; ++q) {
-    tm.bit_src[q] = int64_t(w) << sigma[torder[q]];
-    tm.bit_dst[q] = int64_t(w) << torder[q];
+  for (int k = 0; k < tm.n_tab; ++k) {
+    for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
+      int64_t so = 0, dof = 0;
+      for (int q = 0; q < LL_TAB_BITS; ++q) {
+        const int bit = k * LL_TAB_BITS + q;
+        if (((v >> q) & 1) && bit < tm.n_bits) {
+          so += int64_t(w) << sigma[torder[bit]];
+          dof += int64_t(w) << torder[bit];
+        }
+      }
+      tm.tab[k][v].src = so;
+      tm.tab[k][v].dst = dof;
+    }
   }
   tm.batch_stride_src = int64_t(w) << P.nA;
   tm.batch_stride_dst = int64_t(w) << P.nB;
