@@ -384,7 +384,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   if ((int)O.size() > LL_MAX_OUTER) return false;
   std::vector<int> by_dst = O, by_src = O;
   std::sort(by_src.begin(), by_src.end(), [&](int a, int b) { return sigma[a] < sigma[b]; });
-  const int order_knob = planner_knob("tile_order", 2);
+  const int order_knob = planner_knob("tile_order", 0);
   std::vector<int> torder;
   if (order_knob == 0) {
     torder = by_dst;

@@ -20,7 +20,7 @@ from workloads.values import indices_torch, values_torch  # noqa: E402
 
 
 DEFAULTS = {"tpg": 2, "pipe": 1, "carveout": -1, "pow2": 0, "thread_bytes": 64,
-            "thread_bytes_max": 128, "max_granule": 16, "run_bytes": 256, "tile_order": 2}
+            "thread_bytes_max": 128, "max_granule": 16, "run_bytes": 256, "tile_order": 0}
 
 
 def timeit(step, steps, warm=5):
@@ -101,6 +101,12 @@ def main():
             b = [torch.empty(nbytes // 2, dtype=torch.uint8, device=dev) for _ in range(nsets)]
         ms = timeit(lambda i: b[i % len(b)].copy_(a[i % len(a)]), args.steps)
         emit({"cfg": cfg, "path": "torch_copy_same_bytes", "ms": ms, "GBps": nbytes / ms / 1e6})
+        if cfg == "3":
+            m = 1 << 13
+            ta = [values_torch(m * m, 3 + s, 2, dev).view(m, m) for s in range(2)]
+            tb = [torch.empty(m, m, dtype=torch.int16, device=dev) for _ in range(2)]
+            ms = timeit(lambda i: tb[i % 2].copy_(ta[i % 2].t()), args.steps)
+            emit({"cfg": cfg, "path": "torch_transpose_copy", "ms": ms, "GBps": nbytes / ms / 1e6})
     with open(args.out, "w") as f:
         json.dump(res, f, indent=1)
 
