@@ -279,6 +279,10 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
         ++g_launches;
         return cuda_status(cudaMemcpyAsync(dst, src, dst_bytes * batch, cudaMemcpyDeviceToDevice, st),
                            "ll_convert (copy)");
+      case LL_PATH_SHUFFLE:
+        ++g_launches;
+        return cuda_status(ll::launch_convert_shuffle(P->shp, w, P->nv, src, dst, max_ctas, st),
+                           "ll_convert (shuffle kernel)");
       case LL_PATH_SMEM:
       case LL_PATH_SMEM_NOSWIZZLE:
         ++g_launches;

@@ -64,26 +64,29 @@ struct SmemPlan {
   uint32_t sr_gran[LL_MAX_GRAN];  // read granule j
 };
 
-// Warp-shuffle conversion plan (LL_PATH_SHUFFLE), warp-local tiles.  Word-
-// granular exchange (32-bit payload): per round k every lane sends
-// word k of its (lane-permuted) register file and receives into word k; the
-// lane-dependent parts are XOR masks on the word index.
+// Warp-shuffle conversion plan (LL_PATH_SHUFFLE): warp-local tiles exchanged
+// with shfl.sync.  The payload is one 32-bit word; the
+// load side first makes each word hold the same sub-word elements as on the
+// store side (prmt swaps), so the exchange is word-granular.  Round k of the
+// paper's 2^|R| rounds moves, for every lane l, the word
+//   send  S[k] = R[alpha(k) ^ beta(l)]        from lane  gamma(k) ^ delta(l)
+//   recv  Q[eps(k) ^ zeta(l)] = received word
+// alpha and eps^{-1} are uniform linear maps of the word index, applied as a
+// short list of elementary register operations (bit swaps / bit xors);
+// beta(l), zeta(l) are lane-dependent XOR masks applied with selects.
+#define LL_MAX_LINOPS 12
 struct ShufflePlan {
   TileMap tile;
-  int32_t n_swaps_ld;
-  int8_t swap_a[LL_MAX_SWAPS], swap_b[LL_MAX_SWAPS];   // load-side register-bit swaps
-  int64_t ld_thr[5], st_thr[5];
-  int64_t ld_vec[LL_MAX_VEC], st_vec[LL_MAX_VEC];
-  // send side: word index of round k = k ^ send_xor(lane)
-  int32_t send_lane_xor[5];        // per lane bit: xor into the send word index
-  // source lane of round k for lane l = src_lane_base(l) ^ src_lane_round(k)
-  int32_t srcl_lane[5];            // per lane bit
-  int32_t srcl_round[LL_MAX_GRAN]; // per round (word index)
-  // receive: word k received lands at word dst_word(k, lane) = k ^ recv_xor(lane) after
-  // the final permutation given by the store-side word map
-  int32_t recv_lane_xor[5];
-  int32_t recv_perm[LL_MAX_GRAN];  // uniform word permutation after the exchange
-  int32_t send_perm[LL_MAX_GRAN];  // uniform word permutation before the exchange
+  int32_t n_swaps;
+  int8_t swap_a[LL_MAX_SWAPS], swap_b[LL_MAX_SWAPS];   // sub-word swaps (as SmemPlan)
+  uint32_t ld_thr[5], st_thr[5];                       // byte offsets per lane bit
+  uint32_t ld_vec[LL_MAX_VEC], st_vec[LL_MAX_VEC];     // byte offsets per 16-B vector
+  int32_t n_pre, n_post;                               // elementary ops (word-index bits)
+  int8_t pre_op[LL_MAX_LINOPS], pre_a[LL_MAX_LINOPS], pre_b[LL_MAX_LINOPS];
+  int8_t post_op[LL_MAX_LINOPS], post_a[LL_MAX_LINOPS], post_b[LL_MAX_LINOPS];
+  uint32_t beta_lane[5], zeta_lane[5], delta_lane[5];  // per lane bit
+  uint32_t beta_any, zeta_any;                         // OR of the masks (which bits can flip)
+  uint8_t gamma[LL_MAX_GRAN];                          // per round: xor into the source lane
 };
 
 // Generic pull kernel (LL_PATH_GENERIC): dst[h] = src[X h] for every h.

@@ -9,6 +9,7 @@
 #include "planner.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -177,9 +178,41 @@ void fill_generic(ConvertPlan& P, const std::vector<u64>& X) {
   g.n_vec = per * P.batch;
 }
 
+
+// ------------------------------------------------ word-index linear maps
+// Column-reduce an invertible LB x LB matrix M (columns = images of unit
+// vectors) to the identity; returns the elementary array operations E1..Em
+// such that applying them in order to an array T (T'[k] = T[E k]) yields
+// T'[k] = T[M k].  op 0 = swap bits (a, b); op 1 = "if bit a set, flip bit b".
+bool linop_factor(std::vector<u64> M, int LB, std::vector<std::array<int, 3>>& ops) {
+  std::vector<std::array<int, 3>> F;  // recorded column operations, in order
+  for (int j = 0; j < LB; ++j) {
+    int piv = -1;
+    for (int c = j; c < LB; ++c)
+      if ((M[c] >> j) & 1) { piv = c; break; }
+    if (piv < 0) return false;
+    if (piv != j) { std::swap(M[piv], M[j]); F.push_back({0, j, piv}); }
+    for (int q = 0; q < LB; ++q)
+      if (q != j && ((M[q] >> j) & 1)) { M[q] ^= M[j]; F.push_back({1, q, j}); }
+  }
+  ops.assign(F.rbegin(), F.rend());
+  return true;
+}
+
+u64 linop_apply_index(const std::array<int, 3>& op, u64 k) {
+  if (op[0] == 0) {
+    u64 ba = (k >> op[1]) & 1, bb = (k >> op[2]) & 1;
+    if (ba != bb) k ^= (u64(1) << op[1]) | (u64(1) << op[2]);
+    return k;
+  }
+  if ((k >> op[1]) & 1) k ^= u64(1) << op[2];
+  return k;
+}
+
 // Try to build the shared-memory tile plan; returns false if X is not a bit
 // permutation or the tile does not fit.
-bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ostringstream& js) {
+bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ostringstream& js,
+               bool warp_tile = false) {
   const int n = P.nB, w = P.w;
   if (P.nA != P.nB || n > 62) return false;
   std::vector<int> sigma(n), sinv(n, -1);
@@ -194,7 +227,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   std::vector<int> VD, VS, CD, CS;
   for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
   // coalescing run: run_bytes contiguous bytes on both sides (default one 128-B line)
-  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
+  const int cbits = warp_tile ? 3 : std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
   for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
   auto contains = [](const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
@@ -429,6 +462,158 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   P.pred_wf_ld = lemma_wavefronts(sw, Al, w);
   P.pred_wf_st = lemma_wavefronts(sw, Bw, w);
   if (!swizzle) { P.pred_wf_ld = -1; P.pred_wf_st = -1; }
+  // ---- warp-shuffle exchange, warp tiles only (g == 0), word payload
+  P.shuffle_ok = false;
+  std::ostringstream sjs;
+  if (g == 0 && w <= 4 && swizzle) {
+    // word-level coordinates: tile-local unit vectors of the word bits / lanes
+    std::vector<u64> Aw, Al5, Bw, Bl5;
+    for (int b = 0; b < LB; ++b) Aw.push_back(loc(order[b + nsub]));
+    for (int b = 0; b < LB; ++b) Bw.push_back(loc(st_reg[b + nsub]));
+    for (int c = 0; c < 5; ++c) { Al5.push_back(loc(ld_lane[c])); Bl5.push_back(loc(st_lane[c])); }
+    // I, E, F (ascending), G = {e_i ^ f_i}, R completes span(I u G)
+    std::vector<u64> I, E, F, Gv, R;
+    for (u64 x : Al5) if (std::find(Bl5.begin(), Bl5.end(), x) != Bl5.end()) I.push_back(x);
+    for (u64 x : Al5) if (std::find(I.begin(), I.end(), x) == I.end()) E.push_back(x);
+    for (u64 x : Bl5) if (std::find(I.begin(), I.end(), x) == I.end()) F.push_back(x);
+    std::sort(I.begin(), I.end());
+    std::sort(E.begin(), E.end());
+    std::sort(F.begin(), F.end());
+    for (size_t i = 0; i < E.size() && i < F.size(); ++i) Gv.push_back(E[i] ^ F[i]);
+    {
+      F2Basis bs;
+      for (u64 x : I) bs.add(x);
+      for (u64 x : Gv) bs.add(x);
+      std::vector<u64> units;
+      for (u64 x : Aw) units.push_back(x);
+      for (u64 x : Al5) units.push_back(x);
+      std::sort(units.begin(), units.end());
+      for (u64 x : units) if (bs.add(x)) R.push_back(x);
+    }
+    const int NWd = 1 << LB;
+    bool ok = E.size() == F.size() && (int)R.size() == LB && NWd <= LL_MAX_GRAN;
+    // decompose word-level vectors in the ld and st bases
+    auto decomp = [&](u64 x, const std::vector<u64>& wv, const std::vector<u64>& lv, int& word,
+                      int& lane) {
+      word = 0; lane = 0;
+      for (int b = 0; b < (int)wv.size(); ++b) if (x & wv[b]) word |= 1 << b;
+      for (int c = 0; c < 5; ++c) if (x & lv[c]) lane |= 1 << c;
+    };
+    std::vector<u64> span5;
+    if (ok) {
+      std::vector<u64> gen = I;
+      gen.insert(gen.end(), Gv.begin(), Gv.end());
+      span5.push_back(0);
+      for (u64 gvec : gen) {
+        size_t n0 = span5.size();
+        for (size_t i = 0; i < n0; ++i) span5.push_back(span5[i] ^ gvec);
+      }
+      ok = span5.size() == 32;
+    }
+    std::vector<int> ws(32 * NWd, -1), sl(32 * NWd, -1), wr(32 * NWd, -1);
+    for (int k = 0; ok && k < NWd; ++k) {
+      u64 Rk = 0;
+      for (int j = 0; j < LB; ++j) if ((k >> j) & 1) Rk ^= R[j];
+      for (u64 y : span5) {
+        const u64 x = Rk ^ y;
+        int aw, al, bw, bl;
+        decomp(x, Aw, Al5, aw, al);
+        decomp(x, Bw, Bl5, bw, bl);
+        if (ws[al * NWd + k] >= 0 || wr[bl * NWd + k] >= 0) { ok = false; break; }  // one send / recv per lane
+        ws[al * NWd + k] = aw;
+        sl[bl * NWd + k] = al;
+        wr[bl * NWd + k] = bw;
+      }
+    }
+    std::vector<u64> alpha(LB), epsm(LB);
+    ShufflePlan& sh = P.shp;
+    sh = ShufflePlan{};
+    if (ok) {
+      // linear decomposition: ws(l,k) = alpha(k) ^ beta(l), etc. (checked)
+      for (int l = 0; l < 32 && ok; ++l)
+        for (int k = 0; k < NWd && ok; ++k) {
+          ok = ws[l * NWd + k] == (ws[k] ^ ws[l * NWd]) && sl[l * NWd + k] == (sl[k] ^ sl[l * NWd]) &&
+               wr[l * NWd + k] == (wr[k] ^ wr[l * NWd]);
+        }
+    }
+    std::vector<std::array<int, 3>> pre, post;
+    if (ok) {
+      for (int j = 0; j < LB; ++j) { alpha[j] = (u64)ws[1 << j]; epsm[j] = (u64)wr[1 << j]; }
+      // eps^{-1}
+      std::vector<u64> einv(LB, 0);
+      for (int m = 0; m < NWd; ++m) {
+        int e = 0;
+        for (int j = 0; j < LB; ++j) if ((m >> j) & 1) e ^= (int)epsm[j];
+        for (int j = 0; j < LB; ++j) if (e == (1 << j)) einv[j] = (u64)m;
+      }
+      ok = linop_factor(alpha, LB, pre) && linop_factor(einv, LB, post) &&
+           (int)pre.size() <= LL_MAX_LINOPS && (int)post.size() <= LL_MAX_LINOPS;
+      // verify the factorisations by applying them to index arrays
+      for (int pass = 0; ok && pass < 2; ++pass) {
+        const auto& ops = pass ? post : pre;
+        std::vector<int> T(NWd);
+        for (int k = 0; k < NWd; ++k) T[k] = k;
+        for (const auto& op : ops) {
+          std::vector<int> T2(NWd);
+          for (int k = 0; k < NWd; ++k) T2[k] = T[(int)linop_apply_index(op, (u64)k)];
+          T = T2;
+        }
+        for (int k = 0; k < NWd && ok; ++k) {
+          int want = 0;
+          for (int j = 0; j < LB; ++j) if ((k >> j) & 1) want ^= (int)(pass ? einv[j] : alpha[j]);
+          ok = T[k] == want;
+        }
+      }
+    }
+    if (ok) {
+      sh.tile = sp.tile;
+      sh.n_swaps = sp.n_swaps;
+      for (int i = 0; i < LL_MAX_SWAPS; ++i) { sh.swap_a[i] = sp.swap_a[i]; sh.swap_b[i] = sp.swap_b[i]; }
+      for (int c = 0; c < 5; ++c) {
+        sh.ld_thr[c] = sp.ld_thr[c];
+        sh.st_thr[c] = sp.st_thr[c];
+        sh.beta_lane[c] = (uint32_t)ws[(1 << c) * NWd];
+        sh.delta_lane[c] = (uint32_t)sl[(1 << c) * NWd];
+        sh.zeta_lane[c] = (uint32_t)wr[(1 << c) * NWd];
+        sh.beta_any |= sh.beta_lane[c];
+        sh.zeta_any |= sh.zeta_lane[c];
+      }
+      for (int u = 0; u < LL_MAX_VEC; ++u) { sh.ld_vec[u] = sp.ld_vec[u]; sh.st_vec[u] = sp.st_vec[u]; }
+      sh.n_pre = (int)pre.size();
+      sh.n_post = (int)post.size();
+      for (size_t i = 0; i < pre.size(); ++i) {
+        sh.pre_op[i] = (int8_t)pre[i][0]; sh.pre_a[i] = (int8_t)pre[i][1]; sh.pre_b[i] = (int8_t)pre[i][2];
+      }
+      for (size_t i = 0; i < post.size(); ++i) {
+        sh.post_op[i] = (int8_t)post[i][0]; sh.post_a[i] = (int8_t)post[i][1]; sh.post_b[i] = (int8_t)post[i][2];
+      }
+      for (int k = 0; k < NWd; ++k) sh.gamma[k] = (uint8_t)sl[k];
+      P.shuffle_ok = true;
+      P.shuffle_rounds = NWd;
+    }
+    auto ops_json = [](const std::vector<std::array<int, 3>>& ops) {
+      std::ostringstream o;
+      o << "[";
+      for (size_t i = 0; i < ops.size(); ++i)
+        o << (i ? "," : "") << "[" << ops[i][0] << "," << ops[i][1] << "," << ops[i][2] << "]";
+      o << "]";
+      return o.str();
+    };
+    sjs << ",\"shuffle\":{\"ok\":" << (ok ? "true" : "false") << ",\"I\":" << vec_json(I)
+        << ",\"E\":" << vec_json(E) << ",\"F\":" << vec_json(F) << ",\"G\":" << vec_json(Gv)
+        << ",\"R\":" << vec_json(R) << ",\"rounds\":" << NWd << ",\"word_bits_ld\":" << vec_json(Aw)
+        << ",\"word_bits_st\":" << vec_json(Bw) << ",\"lanes_ld\":" << vec_json(Al5)
+        << ",\"lanes_st\":" << vec_json(Bl5);
+    if (ok) {
+      sjs << ",\"alpha\":" << vec_json(alpha) << ",\"eps\":" << vec_json(epsm)
+          << ",\"pre_ops\":" << ops_json(pre) << ",\"post_ops\":" << ops_json(post)
+          << ",\"beta_lane\":" << u32_json(sh.beta_lane, 5) << ",\"zeta_lane\":" << u32_json(sh.zeta_lane, 5)
+          << ",\"delta_lane\":" << u32_json(sh.delta_lane, 5) << ",\"gamma\":[";
+      for (int k = 0; k < NWd; ++k) sjs << (k ? "," : "") << (int)sh.gamma[k];
+      sjs << "]";
+    }
+    sjs << "}";
+  }
   // ---- description
   auto srcpos = [&](const std::vector<int>& v) {
     std::vector<int> o;
@@ -454,7 +639,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
      << ",\"smem_bytes\":{\"sw_thr\":" << u32_json(sp.sw_thr, 5 + g) << ",\"sr_thr\":"
      << u32_json(sp.sr_thr, 5 + g) << ",\"sw_gran\":" << u32_json(sp.sw_gran, ngran)
      << ",\"sr_gran\":" << u32_json(sp.sr_gran, ngran) << "}"
-     << ",\"tile_order_dst_bits\":" << ivec_json(torder);
+     << ",\"tile_order_dst_bits\":" << ivec_json(torder) << sjs.str();
   return true;
 }
 
@@ -477,16 +662,19 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
      << (ident ? "true" : "false");
   int path = path_req;
   if (path == LL_PATH_AUTO) path = ident ? LL_PATH_COPY : LL_PATH_SMEM;
-  if (path == LL_PATH_SHUFFLE) path = LL_PATH_SMEM;  // shuffle exchange: not yet built (falls back)
   if (path == LL_PATH_COPY && !ident)
     throw Error(LL_ERR_UNSUPPORTED, "copy path requested but the quotient is not the identity");
-  if (path == LL_PATH_SMEM || path == LL_PATH_SMEM_NOSWIZZLE) {
+  if (path == LL_PATH_SMEM || path == LL_PATH_SMEM_NOSWIZZLE || path == LL_PATH_SHUFFLE) {
     std::ostringstream js2;
-    if (plan_smem(*P, X, path == LL_PATH_SMEM, js2)) {
+    if (plan_smem(*P, X, path != LL_PATH_SMEM_NOSWIZZLE, js2, path == LL_PATH_SHUFFLE)) {
       js << js2.str();
+      if (path == LL_PATH_SHUFFLE && !P->shuffle_ok)
+        throw Error(LL_ERR_UNSUPPORTED,
+                    "shuffle path requested but the exchange is not warp-local with a word payload "
+                    "((B^-1 o A)_warp must be the identity on the planner's warp tile, P:624)");
     } else {
-      if (path_req == LL_PATH_SMEM || path_req == LL_PATH_SMEM_NOSWIZZLE)
-        throw Error(LL_ERR_UNSUPPORTED, "smem path requested but the quotient is not a tileable bit permutation");
+      if (path_req != LL_PATH_AUTO)
+        throw Error(LL_ERR_UNSUPPORTED, "smem/shuffle path requested but the quotient is not a tileable bit permutation");
       path = LL_PATH_GENERIC;
     }
   }

@@ -38,6 +38,10 @@ struct ConvertPlan {
   int nv = 0, g = 0;
   int tile_bits = 0, r = 0, gw = 0;
   int pred_wf_ld = 0, pred_wf_st = 0;   // wavefronts per STS / LDS instruction
+  // shuffle path (warp tiles only)
+  ShufflePlan shp{};
+  bool shuffle_ok = false;
+  int shuffle_rounds = 0;
   // generic path
   GenericPlan gp{};
   std::string json;

@@ -85,7 +85,7 @@ def main():
             nsets = 2 if n * w >= (64 << 20) else 4
             sets = [(values_torch(n, 7 + s, w, dev), values_torch(n, 0, w, dev)) for s in range(nsets)]
             for path in args.paths.split(","):
-                for ks in (knob_sets if path.startswith("smem") else [{}]):
+                for ks in (knob_sets if path.startswith("smem") or path == "shuffle" else [{}]):
                     for k, v in ks.items():
                         ll.tune(k, v)
                     try:

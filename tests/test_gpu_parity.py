@@ -71,10 +71,12 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "generic"])
+@pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "shuffle", "generic"])
 @pytest.mark.parametrize("name,mk", CASES)
 def test_convert_configs_small(name, mk, path):
     c = mk()
+    if path == "shuffle" and name.startswith("cfg3"):
+        pytest.skip("transpose exchange is not warp-local (P:624); covered by test_shuffle_rejects")
     src, dst = run_convert(c, path=path)
     exp = expect_convert(c, src)
     assert dst.tobytes() == exp.tobytes()
@@ -117,6 +119,30 @@ def test_convert_random_pairs(w):
         c = rand_pair(rng, d, w)
         src, dst = run_convert(c, seed=rng.randint(0, 1000))
         assert dst.tobytes() == expect_convert(c, src).tobytes()
+
+
+@pytest.mark.parametrize("w", [1, 2, 4])
+def test_convert_random_pairs_shuffle(w):
+    rng = random.Random(500 + w)
+    done = 0
+    while done < 10:
+        d = rng.randint(11, 15)
+        c = rand_pair(rng, d, w)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        try:
+            ll.plan_describe(A, B, 8 * w, "shuffle")
+        except ll.LLError:
+            continue
+        src, dst = run_convert(c, path="shuffle", seed=rng.randint(0, 1000))
+        assert dst.tobytes() == expect_convert(c, src).tobytes()
+        done += 1
+
+
+@pytest.mark.parametrize("batch", [3, 37])
+def test_convert_shuffle_ragged_batch(batch):
+    c = configs.cfg2(batch_bits=0)
+    src, dst = run_convert(c, path="shuffle", batch=batch, seed=13)
+    assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
 
 
 def test_convert_identity_is_copy():
