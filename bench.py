@@ -32,7 +32,7 @@ METRIC = "convert_layout effective GB/s vs 8 TB/s HBM peak; smem bank conflicts/
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5"])
     ap.add_argument("--path", default="auto")
@@ -78,7 +78,7 @@ def algorithmic_bytes(cfg, c):
 class ClockSampler:
     """NVML polling of SM clock and throttle reasons during the timed region."""
 
-    def __init__(self, index=0, period=0.005):
+    def __init__(self, index=0, period=0.001):
         self.period = period
         self.samples = []
         self.reasons = set()
