@@ -36,6 +36,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5"])
     ap.add_argument("--path", default="auto")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank converts the full workload; strong: rank r converts "
+                         "shard r of the top block bits (ll_convert_shard, cfg2/cfg5)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -297,15 +300,25 @@ def main():
         A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
         w = c["elem_bytes"]
         n = 1 << A.in_bits
-        nsets = max(2, -(-(2 * 128 << 20) // (2 * n * w)) + 1) if n * w < (128 << 20) else 2
+        if args.scaling == "strong" and world > 1:
+            # this rank holds and converts only its shard (contiguous slices)
+            s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, world, rank, args.path)
+            n_loc = (s1 - s0) // w
+            nbytes = (s1 - s0) + (d1 - d0)
+        else:
+            n_loc = n
+        nsets = max(2, -(-(2 * 128 << 20) // (2 * n_loc * w)) + 1) if n_loc * w < (128 << 20) else 2
         nsets = min(nsets, 64)
-        sets = [(values_torch(n, 7 + s + 10 * rank, w, dev),
-                 torch.empty(n, dtype=values_torch(1, 0, w, "cpu").dtype, device=dev))
+        sets = [(values_torch(n_loc, 7 + s + 10 * rank, w, dev),
+                 torch.empty(n_loc, dtype=values_torch(1, 0, w, "cpu").dtype, device=dev))
                 for s in range(nsets)]
 
         def step(i):
             s, d = sets[i % len(sets)]
-            ll.convert(s, A, d, B, 8 * w, path=args.path)
+            if args.scaling == "strong" and world > 1:
+                ll.convert_shard(s, A, d, B, 8 * w, world, rank, path=args.path)
+            else:
+                ll.convert(s, A, d, B, 8 * w, path=args.path)
         plan = ll.plan_describe(A, B, 8 * w, args.path)
 
     torch.cuda.synchronize()
@@ -348,13 +361,12 @@ def main():
     if graph is None:
         launches = ll.launch_count() - l0
     total_ms = e0.elapsed_time(e1)
+    from paper_2505_23819_b200 import multigpu
     if world > 1:
         dist.barrier()
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = multigpu.max_over_ranks(total_ms, device=dev)
     ms_per_step = total_ms / K
-    value = world * nbytes / (ms_per_step * 1e-3) / 1e9
+    value = multigpu.aggregate_gbps([nbytes] * world, [ms_per_step] * world, args.scaling)
     avg_launch_ms = total_ms / K
     achieved = nbytes / (avg_launch_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
@@ -410,7 +422,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp16" if cfg in ("1", "2") else
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "fp16" if cfg in ("1", "2") else
             {"3": "bf16", "4": "fp32", "5": "u8"}[cfg], "data": "synthetic",
             "config": {"workload": desc, "bytes_per_step_per_gpu": nbytes,
                        "l2": "%d rotating buffer sets, footprint %.0f MiB > 126 MB L2" % (

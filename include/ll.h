@@ -161,6 +161,24 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
 ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout layout, int axis,
                        int elem_bits, const ll_convert_options* opts, ll_stream stream);
 
+/* Multi-GPU shard: convert only shard `shard` of `n_shards`
+ * (a power of two).  The tensor is split along the top log2(n_shards) index
+ * bits, which must be block bits shared by both layouts (X maps them
+ * identically), so shard s is the contiguous byte range
+ *   src: [s * S_A, (s+1) * S_A),  dst: [s * S_B, (s+1) * S_B),
+ *   S_A = (elem_bytes << in_bits(A)) / n_shards, S_B likewise,
+ * and src_slice / dst_slice point at those ranges in the caller's (e.g. this
+ * rank's) memory.  No collective: ranks run independently.
+ * Errors: LL_ERR_UNSUPPORTED if the layouts cannot be sharded that way,
+ * LL_ERR_ARG for a bad shard index; otherwise as ll_convert_ex. */
+ll_status ll_convert_shard(const void* src_slice, ll_layout src_layout, void* dst_slice,
+                           ll_layout dst_layout, int elem_bits, int n_shards, int shard,
+                           const ll_convert_options* opts, ll_stream stream);
+
+/* Byte ranges of shard `shard`: out4 = {src_begin, src_end, dst_begin, dst_end}. */
+ll_status ll_shard_describe(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
+                            int n_shards, int shard, int64_t* out4);
+
 /* End-to-end conversion of HOST buffers: src_host/dst_host are host pointers
  * (pinned for full speed); the library pipelines host->device copies, the
  * conversion and device->host copies in chunks of whole tiles over two

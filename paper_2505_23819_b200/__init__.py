@@ -10,9 +10,10 @@ PyTorch fallback: if the shared library is missing the import fails loudly.
     ll.convert(src, A, dst, B, elem_bits=16)      # device tensors (torch)
 """
 
-from ._lib import (LLError, Layout, compose, convert, convert_host, gather, gather_describe,
+from ._lib import (LLError, Layout, compose, convert, convert_host, convert_shard, shard_describe, gather, gather_describe,
                    invert, launch_count, lib_path, plan_describe, product, tune, version, PATHS)
 
-__all__ = ["LLError", "Layout", "compose", "convert", "convert_host", "gather", "gather_describe",
+__all__ = ["LLError", "Layout", "compose", "convert", "convert_host", "convert_shard",
+           "shard_describe", "gather", "gather_describe",
            "invert", "launch_count", "lib_path", "plan_describe", "product", "tune", "version",
            "PATHS"]

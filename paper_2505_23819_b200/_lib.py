@@ -58,7 +58,12 @@ _lib.ll_gather_describe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_char_p, ctypes.c_size_t,
                                     ctypes.POINTER(ctypes.c_size_t)]
 _lib.ll_tune.argtypes = [ctypes.c_char_p, ctypes.c_int]
-for _f in ("ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
+_lib.ll_convert_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_void_p, ctypes.c_void_p]
+_lib.ll_shard_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+for _f in ("ll_convert_shard", "ll_shard_describe", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
            "ll_gather_describe"):
@@ -230,6 +235,24 @@ def convert(src, A, dst, B, elem_bits, path="auto", batch=1, max_ctas=0, stream=
     o = _opts(path, batch, max_ctas)
     _check(_lib.ll_convert_ex(_ptr(src), A.handle, _ptr(dst), B.handle, int(elem_bits),
                               ctypes.byref(o), _stream_handle(stream)))
+
+
+def convert_shard(src_slice, A, dst_slice, B, elem_bits, n_shards, shard, path="auto",
+                  max_ctas=0, stream=None):
+    """ll_convert_shard: convert this rank's slice."""
+    o = _opts(path, 1, max_ctas)
+    _check(_lib.ll_convert_shard(_ptr(src_slice), A.handle, _ptr(dst_slice), B.handle,
+                                 int(elem_bits), int(n_shards), int(shard), ctypes.byref(o),
+                                 _stream_handle(stream)))
+
+
+def shard_describe(A, B, elem_bits, n_shards, shard, path="auto"):
+    """Byte ranges (src_begin, src_end, dst_begin, dst_end) of one shard."""
+    out = (ctypes.c_int64 * 4)()
+    _check(_lib.ll_shard_describe(A.handle, B.handle, int(elem_bits),
+                                  PATHS[path] if isinstance(path, str) else int(path),
+                                  int(n_shards), int(shard), out))
+    return tuple(out)
 
 
 def gather(src, idx, out, L, axis, elem_bits, path="auto", batch=1, max_ctas=0, stream=None):

@@ -259,40 +259,86 @@ ll_status ll_gather_describe(ll_layout layout, int axis, int elem_bits, int path
   });
 }
 
+namespace {
+ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
+                      int elem_bits, const ll_convert_options* opts, ll_stream stream,
+                      int n_shards, int shard) {
+  check_layout(src_layout, "ll_convert");
+  check_layout(dst_layout, "ll_convert");
+  const int w = elem_bytes(elem_bits);
+  const int path_req = opts ? opts->path : LL_PATH_AUTO;
+  const int64_t batch = opts && opts->batch > 0 ? opts->batch : 1;
+  const int max_ctas = opts ? opts->max_ctas : 0;
+  if (!src || !dst) return fail(LL_ERR_ARG, "ll_convert: NULL buffer");
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(LL_ERR_ARG, "ll_convert: buffers must be 16-byte aligned");
+  auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, path_req, batch);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ll::TileRange rg{0, 0, 0, 0};
+  if (n_shards > 1) {
+    rg = ll::shard_range(*P, n_shards, shard);
+  } else if (P->path == LL_PATH_SMEM || P->path == LL_PATH_SMEM_NOSWIZZLE) {
+    rg.t1 = P->sp.tile.n_tiles;
+  } else if (P->path == LL_PATH_SHUFFLE) {
+    rg.t1 = P->shp.tile.n_tiles;
+  }
+  const size_t dst_bytes = (size_t)w << P->nB;
+  switch (P->path) {
+    case LL_PATH_COPY: {
+      ++g_launches;
+      const size_t bytes = n_shards > 1 ? dst_bytes / n_shards : dst_bytes * batch;
+      return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st),
+                         "ll_convert (copy)");
+    }
+    case LL_PATH_SHUFFLE:
+      ++g_launches;
+      return cuda_status(ll::launch_convert_shuffle(P->shp, w, P->nv, src, dst, max_ctas, st, rg),
+                         "ll_convert (shuffle kernel)");
+    case LL_PATH_SMEM:
+    case LL_PATH_SMEM_NOSWIZZLE:
+      ++g_launches;
+      return cuda_status(ll::launch_convert_smem(P->sp, w, P->nv, P->g, src, dst, max_ctas, st, rg),
+                         "ll_convert (smem kernel)");
+    default:
+      if (n_shards > 1) return fail(LL_ERR_UNSUPPORTED, "ll_convert_shard: generic plans are not shardable");
+      ++g_launches;
+      return cuda_status(ll::launch_convert_generic(P->gp, w, src, dst, max_ctas, st),
+                         "ll_convert (generic kernel)");
+  }
+}
+}  // namespace
+
 ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
                         int elem_bits, const ll_convert_options* opts, ll_stream stream) {
   return guarded([&]() -> ll_status {
-    check_layout(src_layout, "ll_convert");
-    check_layout(dst_layout, "ll_convert");
+    return run_convert(src, src_layout, dst, dst_layout, elem_bits, opts, stream, 1, 0);
+  });
+}
+
+ll_status ll_convert_shard(const void* src_slice, ll_layout src_layout, void* dst_slice,
+                           ll_layout dst_layout, int elem_bits, int n_shards, int shard,
+                           const ll_convert_options* opts, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    return run_convert(src_slice, src_layout, dst_slice, dst_layout, elem_bits, opts, stream,
+                       n_shards, shard);
+  });
+}
+
+ll_status ll_shard_describe(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
+                            int n_shards, int shard, int64_t* out4) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_shard_describe");
+    check_layout(dst_layout, "ll_shard_describe");
+    if (!out4) return fail(LL_ERR_ARG, "ll_shard_describe: out is NULL");
     const int w = elem_bytes(elem_bits);
-    const int path_req = opts ? opts->path : LL_PATH_AUTO;
-    const int64_t batch = opts && opts->batch > 0 ? opts->batch : 1;
-    const int max_ctas = opts ? opts->max_ctas : 0;
-    if (!src || !dst) return fail(LL_ERR_ARG, "ll_convert: NULL buffer");
-    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
-      return fail(LL_ERR_ARG, "ll_convert: buffers must be 16-byte aligned");
-    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, path_req, batch);
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const size_t dst_bytes = (size_t)w << P->nB;
-    switch (P->path) {
-      case LL_PATH_COPY:
-        ++g_launches;
-        return cuda_status(cudaMemcpyAsync(dst, src, dst_bytes * batch, cudaMemcpyDeviceToDevice, st),
-                           "ll_convert (copy)");
-      case LL_PATH_SHUFFLE:
-        ++g_launches;
-        return cuda_status(ll::launch_convert_shuffle(P->shp, w, P->nv, src, dst, max_ctas, st),
-                           "ll_convert (shuffle kernel)");
-      case LL_PATH_SMEM:
-      case LL_PATH_SMEM_NOSWIZZLE:
-        ++g_launches;
-        return cuda_status(ll::launch_convert_smem(P->sp, w, P->nv, P->g, src, dst, max_ctas, st),
-                           "ll_convert (smem kernel)");
-      default:
-        ++g_launches;
-        return cuda_status(ll::launch_convert_generic(P->gp, w, src, dst, max_ctas, st),
-                           "ll_convert (generic kernel)");
-    }
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, path, 1);
+    auto rg = ll::shard_range(*P, n_shards, shard);
+    const int64_t sbytes = ((int64_t)w << P->nA) / n_shards, dbytes = ((int64_t)w << P->nB) / n_shards;
+    out4[0] = rg.src_shift;
+    out4[1] = rg.src_shift + sbytes;
+    out4[2] = rg.dst_shift;
+    out4[3] = rg.dst_shift + dbytes;
+    return LL_OK;
   });
 }
 

@@ -264,7 +264,7 @@ template <int W, int NV, int G, bool PIPE>
 __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
-                                                           int64_t n_groups) {
+                                                           int64_t n_groups, TileRange rg) {
   constexpr int NW = NV * 4;          // 32-bit words per thread
   constexpr int NG = NV * 16 / G;     // granules per thread
   constexpr int GW = G / 4;           // words per granule
@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       srx ^= p.sr_thr[b];
     }
   }
-  const uint8_t* sthr = src + ld_off;
-  uint8_t* dthr = dst + st_off;
+  const uint8_t* sthr = src + ld_off - rg.src_shift;
+  uint8_t* dthr = dst + st_off - rg.dst_shift;
   const int n_bits = p.tile.n_bits;
   const int n_tab = p.tile.n_tab;
   const int64_t rmask = (int64_t(1) << n_bits) - 1;
@@ -414,7 +414,7 @@ template <int W, int NV, bool PIPE>
 __global__ void __launch_bounds__(256) convert_shuffle_kernel(const __grid_constant__ ShufflePlan p,
                                                               const uint8_t* __restrict__ src,
                                                               uint8_t* __restrict__ dst,
-                                                              int64_t n_groups) {
+                                                              int64_t n_groups, TileRange rg) {
   constexpr int NW = NV * 4;
   const int lane = threadIdx.x & 31;
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -430,8 +430,8 @@ __global__ void __launch_bounds__(256) convert_shuffle_kernel(const __grid_const
       delta ^= p.delta_lane[b];
     }
   }
-  const uint8_t* sthr = src + ld_off;
-  uint8_t* dthr = dst + st_off;
+  const uint8_t* sthr = src + ld_off - rg.src_shift;
+  uint8_t* dthr = dst + st_off - rg.dst_shift;
   const int n_bits = p.tile.n_bits;
   const int n_tab = p.tile.n_tab;
   const int64_t rmask = (int64_t(1) << n_bits) - 1;
@@ -449,10 +449,10 @@ __global__ void __launch_bounds__(256) convert_shuffle_kernel(const __grid_const
       }
     }
   };
-  const int64_t n_tiles = p.tile.n_tiles;
+  const int64_t n_tiles = rg.t1;
   uint32_t R[NW];
   int64_t so, dof;
-  int64_t t = gid;
+  int64_t t = rg.t0 + gid;
   if (PIPE && t < n_tiles) {
     tile_off(t, so, dof);
     load_tile<NV>(R, sthr + so, p.ld_vec);
@@ -734,7 +734,7 @@ int set_knob(const char* name, int value) {
 
 template <int W, int NV, int G, bool PIPE>
 static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, int max_ctas,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const TileRange& rg) {
   auto k = convert_smem_kernel<W, NV, G, PIPE>;
   const int threads = 256;
   const int gpc = (threads / 32) >> p.gw;
@@ -750,7 +750,7 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
     occ_carve = knobs().carveout;
   }
   if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
-  const int64_t n_tiles = p.tile.n_tiles;
+  const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;
   // tile groups: n_tiles / tpg (the hardware block scheduler balances the
   // tail), or the resident capacity when tpg = 0 (persistent)
@@ -760,22 +760,22 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
   const int64_t grid = (groups + gpc - 1) / gpc;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups);
+  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups, rg);
   return cudaGetLastError();
 }
 
 template <int W, int NV, int G>
 static cudaError_t launch_smem_t(const SmemPlan& p, const void* src, void* dst, int max_ctas,
-                                 cudaStream_t st) {
-  if (knobs().pipe) return launch_smem_p<W, NV, G, true>(p, src, dst, max_ctas, st);
-  return launch_smem_p<W, NV, G, false>(p, src, dst, max_ctas, st);
+                                 cudaStream_t st, const TileRange& rg) {
+  if (knobs().pipe) return launch_smem_p<W, NV, G, true>(p, src, dst, max_ctas, st, rg);
+  return launch_smem_p<W, NV, G, false>(p, src, dst, max_ctas, st, rg);
 }
 
 template <int W>
 static cudaError_t launch_smem_w(const SmemPlan& p, int nv, int g, const void* src, void* dst,
-                                 int max_ctas, cudaStream_t st) {
+                                 int max_ctas, cudaStream_t st, const TileRange& rg) {
 #define LL_CASE(NV_, G_) \
-  if (nv == NV_ && g == G_) return launch_smem_t<W, NV_, G_>(p, src, dst, max_ctas, st);
+  if (nv == NV_ && g == G_) return launch_smem_t<W, NV_, G_>(p, src, dst, max_ctas, st, rg);
   LL_CASE(1, 4) LL_CASE(1, 8) LL_CASE(1, 16)
   LL_CASE(2, 4) LL_CASE(2, 8) LL_CASE(2, 16)
   LL_CASE(4, 4) LL_CASE(4, 8) LL_CASE(4, 16)
@@ -785,23 +785,23 @@ static cudaError_t launch_smem_w(const SmemPlan& p, int nv, int g, const void* s
 }
 
 cudaError_t launch_convert_smem(const SmemPlan& p, int w, int nv, int g, const void* src, void* dst,
-                                int max_ctas, cudaStream_t st) {
+                                int max_ctas, cudaStream_t st, const TileRange& rg) {
   switch (w) {
-    case 1: return launch_smem_w<1>(p, nv, g, src, dst, max_ctas, st);
-    case 2: return launch_smem_w<2>(p, nv, g, src, dst, max_ctas, st);
-    case 4: return launch_smem_w<4>(p, nv, g, src, dst, max_ctas, st);
-    case 8: return launch_smem_w<8>(p, nv, g, src, dst, max_ctas, st);
+    case 1: return launch_smem_w<1>(p, nv, g, src, dst, max_ctas, st, rg);
+    case 2: return launch_smem_w<2>(p, nv, g, src, dst, max_ctas, st, rg);
+    case 4: return launch_smem_w<4>(p, nv, g, src, dst, max_ctas, st, rg);
+    case 8: return launch_smem_w<8>(p, nv, g, src, dst, max_ctas, st, rg);
   }
   return cudaErrorNotSupported;
 }
 
 template <int W, int NV, bool PIPE>
 static cudaError_t launch_shuffle_p(const ShufflePlan& p, const void* src, void* dst, int max_ctas,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, const TileRange& rg) {
   auto k = convert_shuffle_kernel<W, NV, PIPE>;
   const int threads = 256;
   const int gpc = threads / 32;
-  const int64_t n_tiles = p.tile.n_tiles;
+  const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;
   static int occ_cache = -1;
   if (occ_cache < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, 0);
@@ -811,28 +811,28 @@ static cudaError_t launch_shuffle_p(const ShufflePlan& p, const void* src, void*
   groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
   const int64_t grid = (groups + gpc - 1) / gpc;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  k<<<(unsigned)grid, threads, 0, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups);
+  k<<<(unsigned)grid, threads, 0, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups, rg);
   return cudaGetLastError();
 }
 
 template <int W>
 static cudaError_t launch_shuffle_w(const ShufflePlan& p, int nv, const void* src, void* dst,
-                                    int max_ctas, cudaStream_t st) {
+                                    int max_ctas, cudaStream_t st, const TileRange& rg) {
   const bool pipe = knobs().pipe != 0;
 #define LL_SCASE(NV_) \
-  if (nv == NV_) return pipe ? launch_shuffle_p<W, NV_, true>(p, src, dst, max_ctas, st) \
-                             : launch_shuffle_p<W, NV_, false>(p, src, dst, max_ctas, st);
+  if (nv == NV_) return pipe ? launch_shuffle_p<W, NV_, true>(p, src, dst, max_ctas, st, rg) \
+                             : launch_shuffle_p<W, NV_, false>(p, src, dst, max_ctas, st, rg);
   LL_SCASE(1) LL_SCASE(2) LL_SCASE(4) LL_SCASE(8)
 #undef LL_SCASE
   return cudaErrorNotSupported;
 }
 
 cudaError_t launch_convert_shuffle(const ShufflePlan& p, int w, int nv, const void* src, void* dst,
-                                   int max_ctas, cudaStream_t st) {
+                                   int max_ctas, cudaStream_t st, const TileRange& rg) {
   switch (w) {
-    case 1: return launch_shuffle_w<1>(p, nv, src, dst, max_ctas, st);
-    case 2: return launch_shuffle_w<2>(p, nv, src, dst, max_ctas, st);
-    case 4: return launch_shuffle_w<4>(p, nv, src, dst, max_ctas, st);
+    case 1: return launch_shuffle_w<1>(p, nv, src, dst, max_ctas, st, rg);
+    case 2: return launch_shuffle_w<2>(p, nv, src, dst, max_ctas, st, rg);
+    case 4: return launch_shuffle_w<4>(p, nv, src, dst, max_ctas, st, rg);
   }
   return cudaErrorNotSupported;
 }

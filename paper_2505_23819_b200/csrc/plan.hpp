@@ -89,6 +89,14 @@ struct ShufflePlan {
   uint8_t gamma[LL_MAX_GRAN];                          // per round: xor into the source lane
 };
 
+// A contiguous range of tile indices [t0, t1) of a smem / shuffle plan, with
+// the byte offsets of the caller's slices (multi-GPU shards: each rank holds
+// only its slice of src and dst).
+struct TileRange {
+  int64_t t0, t1;
+  int64_t src_shift, dst_shift;
+};
+
 // Generic pull kernel (LL_PATH_GENERIC): dst[h] = src[X h] for every h.
 struct GenericPlan {
   int64_t n_vec;           // number of destination 16-byte vectors (incl. batch)

@@ -452,6 +452,12 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   tm.batch_stride_src = int64_t(w) << P.nA;
   tm.batch_stride_dst = int64_t(w) << P.nB;
   tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
+  P.tile_bit_src.clear();
+  P.tile_bit_dst.clear();
+  for (int q = 0; q < tm.n_bits; ++q) {
+    P.tile_bit_src.push_back(sigma[torder[q]]);
+    P.tile_bit_dst.push_back(torder[q]);
+  }
   P.nv = nvec;
   P.g = G;
   P.tile_bits = d;
@@ -714,6 +720,40 @@ std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layou
   std::lock_guard<std::mutex> lk(g_mu);
   g_cache[k] = P;
   return P;
+}
+
+TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
+  if (n_shards < 1 || (n_shards & (n_shards - 1)) || shard < 0 || shard >= n_shards)
+    throw Error(LL_ERR_ARG, "shard: n_shards must be a power of two and 0 <= shard < n_shards");
+  int sb = 0;
+  while ((1 << sb) < n_shards) ++sb;
+  const int64_t w = P.w;
+  TileRange rg{};
+  if (P.batch != 1) throw Error(LL_ERR_UNSUPPORTED, "shard: batch must be 1 (shard the layout's own block bits)");
+  if (P.path == LL_PATH_COPY) {
+    rg.t0 = (int64_t)shard;
+    rg.t1 = (int64_t)shard + 1;
+    rg.src_shift = (int64_t)shard * ((w << P.nA) >> sb);
+    rg.dst_shift = (int64_t)shard * ((w << P.nB) >> sb);
+    return rg;
+  }
+  if (P.path != LL_PATH_SMEM && P.path != LL_PATH_SHUFFLE && P.path != LL_PATH_SMEM_NOSWIZZLE)
+    throw Error(LL_ERR_UNSUPPORTED, "shard: only tiled (smem / shuffle) plans are shardable");
+  const int nb = (int)P.tile_bit_src.size();
+  if (sb > nb) throw Error(LL_ERR_UNSUPPORTED, "shard: more shards than tiles");
+  for (int j = 0; j < sb; ++j) {
+    const int q = nb - sb + j;
+    if (P.tile_bit_src[q] != P.nA - sb + j || P.tile_bit_dst[q] != P.nB - sb + j)
+      throw Error(LL_ERR_UNSUPPORTED,
+                  "shard: the top index bits are not block bits shared by both layouts "
+                  "(a rank's shard would not be a contiguous slice of both buffers)");
+  }
+  const int64_t per = (int64_t(1) << nb) >> sb;
+  rg.t0 = per * shard;
+  rg.t1 = per * (shard + 1);
+  rg.src_shift = (int64_t)shard * ((w << P.nA) >> sb);
+  rg.dst_shift = (int64_t)shard * ((w << P.nB) >> sb);
+  return rg;
 }
 
 // ------------------------------------------------------------------ gather

@@ -38,6 +38,8 @@ struct ConvertPlan {
   int nv = 0, g = 0;
   int tile_bits = 0, r = 0, gw = 0;
   int pred_wf_ld = 0, pred_wf_st = 0;   // wavefronts per STS / LDS instruction
+  // tile order: element positions of each outer (tile-index) bit in src / dst
+  std::vector<int> tile_bit_src, tile_bit_dst;
   // shuffle path (warp tiles only)
   ShufflePlan shp{};
   bool shuffle_ok = false;
@@ -53,6 +55,12 @@ struct GatherPlanHost {
   GatherPlan gp{};
   std::string json;
 };
+
+// Shard `shard` of `n_shards` (a power of two) of a smem / shuffle / copy
+// plan: the top log2(n_shards) bits of the src and dst indices must be the
+// last tile-index bits and mapped identically (so every shard is one
+// contiguous slice of each buffer).  Throws LL_ERR_UNSUPPORTED otherwise.
+TileRange shard_range(const ConvertPlan& P, int n_shards, int shard);
 
 int planner_knob(const char* name, int dflt);
 int planner_knob_version();

@@ -145,6 +145,29 @@ def test_convert_shuffle_ragged_batch(batch):
     assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
 
 
+@pytest.mark.parametrize("name,mk,shards", [("cfg5", lambda: configs.cfg5(m_bits=10, kb_bits=8), 8),
+                                            ("cfg2", lambda: configs.cfg2(batch_bits=3), 4),
+                                            ("cfg2s", lambda: configs.cfg2(batch_bits=3), 2)])
+def test_convert_shards_equal_full(name, mk, shards):
+    """Each rank's shard converted from its own slices (separate allocations,
+    SURVEY 8(e)) reassembles the oracle's full conversion."""
+    c = mk()
+    w = c["elem_bytes"]
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src = values_torch(n, 29, w, "cuda")
+    parts = []
+    for r in range(shards):
+        s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, shards, r)
+        sl = src.view(torch.uint8)[s0:s1].clone()          # this rank's memory only
+        dl = torch.empty(d1 - d0, dtype=torch.uint8, device="cuda")
+        ll.convert_shard(sl, A, dl, B, 8 * w, shards, r)
+        parts.append(dl)
+    torch.cuda.synchronize()
+    got = torch.cat(parts).cpu().numpy().view(_NP[w])
+    assert got.tobytes() == expect_convert(c, _np(src, w)).tobytes()
+
+
 def test_convert_identity_is_copy():
     c = configs.cfg2(batch_bits=1)
     c = {"A": c["A"], "B": c["A"], "elem_bytes": 2}
