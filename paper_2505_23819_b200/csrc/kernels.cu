@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
   const uint32_t amask = (1u << p.ax_bits) - 1;
   const int64_t nwarps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_wvec = p.n_vec >> 5;  // warps' worth of vectors
-  const uint64_t clear = ~(uint64_t)p.axis_mask_buf;
+  const uint32_t clear32 = ~(uint32_t)p.axis_mask_buf;
   const int ybase = p.y_base;
   for (int64_t wv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wv < n_wvec;
        wv += nwarps_total) {
@@ -644,11 +644,12 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
     }
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      const uint64_t h = h0 | (uint64_t)e;
+      // only the warp-local bits (VB + 5) of h* matter here: 32-bit arithmetic
       uint32_t i = (uint32_t)iv[e];
       if (p.check && i > amask) atomicExch(err, 1);
       i &= amask;
-      const uint64_t hs = (h & clear) | ((uint64_t)i << ybase);
+      const uint32_t hl = (((uint32_t)lane << VB) | (uint32_t)e) & clear32;
+      const uint32_t hs = hl | (i << ybase);
       const int src_lane = (int)((hs >> VB) & 31);
       const int src_reg = (int)(hs & (NE - 1));
       if constexpr (ALLC && W == 4) {

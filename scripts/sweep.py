@@ -24,13 +24,23 @@ DEFAULTS = {"tpg": 2, "pipe": 1, "carveout": -1, "pow2": 0, "thread_bytes": 64,
 
 
 def timeit(step, steps, warm=5):
+    """Average ms per step: `steps` steps captured in a CUDA graph, replayed."""
     for i in range(warm):
         step(i)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(g, stream=cap):
+            for i in range(steps):
+                step(i)
+    torch.cuda.current_stream().wait_stream(cap)
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(steps):
-        step(i)
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / steps
