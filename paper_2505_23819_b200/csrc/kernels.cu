@@ -314,11 +314,11 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * p.tile_bytes;
   uint32_t buf = 0;
   const int ga = p.gsel_a, gb = p.gsel_b;
-  const int64_t n_tiles = p.tile.n_tiles;
+  const int64_t n_tiles = rg.t1;
 
   uint32_t R[NW];
   int64_t so, dof;
-  int64_t t = gid;
+  int64_t t = rg.t0 + gid;
   if (PIPE && t < n_tiles) {
     tile_off(t, so, dof);
     load_tile<NV>(R, sthr + so, p.ld_vec);
