@@ -261,7 +261,7 @@ __device__ __forceinline__ void load_tile(uint32_t (&R)[NV * 4], const uint8_t* 
 }
 
 template <int W, int NV, int G, bool PIPE>
-__global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
+__global__ void __launch_bounds__(256, (NV >= 8 ? 4 : 1)) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
                                                            int64_t n_groups, TileRange rg) {
