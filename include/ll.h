@@ -143,7 +143,8 @@ typedef enum {
   LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle    */
   LL_PATH_SHUFFLE = 3,   /* warp-local exchange with warp shuffles                 */
   LL_PATH_GENERIC = 4,   /* element-wise pull (any layouts; the slow baseline)     */
-  LL_PATH_SMEM_NOSWIZZLE = 5 /* smem path with an unswizzled staging buffer (ablation) */
+  LL_PATH_SMEM_NOSWIZZLE = 5, /* smem path with an unswizzled staging buffer (ablation) */
+  LL_PATH_SMEM_ASYNC = 6 /* smem path fed by cp.async (source granules, multi-stage) */
 } ll_path;
 
 typedef struct {

@@ -261,7 +261,7 @@ __device__ __forceinline__ void load_tile(uint32_t (&R)[NV * 4], const uint8_t* 
 }
 
 template <int W, int NV, int G, bool PIPE>
-__global__ void __launch_bounds__(256, (NV >= 8 ? 4 : 1)) convert_smem_kernel(const __grid_constant__ SmemPlan p,
+__global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
                                                            int64_t n_groups, TileRange rg) {
@@ -346,6 +346,143 @@ __global__ void __launch_bounds__(256, (NV >= 8 ? 4 : 1)) convert_smem_kernel(co
       stg_stream(dp + p.st_vec[u], make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
     buf ^= p.tile_bytes;
   }
+}
+
+// ------------------------------------------------------ cp.async smem kernel
+//
+// LL_PATH_SMEM_ASYNC: HBM -> shared memory by cp.async (16-byte source
+// vectors written straight to their swizzled granule, no registers), NS
+// tiles in flight per group; readers load 16-byte granules, fix the sub-word
+// order with prmt and pick destination vectors at compile time.
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NW, int A, int B>
+__device__ __forceinline__ void stg_vectors(const uint32_t (&Q)[NW], uint8_t* dp,
+                                            const uint32_t* st_vec) {
+  constexpr int LB = ilog2(NW);
+#pragma unroll
+  for (int u = 0; u < NW / 4; ++u)
+    stg_stream(dp + st_vec[u], make_uint4(Q[deposit_word(u, 0, LB, A, B)], Q[deposit_word(u, 1, LB, A, B)],
+                                          Q[deposit_word(u, 2, LB, A, B)], Q[deposit_word(u, 3, LB, A, B)]));
+}
+
+template <int NW, int A, int B>
+__device__ __forceinline__ bool stg_try_b(int a, int b, const uint32_t (&Q)[NW], uint8_t* dp,
+                                          const uint32_t* st_vec) {
+  constexpr int LB = ilog2(NW);
+  if constexpr (B >= LB) {
+    return false;
+  } else {
+    if constexpr (A != B) {
+      if (a == A && b == B) {
+        stg_vectors<NW, A, B>(Q, dp, st_vec);
+        return true;
+      }
+    }
+    return stg_try_b<NW, A, B + 1>(a, b, Q, dp, st_vec);
+  }
+}
+
+template <int NW, int A>
+__device__ __forceinline__ bool stg_try_a(int a, int b, const uint32_t (&Q)[NW], uint8_t* dp,
+                                          const uint32_t* st_vec) {
+  constexpr int LB = ilog2(NW);
+  if constexpr (A >= LB) {
+    return false;
+  } else {
+    if (stg_try_b<NW, A, 0>(a, b, Q, dp, st_vec)) return true;
+    return stg_try_a<NW, A + 1>(a, b, Q, dp, st_vec);
+  }
+}
+
+template <int W, int NV, int NS>
+__global__ void __launch_bounds__(256) convert_async_kernel(const __grid_constant__ SmemPlan p,
+                                                            const uint8_t* __restrict__ src,
+                                                            uint8_t* __restrict__ dst,
+                                                            int64_t n_groups, TileRange rg) {
+  constexpr int NW = NV * 4;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gw = p.gw;
+  const int group = warp >> gw;
+  const int tb = lane | ((warp & ((1 << gw) - 1)) << 5);
+  const int gpc = (blockDim.x >> 5) >> gw;
+  const int tbits = 5 + gw;
+  const int64_t gid = (int64_t)blockIdx.x * gpc + group;
+  if (gid >= n_groups) return;
+  uint32_t ld_off = 0, st_off = 0, swx = 0, srx = 0;
+#pragma unroll
+  for (int b = 0; b < LL_MAX_TBITS; ++b) {
+    if (b < tbits && ((tb >> b) & 1)) {
+      ld_off += p.ld_thr[b];
+      st_off += p.st_thr[b];
+      swx ^= p.sw_thr[b];
+      srx ^= p.sr_thr[b];
+    }
+  }
+  const uint8_t* sthr = src + ld_off - rg.src_shift;
+  uint8_t* dthr = dst + st_off - rg.dst_shift;
+  const int n_bits = p.tile.n_bits;
+  const int n_tab = p.tile.n_tab;
+  const int64_t rmask = (int64_t(1) << n_bits) - 1;
+  auto tile_off = [&](int64_t t, int64_t& so, int64_t& dof) {
+    const int64_t inst = t >> n_bits;
+    const int64_t r = t & rmask;
+    so = inst * p.tile.batch_stride_src;
+    dof = inst * p.tile.batch_stride_dst;
+#pragma unroll
+    for (int k = 0; k < LL_MAX_TAB; ++k) {
+      if (k < n_tab) {
+        const TileTab& e = p.tile.tab[k][(int)((r >> (k * LL_TAB_BITS)) & ((1 << LL_TAB_BITS) - 1))];
+        so += e.src;
+        dof += e.dst;
+      }
+    }
+  };
+  const uint32_t tb_bytes = (uint32_t)p.tile_bytes;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * NS * tb_bytes;
+  auto issue = [&](int64_t t, int stg) {
+    if (t < rg.t1) {
+      int64_t so, dof;
+      tile_off(t, so, dof);
+      const uint8_t* sp = sthr + so;
+      const uint32_t st_base = sbase + stg * tb_bytes;
+#pragma unroll
+      for (int u = 0; u < NV; ++u) cp_async16(st_base + (swx ^ p.sw_gran[u]), sp + p.ld_vec[u]);
+    }
+    cp_async_commit();
+  };
+  const int64_t t_first = rg.t0 + gid;
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) issue(t_first + s * n_groups, s);
+  int stage = 0;
+  const int ga = p.gsel_a, gb = p.gsel_b;
+  for (int64_t t = t_first; t < rg.t1; t += n_groups) {
+    cp_async_wait<NS - 2>();
+    group_sync(gw, group);
+    issue(t + (NS - 1) * n_groups, stage == 0 ? NS - 1 : stage - 1);
+    uint32_t Q[NW];
+    const uint32_t rb = sbase + stage * tb_bytes;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) lds<16>(rb + (srx ^ p.sr_gran[j]), &Q[4 * j]);
+    for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(Q, p.swap_a[s], p.swap_b[s]);
+    int64_t so, dof;
+    tile_off(t, so, dof);
+    stg_try_a<NW, 0>(ga, gb, Q, dthr + dof, p.st_vec);
+    stage = stage == NS - 1 ? 0 : stage + 1;
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------- shuffle kernel
@@ -712,11 +849,12 @@ static int env_int(const char* name, int dflt) {
 // group (0 = persistent grid at full occupancy), LL_PIPE = 1 for the
 // software-pipelined kernel.
 struct LaunchKnobs {
-  int tpg, pipe, gather_tpt, carveout, pow2;
+  int tpg, pipe, gather_tpt, carveout, pow2, stages, async_tpg;
   LaunchKnobs()
       : tpg(env_int("LL_TPG", 2)), pipe(env_int("LL_PIPE", 1)),
         gather_tpt(env_int("LL_GATHER_VPT", 2)), carveout(env_int("LL_CARVEOUT", -1)),
-        pow2(env_int("LL_POW2", 0)) {}
+        pow2(env_int("LL_POW2", 0)), stages(env_int("LL_STAGES", 3)),
+        async_tpg(env_int("LL_ASYNC_TPG", 8)) {}
 };
 static LaunchKnobs& knobs() {
   static LaunchKnobs k;
@@ -730,6 +868,8 @@ int set_knob(const char* name, int value) {
   if (n == "gather_vpt") { knobs().gather_tpt = value; return 0; }
   if (n == "carveout") { knobs().carveout = value; return 0; }
   if (n == "pow2") { knobs().pow2 = value; return 0; }
+  if (n == "stages") { knobs().stages = value; return 0; }
+  if (n == "async_tpg") { knobs().async_tpg = value; return 0; }
   return -1;
 }
 
@@ -792,6 +932,60 @@ cudaError_t launch_convert_smem(const SmemPlan& p, int w, int nv, int g, const v
     case 2: return launch_smem_w<2>(p, nv, g, src, dst, max_ctas, st, rg);
     case 4: return launch_smem_w<4>(p, nv, g, src, dst, max_ctas, st, rg);
     case 8: return launch_smem_w<8>(p, nv, g, src, dst, max_ctas, st, rg);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int W, int NV, int NS>
+static cudaError_t launch_async_p(const SmemPlan& p, const void* src, void* dst, int max_ctas,
+                                  cudaStream_t st, const TileRange& rg) {
+  auto k = convert_async_kernel<W, NV, NS>;
+  const int threads = 256;
+  const int gpc = (threads / 32) >> p.gw;
+  const size_t smem = (size_t)gpc * NS * p.tile_bytes;
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  static int occ_cache = -1;
+  static size_t occ_smem = 0;
+  if (occ_cache < 0 || occ_smem != smem) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
+    occ_smem = smem;
+  }
+  if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
+  const int64_t n_tiles = rg.t1 - rg.t0;
+  if (n_tiles <= 0) return cudaSuccess;
+  const int tpg = knobs().async_tpg;
+  int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)occ_cache * num_sms() * gpc;
+  if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
+  groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
+  const int64_t grid = (groups + gpc - 1) / gpc;
+  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups, rg);
+  return cudaGetLastError();
+}
+
+template <int W>
+static cudaError_t launch_async_w(const SmemPlan& p, int nv, const void* src, void* dst,
+                                  int max_ctas, cudaStream_t st, const TileRange& rg) {
+  const int ns = knobs().stages;
+#define LL_ACASE(NV_)                                                        \
+  if (nv == NV_) {                                                           \
+    if (ns <= 2) return launch_async_p<W, NV_, 2>(p, src, dst, max_ctas, st, rg); \
+    if (ns == 3) return launch_async_p<W, NV_, 3>(p, src, dst, max_ctas, st, rg); \
+    return launch_async_p<W, NV_, 4>(p, src, dst, max_ctas, st, rg);         \
+  }
+  LL_ACASE(1) LL_ACASE(2) LL_ACASE(4) LL_ACASE(8)
+#undef LL_ACASE
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_convert_async(const SmemPlan& p, int w, int nv, const void* src, void* dst,
+                                 int max_ctas, cudaStream_t st, const TileRange& rg) {
+  switch (w) {
+    case 1: return launch_async_w<1>(p, nv, src, dst, max_ctas, st, rg);
+    case 2: return launch_async_w<2>(p, nv, src, dst, max_ctas, st, rg);
+    case 4: return launch_async_w<4>(p, nv, src, dst, max_ctas, st, rg);
+    case 8: return launch_async_w<8>(p, nv, src, dst, max_ctas, st, rg);
   }
   return cudaErrorNotSupported;
 }

@@ -12,6 +12,8 @@ cudaError_t launch_convert_smem(const SmemPlan& p, int w, int nv, int g, const v
                                 void* dst, int max_ctas, cudaStream_t st, const TileRange& rg);
 cudaError_t launch_convert_shuffle(const ShufflePlan& p, int w, int nv, const void* src, void* dst,
                                    int max_ctas, cudaStream_t st, const TileRange& rg);
+cudaError_t launch_convert_async(const SmemPlan& p, int w, int nv, const void* src, void* dst,
+                                 int max_ctas, cudaStream_t st, const TileRange& rg);
 cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src, void* dst,
                                    int max_ctas, cudaStream_t st);
 cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* src,

@@ -649,6 +649,230 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   return true;
 }
 
+// Asynchronous-copy variant of the shared-memory path (LL_PATH_SMEM_ASYNC):
+// the source tile goes HBM -> shared memory with cp.async (16-byte chunks,
+// no registers, several tiles in flight per group), so the shared-memory
+// granule is the *source* 16-byte vector V = VS; the reading side holds
+// VS u VD in registers and permutes into destination vectors (prmt for the
+// sub-word bits, compile-time STG operand selection for the word bits).  The
+// swizzle S is the paper's construction for (writer, reader) with V = VS.
+bool plan_async(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js) {
+  const int n = P.nB, w = P.w;
+  if (P.nA != P.nB || n > 62 || w > 8) return false;
+  std::vector<int> sigma(n), sinv(n, -1);
+  for (int k = 0; k < n; ++k) {
+    if (popcount64(X[k]) != 1) return false;
+    sigma[k] = ctz64(X[k]);
+    if (sinv[sigma[k]] >= 0) return false;
+    sinv[sigma[k]] = k;
+  }
+  const int vb = ilog2i(16 / w);
+  if (n < vb + 5) return false;
+  auto contains = [](const std::vector<int>& v, int x) {
+    return std::find(v.begin(), v.end(), x) != v.end();
+  };
+  std::vector<int> VD, VS, CD, CS;
+  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
+  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
+  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
+  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
+  const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("thread_bytes", 64)) / w));
+  std::vector<int> need = VS;
+  for (int x : VD) if (!contains(need, x)) need.push_back(x);
+  if ((int)need.size() > r_max || (int)need.size() + 5 > n) return false;
+  int r = std::min(std::max((int)need.size(), r_pref), std::min(r_max, n - 5));
+  std::vector<int> T = VD;
+  for (auto* s : {&VS, &CD, &CS, &need})
+    for (int x : *s) if (!contains(T, x)) T.push_back(x);
+  for (int k = 0; (int)T.size() < r + 5 && k < n; ++k)
+    if (!contains(T, k)) T.push_back(k);
+  int g = (int)T.size() - r - 5;
+  if (g > 3) {
+    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
+    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
+  }
+  if (g < 0 || g > 3) return false;
+  std::sort(T.begin(), T.end());
+  // reader (store side): rho = VS (granule order), VD \ VS, extra (highest dst, not CD)
+  std::vector<int> rd_reg = VS;
+  for (int x : VD) if (!contains(rd_reg, x)) rd_reg.push_back(x);
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(rd_reg, x) && !contains(CD, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [](int a, int b) { return a > b; });
+    for (int x : cand) { if ((int)rd_reg.size() == r) break; rd_reg.push_back(x); }
+    if ((int)rd_reg.size() != r) return false;
+  }
+  std::vector<int> rd_lane, rd_warp;
+  {
+    for (int x : CD) if (!contains(rd_reg, x) && rd_lane.size() < 5) rd_lane.push_back(x);
+    std::vector<int> cand;
+    for (int x : T) if (!contains(rd_reg, x) && !contains(rd_lane, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end());
+    for (int x : cand) (rd_lane.size() < 5 ? rd_lane : rd_warp).push_back(x);
+  }
+  // writer (cp.async): rho = VS + unroll (highest src, not CS); lanes lowest src
+  std::vector<int> wr_reg = VS;
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(wr_reg, x) && !contains(CS, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) { return sigma[a] > sigma[b]; });
+    for (int x : cand) { if ((int)wr_reg.size() == r) break; wr_reg.push_back(x); }
+    if ((int)wr_reg.size() != r) return false;
+  }
+  std::vector<int> wr_lane, wr_warp;
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(wr_reg, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) { return sigma[a] < sigma[b]; });
+    for (int x : cand) (wr_lane.size() < 5 ? wr_lane : wr_warp).push_back(x);
+  }
+  if (rd_lane.size() != 5 || wr_lane.size() != 5 || (int)rd_warp.size() != g ||
+      (int)wr_warp.size() != g)
+    return false;
+  // reader sub-word swaps (prmt): rho positions 0..nsub-1 must hold VD[0..nsub)
+  const int nsub = w >= 4 ? 0 : ilog2i(4 / w);
+  std::vector<int> order = rd_reg;
+  std::vector<std::pair<int, int>> swaps;
+  for (int t = 0; t < nsub; ++t) {
+    int s = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
+    if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
+  }
+  if ((int)swaps.size() > LL_MAX_SWAPS) return false;
+  auto wordbit = [&](int rho) { return w == 8 ? rho + 1 : rho - nsub; };
+  const int LB = w == 8 ? r + 1 : r - nsub;
+  std::vector<int> ssel;  // word bits forming a 16-byte store vector (2 word bits)
+  if (w == 8) ssel.push_back(0);
+  for (int t = (w == 8 ? 0 : nsub); t < vb; ++t) {
+    int pos = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
+    ssel.push_back(wordbit(pos));
+  }
+  if (ssel.size() != 2) return false;
+  std::vector<int> rest_rho;  // rho positions of the remaining word bits, ascending word bit
+  for (int wb = 0; wb < LB; ++wb) {
+    if (std::find(ssel.begin(), ssel.end(), wb) != ssel.end()) continue;
+    rest_rho.push_back(w == 8 ? wb - 1 : wb + nsub);
+  }
+  // swizzle: paper's construction, V = VS (source vector), writer A, reader B
+  const int d = (int)T.size();
+  auto loc = [&](int k) -> u64 {
+    return u64(1) << (std::find(T.begin(), T.end(), k) - T.begin());
+  };
+  std::vector<u64> Al, Bl, Vl;
+  for (int x : wr_lane) Al.push_back(loc(x));
+  for (int x : rd_lane) Bl.push_back(loc(x));
+  for (int x : VS) Vl.push_back(loc(x));
+  SwizzleResult sw = optimal_swizzle(Al, Bl, Vl, d, w);
+  std::vector<u64> Scols = sw.vect;
+  Scols.insert(Scols.end(), sw.bank.begin(), sw.bank.end());
+  Scols.insert(Scols.end(), sw.idx.begin(), sw.idx.end());
+  auto Sinv = f2_right_inverse(Scols, d);
+  const int lw = ilog2i(w);
+  for (int k : T)
+    if (sigma[k] + lw >= 31 || k + lw >= 31) return false;
+  auto boff = [&](int k) -> uint32_t { return (uint32_t)f2_apply(Sinv, loc(k)) << lw; };
+  SmemPlan& sp = P.sp;
+  sp = SmemPlan{};
+  sp.gw = g;
+  sp.tile_bytes = w << d;
+  sp.n_swaps = (int)swaps.size();
+  for (size_t i = 0; i < swaps.size(); ++i) {
+    sp.swap_a[i] = (int8_t)swaps[i].first;
+    sp.swap_b[i] = (int8_t)swaps[i].second;
+  }
+  sp.gsel_a = (int8_t)ssel[0];
+  sp.gsel_b = (int8_t)ssel[1];
+  for (int b = 0; b < 5; ++b) {
+    sp.ld_thr[b] = uint32_t(w) << sigma[wr_lane[b]];
+    sp.st_thr[b] = uint32_t(w) << rd_lane[b];
+    sp.sw_thr[b] = boff(wr_lane[b]);
+    sp.sr_thr[b] = boff(rd_lane[b]);
+  }
+  for (int b = 0; b < g; ++b) {
+    sp.ld_thr[5 + b] = uint32_t(w) << sigma[wr_warp[b]];
+    sp.st_thr[5 + b] = uint32_t(w) << rd_warp[b];
+    sp.sw_thr[5 + b] = boff(wr_warp[b]);
+    sp.sr_thr[5 + b] = boff(rd_warp[b]);
+  }
+  const int nvec = 1 << (r - vb);
+  if (nvec > LL_MAX_VEC || nvec > LL_MAX_GRAN) return false;
+  for (int u = 0; u < nvec; ++u) {
+    uint32_t lo = 0, wo = 0, ro = 0, so = 0;
+    for (int q = 0; q < r - vb; ++q) {
+      if ((u >> q) & 1) {
+        lo += uint32_t(w) << sigma[wr_reg[vb + q]];   // chunk u: source offset
+        wo ^= boff(wr_reg[vb + q]);                    //          smem offset
+        ro ^= boff(rd_reg[vb + q]);                    // granule u read offset
+        so += uint32_t(w) << order[rest_rho[q]];       // store vector u: dst offset
+      }
+    }
+    sp.ld_vec[u] = lo;
+    sp.sw_gran[u] = wo;
+    sp.sr_gran[u] = ro;
+    sp.st_vec[u] = so;
+  }
+  // tile map (dst order; top bits last)
+  std::vector<int> O;
+  for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
+  if ((int)O.size() > LL_MAX_OUTER) return false;
+  TileMap& tm = sp.tile;
+  tm.n_bits = (int)O.size();
+  tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
+  for (int k = 0; k < tm.n_tab; ++k)
+    for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
+      int64_t so = 0, dof = 0;
+      for (int q = 0; q < LL_TAB_BITS; ++q) {
+        const int bit = k * LL_TAB_BITS + q;
+        if (((v >> q) & 1) && bit < tm.n_bits) {
+          so += int64_t(w) << sigma[O[bit]];
+          dof += int64_t(w) << O[bit];
+        }
+      }
+      tm.tab[k][v].src = so;
+      tm.tab[k][v].dst = dof;
+    }
+  tm.batch_stride_src = int64_t(w) << P.nA;
+  tm.batch_stride_dst = int64_t(w) << P.nB;
+  tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
+  P.tile_bit_src.clear();
+  P.tile_bit_dst.clear();
+  for (int q = 0; q < tm.n_bits; ++q) {
+    P.tile_bit_src.push_back(sigma[O[q]]);
+    P.tile_bit_dst.push_back(O[q]);
+  }
+  P.nv = nvec;
+  P.g = 16;
+  P.tile_bits = d;
+  P.r = r;
+  P.gw = g;
+  P.pred_wf_ld = lemma_wavefronts(sw, Al, w);
+  P.pred_wf_st = lemma_wavefronts(sw, Bl, w);
+  auto srcpos = [&](const std::vector<int>& v) {
+    std::vector<int> o;
+    for (int x : v) o.push_back(sigma[x]);
+    return o;
+  };
+  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
+     << ",\"granule_bytes\":16,\"granule_dst_bits\":" << ivec_json(VS)
+     << ",\"vectors_per_thread\":" << nvec << ",\"swaps\":[";
+  for (size_t i = 0; i < swaps.size(); ++i)
+    js << (i ? "," : "") << "[" << swaps[i].first << "," << swaps[i].second << "]";
+  js << "],\"stg_sel\":" << ivec_json(ssel) << ",\"wr_reg_dst\":" << ivec_json(wr_reg)
+     << ",\"wr_reg_src\":" << ivec_json(srcpos(wr_reg)) << ",\"wr_lane_dst\":" << ivec_json(wr_lane)
+     << ",\"wr_lane_src\":" << ivec_json(srcpos(wr_lane)) << ",\"wr_warp_dst\":" << ivec_json(wr_warp)
+     << ",\"rd_reg\":" << ivec_json(rd_reg) << ",\"rd_rho_after_swaps\":" << ivec_json(order)
+     << ",\"rd_lane\":" << ivec_json(rd_lane) << ",\"rd_warp\":" << ivec_json(rd_warp)
+     << ",\"S_vect\":" << vec_json(sw.vect) << ",\"S_bank\":" << vec_json(sw.bank)
+     << ",\"S_idx\":" << vec_json(sw.idx) << ",\"H\":" << vec_json(sw.H) << ",\"C\":" << vec_json(sw.C)
+     << ",\"unavoidable\":" << (sw.unavoidable ? "true" : "false")
+     << ",\"pred_wavefronts_per_cp_async\":" << P.pred_wf_ld
+     << ",\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"n_tiles\":" << tm.n_tiles
+     << ",\"smem_bytes\":{\"sw_thr\":" << u32_json(sp.sw_thr, 5 + g) << ",\"sr_thr\":"
+     << u32_json(sp.sr_thr, 5 + g) << ",\"sw_gran\":" << u32_json(sp.sw_gran, nvec)
+     << ",\"sr_gran\":" << u32_json(sp.sr_gran, nvec) << "}";
+  return true;
+}
+
 std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B, int w,
                                                 int path_req, int64_t batch) {
   if (!A.same_tensor(B)) throw Error(LL_ERR_SHAPE, "convert: source and destination layouts map to different tensors");
@@ -684,9 +908,18 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
       path = LL_PATH_GENERIC;
     }
   }
+  if (path == LL_PATH_SMEM_ASYNC) {
+    std::ostringstream js2;
+    if (plan_async(*P, X, js2)) {
+      js << js2.str();
+    } else {
+      throw Error(LL_ERR_UNSUPPORTED, "smem_async path requested but the quotient is not a tileable bit permutation");
+    }
+  }
   if (path == LL_PATH_GENERIC) fill_generic(*P, X);
   P->path = path;
-  static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle"};
+  static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle",
+                                "smem_async"};
   js << ",\"path\":\"" << names[path] << "\"}";
   P->json = js.str();
   return P;
@@ -737,7 +970,8 @@ TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
     rg.dst_shift = (int64_t)shard * ((w << P.nB) >> sb);
     return rg;
   }
-  if (P.path != LL_PATH_SMEM && P.path != LL_PATH_SHUFFLE && P.path != LL_PATH_SMEM_NOSWIZZLE)
+  if (P.path != LL_PATH_SMEM && P.path != LL_PATH_SHUFFLE && P.path != LL_PATH_SMEM_NOSWIZZLE &&
+      P.path != LL_PATH_SMEM_ASYNC)
     throw Error(LL_ERR_UNSUPPORTED, "shard: only tiled (smem / shuffle) plans are shardable");
   const int nb = (int)P.tile_bit_src.size();
   if (sb > nb) throw Error(LL_ERR_UNSUPPORTED, "shard: more shards than tiles");

@@ -19,7 +19,7 @@ from workloads import configs  # noqa: E402
 from workloads.values import indices_torch, values_torch  # noqa: E402
 
 
-DEFAULTS = {"tpg": 2, "pipe": 1, "carveout": -1, "pow2": 0, "thread_bytes": 64,
+DEFAULTS = {"tpg": 2, "pipe": 1, "carveout": -1, "pow2": 0, "stages": 3, "async_tpg": 8, "thread_bytes": 64,
             "thread_bytes_max": 128, "max_granule": 16, "run_bytes": 256, "tile_order": 0}
 
 

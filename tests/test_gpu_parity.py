@@ -71,12 +71,15 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "shuffle", "generic"])
+@pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "shuffle", "smem_async",
+                                  "generic"])
 @pytest.mark.parametrize("name,mk", CASES)
 def test_convert_configs_small(name, mk, path):
     c = mk()
     if path == "shuffle" and name.startswith("cfg3"):
         pytest.skip("transpose exchange is not warp-local (P:624); covered by test_shuffle_rejects")
+    if path == "smem_async" and name.startswith("cfg1"):
+        pytest.skip("16x16 tensor is smaller than one async tile")
     src, dst = run_convert(c, path=path)
     exp = expect_convert(c, src)
     assert dst.tobytes() == exp.tobytes()
@@ -136,6 +139,30 @@ def test_convert_random_pairs_shuffle(w):
         src, dst = run_convert(c, path="shuffle", seed=rng.randint(0, 1000))
         assert dst.tobytes() == expect_convert(c, src).tobytes()
         done += 1
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_random_pairs_async(w):
+    rng = random.Random(600 + w)
+    done = 0
+    while done < 10:
+        d = rng.randint(12, 16)
+        c = rand_pair(rng, d, w)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        try:
+            ll.plan_describe(A, B, 8 * w, "smem_async")
+        except ll.LLError:
+            continue
+        src, dst = run_convert(c, path="smem_async", seed=rng.randint(0, 1000))
+        assert dst.tobytes() == expect_convert(c, src).tobytes()
+        done += 1
+
+
+@pytest.mark.parametrize("batch", [3, 37])
+def test_convert_async_ragged_batch(batch):
+    c = configs.cfg2(batch_bits=0)
+    src, dst = run_convert(c, path="smem_async", batch=batch, seed=17)
+    assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
 
 
 @pytest.mark.parametrize("batch", [3, 37])

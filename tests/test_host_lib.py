@@ -225,3 +225,32 @@ def test_gather_plan_config4():
     assert ll.gather_describe(Lf, cf["axis"], 32)["path"] == "direct"
     with pytest.raises(ll.LLError):
         ll.gather_describe(Lf, cf["axis"], 32, "shuffle")
+
+
+@pytest.mark.parametrize("name,c", PLAN_CASES[2:])
+def test_async_plan_swizzle_conflict_free(name, c):
+    """cp.async path: granule = the source 16-byte vector; the paper's
+    construction for (writer, reader) with V = VS; brute-force bank counter."""
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    w = c["elem_bytes"]
+    d = ll.plan_describe(A, B, 8 * w, "smem_async")
+    assert d["path"] == "smem_async"
+    T = d["tile_dst_bits"]
+    loc = {k: 1 << i for i, k in enumerate(T)}
+    n = len(T)
+
+    def mk(reg, lane, warp):
+        return OLayout([("reg", len(reg)), ("lane", len(lane)), ("warp", len(warp))], [("t", n)],
+                       {"reg": [(loc[k],) for k in reg], "lane": [(loc[k],) for k in lane],
+                        "warp": [(loc[k],) for k in warp]})
+    Ao = mk(d["wr_reg_dst"], d["wr_lane_dst"], d["wr_warp_dst"])
+    Bo = mk(d["rd_reg"], d["rd_lane"], d["rd_warp"])
+    V = [loc[k] for k in d["granule_dst_bits"]]
+    S = OLayout([("offset", n)], [("t", n)], {"offset": [(x,) for x in d["S_vect"] + d["S_bank"] + d["S_idx"]]})
+    So, info = swizzle.optimal_swizzle(Ao, Bo, w, V=V)
+    assert So.cols == S.cols
+    vA = [d["wr_reg_dst"].index(k) for k in d["granule_dst_bits"]]
+    vB = [d["rd_reg"].index(k) for k in d["granule_dst_bits"]]
+    n_instr = (1 << (Ao.in_bits - 5)) // (1 << len(V))
+    assert banks.count_wavefronts(S, Ao, w, vA) == n_instr * 4
+    assert banks.count_wavefronts(S, Bo, w, vB) == n_instr * 4
