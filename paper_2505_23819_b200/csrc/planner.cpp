@@ -1031,7 +1031,10 @@ std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis,
   g.n_vec = (int64_t(1) << (n - vb)) * batch;
   const bool shuffle_ok = contig && n >= vb + 5 && (g.y_base + g.ax_bits) <= vb + 5;
   int path = path_req;
-  if (path == LL_PATH_AUTO) path = shuffle_ok ? LL_PATH_SHUFFLE : LL_PATH_GENERIC;
+  // AUTO: the direct (L1) gather -- measured faster than the warp-shuffle
+  // gather on B200 for HBM-resident data (profiles/r01/SUMMARY.md); the
+  // paper's shuffle gather is LL_PATH_SHUFFLE.
+  if (path == LL_PATH_AUTO) path = LL_PATH_GENERIC;
   if (path == LL_PATH_SHUFFLE && !shuffle_ok)
     throw Error(LL_ERR_UNSUPPORTED, "gather: shuffle path needs the axis inside one warp's registers and lanes (L_warp^axis = 0, P:722)");
   if (path != LL_PATH_SHUFFLE && path != LL_PATH_GENERIC)

@@ -218,8 +218,9 @@ def test_planner_random_pairs_conflict_free(w):
 def test_gather_plan_config4():
     c = configs.cfg4()
     L = ll.Layout.from_spec(c["L"])
-    d = ll.gather_describe(L, c["axis"], 32)
+    d = ll.gather_describe(L, c["axis"], 32, "shuffle")
     assert d["path"] == "shuffle" and d["candidate_shuffles"] == 4      # reading A19: 2^|L_reg^axis|
+    assert ll.gather_describe(L, c["axis"], 32)["path"] == "direct"     # AUTO: measured fastest
     cf = configs.cfg4(variant="full")
     Lf = ll.Layout.from_spec(cf["L"])
     assert ll.gather_describe(Lf, cf["axis"], 32)["path"] == "direct"
