@@ -213,25 +213,36 @@ u64 linop_apply_index(const std::array<int, 3>& op, u64 k) {
 // permutation or the tile does not fit.
 bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ostringstream& js,
                bool warp_tile = false) {
-  const int n = P.nB, w = P.w;
-  if (P.nA != P.nB || n > 62) return false;
-  std::vector<int> sigma(n), sinv(n, -1);
+  const int n = P.nB, nA = P.nA, w = P.w;
+  if (n > 62 || nA > 62) return false;
+  // sigma: dst bit -> src bit; -1 for destination broadcast bits (zero columns
+  // of X: the min-weight quotient makes every copy read the same source,
+  // P:607-610).  Source bits outside the image of sigma are source broadcast
+  // copies that are never read.
+  std::vector<int> sigma(n, -1), sinv(nA, -1), Zd;
   for (int k = 0; k < n; ++k) {
+    if (X[k] == 0) { Zd.push_back(k); continue; }
     if (popcount64(X[k]) != 1) return false;
     sigma[k] = ctz64(X[k]);
     if (sinv[sigma[k]] >= 0) return false;
     sinv[sigma[k]] = k;
   }
-  const int vb = ilog2i(16 / w);
-  if (n < vb + 5) return false;
-  std::vector<int> VD, VS, CD, CS;
-  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
-  // coalescing run: run_bytes contiguous bytes on both sides (default one 128-B line)
-  const int cbits = warp_tile ? 3 : std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
-  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
   auto contains = [](const std::vector<int>& v, int x) {
     return std::find(v.begin(), v.end(), x) != v.end();
   };
+  const int vb = ilog2i(16 / w);
+  const int neff = n - (int)Zd.size();  // bits of distinct elements
+  if (neff < vb + 5 || nA < vb) return false;
+  std::vector<int> VD, VS, CD, CS;
+  for (int k = 0; k < vb; ++k) {
+    if (sigma[k] < 0 || sinv[k] < 0) return false;  // vectors must be broadcast-free
+    VD.push_back(k);
+    VS.push_back(sinv[k]);
+  }
+  // coalescing run: run_bytes contiguous bytes on both sides (skipping broadcast bits)
+  const int cbits = warp_tile ? 3 : std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
+  for (int k = vb; k < n && (int)CD.size() < cbits; ++k) if (sigma[k] >= 0) CD.push_back(k);
+  for (int k = vb; k < nA && (int)CS.size() < cbits; ++k) if (sinv[k] >= 0) CS.push_back(sinv[k]);
   const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
   const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("thread_bytes", 64)) / w));
   int G = 0, gbits = 0, r = 0;
@@ -247,12 +258,12 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       std::vector<int> nd = VS;
       for (int x : Vc) if (!contains(nd, x)) nd.push_back(x);
       int rn = (int)nd.size();
-      if (rn > r_max || rn + 5 > n) continue;
+      if (rn > r_max || rn + 5 > neff) continue;
       bool clash = false;
       for (int x : nd) if (contains(CS, x)) clash = true;
       if (clash && pass == 0) continue;
       G = Gc; gbits = gb; V = Vc; need = nd;
-      r = std::min(std::max(rn, r_pref), std::min(r_max, n - 5));
+      r = std::min(std::max(rn, r_pref), std::min(r_max, neff - 5));
       break;
     }
   }
@@ -262,7 +273,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   for (auto* s : {&VS, &CD, &CS, &need})
     for (int x : *s) if (!contains(T, x)) T.push_back(x);
   for (int k = 0; (int)T.size() < r + 5 && k < n; ++k)
-    if (!contains(T, k)) T.push_back(k);
+    if (!contains(T, k) && sigma[k] >= 0) T.push_back(k);
   int g = (int)T.size() - r - 5;
   if (g > 3) {
     int r2 = std::min(r_max, (int)T.size() - 5 - 3);
@@ -418,11 +429,16 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   std::vector<int> by_dst = O, by_src = O;
   std::sort(by_src.begin(), by_src.end(), [&](int a, int b) { return sigma[a] < sigma[b]; });
   const int order_knob = planner_knob("tile_order", 0);
-  std::vector<int> torder;
+  // destination broadcast bits first: consecutive tiles then reuse the same
+  // source tile from L2 (each copy of a broadcast element is written, its
+  // source is fetched from HBM once)
+  std::vector<int> torder(Zd.begin(), Zd.end());
+  by_dst.erase(std::remove_if(by_dst.begin(), by_dst.end(), [&](int k) { return sigma[k] < 0; }), by_dst.end());
+  by_src.erase(std::remove_if(by_src.begin(), by_src.end(), [&](int k) { return sigma[k] < 0; }), by_src.end());
   if (order_knob == 0) {
-    torder = by_dst;
+    torder.insert(torder.end(), by_dst.begin(), by_dst.end());
   } else if (order_knob == 1) {
-    torder = by_src;
+    torder.insert(torder.end(), by_src.begin(), by_src.end());
   } else {
     size_t i = 0, j = 0;
     while (torder.size() < O.size()) {
@@ -441,7 +457,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       for (int q = 0; q < LL_TAB_BITS; ++q) {
         const int bit = k * LL_TAB_BITS + q;
         if (((v >> q) & 1) && bit < tm.n_bits) {
-          so += int64_t(w) << sigma[torder[bit]];
+          if (sigma[torder[bit]] >= 0) so += int64_t(w) << sigma[torder[bit]];
           dof += int64_t(w) << torder[bit];
         }
       }

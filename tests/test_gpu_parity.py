@@ -344,3 +344,56 @@ def test_misaligned_pointer_rejected():
     with pytest.raises(ll.LLError) as e:
         ll.convert(buf[1:], A, buf, B, 16)
     assert e.value.name == "LL_ERR_ARG"
+
+
+# ------------------------------------------------------------ broadcast layouts
+
+def _bcast_pair(rng, d, w, zeros_a, zeros_b, low_ok=False):
+    """Distributed layouts over a d-bit tensor with zero columns (broadcast,
+    P:528-537): zeros_a / zeros_b extra warp/block bits of A / B map to 0
+    (replicated warps / blocks), or anywhere when low_ok."""
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    out = [("i", d // 2), ("j", d - d // 2)]
+    tmp = OLayout([], out, {})
+    specs = []
+    for z in (zeros_a, zeros_b):
+        n = d + z
+        names = [("reg", vb + 1), ("lane", 5)]
+        rest = n - vb - 1 - 5
+        nw = min(rest, 2)
+        names += [("warp", nw), ("block", rest - nw)]
+        cols = [1 << k for k in range(d)]
+        rng.shuffle(cols)
+        if low_ok:
+            allc = cols + [0] * z
+            rng.shuffle(allc)
+        else:
+            # zeros in the high (warp / block) positions only
+            head = cols[:vb + 1 + 5]
+            tail = cols[vb + 1 + 5:] + [0] * z
+            rng.shuffle(tail)
+            allc = head + tail
+        bases, k = {}, 0
+        for nme, b in names:
+            bases[nme] = [tmp.unflatten(x) for x in allc[k:k + b]]
+            k += b
+        specs.append({"in_dims": names, "out_dims": out, "bases": bases})
+    return {"A": specs[0], "B": specs[1], "elem_bytes": w}
+
+
+@pytest.mark.parametrize("w", [1, 2, 4])
+@pytest.mark.parametrize("za,zb,low", [(0, 2, False), (2, 0, False), (1, 1, False), (2, 2, True)])
+def test_convert_broadcast_layouts(w, za, zb, low):
+    """Zero columns in B (destination copies, every copy written) and in A
+    (source copies, the lowest preimage is read).  High zero
+    columns stay on the tiled smem path; low ones fall back to the generic
+    kernel."""
+    rng = random.Random(700 + 10 * w + za + 3 * zb + (100 if low else 0))
+    for _ in range(4):
+        c = _bcast_pair(rng, rng.randint(12, 14), w, za, zb, low)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        path = ll.plan_describe(A, B, 8 * w)["path"]
+        if not low:
+            assert path == "smem", path
+        src, dst = run_convert(c, seed=rng.randint(0, 999))
+        assert dst.tobytes() == expect_convert(c, src).tobytes()

@@ -255,3 +255,18 @@ def test_async_plan_swizzle_conflict_free(name, c):
     n_instr = (1 << (Ao.in_bits - 5)) // (1 << len(V))
     assert banks.count_wavefronts(S, Ao, w, vA) == n_instr * 4
     assert banks.count_wavefronts(S, Bo, w, vB) == n_instr * 4
+
+
+def test_broadcast_plans_stay_tiled():
+    """Replicated warps / blocks (zero columns at high bits) keep the smem
+    path; the destination broadcast bits become the lowest tile-index bits."""
+    from tests.test_gpu_parity import _bcast_pair   # layout generator only
+    rng = random.Random(11)
+    for w in (1, 2, 4):
+        c = _bcast_pair(rng, 13, w, 1, 2)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        d = ll.plan_describe(A, B, 8 * w)
+        assert d["path"] == "smem"
+        X = d["X"]
+        zd = [k for k, x in enumerate(X) if x == 0]
+        assert len(zd) == 2 and d["tile_order_dst_bits"][:2] == zd
