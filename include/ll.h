@@ -144,7 +144,8 @@ typedef enum {
   LL_PATH_SHUFFLE = 3,   /* warp-local exchange with warp shuffles                 */
   LL_PATH_GENERIC = 4,   /* element-wise pull (any layouts; the slow baseline)     */
   LL_PATH_SMEM_NOSWIZZLE = 5, /* smem path with an unswizzled staging buffer (ablation) */
-  LL_PATH_SMEM_ASYNC = 6 /* smem path fed by cp.async (source granules, multi-stage) */
+  LL_PATH_SMEM_ASYNC = 6, /* smem path fed by cp.async (source granules, multi-stage)  */
+  LL_PATH_SMEM_PADDED = 7 /* legacy heuristic: unswizzled staging + 16 B pad per 128 B (ablation) */
 } ll_path;
 
 typedef struct {

@@ -278,7 +278,7 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
   if (n_shards > 1) {
     rg = ll::shard_range(*P, n_shards, shard);
   } else if (P->path == LL_PATH_SMEM || P->path == LL_PATH_SMEM_NOSWIZZLE ||
-             P->path == LL_PATH_SMEM_ASYNC) {
+             P->path == LL_PATH_SMEM_ASYNC || P->path == LL_PATH_SMEM_PADDED) {
     rg.t1 = P->sp.tile.n_tiles;
   } else if (P->path == LL_PATH_SHUFFLE) {
     rg.t1 = P->shp.tile.n_tiles;
@@ -301,6 +301,7 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
                          "ll_convert (async smem kernel)");
     case LL_PATH_SMEM:
     case LL_PATH_SMEM_NOSWIZZLE:
+    case LL_PATH_SMEM_PADDED:
       ++g_launches;
       return cuda_status(ll::launch_convert_smem(P->sp, w, P->nv, P->g, src, dst, max_ctas, st, rg),
                          "ll_convert (smem kernel)");

@@ -179,7 +179,7 @@ __host__ __device__ constexpr int deposit_word(int j, int k, int LB, int A, int 
 // wbase: (region base + buffer); wx: the thread's xor offset; the swizzled
 // offsets are combined by XOR *within* the region, then added to the base
 // (the dynamic shared window need not be aligned to the tile size).
-template <int NW, int GW, int A, int B>
+template <int NW, int GW, int A, int B, bool PAD = false>
 __device__ __forceinline__ void sts_granules(const uint32_t (&R)[NW], uint32_t wbase, uint32_t wx,
                                              const uint32_t* gran) {
   constexpr int LB = ilog2(NW);
@@ -189,11 +189,12 @@ __device__ __forceinline__ void sts_granules(const uint32_t (&R)[NW], uint32_t w
     uint32_t v[GW];
 #pragma unroll
     for (int k = 0; k < GW; ++k) v[k] = R[deposit_word(j, k, LB, A, B)];
-    sts<GW * 4>(wbase + (wx ^ gran[j]), v);
+    const uint32_t o = wx ^ gran[j];
+    sts<GW * 4>(wbase + (PAD ? o + ((o >> 7) << 4) : o), v);
   }
 }
 
-template <int NW, int GW, int A, int B>
+template <int NW, int GW, int A, int B, bool PAD>
 __device__ __forceinline__ bool sts_try_b(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
                                           uint32_t wx, const uint32_t* gran) {
   constexpr int LB = ilog2(NW);
@@ -202,15 +203,15 @@ __device__ __forceinline__ bool sts_try_b(int a, int b, const uint32_t (&R)[NW],
   } else {
     if constexpr (A != B) {
       if (a == A && b == B) {
-        sts_granules<NW, GW, A, B>(R, wbase, wx, gran);
+        sts_granules<NW, GW, A, B, PAD>(R, wbase, wx, gran);
         return true;
       }
     }
-    return sts_try_b<NW, GW, A, B + 1>(a, b, R, wbase, wx, gran);
+    return sts_try_b<NW, GW, A, B + 1, PAD>(a, b, R, wbase, wx, gran);
   }
 }
 
-template <int NW, int GW, int A>
+template <int NW, int GW, int A, bool PAD>
 __device__ __forceinline__ bool sts_try_a(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
                                           uint32_t wx, const uint32_t* gran) {
   constexpr int LB = ilog2(NW);
@@ -221,24 +222,24 @@ __device__ __forceinline__ bool sts_try_a(int a, int b, const uint32_t (&R)[NW],
     if constexpr (GW == 2) {
       done = false;
       if (a == A) {
-        sts_granules<NW, 2, A, -1>(R, wbase, wx, gran);
+        sts_granules<NW, 2, A, -1, PAD>(R, wbase, wx, gran);
         done = true;
       }
     } else {
-      done = sts_try_b<NW, GW, A, 0>(a, b, R, wbase, wx, gran);
+      done = sts_try_b<NW, GW, A, 0, PAD>(a, b, R, wbase, wx, gran);
     }
     if (done) return true;
-    return sts_try_a<NW, GW, A + 1>(a, b, R, wbase, wx, gran);
+    return sts_try_a<NW, GW, A + 1, PAD>(a, b, R, wbase, wx, gran);
   }
 }
 
-template <int NW, int GW>
+template <int NW, int GW, bool PAD = false>
 __device__ __forceinline__ void sts_dispatch(int a, int b, const uint32_t (&R)[NW], uint32_t wbase,
                                              uint32_t wx, const uint32_t* gran) {
   if constexpr (GW == 1) {
-    sts_granules<NW, 1, -1, -1>(R, wbase, wx, gran);
+    sts_granules<NW, 1, -1, -1, PAD>(R, wbase, wx, gran);
   } else {
-    sts_try_a<NW, GW, 0>(a, b, R, wbase, wx, gran);
+    sts_try_a<NW, GW, 0, PAD>(a, b, R, wbase, wx, gran);
   }
 }
 
@@ -260,7 +261,11 @@ __device__ __forceinline__ void load_tile(uint32_t (&R)[NV * 4], const uint8_t* 
   }
 }
 
-template <int W, int NV, int G, bool PIPE>
+// PAD: the legacy padding heuristic (ablation, LL_PATH_SMEM_PADDED): the
+// staging offsets are unswizzled and 16 bytes of padding follow every 128 B.
+__device__ __forceinline__ uint32_t pad_off(uint32_t o) { return o + ((o >> 7) << 4); }
+
+template <int W, int NV, int G, bool PIPE, bool PAD>
 __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
     if (!PIPE) load_tile<NV>(R, sthr + so, p.ld_vec);
     const int64_t dcur = dof;
     for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
-    sts_dispatch<NW, GW>(ga, gb, R, sbase + buf, swx, p.sw_gran);
+    sts_dispatch<NW, GW, PAD>(ga, gb, R, sbase + buf, swx, p.sw_gran);
     if (PIPE) {
       const int64_t tn = t + n_groups;
       if (tn < n_tiles) {
@@ -339,7 +344,10 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
     group_sync(gw, group);
     uint32_t Q[NW];
 #pragma unroll
-    for (int j = 0; j < NG; ++j) lds<G>(sbase + buf + (srx ^ p.sr_gran[j]), &Q[j * GW]);
+    for (int j = 0; j < NG; ++j) {
+      const uint32_t o = srx ^ p.sr_gran[j];
+      lds<G>(sbase + buf + (PAD ? pad_off(o) : o), &Q[j * GW]);
+    }
     uint8_t* dp = dthr + dcur;
 #pragma unroll
     for (int u = 0; u < NV; ++u)
@@ -876,13 +884,13 @@ int set_knob(const char* name, int value) {
   return -1;
 }
 
-template <int W, int NV, int G, bool PIPE>
+template <int W, int NV, int G, bool PIPE, bool PAD>
 static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, int max_ctas,
                                  cudaStream_t st, const TileRange& rg) {
-  auto k = convert_smem_kernel<W, NV, G, PIPE>;
+  auto k = convert_smem_kernel<W, NV, G, PIPE, PAD>;
   const int threads = 256;
   const int gpc = (threads / 32) >> p.gw;
-  const size_t smem = (size_t)gpc * 2 * p.tile_bytes;
+  const size_t smem = (size_t)gpc * 2 * p.tile_bytes;  // tile_bytes includes any padding
   static int occ_cache = -1;
   static size_t occ_smem = 0;
   static int occ_carve = -2;
@@ -911,8 +919,9 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
 template <int W, int NV, int G>
 static cudaError_t launch_smem_t(const SmemPlan& p, const void* src, void* dst, int max_ctas,
                                  cudaStream_t st, const TileRange& rg) {
-  if (knobs().pipe) return launch_smem_p<W, NV, G, true>(p, src, dst, max_ctas, st, rg);
-  return launch_smem_p<W, NV, G, false>(p, src, dst, max_ctas, st, rg);
+  if (p.pad) return launch_smem_p<W, NV, G, true, true>(p, src, dst, max_ctas, st, rg);
+  if (knobs().pipe) return launch_smem_p<W, NV, G, true, false>(p, src, dst, max_ctas, st, rg);
+  return launch_smem_p<W, NV, G, false, false>(p, src, dst, max_ctas, st, rg);
 }
 
 template <int W>
@@ -1065,8 +1074,8 @@ static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void
                                    cudaStream_t st) {
   const int threads = 256;
   // 16-byte output vectors per thread (measured on B200: 4 for the shuffle
-  // kernel, 2 for the direct kernel); the knob overrides
-  const int vpt = knobs().gather_tpt > 0 ? knobs().gather_tpt : (shuffle ? 4 : 2);
+  // kernel, 1 for the direct kernel); the knob overrides
+  const int vpt = knobs().gather_tpt > 0 ? knobs().gather_tpt : (shuffle ? 4 : 1);
   int64_t want = (p.n_vec + (int64_t)threads * vpt - 1) / ((int64_t)threads * vpt);
   if (max_ctas > 0 && want > max_ctas) want = max_ctas;
   int grid = (int)(want < 0x7fffffff ? want : 0x7fffffff);

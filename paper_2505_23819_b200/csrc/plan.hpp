@@ -50,7 +50,8 @@ struct TileMap {
 struct SmemPlan {
   TileMap tile;
   int32_t gw;           // log2 warps per tile group
-  int32_t tile_bytes;   // bytes per tile (smem per buffer)
+  int32_t tile_bytes;   // bytes per tile (smem per buffer, padding included)
+  int32_t pad;          // 1: unswizzled + 16 B padding per 128 B (legacy heuristic, ablation)
   int32_t n_swaps;      // sub-word register-bit swaps (prmt), swap_a < sub-word bits
   int8_t swap_a[LL_MAX_SWAPS], swap_b[LL_MAX_SWAPS];
   int8_t gsel_a, gsel_b;          // register word bits forming a write granule (-1: unused)

@@ -381,6 +381,10 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     if (sigma[k] + lw >= 31 || k + lw >= 31) return false;  // 32-bit in-tile byte offsets
   sp.gw = g;
   sp.tile_bytes = w << d;
+  if (P.padded) {
+    sp.pad = 1;
+    sp.tile_bytes += sp.tile_bytes / 8;
+  }
   sp.n_swaps = (int)swaps.size();
   for (size_t i = 0; i < swaps.size(); ++i) {
     sp.swap_a[i] = (int8_t)swaps[i].first;
@@ -910,9 +914,12 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
   if (path == LL_PATH_AUTO) path = ident ? LL_PATH_COPY : LL_PATH_SMEM;
   if (path == LL_PATH_COPY && !ident)
     throw Error(LL_ERR_UNSUPPORTED, "copy path requested but the quotient is not the identity");
-  if (path == LL_PATH_SMEM || path == LL_PATH_SMEM_NOSWIZZLE || path == LL_PATH_SHUFFLE) {
+  if (path == LL_PATH_SMEM_PADDED) P->padded = true;
+  if (path == LL_PATH_SMEM || path == LL_PATH_SMEM_NOSWIZZLE || path == LL_PATH_SHUFFLE ||
+      path == LL_PATH_SMEM_PADDED) {
     std::ostringstream js2;
-    if (plan_smem(*P, X, path != LL_PATH_SMEM_NOSWIZZLE, js2, path == LL_PATH_SHUFFLE)) {
+    if (plan_smem(*P, X, path == LL_PATH_SMEM || path == LL_PATH_SHUFFLE, js2,
+                  path == LL_PATH_SHUFFLE)) {
       js << js2.str();
       if (path == LL_PATH_SHUFFLE && !P->shuffle_ok)
         throw Error(LL_ERR_UNSUPPORTED,
@@ -935,7 +942,7 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
   if (path == LL_PATH_GENERIC) fill_generic(*P, X);
   P->path = path;
   static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle",
-                                "smem_async"};
+                                "smem_async", "smem_padded"};
   js << ",\"path\":\"" << names[path] << "\"}";
   P->json = js.str();
   return P;
@@ -987,7 +994,7 @@ TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
     return rg;
   }
   if (P.path != LL_PATH_SMEM && P.path != LL_PATH_SHUFFLE && P.path != LL_PATH_SMEM_NOSWIZZLE &&
-      P.path != LL_PATH_SMEM_ASYNC)
+      P.path != LL_PATH_SMEM_ASYNC && P.path != LL_PATH_SMEM_PADDED)
     throw Error(LL_ERR_UNSUPPORTED, "shard: only tiled (smem / shuffle) plans are shardable");
   const int nb = (int)P.tile_bit_src.size();
   if (sb > nb) throw Error(LL_ERR_UNSUPPORTED, "shard: more shards than tiles");

@@ -33,6 +33,7 @@ struct ConvertPlan {
   int nA = 0, nB = 0;
   int64_t batch = 1;
   bool identity = false;
+  bool padded = false;
   // smem path
   SmemPlan sp{};
   int nv = 0, g = 0;

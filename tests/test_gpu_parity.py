@@ -71,8 +71,8 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "shuffle", "smem_async",
-                                  "generic"])
+@pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "smem_padded", "shuffle",
+                                  "smem_async", "generic"])
 @pytest.mark.parametrize("name,mk", CASES)
 def test_convert_configs_small(name, mk, path):
     c = mk()
@@ -397,3 +397,14 @@ def test_convert_broadcast_layouts(w, za, zb, low):
             assert path == "smem", path
         src, dst = run_convert(c, seed=rng.randint(0, 999))
         assert dst.tobytes() == expect_convert(c, src).tobytes()
+
+
+@pytest.mark.parametrize("mb,nb", [(6, 6), (7, 9), (10, 8)])
+def test_fp8_transpose_paths(mb, nb):
+    """fig:matrix-size workload: fp8 transposes through the three
+    staging layouts agree with the oracle."""
+    c = configs.cfg3(n_bits=nb, m_bits=mb)
+    c = dict(c, elem_bytes=1)
+    for path in ("smem", "smem_padded", "smem_noswizzle"):
+        src, dst = run_convert(c, path=path, seed=mb * 31 + nb)
+        assert dst.tobytes() == expect_convert(c, src).tobytes(), path
