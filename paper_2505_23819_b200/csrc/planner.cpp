@@ -239,45 +239,53 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     VD.push_back(k);
     VS.push_back(sinv[k]);
   }
-  // coalescing run: run_bytes contiguous bytes on both sides (skipping broadcast bits)
-  const int cbits = warp_tile ? 3 : std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
-  for (int k = vb; k < n && (int)CD.size() < cbits; ++k) if (sigma[k] >= 0) CD.push_back(k);
-  for (int k = vb; k < nA && (int)CS.size() < cbits; ++k) if (sinv[k] >= 0) CS.push_back(sinv[k]);
   const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
   const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("thread_bytes", 64)) / w));
-  int G = 0, gbits = 0, r = 0;
-  std::vector<int> V, need;
-  // Granule choice: the largest prefix of the destination vector that the
-  // load side can also hold in registers; prefer choices that keep the
-  // source coalescing bits out of the registers.
-  for (int pass = 0; pass < 2 && !G; ++pass) {
-    for (int Gc : {16, 8, 4}) {
-      if (Gc < w || Gc < 4 || Gc > planner_knob("max_granule", 16)) continue;
-      int gb = ilog2i(Gc / w);
-      std::vector<int> Vc(VD.begin(), VD.begin() + gb);
-      std::vector<int> nd = VS;
-      for (int x : Vc) if (!contains(nd, x)) nd.push_back(x);
-      int rn = (int)nd.size();
-      if (rn > r_max || rn + 5 > neff) continue;
-      bool clash = false;
-      for (int x : nd) if (contains(CS, x)) clash = true;
-      if (clash && pass == 0) continue;
-      G = Gc; gbits = gb; V = Vc; need = nd;
-      r = std::min(std::max(rn, r_pref), std::min(r_max, neff - 5));
-      break;
+  int G = 0, gbits = 0, r = 0, g = -1;
+  std::vector<int> V, need, T;
+  // coalescing run: run_bytes contiguous bytes on both sides (skipping broadcast
+  // bits); shortened (down to 128 B) when the tile would not fit 8 warps
+  int cbits = warp_tile ? 3 : std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
+  for (; cbits >= std::min(cbits, 3); --cbits) {
+    CD.clear();
+    CS.clear();
+    for (int k = vb; k < n && (int)CD.size() < cbits; ++k) if (sigma[k] >= 0) CD.push_back(k);
+    for (int k = vb; k < nA && (int)CS.size() < cbits; ++k) if (sinv[k] >= 0) CS.push_back(sinv[k]);
+    G = 0;
+    // Granule choice: the largest prefix of the destination vector that the
+    // load side can also hold in registers; prefer choices that keep the
+    // source coalescing bits out of the registers.
+    for (int pass = 0; pass < 2 && !G; ++pass) {
+      for (int Gc : {16, 8, 4}) {
+        if (Gc < w || Gc < 4 || Gc > planner_knob("max_granule", 16)) continue;
+        int gb = ilog2i(Gc / w);
+        std::vector<int> Vc(VD.begin(), VD.begin() + gb);
+        std::vector<int> nd = VS;
+        for (int x : Vc) if (!contains(nd, x)) nd.push_back(x);
+        int rn = (int)nd.size();
+        if (rn > r_max || rn + 5 > neff) continue;
+        bool clash = false;
+        for (int x : nd) if (contains(CS, x)) clash = true;
+        if (clash && pass == 0) continue;
+        G = Gc; gbits = gb; V = Vc; need = nd;
+        r = std::min(std::max(rn, r_pref), std::min(r_max, neff - 5));
+        break;
+      }
     }
-  }
-  if (!G) return false;
-  // tile bits T (dst bit ids)
-  std::vector<int> T = VD;
-  for (auto* s : {&VS, &CD, &CS, &need})
-    for (int x : *s) if (!contains(T, x)) T.push_back(x);
-  for (int k = 0; (int)T.size() < r + 5 && k < n; ++k)
-    if (!contains(T, k) && sigma[k] >= 0) T.push_back(k);
-  int g = (int)T.size() - r - 5;
-  if (g > 3) {
-    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
-    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
+    if (!G) return false;
+    // tile bits T (dst bit ids)
+    T = VD;
+    for (auto* s : {&VS, &CD, &CS, &need})
+      for (int x : *s) if (!contains(T, x)) T.push_back(x);
+    for (int k = 0; (int)T.size() < r + 5 && k < n; ++k)
+      if (!contains(T, k) && sigma[k] >= 0) T.push_back(k);
+    g = (int)T.size() - r - 5;
+    if (g > 3) {
+      int r2 = std::min(r_max, (int)T.size() - 5 - 3);
+      if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
+    }
+    if (g >= 0 && g <= 3) break;
+    if (cbits <= 3) break;
   }
   if (g < 0 || g > 3) return false;
   std::sort(T.begin(), T.end());
