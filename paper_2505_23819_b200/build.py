@@ -20,9 +20,9 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["kernels.cu"]
+CU_SOURCES = ["kernel_smem.cu", "kernel_async.cu", "kernel_shuffle.cu", "kernel_misc.cu"]
 CPP_SOURCES = ["core.cpp", "planner.cpp", "capi.cpp"]
-HEADERS = ["core.hpp", "plan.hpp", "planner.hpp", "kernels.hpp"]
+HEADERS = ["core.hpp", "plan.hpp", "planner.hpp", "kernels.hpp", "device_common.cuh"]
 
 
 def _mtime(p):
@@ -54,6 +54,10 @@ def _compile(src, force):
 def build(force=False, verbose=False):
     os.makedirs(BUILD, exist_ok=True)
     srcs = CU_SOURCES + CPP_SOURCES
+    # stale objects of renamed sources must not be linked
+    for f in os.listdir(BUILD):
+        if f.endswith(".o") and f[:-2] not in srcs:
+            os.remove(os.path.join(BUILD, f))
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         results = list(ex.map(lambda s: _compile(s, force), srcs))
     objs = [o for o, _ in results]

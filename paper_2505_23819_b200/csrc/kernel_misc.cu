@@ -1,0 +1,320 @@
+// kernel_misc.cu -- generic pull kernel, gather kernels, launch knobs.
+#include "device_common.cuh"
+
+namespace ll {
+
+// ------------------------------------------------------------ generic kernel
+
+// dst[h] = src[X h]: each thread writes one 16-byte destination vector; the
+// source elements are fetched one by one (the slow, always-applicable path).
+template <int W>
+__global__ void __launch_bounds__(256) convert_generic_kernel(const __grid_constant__ GenericPlan p,
+                                                              const uint8_t* __restrict__ src,
+                                                              uint8_t* __restrict__ dst) {
+  constexpr int NE = 16 / W;
+  constexpr int VB = ilog2(NE);
+  using T = typename std::conditional<W == 1, uint8_t,
+            typename std::conditional<W == 2, uint16_t,
+            typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
+  const int64_t per_batch = (p.nB >= VB) ? (int64_t(1) << (p.nB - VB)) : 1;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n_vec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = v / per_batch;
+    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    uint64_t x0 = 0;
+    for (int k = VB; k < p.nB; ++k)
+      if ((h0 >> k) & 1) x0 ^= (uint64_t)p.x[k];
+    const T* s = reinterpret_cast<const T*>(src) + b * p.batch_stride_src;
+    T* d = reinterpret_cast<T*>(dst) + b * p.batch_stride_dst + h0;
+    union {
+      uint4 v4;
+      T e[NE];
+    } out;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      uint64_t x = x0;
+#pragma unroll
+      for (int k = 0; k < VB; ++k)
+        if ((e >> k) & 1) x ^= (uint64_t)p.x[k];
+      out.e[e] = (e < (1 << (p.nB < VB ? p.nB : VB))) ? __ldg(s + x) : T(0);
+    }
+    if (p.nB >= VB) {
+      *reinterpret_cast<uint4*>(d) = out.v4;
+    } else {
+      for (int e = 0; e < (1 << p.nB); ++e) d[e] = out.e[e];
+    }
+  }
+}
+
+// ------------------------------------------------------------ gather kernels
+
+// Direct gather: each thread produces one 16-byte output vector; source
+// elements are read through L1 (the rows a warp gathers from are the rows it
+// covers, so L1 absorbs the reuse).  Works for any axis placement.
+template <int W>
+__global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constant__ GatherPlan p,
+                                                            const uint8_t* __restrict__ src,
+                                                            const int32_t* __restrict__ idx,
+                                                            uint8_t* __restrict__ out,
+                                                            int* __restrict__ err) {
+  constexpr int NE = 16 / W;
+  constexpr int VB = ilog2(NE);
+  using T = typename std::conditional<W == 1, uint8_t,
+            typename std::conditional<W == 2, uint16_t,
+            typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
+  const int64_t per_batch = int64_t(1) << (p.nbits - VB);
+  const uint32_t amask = (1u << p.ax_bits) - 1;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n_vec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = v / per_batch;
+    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    const T* s = reinterpret_cast<const T*>(src) + b * p.batch_stride;
+    const int32_t* ip = idx + b * p.batch_stride + h0;
+    // warm L1 with this thread's own source vector while the indices load: for
+    // row-local axes the warp's gathers then hit lines already in flight
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(s + h0));
+    int32_t iv[NE];
+    if constexpr (NE >= 4) {
+#pragma unroll
+      for (int q = 0; q < NE / 4; ++q) {
+        int4 t = __ldg(reinterpret_cast<const int4*>(ip) + q);
+        iv[4 * q] = t.x; iv[4 * q + 1] = t.y; iv[4 * q + 2] = t.z; iv[4 * q + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NE; ++q) iv[q] = __ldg(ip + q);
+    }
+    union {
+      uint4 v4;
+      T e[NE];
+    } o;
+    // axis coordinate of h0's elements and the "cleared" base
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const uint64_t h = h0 | (uint64_t)e;
+      uint64_t hs;
+      uint32_t i = (uint32_t)iv[e];
+      if (p.check && i > amask) atomicExch(err, 1);
+      i &= amask;
+      if (p.y_contig) {
+        hs = (h & ~(uint64_t)p.axis_mask_buf) | ((uint64_t)i << p.y_base);
+      } else {
+        // h* = h ^ Y(axis(h) ^ idx)
+        uint64_t t = 0;
+        for (int k = 0; k < p.nbits; ++k)
+          if ((h >> k) & 1) t ^= (uint64_t)p.L[k];
+        uint32_t a = (uint32_t)(t >> p.ax_shift) & amask;
+        uint32_t dlt = a ^ i;
+        hs = h;
+        for (int k = 0; k < p.ax_bits; ++k)
+          if ((dlt >> k) & 1) hs ^= (uint64_t)p.Y[k];
+      }
+      o.e[e] = __ldg(s + hs);
+    }
+    *reinterpret_cast<uint4*>(reinterpret_cast<T*>(out) + b * p.batch_stride + h0) = o.v4;
+  }
+}
+
+// Warp-shuffle gather (reading A19): each lane holds one 16-byte
+// vector of src (registers = the vector's elements, lanes = the next five
+// buffer bits).  For each output element the source (register, lane) comes
+// from h* = (h with axis replaced); one shuffle per candidate register
+// (2^|L_reg^axis|, mask `cand_mask`), keeping the value whose register
+// matches.  Requires the axis to live in the warp's buffer bits (vb + 5).
+// ALLC: the axis covers every register bit (cand_mask = NE-1): all NE words
+// are shuffled from the source lane and a select tree picks the element.
+template <int W, bool ALLC>
+__global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_constant__ GatherPlan p,
+                                                             const uint8_t* __restrict__ src,
+                                                             const int32_t* __restrict__ idx,
+                                                             uint8_t* __restrict__ out,
+                                                             int* __restrict__ err) {
+  constexpr int NE = 16 / W;
+  constexpr int VB = ilog2(NE);
+  using T = typename std::conditional<W == 1, uint8_t,
+            typename std::conditional<W == 2, uint16_t,
+            typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t per_batch = int64_t(1) << (p.nbits - VB);
+  const uint32_t amask = (1u << p.ax_bits) - 1;
+  const int64_t nwarps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_wvec = p.n_vec >> 5;  // warps' worth of vectors
+  const uint32_t clear32 = ~(uint32_t)p.axis_mask_buf;
+  const int ybase = p.y_base;
+  for (int64_t wv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wv < n_wvec;
+       wv += nwarps_total) {
+    const int64_t v = (wv << 5) | lane;
+    const int64_t b = v / per_batch;
+    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    const uint8_t* sbase = src + (b * p.batch_stride) * W;
+    union {
+      uint4 v4;
+      T e[NE];
+      uint32_t w[4];
+    } sv, o;
+    sv.v4 = ldg_stream(sbase + h0 * W);
+    const int32_t* ip = idx + b * p.batch_stride + h0;
+    int32_t iv[NE];
+    if constexpr (NE >= 4) {
+#pragma unroll
+      for (int q = 0; q < NE / 4; ++q) {
+        int4 t = __ldg(reinterpret_cast<const int4*>(ip) + q);
+        iv[4 * q] = t.x; iv[4 * q + 1] = t.y; iv[4 * q + 2] = t.z; iv[4 * q + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NE; ++q) iv[q] = __ldg(ip + q);
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      // only the warp-local bits (VB + 5) of h* matter here: 32-bit arithmetic
+      uint32_t i = (uint32_t)iv[e];
+      if (p.check && i > amask) atomicExch(err, 1);
+      i &= amask;
+      const uint32_t hl = (((uint32_t)lane << VB) | (uint32_t)e) & clear32;
+      const uint32_t hs = hl | (i << ybase);
+      const int src_lane = (int)((hs >> VB) & 31);
+      const int src_reg = (int)(hs & (NE - 1));
+      if constexpr (ALLC && W == 4) {
+        // four shuffles, then a 2-level select on the register index
+        const uint32_t g0 = __shfl_sync(0xffffffffu, sv.w[0], src_lane);
+        const uint32_t g1 = __shfl_sync(0xffffffffu, sv.w[1], src_lane);
+        const uint32_t g2 = __shfl_sync(0xffffffffu, sv.w[2], src_lane);
+        const uint32_t g3 = __shfl_sync(0xffffffffu, sv.w[3], src_lane);
+        const uint32_t lo = (src_reg & 1) ? g1 : g0;
+        const uint32_t hi = (src_reg & 1) ? g3 : g2;
+        o.e[e] = (T)((src_reg & 2) ? hi : lo);
+      } else {
+        T val = 0;
+        // candidate rounds: every register index the axis can select, i.e. the
+        // registers that agree with e outside cand_mask (2^|L_reg^axis| shuffles)
+#pragma unroll
+        for (int c = 0; c < NE; ++c) {
+          if (ALLC || ((c ^ e) & ~p.cand_mask) == 0) {
+            T got;
+            if constexpr (W == 8) {
+              uint32_t lo = __shfl_sync(0xffffffffu, sv.w[2 * c], src_lane);
+              uint32_t hi = __shfl_sync(0xffffffffu, sv.w[2 * c + 1], src_lane);
+              got = (T)(((uint64_t)hi << 32) | lo);
+            } else if constexpr (W == 4) {
+              got = (T)__shfl_sync(0xffffffffu, sv.w[c], src_lane);
+            } else {
+              // sub-word elements: shuffle the containing word, then extract
+              uint32_t wd = __shfl_sync(0xffffffffu, sv.w[(c * W) >> 2], src_lane);
+              got = (T)(wd >> (((c * W) & 3) * 8));
+            }
+            if (src_reg == c) val = got;
+          }
+        }
+        o.e[e] = val;
+      }
+    }
+    stg_stream(out + (b * p.batch_stride + h0) * W, o.v4);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+
+static int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Launch configuration knobs (env, read once): LL_TPG = target tiles per tile
+// group (0 = persistent grid at full occupancy), LL_PIPE = 1 for the
+// software-pipelined kernel.
+LaunchKnobs::LaunchKnobs()
+      : tpg(env_int("LL_TPG", 2)), pipe(env_int("LL_PIPE", 1)),
+        gather_tpt(env_int("LL_GATHER_VPT", 0)), carveout(env_int("LL_CARVEOUT", -1)),
+        pow2(env_int("LL_POW2", 0)), stages(env_int("LL_STAGES", 3)),
+        async_tpg(env_int("LL_ASYNC_TPG", 8)) {}
+LaunchKnobs& knobs() {
+  static LaunchKnobs k;
+  return k;
+}
+
+int set_knob(const char* name, int value) {
+  std::string n(name ? name : "");
+  if (n == "tpg") { knobs().tpg = value; return 0; }
+  if (n == "pipe") { knobs().pipe = value; return 0; }
+  if (n == "gather_vpt") { knobs().gather_tpt = value; return 0; }
+  if (n == "carveout") { knobs().carveout = value; return 0; }
+  if (n == "pow2") { knobs().pow2 = value; return 0; }
+  if (n == "stages") { knobs().stages = value; return 0; }
+  if (n == "async_tpg") { knobs().async_tpg = value; return 0; }
+  return -1;
+}
+
+template <int W>
+static cudaError_t launch_generic_t(const GenericPlan& p, const void* src, void* dst, int max_ctas,
+                                    cudaStream_t st) {
+  const int threads = 256;
+  int64_t want = (p.n_vec + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (max_ctas > 0 && cap > max_ctas) cap = max_ctas;
+  int grid = (int)(want < cap ? want : cap);
+  if (grid < 1) grid = 1;
+  convert_generic_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, (uint8_t*)dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src, void* dst,
+                                   int max_ctas, cudaStream_t st) {
+  switch (w) {
+    case 1: return launch_generic_t<1>(p, src, dst, max_ctas, st);
+    case 2: return launch_generic_t<2>(p, src, dst, max_ctas, st);
+    case 4: return launch_generic_t<4>(p, src, dst, max_ctas, st);
+    case 8: return launch_generic_t<8>(p, src, dst, max_ctas, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int W>
+static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void* src,
+                                   const int32_t* idx, void* out, int* err, int max_ctas,
+                                   cudaStream_t st) {
+  const int threads = 256;
+  // 16-byte output vectors per thread (measured on B200: 4 for the shuffle
+  // kernel, 1 for the direct kernel); the knob overrides
+  const int vpt = knobs().gather_tpt > 0 ? knobs().gather_tpt : (shuffle ? 4 : 1);
+  int64_t want = (p.n_vec + (int64_t)threads * vpt - 1) / ((int64_t)threads * vpt);
+  if (max_ctas > 0 && want > max_ctas) want = max_ctas;
+  int grid = (int)(want < 0x7fffffff ? want : 0x7fffffff);
+  if (grid < 1) grid = 1;
+  if (shuffle && p.cand_mask == (16 / W) - 1)
+    gather_shuffle_kernel<W, true><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx,
+                                                            (uint8_t*)out, err);
+  else if (shuffle)
+    gather_shuffle_kernel<W, false><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx,
+                                                             (uint8_t*)out, err);
+  else
+    gather_direct_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
+                                                     err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* src,
+                          const int32_t* idx, void* out, int* err, int max_ctas, cudaStream_t st) {
+  switch (w) {
+    case 1: return launch_gather_t<1>(p, shuffle, src, idx, out, err, max_ctas, st);
+    case 2: return launch_gather_t<2>(p, shuffle, src, idx, out, err, max_ctas, st);
+    case 4: return launch_gather_t<4>(p, shuffle, src, idx, out, err, max_ctas, st);
+    case 8: return launch_gather_t<8>(p, shuffle, src, idx, out, err, max_ctas, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+int device_sm_count() { return num_sms(); }
+
+}  // namespace ll

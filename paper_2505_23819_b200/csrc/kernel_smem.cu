@@ -1,0 +1,161 @@
+// kernel_smem.cu -- shared-memory conversion kernel (paper's optimal swizzle) and launcher.
+#include "device_common.cuh"
+
+namespace ll {
+
+template <int W, int NV, int G, bool PIPE, bool PAD>
+__global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
+                                                           const uint8_t* __restrict__ src,
+                                                           uint8_t* __restrict__ dst,
+                                                           int64_t n_groups, TileRange rg) {
+  constexpr int NW = NV * 4;          // 32-bit words per thread
+  constexpr int NG = NV * 16 / G;     // granules per thread
+  constexpr int GW = G / 4;           // words per granule
+  extern __shared__ __align__(16) uint8_t smem[];
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gw = p.gw;
+  const int group = warp >> gw;
+  const int tb = lane | ((warp & ((1 << gw) - 1)) << 5);
+  const int gpc = (blockDim.x >> 5) >> gw;
+  const int tbits = 5 + gw;
+
+  const int64_t gid = (int64_t)blockIdx.x * gpc + group;
+  if (gid >= n_groups) return;  // idle group (whole warps: barriers stay consistent)
+
+  uint32_t ld_off = 0, st_off = 0, swx = 0, srx = 0;
+#pragma unroll
+  for (int b = 0; b < LL_MAX_TBITS; ++b) {
+    if (b < tbits && ((tb >> b) & 1)) {
+      ld_off += p.ld_thr[b];
+      st_off += p.st_thr[b];
+      swx ^= p.sw_thr[b];
+      srx ^= p.sr_thr[b];
+    }
+  }
+  const uint8_t* sthr = src + ld_off - rg.src_shift;
+  uint8_t* dthr = dst + st_off - rg.dst_shift;
+  const int n_bits = p.tile.n_bits;
+  const int n_tab = p.tile.n_tab;
+  const int64_t rmask = (int64_t(1) << n_bits) - 1;
+  auto tile_off = [&](int64_t t, int64_t& so, int64_t& dof) {
+    const int64_t inst = t >> n_bits;
+    const int64_t r = t & rmask;
+    so = inst * p.tile.batch_stride_src;
+    dof = inst * p.tile.batch_stride_dst;
+#pragma unroll
+    for (int k = 0; k < LL_MAX_TAB; ++k) {
+      if (k < n_tab) {
+        const TileTab& e = p.tile.tab[k][(int)((r >> (k * LL_TAB_BITS)) & ((1 << LL_TAB_BITS) - 1))];
+        so += e.src;
+        dof += e.dst;
+      }
+    }
+  };
+
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem) + group * 2 * p.tile_bytes;
+  uint32_t buf = 0;
+  const int ga = p.gsel_a, gb = p.gsel_b;
+  const int64_t n_tiles = rg.t1;
+
+  uint32_t R[NW];
+  int64_t so, dof;
+  int64_t t = rg.t0 + gid;
+  if (PIPE && t < n_tiles) {
+    tile_off(t, so, dof);
+    load_tile<NV>(R, sthr + so, p.ld_vec);
+  }
+  for (; t < n_tiles; t += n_groups) {
+    if (!PIPE) tile_off(t, so, dof);
+    if (!PIPE) load_tile<NV>(R, sthr + so, p.ld_vec);
+    const int64_t dcur = dof;
+    for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
+    sts_dispatch<NW, GW, PAD>(ga, gb, R, sbase + buf, swx, p.sw_gran);
+    if (PIPE) {
+      const int64_t tn = t + n_groups;
+      if (tn < n_tiles) {
+        tile_off(tn, so, dof);
+        load_tile<NV>(R, sthr + so, p.ld_vec);
+      }
+    }
+    group_sync(gw, group);
+    uint32_t Q[NW];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const uint32_t o = srx ^ p.sr_gran[j];
+      lds<G>(sbase + buf + (PAD ? pad_off(o) : o), &Q[j * GW]);
+    }
+    uint8_t* dp = dthr + dcur;
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+      stg_stream(dp + p.st_vec[u], make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
+    buf ^= p.tile_bytes;
+  }
+}
+
+template <int W, int NV, int G, bool PIPE, bool PAD>
+static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, int max_ctas,
+                                 cudaStream_t st, const TileRange& rg) {
+  auto k = convert_smem_kernel<W, NV, G, PIPE, PAD>;
+  const int threads = 256;
+  const int gpc = (threads / 32) >> p.gw;
+  const size_t smem = (size_t)gpc * 2 * p.tile_bytes;  // tile_bytes includes any padding
+  static int occ_cache = -1;
+  static size_t occ_smem = 0;
+  static int occ_carve = -2;
+  if (occ_cache < 0 || occ_smem != smem || occ_carve != knobs().carveout) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, knobs().carveout);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
+    occ_smem = smem;
+    occ_carve = knobs().carveout;
+  }
+  if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
+  const int64_t n_tiles = rg.t1 - rg.t0;
+  if (n_tiles <= 0) return cudaSuccess;
+  // tile groups: n_tiles / tpg (the hardware block scheduler balances the
+  // tail), or the resident capacity when tpg = 0 (persistent)
+  const int tpg = knobs().tpg;
+  int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)occ_cache * num_sms() * gpc;
+  if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
+  groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
+  const int64_t grid = (groups + gpc - 1) / gpc;
+  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups, rg);
+  return cudaGetLastError();
+}
+
+template <int W, int NV, int G>
+static cudaError_t launch_smem_t(const SmemPlan& p, const void* src, void* dst, int max_ctas,
+                                 cudaStream_t st, const TileRange& rg) {
+  if (p.pad) return launch_smem_p<W, NV, G, true, true>(p, src, dst, max_ctas, st, rg);
+  if (knobs().pipe) return launch_smem_p<W, NV, G, true, false>(p, src, dst, max_ctas, st, rg);
+  return launch_smem_p<W, NV, G, false, false>(p, src, dst, max_ctas, st, rg);
+}
+
+template <int W>
+static cudaError_t launch_smem_w(const SmemPlan& p, int nv, int g, const void* src, void* dst,
+                                 int max_ctas, cudaStream_t st, const TileRange& rg) {
+#define LL_CASE(NV_, G_) \
+  if (nv == NV_ && g == G_) return launch_smem_t<W, NV_, G_>(p, src, dst, max_ctas, st, rg);
+  LL_CASE(1, 4) LL_CASE(1, 8) LL_CASE(1, 16)
+  LL_CASE(2, 4) LL_CASE(2, 8) LL_CASE(2, 16)
+  LL_CASE(4, 4) LL_CASE(4, 8) LL_CASE(4, 16)
+  LL_CASE(8, 4) LL_CASE(8, 8) LL_CASE(8, 16)
+#undef LL_CASE
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_convert_smem(const SmemPlan& p, int w, int nv, int g, const void* src, void* dst,
+                                int max_ctas, cudaStream_t st, const TileRange& rg) {
+  switch (w) {
+    case 1: return launch_smem_w<1>(p, nv, g, src, dst, max_ctas, st, rg);
+    case 2: return launch_smem_w<2>(p, nv, g, src, dst, max_ctas, st, rg);
+    case 4: return launch_smem_w<4>(p, nv, g, src, dst, max_ctas, st, rg);
+    case 8: return launch_smem_w<8>(p, nv, g, src, dst, max_ctas, st, rg);
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace ll
