@@ -104,6 +104,30 @@ ll_status ll_invert(ll_layout l, ll_layout* out);
  * for a shared label a's bits are low, b's high. */
 ll_status ll_product(ll_layout a, ll_layout b, ll_layout* out);
 
+/* Shape-operation transfer functions (Appendix theorem):
+ * for an input layout, the output layout for which the shape operation moves
+ * no data between hardware indices (every hardware index keeps its value).
+ *   ll_transpose   tt.trans: out dim i of the result = out dim perm[i] of l
+ *   ll_reshape     tt.reshape: new row-major dims, same element count (flat
+ *                  columns unchanged)
+ *   ll_expand_dims tt.expand_dims: insert a size-1 dim `name` at `axis`
+ *   ll_broadcast   tt.broadcast: size-1 dim `axis` grows to 2^bits; zero
+ *                  columns (copies, lowest first) index the new dim, extra
+ *                  register bits are added if there are too few copies
+ *   ll_join        tt.join: new fastest dim `name` of size 2 held by a new
+ *                  register bit 0 (the two values sit in adjacent registers)
+ *   ll_split       tt.split: inverse of join (the last dim, size 2, must be
+ *                  held by a single register bit)
+ * Errors: LL_ERR_ARG (bad permutation / axis / name), LL_ERR_SHAPE (size
+ * mismatch), LL_ERR_UNSUPPORTED (split of a dim not held in registers). */
+ll_status ll_transpose(ll_layout l, const int* perm, ll_layout* out);
+ll_status ll_reshape(ll_layout l, int n_out, const char* const* out_names, const int* out_bits,
+                     ll_layout* out);
+ll_status ll_expand_dims(ll_layout l, int axis, const char* name, ll_layout* out);
+ll_status ll_broadcast(ll_layout l, int axis, int bits, ll_layout* out);
+ll_status ll_join(ll_layout l, const char* name, ll_layout* out);
+ll_status ll_split(ll_layout l, ll_layout* out);
+
 /* Apply to one point ("w = Av"): in_coords[n_in] -> out_coords[n_out].
  * LL_ERR_RANGE if a coordinate does not fit its dim. */
 ll_status ll_apply(ll_layout l, const int64_t* in_coords, int64_t* out_coords);

@@ -58,12 +58,21 @@ _lib.ll_gather_describe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_char_p, ctypes.c_size_t,
                                     ctypes.POINTER(ctypes.c_size_t)]
 _lib.ll_tune.argtypes = [ctypes.c_char_p, ctypes.c_int]
+_VP = ctypes.c_void_p
+_lib.ll_transpose.argtypes = [_VP, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_VP)]
+_lib.ll_reshape.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_VP)]
+_lib.ll_expand_dims.argtypes = [_VP, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_VP)]
+_lib.ll_broadcast.argtypes = [_VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_VP)]
+_lib.ll_join.argtypes = [_VP, ctypes.c_char_p, ctypes.POINTER(_VP)]
+_lib.ll_split.argtypes = [_VP, ctypes.POINTER(_VP)]
 _lib.ll_convert_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_void_p, ctypes.c_void_p]
 _lib.ll_shard_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
-for _f in ("ll_convert_shard", "ll_shard_describe", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
+for _f in ("ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+           "ll_convert_shard", "ll_shard_describe", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
            "ll_gather_describe"):
@@ -207,6 +216,48 @@ def invert(layout):
 def product(a, b):
     h = ctypes.c_void_p()
     _check(_lib.ll_product(a.handle, b.handle, ctypes.byref(h)))
+    return _wrap(h)
+
+
+def transpose(layout, perm):
+    """ll_transpose: tt.trans transfer function."""
+    h = ctypes.c_void_p()
+    p = (ctypes.c_int * max(1, len(perm)))(*[int(x) for x in perm])
+    _check(_lib.ll_transpose(layout.handle, p, ctypes.byref(h)))
+    return _wrap(h)
+
+
+def reshape(layout, out_dims):
+    """ll_reshape: tt.reshape transfer function; out_dims = [(name, bits)]."""
+    h = ctypes.c_void_p()
+    n = len(out_dims)
+    names = (ctypes.c_char_p * max(1, n))(*[str(a).encode() for a, _ in out_dims])
+    bits = (ctypes.c_int * max(1, n))(*[int(b) for _, b in out_dims])
+    _check(_lib.ll_reshape(layout.handle, n, names, bits, ctypes.byref(h)))
+    return _wrap(h)
+
+
+def expand_dims(layout, axis, name):
+    h = ctypes.c_void_p()
+    _check(_lib.ll_expand_dims(layout.handle, int(axis), name.encode(), ctypes.byref(h)))
+    return _wrap(h)
+
+
+def broadcast(layout, axis, bits):
+    h = ctypes.c_void_p()
+    _check(_lib.ll_broadcast(layout.handle, int(axis), int(bits), ctypes.byref(h)))
+    return _wrap(h)
+
+
+def join(layout, name):
+    h = ctypes.c_void_p()
+    _check(_lib.ll_join(layout.handle, name.encode(), ctypes.byref(h)))
+    return _wrap(h)
+
+
+def split(layout):
+    h = ctypes.c_void_p()
+    _check(_lib.ll_split(layout.handle, ctypes.byref(h)))
     return _wrap(h)
 
 

@@ -199,6 +199,70 @@ ll_status ll_product(ll_layout a, ll_layout b, ll_layout* out) {
   });
 }
 
+ll_status ll_transpose(ll_layout l, const int* perm, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_transpose");
+    if (!out || (!perm && !l->L.out.empty())) return fail(LL_ERR_ARG, "ll_transpose: NULL argument");
+    std::vector<int> p(perm, perm + l->L.out.size());
+    *out = wrap(ll::shape_transpose(l->L, p));
+    return LL_OK;
+  });
+}
+
+ll_status ll_reshape(ll_layout l, int n_out, const char* const* out_names, const int* out_bits,
+                     ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_reshape");
+    if (!out || n_out < 0 || n_out > 16 || (n_out && (!out_names || !out_bits)))
+      return fail(LL_ERR_ARG, "ll_reshape: bad arguments");
+    std::vector<ll::Dim> d;
+    std::set<std::string> seen;
+    for (int i = 0; i < n_out; ++i) {
+      if (!out_names[i] || !seen.insert(out_names[i]).second)
+        return fail(LL_ERR_ARG, "ll_reshape: NULL or duplicate dim name");
+      d.push_back({out_names[i], out_bits[i]});
+    }
+    *out = wrap(ll::shape_reshape(l->L, d));
+    return LL_OK;
+  });
+}
+
+ll_status ll_expand_dims(ll_layout l, int axis, const char* name, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_expand_dims");
+    if (!out || !name) return fail(LL_ERR_ARG, "ll_expand_dims: NULL argument");
+    *out = wrap(ll::shape_expand_dims(l->L, axis, name));
+    return LL_OK;
+  });
+}
+
+ll_status ll_broadcast(ll_layout l, int axis, int bits, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_broadcast");
+    if (!out) return fail(LL_ERR_ARG, "ll_broadcast: NULL argument");
+    *out = wrap(ll::shape_broadcast(l->L, axis, bits));
+    return LL_OK;
+  });
+}
+
+ll_status ll_join(ll_layout l, const char* name, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_join");
+    if (!out || !name) return fail(LL_ERR_ARG, "ll_join: NULL argument");
+    *out = wrap(ll::shape_join(l->L, name));
+    return LL_OK;
+  });
+}
+
+ll_status ll_split(ll_layout l, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_split");
+    if (!out) return fail(LL_ERR_ARG, "ll_split: NULL argument");
+    *out = wrap(ll::shape_split(l->L));
+    return LL_OK;
+  });
+}
+
 ll_status ll_apply(ll_layout l, const int64_t* in_coords, int64_t* out_coords) {
   return guarded([&]() -> ll_status {
     check_layout(l, "ll_apply");

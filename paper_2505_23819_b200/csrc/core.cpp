@@ -220,3 +220,140 @@ Layout product(const Layout& a, const Layout& b) {
 }
 
 }  // namespace ll
+
+namespace ll {
+
+// tt.trans: permute the output dims; every column keeps its coordinates.
+Layout shape_transpose(const Layout& l, const std::vector<int>& perm) {
+  const int r = (int)l.out.size();
+  if ((int)perm.size() != r) throw Error(LL_ERR_ARG, "transpose: permutation size != rank");
+  std::vector<int> seen(r, 0);
+  for (int p : perm) {
+    if (p < 0 || p >= r || seen[p]++) throw Error(LL_ERR_ARG, "transpose: not a permutation");
+  }
+  Layout o;
+  o.in = l.in;
+  for (int i = 0; i < r; ++i) o.out.push_back(l.out[perm[i]]);
+  for (u64 c : l.cols) {
+    auto x = l.unflatten(c);
+    std::vector<int64_t> y(r);
+    for (int i = 0; i < r; ++i) y[i] = x[perm[i]];
+    o.cols.push_back(o.flatten(y));
+  }
+  return o;
+}
+
+// tt.reshape: row-major flattening is preserved, so the flat columns
+// are unchanged; only the split of the flat index into dims changes.
+Layout shape_reshape(const Layout& l, const std::vector<Dim>& new_out) {
+  int t = 0;
+  for (auto& d : new_out) {
+    if (d.bits < 0) throw Error(LL_ERR_ARG, "reshape: negative dim");
+    t += d.bits;
+  }
+  if (t != l.out_bits()) throw Error(LL_ERR_SHAPE, "reshape: element count changes");
+  Layout o;
+  o.in = l.in;
+  o.out = new_out;
+  o.cols = l.cols;
+  return o;
+}
+
+// tt.expand_dims: a new size-1 dim at position `axis`.
+Layout shape_expand_dims(const Layout& l, int axis, const std::string& name) {
+  if (axis < 0 || axis > (int)l.out.size()) throw Error(LL_ERR_ARG, "expand_dims: axis out of range");
+  if (l.out_index(name) >= 0) throw Error(LL_ERR_ARG, "expand_dims: duplicate dim name");
+  Layout o;
+  o.in = l.in;
+  o.out = l.out;
+  o.out.insert(o.out.begin() + axis, Dim{name, 0});
+  o.cols = l.cols;  // a 0-bit dim adds no flat bits
+  return o;
+}
+
+// tt.broadcast: a size-1 dim grows to 2^bits.  Hardware
+// indices that held copies (zero columns, lowest first) now index the new
+// dim; if there are fewer copies than new bits, registers are added.
+Layout shape_broadcast(const Layout& l, int axis, int bits) {
+  if (axis < 0 || axis >= (int)l.out.size()) throw Error(LL_ERR_ARG, "broadcast: axis out of range");
+  if (l.out[axis].bits != 0) throw Error(LL_ERR_SHAPE, "broadcast: the dim must have size 1");
+  if (bits < 0 || l.out_bits() + bits > 62) throw Error(LL_ERR_ARG, "broadcast: bad size");
+  Layout o;
+  o.in = l.in;
+  o.out = l.out;
+  o.out[axis].bits = bits;
+  int used = 0;
+  for (u64 c : l.cols) {
+    auto x = l.unflatten(c);
+    if (c == 0 && used < bits) x[axis] = int64_t(1) << used++;
+    o.cols.push_back(o.flatten(x));
+  }
+  // remaining new bits: extra register bits (appended at the top of "reg")
+  if (used < bits) {
+    int roff = o.in_offset("reg");
+    int rbits = o.in_size("reg");
+    if (roff < 0) {
+      o.in.insert(o.in.begin(), Dim{"reg", 0});
+      roff = 0;
+      rbits = 0;
+    }
+    std::vector<u64> add;
+    for (; used < bits; ++used) {
+      std::vector<int64_t> x(o.out.size(), 0);
+      x[axis] = int64_t(1) << used;
+      add.push_back(o.flatten(x));
+    }
+    o.cols.insert(o.cols.begin() + roff + rbits, add.begin(), add.end());
+    for (auto& d : o.in)
+      if (d.name == "reg") d.bits += (int)add.size();
+  }
+  return o;
+}
+
+// tt.join: two tensors of the same layout become a new fastest dim of
+// size 2, the two values of a hardware index sitting in adjacent registers:
+// a new register bit 0 maps to the new dim; existing register bits shift up.
+Layout shape_join(const Layout& l, const std::string& name) {
+  if (l.out_index(name) >= 0) throw Error(LL_ERR_ARG, "join: duplicate dim name");
+  Layout o;
+  o.in = l.in;
+  o.out = l.out;
+  o.out.push_back(Dim{name, 1});
+  int roff = o.in_offset("reg");
+  if (roff < 0) {
+    o.in.insert(o.in.begin(), Dim{"reg", 0});
+    roff = 0;
+  }
+  for (u64 c : l.cols) o.cols.push_back(c << 1);  // the new dim is the lowest flat bit
+  o.cols.insert(o.cols.begin() + roff, u64(1));
+  for (auto& d : o.in)
+    if (d.name == "reg") d.bits += 1;
+  return o;
+}
+
+// tt.split: inverse of join -- the last dim (size 2) must be held by
+// exactly one register bit, which is removed together with the dim.
+Layout shape_split(const Layout& l) {
+  if (l.out.empty() || l.out.back().bits != 1) throw Error(LL_ERR_SHAPE, "split: the last dim must have size 2");
+  const int roff = l.in_offset("reg");
+  const int rbits = l.in_size("reg");
+  int hold = -1;
+  for (int k = 0; k < (int)l.cols.size(); ++k) {
+    if (l.cols[k] & 1) {
+      if (hold >= 0 || l.cols[k] != 1 || roff < 0 || k < roff || k >= roff + rbits)
+        throw Error(LL_ERR_UNSUPPORTED, "split: the size-2 dim is not held by a single register bit");
+      hold = k;
+    }
+  }
+  if (hold < 0) throw Error(LL_ERR_UNSUPPORTED, "split: the size-2 dim is not held by any register");
+  Layout o;
+  o.in = l.in;
+  o.out.assign(l.out.begin(), l.out.end() - 1);
+  for (int k = 0; k < (int)l.cols.size(); ++k)
+    if (k != hold) o.cols.push_back(l.cols[k] >> 1);
+  for (auto& d : o.in)
+    if (d.name == "reg") d.bits -= 1;
+  return o;
+}
+
+}  // namespace ll

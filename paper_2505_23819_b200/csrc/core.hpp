@@ -101,3 +101,15 @@ Layout right_inverse(const Layout& l);
 Layout product(const Layout& a, const Layout& b);
 
 }  // namespace ll
+
+namespace ll {
+// Shape-operation transfer functions on layouts (Appendix theorem
+// P:1057-1064): for a distributed input layout, the output layout for which
+// the shape operation moves no data between hardware indices.
+Layout shape_transpose(const Layout& l, const std::vector<int>& perm);
+Layout shape_reshape(const Layout& l, const std::vector<Dim>& new_out);
+Layout shape_expand_dims(const Layout& l, int axis, const std::string& name);
+Layout shape_broadcast(const Layout& l, int axis, int bits);
+Layout shape_join(const Layout& l, const std::string& name);
+Layout shape_split(const Layout& l);
+}  // namespace ll
