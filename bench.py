@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5"])
     ap.add_argument("--path", default="auto")
+    ap.add_argument("--upcast", action="store_true",
+                    help="config 5 only: fused mxfp4 dequantisation to bf16 (NEXT #1)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: each rank converts the full workload; strong: rank r converts "
                          "shard r of the top block bits (ll_convert_shard, cfg2/cfg5)")
@@ -313,8 +315,18 @@ def main():
                  torch.empty(n_loc, dtype=values_torch(1, 0, w, "cpu").dtype, device=dev))
                 for s in range(nsets)]
 
+        if args.upcast:
+            # fused mxfp4 -> bf16: 2 bf16 per packed byte, scales [M][K/32]
+            n_sc = n // 16
+            scales = (indices_torch(n_sc, 42, 16, dev) + 120).to(torch.uint8)
+            sets = [(s_, torch.empty(2 * n_loc, dtype=torch.int16, device=dev)) for s_, _ in sets]
+            nbytes = n * w + n_sc + 4 * n * w
+
         def step(i):
             s, d = sets[i % len(sets)]
+            if args.upcast:
+                ll.mxfp4_upcast(s, A, scales, d, B)
+                return
             if args.scaling == "strong" and world > 1:
                 ll.convert_shard(s, A, d, B, 8 * w, world, rank, path=args.path)
             else:

@@ -187,6 +187,24 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
 ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout layout, int axis,
                        int elem_bits, const ll_convert_options* opts, ll_stream stream);
 
+/* Fused mxfp4 dequantisation with the layout conversion (
+ * "Software Emulation" / "Data Shuffling"; OCP MX):
+ *   packed    u8 buffer in layout src_layout over (m, kb): byte (m, kb) holds
+ *             the E2M1 values of k = 2kb (low nibble) and k = 2kb + 1 (high)
+ *   scales    E8M0 bytes, row-major [M][K/32] (K = 2 * 2^kb_bits; one scale
+ *             per 32 consecutive k, i.e. per 16 packed bytes), 0xFF = NaN
+ *   dst_bf16  2 bf16 per byte of dst_layout (the packed image of the bf16
+ *             operand layout, e.g. config 5's destination): bf16 element
+ *             2h + n holds  e2m1(m, 2kb + n) * 2^(scale[m][kb/16] - 127),
+ *             (m, kb) = dst_layout(h); exact (the products are representable
+ *             in bf16, subnormals included), overflow -> +-inf, NaN scale ->
+ *             NaN.
+ * The conversion runs on the smem path (LL_ERR_UNSUPPORTED otherwise); the
+ * decode is fused into its store stage (2 GiB written for config 5). */
+ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_t* scales,
+                          void* dst_bf16, ll_layout dst_layout, const ll_convert_options* opts,
+                          ll_stream stream);
+
 /* Multi-GPU shard: convert only shard `shard` of `n_shards`
  * (a power of two).  The tensor is split along the top log2(n_shards) index
  * bits, which must be block bits shared by both layouts (X maps them

@@ -11,11 +11,11 @@ PyTorch fallback: if the shared library is missing the import fails loudly.
 """
 
 from ._lib import (LLError, Layout, broadcast, compose, convert, convert_host, convert_shard,
-                   expand_dims, join, reshape, shard_describe, split, transpose, gather, gather_describe,
+                   expand_dims, join, mxfp4_upcast, reshape, shard_describe, split, transpose, gather, gather_describe,
                    invert, launch_count, lib_path, plan_describe, product, tune, version, PATHS)
 
 __all__ = ["LLError", "Layout", "broadcast", "compose", "convert", "convert_host", "convert_shard",
-           "expand_dims", "join", "reshape", "split", "transpose",
+           "expand_dims", "join", "mxfp4_upcast", "reshape", "split", "transpose",
            "shard_describe", "gather", "gather_describe",
            "invert", "launch_count", "lib_path", "plan_describe", "product", "tune", "version",
            "PATHS"]

@@ -59,6 +59,7 @@ _lib.ll_gather_describe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                     ctypes.POINTER(ctypes.c_size_t)]
 _lib.ll_tune.argtypes = [ctypes.c_char_p, ctypes.c_int]
 _VP = ctypes.c_void_p
+_lib.ll_mxfp4_upcast.argtypes = [_VP, _VP, _VP, _VP, _VP, _VP, _VP]
 _lib.ll_transpose.argtypes = [_VP, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_VP)]
 _lib.ll_reshape.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
                             ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_VP)]
@@ -71,7 +72,7 @@ _lib.ll_convert_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_voi
                                   ctypes.c_void_p, ctypes.c_void_p]
 _lib.ll_shard_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
-for _f in ("ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+for _f in ("ll_mxfp4_upcast", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
@@ -296,6 +297,14 @@ def convert_shard(src_slice, A, dst_slice, B, elem_bits, n_shards, shard, path="
     _check(_lib.ll_convert_shard(_ptr(src_slice), A.handle, _ptr(dst_slice), B.handle,
                                  int(elem_bits), int(n_shards), int(shard), ctypes.byref(o),
                                  _stream_handle(stream)))
+
+
+def mxfp4_upcast(packed, A, scales, dst_bf16, B, max_ctas=0, stream=None):
+    """ll_mxfp4_upcast: packed E2M1 bytes (layout A) + E8M0 scales [M][K/32]
+    -> bf16, two per byte of B (fused with the conversion)."""
+    o = _opts("auto", 1, max_ctas)
+    _check(_lib.ll_mxfp4_upcast(_ptr(packed), A.handle, _ptr(scales), _ptr(dst_bf16), B.handle,
+                                ctypes.byref(o), _stream_handle(stream)))
 
 
 def shard_describe(A, B, elem_bits, n_shards, shard, path="auto"):

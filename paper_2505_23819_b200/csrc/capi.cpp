@@ -385,6 +385,27 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
   });
 }
 
+ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_t* scales,
+                          void* dst_bf16, ll_layout dst_layout, const ll_convert_options* opts,
+                          ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_mxfp4_upcast");
+    check_layout(dst_layout, "ll_mxfp4_upcast");
+    if (!packed || !scales || !dst_bf16) return fail(LL_ERR_ARG, "ll_mxfp4_upcast: NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(packed) | reinterpret_cast<uintptr_t>(dst_bf16)) & 15)
+      return fail(LL_ERR_ARG, "ll_mxfp4_upcast: buffers must be 16-byte aligned");
+    const int64_t batch = opts && opts->batch > 0 ? opts->batch : 1;
+    if (batch != 1) return fail(LL_ERR_UNSUPPORTED, "ll_mxfp4_upcast: batch must be 1");
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, 1, LL_PATH_AUTO, 1, 1);
+    ll::TileRange rg{0, P->sp.tile.n_tiles, 0, 0};
+    ++g_launches;
+    return cuda_status(ll::launch_mxfp4_upcast(P->sp, P->nv, P->g, packed, dst_bf16, scales,
+                                               opts ? opts->max_ctas : 0,
+                                               reinterpret_cast<cudaStream_t>(stream), rg),
+                       "ll_mxfp4_upcast");
+  });
+}
+
 ll_status ll_convert_shard(const void* src_slice, ll_layout src_layout, void* dst_slice,
                            ll_layout dst_layout, int elem_bits, int n_shards, int shard,
                            const ll_convert_options* opts, ll_stream stream) {

@@ -3,11 +3,25 @@
 
 namespace ll {
 
-template <int W, int NV, int G, bool PIPE, bool PAD>
+// UP: fused mxfp4 dequantisation (NEXT #1; W == 1): every
+// destination byte (two E2M1 values, even k in the low nibble) becomes two
+// bf16 = e2m1 x 2^(E8M0 scale - 127), computed exactly in fp32 (the products
+// are representable; overflow -> inf, scale 0xFF -> NaN) and truncated to bf16.
+__device__ __forceinline__ uint32_t mx_scale_f32(uint32_t x) {
+  return x == 255u ? 0x7FC00000u : (x == 0u ? 0x00400000u : (x << 23));
+}
+__device__ __forceinline__ uint32_t e2m1_f32(uint32_t n) {
+  const uint32_t e = (n >> 1) & 3u, m = n & 1u;
+  const uint32_t b = e ? (((e + 126u) << 23) | (m << 22)) : (m ? 0x3F000000u : 0u);
+  return b | ((n & 8u) << 28);
+}
+
+template <int W, int NV, int G, bool PIPE, bool PAD, bool UP = false>
 __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
-                                                           int64_t n_groups, TileRange rg) {
+                                                           int64_t n_groups, TileRange rg,
+                                                           const uint8_t* __restrict__ scales) {
   constexpr int NW = NV * 4;          // 32-bit words per thread
   constexpr int NG = NV * 16 / G;     // granules per thread
   constexpr int GW = G / 4;           // words per granule
@@ -24,7 +38,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const int64_t gid = (int64_t)blockIdx.x * gpc + group;
   if (gid >= n_groups) return;  // idle group (whole warps: barriers stay consistent)
 
-  uint32_t ld_off = 0, st_off = 0, swx = 0, srx = 0;
+  uint32_t ld_off = 0, st_off = 0, swx = 0, srx = 0, sc_off = 0;
 #pragma unroll
   for (int b = 0; b < LL_MAX_TBITS; ++b) {
     if (b < tbits && ((tb >> b) & 1)) {
@@ -32,6 +46,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       st_off += p.st_thr[b];
       swx ^= p.sw_thr[b];
       srx ^= p.sr_thr[b];
+      if (UP) sc_off += p.sc_thr[b];
     }
   }
   const uint8_t* sthr = src + ld_off - rg.src_shift;
@@ -39,17 +54,20 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const int n_bits = p.tile.n_bits;
   const int n_tab = p.tile.n_tab;
   const int64_t rmask = (int64_t(1) << n_bits) - 1;
+  int64_t sct = 0;  // scale-index contribution of the current tile (UP)
   auto tile_off = [&](int64_t t, int64_t& so, int64_t& dof) {
     const int64_t inst = t >> n_bits;
     const int64_t r = t & rmask;
     so = inst * p.tile.batch_stride_src;
     dof = inst * p.tile.batch_stride_dst;
+    if (UP) sct = 0;
 #pragma unroll
     for (int k = 0; k < LL_MAX_TAB; ++k) {
       if (k < n_tab) {
         const TileTab& e = p.tile.tab[k][(int)((r >> (k * LL_TAB_BITS)) & ((1 << LL_TAB_BITS) - 1))];
         so += e.src;
         dof += e.dst;
+        if (UP) sct += e.sc;
       }
     }
   };
@@ -70,6 +88,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
     if (!PIPE) tile_off(t, so, dof);
     if (!PIPE) load_tile<NV>(R, sthr + so, p.ld_vec);
     const int64_t dcur = dof;
+    const int64_t sct_cur = sct;
     for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
     sts_dispatch<NW, GW, PAD>(ga, gb, R, sbase + buf, swx, p.sw_gran);
     if (PIPE) {
@@ -86,18 +105,42 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       const uint32_t o = srx ^ p.sr_gran[j];
       lds<G>(sbase + buf + (PAD ? pad_off(o) : o), &Q[j * GW]);
     }
-    uint8_t* dp = dthr + dcur;
+    if constexpr (UP) {
+      // fused dequantisation: 16 packed bytes -> 32 bf16 (64 bytes) per vector
+      const int64_t dbyte = (int64_t)st_off - rg.dst_shift + dcur;
+      const int64_t scur = sct_cur + sc_off;
 #pragma unroll
-    for (int u = 0; u < NV; ++u)
-      stg_stream(dp + p.st_vec[u], make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
+      for (int u = 0; u < NV; ++u) {
+        const uint8_t* scp = scales + scur + p.sc_vec[u];
+        uint32_t ow[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t byte = (Q[4 * u + (e >> 2)] >> ((e & 3) * 8)) & 0xFFu;
+          const float sf = __uint_as_float(mx_scale_f32(__ldg(scp + p.sc_e[e])));
+          const uint32_t lo = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte & 15u)), sf));
+          const uint32_t hi = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte >> 4)), sf));
+          ow[e] = (hi & 0xFFFF0000u) | (lo >> 16);
+        }
+        uint8_t* op = dst + 4 * (dbyte + p.st_vec[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          stg_stream(op + 16 * q, make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
+      }
+    } else {
+      uint8_t* dp = dthr + dcur;
+#pragma unroll
+      for (int u = 0; u < NV; ++u)
+        stg_stream(dp + p.st_vec[u], make_uint4(Q[4 * u + 0], Q[4 * u + 1], Q[4 * u + 2], Q[4 * u + 3]));
+    }
     buf ^= p.tile_bytes;
   }
 }
 
-template <int W, int NV, int G, bool PIPE, bool PAD>
+template <int W, int NV, int G, bool PIPE, bool PAD, bool UP = false>
 static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, int max_ctas,
-                                 cudaStream_t st, const TileRange& rg) {
-  auto k = convert_smem_kernel<W, NV, G, PIPE, PAD>;
+                                 cudaStream_t st, const TileRange& rg,
+                                 const uint8_t* scales = nullptr) {
+  auto k = convert_smem_kernel<W, NV, G, PIPE, PAD, UP>;
   const int threads = 256;
   const int gpc = (threads / 32) >> p.gw;
   const size_t smem = (size_t)gpc * 2 * p.tile_bytes;  // tile_bytes includes any padding
@@ -122,7 +165,8 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
   const int64_t grid = (groups + gpc - 1) / gpc;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups, rg);
+  k<<<(unsigned)grid, threads, smem, st>>>(p, (const uint8_t*)src, (uint8_t*)dst, groups, rg,
+                                           scales);
   return cudaGetLastError();
 }
 
@@ -155,6 +199,18 @@ cudaError_t launch_convert_smem(const SmemPlan& p, int w, int nv, int g, const v
     case 4: return launch_smem_w<4>(p, nv, g, src, dst, max_ctas, st, rg);
     case 8: return launch_smem_w<8>(p, nv, g, src, dst, max_ctas, st, rg);
   }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_mxfp4_upcast(const SmemPlan& p, int nv, int g, const void* src, void* dst,
+                                const uint8_t* scales, int max_ctas, cudaStream_t st,
+                                const TileRange& rg) {
+#define LL_UCASE(NV_, G_) \
+  if (nv == NV_ && g == G_)  \
+    return launch_smem_p<1, NV_, G_, true, false, true>(p, src, dst, max_ctas, st, rg, scales);
+  LL_UCASE(1, 4) LL_UCASE(1, 8) LL_UCASE(1, 16) LL_UCASE(2, 4) LL_UCASE(2, 8) LL_UCASE(2, 16)
+  LL_UCASE(4, 4) LL_UCASE(4, 8) LL_UCASE(4, 16) LL_UCASE(8, 4) LL_UCASE(8, 8) LL_UCASE(8, 16)
+#undef LL_UCASE
   return cudaErrorNotSupported;
 }
 

@@ -18,6 +18,9 @@ cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src,
                                    int max_ctas, cudaStream_t st);
 cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* src,
                           const int32_t* idx, void* out, int* err, int max_ctas, cudaStream_t st);
+cudaError_t launch_mxfp4_upcast(const SmemPlan& p, int nv, int g, const void* src, void* dst,
+                                const uint8_t* scales, int max_ctas, cudaStream_t st,
+                                const TileRange& rg);
 int device_sm_count();
 int set_knob(const char* name, int value);
 

@@ -29,6 +29,7 @@ namespace ll {
 #define LL_MAX_TAB 3
 struct TileTab {
   int64_t src, dst;
+  int64_t sc;   // mxfp4 upcast: scale-index contribution (0 otherwise)
 };
 struct TileMap {
   int64_t n_tiles;                               // tiles incl. batch
@@ -63,6 +64,12 @@ struct SmemPlan {
   uint32_t sr_thr[LL_MAX_TBITS];  // read side
   uint32_t sw_gran[LL_MAX_GRAN];  // smem byte offset (xor) of write granule j
   uint32_t sr_gran[LL_MAX_GRAN];  // read granule j
+  // fused mxfp4 dequantisation (NEXT #1): scale index (row-major [M][K/32])
+  // contributions of the destination bits, split like the offsets above
+  int32_t upcast;
+  uint32_t sc_thr[LL_MAX_TBITS];
+  uint32_t sc_vec[LL_MAX_VEC];
+  uint32_t sc_e[16];              // byte e of a 16-byte destination vector
 };
 
 // Warp-shuffle conversion plan (LL_PATH_SHUFFLE): warp-local tiles exchanged

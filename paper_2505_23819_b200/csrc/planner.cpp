@@ -209,6 +209,16 @@ u64 linop_apply_index(const std::array<int, 3>& op, u64 k) {
   return k;
 }
 
+// mxfp4 upcast: scale-index contribution of destination (byte-layout) index
+// bit k, for scales stored row-major [M][K/32] = [M][KB/16]
+int64_t scale_contrib(const ConvertPlan& P, int k) {
+  const u64 c = P.dst_cols[k];
+  if (!c) return 0;
+  const int pos = ctz64(c);                 // flat (m, kb) bit; kb is the fastest dim
+  if (pos >= P.kb_bits) return P.scale_row << (pos - P.kb_bits);   // m bit
+  return pos >= 4 ? (int64_t(1) << (pos - 4)) : 0;                 // kb bit (32 fp4 = 16 bytes per scale)
+}
+
 // Try to build the shared-memory tile plan; returns false if X is not a bit
 // permutation or the tile does not fit.
 bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ostringstream& js,
@@ -431,6 +441,24 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     sp.sw_gran[j] = wo;
     sp.sr_gran[j] = ro;
   }
+  if (P.op == 1) {
+    // mxfp4 upcast: the scale of destination byte (m, kb) is scales[m][kb >> 4]
+    sp.upcast = 1;
+    for (int b = 0; b < 5; ++b) sp.sc_thr[b] = (uint32_t)scale_contrib(P, st_lane[b]);
+    for (int b = 0; b < g; ++b) sp.sc_thr[5 + b] = (uint32_t)scale_contrib(P, st_warp[b]);
+    for (int u = 0; u < nvec; ++u) {
+      int64_t c = 0;
+      for (int q = 0; q < r - vb; ++q)
+        if ((u >> q) & 1) c += scale_contrib(P, st_reg[vb + q]);
+      sp.sc_vec[u] = (uint32_t)c;
+    }
+    for (int e = 0; e < (1 << vb); ++e) {
+      int64_t c = 0;
+      for (int q = 0; q < vb; ++q)
+        if ((e >> q) & 1) c += scale_contrib(P, st_reg[q]);
+      sp.sc_e[e] = (uint32_t)c;
+    }
+  }
   // ---- tile map: outer dst bits in the planner's tile order.  Order 2
   // (default) interleaves "next lowest destination bit" and "next lowest
   // source bit", so the tiles in flight at the same time form a 2-D block
@@ -465,16 +493,18 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
   for (int k = 0; k < tm.n_tab; ++k) {
     for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
-      int64_t so = 0, dof = 0;
+      int64_t so = 0, dof = 0, sc = 0;
       for (int q = 0; q < LL_TAB_BITS; ++q) {
         const int bit = k * LL_TAB_BITS + q;
         if (((v >> q) & 1) && bit < tm.n_bits) {
           if (sigma[torder[bit]] >= 0) so += int64_t(w) << sigma[torder[bit]];
           dof += int64_t(w) << torder[bit];
+          if (P.op == 1) sc += scale_contrib(P, torder[bit]);
         }
       }
       tm.tab[k][v].src = so;
       tm.tab[k][v].dst = dof;
+      tm.tab[k][v].sc = sc;
     }
   }
   tm.batch_stride_src = int64_t(w) << P.nA;
@@ -902,10 +932,21 @@ bool plan_async(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& j
 }
 
 std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B, int w,
-                                                int path_req, int64_t batch) {
+                                                int path_req, int64_t batch, int op) {
   if (!A.same_tensor(B)) throw Error(LL_ERR_SHAPE, "convert: source and destination layouts map to different tensors");
   if (!A.surjective()) throw Error(LL_ERR_NOT_SURJECTIVE, "convert: the source layout is not surjective");
   auto P = std::make_shared<ConvertPlan>();
+  P->op = op;
+  if (op == 1) {
+    if (w != 1 || B.out.size() != 2 || B.out[1].bits < 4)
+      throw Error(LL_ERR_ARG, "mxfp4 upcast: byte layouts over (m, kb) with >= 16 bytes per row");
+    if (path_req != LL_PATH_AUTO && path_req != LL_PATH_SMEM)
+      throw Error(LL_ERR_UNSUPPORTED, "mxfp4 upcast: only the smem path");
+    P->kb_bits = B.out[1].bits;
+    P->scale_row = int64_t(1) << (B.out[1].bits - 4);
+    P->dst_cols = B.cols;
+    path_req = LL_PATH_SMEM;
+  }
   P->w = w;
   P->nA = A.in_bits();
   P->nB = B.in_bits();
@@ -947,6 +988,8 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
       throw Error(LL_ERR_UNSUPPORTED, "smem_async path requested but the quotient is not a tileable bit permutation");
     }
   }
+  if (op == 1 && path != LL_PATH_SMEM)
+    throw Error(LL_ERR_UNSUPPORTED, "mxfp4 upcast: the layouts are not a tileable bit permutation");
   if (path == LL_PATH_GENERIC) fill_generic(*P, X);
   P->path = path;
   static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle",
@@ -973,14 +1016,14 @@ std::map<Key, std::shared_ptr<const GatherPlanHost>> g_gcache;
 }  // namespace
 
 std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
-                                                    int path_req, int64_t batch) {
-  Key k{A.hash(), B.hash(), w, path_req, batch, planner_knob_version()};
+                                                    int path_req, int64_t batch, int op) {
+  Key k{A.hash(), B.hash(), w, path_req + 1000 * op, batch, planner_knob_version()};
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_cache.find(k);
     if (it != g_cache.end()) return it->second;
   }
-  auto P = build_convert_plan(A, B, w, path_req, batch);
+  auto P = build_convert_plan(A, B, w, path_req, batch, op);
   std::lock_guard<std::mutex> lk(g_mu);
   g_cache[k] = P;
   return P;

@@ -34,6 +34,10 @@ struct ConvertPlan {
   int64_t batch = 1;
   bool identity = false;
   bool padded = false;
+  int op = 0;        // 0 = convert, 1 = fused mxfp4 upcast (NEXT #1)
+  int64_t scale_row = 0;  // scales per row (K/32)
+  int kb_bits = 0;        // bits of the packed-byte dim
+  std::vector<u64> dst_cols;
   // smem path
   SmemPlan sp{};
   int nv = 0, g = 0;
@@ -69,7 +73,7 @@ bool set_planner_knob(const std::string& name, int value);
 
 // path_req: ll_path value (AUTO lets the planner choose).  Throws ll::Error.
 std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
-                                                    int path_req, int64_t batch);
+                                                    int path_req, int64_t batch, int op = 0);
 std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
                                                       int path_req, int64_t batch);
 

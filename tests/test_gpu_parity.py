@@ -408,3 +408,24 @@ def test_fp8_transpose_paths(mb, nb):
     for path in ("smem", "smem_padded", "smem_noswizzle"):
         src, dst = run_convert(c, path=path, seed=mb * 31 + nb)
         assert dst.tobytes() == expect_convert(c, src).tobytes(), path
+
+
+# ------------------------------------------------------------- mxfp4 upcast
+
+@pytest.mark.parametrize("mb,kb", [(8, 7), (9, 9)])
+def test_mxfp4_upcast(mb, kb):
+    """NEXT #1: config-5 layouts, E2M1 bytes + E8M0 scales in
+    [120, 134] plus edge scales (0, 1, 254, 255 = NaN), bit-exact bf16."""
+    from oracle import mxfp4
+    c = configs.cfg5(m_bits=mb, kb_bits=kb)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    packed = values_torch(n, 41, 1, "cuda")
+    n_sc = (1 << mb) * (1 << (kb - 4))
+    sc = (indices_torch(n_sc, 42, 16, "cuda") + 120).to(torch.uint8)
+    sc[:4] = torch.tensor([0, 1, 254, 255], dtype=torch.uint8)
+    out = torch.empty(2 * n, dtype=torch.int16, device="cuda")
+    ll.mxfp4_upcast(packed, A, sc, out, B)
+    torch.cuda.synchronize()
+    exp = mxfp4.upcast_np(_np(packed, 1), _olayout(c["A"]), sc.cpu().numpy(), _olayout(c["B"]))
+    assert out.cpu().numpy().view(np.uint16).tobytes() == exp.tobytes()
