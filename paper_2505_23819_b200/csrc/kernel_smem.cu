@@ -113,13 +113,22 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       for (int u = 0; u < NV; ++u) {
         const uint8_t* scp = scales + scur + p.sc_vec[u];
         uint32_t ow[16];
+        uint32_t pk = 0;
+        if (p.sc_nz <= 2) {  // the 4 distinct scales of this vector, packed in a word
+          pk = (uint32_t)__ldg(scp) | ((uint32_t)__ldg(scp + p.sc_c[0]) << 8) |
+               ((uint32_t)__ldg(scp + p.sc_c[1]) << 16) |
+               ((uint32_t)__ldg(scp + p.sc_c[0] + p.sc_c[1]) << 24);
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const uint32_t byte = (Q[4 * u + (e >> 2)] >> ((e & 3) * 8)) & 0xFFu;
-          const float sf = __uint_as_float(mx_scale_f32(__ldg(scp + p.sc_e[e])));
+          const uint32_t sb = p.sc_nz <= 2 ? (pk >> (8 * p.sc_slot[e])) & 0xFFu
+                                           : (uint32_t)__ldg(scp + p.sc_e[e]);
+          const float sf = __uint_as_float(mx_scale_f32(sb));
           const uint32_t lo = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte & 15u)), sf));
           const uint32_t hi = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte >> 4)), sf));
-          ow[e] = (hi & 0xFFFF0000u) | (lo >> 16);
+          // NaN scale -> the canonical bf16 quiet NaN 0x7FC0 for both values
+          ow[e] = sb == 255u ? 0x7FC07FC0u : ((hi & 0xFFFF0000u) | (lo >> 16));
         }
         uint8_t* op = dst + 4 * (dbyte + p.st_vec[u]);
 #pragma unroll

@@ -70,6 +70,9 @@ struct SmemPlan {
   uint32_t sc_thr[LL_MAX_TBITS];
   uint32_t sc_vec[LL_MAX_VEC];
   uint32_t sc_e[16];              // byte e of a 16-byte destination vector
+  int32_t sc_nz;                  // vector bits moving the scale (<= 2: 4-slot fast path)
+  uint32_t sc_c[2];               // their scale-index contributions
+  uint8_t sc_slot[16];            // slot (0..3) of byte e among the 4 loaded scales
 };
 
 // Warp-shuffle conversion plan (LL_PATH_SHUFFLE): warp-local tiles exchanged

@@ -458,6 +458,18 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
         if ((e >> q) & 1) c += scale_contrib(P, st_reg[q]);
       sp.sc_e[e] = (uint32_t)c;
     }
+    // the scale of byte e depends only on the vector bits with a nonzero
+    // contribution: <= 2 such bits -> 4 scale loads per vector + byte select
+    std::vector<int> nzq;
+    for (int q = 0; q < vb; ++q)
+      if (scale_contrib(P, st_reg[q])) nzq.push_back(q);
+    sp.sc_nz = (int)nzq.size();
+    for (size_t i = 0; i < nzq.size() && i < 2; ++i) sp.sc_c[i] = (uint32_t)scale_contrib(P, st_reg[nzq[i]]);
+    for (int e = 0; e < (1 << vb); ++e) {
+      int slot = 0;
+      for (size_t i = 0; i < nzq.size() && i < 2; ++i) slot |= ((e >> nzq[i]) & 1) << i;
+      sp.sc_slot[e] = (uint8_t)slot;
+    }
   }
   // ---- tile map: outer dst bits in the planner's tile order.  Order 2
   // (default) interleaves "next lowest destination bit" and "next lowest
