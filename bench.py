@@ -397,7 +397,14 @@ def main():
             nb = n >> 14
         else:
             At, Bt, nb = A, B, 1
-        scratch = min(n * w, 32 << 20) if nb > 1 else n * w
+        # scratch: 16 MiB per side (the library chunks by instances or shards);
+        # layouts that cannot be chunked need the whole buffer
+        try:
+            ll.shard_describe(At, Bt, 8 * w, 2, 0)
+            shardable = True
+        except ll.LLError:
+            shardable = False
+        scratch = min(n * w, 16 << 20) if (nb > 1 or shardable) else n * w
         ds = torch.empty(scratch, dtype=torch.uint8, device=dev)
         dd = torch.empty(scratch, dtype=torch.uint8, device=dev)
         ll.convert_host(src_h, At, dst_h, Bt, 8 * w, nb, ds, dd, scratch)

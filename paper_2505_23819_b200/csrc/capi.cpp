@@ -493,26 +493,90 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     if (batch < 1) batch = 1;
     const size_t sb = (size_t)w << src_layout->L.in_bits();
     const size_t db = (size_t)w << dst_layout->L.in_bits();
-    const size_t unit = sb > db ? sb : db;
+    size_t unit = sb > db ? sb : db;
+    // a single large instance: chunk it by shards (contiguous slices of both
+    // buffers) when the layouts allow it
+    int n_sh = 1;
+    if (batch == 1 && unit > ((size_t)4 << 20)) {
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
+      int want = 1;
+      while ((unit / want) > ((size_t)4 << 20) && want < (1 << 12)) want *= 2;
+      for (int ns = want; ns > 1; ns /= 2) {
+        try {
+          ll::shard_range(*P, ns, 0);
+          n_sh = ns;
+          break;
+        } catch (const ll::Error&) {
+        }
+      }
+    }
+    if (n_sh > 1) {
+      const size_t ssb = sb / n_sh, sdb = db / n_sh, su = ssb > sdb ? ssb : sdb;
+      if (scratch_bytes < su) return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one chunk");
+      int nslot = (int)std::min<size_t>(4, scratch_bytes / su);
+      cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+      cudaStream_t cs[4];
+      cudaEvent_t done[4];
+      cudaEvent_t start;
+      cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+      cudaEventRecord(start, st);
+      for (int i = 0; i < nslot; ++i) {
+        cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+        cudaStreamWaitEvent(cs[i], start, 0);
+      }
+      ll_status s = LL_OK;
+      for (int k = 0; k < n_sh && s == LL_OK; ++k) {
+        const int slot = k % nslot;
+        cudaStream_t c = cs[slot];
+        char* ds = (char*)dev_src + (size_t)slot * su;
+        char* dd = (char*)dev_dst + (size_t)slot * su;
+        cudaMemcpyAsync(ds, (const char*)src_host + k * ssb, ssb, cudaMemcpyHostToDevice, c);
+        s = ll_convert_shard(ds, src_layout, dd, dst_layout, elem_bits, n_sh, k, nullptr, (ll_stream)c);
+        cudaMemcpyAsync((char*)dst_host + k * sdb, dd, sdb, cudaMemcpyDeviceToHost, c);
+      }
+      for (int i = 0; i < nslot; ++i) {
+        cudaEventRecord(done[i], cs[i]);
+        cudaStreamWaitEvent(st, done[i], 0);
+      }
+      cudaError_t e = cudaStreamSynchronize(st);
+      for (int i = 0; i < nslot; ++i) {
+        cudaEventDestroy(done[i]);
+        cudaStreamDestroy(cs[i]);
+      }
+      cudaEventDestroy(start);
+      if (s != LL_OK) return s;
+      return cuda_status(e, "ll_convert_host");
+    }
     if (scratch_bytes < unit)
       return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one layout instance");
-    // chunk = whole layout instances (batch elements); two halves of the
-    // scratch alternate so that copies of chunk i+1 overlap the kernel of i.
-    int64_t per_chunk = (int64_t)((scratch_bytes / 2) / unit);
+    // chunk = whole layout instances (batch elements), ~4 MiB so that the
+    // pipeline fill / drain is short; up to 4 slots of the scratch rotate over
+    // as many streams: the H2D copy of chunk i+1, the kernel of chunk i and the
+    // D2H copy of chunk i-1 overlap (copy engines run both directions at once).
+    const size_t target = (size_t)4 << 20;
+    int64_t per_chunk = (int64_t)std::max<size_t>(1, target / unit);
+    if ((size_t)per_chunk * unit > scratch_bytes) per_chunk = (int64_t)(scratch_bytes / unit);
     if (per_chunk < 1) per_chunk = 1;
-    const bool dbl = (size_t)per_chunk * unit * 2 <= scratch_bytes;
+    int nslot = (int)std::min<size_t>(4, scratch_bytes / ((size_t)per_chunk * unit));
+    if (nslot < 1) nslot = 1;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    cudaStream_t cs[2];
-    cudaEvent_t done[2];
-    for (int i = 0; i < 2; ++i) {
+    cudaStream_t cs[4];
+    cudaEvent_t done[4];
+    for (int i = 0; i < nslot; ++i) {
       cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
     }
+    // the copies must not start before work already queued on `stream`
+    cudaEvent_t start;
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    cudaEventRecord(start, st);
+    for (int i = 0; i < nslot; ++i) cudaStreamWaitEvent(cs[i], start, 0);
     ll_status s = LL_OK;
     int64_t chunk = 0;
     for (int64_t b0 = 0; b0 < batch && s == LL_OK; b0 += per_chunk, ++chunk) {
       const int64_t nb = std::min<int64_t>(per_chunk, batch - b0);
-      const int slot = dbl ? (int)(chunk & 1) : 0;
+      const int slot = (int)(chunk % nslot);
       cudaStream_t c = cs[slot];
       char* ds = (char*)dev_src + (size_t)slot * per_chunk * sb;
       char* dd = (char*)dev_dst + (size_t)slot * per_chunk * db;
@@ -523,15 +587,16 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
       s = ll_convert_ex(ds, src_layout, dd, dst_layout, elem_bits, &o, (ll_stream)c);
       cudaMemcpyAsync((char*)dst_host + b0 * db, dd, nb * db, cudaMemcpyDeviceToHost, c);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < nslot; ++i) {
       cudaEventRecord(done[i], cs[i]);
       cudaStreamWaitEvent(st, done[i], 0);
     }
     cudaError_t e = cudaStreamSynchronize(st);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < nslot; ++i) {
       cudaEventDestroy(done[i]);
       cudaStreamDestroy(cs[i]);
     }
+    cudaEventDestroy(start);
     if (s != LL_OK) return s;
     return cuda_status(e, "ll_convert_host");
   });

@@ -429,3 +429,18 @@ def test_mxfp4_upcast(mb, kb):
     torch.cuda.synchronize()
     exp = mxfp4.upcast_np(_np(packed, 1), _olayout(c["A"]), sc.cpu().numpy(), _olayout(c["B"]))
     assert out.cpu().numpy().view(np.uint16).tobytes() == exp.tobytes()
+
+
+def test_convert_host_sharded_single_instance():
+    """One large instance (8 MiB) chunked by shards through ll_convert_host."""
+    c = configs.cfg5(m_bits=12, kb_bits=11)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src_h = values_torch(n, 23, 1, "cpu").pin_memory()
+    dst_h = torch.empty_like(src_h).pin_memory()
+    scratch = 4 << 20
+    ds = torch.empty(scratch, dtype=torch.uint8, device="cuda")
+    dd = torch.empty(scratch, dtype=torch.uint8, device="cuda")
+    ll.convert_host(src_h, A, dst_h, B, 8, 1, ds, dd, scratch)
+    exp = expect_convert(c, src_h.numpy())
+    assert dst_h.numpy().tobytes() == exp.tobytes()
