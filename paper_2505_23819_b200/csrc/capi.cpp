@@ -497,10 +497,12 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     // a single large instance: chunk it by shards (contiguous slices of both
     // buffers) when the layouts allow it
     int n_sh = 1;
-    if (batch == 1 && unit > ((size_t)4 << 20)) {
+    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 4)) << 20;
+    const int max_slots = std::max(1, std::min(4, ll::planner_knob("host_slots", 4)));
+    if (batch == 1 && unit > target) {
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
       int want = 1;
-      while ((unit / want) > ((size_t)4 << 20) && want < (1 << 12)) want *= 2;
+      while ((unit / want) > target && want < (1 << 12)) want *= 2;
       for (int ns = want; ns > 1; ns /= 2) {
         try {
           ll::shard_range(*P, ns, 0);
@@ -513,7 +515,7 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     if (n_sh > 1) {
       const size_t ssb = sb / n_sh, sdb = db / n_sh, su = ssb > sdb ? ssb : sdb;
       if (scratch_bytes < su) return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one chunk");
-      int nslot = (int)std::min<size_t>(4, scratch_bytes / su);
+      int nslot = (int)std::min<size_t>(max_slots, scratch_bytes / su);
       cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
       cudaStream_t cs[4];
       cudaEvent_t done[4];
@@ -554,11 +556,10 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     // pipeline fill / drain is short; up to 4 slots of the scratch rotate over
     // as many streams: the H2D copy of chunk i+1, the kernel of chunk i and the
     // D2H copy of chunk i-1 overlap (copy engines run both directions at once).
-    const size_t target = (size_t)4 << 20;
     int64_t per_chunk = (int64_t)std::max<size_t>(1, target / unit);
     if ((size_t)per_chunk * unit > scratch_bytes) per_chunk = (int64_t)(scratch_bytes / unit);
     if (per_chunk < 1) per_chunk = 1;
-    int nslot = (int)std::min<size_t>(4, scratch_bytes / ((size_t)per_chunk * unit));
+    int nslot = (int)std::min<size_t>(max_slots, scratch_bytes / ((size_t)per_chunk * unit));
     if (nslot < 1) nslot = 1;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     cudaStream_t cs[4];

@@ -144,7 +144,8 @@ int planner_knob_version() {
 }
 bool set_planner_knob(const std::string& name, int value) {
   if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule" &&
-      name != "run_bytes" && name != "tile_order")
+      name != "run_bytes" && name != "tile_order" && name != "host_chunk_mb" &&
+      name != "host_slots")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
