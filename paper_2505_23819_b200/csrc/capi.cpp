@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <set>
 #include <string>
@@ -324,6 +325,47 @@ ll_status ll_gather_describe(ll_layout layout, int axis, int elem_bits, int path
 }
 
 namespace {
+// Streams and events of ll_convert_host, created once per device and reused
+// (stream / event creation costs tens of microseconds per call).
+struct HostPipe {
+  static constexpr int kSlots = 4;
+  std::mutex mu;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  cudaEvent_t start, fin[3], ev_h2d[kSlots], ev_comp[kSlots], ev_d2h[kSlots];
+};
+
+HostPipe& host_pipe() {
+  static std::mutex m;
+  static HostPipe* pipes[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) throw ll::Error(LL_ERR_CUDA, "ll_convert_host: bad device");
+  std::lock_guard<std::mutex> lk(m);
+  if (!pipes[dev]) {
+    HostPipe* p = new HostPipe();
+    auto ev = [](cudaEvent_t* e) { cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
+    cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking);
+    ev(&p->start);
+    for (auto& e : p->fin) ev(&e);
+    for (int i = 0; i < HostPipe::kSlots; ++i) {
+      ev(&p->ev_h2d[i]);
+      ev(&p->ev_comp[i]);
+      ev(&p->ev_d2h[i]);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      delete p;
+      throw ll::Error(LL_ERR_CUDA, std::string("ll_convert_host: ") + cudaGetErrorString(e));
+    }
+    pipes[dev] = p;
+  }
+  return *pipes[dev];
+}
+}  // namespace
+
+namespace {
 ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
                       int elem_bits, const ll_convert_options* opts, ll_stream stream,
                       int n_shards, int shard) {
@@ -493,12 +535,12 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     if (batch < 1) batch = 1;
     const size_t sb = (size_t)w << src_layout->L.in_bits();
     const size_t db = (size_t)w << dst_layout->L.in_bits();
-    size_t unit = sb > db ? sb : db;
-    // a single large instance: chunk it by shards (contiguous slices of both
-    // buffers) when the layouts allow it
+    const size_t unit = sb > db ? sb : db;
+    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 8)) << 20;
+    const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 3)));
+    // chunking: whole layout instances (batch elements), or -- for a single
+    // large instance -- shards (contiguous slices of both buffers)
     int n_sh = 1;
-    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 4)) << 20;
-    const int max_slots = std::max(1, std::min(4, ll::planner_knob("host_slots", 4)));
     if (batch == 1 && unit > target) {
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
       int want = 1;
@@ -512,92 +554,87 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
         }
       }
     }
+    int64_t n_chunks, per_chunk = 1;
+    size_t cs_src, cs_dst;  // bytes per chunk (src / dst side)
     if (n_sh > 1) {
-      const size_t ssb = sb / n_sh, sdb = db / n_sh, su = ssb > sdb ? ssb : sdb;
-      if (scratch_bytes < su) return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one chunk");
-      int nslot = (int)std::min<size_t>(max_slots, scratch_bytes / su);
-      cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-      cudaStream_t cs[4];
-      cudaEvent_t done[4];
-      cudaEvent_t start;
-      cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-      cudaEventRecord(start, st);
-      for (int i = 0; i < nslot; ++i) {
-        cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
-        cudaStreamWaitEvent(cs[i], start, 0);
-      }
-      ll_status s = LL_OK;
-      for (int k = 0; k < n_sh && s == LL_OK; ++k) {
-        const int slot = k % nslot;
-        cudaStream_t c = cs[slot];
-        char* ds = (char*)dev_src + (size_t)slot * su;
-        char* dd = (char*)dev_dst + (size_t)slot * su;
-        cudaMemcpyAsync(ds, (const char*)src_host + k * ssb, ssb, cudaMemcpyHostToDevice, c);
-        s = ll_convert_shard(ds, src_layout, dd, dst_layout, elem_bits, n_sh, k, nullptr, (ll_stream)c);
-        cudaMemcpyAsync((char*)dst_host + k * sdb, dd, sdb, cudaMemcpyDeviceToHost, c);
-      }
-      for (int i = 0; i < nslot; ++i) {
-        cudaEventRecord(done[i], cs[i]);
-        cudaStreamWaitEvent(st, done[i], 0);
-      }
-      cudaError_t e = cudaStreamSynchronize(st);
-      for (int i = 0; i < nslot; ++i) {
-        cudaEventDestroy(done[i]);
-        cudaStreamDestroy(cs[i]);
-      }
-      cudaEventDestroy(start);
-      if (s != LL_OK) return s;
-      return cuda_status(e, "ll_convert_host");
+      n_chunks = n_sh;
+      cs_src = sb / n_sh;
+      cs_dst = db / n_sh;
+    } else {
+      if (scratch_bytes < unit)
+        return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one layout instance");
+      per_chunk = (int64_t)std::max<size_t>(1, target / unit);
+      per_chunk = std::min<int64_t>(per_chunk, (int64_t)(scratch_bytes / unit));
+      per_chunk = std::min<int64_t>(per_chunk, batch);
+      n_chunks = (batch + per_chunk - 1) / per_chunk;
+      cs_src = per_chunk * sb;
+      cs_dst = per_chunk * db;
     }
-    if (scratch_bytes < unit)
-      return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one layout instance");
-    // chunk = whole layout instances (batch elements), ~4 MiB so that the
-    // pipeline fill / drain is short; up to 4 slots of the scratch rotate over
-    // as many streams: the H2D copy of chunk i+1, the kernel of chunk i and the
-    // D2H copy of chunk i-1 overlap (copy engines run both directions at once).
-    int64_t per_chunk = (int64_t)std::max<size_t>(1, target / unit);
-    if ((size_t)per_chunk * unit > scratch_bytes) per_chunk = (int64_t)(scratch_bytes / unit);
-    if (per_chunk < 1) per_chunk = 1;
-    int nslot = (int)std::min<size_t>(max_slots, scratch_bytes / ((size_t)per_chunk * unit));
-    if (nslot < 1) nslot = 1;
+    const size_t cs = cs_src > cs_dst ? cs_src : cs_dst;
+    if (scratch_bytes < cs) return fail(LL_ERR_ARG, "ll_convert_host: scratch smaller than one chunk");
+    const int nslot = (int)std::max<size_t>(1, std::min<size_t>(max_slots, scratch_bytes / cs));
+
+    // Three streams: copy-in (H2D), compute, copy-out (D2H).  One stream per
+    // direction keeps each copy engine working on one chunk at a time in
+    // order (copies of one direction on several streams share the link and
+    // finish later); per-slot events hand chunks down the pipeline and guard
+    // slot reuse: H2D(i) waits for the kernel of chunk i-nslot (its source
+    // slot), the kernel of chunk i waits for D2H(i-nslot) (its destination
+    // slot).  The H2D of chunk i+1, the kernel of chunk i and the D2H of
+    // chunk i-1 overlap.
+    HostPipe& hp = host_pipe();
+    std::lock_guard<std::mutex> lk(hp.mu);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    cudaStream_t cs[4];
-    cudaEvent_t done[4];
-    for (int i = 0; i < nslot; ++i) {
-      cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
-    }
-    // the copies must not start before work already queued on `stream`
-    cudaEvent_t start;
-    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-    cudaEventRecord(start, st);
-    for (int i = 0; i < nslot; ++i) cudaStreamWaitEvent(cs[i], start, 0);
+    cudaEventRecord(hp.start, st);
+    cudaStreamWaitEvent(hp.h2d, hp.start, 0);
+    cudaStreamWaitEvent(hp.comp, hp.start, 0);
+    cudaStreamWaitEvent(hp.d2h, hp.start, 0);
     ll_status s = LL_OK;
-    int64_t chunk = 0;
-    for (int64_t b0 = 0; b0 < batch && s == LL_OK; b0 += per_chunk, ++chunk) {
-      const int64_t nb = std::min<int64_t>(per_chunk, batch - b0);
-      const int slot = (int)(chunk % nslot);
-      cudaStream_t c = cs[slot];
-      char* ds = (char*)dev_src + (size_t)slot * per_chunk * sb;
-      char* dd = (char*)dev_dst + (size_t)slot * per_chunk * db;
-      cudaMemcpyAsync(ds, (const char*)src_host + b0 * sb, nb * sb, cudaMemcpyHostToDevice, c);
-      ll_convert_options o{};
-      o.path = LL_PATH_AUTO;
-      o.batch = nb;
-      s = ll_convert_ex(ds, src_layout, dd, dst_layout, elem_bits, &o, (ll_stream)c);
-      cudaMemcpyAsync((char*)dst_host + b0 * db, dd, nb * db, cudaMemcpyDeviceToHost, c);
+    for (int64_t i = 0; i < n_chunks && s == LL_OK; ++i) {
+      const int slot = (int)(i % nslot);
+      char* ds = (char*)dev_src + (size_t)slot * cs;
+      char* dd = (char*)dev_dst + (size_t)slot * cs;
+      size_t in_off, in_len, out_off, out_len;
+      int64_t nb = 1;
+      if (n_sh > 1) {
+        in_off = i * cs_src;
+        in_len = cs_src;
+        out_off = i * cs_dst;
+        out_len = cs_dst;
+      } else {
+        const int64_t b0 = i * per_chunk;
+        nb = std::min<int64_t>(per_chunk, batch - b0);
+        in_off = b0 * sb;
+        in_len = nb * sb;
+        out_off = b0 * db;
+        out_len = nb * db;
+      }
+      if (i >= nslot) cudaStreamWaitEvent(hp.h2d, hp.ev_comp[slot], 0);
+      cudaMemcpyAsync(ds, (const char*)src_host + in_off, in_len, cudaMemcpyHostToDevice, hp.h2d);
+      cudaEventRecord(hp.ev_h2d[slot], hp.h2d);
+      cudaStreamWaitEvent(hp.comp, hp.ev_h2d[slot], 0);
+      if (i >= nslot) cudaStreamWaitEvent(hp.comp, hp.ev_d2h[slot], 0);
+      if (n_sh > 1) {
+        s = ll_convert_shard(ds, src_layout, dd, dst_layout, elem_bits, n_sh, (int)i, nullptr,
+                             (ll_stream)hp.comp);
+      } else {
+        ll_convert_options o{};
+        o.path = LL_PATH_AUTO;
+        o.batch = nb;
+        s = ll_convert_ex(ds, src_layout, dd, dst_layout, elem_bits, &o, (ll_stream)hp.comp);
+      }
+      cudaEventRecord(hp.ev_comp[slot], hp.comp);
+      cudaStreamWaitEvent(hp.d2h, hp.ev_comp[slot], 0);
+      cudaMemcpyAsync((char*)dst_host + out_off, dd, out_len, cudaMemcpyDeviceToHost, hp.d2h);
+      cudaEventRecord(hp.ev_d2h[slot], hp.d2h);
     }
-    for (int i = 0; i < nslot; ++i) {
-      cudaEventRecord(done[i], cs[i]);
-      cudaStreamWaitEvent(st, done[i], 0);
-    }
+    // the caller's stream resumes after the last copy-out (and the other two
+    // streams are drained, so the next call starts from a clean pipeline)
+    cudaEventRecord(hp.fin[0], hp.h2d);
+    cudaEventRecord(hp.fin[1], hp.comp);
+    cudaEventRecord(hp.fin[2], hp.d2h);
+    for (int k = 0; k < 3; ++k) cudaStreamWaitEvent(st, hp.fin[k], 0);
     cudaError_t e = cudaStreamSynchronize(st);
-    for (int i = 0; i < nslot; ++i) {
-      cudaEventDestroy(done[i]);
-      cudaStreamDestroy(cs[i]);
-    }
-    cudaEventDestroy(start);
     if (s != LL_OK) return s;
     return cuda_status(e, "ll_convert_host");
   });

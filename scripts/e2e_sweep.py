@@ -37,7 +37,7 @@ for cfg in ("2", "5"):
     w = c["elem_bytes"]
     src = values_torch(n, 9, w, "cpu").pin_memory()
     dst = torch.empty_like(src).pin_memory()
-    for mb in (2, 4, 8, 16, 32):
+    for mb in (2, 4, 8, 16):
         for slots in (2, 3, 4):
             ll.tune("host_chunk_mb", mb)
             ll.tune("host_slots", slots)
@@ -71,5 +71,22 @@ for name, fn, nbytes in (("h2d", lambda: x.copy_(h, non_blocking=True), 1 << 28)
     r = {"copy": name, "GBps": round(nbytes / ms / 1e6, 1)}
     res.append(r)
     print(json.dumps(r), flush=True)
+# host-side enqueue cost of one conversion launch (no sync inside the loop)
+import time  # noqa: E402
+c = configs.cfg2(batch_bits=0)
+A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+xs = torch.zeros(1 << 14, dtype=torch.int16, device="cuda")
+xd = torch.empty_like(xs)
+for _ in range(100):
+    ll.convert(xs, A, xd, B, 16)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(2000):
+    ll.convert(xs, A, xd, B, 16)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+r = {"host_enqueue_us_per_convert": round((t1 - t0) / 2000 * 1e6, 2)}
+res.append(r)
+print(json.dumps(r), flush=True)
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump(res, open(os.path.join(ROOT, "gpurun_out", "e2e_sweep.json"), "w"), indent=1)
