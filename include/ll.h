@@ -225,9 +225,9 @@ ll_status ll_shard_describe(ll_layout src_layout, ll_layout dst_layout, int elem
 
 /* End-to-end conversion of HOST buffers: src_host/dst_host are host pointers
  * (pinned for full speed); the library pipelines host->device copies, the
- * conversion and device->host copies in chunks (~8 MiB: whole layout
+ * conversion and device->host copies in chunks (~16 MiB: whole layout
  * instances, or shards of a single large instance) over a copy-in, a compute
- * and a copy-out stream of its own, rotating up to 3 slots of the caller's
+ * and a copy-out stream of its own, rotating 2 slots (knob: up to 4) of the caller's
  * device scratch buffers dev_src/dev_dst of scratch_bytes each (>= one
  * chunk).  Ordered after work already queued on `stream`; synchronous:
  * returns when dst_host is complete.  Knobs (ll_tune): "host_chunk_mb",

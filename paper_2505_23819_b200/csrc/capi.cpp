@@ -536,8 +536,8 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     const size_t sb = (size_t)w << src_layout->L.in_bits();
     const size_t db = (size_t)w << dst_layout->L.in_bits();
     const size_t unit = sb > db ? sb : db;
-    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 8)) << 20;
-    const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 3)));
+    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 16)) << 20;
+    const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 2)));
     // chunking: whole layout instances (batch elements), or -- for a single
     // large instance -- shards (contiguous slices of both buffers)
     int n_sh = 1;
