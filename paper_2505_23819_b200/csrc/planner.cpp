@@ -1012,15 +1012,40 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
   return P;
 }
 
+// Exact cache key: the full layouts (dims and columns), not a hash of them,
+// so two different layouts can never share a plan.
+void append_sig(std::vector<u64>& s, const Layout& L) {
+  auto dims = [&](const std::vector<Dim>& ds) {
+    s.push_back(0x5eedull << 32 | ds.size());
+    for (auto& d : ds) {
+      s.push_back(((u64)d.bits << 32) | d.name.size());
+      for (char ch : d.name) s.push_back((unsigned char)ch);
+    }
+  };
+  dims(L.in);
+  dims(L.out);
+  s.insert(s.end(), L.cols.begin(), L.cols.end());
+}
+
 struct Key {
-  u64 a, b;
+  std::vector<u64> sig;
   int w, path;
   int64_t batch;
   int knobs;
   bool operator<(const Key& o) const {
-    return std::tie(a, b, w, path, batch, knobs) < std::tie(o.a, o.b, o.w, o.path, o.batch, o.knobs);
+    return std::tie(w, path, batch, knobs, sig) < std::tie(o.w, o.path, o.batch, o.knobs, o.sig);
   }
 };
+
+Key make_key(const Layout& A, const Layout* B, u64 extra, int w, int path, int64_t batch) {
+  Key k{{}, w, path, batch, planner_knob_version()};
+  k.sig.reserve(160);
+  append_sig(k.sig, A);
+  if (B) append_sig(k.sig, *B);
+  k.sig.push_back(extra);
+  return k;
+}
+constexpr size_t kMaxCached = 4096;
 
 std::mutex g_mu;
 std::map<Key, std::shared_ptr<const ConvertPlan>> g_cache;
@@ -1030,7 +1055,7 @@ std::map<Key, std::shared_ptr<const GatherPlanHost>> g_gcache;
 
 std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
                                                     int path_req, int64_t batch, int op) {
-  Key k{A.hash(), B.hash(), w, path_req + 1000 * op, batch, planner_knob_version()};
+  Key k = make_key(A, &B, 0, w, path_req + 1000 * op, batch);
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_cache.find(k);
@@ -1038,6 +1063,7 @@ std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layou
   }
   auto P = build_convert_plan(A, B, w, path_req, batch, op);
   std::lock_guard<std::mutex> lk(g_mu);
+  if (g_cache.size() >= kMaxCached) g_cache.clear();
   g_cache[k] = P;
   return P;
 }
@@ -1080,7 +1106,7 @@ TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
 // ------------------------------------------------------------------ gather
 std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
                                                       int path_req, int64_t batch) {
-  Key k{L.hash(), (u64)axis, w, path_req, batch, planner_knob_version()};
+  Key k = make_key(L, nullptr, (u64)axis, w, path_req, batch);
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_gcache.find(k);
@@ -1136,6 +1162,7 @@ std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis,
      << "}";
   P->json = js.str();
   std::lock_guard<std::mutex> lk(g_mu);
+  if (g_gcache.size() >= kMaxCached) g_gcache.clear();
   g_gcache[k] = P;
   return P;
 }
