@@ -16,6 +16,17 @@ __device__ __forceinline__ uint32_t e2m1_f32(uint32_t n) {
   return b | ((n & 8u) << 28);
 }
 
+// bf16 bits of the e2m1 magnitudes 0, 0.5, 1, 1.5, 2, 3, 4, 6 (index = the
+// nibble's low 3 bits), split into low-byte and high-byte permute tables
+constexpr uint32_t kE2M1Lo0 = 0xC0800000u, kE2M1Lo1 = 0xC0804000u;
+constexpr uint32_t kE2M1Hi0 = 0x3F3F3F00u, kE2M1Hi1 = 0x40404040u;
+// exact here: both operands are bf16 and the product is a normal number
+__device__ __forceinline__ uint32_t bf16x2_mul(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 template <int W, int NV, int G, bool PIPE, bool PAD, bool UP = false>
 __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
@@ -113,22 +124,47 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       for (int u = 0; u < NV; ++u) {
         const uint8_t* scp = scales + scur + p.sc_vec[u];
         uint32_t ow[16];
+        bool fast = false;
         uint32_t pk = 0;
         if (p.sc_nz <= 2) {  // the 4 distinct scales of this vector, packed in a word
-          pk = (uint32_t)__ldg(scp) | ((uint32_t)__ldg(scp + p.sc_c[0]) << 8) |
-               ((uint32_t)__ldg(scp + p.sc_c[1]) << 16) |
-               ((uint32_t)__ldg(scp + p.sc_c[0] + p.sc_c[1]) << 24);
+          const uint32_t s0 = __ldg(scp), s1 = __ldg(scp + p.sc_c[0]), s2 = __ldg(scp + p.sc_c[1]),
+                         s3 = __ldg(scp + p.sc_c[0] + p.sc_c[1]);
+          pk = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
+          // all four scales in [2, 252]: every product is a normal number
+          fast = (s0 - 2u < 251u) & (s1 - 2u < 251u) & (s2 - 2u < 251u) & (s3 - 2u < 251u);
         }
+        if (fast) {
+          // e2m1 magnitude -> bf16 by byte-permute table lookups, the sign
+          // bits moved into place, then one exact bf16x2 multiply by
+          // (2^(s-127), 2^(s-127)) per destination word
+          const uint32_t plo = (pk << 7) & 0x80808080u, phi = (pk >> 1) & 0x7F7F7F7Fu;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t byte = (Q[4 * u + (e >> 2)] >> ((e & 3) * 8)) & 0xFFu;
-          const uint32_t sb = p.sc_nz <= 2 ? (pk >> (8 * p.sc_slot[e])) & 0xFFu
-                                           : (uint32_t)__ldg(scp + p.sc_e[e]);
-          const float sf = __uint_as_float(mx_scale_f32(sb));
-          const uint32_t lo = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte & 15u)), sf));
-          const uint32_t hi = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte >> 4)), sf));
-          // NaN scale -> the canonical bf16 quiet NaN 0x7FC0 for both values
-          ow[e] = sb == 255u ? 0x7FC07FC0u : ((hi & 0xFFFF0000u) | (lo >> 16));
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t wq = Q[4 * u + j];
+            const uint32_t m = wq & 0x77777777u, mh = m >> 16, x = wq & 0x88888888u;
+            const uint32_t L01 = __byte_perm(kE2M1Lo0, kE2M1Lo1, m), H01 = __byte_perm(kE2M1Hi0, kE2M1Hi1, m);
+            const uint32_t L23 = __byte_perm(kE2M1Lo0, kE2M1Lo1, mh), H23 = __byte_perm(kE2M1Hi0, kE2M1Hi1, mh);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int e = 4 * j + k;
+              const uint32_t mag = __byte_perm(k < 2 ? L01 : L23, k < 2 ? H01 : H23, (k & 1) ? 0x7362 : 0x5140);
+              const uint32_t t = __byte_perm(x, 0u, 0x4440 | k) * 0x01001000u;  // bits 3,7 -> 15,31
+              const uint32_t v = mag | (t & 0x80008000u);
+              ow[e] = bf16x2_mul(v, __byte_perm(plo, phi, p.sc_sel[e]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t byte = (Q[4 * u + (e >> 2)] >> ((e & 3) * 8)) & 0xFFu;
+            const uint32_t sb = p.sc_nz <= 2 ? (pk >> (8 * p.sc_slot[e])) & 0xFFu
+                                             : (uint32_t)__ldg(scp + p.sc_e[e]);
+            const float sf = __uint_as_float(mx_scale_f32(sb));
+            const uint32_t lo = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte & 15u)), sf));
+            const uint32_t hi = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte >> 4)), sf));
+            // NaN scale -> the canonical bf16 quiet NaN 0x7FC0 for both values
+            ow[e] = sb == 255u ? 0x7FC07FC0u : ((hi & 0xFFFF0000u) | (lo >> 16));
+          }
         }
         uint8_t* op = dst + 4 * (dbyte + p.st_vec[u]);
 #pragma unroll

@@ -73,6 +73,7 @@ struct SmemPlan {
   int32_t sc_nz;                  // vector bits moving the scale (<= 2: 4-slot fast path)
   uint32_t sc_c[2];               // their scale-index contributions
   uint8_t sc_slot[16];            // slot (0..3) of byte e among the 4 loaded scales
+  uint32_t sc_sel[16];            // prmt selector: bf16x2 factor of byte e's slot
 };
 
 // Warp-shuffle conversion plan (LL_PATH_SHUFFLE): warp-local tiles exchanged

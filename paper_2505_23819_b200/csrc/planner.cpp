@@ -470,6 +470,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       int slot = 0;
       for (size_t i = 0; i < nzq.size() && i < 2; ++i) slot |= ((e >> nzq[i]) & 1) << i;
       sp.sc_slot[e] = (uint8_t)slot;
+      sp.sc_sel[e] = (uint32_t)(slot | (4 + slot) << 4 | slot << 8 | (4 + slot) << 12);
     }
   }
   // ---- tile map: outer dst bits in the planner's tile order.  Order 2

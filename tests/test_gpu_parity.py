@@ -412,18 +412,28 @@ def test_fp8_transpose_paths(mb, nb):
 
 # ------------------------------------------------------------- mxfp4 upcast
 
-@pytest.mark.parametrize("mb,kb", [(8, 7), (9, 9)])
-def test_mxfp4_upcast(mb, kb):
-    """NEXT #1: config-5 layouts, E2M1 bytes + E8M0 scales in
-    [120, 134] plus edge scales (0, 1, 254, 255 = NaN), bit-exact bf16."""
+@pytest.mark.parametrize("mb,kb,dist", [(8, 7, "narrow"), (9, 9, "narrow"), (9, 8, "uniform"),
+                                        (8, 8, "edges")])
+def test_mxfp4_upcast(mb, kb, dist):
+    """NEXT #1: config-5 layouts, E2M1 bytes + E8M0 scales, bit-exact
+    bf16.  narrow: scales in [120, 135] plus edge scales (0, 1, 254, 255 = NaN);
+    uniform: every scale byte 0..255 (vectors mix the kernel's normal-product
+    fast path with its general path); edges: only 0-3 and 251-255 (the fast
+    path's bounds 2 and 252, subnormal and infinite products)."""
     from oracle import mxfp4
     c = configs.cfg5(m_bits=mb, kb_bits=kb)
     A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
     n = 1 << A.in_bits
     packed = values_torch(n, 41, 1, "cuda")
     n_sc = (1 << mb) * (1 << (kb - 4))
-    sc = (indices_torch(n_sc, 42, 16, "cuda") + 120).to(torch.uint8)
-    sc[:4] = torch.tensor([0, 1, 254, 255], dtype=torch.uint8)
+    if dist == "narrow":
+        sc = (indices_torch(n_sc, 42, 16, "cuda") + 120).to(torch.uint8)
+        sc[:4] = torch.tensor([0, 1, 254, 255], dtype=torch.uint8)
+    elif dist == "uniform":
+        sc = indices_torch(n_sc, 43, 256, "cuda").to(torch.uint8)
+    else:
+        pick = torch.tensor([0, 1, 2, 3, 251, 252, 253, 254, 255], dtype=torch.uint8, device="cuda")
+        sc = pick[indices_torch(n_sc, 44, 9, "cuda").long()]
     out = torch.empty(2 * n, dtype=torch.int16, device="cuda")
     ll.mxfp4_upcast(packed, A, sc, out, B)
     torch.cuda.synchronize()
