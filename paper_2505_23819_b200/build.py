@@ -40,8 +40,10 @@ def _compile(src, force):
     if not force and _mtime(o) > max(_mtime(s), _hdr_mtime()):
         return o, None
     if src.endswith(".cu"):
+        # LL_NVCC_EXTRA: extra nvcc flags for tuning experiments (e.g. -DLL_UP_MINB=3)
+        extra = os.environ.get("LL_NVCC_EXTRA", "").split()
         cmd = [NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
-               "-Xptxas", "-v", "-c", s, "-o", o]
+               "-Xptxas", "-v", *extra, "-c", s, "-o", o]
     else:
         cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-I", os.path.join(CUDA, "include"),
                "-c", s, "-o", o]

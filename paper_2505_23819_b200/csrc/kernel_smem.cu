@@ -1,6 +1,13 @@
 // kernel_smem.cu -- shared-memory conversion kernel (paper's optimal swizzle) and launcher.
 #include "device_common.cuh"
 
+#ifndef LL_UP_PREFETCH
+#define LL_UP_PREFETCH 1  // upcast: load the next tile's scales with its data
+#endif
+#ifndef LL_UP_MINB
+#define LL_UP_MINB 2  // resident CTAs the upcast kernel is compiled for (sweep: 2 > 3 > 4 > 1)
+#endif
+
 namespace ll {
 
 // UP: fused mxfp4 dequantisation (NEXT #1; W == 1): every
@@ -28,7 +35,7 @@ __device__ __forceinline__ uint32_t bf16x2_mul(uint32_t a, uint32_t b) {
 }
 
 template <int W, int NV, int G, bool PIPE, bool PAD, bool UP = false>
-__global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant__ SmemPlan p,
+__global__ void __launch_bounds__(256, UP ? LL_UP_MINB : 1) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
                                                            int64_t n_groups, TileRange rg,
@@ -88,18 +95,47 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
   const int ga = p.gsel_a, gb = p.gsel_b;
   const int64_t n_tiles = rg.t1;
 
+  // UP: the 4 distinct scales of each destination vector, packed per vector,
+  // and a bit per vector when all four give normal products (fast path);
+  // loaded together with the tile so their latency overlaps the staging
+  uint32_t PK[UP ? NV : 1];
+  uint32_t fastm = 0;
+  auto load_scales = [&]() {
+    if constexpr (UP) {
+      fastm = 0;
+      if (p.sc_nz <= 2) {
+#pragma unroll
+        for (int u = 0; u < NV; ++u) {
+          const uint8_t* scp = scales + sct + sc_off + p.sc_vec[u];
+          const uint32_t s0 = __ldg(scp), s1 = __ldg(scp + p.sc_c[0]), s2 = __ldg(scp + p.sc_c[1]),
+                         s3 = __ldg(scp + p.sc_c[0] + p.sc_c[1]);
+          PK[u] = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
+          // all four scales in [2, 252]: every product is a normal number
+          const bool ok = (s0 - 2u < 251u) & (s1 - 2u < 251u) & (s2 - 2u < 251u) & (s3 - 2u < 251u);
+          fastm |= (uint32_t)ok << u;
+        }
+      }
+    }
+  };
+
   uint32_t R[NW];
   int64_t so, dof;
   int64_t t = rg.t0 + gid;
   if (PIPE && t < n_tiles) {
     tile_off(t, so, dof);
     load_tile<NV>(R, sthr + so, p.ld_vec);
+    if (LL_UP_PREFETCH) load_scales();
   }
   for (; t < n_tiles; t += n_groups) {
     if (!PIPE) tile_off(t, so, dof);
     if (!PIPE) load_tile<NV>(R, sthr + so, p.ld_vec);
+    if (!PIPE || !LL_UP_PREFETCH) load_scales();
     const int64_t dcur = dof;
     const int64_t sct_cur = sct;
+    uint32_t PKc[UP ? NV : 1];
+#pragma unroll
+    for (int u = 0; u < (UP ? NV : 1); ++u) PKc[u] = PK[u];
+    const uint32_t fastc = fastm;
     for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(R, p.swap_a[s], p.swap_b[s]);
     sts_dispatch<NW, GW, PAD>(ga, gb, R, sbase + buf, swx, p.sw_gran);
     if (PIPE) {
@@ -107,6 +143,7 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       if (tn < n_tiles) {
         tile_off(tn, so, dof);
         load_tile<NV>(R, sthr + so, p.ld_vec);
+        if (LL_UP_PREFETCH) load_scales();
       }
     }
     group_sync(gw, group);
@@ -124,15 +161,8 @@ __global__ void __launch_bounds__(256) convert_smem_kernel(const __grid_constant
       for (int u = 0; u < NV; ++u) {
         const uint8_t* scp = scales + scur + p.sc_vec[u];
         uint32_t ow[16];
-        bool fast = false;
-        uint32_t pk = 0;
-        if (p.sc_nz <= 2) {  // the 4 distinct scales of this vector, packed in a word
-          const uint32_t s0 = __ldg(scp), s1 = __ldg(scp + p.sc_c[0]), s2 = __ldg(scp + p.sc_c[1]),
-                         s3 = __ldg(scp + p.sc_c[0] + p.sc_c[1]);
-          pk = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
-          // all four scales in [2, 252]: every product is a normal number
-          fast = (s0 - 2u < 251u) & (s1 - 2u < 251u) & (s2 - 2u < 251u) & (s3 - 2u < 251u);
-        }
+        const bool fast = (fastc >> u) & 1u;
+        const uint32_t pk = PKc[u];
         if (fast) {
           // e2m1 magnitude -> bf16 by byte-permute table lookups, the sign
           // bits moved into place, then one exact bf16x2 multiply by
