@@ -251,12 +251,23 @@ ll_status ll_gather_describe(ll_layout layout, int axis, int elem_bits, int path
  * benchmark's gpu_launches claim). */
 int64_t ll_launch_count(void);
 
-/* Launch-configuration knobs (process-wide; defaults from the environment):
+/* Tuning knobs (process-wide).  Launch configuration (defaults from the
+ * environment, read once):
  *   "tpg"        target tiles per tile group of the smem kernel (0 = persistent
  *                grid at full occupancy; env LL_TPG, default 2)
- *   "pipe"       1 = software-pipelined smem kernel (env LL_PIPE, default 0)
+ *   "pipe"       1 = software-pipelined smem kernel (env LL_PIPE, default 1)
+ *   "up_tpg"     tiles per group of the mxfp4 upcast kernel (env LL_UP_TPG,
+ *                default 0 = persistent)
  *   "gather_vpt" 16-byte output vectors per thread of the gather kernels
- *                (env LL_GATHER_VPT, default 2)
+ *                (env LL_GATHER_VPT; 0 = per path: shuffle 4, direct 1)
+ *   "carveout", "pow2", "stages", "async_tpg"  ablation knobs of the smem /
+ *                cp.async kernels (env LL_CARVEOUT, LL_POW2, LL_STAGES,
+ *                LL_ASYNC_TPG)
+ * Planner (new plans only; cached plans are rebuilt):
+ *   "thread_bytes", "thread_bytes_max", "max_granule", "run_bytes",
+ *   "tile_order"  thread vector bytes, granule cap, coalescing run bytes,
+ *                tile index order
+ * ll_convert_host: "host_chunk_mb" (default 16), "host_slots" (default 2).
  * LL_ERR_ARG for an unknown name.  Used by the tuning sweeps. */
 ll_status ll_tune(const char* name, int value);
 

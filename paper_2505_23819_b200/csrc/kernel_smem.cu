@@ -154,36 +154,60 @@ __global__ void __launch_bounds__(256, UP ? LL_UP_MINB : 1) convert_smem_kernel(
       lds<G>(sbase + buf + (PAD ? pad_off(o) : o), &Q[j * GW]);
     }
     if constexpr (UP) {
-      // fused dequantisation: 16 packed bytes -> 32 bf16 (64 bytes) per vector
+      // fused dequantisation: 16 packed bytes -> 32 bf16 (64 bytes) per vector.
+      // Lanes l and l^1 form a pair: every store instruction of the pair
+      // fills one whole 32-byte sector (the even lane the first 16 bytes, the
+      // odd lane the next 16) -- 16 bytes per lane at a 64-byte stride would
+      // leave each sector half written per instruction, which runs at half
+      // the HBM write rate (tools/bwprobe.cu: r1w4_lane vs r1w4_coal).  The
+      // pair trades packed input words (4 bytes -> one 16-byte output chunk)
+      // and scales: the even lane converts chunks 0 and 2 of both lanes'
+      // vectors, the odd lane chunks 1 and 3.
       const int64_t dbyte = (int64_t)st_off - rg.dst_shift + dcur;
       const int64_t scur = sct_cur + sc_off;
+      const bool odd = lane & 1;
+      const uint32_t fpair = fastc & __shfl_xor_sync(0xFFFFFFFFu, fastc, 1);
 #pragma unroll
       for (int u = 0; u < NV; ++u) {
-        const uint8_t* scp = scales + scur + p.sc_vec[u];
-        uint32_t ow[16];
-        const bool fast = (fastc >> u) & 1u;
         const uint32_t pk = PKc[u];
-        if (fast) {
-          // e2m1 magnitude -> bf16 by byte-permute table lookups, the sign
-          // bits moved into place, then one exact bf16x2 multiply by
-          // (2^(s-127), 2^(s-127)) per destination word
-          const uint32_t plo = (pk << 7) & 0x80808080u, phi = (pk >> 1) & 0x7F7F7F7Fu;
+        const uint32_t w0 = Q[4 * u], w1 = Q[4 * u + 1], w2 = Q[4 * u + 2], w3 = Q[4 * u + 3];
+        const uint32_t r0 = __shfl_xor_sync(0xFFFFFFFFu, odd ? w0 : w1, 1);
+        const uint32_t r1 = __shfl_xor_sync(0xFFFFFFFFu, odd ? w2 : w3, 1);
+        const uint32_t pkp = __shfl_xor_sync(0xFFFFFFFFu, pk, 1);
+        uint8_t* op = dst + 4 * (dbyte + p.st_vec[u]);
+        if ((fpair >> u) & 1u) {
+          // chunk q of this lane's work: the lane's own vector (A/B) and word
+          uint8_t* opp = op + (odd ? -4 * (int64_t)p.st_thr[0] : 4 * (int64_t)p.st_thr[0]);
+          uint8_t* oA = (odd ? opp : op) + (odd ? 16 : 0);
+          uint8_t* oB = (odd ? op : opp) + (odd ? 16 : 0);
+          const uint32_t in[4] = {odd ? r0 : w0, odd ? r1 : w2, odd ? w1 : r0, odd ? w3 : r1};
+          // the odd lane's chunks are the even lane's byte indices + 4: the
+          // same selectors apply after permuting the packed scales
+          const uint32_t psel = odd ? p.sc_psel : 0x3210u;
+          const uint32_t pkA = __byte_perm(odd ? pkp : pk, 0u, psel);
+          const uint32_t pkB = __byte_perm(odd ? pk : pkp, 0u, psel);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t wq = Q[4 * u + j];
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t pq = q < 2 ? pkA : pkB;
+            const uint32_t plo = (pq << 7) & 0x80808080u, phi = (pq >> 1) & 0x7F7F7F7Fu;
+            const uint32_t wq = in[q];
             const uint32_t m = wq & 0x77777777u, mh = m >> 16, x = wq & 0x88888888u;
             const uint32_t L01 = __byte_perm(kE2M1Lo0, kE2M1Lo1, m), H01 = __byte_perm(kE2M1Hi0, kE2M1Hi1, m);
             const uint32_t L23 = __byte_perm(kE2M1Lo0, kE2M1Lo1, mh), H23 = __byte_perm(kE2M1Hi0, kE2M1Hi1, mh);
+            uint32_t o4[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const int e = 4 * j + k;
+              const int e = 8 * (q & 1) + k;
               const uint32_t mag = __byte_perm(k < 2 ? L01 : L23, k < 2 ? H01 : H23, (k & 1) ? 0x7362 : 0x5140);
               const uint32_t t = __byte_perm(x, 0u, 0x4440 | k) * 0x01001000u;  // bits 3,7 -> 15,31
               const uint32_t v = mag | (t & 0x80008000u);
-              ow[e] = bf16x2_mul(v, __byte_perm(plo, phi, p.sc_sel[e]));
+              o4[k] = bf16x2_mul(v, __byte_perm(plo, phi, p.sc_sel[e]));
             }
+            stg_stream((q < 2 ? oA : oB) + 32 * (q & 1), make_uint4(o4[0], o4[1], o4[2], o4[3]));
           }
         } else {
+          const uint8_t* scp = scales + scur + p.sc_vec[u];
+          uint32_t ow[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const uint32_t byte = (Q[4 * u + (e >> 2)] >> ((e & 3) * 8)) & 0xFFu;
@@ -195,11 +219,10 @@ __global__ void __launch_bounds__(256, UP ? LL_UP_MINB : 1) convert_smem_kernel(
             // NaN scale -> the canonical bf16 quiet NaN 0x7FC0 for both values
             ow[e] = sb == 255u ? 0x7FC07FC0u : ((hi & 0xFFFF0000u) | (lo >> 16));
           }
-        }
-        uint8_t* op = dst + 4 * (dbyte + p.st_vec[u]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          stg_stream(op + 16 * q, make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
+          for (int q = 0; q < 4; ++q)
+            stg_stream(op + 16 * q, make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
+        }
       }
     } else {
       uint8_t* dp = dthr + dcur;
@@ -234,7 +257,7 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   if (n_tiles <= 0) return cudaSuccess;
   // tile groups: n_tiles / tpg (the hardware block scheduler balances the
   // tail), or the resident capacity when tpg = 0 (persistent)
-  const int tpg = knobs().tpg;
+  const int tpg = UP ? knobs().up_tpg : knobs().tpg;
   int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)occ_cache * num_sms() * gpc;
   if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
   groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));

@@ -74,6 +74,7 @@ struct SmemPlan {
   uint32_t sc_c[2];               // their scale-index contributions
   uint8_t sc_slot[16];            // slot (0..3) of byte e among the 4 loaded scales
   uint32_t sc_sel[16];            // prmt selector: bf16x2 factor of byte e's slot
+  uint32_t sc_psel;               // prmt: slots of bytes e + 4 from those of bytes e
 };
 
 // Warp-shuffle conversion plan (LL_PATH_SHUFFLE): warp-local tiles exchanged

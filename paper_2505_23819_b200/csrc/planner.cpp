@@ -466,6 +466,14 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       if (scale_contrib(P, st_reg[q])) nzq.push_back(q);
     sp.sc_nz = (int)nzq.size();
     for (size_t i = 0; i < nzq.size() && i < 2; ++i) sp.sc_c[i] = (uint32_t)scale_contrib(P, st_reg[nzq[i]]);
+    // byte e + 4 (vector bit 2 set) has the slot of byte e with the slot bit
+    // of vector bit 2 (if it moves the scale) flipped
+    sp.sc_psel = 0x3210u;
+    for (size_t i = 0; i < nzq.size() && i < 2; ++i)
+      if (nzq[i] == 2) {
+        sp.sc_psel = 0;
+        for (int q = 0; q < 4; ++q) sp.sc_psel |= (uint32_t)(q ^ (1 << i)) << (4 * q);
+      }
     for (int e = 0; e < (1 << vb); ++e) {
       int slot = 0;
       for (size_t i = 0; i < nzq.size() && i < 2; ++i) slot |= ((e >> nzq[i]) & 1) << i;

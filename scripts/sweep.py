@@ -94,7 +94,25 @@ def main():
             nbytes = 2 * n * w
             nsets = 2 if n * w >= (64 << 20) else 4
             sets = [(values_torch(n, 7 + s, w, dev), values_torch(n, 0, w, dev)) for s in range(nsets)]
-            for path in args.paths.split(","):
+            if "upcast" in args.paths.split(",") and cfg == "5":
+                # fused mxfp4 -> bf16 (2 bf16 per packed byte), scales in [120, 135]
+                scales = (indices_torch(n // 16, 42, 16, dev) + 120).to(torch.uint8)
+                usets = [(sets[s][0], torch.empty(2 * n, dtype=torch.int16, device=dev))
+                         for s in range(nsets)]
+                for ks in knob_sets:
+                    for k, v in ks.items():
+                        ll.tune(k, v)
+                    try:
+                        ms = timeit(lambda i: ll.mxfp4_upcast(usets[i % nsets][0], A, scales,
+                                                              usets[i % nsets][1], B), args.steps)
+                        emit(dict({"cfg": cfg, "path": "upcast", "ms": ms,
+                                   "GBps": (n + n // 16 + 4 * n) / ms / 1e6}, **ks))
+                    except ll.LLError as e:
+                        emit(dict({"cfg": cfg, "path": "upcast", "error": str(e)}, **ks))
+                    for k, v in DEFAULTS.items():
+                        ll.tune(k, v)
+                del usets
+            for path in [q for q in args.paths.split(",") if q != "upcast"]:
                 for ks in (knob_sets if path.startswith("smem") or path == "shuffle" else [{}]):
                     for k, v in ks.items():
                         ll.tune(k, v)
