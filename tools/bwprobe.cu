@@ -6,7 +6,10 @@
 //   r1w4_coal  read 16 B, write 64 B per thread; each warp store instruction
 //              covers 512 contiguous bytes (fully coalesced)
 //   r1w4_lane  read 16 B, write 64 B per thread as 4 x 16 B at +0/16/32/48 of
-//              the thread's own 64 B (the upcast kernel's store pattern)
+//              the thread's own 64 B
+//   r1w4_pair  lane pairs fill one 32-byte sector per store instruction (the
+//              upcast kernel's store pattern)
+//   r1w4_quad  lane quads fill 64 contiguous bytes per store instruction
 // Prints one JSON line per case: GB/s = (read + write bytes) / time, best of
 // 20 launches over two rotating buffer sets larger than L2.
 #include <cstdint>
@@ -51,6 +54,29 @@ __global__ void k_r1w4_lane(const uint4* __restrict__ a, uint4* __restrict__ b, 
   }
 }
 
+// lane pairs: instruction q writes one whole 32-byte sector per pair (the
+// upcast kernel's pattern): lane 2i+o stores 16 B at 64*(2i + (q>>1)) + 32*(q&1) + 16*o
+__global__ void k_r1w4_pair(const uint4* __restrict__ a, uint4* __restrict__ b, size_t n) {
+  const int o = threadIdx.x & 1;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 x = ldg_stream(a + i);
+    const size_t pair0 = (i - o) * 4;  // the pair's 2 x 64 B block, in 16-B units
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      stg(b + pair0 + 4 * (q >> 1) + 2 * (q & 1) + o, make_uint4(x.x ^ q, x.y, x.z, x.w));
+  }
+}
+// quads: instruction q writes 64 contiguous bytes per 4 lanes
+__global__ void k_r1w4_quad(const uint4* __restrict__ a, uint4* __restrict__ b, size_t n) {
+  const int o = threadIdx.x & 3;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 x = ldg_stream(a + i);
+    const size_t q0 = (i - o) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) stg(b + q0 + 4 * q + o, make_uint4(x.x ^ q, x.y, x.z, x.w));
+  }
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -86,6 +112,8 @@ int main() {
     run("write 2GiB", 1.0 * out_bytes, [&](int s) { k_write<<<grid, threads>>>(b[s], out_bytes / 16, s); });
     run("r1w4_coal 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_coal<<<grid, threads>>>(a[s], b[s], nv); });
     run("r1w4_lane 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_lane<<<grid, threads>>>(a[s], b[s], nv); });
+    run("r1w4_pair 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_pair<<<grid, threads>>>(a[s], b[s], nv); });
+    run("r1w4_quad 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_quad<<<grid, threads>>>(a[s], b[s], nv); });
   }
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) {
