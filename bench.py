@@ -383,6 +383,28 @@ def main():
     achieved = nbytes / (avg_launch_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
 
+    from paper_2505_23819_b200 import multigpu
+    # row a12 (untimed): checksum record of the last step's destination per
+    # rank (ll_checksum, indexed), and for conversions the permutation
+    # property on the whole buffer (index-free checksums of src and dst agree)
+    last = sets[(K - 1) % len(sets)]
+    dst_t = last[2] if cfg == "4" else last[1]
+    ck = torch.zeros(3, dtype=torch.int64, device=dev)
+    ll.checksum(dst_t, dst_t.numel(), 8 * dst_t.element_size(), ck[0:1], stream=stream)
+    perm_check = cfg != "4" and not args.upcast
+    if perm_check:
+        ll.checksum(last[0], last[0].numel(), 8 * last[0].element_size(), ck[1:2], indexed=False,
+                    stream=stream)
+        ll.checksum(dst_t, dst_t.numel(), 8 * dst_t.element_size(), ck[2:3], indexed=False,
+                    stream=stream)
+    torch.cuda.synchronize()
+    ckv = [int(x) & ((1 << 64) - 1) for x in ck.cpu().tolist()]
+    records = multigpu.gather_objects(["%016x" % ckv[0], (ckv[1] == ckv[2]) if perm_check else None])
+    verify = {"dst_checksum_per_rank": [r[0] for r in records],
+              "permutation_ok": all(r[1] for r in records) if perm_check else None,
+              "how": "ll_checksum (row a12): indexed splitmix64 sum of the last step's destination; "
+                     "permutation_ok = index-free sums of src and dst agree"}
+
     # end to end through the C ABI with HOST buffers (pinned), copies in the region
     e2e = None
     if cfg != "4" and args.e2e_steps > 0:
@@ -461,6 +483,7 @@ def main():
             "timing": "CUDA graph of K steps replayed once" if graph is not None else "K launches from Python",
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "verify": verify,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -223,6 +223,23 @@ ll_status ll_convert_shard(const void* src_slice, ll_layout src_layout, void* ds
 ll_status ll_shard_describe(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
                             int n_shards, int shard, int64_t* out4);
 
+/* Checksum of a device buffer (untimed; ours -- the
+ * paper has no such step): the 64-bit sum, mod 2^64, over elements h of
+ *     fmix( v_h + (index_base + h + 1) * 0x9E3779B97F4A7C15 )     (indexed)
+ *     fmix( v_h )                                                  (!indexed)
+ * where v_h is element h zero-extended to 64 bits and fmix is the splitmix64
+ * output function (z ^= z >> 30; z *= 0xBF58476D1CE4E5B9; z ^= z >> 27;
+ * z *= 0x94D049BB133111EB; z ^= z >> 31).  Indexed sums see misplaced
+ * elements; the sums of a partition's pieces (index_base = the piece's first
+ * element) add up to the whole buffer's.  The index-free sum is invariant
+ * under any permutation (a full-size property of bijective conversions).
+ *   buf        n_elems elements of elem_bits (8/16/32/64), 16-byte aligned
+ *   result     DEVICE pointer to one uint64; overwritten (zeroed, then
+ *              accumulated) on `stream`; read it after the stream completes
+ * Errors: LL_ERR_ARG (NULL / misaligned / elem_bits / n_elems < 0). */
+ll_status ll_checksum(const void* buf, int64_t n_elems, int elem_bits, int indexed,
+                      int64_t index_base, uint64_t* result, ll_stream stream);
+
 /* End-to-end conversion of HOST buffers: src_host/dst_host are host pointers
  * (pinned for full speed); the library pipelines host->device copies, the
  * conversion and device->host copies in chunks (~16 MiB: whole layout

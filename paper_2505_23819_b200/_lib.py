@@ -60,6 +60,7 @@ _lib.ll_gather_describe.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
 _lib.ll_tune.argtypes = [ctypes.c_char_p, ctypes.c_int]
 _VP = ctypes.c_void_p
 _lib.ll_mxfp4_upcast.argtypes = [_VP, _VP, _VP, _VP, _VP, _VP, _VP]
+_lib.ll_checksum.argtypes = [_VP, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _VP, _VP]
 _lib.ll_transpose.argtypes = [_VP, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_VP)]
 _lib.ll_reshape.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
                             ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_VP)]
@@ -72,7 +73,7 @@ _lib.ll_convert_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_voi
                                   ctypes.c_void_p, ctypes.c_void_p]
 _lib.ll_shard_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
-for _f in ("ll_mxfp4_upcast", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+for _f in ("ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
@@ -305,6 +306,13 @@ def mxfp4_upcast(packed, A, scales, dst_bf16, B, max_ctas=0, stream=None):
     o = _opts("auto", 1, max_ctas)
     _check(_lib.ll_mxfp4_upcast(_ptr(packed), A.handle, _ptr(scales), _ptr(dst_bf16), B.handle,
                                 ctypes.byref(o), _stream_handle(stream)))
+
+
+def checksum(buf, n_elems, elem_bits, result, indexed=True, index_base=0, stream=None):
+    """ll_checksum into the device uint64 `result` (a 1-element int64 tensor or
+    a device pointer); enqueued on `stream`, no synchronisation."""
+    _check(_lib.ll_checksum(_ptr(buf), int(n_elems), int(elem_bits), 1 if indexed else 0,
+                            int(index_base), _ptr(result), _stream_handle(stream)))
 
 
 def shard_describe(A, B, elem_bits, n_shards, shard, path="auto"):

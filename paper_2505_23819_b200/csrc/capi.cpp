@@ -448,6 +448,22 @@ ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_
   });
 }
 
+ll_status ll_checksum(const void* buf, int64_t n_elems, int elem_bits, int indexed,
+                      int64_t index_base, uint64_t* result, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    const int w = elem_bytes(elem_bits);
+    if (!buf || !result) return fail(LL_ERR_ARG, "ll_checksum: NULL pointer");
+    if (n_elems < 0) return fail(LL_ERR_ARG, "ll_checksum: n_elems < 0");
+    if (reinterpret_cast<uintptr_t>(buf) & 15)
+      return fail(LL_ERR_ARG, "ll_checksum: buffer must be 16-byte aligned");
+    ++g_launches;
+    return cuda_status(ll::launch_checksum(buf, n_elems, w, indexed != 0, index_base,
+                                           reinterpret_cast<unsigned long long*>(result),
+                                           reinterpret_cast<cudaStream_t>(stream)),
+                       "ll_checksum");
+  });
+}
+
 ll_status ll_convert_shard(const void* src_slice, ll_layout src_layout, void* dst_slice,
                            ll_layout dst_layout, int elem_bits, int n_shards, int shard,
                            const ll_convert_options* opts, ll_stream stream) {

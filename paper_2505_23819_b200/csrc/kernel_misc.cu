@@ -319,4 +319,75 @@ cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* 
 
 int device_sm_count() { return num_sms(); }
 
+// ------------------------------------------------------------- checksum (a12)
+// Sum over elements of fmix(v + (base + h + 1) * gamma) (indexed) or fmix(v),
+// mod 2^64 (order-free, so a grid-stride reduction with 64-bit atomics).
+__device__ __forceinline__ unsigned long long ck_fmix(unsigned long long z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) checksum_kernel(const uint8_t* __restrict__ buf, int64_t n,
+                                                       bool indexed, int64_t base,
+                                                       unsigned long long* result) {
+  constexpr int E = 16 / W;  // elements per 16-byte vector
+  constexpr unsigned long long G = 0x9E3779B97F4A7C15ull;
+  unsigned long long acc = 0;
+  const int64_t nvec = n / E;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(buf) + v);
+    const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      unsigned long long x;
+      if (W == 8) x = (unsigned long long)wd[2 * e] | ((unsigned long long)wd[2 * e + 1] << 32);
+      else x = (wd[(e * W) / 4] >> (8 * ((e * W) % 4))) & (W == 4 ? 0xFFFFFFFFu : (1u << (8 * W)) - 1u);
+      const unsigned long long h = (unsigned long long)(v * E + e);
+      acc += ck_fmix(indexed ? x + ((unsigned long long)base + h + 1ull) * G : x);
+    }
+  }
+  // ragged tail (n not a multiple of E): the first threads take one element each
+  const int64_t tail0 = nvec * E;
+  const int64_t ti = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ti < n - tail0) {
+    const uint8_t* ep = buf + (tail0 + ti) * W;
+    unsigned long long x = 0;
+    for (int b = 0; b < W; ++b) x |= (unsigned long long)ep[b] << (8 * b);
+    const unsigned long long h = (unsigned long long)(tail0 + ti);
+    acc += ck_fmix(indexed ? x + ((unsigned long long)base + h + 1ull) * G : x);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  __shared__ unsigned long long part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += part[i];
+    atomicAdd(result, s);
+  }
+}
+
+cudaError_t launch_checksum(const void* buf, int64_t n, int w, bool indexed, int64_t base,
+                            unsigned long long* result, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(result, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess || n == 0) return e;
+  const int64_t nvec = std::max<int64_t>(1, n / (16 / w));
+  const int64_t grid = std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 8);
+  const uint8_t* b = static_cast<const uint8_t*>(buf);
+  switch (w) {
+    case 1: checksum_kernel<1><<<(unsigned)grid, 256, 0, st>>>(b, n, indexed, base, result); break;
+    case 2: checksum_kernel<2><<<(unsigned)grid, 256, 0, st>>>(b, n, indexed, base, result); break;
+    case 4: checksum_kernel<4><<<(unsigned)grid, 256, 0, st>>>(b, n, indexed, base, result); break;
+    case 8: checksum_kernel<8><<<(unsigned)grid, 256, 0, st>>>(b, n, indexed, base, result); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace ll

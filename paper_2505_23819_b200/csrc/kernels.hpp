@@ -21,6 +21,8 @@ cudaError_t launch_gather(const GatherPlan& p, int w, bool shuffle, const void* 
 cudaError_t launch_mxfp4_upcast(const SmemPlan& p, int nv, int g, const void* src, void* dst,
                                 const uint8_t* scales, int max_ctas, cudaStream_t st,
                                 const TileRange& rg);
+cudaError_t launch_checksum(const void* buf, int64_t n, int w, bool indexed, int64_t base,
+                            unsigned long long* result, cudaStream_t st);
 int device_sm_count();
 int set_knob(const char* name, int value);
 

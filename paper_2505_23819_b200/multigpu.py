@@ -59,6 +59,15 @@ def gather_records(record, device=None):
     return [o.tolist() for o in out]
 
 
+def gather_objects(obj):
+    """All-gather one picklable record per rank (e.g. checksum strings)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
 def aggregate_gbps(bytes_per_rank, time_ms_per_rank, scaling):
     """Whole-job GB/s: all ranks' bytes / the slowest rank's time.
 

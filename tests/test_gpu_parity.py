@@ -441,6 +441,82 @@ def test_mxfp4_upcast(mb, kb, dist):
     assert out.cpu().numpy().view(np.uint16).tobytes() == exp.tobytes()
 
 
+@pytest.mark.parametrize("dist", ["narrow", "uniform"])
+def test_mxfp4_upcast_full_size_sampled(dist):
+    """Config 5 at the BASELINE size (packed [32768, 16384] u8 -> 2 GiB of
+    bf16), the launch bench.py --upcast times; sampled destination bytes
+    computed one by one by the oracle (A^{-1} o B per index, OCP MX table)."""
+    from oracle import mxfp4
+    c = configs.cfg5()
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    packed = values_torch(n, 51, 1, "cuda")
+    n_sc = n // 16
+    if dist == "narrow":
+        sc = (indices_torch(n_sc, 52, 16, "cuda") + 120).to(torch.uint8)
+    else:
+        sc = indices_torch(n_sc, 53, 256, "cuda").to(torch.uint8)
+    out = torch.empty(2 * n, dtype=torch.int16, device="cuda")
+    ll.mxfp4_upcast(packed, A, sc, out, B)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(11)
+    h = np.concatenate([rng.integers(0, n, 200000), np.arange(4096), np.arange(n - 4096, n)]).astype(np.int64)
+    Ao, Bo = _olayout(c["A"]), _olayout(c["B"])
+    Ainv = f2.right_inverse(Ao.cols, Ao.out_bits)
+    x = oconv.apply_np(Bo.cols, h)
+    kb_bits = Bo.out_dims[1][1]
+    m, kb = x >> kb_bits, x & ((1 << kb_bits) - 1)
+    src_np = _np(packed, 1)
+    byte = src_np[oconv.apply_np(Ainv, x)].astype(np.int64)
+    scale = sc.cpu().numpy()[m * (1 << (kb_bits - 4)) + (kb >> 4)].astype(np.int64)
+    tab = mxfp4.dequant_table()
+    hh = torch.from_numpy(h).cuda()
+    got = out.view(torch.int32)[hh].cpu().numpy().view(np.uint32)
+    exp = tab[scale, byte & 15].astype(np.uint32) | (tab[scale, byte >> 4].astype(np.uint32) << 16)
+    assert (got == exp).all()
+
+
+# ------------------------------------------------------------- checksum (a12)
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+@pytest.mark.parametrize("n,base", [(0, 0), (1, 0), (37, 5), (4099, 0), (1 << 20, 123456789)])
+def test_checksum_matches_oracle(w, n, base):
+    from oracle import checksum as ock
+    buf = values_torch(max(n, 1), 61 + w, w, "cuda")
+    res = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for indexed in (True, False):
+        ll.checksum(buf, n, 8 * w, res, indexed=indexed, index_base=base)
+        torch.cuda.synchronize()
+        got = int(res.item()) & ((1 << 64) - 1)
+        assert got == ock.checksum_np(_np(buf, w)[:n], indexed=indexed, base=base)
+
+
+def test_checksum_full_size_conversion_properties():
+    """cfg5 at full size: the index-free checksum of dst equals src's (the
+    conversion is a permutation); per-shard indexed checksums (each with its
+    slice's base) add up to the whole destination's."""
+    c = configs.cfg5()
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src = values_torch(n, 71, 1, "cuda")
+    dst = torch.empty_like(src)
+    ll.convert(src, A, dst, B, 8)
+    res = torch.zeros(4, dtype=torch.int64, device="cuda")
+    ll.checksum(src, n, 8, res[0:1], indexed=False)
+    ll.checksum(dst, n, 8, res[1:2], indexed=False)
+    ll.checksum(dst, n, 8, res[2:3], indexed=True)
+    parts = 0
+    for k in range(8):
+        s0, s1, d0, d1 = ll.shard_describe(A, B, 8, 8, k)
+        ll.checksum(dst[d0:], d1 - d0, 8, res[3:4], indexed=True, index_base=d0)
+        torch.cuda.synchronize()
+        parts = (parts + int(res[3].item())) & ((1 << 64) - 1)
+    torch.cuda.synchronize()
+    r = [int(x) & ((1 << 64) - 1) for x in res.cpu().tolist()]
+    assert r[0] == r[1]
+    assert parts == r[2]
+
+
 def test_convert_host_sharded_single_instance():
     """One large instance (8 MiB) chunked by shards through ll_convert_host."""
     c = configs.cfg5(m_bits=12, kb_bits=11)

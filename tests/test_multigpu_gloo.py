@@ -60,6 +60,8 @@ def _worker(rank, world, port, q):
         outside = np.ones(n, dtype=bool)
         outside[d0:d1] = False
         ok_outside = bool((part[outside] == 0).all())
+        objs = multigpu.gather_objects(["%016x" % (rank + 1), rank == 0])
+        assert objs == [["%016x" % 1, True], ["%016x" % 2, False]]
         t = multigpu.max_over_ranks(10.0 + rank)
         agg = multigpu.aggregate_gbps([2 * (s1 - s0)] * world, [10.0, 11.0], "strong")
         q.put((rank, ok_partition, ok_slice, ok_outside, t, agg))
@@ -93,5 +95,6 @@ def test_aggregate_single_process():
     from paper_2505_23819_b200 import multigpu
     assert multigpu.max_over_ranks(3.5) == 3.5
     assert multigpu.gather_records([1, 2]) == [[1, 2]]
+    assert multigpu.gather_objects(["ab", None]) == [["ab", None]]
     with pytest.raises(ValueError):
         multigpu.aggregate_gbps([1], [1.0], "sideways")
