@@ -556,11 +556,13 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 2)));
     // chunking: whole layout instances (batch elements), or -- for a single
     // large instance -- shards (contiguous slices of both buffers)
+    // (a chunk must also fit one slot of the caller's scratch)
+    const size_t cap = std::max<size_t>(1, std::min(target, scratch_bytes));
     int n_sh = 1;
-    if (batch == 1 && unit > target) {
+    if (batch == 1 && unit > cap) {
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
       int want = 1;
-      while ((unit / want) > target && want < (1 << 12)) want *= 2;
+      while ((unit / want) > cap && want < (1 << 12)) want *= 2;
       for (int ns = want; ns > 1; ns /= 2) {
         try {
           ll::shard_range(*P, ns, 0);
