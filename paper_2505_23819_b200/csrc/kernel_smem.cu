@@ -7,6 +7,17 @@
 #ifndef LL_UP_MINB
 #define LL_UP_MINB 2  // resident CTAs the upcast kernel is compiled for (sweep: 2 > 3 > 4 > 1)
 #endif
+// Resident CTAs (256 threads) the conversion kernel is compiled for, i.e. a
+// register cap of 64 (4 CTAs) / 80 (3 CTAs) per thread.  Without it ptxas
+// takes 72-116 registers and the occupancy drop costs 3-11 % of HBM bandwidth
+// (cfg2/3/5 measured against the 64/80-register build of the same kernel).
+// 4-byte granules (G = 4) keep the uncapped allocation: capped, they spill.
+#ifndef LL_SMEM_MINB
+#define LL_SMEM_MINB 4   // NV <= 4 vectors per thread
+#endif
+#ifndef LL_SMEM_MINB8
+#define LL_SMEM_MINB8 3  // NV = 8
+#endif
 
 namespace ll {
 
@@ -35,7 +46,7 @@ __device__ __forceinline__ uint32_t bf16x2_mul(uint32_t a, uint32_t b) {
 }
 
 template <int W, int NV, int G, bool PIPE, bool PAD, bool UP = false>
-__global__ void __launch_bounds__(256, UP ? LL_UP_MINB : 1) convert_smem_kernel(const __grid_constant__ SmemPlan p,
+__global__ void __launch_bounds__(256, UP ? LL_UP_MINB : (G < 8 ? 1 : (NV >= 8 ? LL_SMEM_MINB8 : LL_SMEM_MINB))) convert_smem_kernel(const __grid_constant__ SmemPlan p,
                                                            const uint8_t* __restrict__ src,
                                                            uint8_t* __restrict__ dst,
                                                            int64_t n_groups, TileRange rg,
