@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tune", action="append", default=[], metavar="KNOB=VALUE",
+                    help="ll_tune knob before planning (e.g. tma_stages=4); repeatable")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch each step from Python instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -275,6 +277,9 @@ def main():
     import torch.distributed as dist
     import paper_2505_23819_b200 as ll
     from workloads.values import indices_torch, values_torch
+    for kv in args.tune:
+        k, v = kv.split("=")
+        ll.tune(k, int(v))
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -458,6 +463,8 @@ def main():
                 cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "oracle",
                        "sample": "failed: %s" % ex}
         kernel = {"smem": "convert_smem_kernel", "generic": "convert_generic_kernel",
+                  "smem_noswizzle": "convert_smem_kernel", "smem_padded": "convert_smem_kernel",
+                  "smem_async": "convert_async_kernel", "smem_tma": "convert_tma_kernel",
                   "copy": "cudaMemcpyAsync", "shuffle": "gather_shuffle_kernel",
                   "direct": "gather_direct_kernel"}.get(plan.get("path"), plan.get("path"))
         line = {
@@ -472,6 +479,7 @@ def main():
                        "tile_bits": len(plan.get("tile_dst_bits") or []) or None,
                        "pred_wavefronts_per_sts": plan.get("pred_wavefronts_per_sts"),
                        "pred_wavefronts_per_lds": plan.get("pred_wavefronts_per_lds"),
+                       "tma": plan.get("tma"), "tune": args.tune or None,
                        "parallelism": "dp%d" % world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg),

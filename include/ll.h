@@ -169,7 +169,12 @@ typedef enum {
   LL_PATH_GENERIC = 4,   /* element-wise pull (any layouts; the slow baseline)     */
   LL_PATH_SMEM_NOSWIZZLE = 5, /* smem path with an unswizzled staging buffer (ablation) */
   LL_PATH_SMEM_ASYNC = 6, /* smem path fed by cp.async (source granules, multi-stage)  */
-  LL_PATH_SMEM_PADDED = 7 /* legacy heuristic: unswizzled staging + 16 B pad per 128 B (ablation) */
+  LL_PATH_SMEM_PADDED = 7, /* legacy heuristic: unswizzled staging + 16 B pad per 128 B (ablation) */
+  LL_PATH_SMEM_TMA = 8   /* smem path fed by TMA tensor loads (cp.async.bulk.tensor) into a
+                            hardware-swizzled image: the 32/64/128-byte swizzle modes are
+                            Def. 5 instances; the planner picks the mode and the
+                            reader's lanes so the reads are conflict-free.
+                            LL_ERR_UNSUPPORTED when the source tile needs > 5 box dims. */
 } ll_path;
 
 typedef struct {

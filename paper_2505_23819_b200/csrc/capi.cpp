@@ -384,7 +384,8 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
   if (n_shards > 1) {
     rg = ll::shard_range(*P, n_shards, shard);
   } else if (P->path == LL_PATH_SMEM || P->path == LL_PATH_SMEM_NOSWIZZLE ||
-             P->path == LL_PATH_SMEM_ASYNC || P->path == LL_PATH_SMEM_PADDED) {
+             P->path == LL_PATH_SMEM_ASYNC || P->path == LL_PATH_SMEM_PADDED ||
+             P->path == LL_PATH_SMEM_TMA) {
     rg.t1 = P->sp.tile.n_tiles;
   } else if (P->path == LL_PATH_SHUFFLE) {
     rg.t1 = P->shp.tile.n_tiles;
@@ -405,6 +406,10 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
       ++g_launches;
       return cuda_status(ll::launch_convert_async(P->sp, w, P->nv, src, dst, max_ctas, st, rg),
                          "ll_convert (async smem kernel)");
+    case LL_PATH_SMEM_TMA:
+      ++g_launches;
+      return cuda_status(ll::launch_convert_tma(P->sp, P->td, w, P->nv, src, dst, max_ctas, st, rg),
+                         "ll_convert (TMA smem kernel)");
     case LL_PATH_SMEM:
     case LL_PATH_SMEM_NOSWIZZLE:
     case LL_PATH_SMEM_PADDED:

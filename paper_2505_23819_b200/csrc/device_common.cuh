@@ -386,7 +386,7 @@ __device__ __forceinline__ void lin_op(uint32_t (&T)[NW], int op, int a, int b) 
 // ------------------------------------------------------------- launch knobs
 int num_sms();
 struct LaunchKnobs {
-  int tpg, pipe, gather_tpt, carveout, pow2, stages, async_tpg, up_tpg;
+  int tpg, pipe, gather_tpt, carveout, pow2, stages, async_tpg, up_tpg, tma_tpg, tma_stages;
   LaunchKnobs();
 };
 LaunchKnobs& knobs();

@@ -234,12 +234,15 @@ static int env_int(const char* name, int dflt) {
 // Launch configuration knobs (env, read once): LL_TPG = target tiles per tile
 // group (0 = persistent grid at full occupancy), LL_PIPE = 1 for the
 // software-pipelined kernel, LL_UP_TPG = tiles per group of the mxfp4 upcast
-// kernel (default 0: persistent; sweep 4.78 vs 4.46 TB/s at 2).
+// kernel (default 0: persistent; sweep 4.78 vs 4.46 TB/s at 2), LL_TMA_TPG /
+// LL_TMA_STAGES = tiles per group (0: persistent, -1: by wave count) and ring
+// depth of the TMA path.
 LaunchKnobs::LaunchKnobs()
       : tpg(env_int("LL_TPG", 2)), pipe(env_int("LL_PIPE", 1)),
         gather_tpt(env_int("LL_GATHER_VPT", 0)), carveout(env_int("LL_CARVEOUT", -1)),
         pow2(env_int("LL_POW2", 0)), stages(env_int("LL_STAGES", 3)),
-        async_tpg(env_int("LL_ASYNC_TPG", 8)), up_tpg(env_int("LL_UP_TPG", 0)) {}
+        async_tpg(env_int("LL_ASYNC_TPG", 8)), up_tpg(env_int("LL_UP_TPG", 0)),
+        tma_tpg(env_int("LL_TMA_TPG", -1)), tma_stages(env_int("LL_TMA_STAGES", 3)) {}
 LaunchKnobs& knobs() {
   static LaunchKnobs k;
   return k;
@@ -255,6 +258,8 @@ int set_knob(const char* name, int value) {
   if (n == "stages") { knobs().stages = value; return 0; }
   if (n == "async_tpg") { knobs().async_tpg = value; return 0; }
   if (n == "up_tpg") { knobs().up_tpg = value; return 0; }
+  if (n == "tma_tpg") { knobs().tma_tpg = value; return 0; }
+  if (n == "tma_stages") { knobs().tma_stages = value; return 0; }
   return -1;
 }
 

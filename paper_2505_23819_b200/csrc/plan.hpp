@@ -102,6 +102,22 @@ struct ShufflePlan {
   uint8_t gamma[LL_MAX_GRAN];                          // per round: xor into the source lane
 };
 
+// TMA-fed smem path (LL_PATH_SMEM_TMA): the source tile is one box of a
+// <= 5-D tensor view of the source buffer whose dims are runs of source index
+// bits (dim i = element bits [shift[i], shift[i] + size_bits[i]), box =
+// the low box_bits[i] of them; the top dim also carries the batch).  The box
+// lands in shared memory densely (tile bits in ascending source order) and
+// permuted by the hardware swizzle `swizzle` (0 none, 1/2/3 = 32/64/128 B:
+// byte-address bits [4, 4+m) ^= bits [7, 7+m)).  The reader side reuses the
+// SmemPlan fields (sr_thr / sr_gran / swaps / st_*).
+struct TmaDesc {
+  int32_t ndim;
+  int32_t swizzle;
+  int32_t shift[5];
+  int32_t box_bits[5];
+  int32_t size_bits[5];   // top dim: ignored (computed from the launch range)
+};
+
 // A contiguous range of tile indices [t0, t1) of a smem / shuffle plan, with
 // the byte offsets of the caller's slices (multi-GPU shards: each rank holds
 // only its slice of src and dst).

@@ -145,7 +145,8 @@ int planner_knob_version() {
 bool set_planner_knob(const std::string& name, int value) {
   if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule" &&
       name != "run_bytes" && name != "tile_order" && name != "host_chunk_mb" &&
-      name != "host_slots")
+      name != "host_slots" && name != "tma_run_bytes" && name != "tma_thread_bytes" &&
+      name != "tma_tile_bytes" && name != "tma_force_swizzle")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -953,6 +954,290 @@ bool plan_async(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& j
   return true;
 }
 
+// TMA-fed variant of the shared-memory path (LL_PATH_SMEM_TMA).  The source
+// tile is fetched by one cp.async.bulk.tensor per tile into a dense image
+// (tile bits in ascending source order) permuted by a hardware swizzle mode
+// m in {none, 32 B, 64 B, 128 B}: byte-address bits [4, 4+m) ^= [7, 7+m).
+// That map is Def. 5 with vec = 16 bytes, per_phase = 1 and
+// max_phase = 2^m on rows of 16 << m bytes (tests: test_oracle_swizzle.py),
+// i.e. a fixed member of the family the paper's construction searches; the
+// planner therefore cannot choose S, but chooses (a) the mode and (b) the
+// reader's lanes so that the reader's 16-byte granules are conflict-free
+// under it (wavefronts = 4 * 2^(rank(phase cols) - rank(bank projection)),
+// the lemma P:1083-1089 for 16-byte granules), and among conflict-free
+// choices the one with the longest coalesced destination runs.  The reader
+// holds VS u VD in registers and permutes into destination vectors exactly
+// as the cp.async path does.
+bool plan_tma(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js) {
+  const int n = P.nB, w = P.w;
+  if (P.nA != P.nB || n > 62 || w > 8) return false;
+  std::vector<int> sigma(n), sinv(n, -1);
+  for (int k = 0; k < n; ++k) {
+    if (popcount64(X[k]) != 1) return false;
+    sigma[k] = ctz64(X[k]);
+    if (sinv[sigma[k]] >= 0) return false;
+    sinv[sigma[k]] = k;
+  }
+  const int vb = ilog2i(16 / w);
+  const int lw = ilog2i(w);
+  if (n < vb + 5) return false;
+  auto contains = [](const std::vector<int>& v, int x) {
+    return std::find(v.begin(), v.end(), x) != v.end();
+  };
+  std::vector<int> VD, VS, CD, CS;
+  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
+  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("tma_run_bytes", 256)) / 16));
+  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
+  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
+  const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("tma_thread_bytes", 64)) / w));
+  std::vector<int> need = VS;
+  for (int x : VD) if (!contains(need, x)) need.push_back(x);
+  if ((int)need.size() > r_max || (int)need.size() + 5 > n) return false;
+  int r = std::min(std::max((int)need.size(), r_pref), std::min(r_max, n - 5));
+  // tile: the vectors and coalescing runs of both sides, then the lowest
+  // destination bits; at least tma_tile_bytes (several KB in flight per TMA)
+  const int tile_min = ilog2i(std::max(1024, planner_knob("tma_tile_bytes", 8192)) / w);
+  std::vector<int> T = VD;
+  for (auto* s : {&VS, &CD, &CS, &need})
+    for (int x : *s) if (!contains(T, x)) T.push_back(x);
+  for (int k = 0; (int)T.size() < std::max(r + 5, std::min(n, tile_min)) && k < n; ++k)
+    if (!contains(T, k)) T.push_back(k);
+  int g = (int)T.size() - r - 5;
+  if (g > 3) {
+    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
+    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
+  }
+  if (g < 0 || g > 3) return false;
+  std::sort(T.begin(), T.end());
+  const int d = (int)T.size();
+  // dense image: rank of the source bit among the tile's source bits
+  std::vector<int> Ts;
+  for (int k : T) Ts.push_back(sigma[k]);
+  std::sort(Ts.begin(), Ts.end());
+  auto dense = [&](int k) -> uint32_t {
+    return uint32_t(w) << (std::find(Ts.begin(), Ts.end(), sigma[k]) - Ts.begin());
+  };
+  for (int k : T)
+    if (sigma[k] + lw >= 40 || d + lw > 20) return false;
+  // reader registers: VS (granule order), VD \ VS, extra (highest dst, not CD)
+  std::vector<int> rd_reg = VS;
+  for (int x : VD) if (!contains(rd_reg, x)) rd_reg.push_back(x);
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(rd_reg, x) && !contains(CD, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [](int a, int b) { return a > b; });
+    for (int x : cand) { if ((int)rd_reg.size() == r) break; rd_reg.push_back(x); }
+    if ((int)rd_reg.size() != r) return false;
+  }
+  // TMA box dims for swizzle mode m: runs of consecutive source bits; the
+  // first run is split at the swizzle span (16 << m bytes), every box dim is
+  // at most 256 elements; <= 5 dims
+  auto make_desc = [&](int m, TmaDesc& td) -> bool {
+    td = TmaDesc{};
+    td.swizzle = m;
+    std::vector<std::pair<int, int>> runs;  // (first source bit, length)
+    for (int b : Ts) {
+      if (!runs.empty() && runs.back().first + runs.back().second == b) ++runs.back().second;
+      else runs.push_back({b, 1});
+    }
+    if (runs.empty() || runs[0].first != 0) return false;
+    const int span_bits = m ? ilog2i((16 << m) / w) : 8;
+    std::vector<std::pair<int, int>> dims;  // (shift, box bits)
+    for (size_t i = 0; i < runs.size(); ++i) {
+      int a = runs[i].first, len = runs[i].second;
+      if (i == 0 && m) {
+        if (len < span_bits) return false;
+        dims.push_back({a, span_bits});
+        a += span_bits;
+        len -= span_bits;
+      }
+      while (len > 0) {
+        const int piece = std::min(len, 8);
+        dims.push_back({a, piece});
+        a += piece;
+        len -= piece;
+      }
+    }
+    if (dims.size() > 5) return false;
+    if (!m && dims[0].second > 8) return false;
+    td.ndim = (int)dims.size();
+    for (int i = 0; i < td.ndim; ++i) {
+      td.shift[i] = dims[i].first;
+      td.box_bits[i] = dims[i].second;
+      td.size_bits[i] = i + 1 < td.ndim ? dims[i + 1].first - dims[i].first : 0;
+      if (i > 0 && (dims[i].first + lw) < 4) return false;  // strides: multiples of 16 B
+    }
+    return true;
+  };
+  auto swz = [](uint32_t a, int m) -> uint32_t {
+    return m ? a ^ (((a >> 7) & ((1u << m) - 1)) << 4) : a;
+  };
+  struct Choice {
+    int m = -1, wf = 1 << 30, run = -1;
+    std::vector<int> lane, warp;
+    TmaDesc td{};
+  } best;
+  const int force = planner_knob("tma_force_swizzle", -1);
+  for (int m = 0; m <= 3; ++m) {
+    if (force >= 0 && m != force) continue;
+    Choice c;
+    c.m = m;
+    if (!make_desc(m, c.td)) continue;
+    auto addr = [&](int k) { return swz(dense(k), m); };
+    std::vector<int> cand;
+    for (int x : T) if (!contains(rd_reg, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end());
+    // phase lanes (lane bits 0-2 of a 16-byte access): independent bank
+    // projections (address bits 4-6), lowest destination bits first
+    std::vector<int> phase;
+    std::vector<u64> proj;
+    for (int x : cand) {
+      if (phase.size() == 3) break;
+      std::vector<u64> p2 = proj;
+      p2.push_back((addr(x) >> 4) & 7u);
+      if (f2_rank(p2) > f2_rank(proj)) { phase.push_back(x); proj = p2; }
+    }
+    for (int x : cand) {
+      if (phase.size() == 3) break;
+      if (!contains(phase, x)) phase.push_back(x);
+    }
+    c.lane = phase;
+    for (int x : cand) {
+      if (c.lane.size() == 5) break;
+      if (!contains(c.lane, x)) c.lane.push_back(x);
+    }
+    for (int x : cand) if (!contains(c.lane, x)) c.warp.push_back(x);
+    std::vector<u64> pc, pp;
+    for (int i = 0; i < 3; ++i) {
+      pc.push_back(addr(c.lane[i]));
+      pp.push_back((addr(c.lane[i]) >> 4) & 7u);
+    }
+    c.wf = 4 << (f2_rank(pc) - f2_rank(pp));
+    // destination run of one store instruction: 16 B x 2^(lane bits that
+    // extend the vector contiguously, in lane order)
+    std::vector<int> sl = c.lane;
+    int run = 0;
+    for (int q = 0;; ++q) {
+      if (!contains(sl, vb + q)) break;
+      ++run;
+    }
+    c.run = run;
+    if (c.wf < best.wf || (c.wf == best.wf && c.run > best.run)) best = c;
+  }
+  if (best.m < 0 || (int)best.warp.size() != g) return false;
+  const int m = best.m;
+  std::vector<int> rd_lane = best.lane, rd_warp = best.warp;
+  // reader sub-word swaps / store selection: as in plan_async
+  const int nsub = w >= 4 ? 0 : ilog2i(4 / w);
+  std::vector<int> order = rd_reg;
+  std::vector<std::pair<int, int>> swaps;
+  for (int t = 0; t < nsub; ++t) {
+    int s = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
+    if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
+  }
+  if ((int)swaps.size() > LL_MAX_SWAPS) return false;
+  auto wordbit = [&](int rho) { return w == 8 ? rho + 1 : rho - nsub; };
+  const int LB = w == 8 ? r + 1 : r - nsub;
+  std::vector<int> ssel;
+  if (w == 8) ssel.push_back(0);
+  for (int t = (w == 8 ? 0 : nsub); t < vb; ++t) {
+    int pos = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
+    ssel.push_back(wordbit(pos));
+  }
+  if (ssel.size() != 2) return false;
+  std::vector<int> rest_rho;
+  for (int wb = 0; wb < LB; ++wb) {
+    if (std::find(ssel.begin(), ssel.end(), wb) != ssel.end()) continue;
+    rest_rho.push_back(w == 8 ? wb - 1 : wb + nsub);
+  }
+  auto boff = [&](int k) -> uint32_t { return swz(dense(k), m); };
+  SmemPlan& sp = P.sp;
+  sp = SmemPlan{};
+  sp.gw = g;
+  sp.tile_bytes = w << d;
+  sp.n_swaps = (int)swaps.size();
+  for (size_t i = 0; i < swaps.size(); ++i) {
+    sp.swap_a[i] = (int8_t)swaps[i].first;
+    sp.swap_b[i] = (int8_t)swaps[i].second;
+  }
+  sp.gsel_a = (int8_t)ssel[0];
+  sp.gsel_b = (int8_t)ssel[1];
+  for (int b = 0; b < 5 + g; ++b) {
+    const int k = b < 5 ? rd_lane[b] : rd_warp[b - 5];
+    sp.st_thr[b] = uint32_t(w) << k;
+    sp.sr_thr[b] = boff(k);
+  }
+  const int nvec = 1 << (r - vb);
+  if (nvec > LL_MAX_VEC || nvec > LL_MAX_GRAN) return false;
+  for (int u = 0; u < nvec; ++u) {
+    uint32_t ro = 0, so = 0;
+    for (int q = 0; q < r - vb; ++q) {
+      if ((u >> q) & 1) {
+        ro ^= boff(rd_reg[vb + q]);
+        so += uint32_t(w) << order[rest_rho[q]];
+      }
+    }
+    sp.sr_gran[u] = ro;
+    sp.st_vec[u] = so;
+  }
+  std::vector<int> O;
+  for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
+  if ((int)O.size() > LL_MAX_OUTER) return false;
+  TileMap& tm = sp.tile;
+  tm.n_bits = (int)O.size();
+  tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
+  for (int k = 0; k < tm.n_tab; ++k)
+    for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
+      int64_t so = 0, dof = 0;
+      for (int q = 0; q < LL_TAB_BITS; ++q) {
+        const int bit = k * LL_TAB_BITS + q;
+        if (((v >> q) & 1) && bit < tm.n_bits) {
+          so += int64_t(w) << sigma[O[bit]];
+          dof += int64_t(w) << O[bit];
+        }
+      }
+      tm.tab[k][v].src = so;
+      tm.tab[k][v].dst = dof;
+    }
+  tm.batch_stride_src = int64_t(w) << P.nA;
+  tm.batch_stride_dst = int64_t(w) << P.nB;
+  tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
+  P.tile_bit_src.clear();
+  P.tile_bit_dst.clear();
+  for (int q = 0; q < tm.n_bits; ++q) {
+    P.tile_bit_src.push_back(sigma[O[q]]);
+    P.tile_bit_dst.push_back(O[q]);
+  }
+  P.td = best.td;
+  P.nv = nvec;
+  P.g = 16;
+  P.tile_bits = d;
+  P.r = r;
+  P.gw = g;
+  P.pred_wf_ld = 0;  // the TMA write has no bank conflicts to predict
+  P.pred_wf_st = best.wf;
+  std::vector<int> shifts, boxes;
+  for (int i = 0; i < P.td.ndim; ++i) {
+    shifts.push_back(P.td.shift[i]);
+    boxes.push_back(P.td.box_bits[i]);
+  }
+  static const char* mode_names[] = {"none", "32B", "64B", "128B"};
+  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
+     << ",\"granule_bytes\":16,\"granule_dst_bits\":" << ivec_json(VS)
+     << ",\"vectors_per_thread\":" << nvec << ",\"swaps\":[";
+  for (size_t i = 0; i < swaps.size(); ++i)
+    js << (i ? "," : "") << "[" << swaps[i].first << "," << swaps[i].second << "]";
+  js << "],\"stg_sel\":" << ivec_json(ssel) << ",\"rd_reg\":" << ivec_json(rd_reg)
+     << ",\"rd_rho_after_swaps\":" << ivec_json(order) << ",\"rd_lane\":" << ivec_json(rd_lane)
+     << ",\"rd_warp\":" << ivec_json(rd_warp) << ",\"tma\":{\"swizzle\":\"" << mode_names[m]
+     << "\",\"ndim\":" << P.td.ndim << ",\"dim_src_shift\":" << ivec_json(shifts)
+     << ",\"box_bits\":" << ivec_json(boxes) << ",\"store_run_bytes\":" << (16 << best.run)
+     << "},\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"n_tiles\":" << tm.n_tiles
+     << ",\"smem_bytes\":{\"sr_thr\":" << u32_json(sp.sr_thr, 5 + g)
+     << ",\"sr_gran\":" << u32_json(sp.sr_gran, nvec) << "}";
+  return true;
+}
+
 std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B, int w,
                                                 int path_req, int64_t batch, int op) {
   if (!A.same_tensor(B)) throw Error(LL_ERR_SHAPE, "convert: source and destination layouts map to different tensors");
@@ -1010,12 +1295,21 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
       throw Error(LL_ERR_UNSUPPORTED, "smem_async path requested but the quotient is not a tileable bit permutation");
     }
   }
+  if (path == LL_PATH_SMEM_TMA) {
+    std::ostringstream js2;
+    if (plan_tma(*P, X, js2)) {
+      js << js2.str();
+    } else {
+      throw Error(LL_ERR_UNSUPPORTED, "smem_tma path requested but the quotient is not a tileable "
+                                      "bit permutation or the source tile needs more than 5 TMA box dims");
+    }
+  }
   if (op == 1 && path != LL_PATH_SMEM)
     throw Error(LL_ERR_UNSUPPORTED, "mxfp4 upcast: the layouts are not a tileable bit permutation");
   if (path == LL_PATH_GENERIC) fill_generic(*P, X);
   P->path = path;
   static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle",
-                                "smem_async", "smem_padded"};
+                                "smem_async", "smem_padded", "smem_tma"};
   js << ",\"path\":\"" << names[path] << "\"}";
   P->json = js.str();
   return P;
@@ -1093,7 +1387,7 @@ TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
     return rg;
   }
   if (P.path != LL_PATH_SMEM && P.path != LL_PATH_SHUFFLE && P.path != LL_PATH_SMEM_NOSWIZZLE &&
-      P.path != LL_PATH_SMEM_ASYNC && P.path != LL_PATH_SMEM_PADDED)
+      P.path != LL_PATH_SMEM_ASYNC && P.path != LL_PATH_SMEM_PADDED && P.path != LL_PATH_SMEM_TMA)
     throw Error(LL_ERR_UNSUPPORTED, "shard: only tiled (smem / shuffle) plans are shardable");
   const int nb = (int)P.tile_bit_src.size();
   if (sb > nb) throw Error(LL_ERR_UNSUPPORTED, "shard: more shards than tiles");

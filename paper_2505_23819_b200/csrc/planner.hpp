@@ -40,6 +40,7 @@ struct ConvertPlan {
   std::vector<u64> dst_cols;
   // smem path
   SmemPlan sp{};
+  TmaDesc td{};      // LL_PATH_SMEM_TMA
   int nv = 0, g = 0;
   int tile_bits = 0, r = 0, gw = 0;
   int pred_wf_ld = 0, pred_wf_st = 0;   // wavefronts per STS / LDS instruction

@@ -72,13 +72,13 @@ CASES = [
 
 
 @pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "smem_padded", "shuffle",
-                                  "smem_async", "generic"])
+                                  "smem_async", "smem_tma", "generic"])
 @pytest.mark.parametrize("name,mk", CASES)
 def test_convert_configs_small(name, mk, path):
     c = mk()
     if path == "shuffle" and name.startswith("cfg3"):
         pytest.skip("transpose exchange is not warp-local (P:624); covered by test_shuffle_rejects")
-    if path == "smem_async" and name.startswith("cfg1"):
+    if path in ("smem_async", "smem_tma") and name.startswith("cfg1"):
         pytest.skip("16x16 tensor is smaller than one async tile")
     src, dst = run_convert(c, path=path)
     exp = expect_convert(c, src)
@@ -165,6 +165,56 @@ def test_convert_async_ragged_batch(batch):
     assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
 
 
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_random_pairs_tma(w):
+    """TMA-fed path: random bit-permutation pairs (box dims, swizzle modes and
+    reader lanes all chosen by the planner) against the oracle."""
+    rng = random.Random(700 + w)
+    done, tried = 0, 0
+    modes = set()
+    while done < 12 and tried < 200:
+        tried += 1
+        d = rng.randint(12, 17)
+        c = rand_pair(rng, d, w)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        try:
+            plan = ll.plan_describe(A, B, 8 * w, "smem_tma")
+        except ll.LLError:
+            continue
+        modes.add(plan["tma"]["swizzle"])
+        src, dst = run_convert(c, path="smem_tma", seed=rng.randint(0, 1000))
+        assert dst.tobytes() == expect_convert(c, src).tobytes(), plan["tma"]
+        done += 1
+    assert done >= 6, (done, tried)
+
+
+@pytest.mark.parametrize("swz", [0, 1, 2, 3])
+def test_convert_tma_each_swizzle_mode(swz):
+    """Every hardware swizzle mode (the Def. 5 instances) executed on the
+    device: the planner is pinned to one mode and must stay byte-exact."""
+    ll.tune("tma_force_swizzle", swz)
+    try:
+        for c in (configs.cfg5(m_bits=9, kb_bits=9), configs.cfg3(n_bits=9),
+                  configs.cfg2(batch_bits=2)):
+            A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+            try:
+                plan = ll.plan_describe(A, B, 8 * c["elem_bytes"], "smem_tma")
+            except ll.LLError:
+                continue
+            assert plan["tma"]["swizzle"] == ["none", "32B", "64B", "128B"][swz]
+            src, dst = run_convert(c, path="smem_tma", seed=40 + swz)
+            assert dst.tobytes() == expect_convert(c, src).tobytes()
+    finally:
+        ll.tune("tma_force_swizzle", -1)
+
+
+@pytest.mark.parametrize("batch", [3, 37])
+def test_convert_tma_ragged_batch(batch):
+    c = configs.cfg2(batch_bits=0)
+    src, dst = run_convert(c, path="smem_tma", batch=batch, seed=19)
+    assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
+
+
 @pytest.mark.parametrize("batch", [3, 37])
 def test_convert_shuffle_ragged_batch(batch):
     c = configs.cfg2(batch_bits=0)
@@ -175,7 +225,8 @@ def test_convert_shuffle_ragged_batch(batch):
 @pytest.mark.parametrize("name,mk,shards", [("cfg5", lambda: configs.cfg5(m_bits=10, kb_bits=8), 8),
                                             ("cfg2", lambda: configs.cfg2(batch_bits=3), 4),
                                             ("cfg2s", lambda: configs.cfg2(batch_bits=3), 2)])
-def test_convert_shards_equal_full(name, mk, shards):
+@pytest.mark.parametrize("path", ["auto", "smem_tma"])
+def test_convert_shards_equal_full(name, mk, shards, path):
     """Each rank's shard converted from its own slices (separate allocations,
     SURVEY 8(e)) reassembles the oracle's full conversion."""
     c = mk()
@@ -185,10 +236,10 @@ def test_convert_shards_equal_full(name, mk, shards):
     src = values_torch(n, 29, w, "cuda")
     parts = []
     for r in range(shards):
-        s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, shards, r)
+        s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, shards, r, path)
         sl = src.view(torch.uint8)[s0:s1].clone()          # this rank's memory only
         dl = torch.empty(d1 - d0, dtype=torch.uint8, device="cuda")
-        ll.convert_shard(sl, A, dl, B, 8 * w, shards, r)
+        ll.convert_shard(sl, A, dl, B, 8 * w, shards, r, path=path)
         parts.append(dl)
     torch.cuda.synchronize()
     got = torch.cat(parts).cpu().numpy().view(_NP[w])
@@ -228,14 +279,15 @@ def sampled_expected(c, src_np, h):
 @pytest.mark.parametrize("name,mk", [("cfg2", lambda: configs.cfg2()),
                                      ("cfg3", lambda: configs.cfg3()),
                                      ("cfg5", lambda: configs.cfg5(m_bits=15, kb_bits=14))])
-def test_convert_full_size_sampled(name, mk):
+@pytest.mark.parametrize("path", ["auto", "smem_tma"])
+def test_convert_full_size_sampled(name, mk, path):
     c = mk()
     w = c["elem_bytes"]
     A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
     n = 1 << A.in_bits
     src = values_torch(n, 17, w, "cuda")
     dst = torch.empty_like(src)
-    ll.convert(src, A, dst, B, 8 * w)
+    ll.convert(src, A, dst, B, 8 * w, path=path)
     torch.cuda.synchronize()
     # property at any size: dst is a permutation of src
     key = (lambda t: t.view(torch.int16).to(torch.int32)) if w == 2 else \
@@ -405,7 +457,13 @@ def test_fp8_transpose_paths(mb, nb):
     staging layouts agree with the oracle."""
     c = configs.cfg3(n_bits=nb, m_bits=mb)
     c = dict(c, elem_bytes=1)
-    for path in ("smem", "smem_padded", "smem_noswizzle"):
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    for path in ("smem", "smem_padded", "smem_noswizzle", "smem_tma"):
+        if path == "smem_tma":
+            try:   # fp8 transposes need 16x16 elements (256 B) per reader thread
+                ll.plan_describe(A, B, 8, path)
+            except ll.LLError:
+                continue
         src, dst = run_convert(c, path=path, seed=mb * 31 + nb)
         assert dst.tobytes() == expect_convert(c, src).tobytes(), path
 

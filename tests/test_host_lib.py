@@ -270,3 +270,71 @@ def test_broadcast_plans_stay_tiled():
         X = d["X"]
         zd = [k for k, x in enumerate(X) if x == 0]
         assert len(zd) == 2 and d["tile_order_dst_bits"][:2] == zd
+
+
+def _reader_wavefronts(d):
+    """Brute force over the TMA plan's reader: every (warp, granule) LDS.128
+    instruction, lane addresses from the plan's per-thread-bit / per-granule
+    byte offsets (XOR-linear), quarter-warp phases, max over banks of distinct
+    4-byte words (the bank model of oracle.banks, reading A18)."""
+    thr, gran = d["smem_bytes"]["sr_thr"], d["smem_bytes"]["sr_gran"]
+    nthr = len(thr)
+    total, n_instr = 0, 0
+    for wv in range(1 << (nthr - 5)):
+        for gj in gran:
+            addrs = []
+            for l in range(32):
+                t = l | (wv << 5)
+                a = gj
+                for b in range(nthr):
+                    if (t >> b) & 1:
+                        a ^= thr[b]
+                addrs.append(a)
+            for p0 in range(0, 32, 8):
+                banks_ = {}
+                for a in addrs[p0:p0 + 8]:
+                    assert a % 16 == 0
+                    for wd in range(a // 4, a // 4 + 4):
+                        banks_.setdefault(wd % 32, set()).add(wd)
+                total += max(len(s) for s in banks_.values())
+            n_instr += 1
+    return total, n_instr
+
+
+@pytest.mark.parametrize("name,c", PLAN_CASES[2:])
+def test_tma_plan_reader_conflict_free(name, c):
+    """TMA-fed path: the hardware swizzle is fixed (a Def. 5 instance), so the
+    planner picks the mode and the reader's lanes; brute force confirms the
+    reads cost the ideal 4 wavefronts per 16-byte LDS, and the source tile is
+    one TMA box of <= 5 dims whose inner extent fits the swizzle span."""
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    w = c["elem_bytes"]
+    d = ll.plan_describe(A, B, 8 * w, "smem_tma")
+    assert d["path"] == "smem_tma"
+    t = d["tma"]
+    assert 1 <= t["ndim"] <= 5 and t["dim_src_shift"][0] == 0
+    span = {"none": None, "32B": 32, "64B": 64, "128B": 128}[t["swizzle"]]
+    if span:
+        assert (w << t["box_bits"][0]) == span
+    assert all(b <= 8 for b in t["box_bits"])
+    assert sum(t["box_bits"]) == len(d["tile_dst_bits"])
+    total, n_instr = _reader_wavefronts(d)
+    assert total == 4 * n_instr == d["pred_wavefronts_per_lds"] * n_instr
+
+
+def test_tma_plan_needs_swizzle_for_cfg5():
+    """cfg5's reader cannot be conflict-free on the unswizzled image (2-way,
+    predicted and brute-forced), and is under the 128-byte mode the planner
+    picks -- the TMA counterpart of the paper's swizzling argument."""
+    c = configs.cfg5(m_bits=9, kb_bits=9)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    try:
+        ll.tune("tma_force_swizzle", 0)
+        d0 = ll.plan_describe(A, B, 8, "smem_tma")
+    finally:
+        ll.tune("tma_force_swizzle", -1)
+    d = ll.plan_describe(A, B, 8, "smem_tma")
+    assert d0["pred_wavefronts_per_lds"] == 8
+    tot0, n0 = _reader_wavefronts(d0)
+    assert tot0 == 8 * n0
+    assert d["tma"]["swizzle"] == "128B" and d["pred_wavefronts_per_lds"] == 4

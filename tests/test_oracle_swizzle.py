@@ -254,3 +254,34 @@ def test_shuffle_plan_preconditions():
                {"reg": [(4,)], "lane": [(2,)], "warp": [(1,)]})
     with pytest.raises(ValueError):
         shuffle.shuffle_plan(A, B, 4)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+@pytest.mark.parametrize("w", [1, 2, 4])
+def test_tma_swizzle_modes_are_def5_instances(m, w):
+    """The TMA tensor-copy swizzle modes (32/64/128 B: 16-byte chunk bits
+    [4, 4+m) of the shared-memory byte address XOR-ed with bits [7, 7+m), the
+    CUDA programming guide's pattern, written out here) place every element
+    exactly where Def. 5 puts it with vec = 16 bytes,
+    per_phase = 128 / row bytes and max_phase = row bytes / 16, rows of 16 << m
+    bytes.  This is what lets the TMA-fed path (LL_PATH_SMEM_TMA) reason about
+    the hardware's image with the paper's machinery."""
+    from oracle.constructors import mma_swizzle_layout, mma_swizzle_offset
+    row_bytes = 16 << m
+    n = (row_bytes // w).bit_length() - 1          # column bits per row
+    rows = 32
+    vec, per_phase, max_phase = 16 // w, 128 // row_bytes, row_bytes // 16
+    mask = (1 << m) - 1
+    for i in range(rows):
+        for j in range(1 << n):
+            a = i * row_bytes + j * w                 # dense (unswizzled) byte address
+            hw = a ^ (((a >> 7) & mask) << 4)          # hardware swizzle
+            assert hw % w == 0
+            assert hw // w == mma_swizzle_offset(i, j, n, vec, per_phase, max_phase), (i, j)
+    # and the matrix form printed after Def. 5 maps each hardware offset back
+    L = mma_swizzle_layout(5, n, vec, per_phase, max_phase)
+    for i in range(rows):
+        for j in range(1 << n):
+            a = i * row_bytes + j * w
+            hw = (a ^ (((a >> 7) & mask) << 4)) // w
+            assert L.apply_flat(hw) == (i << n) | j
