@@ -465,6 +465,7 @@ def main():
         kernel = {"smem": "convert_smem_kernel", "generic": "convert_generic_kernel",
                   "smem_noswizzle": "convert_smem_kernel", "smem_padded": "convert_smem_kernel",
                   "smem_async": "convert_async_kernel", "smem_tma": "convert_tma_kernel",
+                  "regs": "convert_regs_kernel",
                   "copy": "cudaMemcpyAsync", "shuffle": "gather_shuffle_kernel",
                   "direct": "gather_direct_kernel"}.get(plan.get("path"), plan.get("path"))
         line = {

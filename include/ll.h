@@ -104,6 +104,15 @@ ll_status ll_invert(ll_layout l, ll_layout* out);
  * for a shared label a's bits are low, b's high. */
 ll_status ll_product(ll_layout a, ll_layout b, ll_layout* out);
 
+/* Left division (Definition "Left Division"): m = [[m1, 0], [0, m2]]
+ * label-wise (for every input label, m's first in_size(m1) bits are m1's
+ * columns embedded at the low bits of each output dim, and m's other bits
+ * have a zero m1 block); *out = m2 = the remaining columns with m1's output
+ * bits removed.  Used to decide whether an instruction tile T (vectorised
+ * ld/st.shared, ldmatrix/stmatrix) can lower a layout.  Caller
+ * owns *out.  LL_ERR_SHAPE when m is not divisible by m1. */
+ll_status ll_left_divide(ll_layout m, ll_layout m1, ll_layout* out);
+
 /* Shape-operation transfer functions (Appendix theorem):
  * for an input layout, the output layout for which the shape operation moves
  * no data between hardware indices (every hardware index keeps its value).
@@ -170,11 +179,18 @@ typedef enum {
   LL_PATH_SMEM_NOSWIZZLE = 5, /* smem path with an unswizzled staging buffer (ablation) */
   LL_PATH_SMEM_ASYNC = 6, /* smem path fed by cp.async (source granules, multi-stage)  */
   LL_PATH_SMEM_PADDED = 7, /* legacy heuristic: unswizzled staging + 16 B pad per 128 B (ablation) */
-  LL_PATH_SMEM_TMA = 8   /* smem path fed by TMA tensor loads (cp.async.bulk.tensor) into a
+  LL_PATH_SMEM_TMA = 8,  /* smem path fed by TMA tensor loads (cp.async.bulk.tensor) into a
                             hardware-swizzled image: the 32/64/128-byte swizzle modes are
                             Def. 5 instances; the planner picks the mode and the
                             reader's lanes so the reads are conflict-free.
                             LL_ERR_UNSUPPORTED when the source tile needs > 5 box dims. */
+  LL_PATH_REGS = 9       /* register-faithful: threads are the layouts' own lanes / warps (one
+                            CTA per block index, each thread's registers contiguous in the
+                            buffers), exchange registers -> smem (optimal swizzle) -> registers
+                            with stmatrix / ldmatrix where the layout is divisible by their tile
+                            (P:588-591), else vectorised st/ld.shared.  Needs reg/lane/warp/block
+                            layouts with equal lane (5) and warp (<= 3) bits, identical block
+                            columns and elements of <= 4 bytes; else LL_ERR_UNSUPPORTED. */
 } ll_path;
 
 typedef struct {
@@ -209,6 +225,18 @@ ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout
 ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_t* scales,
                           void* dst_bf16, ll_layout dst_layout, const ll_convert_options* opts,
                           ll_stream stream);
+
+/* Register-faithful conversion (LL_PATH_REGS) with in-kernel timing: as
+ * ll_convert_ex with path LL_PATH_REGS and `batch`, but the register -> smem
+ * -> register exchange is repeated `reps` (>= 1) times inside the kernel and
+ * thread 0 of CTA c writes the clock64 cycles of the repeated section to
+ * cycles[c] (device buffer of >= min(n_tiles, grid) entries, or NULL), the
+ * paper's in-kernel view of a conversion (microbenchmarks: one CTA).
+ * dst receives the conversion (identical for every reps).  Errors as
+ * ll_convert_ex; LL_ERR_UNSUPPORTED if the layouts are not regs-compatible. */
+ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst,
+                                ll_layout dst_layout, int elem_bits, int64_t batch, int reps,
+                                long long* cycles, ll_stream stream);
 
 /* Multi-GPU shard: convert only shard `shard` of `n_shards`
  * (a power of two).  The tensor is split along the top log2(n_shards) index

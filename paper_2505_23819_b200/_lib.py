@@ -73,7 +73,10 @@ _lib.ll_convert_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_voi
                                   ctypes.c_void_p, ctypes.c_void_p]
 _lib.ll_shard_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
-for _f in ("ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+_lib.ll_left_divide.argtypes = [_VP, _VP, ctypes.POINTER(_VP)]
+_lib.ll_convert_regs_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int64,
+                                       ctypes.c_int, _VP, _VP]
+for _f in ("ll_left_divide", "ll_convert_regs_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
@@ -84,7 +87,8 @@ STATUS = {0: "LL_OK", 1: "LL_ERR_ARG", 2: "LL_ERR_SHAPE", 3: "LL_ERR_LABEL",
           4: "LL_ERR_NOT_SURJECTIVE", 5: "LL_ERR_NOT_INVERTIBLE", 6: "LL_ERR_RANGE",
           7: "LL_ERR_UNSUPPORTED", 8: "LL_ERR_CUDA", 9: "LL_ERR_OOM"}
 PATHS = {"auto": 0, "copy": 1, "smem": 2, "shuffle": 3, "generic": 4, "smem_noswizzle": 5,
-         "smem_async": 6, "smem_padded": 7, "smem_tma": 8}
+         "smem_async": 6, "smem_padded": 7, "smem_tma": 8,
+         "regs": 9}
 
 
 class LLError(RuntimeError):
@@ -221,6 +225,13 @@ def product(a, b):
     return _wrap(h)
 
 
+def left_divide(m, m1):
+    """ll_left_divide (P:354-365): m2 with m = [[m1, 0], [0, m2]] label-wise."""
+    h = ctypes.c_void_p()
+    _check(_lib.ll_left_divide(m.handle, m1.handle, ctypes.byref(h)))
+    return _wrap(h)
+
+
 def transpose(layout, perm):
     """ll_transpose: tt.trans transfer function."""
     h = ctypes.c_void_p()
@@ -289,6 +300,16 @@ def convert(src, A, dst, B, elem_bits, path="auto", batch=1, max_ctas=0, stream=
     o = _opts(path, batch, max_ctas)
     _check(_lib.ll_convert_ex(_ptr(src), A.handle, _ptr(dst), B.handle, int(elem_bits),
                               ctypes.byref(o), _stream_handle(stream)))
+
+
+def convert_regs_timed(src, A, dst, B, elem_bits, reps=1, cycles=None, batch=1, stream=None):
+    """ll_convert_regs_timed: register-faithful conversion, the exchange
+    repeated `reps` times in-kernel; per-CTA clock64 cycles into `cycles`
+    (an int64 device tensor) when given."""
+    _check(_lib.ll_convert_regs_timed(_ptr(src), A.handle, _ptr(dst), B.handle, int(elem_bits),
+                                      int(batch), int(reps),
+                                      _ptr(cycles) if cycles is not None else None,
+                                      _stream_handle(stream)))
 
 
 def convert_shard(src_slice, A, dst_slice, B, elem_bits, n_shards, shard, path="auto",

@@ -20,7 +20,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["kernel_smem.cu", "kernel_async.cu", "kernel_tma.cu", "kernel_shuffle.cu", "kernel_misc.cu"]
+CU_SOURCES = ["kernel_smem.cu", "kernel_async.cu", "kernel_tma.cu", "kernel_regs.cu", "kernel_shuffle.cu", "kernel_misc.cu"]
 CPP_SOURCES = ["core.cpp", "planner.cpp", "capi.cpp"]
 HEADERS = ["core.hpp", "plan.hpp", "planner.hpp", "kernels.hpp", "device_common.cuh"]
 

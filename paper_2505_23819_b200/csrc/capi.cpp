@@ -200,6 +200,16 @@ ll_status ll_product(ll_layout a, ll_layout b, ll_layout* out) {
   });
 }
 
+ll_status ll_left_divide(ll_layout m, ll_layout m1, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(m, "ll_left_divide");
+    check_layout(m1, "ll_left_divide");
+    if (!out) return fail(LL_ERR_ARG, "ll_left_divide: out is NULL");
+    *out = wrap(ll::left_divide(m->L, m1->L));
+    return LL_OK;
+  });
+}
+
 ll_status ll_transpose(ll_layout l, const int* perm, ll_layout* out) {
   return guarded([&]() -> ll_status {
     check_layout(l, "ll_transpose");
@@ -406,6 +416,11 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
       ++g_launches;
       return cuda_status(ll::launch_convert_async(P->sp, w, P->nv, src, dst, max_ctas, st, rg),
                          "ll_convert (async smem kernel)");
+    case LL_PATH_REGS:
+      if (n_shards > 1) return fail(LL_ERR_UNSUPPORTED, "ll_convert_shard: the regs path is not shardable");
+      ++g_launches;
+      return cuda_status(ll::launch_convert_regs(P->rp, w, src, dst, max_ctas, 1, nullptr, st),
+                         "ll_convert (register-faithful kernel)");
     case LL_PATH_SMEM_TMA:
       ++g_launches;
       return cuda_status(ll::launch_convert_tma(P->sp, P->td, w, P->nv, src, dst, max_ctas, st, rg),
@@ -429,6 +444,26 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
                         int elem_bits, const ll_convert_options* opts, ll_stream stream) {
   return guarded([&]() -> ll_status {
     return run_convert(src, src_layout, dst, dst_layout, elem_bits, opts, stream, 1, 0);
+  });
+}
+
+ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst,
+                                ll_layout dst_layout, int elem_bits, int64_t batch, int reps,
+                                long long* cycles, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_convert_regs_timed");
+    check_layout(dst_layout, "ll_convert_regs_timed");
+    const int w = elem_bytes(elem_bits);
+    if (!src || !dst) return fail(LL_ERR_ARG, "ll_convert_regs_timed: NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+      return fail(LL_ERR_ARG, "ll_convert_regs_timed: buffers must be 16-byte aligned");
+    if (reps < 1) return fail(LL_ERR_ARG, "ll_convert_regs_timed: reps < 1");
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_REGS,
+                                  batch > 0 ? batch : 1);
+    ++g_launches;
+    return cuda_status(ll::launch_convert_regs(P->rp, w, src, dst, 0, reps, cycles,
+                                               reinterpret_cast<cudaStream_t>(stream)),
+                       "ll_convert_regs_timed");
   });
 }
 

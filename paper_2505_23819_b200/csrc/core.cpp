@@ -219,6 +219,54 @@ Layout product(const Layout& a, const Layout& b) {
   return r;
 }
 
+Layout left_divide(const Layout& m, const Layout& m1) {
+  // Definition "Left Division", label-wise: m = [[m1, 0], [0, m2]]
+  // -- for every input label the first m1.in_size bits are m1's columns
+  // (embedded at the low bits of each output dim) and the other bits have
+  // zero m1 block; m2 = the remaining columns shifted down.
+  for (auto& d : m1.out) {
+    int i = m.out_index(d.name);
+    if (i < 0 || m.out[i].bits < d.bits)
+      throw Error(LL_ERR_SHAPE, "left_divide: output dim " + d.name + " missing or too small");
+  }
+  for (auto& d : m1.in)
+    if (m.in_size(d.name) < d.bits && !(m.in_offset(d.name) >= 0 && d.bits == 0))
+      throw Error(LL_ERR_SHAPE, "left_divide: input dim " + d.name + " missing or too small");
+  auto low_bits = [&](const std::string& name) {
+    int i = m1.out_index(name);
+    return i < 0 ? 0 : m1.out[i].bits;
+  };
+  Layout r;
+  for (auto& d : m.out) r.out.push_back({d.name, d.bits - low_bits(d.name)});
+  for (auto& d : m.in) {
+    const int k1 = m1.in_size(d.name);
+    auto mv = m.sub(d.name);
+    auto m1v = m1.sub(d.name);
+    for (int k = 0; k < k1; ++k) {
+      auto c1 = m1.unflatten(m1v[k]);
+      std::vector<int64_t> want(m.out.size(), 0);
+      for (size_t o = 0; o < m1.out.size(); ++o) want[m.out_index(m1.out[o].name)] = c1[o];
+      if (mv[k] != m.flatten(want))
+        throw Error(LL_ERR_SHAPE, "left_divide: " + d.name + " bit " + std::to_string(k) +
+                                      " is not the divisor's column");
+    }
+    for (int k = k1; k < d.bits; ++k) {
+      auto c = m.unflatten(mv[k]);
+      std::vector<int64_t> rc(m.out.size(), 0);
+      for (size_t o = 0; o < m.out.size(); ++o) {
+        const int lb = low_bits(m.out[o].name);
+        if (c[o] & ((int64_t(1) << lb) - 1))
+          throw Error(LL_ERR_SHAPE, "left_divide: " + d.name + " bit " + std::to_string(k) +
+                                        " has a non-zero divisor block");
+        rc[o] = c[o] >> lb;
+      }
+      r.cols.push_back(r.flatten(rc));
+    }
+    r.in.push_back({d.name, d.bits - k1});
+  }
+  return r;
+}
+
 }  // namespace ll
 
 namespace ll {

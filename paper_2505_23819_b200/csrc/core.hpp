@@ -99,6 +99,9 @@ struct Layout {
 Layout compose(const Layout& outer, const Layout& inner);
 Layout right_inverse(const Layout& l);
 Layout product(const Layout& a, const Layout& b);
+// Left division: m = [[m1, 0], [0, m2]] label-wise -> m2; throws
+// LL_ERR_SHAPE when m has no such structure.
+Layout left_divide(const Layout& m, const Layout& m1);
 
 }  // namespace ll
 

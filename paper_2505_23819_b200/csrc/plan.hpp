@@ -118,6 +118,34 @@ struct TmaDesc {
   int32_t size_bits[5];   // top dim: ignored (computed from the launch range)
 };
 
+// Register-faithful conversion plan (LL_PATH_REGS): threads ARE the layouts'
+// lanes and warps (one CTA per block index), each thread holds its own
+// registers (2^reg elements, contiguous in the buffers' hardware order), and
+// the exchange goes registers -> shared memory (layout S, the paper's optimal
+// swizzle) -> registers, as in the paper's in-kernel convert_layout.  Each
+// side uses vectorised st/ld.shared or, when its layout is divisible by the
+// tile id^{reg,offset}_k x id^{thread,offset}_2, stmatrix /
+// ldmatrix (m8n8 b16 rows of 16 bytes).  Offsets are bytes, XOR-combined.
+#define LL_REGS_MAX_INST 64
+struct RegsPlan {
+  int32_t nw;            // log2 warps per CTA
+  int32_t nwords;        // 32-bit words per thread
+  int64_t tile_bytes;    // bytes per CTA tile (= per block index)
+  int64_t n_tiles;       // blocks x batch
+  int32_t wr_mat, rd_mat;    // 1: stmatrix / ldmatrix; 0: st/ld.shared
+  int32_t wr_gw, rd_gw;      // words per thread per instruction (1, 2, 4)
+  int32_t n_swaps;           // load-side element-bit swaps (A's word order -> B's)
+  int8_t swap_a[LL_MAX_SWAPS], swap_b[LL_MAX_SWAPS];
+  // word-bit transpositions bringing each side's instruction words to word
+  // bits 0 (and 1): applied to the source registers once before the exchange
+  // (write side), and in reverse to the received registers (read side), so the
+  // exchange itself has one fixed operand pattern
+  int32_t n_wsw, n_rsw;
+  int8_t wsw_a[4], wsw_b[4], rsw_a[4], rsw_b[4];
+  uint32_t sw_thr[LL_MAX_TBITS], sr_thr[LL_MAX_TBITS];  // per lane / address-provider bit, warp bit
+  uint32_t sw_inst[LL_REGS_MAX_INST], sr_inst[LL_REGS_MAX_INST];  // per instruction
+};
+
 // A contiguous range of tile indices [t0, t1) of a smem / shuffle plan, with
 // the byte offsets of the caller's slices (multi-GPU shards: each rank holds
 // only its slice of src and dst).

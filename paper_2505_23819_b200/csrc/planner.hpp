@@ -41,6 +41,7 @@ struct ConvertPlan {
   // smem path
   SmemPlan sp{};
   TmaDesc td{};      // LL_PATH_SMEM_TMA
+  RegsPlan rp{};     // LL_PATH_REGS
   int nv = 0, g = 0;
   int tile_bits = 0, r = 0, gw = 0;
   int pred_wf_ld = 0, pred_wf_st = 0;   // wavefronts per STS / LDS instruction

@@ -588,3 +588,99 @@ def test_convert_host_sharded_single_instance():
     ll.convert_host(src_h, A, dst_h, B, 8, 1, ds, dd, scratch)
     exp = expect_convert(c, src_h.numpy())
     assert dst_h.numpy().tobytes() == exp.tobytes()
+
+
+# ------------------------------------------------ register-faithful path (regs)
+
+def rand_faithful_pair(rng, w, match_lanes):
+    """A: random bit-permutation layout (reg, lane, warp, block); B: the same
+    block columns, its (reg, lane, warp) a random permutation of A's; with
+    match_lanes B keeps A's lanes 0, 1 (ldmatrix / stmatrix both apply)."""
+    kw = {1: 2, 2: 1, 4: 0}[w]
+    r = rng.randint(max(kw, 1), 6)
+    nw = rng.randint(0, 3)
+    nb = rng.randint(0, 3)
+    d = r + 5 + nw
+    tot = d + nb
+    out = [("i", tot // 2), ("j", tot - tot // 2)]
+    tmp = OLayout([], out, {})
+    cols = [1 << k for k in range(tot)]
+    rng.shuffle(cols)
+    tile, blk = cols[:d], cols[d:]
+    perm = tile[:]
+    while True:
+        rng.shuffle(perm)
+        if match_lanes:
+            a0, a1 = tile[r], tile[r + 1]
+            perm.remove(a0)
+            perm.remove(a1)
+            perm[r:r] = [a0, a1]
+        # B's word must hold elements A holds in registers (prmt on load)
+        if all(x in tile[:r] for x in perm[:kw]):
+            break
+        perm = tile[:]
+    names = [("reg", r), ("lane", 5), ("warp", nw), ("block", nb)]
+
+    def spec(v):
+        bases, k = {}, 0
+        for n, b in names:
+            bases[n] = [tmp.unflatten(x) for x in v[k:k + b]]
+            k += b
+        return {"in_dims": names, "out_dims": out, "bases": bases}
+    return {"A": spec(tile + blk), "B": spec(perm + blk), "elem_bytes": w}
+
+
+@pytest.mark.parametrize("mat", [1, 0])
+@pytest.mark.parametrize("name,mk", [("cfg1a", lambda: configs.cfg1("mma")),
+                                     ("cfg1b", lambda: configs.cfg1("T")),
+                                     ("cfg2_b3", lambda: configs.cfg2(batch_bits=3))])
+def test_convert_regs_configs(name, mk, mat):
+    """Register-faithful execution of configs 1-2 (threads = the layouts' own
+    lanes and warps), with stmatrix / ldmatrix allowed or not."""
+    c = mk()
+    ll.tune("regs_matrix", mat)
+    try:
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        plan = ll.plan_describe(A, B, 8 * c["elem_bytes"], "regs")
+        if name == "cfg1a":
+            assert (plan["regs"]["write"] == "stmatrix") == bool(mat)
+        src, dst = run_convert(c, path="regs")
+        assert dst.tobytes() == expect_convert(c, src).tobytes(), plan["regs"]
+    finally:
+        ll.tune("regs_matrix", 1)
+
+
+@pytest.mark.parametrize("w", [1, 2, 4])
+@pytest.mark.parametrize("match_lanes", [False, True])
+def test_convert_regs_random_pairs(w, match_lanes):
+    rng = random.Random(800 + 10 * w + match_lanes)
+    kinds = set()
+    for _ in range(12):
+        c = rand_faithful_pair(rng, w, match_lanes)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        plan = ll.plan_describe(A, B, 8 * w, "regs")
+        kinds.add((plan["regs"]["write"], plan["regs"]["read"]))
+        batch = rng.choice([1, 3])
+        src, dst = run_convert(c, path="regs", seed=rng.randint(0, 999), batch=batch)
+        assert dst.tobytes() == expect_convert(c, src, batch).tobytes(), plan["regs"]
+    if match_lanes:
+        assert ("stmatrix", "ldmatrix") in kinds
+
+
+def test_convert_regs_timed_cycles():
+    """In-kernel repetition (reps) leaves the result unchanged and reports
+    per-CTA cycles that grow with reps."""
+    c = configs.cfg1("mma")
+    w = 2
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    src = values_torch(1 << A.in_bits, 9, w, "cuda")
+    exp = expect_convert(c, _np(src, w))
+    cyc = []
+    for reps in (1, 64):
+        dst = torch.zeros_like(src)
+        cy = torch.zeros(4, dtype=torch.int64, device="cuda")
+        ll.convert_regs_timed(src, A, dst, B, 16, reps=reps, cycles=cy)
+        torch.cuda.synchronize()
+        assert _np(dst, w).tobytes() == exp.tobytes()
+        cyc.append(int(cy[0].item()))
+    assert 0 < cyc[0] < cyc[1]

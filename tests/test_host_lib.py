@@ -338,3 +338,79 @@ def test_tma_plan_needs_swizzle_for_cfg5():
     tot0, n0 = _reader_wavefronts(d0)
     assert tot0 == 8 * n0
     assert d["tma"]["swizzle"] == "128B" and d["pred_wavefronts_per_lds"] == 4
+
+
+# ------------------------------------------------ left division, regs path plans
+
+def test_left_divide_matches_oracle_on_products():
+    """ll_left_divide (C++) vs oracle.left_divide on product(m1, m2): both
+    recover m2 (Definition "Left Division" is the inverse of "Product",
+    P:331-365), and both reject a layout without the block structure."""
+    from oracle.layout import left_divide as oldiv, product as oprod
+    rng = random.Random(77)
+    for _ in range(20):
+        m1 = rand_spec(rng, [("reg", 2), ("lane", 2)], [("offset", 4)])
+        m2 = rand_spec(rng, [("reg", 3), ("lane", 3), ("warp", 1)], [("offset", 7)])
+        O1 = OLayout(m1["in_dims"], m1["out_dims"], m1["bases"])
+        O2 = OLayout(m2["in_dims"], m2["out_dims"], m2["bases"])
+        P = oprod(O1, O2)
+        assert oldiv(P, O1) == O2
+        L = ll.left_divide(ll.Layout(P.in_dims, P.out_dims, P.bases),
+                           ll.Layout(O1.in_dims, O1.out_dims, O1.bases))
+        spec = L.spec()
+        assert OLayout(spec["in_dims"], spec["out_dims"], spec["bases"]) == O2
+        # break the structure: xor an m1 column into an m2 column
+        bases = {k: list(v) for k, v in P.bases.items()}
+        bases["warp"][0] = tuple(a ^ b for a, b in zip(bases["warp"][0], bases["reg"][0]))
+        Q = OLayout(P.in_dims, P.out_dims, bases)
+        with pytest.raises(ValueError):
+            oldiv(Q, O1)
+        with pytest.raises(ll.LLError):
+            ll.left_divide(ll.Layout(Q.in_dims, Q.out_dims, Q.bases),
+                           ll.Layout(O1.in_dims, O1.out_dims, O1.bases))
+
+
+def _regs_S_inverse_compose(d, c, side):
+    """S^{-1} o L for one side of a regs plan, as an oracle layout from the
+    plan's S columns (tile vectors in A's (reg, lane, warp) index space)."""
+    from oracle.layout import from_flat
+    Scols = d["S_vect"] + d["S_bank"] + d["S_idx"]
+    n = len(Scols)
+    Sinv = f2.right_inverse(Scols, n)
+    spec = c[side]
+    in_dims = [(nm, b) for nm, b in spec["in_dims"] if nm != "block"]
+    if side == "A":
+        cols = [1 << k for k in range(n)]
+    else:
+        Ao = OLayout(c["A"]["in_dims"], c["A"]["out_dims"], c["A"]["bases"])
+        Bo = OLayout(c["B"]["in_dims"], c["B"]["out_dims"], c["B"]["bases"])
+        Ainv = f2.right_inverse(Ao.cols, Ao.out_bits)
+        cols = [f2.apply(Ainv, x) for x in Bo.cols[:n]]
+    return from_flat(in_dims, [("offset", n)], [f2.apply(Sinv, x) for x in cols])
+
+
+@pytest.mark.parametrize("w", [2, 4])
+def test_regs_plan_matrix_tiles_divide(w):
+    """Config 1a under the register-faithful path: both sides are lowered to
+    stmatrix / ldmatrix, and the oracle's left division confirms the tile
+    T = id^{reg,offset}_k x id^{lane,offset}_2 divides S^{-1} o A
+    and S^{-1} o B; disabling matrices falls back to 4-byte vectors (V =
+    A_reg n B_reg = {j0})."""
+    from oracle.layout import left_divide as oldiv
+    c = dict(configs.cfg1("mma"), elem_bytes=w)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    d = ll.plan_describe(A, B, 8 * w, "regs")
+    assert d["regs"]["write"] == "stmatrix" and d["regs"]["read"] == "ldmatrix"
+    assert d["granule_bytes"] == 16
+    k = {1: 2, 2: 1, 4: 0}[w]
+    T = OLayout([("reg", k), ("lane", 2)], [("offset", k + 2)],
+                {"reg": [(1 << t,) for t in range(k)], "lane": [(1 << (k + t),) for t in range(2)]})
+    for side in ("A", "B"):
+        oldiv(_regs_S_inverse_compose(d, c, side), T)   # raises if not divisible
+    try:
+        ll.tune("regs_matrix", 0)
+        d0 = ll.plan_describe(A, B, 8 * w, "regs")
+    finally:
+        ll.tune("regs_matrix", 1)
+    assert d0["regs"]["write"] == "st.shared" and d0["regs"]["read"] == "ld.shared"
+    assert d0["regs"]["write_instr_per_thread"] > d["regs"]["write_instr_per_thread"]
