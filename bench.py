@@ -159,7 +159,8 @@ def measured_peak():
 
 
 def ncu_traffic(cfg):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary; cfg is the key ("2", "5_upcast", "3_tma", "2_regs", ...)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
@@ -483,7 +484,9 @@ def main():
                        "tma": plan.get("tma"), "tune": args.tune or None,
                        "parallelism": "dp%d" % world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(cfg),
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic(cfg + ("_upcast" if args.upcast else "") +
+                                                {"smem_tma": "_tma", "regs": "_regs"}.get(plan.get("path"), "")),
                          "peak_source": peak_src, "kernel": kernel,
                          "avg_launch_us": avg_launch_ms * 1000,
                          "frac_of_8TBs": achieved / 8000.0},
