@@ -466,7 +466,7 @@ def main():
         kernel = {"smem": "convert_smem_kernel", "generic": "convert_generic_kernel",
                   "smem_noswizzle": "convert_smem_kernel", "smem_padded": "convert_smem_kernel",
                   "smem_async": "convert_async_kernel", "smem_tma": "convert_tma_kernel",
-                  "regs": "convert_regs_kernel",
+                  "regs": "convert_regs_kernel", "smem_tma_store": "convert_tma_store_kernel",
                   "copy": "cudaMemcpyAsync", "shuffle": "gather_shuffle_kernel",
                   "direct": "gather_direct_kernel"}.get(plan.get("path"), plan.get("path"))
         line = {
@@ -486,7 +486,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic(cfg + ("_upcast" if args.upcast else "") +
-                                                {"smem_tma": "_tma", "regs": "_regs"}.get(plan.get("path"), "")),
+                                                {"smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas"}.get(
+                                                    plan.get("path"), "")),
                          "peak_source": peak_src, "kernel": kernel,
                          "avg_launch_us": avg_launch_ms * 1000,
                          "frac_of_8TBs": achieved / 8000.0},

@@ -184,13 +184,18 @@ typedef enum {
                             Def. 5 instances; the planner picks the mode and the
                             reader's lanes so the reads are conflict-free.
                             LL_ERR_UNSUPPORTED when the source tile needs > 5 box dims. */
-  LL_PATH_REGS = 9       /* register-faithful: threads are the layouts' own lanes / warps (one
+  LL_PATH_REGS = 9,      /* register-faithful: threads are the layouts' own lanes / warps (one
                             CTA per block index, each thread's registers contiguous in the
                             buffers), exchange registers -> smem (optimal swizzle) -> registers
                             with stmatrix / ldmatrix where the layout is divisible by their tile
                             (P:588-591), else vectorised st/ld.shared.  Needs reg/lane/warp/block
                             layouts with equal lane (5) and warp (<= 3) bits, identical block
                             columns and elements of <= 4 bytes; else LL_ERR_UNSUPPORTED. */
+  LL_PATH_SMEM_TMA_STORE = 10 /* as SMEM_TMA, and the destination tile is written to a second
+                            hardware-swizzled shared-memory image and stored by one TMA tensor
+                            store; the readers' lanes (possibly XOR "diagonals" of tile bits)
+                            are chosen so reads AND writes are conflict-free.  No thread issues a
+                            global load or store. */
 } ll_path;
 
 typedef struct {

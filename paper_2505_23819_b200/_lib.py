@@ -88,7 +88,7 @@ STATUS = {0: "LL_OK", 1: "LL_ERR_ARG", 2: "LL_ERR_SHAPE", 3: "LL_ERR_LABEL",
           7: "LL_ERR_UNSUPPORTED", 8: "LL_ERR_CUDA", 9: "LL_ERR_OOM"}
 PATHS = {"auto": 0, "copy": 1, "smem": 2, "shuffle": 3, "generic": 4, "smem_noswizzle": 5,
          "smem_async": 6, "smem_padded": 7, "smem_tma": 8,
-         "regs": 9}
+         "regs": 9, "smem_tma_store": 10}
 
 
 class LLError(RuntimeError):

@@ -395,7 +395,7 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
     rg = ll::shard_range(*P, n_shards, shard);
   } else if (P->path == LL_PATH_SMEM || P->path == LL_PATH_SMEM_NOSWIZZLE ||
              P->path == LL_PATH_SMEM_ASYNC || P->path == LL_PATH_SMEM_PADDED ||
-             P->path == LL_PATH_SMEM_TMA) {
+             P->path == LL_PATH_SMEM_TMA || P->path == LL_PATH_SMEM_TMA_STORE) {
     rg.t1 = P->sp.tile.n_tiles;
   } else if (P->path == LL_PATH_SHUFFLE) {
     rg.t1 = P->shp.tile.n_tiles;
@@ -421,6 +421,11 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
       ++g_launches;
       return cuda_status(ll::launch_convert_regs(P->rp, w, src, dst, max_ctas, 1, nullptr, st),
                          "ll_convert (register-faithful kernel)");
+    case LL_PATH_SMEM_TMA_STORE:
+      ++g_launches;
+      return cuda_status(ll::launch_convert_tma_store(P->sp, P->td, P->td_dst, w, P->nv, src, dst,
+                                                      max_ctas, st, rg),
+                         "ll_convert (TMA load/store kernel)");
     case LL_PATH_SMEM_TMA:
       ++g_launches;
       return cuda_status(ll::launch_convert_tma(P->sp, P->td, w, P->nv, src, dst, max_ctas, st, rg),

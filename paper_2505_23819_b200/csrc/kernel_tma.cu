@@ -74,6 +74,50 @@ __device__ __forceinline__ void tma_load(uint32_t sdst, const CUtensorMap* tm, c
   }
 }
 
+__device__ __forceinline__ void tma_store(const CUtensorMap* tm, const int32_t* c, int nd,
+                                          uint32_t ssrc) {
+  const uint64_t tp = reinterpret_cast<uint64_t>(tm);
+  switch (nd) {
+    case 1:
+      asm volatile("cp.async.bulk.tensor.1d.global.shared::cta.bulk_group [%0, {%1}], [%2];" ::"l"(tp),
+                   "r"(c[0]), "r"(ssrc)
+                   : "memory");
+      break;
+    case 2:
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tp),
+                   "r"(c[0]), "r"(c[1]), "r"(ssrc)
+                   : "memory");
+      break;
+    case 3:
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tp),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(ssrc)
+                   : "memory");
+      break;
+    case 4:
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tp),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(ssrc)
+                   : "memory");
+      break;
+    default:
+      asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(tp),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(ssrc)
+                   : "memory");
+      break;
+  }
+}
+
+__device__ __forceinline__ void tile_coords(int64_t e, const TmaDesc& td, int32_t* c) {
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    if (i < td.ndim) {
+      const int64_t v = e >> td.shift[i];
+      c[i] = (int32_t)(i + 1 < td.ndim ? (v & ((int64_t(1) << td.size_bits[i]) - 1)) : v);
+    } else {
+      c[i] = 0;
+    }
+  }
+}
+
 #define LL_TMA_MAX_GROUPS 8
 #define LL_TMA_MAX_STAGES 4
 
@@ -179,6 +223,112 @@ __global__ void __launch_bounds__(256) convert_tma_kernel(const __grid_constant_
   }
 }
 
+// TMA load + TMA store (LL_PATH_SMEM_TMA_STORE): as convert_tma_kernel, but
+// the readers write their destination vectors into one of two destination
+// images (STS.128, conflict-free by the planner's lanes), fence the generic
+// proxy against the async proxy, and the leader stores the image with one
+// cp.async.bulk.tensor (bulk group); the image is rewritten only after that
+// store has finished reading it (cp.async.bulk.wait_group.read 1).
+template <int W, int NV, int NS>
+__global__ void __launch_bounds__(256) convert_tma_store_kernel(
+    const __grid_constant__ SmemPlan p, const __grid_constant__ CUtensorMap tsrc,
+    const __grid_constant__ CUtensorMap tdst, const TmaDesc tds, const TmaDesc tdd,
+    int64_t n_groups, TileRange rg) {
+  constexpr int NW = NV * 4;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[LL_TMA_MAX_GROUPS][NS];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gw = p.gw;
+  const int group = warp >> gw;
+  const int tb = lane | ((warp & ((1 << gw) - 1)) << 5);
+  const int gpc = (blockDim.x >> 5) >> gw;
+  const int tbits = 5 + gw;
+  const int64_t gid = (int64_t)blockIdx.x * gpc + group;
+  if (gid >= n_groups) return;
+  uint32_t swx = 0, srx = 0;
+#pragma unroll
+  for (int b = 0; b < LL_MAX_TBITS; ++b) {
+    if (b < tbits && ((tb >> b) & 1)) {
+      swx ^= p.sw_thr[b];
+      srx ^= p.sr_thr[b];
+    }
+  }
+  const int n_bits = p.tile.n_bits;
+  const int n_tab = p.tile.n_tab;
+  const int64_t rmask = (int64_t(1) << n_bits) - 1;
+  auto tile_off = [&](int64_t t, int64_t& so, int64_t& dof) {
+    const int64_t inst = t >> n_bits;
+    const int64_t r = t & rmask;
+    so = inst * p.tile.batch_stride_src;
+    dof = inst * p.tile.batch_stride_dst;
+#pragma unroll
+    for (int k = 0; k < LL_MAX_TAB; ++k) {
+      if (k < n_tab) {
+        const TileTab& e = p.tile.tab[k][(int)((r >> (k * LL_TAB_BITS)) & ((1 << LL_TAB_BITS) - 1))];
+        so += e.src;
+        dof += e.dst;
+      }
+    }
+  };
+  const uint32_t tb_bytes = (uint32_t)p.tile_bytes;
+  const uint32_t sraw = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t sbase = ((sraw + 1023u) & ~1023u) + group * (NS + 2) * tb_bytes;
+  const uint32_t dbase = sbase + NS * tb_bytes;
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[group][0]);
+  const bool leader = tb == 0;
+  if (leader) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  group_sync(gw, group);
+  constexpr int lw = ilog2(W);
+  auto issue = [&](int64_t t, int stg) {
+    if (leader && t < rg.t1) {
+      int64_t so, dof;
+      tile_off(t, so, dof);
+      int32_t c[5];
+      tile_coords((so - rg.src_shift) >> lw, tds, c);
+      const uint32_t bar = bar0 + 8 * stg;
+      mbar_expect_tx(bar, tb_bytes);
+      tma_load(sbase + stg * tb_bytes, &tsrc, c, tds.ndim, bar);
+    }
+  };
+  const int64_t t_first = rg.t0 + gid;
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) issue(t_first + s * n_groups, s);
+  int stage = 0;
+  uint32_t phase = 0, it = 0;
+  const int ga = p.gsel_a, gb = p.gsel_b;
+  for (int64_t t = t_first; t < rg.t1; t += n_groups, ++it) {
+    mbar_wait(bar0 + 8 * stage, (phase >> stage) & 1u);
+    phase ^= 1u << stage;
+    if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    group_sync(gw, group);
+    issue(t + (NS - 1) * n_groups, stage == 0 ? NS - 1 : stage - 1);
+    uint32_t Q[NW];
+    const uint32_t rb = sbase + stage * tb_bytes;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) lds<16>(rb + (srx ^ p.sr_gran[j]), &Q[4 * j]);
+    for (int s = 0; s < p.n_swaps; ++s) apply_swap<W, NW>(Q, p.swap_a[s], p.swap_b[s]);
+    const uint32_t db = dbase + (it & 1u) * tb_bytes;
+    sts_dispatch<NW, 4>(ga, gb, Q, db, swx, p.sw_gran);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    group_sync(gw, group);
+    if (leader) {
+      int64_t so, dof;
+      tile_off(t, so, dof);
+      int32_t c[5];
+      tile_coords((dof - rg.dst_shift) >> lw, tdd, c);
+      tma_store(&tdst, c, tdd.ndim, db);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    stage = stage == NS - 1 ? 0 : stage + 1;
+  }
+  if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------ tensor maps
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -264,6 +414,71 @@ static cudaError_t launch_tma_p(const SmemPlan& p, const TmaDesc& td, const void
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
   k<<<(unsigned)grid, threads, smem, st>>>(p, tm, td, (uint8_t*)dst, groups, rg);
   return cudaGetLastError();
+}
+
+template <int W, int NV, int NS>
+static cudaError_t launch_tma_store_p(const SmemPlan& p, const TmaDesc& tds, const TmaDesc& tdd,
+                                      const void* src, void* dst, int max_ctas, cudaStream_t st,
+                                      const TileRange& rg) {
+  auto k = convert_tma_store_kernel<W, NV, NS>;
+  const int threads = 256;
+  const int gpc = (threads / 32) >> p.gw;
+  const size_t smem = (size_t)gpc * (NS + 2) * p.tile_bytes + 1024;
+  if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+  static int occ_cache = -1;
+  static size_t occ_smem = 0;
+  if (occ_cache < 0 || occ_smem != smem) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
+    occ_smem = smem;
+  }
+  if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
+  const int64_t n_tiles = rg.t1 - rg.t0;
+  if (n_tiles <= 0) return cudaSuccess;
+  CUtensorMap ms, md;
+  const int64_t slice_elems = n_tiles * (int64_t(p.tile_bytes) / W);
+  cudaError_t e = encode_src_map(&ms, tds, W, src, slice_elems);
+  if (e != cudaSuccess) return e;
+  e = encode_src_map(&md, tdd, W, dst, slice_elems);
+  if (e != cudaSuccess) return e;
+  const int64_t resident = (int64_t)occ_cache * num_sms() * gpc;
+  int tpg = knobs().tma_tpg;
+  if (tpg < 0) tpg = (n_tiles / 4 >= 8 * resident) ? 4 : 0;
+  int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : resident;
+  if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
+  groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
+  const int64_t grid = (groups + gpc - 1) / gpc;
+  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  k<<<(unsigned)grid, threads, smem, st>>>(p, ms, md, tds, tdd, groups, rg);
+  return cudaGetLastError();
+}
+
+template <int W>
+static cudaError_t launch_tma_store_w(const SmemPlan& p, const TmaDesc& tds, const TmaDesc& tdd,
+                                      int nv, const void* src, void* dst, int max_ctas,
+                                      cudaStream_t st, const TileRange& rg) {
+  const int ns = knobs().tma_stages;
+#define LL_TSCASE(NV_)                                                                          \
+  if (nv == NV_) {                                                                              \
+    if (ns <= 2) return launch_tma_store_p<W, NV_, 2>(p, tds, tdd, src, dst, max_ctas, st, rg); \
+    return launch_tma_store_p<W, NV_, 3>(p, tds, tdd, src, dst, max_ctas, st, rg);              \
+  }
+  LL_TSCASE(1) LL_TSCASE(2) LL_TSCASE(4) LL_TSCASE(8)
+#undef LL_TSCASE
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_convert_tma_store(const SmemPlan& p, const TmaDesc& tds, const TmaDesc& tdd,
+                                     int w, int nv, const void* src, void* dst, int max_ctas,
+                                     cudaStream_t st, const TileRange& rg) {
+  if (tds.ndim < 1 || tds.ndim > 5 || tdd.ndim < 1 || tdd.ndim > 5) return cudaErrorInvalidValue;
+  switch (w) {
+    case 1: return launch_tma_store_w<1>(p, tds, tdd, nv, src, dst, max_ctas, st, rg);
+    case 2: return launch_tma_store_w<2>(p, tds, tdd, nv, src, dst, max_ctas, st, rg);
+    case 4: return launch_tma_store_w<4>(p, tds, tdd, nv, src, dst, max_ctas, st, rg);
+    case 8: return launch_tma_store_w<8>(p, tds, tdd, nv, src, dst, max_ctas, st, rg);
+  }
+  return cudaErrorNotSupported;
 }
 
 template <int W>

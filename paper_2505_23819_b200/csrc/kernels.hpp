@@ -17,6 +17,9 @@ cudaError_t launch_convert_async(const SmemPlan& p, int w, int nv, const void* s
 cudaError_t launch_convert_tma(const SmemPlan& p, const TmaDesc& td, int w, int nv,
                                const void* src, void* dst, int max_ctas, cudaStream_t st,
                                const TileRange& rg);
+cudaError_t launch_convert_tma_store(const SmemPlan& p, const TmaDesc& tds, const TmaDesc& tdd,
+                                     int w, int nv, const void* src, void* dst, int max_ctas,
+                                     cudaStream_t st, const TileRange& rg);
 cudaError_t launch_convert_regs(const RegsPlan& p, int w, const void* src, void* dst,
                                 int max_ctas, int reps, long long* cycles, cudaStream_t st);
 cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src, void* dst,

@@ -221,6 +221,139 @@ int64_t scale_contrib(const ConvertPlan& P, int k) {
   return pos >= 4 ? (int64_t(1) << (pos - 4)) : 0;                 // kb bit (32 fp4 = 16 bytes per scale)
 }
 
+// The paper's warp-shuffle exchange between two warp-local
+// thread layouts given by their word-level register vectors (Aw / Bw, word
+// order) and lane vectors (Al5 / Bl5): V is the word, I, E, F (ascending),
+// G = {e_i ^ f_i}, R completes span(I u G); round k sends
+// R[alpha(k) ^ beta(l)] to lane gamma(k) ^ delta(l), which stores it at word
+// eps(k) ^ zeta(l).  ok = false if the exchange is not expressible so.
+struct ShuffleCore {
+  bool ok = false;
+  int rounds = 0;
+  std::vector<u64> I, E, F, Gv, R, alpha, epsm;
+  std::vector<std::array<int, 3>> pre, post;
+  uint32_t beta[5] = {0}, zeta[5] = {0}, delta[5] = {0}, beta_any = 0, zeta_any = 0;
+  std::vector<uint8_t> gamma;
+};
+
+ShuffleCore shuffle_core(const std::vector<u64>& Aw, const std::vector<u64>& Al5,
+                         const std::vector<u64>& Bw, const std::vector<u64>& Bl5, int LB) {
+  ShuffleCore sc;
+    // I, E, F (ascending), G = {e_i ^ f_i}, R completes span(I u G) (P:634-650)
+    std::vector<u64>& I = sc.I;
+    std::vector<u64>& E = sc.E;
+    std::vector<u64>& F = sc.F;
+    std::vector<u64>& Gv = sc.Gv;
+    std::vector<u64>& R = sc.R;
+    for (u64 x : Al5) if (std::find(Bl5.begin(), Bl5.end(), x) != Bl5.end()) I.push_back(x);
+    for (u64 x : Al5) if (std::find(I.begin(), I.end(), x) == I.end()) E.push_back(x);
+    for (u64 x : Bl5) if (std::find(I.begin(), I.end(), x) == I.end()) F.push_back(x);
+    std::sort(I.begin(), I.end());
+    std::sort(E.begin(), E.end());
+    std::sort(F.begin(), F.end());
+    for (size_t i = 0; i < E.size() && i < F.size(); ++i) Gv.push_back(E[i] ^ F[i]);
+    {
+      F2Basis bs;
+      for (u64 x : I) bs.add(x);
+      for (u64 x : Gv) bs.add(x);
+      std::vector<u64> units;
+      for (u64 x : Aw) units.push_back(x);
+      for (u64 x : Al5) units.push_back(x);
+      std::sort(units.begin(), units.end());
+      for (u64 x : units) if (bs.add(x)) R.push_back(x);
+    }
+    const int NWd = 1 << LB;
+    bool ok = E.size() == F.size() && (int)R.size() == LB && NWd <= LL_MAX_GRAN;
+    // decompose word-level vectors in the ld and st bases
+    auto decomp = [&](u64 x, const std::vector<u64>& wv, const std::vector<u64>& lv, int& word,
+                      int& lane) {
+      word = 0; lane = 0;
+      for (int b = 0; b < (int)wv.size(); ++b) if (x & wv[b]) word |= 1 << b;
+      for (int c = 0; c < 5; ++c) if (x & lv[c]) lane |= 1 << c;
+    };
+    std::vector<u64> span5;
+    if (ok) {
+      std::vector<u64> gen = I;
+      gen.insert(gen.end(), Gv.begin(), Gv.end());
+      span5.push_back(0);
+      for (u64 gvec : gen) {
+        size_t n0 = span5.size();
+        for (size_t i = 0; i < n0; ++i) span5.push_back(span5[i] ^ gvec);
+      }
+      ok = span5.size() == 32;
+    }
+    std::vector<int> ws(32 * NWd, -1), sl(32 * NWd, -1), wr(32 * NWd, -1);
+    for (int k = 0; ok && k < NWd; ++k) {
+      u64 Rk = 0;
+      for (int j = 0; j < LB; ++j) if ((k >> j) & 1) Rk ^= R[j];
+      for (u64 y : span5) {
+        const u64 x = Rk ^ y;
+        int aw, al, bw, bl;
+        decomp(x, Aw, Al5, aw, al);
+        decomp(x, Bw, Bl5, bw, bl);
+        if (ws[al * NWd + k] >= 0 || wr[bl * NWd + k] >= 0) { ok = false; break; }  // one send / recv per lane
+        ws[al * NWd + k] = aw;
+        sl[bl * NWd + k] = al;
+        wr[bl * NWd + k] = bw;
+      }
+    }
+    std::vector<u64>& alpha = sc.alpha;
+    std::vector<u64>& epsm = sc.epsm;
+    alpha.assign(LB, 0);
+    epsm.assign(LB, 0);
+    if (ok) {
+      // linear decomposition: ws(l,k) = alpha(k) ^ beta(l), etc. (checked)
+      for (int l = 0; l < 32 && ok; ++l)
+        for (int k = 0; k < NWd && ok; ++k) {
+          ok = ws[l * NWd + k] == (ws[k] ^ ws[l * NWd]) && sl[l * NWd + k] == (sl[k] ^ sl[l * NWd]) &&
+               wr[l * NWd + k] == (wr[k] ^ wr[l * NWd]);
+        }
+    }
+    std::vector<std::array<int, 3>>& pre = sc.pre;
+    std::vector<std::array<int, 3>>& post = sc.post;
+    if (ok) {
+      for (int j = 0; j < LB; ++j) { alpha[j] = (u64)ws[1 << j]; epsm[j] = (u64)wr[1 << j]; }
+      // eps^{-1}
+      std::vector<u64> einv(LB, 0);
+      for (int m = 0; m < NWd; ++m) {
+        int e = 0;
+        for (int j = 0; j < LB; ++j) if ((m >> j) & 1) e ^= (int)epsm[j];
+        for (int j = 0; j < LB; ++j) if (e == (1 << j)) einv[j] = (u64)m;
+      }
+      ok = linop_factor(alpha, LB, pre) && linop_factor(einv, LB, post) &&
+           (int)pre.size() <= LL_MAX_LINOPS && (int)post.size() <= LL_MAX_LINOPS;
+      // verify the factorisations by applying them to index arrays
+      for (int pass = 0; ok && pass < 2; ++pass) {
+        const auto& ops = pass ? post : pre;
+        std::vector<int> T(NWd);
+        for (int k = 0; k < NWd; ++k) T[k] = k;
+        for (const auto& op : ops) {
+          std::vector<int> T2(NWd);
+          for (int k = 0; k < NWd; ++k) T2[k] = T[(int)linop_apply_index(op, (u64)k)];
+          T = T2;
+        }
+        for (int k = 0; k < NWd && ok; ++k) {
+          int want = 0;
+          for (int j = 0; j < LB; ++j) if ((k >> j) & 1) want ^= (int)(pass ? einv[j] : alpha[j]);
+          ok = T[k] == want;
+        }
+      }
+    }
+    if (ok) {
+      for (int c = 0; c < 5; ++c) {
+        sc.beta[c] = (uint32_t)ws[(1 << c) * NWd];
+        sc.delta[c] = (uint32_t)sl[(1 << c) * NWd];
+        sc.zeta[c] = (uint32_t)wr[(1 << c) * NWd];
+        sc.beta_any |= sc.beta[c];
+        sc.zeta_any |= sc.zeta[c];
+      }
+      for (int k = 0; k < NWd; ++k) sc.gamma.push_back((uint8_t)sl[k]);
+    }
+    sc.ok = ok;
+    sc.rounds = NWd;
+  return sc;
+}
+
 // Try to build the shared-memory tile plan; returns false if X is not a bit
 // permutation or the tile does not fit.
 bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ostringstream& js,
@@ -558,100 +691,14 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     for (int b = 0; b < LB; ++b) Aw.push_back(loc(order[b + nsub]));
     for (int b = 0; b < LB; ++b) Bw.push_back(loc(st_reg[b + nsub]));
     for (int c = 0; c < 5; ++c) { Al5.push_back(loc(ld_lane[c])); Bl5.push_back(loc(st_lane[c])); }
-    // I, E, F (ascending), G = {e_i ^ f_i}, R completes span(I u G) (P:634-650)
-    std::vector<u64> I, E, F, Gv, R;
-    for (u64 x : Al5) if (std::find(Bl5.begin(), Bl5.end(), x) != Bl5.end()) I.push_back(x);
-    for (u64 x : Al5) if (std::find(I.begin(), I.end(), x) == I.end()) E.push_back(x);
-    for (u64 x : Bl5) if (std::find(I.begin(), I.end(), x) == I.end()) F.push_back(x);
-    std::sort(I.begin(), I.end());
-    std::sort(E.begin(), E.end());
-    std::sort(F.begin(), F.end());
-    for (size_t i = 0; i < E.size() && i < F.size(); ++i) Gv.push_back(E[i] ^ F[i]);
-    {
-      F2Basis bs;
-      for (u64 x : I) bs.add(x);
-      for (u64 x : Gv) bs.add(x);
-      std::vector<u64> units;
-      for (u64 x : Aw) units.push_back(x);
-      for (u64 x : Al5) units.push_back(x);
-      std::sort(units.begin(), units.end());
-      for (u64 x : units) if (bs.add(x)) R.push_back(x);
-    }
-    const int NWd = 1 << LB;
-    bool ok = E.size() == F.size() && (int)R.size() == LB && NWd <= LL_MAX_GRAN;
-    // decompose word-level vectors in the ld and st bases
-    auto decomp = [&](u64 x, const std::vector<u64>& wv, const std::vector<u64>& lv, int& word,
-                      int& lane) {
-      word = 0; lane = 0;
-      for (int b = 0; b < (int)wv.size(); ++b) if (x & wv[b]) word |= 1 << b;
-      for (int c = 0; c < 5; ++c) if (x & lv[c]) lane |= 1 << c;
-    };
-    std::vector<u64> span5;
-    if (ok) {
-      std::vector<u64> gen = I;
-      gen.insert(gen.end(), Gv.begin(), Gv.end());
-      span5.push_back(0);
-      for (u64 gvec : gen) {
-        size_t n0 = span5.size();
-        for (size_t i = 0; i < n0; ++i) span5.push_back(span5[i] ^ gvec);
-      }
-      ok = span5.size() == 32;
-    }
-    std::vector<int> ws(32 * NWd, -1), sl(32 * NWd, -1), wr(32 * NWd, -1);
-    for (int k = 0; ok && k < NWd; ++k) {
-      u64 Rk = 0;
-      for (int j = 0; j < LB; ++j) if ((k >> j) & 1) Rk ^= R[j];
-      for (u64 y : span5) {
-        const u64 x = Rk ^ y;
-        int aw, al, bw, bl;
-        decomp(x, Aw, Al5, aw, al);
-        decomp(x, Bw, Bl5, bw, bl);
-        if (ws[al * NWd + k] >= 0 || wr[bl * NWd + k] >= 0) { ok = false; break; }  // one send / recv per lane
-        ws[al * NWd + k] = aw;
-        sl[bl * NWd + k] = al;
-        wr[bl * NWd + k] = bw;
-      }
-    }
-    std::vector<u64> alpha(LB), epsm(LB);
+    ShuffleCore sc = shuffle_core(Aw, Al5, Bw, Bl5, LB);
+    const bool ok = sc.ok;
+    const int NWd = sc.rounds;
+    const auto& I = sc.I; const auto& E = sc.E; const auto& F = sc.F; const auto& Gv = sc.Gv;
+    const auto& R = sc.R; const auto& alpha = sc.alpha; const auto& epsm = sc.epsm;
+    const auto& pre = sc.pre; const auto& post = sc.post;
     ShufflePlan& sh = P.shp;
     sh = ShufflePlan{};
-    if (ok) {
-      // linear decomposition: ws(l,k) = alpha(k) ^ beta(l), etc. (checked)
-      for (int l = 0; l < 32 && ok; ++l)
-        for (int k = 0; k < NWd && ok; ++k) {
-          ok = ws[l * NWd + k] == (ws[k] ^ ws[l * NWd]) && sl[l * NWd + k] == (sl[k] ^ sl[l * NWd]) &&
-               wr[l * NWd + k] == (wr[k] ^ wr[l * NWd]);
-        }
-    }
-    std::vector<std::array<int, 3>> pre, post;
-    if (ok) {
-      for (int j = 0; j < LB; ++j) { alpha[j] = (u64)ws[1 << j]; epsm[j] = (u64)wr[1 << j]; }
-      // eps^{-1}
-      std::vector<u64> einv(LB, 0);
-      for (int m = 0; m < NWd; ++m) {
-        int e = 0;
-        for (int j = 0; j < LB; ++j) if ((m >> j) & 1) e ^= (int)epsm[j];
-        for (int j = 0; j < LB; ++j) if (e == (1 << j)) einv[j] = (u64)m;
-      }
-      ok = linop_factor(alpha, LB, pre) && linop_factor(einv, LB, post) &&
-           (int)pre.size() <= LL_MAX_LINOPS && (int)post.size() <= LL_MAX_LINOPS;
-      // verify the factorisations by applying them to index arrays
-      for (int pass = 0; ok && pass < 2; ++pass) {
-        const auto& ops = pass ? post : pre;
-        std::vector<int> T(NWd);
-        for (int k = 0; k < NWd; ++k) T[k] = k;
-        for (const auto& op : ops) {
-          std::vector<int> T2(NWd);
-          for (int k = 0; k < NWd; ++k) T2[k] = T[(int)linop_apply_index(op, (u64)k)];
-          T = T2;
-        }
-        for (int k = 0; k < NWd && ok; ++k) {
-          int want = 0;
-          for (int j = 0; j < LB; ++j) if ((k >> j) & 1) want ^= (int)(pass ? einv[j] : alpha[j]);
-          ok = T[k] == want;
-        }
-      }
-    }
     if (ok) {
       sh.tile = sp.tile;
       sh.n_swaps = sp.n_swaps;
@@ -659,12 +706,12 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       for (int c = 0; c < 5; ++c) {
         sh.ld_thr[c] = sp.ld_thr[c];
         sh.st_thr[c] = sp.st_thr[c];
-        sh.beta_lane[c] = (uint32_t)ws[(1 << c) * NWd];
-        sh.delta_lane[c] = (uint32_t)sl[(1 << c) * NWd];
-        sh.zeta_lane[c] = (uint32_t)wr[(1 << c) * NWd];
-        sh.beta_any |= sh.beta_lane[c];
-        sh.zeta_any |= sh.zeta_lane[c];
+        sh.beta_lane[c] = sc.beta[c];
+        sh.delta_lane[c] = sc.delta[c];
+        sh.zeta_lane[c] = sc.zeta[c];
       }
+      sh.beta_any = sc.beta_any;
+      sh.zeta_any = sc.zeta_any;
       for (int u = 0; u < LL_MAX_VEC; ++u) { sh.ld_vec[u] = sp.ld_vec[u]; sh.st_vec[u] = sp.st_vec[u]; }
       sh.n_pre = (int)pre.size();
       sh.n_post = (int)post.size();
@@ -674,7 +721,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       for (size_t i = 0; i < post.size(); ++i) {
         sh.post_op[i] = (int8_t)post[i][0]; sh.post_a[i] = (int8_t)post[i][1]; sh.post_b[i] = (int8_t)post[i][2];
       }
-      for (int k = 0; k < NWd; ++k) sh.gamma[k] = (uint8_t)sl[k];
+      for (int k = 0; k < NWd; ++k) sh.gamma[k] = sc.gamma[k];
       P.shuffle_ok = true;
       P.shuffle_rounds = NWd;
     }
@@ -1238,6 +1285,292 @@ bool plan_tma(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js)
   return true;
 }
 
+// TMA load + TMA store variant (LL_PATH_SMEM_TMA_STORE).  As plan_tma, but
+// the readers write their destination vectors into a second shared-memory
+// image (the destination tile, dense in destination-bit order, hardware
+// swizzle md) that one cp.async.bulk.tensor store sends to HBM.  The
+// readers' lanes are then free of global coalescing and must make BOTH the
+// 16-byte reads of the source image and the 16-byte writes of the
+// destination image conflict-free; when no set of single tile bits does,
+// XOR combinations are used (a lane bit then moves along a "diagonal" of the
+// tile -- the paper's swizzling idea applied to the thread layout).
+bool plan_tma_store(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js) {
+  const int n = P.nB, w = P.w;
+  if (P.nA != P.nB || n > 62 || w > 8) return false;
+  std::vector<int> sigma(n), sinv(n, -1);
+  for (int k = 0; k < n; ++k) {
+    if (popcount64(X[k]) != 1) return false;
+    sigma[k] = ctz64(X[k]);
+    if (sinv[sigma[k]] >= 0) return false;
+    sinv[sigma[k]] = k;
+  }
+  const int vb = ilog2i(16 / w);
+  const int lw = ilog2i(w);
+  if (n < vb + 5) return false;
+  auto contains = [](const std::vector<int>& v, int x) {
+    return std::find(v.begin(), v.end(), x) != v.end();
+  };
+  std::vector<int> VD, VS, CD, CS;
+  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
+  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("tma_run_bytes", 256)) / 16));
+  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
+  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
+  const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("tma_thread_bytes", 64)) / w));
+  std::vector<int> need = VS;
+  for (int x : VD) if (!contains(need, x)) need.push_back(x);
+  if ((int)need.size() > r_max || (int)need.size() + 5 > n) return false;
+  int r = std::min(std::max((int)need.size(), r_pref), std::min(r_max, n - 5));
+  const int tile_min = ilog2i(std::max(1024, planner_knob("tma_tile_bytes", 8192)) / w);
+  std::vector<int> T = VD;
+  for (auto* s : {&VS, &CD, &CS, &need})
+    for (int x : *s) if (!contains(T, x)) T.push_back(x);
+  for (int k = 0; (int)T.size() < std::max(r + 5, std::min(n, tile_min)) && k < n; ++k)
+    if (!contains(T, k)) T.push_back(k);
+  int g = (int)T.size() - r - 5;
+  if (g > 3) {
+    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
+    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
+  }
+  if (g < 0 || g > 3) return false;
+  std::sort(T.begin(), T.end());
+  const int d = (int)T.size();
+  if (d + lw > 20) return false;
+  std::vector<int> Ts;
+  for (int k : T) Ts.push_back(sigma[k]);
+  std::sort(Ts.begin(), Ts.end());
+  // dense images (byte offsets before the swizzle), linear in tile vectors
+  auto dense_s = [&](u64 v) -> uint32_t {
+    uint32_t o = 0;
+    for (int k = 0; k < n; ++k)
+      if ((v >> k) & 1) o ^= uint32_t(w) << (std::find(Ts.begin(), Ts.end(), sigma[k]) - Ts.begin());
+    return o;
+  };
+  auto dense_d = [&](u64 v) -> uint32_t {
+    uint32_t o = 0;
+    for (int k = 0; k < n; ++k)
+      if ((v >> k) & 1) o ^= uint32_t(w) << (std::find(T.begin(), T.end(), k) - T.begin());
+    return o;
+  };
+  auto swz = [](uint32_t a, int m) -> uint32_t {
+    return m ? a ^ (((a >> 7) & ((1u << m) - 1)) << 4) : a;
+  };
+  std::vector<int> rd_reg = VS;
+  for (int x : VD) if (!contains(rd_reg, x)) rd_reg.push_back(x);
+  {
+    std::vector<int> cand;
+    for (int x : T) if (!contains(rd_reg, x) && !contains(CD, x)) cand.push_back(x);
+    std::sort(cand.begin(), cand.end(), [](int a, int b) { return a > b; });
+    for (int x : cand) { if ((int)rd_reg.size() == r) break; rd_reg.push_back(x); }
+    if ((int)rd_reg.size() != r) return false;
+  }
+  auto make_desc = [&](const std::vector<int>& bits, int m, TmaDesc& td) -> bool {
+    td = TmaDesc{};
+    td.swizzle = m;
+    std::vector<std::pair<int, int>> runs;
+    for (int b : bits) {
+      if (!runs.empty() && runs.back().first + runs.back().second == b) ++runs.back().second;
+      else runs.push_back({b, 1});
+    }
+    if (runs.empty() || runs[0].first != 0) return false;
+    const int span_bits = m ? ilog2i((16 << m) / w) : 8;
+    std::vector<std::pair<int, int>> dims;
+    for (size_t i = 0; i < runs.size(); ++i) {
+      int a = runs[i].first, len = runs[i].second;
+      if (i == 0 && m) {
+        if (len < span_bits) return false;
+        dims.push_back({a, span_bits});
+        a += span_bits;
+        len -= span_bits;
+      }
+      while (len > 0) {
+        const int piece = std::min(len, 8);
+        dims.push_back({a, piece});
+        a += piece;
+        len -= piece;
+      }
+    }
+    if (dims.size() > 5) return false;
+    td.ndim = (int)dims.size();
+    for (int i = 0; i < td.ndim; ++i) {
+      td.shift[i] = dims[i].first;
+      td.box_bits[i] = dims[i].second;
+      td.size_bits[i] = i + 1 < td.ndim ? dims[i + 1].first - dims[i].first : 0;
+      if (i > 0 && (dims[i].first + lw) < 4) return false;
+    }
+    return true;
+  };
+  // candidate lane vectors: single non-register tile bits (lowest
+  // destination bit first), then their pairwise XORs
+  std::vector<u64> singles, cands;
+  for (int x : T) if (!contains(rd_reg, x)) singles.push_back(u64(1) << x);
+  cands = singles;
+  for (size_t i = 0; i < singles.size(); ++i)
+    for (size_t j = i + 1; j < singles.size(); ++j) cands.push_back(singles[i] | singles[j]);
+  struct Choice {
+    int ms = -1, md = -1, wf = 1 << 30, diag = 0;
+    std::vector<u64> thr;   // 5 lanes then g warps
+    TmaDesc tds{}, tdd{};
+  } best;
+  for (int ms = 0; ms <= 3; ++ms) {
+    for (int md = 0; md <= 3; ++md) {
+      Choice c;
+      c.ms = ms;
+      c.md = md;
+      if (!make_desc(Ts, ms, c.tds) || !make_desc(T, md, c.tdd)) continue;
+      auto ps = [&](u64 v) -> u64 { return (swz(dense_s(v), ms) >> 4) & 7u; };
+      auto pd = [&](u64 v) -> u64 { return (swz(dense_d(v), md) >> 4) & 7u; };
+      std::vector<u64> phase, prs, prd;
+      F2Basis span;
+      for (u64 v : cands) {
+        if (phase.size() == 3) break;
+        if (span.in_span(v)) continue;
+        std::vector<u64> a = prs, b = prd;
+        a.push_back(ps(v));
+        b.push_back(pd(v));
+        if (f2_rank(a) > f2_rank(prs) && f2_rank(b) > f2_rank(prd)) {
+          phase.push_back(v);
+          prs = a;
+          prd = b;
+          span.add(v);
+        }
+      }
+      for (u64 v : singles) {
+        if (phase.size() == 3) break;
+        if (span.add(v)) phase.push_back(v);
+      }
+      c.thr = phase;
+      for (u64 v : singles)
+        if (span.add(v)) c.thr.push_back(v);
+      if ((int)c.thr.size() != 5 + g) continue;
+      std::vector<u64> as, ad, qs, qd;
+      for (int i = 0; i < 3; ++i) {
+        as.push_back(swz(dense_s(c.thr[i]), ms));
+        ad.push_back(swz(dense_d(c.thr[i]), md));
+        qs.push_back(ps(c.thr[i]));
+        qd.push_back(pd(c.thr[i]));
+      }
+      c.wf = (4 << (f2_rank(as) - f2_rank(qs))) + (4 << (f2_rank(ad) - f2_rank(qd)));
+      for (u64 v : c.thr) c.diag += popcount64(v) > 1;
+      if (c.wf < best.wf || (c.wf == best.wf && c.diag < best.diag)) best = c;
+    }
+  }
+  if (best.ms < 0) return false;
+  const int nsub = w >= 4 ? 0 : ilog2i(4 / w);
+  std::vector<int> order = rd_reg;
+  std::vector<std::pair<int, int>> swaps;
+  for (int t = 0; t < nsub; ++t) {
+    int s = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
+    if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
+  }
+  if ((int)swaps.size() > LL_MAX_SWAPS) return false;
+  auto wordbit = [&](int rho) { return w == 8 ? rho + 1 : rho - nsub; };
+  const int LB = w == 8 ? r + 1 : r - nsub;
+  std::vector<int> ssel;
+  if (w == 8) ssel.push_back(0);
+  for (int t = (w == 8 ? 0 : nsub); t < vb; ++t) {
+    int pos = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
+    ssel.push_back(wordbit(pos));
+  }
+  if (ssel.size() != 2) return false;
+  std::vector<int> rest_rho;
+  for (int wb = 0; wb < LB; ++wb) {
+    if (std::find(ssel.begin(), ssel.end(), wb) != ssel.end()) continue;
+    rest_rho.push_back(w == 8 ? wb - 1 : wb + nsub);
+  }
+  auto roff = [&](u64 v) -> uint32_t { return swz(dense_s(v), best.ms); };
+  auto woff = [&](u64 v) -> uint32_t { return swz(dense_d(v), best.md); };
+  SmemPlan& sp = P.sp;
+  sp = SmemPlan{};
+  sp.gw = g;
+  sp.tile_bytes = w << d;
+  sp.n_swaps = (int)swaps.size();
+  for (size_t i = 0; i < swaps.size(); ++i) {
+    sp.swap_a[i] = (int8_t)swaps[i].first;
+    sp.swap_b[i] = (int8_t)swaps[i].second;
+  }
+  sp.gsel_a = (int8_t)ssel[0];
+  sp.gsel_b = (int8_t)ssel[1];
+  for (int b = 0; b < 5 + g; ++b) {
+    sp.sr_thr[b] = roff(best.thr[b]);
+    sp.sw_thr[b] = woff(best.thr[b]);
+  }
+  const int nvec = 1 << (r - vb);
+  if (nvec > LL_MAX_VEC || nvec > LL_MAX_GRAN) return false;
+  for (int u = 0; u < nvec; ++u) {
+    uint32_t ro = 0, wo = 0;
+    for (int q = 0; q < r - vb; ++q) {
+      if ((u >> q) & 1) {
+        ro ^= roff(u64(1) << rd_reg[vb + q]);            // source granule u
+        wo ^= woff(u64(1) << order[rest_rho[q]]);        // destination vector u
+      }
+    }
+    sp.sr_gran[u] = ro;
+    sp.sw_gran[u] = wo;
+  }
+  std::vector<int> O;
+  for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
+  if ((int)O.size() > LL_MAX_OUTER) return false;
+  TileMap& tm = sp.tile;
+  tm.n_bits = (int)O.size();
+  tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
+  for (int k = 0; k < tm.n_tab; ++k)
+    for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
+      int64_t so = 0, dof = 0;
+      for (int q = 0; q < LL_TAB_BITS; ++q) {
+        const int bit = k * LL_TAB_BITS + q;
+        if (((v >> q) & 1) && bit < tm.n_bits) {
+          so += int64_t(w) << sigma[O[bit]];
+          dof += int64_t(w) << O[bit];
+        }
+      }
+      tm.tab[k][v].src = so;
+      tm.tab[k][v].dst = dof;
+    }
+  tm.batch_stride_src = int64_t(w) << P.nA;
+  tm.batch_stride_dst = int64_t(w) << P.nB;
+  tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
+  P.tile_bit_src.clear();
+  P.tile_bit_dst.clear();
+  for (int q = 0; q < tm.n_bits; ++q) {
+    P.tile_bit_src.push_back(sigma[O[q]]);
+    P.tile_bit_dst.push_back(O[q]);
+  }
+  P.td = best.tds;
+  P.td_dst = best.tdd;
+  P.nv = nvec;
+  P.g = 16;
+  P.tile_bits = d;
+  P.r = r;
+  P.gw = g;
+  std::vector<u64> as, ad, qs, qd;
+  for (int i = 0; i < 3; ++i) {
+    as.push_back(roff(best.thr[i]));
+    ad.push_back(woff(best.thr[i]));
+    qs.push_back((roff(best.thr[i]) >> 4) & 7u);
+    qd.push_back((woff(best.thr[i]) >> 4) & 7u);
+  }
+  P.pred_wf_st = 4 << (f2_rank(as) - f2_rank(qs));   // LDS of the source image
+  P.pred_wf_ld = 4 << (f2_rank(ad) - f2_rank(qd));   // STS of the destination image
+  static const char* mode_names[] = {"none", "32B", "64B", "128B"};
+  auto td_json = [&](const TmaDesc& t) {
+    std::vector<int> sh, bx;
+    for (int i = 0; i < t.ndim; ++i) { sh.push_back(t.shift[i]); bx.push_back(t.box_bits[i]); }
+    std::ostringstream o;
+    o << "{\"swizzle\":\"" << mode_names[t.swizzle] << "\",\"ndim\":" << t.ndim
+      << ",\"dim_shift\":" << ivec_json(sh) << ",\"box_bits\":" << ivec_json(bx) << "}";
+    return o.str();
+  };
+  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
+     << ",\"granule_bytes\":16,\"vectors_per_thread\":" << nvec << ",\"rd_reg\":" << ivec_json(rd_reg)
+     << ",\"thread_vecs_dst_bits\":" << vec_json(best.thr) << ",\"diagonal_lanes\":" << best.diag
+     << ",\"tma\":{\"src\":" << td_json(best.tds) << ",\"dst\":" << td_json(best.tdd) << "}"
+     << ",\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"pred_wavefronts_per_sts\":" << P.pred_wf_ld
+     << ",\"n_tiles\":" << tm.n_tiles << ",\"smem_bytes\":{\"sr_thr\":" << u32_json(sp.sr_thr, 5 + g)
+     << ",\"sw_thr\":" << u32_json(sp.sw_thr, 5 + g) << ",\"sr_gran\":" << u32_json(sp.sr_gran, nvec)
+     << ",\"sw_gran\":" << u32_json(sp.sw_gran, nvec) << "}";
+  return true;
+}
+
 // Register-faithful plan (LL_PATH_REGS): the paper's in-kernel conversion.
 // Tile-local vectors live in A's (reg, lane, warp) index space: A's input bit
 // i is e_i, B's input bit k is X[k].  Shared memory S = the paper's optimal
@@ -1569,6 +1902,15 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
                                       "bit permutation or the source tile needs more than 5 TMA box dims");
     }
   }
+  if (path == LL_PATH_SMEM_TMA_STORE) {
+    std::ostringstream js2;
+    if (plan_tma_store(*P, X, js2)) {
+      js << js2.str();
+    } else {
+      throw Error(LL_ERR_UNSUPPORTED, "smem_tma_store path requested but the quotient is not a tileable "
+                                      "bit permutation or a tile needs more than 5 TMA box dims");
+    }
+  }
   if (path == LL_PATH_REGS) {
     std::ostringstream js2;
     if (plan_regs(*P, A, B, X, js2)) {
@@ -1585,7 +1927,7 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
   if (path == LL_PATH_GENERIC) fill_generic(*P, X);
   P->path = path;
   static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle",
-                                "smem_async", "smem_padded", "smem_tma", "regs"};
+                                "smem_async", "smem_padded", "smem_tma", "regs", "smem_tma_store"};
   js << ",\"path\":\"" << names[path] << "\"}";
   P->json = js.str();
   return P;
@@ -1663,7 +2005,8 @@ TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
     return rg;
   }
   if (P.path != LL_PATH_SMEM && P.path != LL_PATH_SHUFFLE && P.path != LL_PATH_SMEM_NOSWIZZLE &&
-      P.path != LL_PATH_SMEM_ASYNC && P.path != LL_PATH_SMEM_PADDED && P.path != LL_PATH_SMEM_TMA)
+      P.path != LL_PATH_SMEM_ASYNC && P.path != LL_PATH_SMEM_PADDED && P.path != LL_PATH_SMEM_TMA &&
+      P.path != LL_PATH_SMEM_TMA_STORE)
     throw Error(LL_ERR_UNSUPPORTED, "shard: only tiled (smem / shuffle) plans are shardable");
   const int nb = (int)P.tile_bit_src.size();
   if (sb > nb) throw Error(LL_ERR_UNSUPPORTED, "shard: more shards than tiles");

@@ -40,7 +40,8 @@ struct ConvertPlan {
   std::vector<u64> dst_cols;
   // smem path
   SmemPlan sp{};
-  TmaDesc td{};      // LL_PATH_SMEM_TMA
+  TmaDesc td{};      // LL_PATH_SMEM_TMA (source box)
+  TmaDesc td_dst{};  // LL_PATH_SMEM_TMA_STORE (destination box)
   RegsPlan rp{};     // LL_PATH_REGS
   int nv = 0, g = 0;
   int tile_bits = 0, r = 0, gw = 0;

@@ -72,13 +72,13 @@ CASES = [
 
 
 @pytest.mark.parametrize("path", ["auto", "smem", "smem_noswizzle", "smem_padded", "shuffle",
-                                  "smem_async", "smem_tma", "generic"])
+                                  "smem_async", "smem_tma", "smem_tma_store", "generic"])
 @pytest.mark.parametrize("name,mk", CASES)
 def test_convert_configs_small(name, mk, path):
     c = mk()
     if path == "shuffle" and name.startswith("cfg3"):
         pytest.skip("transpose exchange is not warp-local (P:624); covered by test_shuffle_rejects")
-    if path in ("smem_async", "smem_tma") and name.startswith("cfg1"):
+    if path in ("smem_async", "smem_tma", "smem_tma_store") and name.startswith("cfg1"):
         pytest.skip("16x16 tensor is smaller than one async tile")
     src, dst = run_convert(c, path=path)
     exp = expect_convert(c, src)
@@ -188,6 +188,26 @@ def test_convert_random_pairs_tma(w):
     assert done >= 6, (done, tried)
 
 
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_random_pairs_tma_store(w):
+    """TMA load + TMA store path on random bit-permutation pairs."""
+    rng = random.Random(900 + w)
+    done, tried = 0, 0
+    while done < 12 and tried < 200:
+        tried += 1
+        c = rand_pair(rng, rng.randint(12, 17), w)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        try:
+            plan = ll.plan_describe(A, B, 8 * w, "smem_tma_store")
+        except ll.LLError:
+            continue
+        batch = rng.choice([1, 2, 5])
+        src, dst = run_convert(c, path="smem_tma_store", seed=rng.randint(0, 1000), batch=batch)
+        assert dst.tobytes() == expect_convert(c, src, batch).tobytes(), plan["tma"]
+        done += 1
+    assert done >= 6, (done, tried)
+
+
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
 def test_convert_tma_each_swizzle_mode(swz):
     """Every hardware swizzle mode (the Def. 5 instances) executed on the
@@ -225,7 +245,7 @@ def test_convert_shuffle_ragged_batch(batch):
 @pytest.mark.parametrize("name,mk,shards", [("cfg5", lambda: configs.cfg5(m_bits=10, kb_bits=8), 8),
                                             ("cfg2", lambda: configs.cfg2(batch_bits=3), 4),
                                             ("cfg2s", lambda: configs.cfg2(batch_bits=3), 2)])
-@pytest.mark.parametrize("path", ["auto", "smem_tma"])
+@pytest.mark.parametrize("path", ["auto", "smem_tma", "smem_tma_store"])
 def test_convert_shards_equal_full(name, mk, shards, path):
     """Each rank's shard converted from its own slices (separate allocations,
     SURVEY 8(e)) reassembles the oracle's full conversion."""
@@ -279,7 +299,7 @@ def sampled_expected(c, src_np, h):
 @pytest.mark.parametrize("name,mk", [("cfg2", lambda: configs.cfg2()),
                                      ("cfg3", lambda: configs.cfg3()),
                                      ("cfg5", lambda: configs.cfg5(m_bits=15, kb_bits=14))])
-@pytest.mark.parametrize("path", ["auto", "smem_tma"])
+@pytest.mark.parametrize("path", ["auto", "smem_tma", "smem_tma_store"])
 def test_convert_full_size_sampled(name, mk, path):
     c = mk()
     w = c["elem_bytes"]

@@ -272,12 +272,13 @@ def test_broadcast_plans_stay_tiled():
         assert len(zd) == 2 and d["tile_order_dst_bits"][:2] == zd
 
 
-def _reader_wavefronts(d):
+def _reader_wavefronts(d, side="r"):
     """Brute force over the TMA plan's reader: every (warp, granule) LDS.128
     instruction, lane addresses from the plan's per-thread-bit / per-granule
     byte offsets (XOR-linear), quarter-warp phases, max over banks of distinct
-    4-byte words (the bank model of oracle.banks, reading A18)."""
-    thr, gran = d["smem_bytes"]["sr_thr"], d["smem_bytes"]["sr_gran"]
+    4-byte words (the bank model of oracle.banks, reading A18).  side "w":
+    the destination-image STS.128 of the TMA-store plan."""
+    thr, gran = d["smem_bytes"]["s%s_thr" % side], d["smem_bytes"]["s%s_gran" % side]
     nthr = len(thr)
     total, n_instr = 0, 0
     for wv in range(1 << (nthr - 5)):
@@ -414,3 +415,22 @@ def test_regs_plan_matrix_tiles_divide(w):
         ll.tune("regs_matrix", 1)
     assert d0["regs"]["write"] == "st.shared" and d0["regs"]["read"] == "ld.shared"
     assert d0["regs"]["write_instr_per_thread"] > d["regs"]["write_instr_per_thread"]
+
+
+@pytest.mark.parametrize("name,c", PLAN_CASES[2:])
+def test_tma_store_plan_conflict_free(name, c):
+    """TMA load + TMA store: the readers' 16-byte reads of the source image and
+    16-byte writes of the destination image are both conflict-free (brute
+    force), using XOR "diagonal" lanes where single bits cannot serve both
+    (the transposes); both tiles are TMA boxes of <= 5 dims."""
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    w = c["elem_bytes"]
+    d = ll.plan_describe(A, B, 8 * w, "smem_tma_store")
+    assert d["path"] == "smem_tma_store"
+    for side in ("src", "dst"):
+        assert 1 <= d["tma"][side]["ndim"] <= 5
+    tr, nr = _reader_wavefronts(d, "r")
+    tw, nw = _reader_wavefronts(d, "w")
+    assert tr == 4 * nr and tw == 4 * nw
+    if name.startswith("cfg3"):
+        assert d["diagonal_lanes"] >= 3   # a transpose needs the diagonals
