@@ -190,12 +190,19 @@ typedef enum {
                             with stmatrix / ldmatrix where the layout is divisible by their tile
                             (P:588-591), else vectorised st/ld.shared.  Needs reg/lane/warp/block
                             layouts with equal lane (5) and warp (<= 3) bits, identical block
-                            columns and elements of <= 4 bytes; else LL_ERR_UNSUPPORTED. */
-  LL_PATH_SMEM_TMA_STORE = 10 /* as SMEM_TMA, and the destination tile is written to a second
+                            columns and elements of <= 4 bytes; else LL_ERR_UNSUPPORTED.
+                            Cost model: a warp-local pair whose shuffle exchange needs <= 4
+                            rounds (knob regs_shuffle_max_rounds; 0 = never) runs as
+                            LL_PATH_REGS_SHUFFLE (measured faster in-kernel on B200). */
+  LL_PATH_SMEM_TMA_STORE = 10, /* as SMEM_TMA, and the destination tile is written to a second
                             hardware-swizzled shared-memory image and stored by one TMA tensor
                             store; the readers' lanes (possibly XOR "diagonals" of tile bits)
                             are chosen so reads AND writes are conflict-free.  No thread issues a
                             global load or store. */
+  LL_PATH_REGS_SHUFFLE = 11 /* register-faithful warp-shuffle exchange for warp-local
+                            pairs ((B^-1 o A)_warp = I), in a kernel specialised for the
+                            plan at run time (NVRTC: every register index a compile-time
+                            constant); LL_ERR_UNSUPPORTED otherwise. */
 } ll_path;
 
 typedef struct {
@@ -242,6 +249,22 @@ ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_
 ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst,
                                 ll_layout dst_layout, int elem_bits, int64_t batch, int reps,
                                 long long* cycles, ll_stream stream);
+
+/* The CUDA source of the run-time specialised LL_PATH_REGS_SHUFFLE kernel for
+ * (src_layout, dst_layout) into buf (cap bytes, NUL-terminated; *need = the
+ * size needed); compile != 0 instead compiles it with NVRTC for sm_100a (no
+ * device needed) and returns {"compiled": true, "cubin_bytes": n}.
+ * LL_ERR_UNSUPPORTED if the pair has no such plan or NVRTC fails. */
+ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int compile,
+                        char* buf, size_t cap, size_t* need);
+
+/* The same for path LL_PATH_REGS (shared memory, repeats A -> B) or
+ * LL_PATH_REGS_SHUFFLE (warp shuffles; each repetition converts A -> B -> A
+ * so the data are loop-carried, i.e. `reps` repetitions are 2 * reps
+ * conversions).  LL_ERR_ARG for any other path. */
+ll_status ll_convert_inkernel_timed(const void* src, ll_layout src_layout, void* dst,
+                                    ll_layout dst_layout, int elem_bits, int64_t batch, int path,
+                                    int reps, long long* cycles, ll_stream stream);
 
 /* Multi-GPU shard: convert only shard `shard` of `n_shards`
  * (a power of two).  The tensor is split along the top log2(n_shards) index

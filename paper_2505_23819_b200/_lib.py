@@ -76,7 +76,11 @@ _lib.ll_shard_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_in
 _lib.ll_left_divide.argtypes = [_VP, _VP, ctypes.POINTER(_VP)]
 _lib.ll_convert_regs_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int64,
                                        ctypes.c_int, _VP, _VP]
-for _f in ("ll_left_divide", "ll_convert_regs_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+_lib.ll_convert_inkernel_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int64,
+                                           ctypes.c_int, ctypes.c_int, _VP, _VP]
+_lib.ll_jit_source.argtypes = [_VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                               ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+for _f in ("ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
@@ -88,7 +92,7 @@ STATUS = {0: "LL_OK", 1: "LL_ERR_ARG", 2: "LL_ERR_SHAPE", 3: "LL_ERR_LABEL",
           7: "LL_ERR_UNSUPPORTED", 8: "LL_ERR_CUDA", 9: "LL_ERR_OOM"}
 PATHS = {"auto": 0, "copy": 1, "smem": 2, "shuffle": 3, "generic": 4, "smem_noswizzle": 5,
          "smem_async": 6, "smem_padded": 7, "smem_tma": 8,
-         "regs": 9, "smem_tma_store": 10}
+         "regs": 9, "smem_tma_store": 10, "regs_shuffle": 11}
 
 
 class LLError(RuntimeError):
@@ -302,14 +306,30 @@ def convert(src, A, dst, B, elem_bits, path="auto", batch=1, max_ctas=0, stream=
                               ctypes.byref(o), _stream_handle(stream)))
 
 
-def convert_regs_timed(src, A, dst, B, elem_bits, reps=1, cycles=None, batch=1, stream=None):
-    """ll_convert_regs_timed: register-faithful conversion, the exchange
-    repeated `reps` times in-kernel; per-CTA clock64 cycles into `cycles`
-    (an int64 device tensor) when given."""
-    _check(_lib.ll_convert_regs_timed(_ptr(src), A.handle, _ptr(dst), B.handle, int(elem_bits),
-                                      int(batch), int(reps),
-                                      _ptr(cycles) if cycles is not None else None,
-                                      _stream_handle(stream)))
+def convert_regs_timed(src, A, dst, B, elem_bits, reps=1, cycles=None, batch=1, stream=None,
+                       path="regs"):
+    """ll_convert_inkernel_timed: register-faithful conversion (path "regs":
+    shared memory; "regs_shuffle": warp shuffles, A -> B -> A per rep), the
+    exchange repeated `reps` times in-kernel; per-CTA clock64 cycles into
+    `cycles` (an int64 device tensor) when given."""
+    _check(_lib.ll_convert_inkernel_timed(_ptr(src), A.handle, _ptr(dst), B.handle,
+                                          int(elem_bits), int(batch),
+                                          PATHS[path] if isinstance(path, str) else int(path),
+                                          int(reps), _ptr(cycles) if cycles is not None else None,
+                                          _stream_handle(stream)))
+
+
+def jit_source(A, B, elem_bits, compile=False):
+    """ll_jit_source: the NVRTC-specialised regs_shuffle kernel source (or,
+    with compile=True, the compile result as a dict)."""
+    need = ctypes.c_size_t()
+    _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), int(compile), None, 0,
+                              ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), int(compile), buf, need.value,
+                              ctypes.byref(need)))
+    out = buf.value.decode()
+    return json.loads(out) if compile else out
 
 
 def convert_shard(src_slice, A, dst_slice, B, elem_bits, n_shards, shard, path="auto",

@@ -21,7 +21,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernel_smem.cu", "kernel_async.cu", "kernel_tma.cu", "kernel_regs.cu", "kernel_shuffle.cu", "kernel_misc.cu"]
-CPP_SOURCES = ["core.cpp", "planner.cpp", "capi.cpp"]
+CPP_SOURCES = ["core.cpp", "planner.cpp", "capi.cpp", "jit.cpp"]
 HEADERS = ["core.hpp", "plan.hpp", "planner.hpp", "kernels.hpp", "device_common.cuh"]
 
 
@@ -69,7 +69,10 @@ def build(force=False, verbose=False):
                 sys.stderr.write(log)
     if force or not os.path.exists(OUT) or _mtime(OUT) < max(_mtime(o) for o in objs):
         tmp = OUT + ".tmp"
+        # NVRTC (jit.cpp) from the toolkit, found through the rpath at run time
+        lib64 = os.path.join(CUDA, "lib64")
         cmd = [NVCC, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs,
+               "-L" + lib64, "-lnvrtc", "-Xlinker", "-rpath," + lib64,
                "-Xlinker", "-soname,libll_b200.so"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

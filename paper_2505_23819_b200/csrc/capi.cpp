@@ -416,6 +416,14 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
       ++g_launches;
       return cuda_status(ll::launch_convert_async(P->sp, w, P->nv, src, dst, max_ctas, st, rg),
                          "ll_convert (async smem kernel)");
+    case LL_PATH_REGS_SHUFFLE: {
+      if (n_shards > 1) return fail(LL_ERR_UNSUPPORTED, "ll_convert_shard: the regs_shuffle path is not shardable");
+      ++g_launches;
+      std::string err;
+      cudaError_t e = ll::launch_regs_shuffle(P->rsp, w, src, dst, max_ctas, 1, nullptr, st, &err);
+      if (e != cudaSuccess && !err.empty()) return fail(LL_ERR_CUDA, "ll_convert (regs_shuffle): " + err);
+      return cuda_status(e, "ll_convert (register-faithful shuffle kernel)");
+    }
     case LL_PATH_REGS:
       if (n_shards > 1) return fail(LL_ERR_UNSUPPORTED, "ll_convert_shard: the regs path is not shardable");
       ++g_launches;
@@ -452,24 +460,63 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
   });
 }
 
+ll_status ll_convert_inkernel_timed(const void* src, ll_layout src_layout, void* dst,
+                                    ll_layout dst_layout, int elem_bits, int64_t batch, int path,
+                                    int reps, long long* cycles, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_convert_inkernel_timed");
+    check_layout(dst_layout, "ll_convert_inkernel_timed");
+    const int w = elem_bytes(elem_bits);
+    if (!src || !dst) return fail(LL_ERR_ARG, "ll_convert_inkernel_timed: NULL buffer");
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+      return fail(LL_ERR_ARG, "ll_convert_inkernel_timed: buffers must be 16-byte aligned");
+    if (reps < 1) return fail(LL_ERR_ARG, "ll_convert_inkernel_timed: reps < 1");
+    if (path != LL_PATH_REGS && path != LL_PATH_REGS_SHUFFLE)
+      return fail(LL_ERR_ARG, "ll_convert_inkernel_timed: path must be LL_PATH_REGS or LL_PATH_REGS_SHUFFLE");
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, path, batch > 0 ? batch : 1);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    ++g_launches;
+    if (P->path == LL_PATH_REGS)
+      return cuda_status(ll::launch_convert_regs(P->rp, w, src, dst, 0, reps, cycles, st),
+                         "ll_convert_inkernel_timed");
+    std::string err;
+    cudaError_t e = ll::launch_regs_shuffle(P->rsp, w, src, dst, 0, reps, cycles, st, &err);
+    if (e != cudaSuccess && !err.empty()) return fail(LL_ERR_CUDA, "ll_convert_inkernel_timed: " + err);
+    return cuda_status(e, "ll_convert_inkernel_timed");
+  });
+}
+
+ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int compile,
+                        char* buf, size_t cap, size_t* need) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_jit_source");
+    check_layout(dst_layout, "ll_jit_source");
+    const int w = elem_bytes(elem_bits);
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_REGS_SHUFFLE, 1);
+    std::string out = ll::regs_shuffle_kernel_source(P->rsp, w);
+    if (compile) {
+      std::string log;
+      size_t cubin = 0;
+      const bool ok = ll::regs_shuffle_compile_check(P->rsp, w, &log, &cubin);
+      out = std::string("{\"compiled\":") + (ok ? "true" : "false") + ",\"cubin_bytes\":" +
+            std::to_string(cubin) + "}";
+      if (!ok) return fail(LL_ERR_UNSUPPORTED, "ll_jit_source: NVRTC failed: " + log.substr(0, 300));
+    }
+    if (need) *need = out.size() + 1;
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, out.size());
+      std::memcpy(buf, out.data(), n);
+      buf[n] = 0;
+    }
+    return LL_OK;
+  });
+}
+
 ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst,
                                 ll_layout dst_layout, int elem_bits, int64_t batch, int reps,
                                 long long* cycles, ll_stream stream) {
-  return guarded([&]() -> ll_status {
-    check_layout(src_layout, "ll_convert_regs_timed");
-    check_layout(dst_layout, "ll_convert_regs_timed");
-    const int w = elem_bytes(elem_bits);
-    if (!src || !dst) return fail(LL_ERR_ARG, "ll_convert_regs_timed: NULL buffer");
-    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
-      return fail(LL_ERR_ARG, "ll_convert_regs_timed: buffers must be 16-byte aligned");
-    if (reps < 1) return fail(LL_ERR_ARG, "ll_convert_regs_timed: reps < 1");
-    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_REGS,
-                                  batch > 0 ? batch : 1);
-    ++g_launches;
-    return cuda_status(ll::launch_convert_regs(P->rp, w, src, dst, 0, reps, cycles,
-                                               reinterpret_cast<cudaStream_t>(stream)),
-                       "ll_convert_regs_timed");
-  });
+  return ll_convert_inkernel_timed(src, src_layout, dst, dst_layout, elem_bits, batch,
+                                   LL_PATH_REGS, reps, cycles, stream);
 }
 
 ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_t* scales,

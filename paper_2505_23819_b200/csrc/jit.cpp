@@ -1,0 +1,270 @@
+// jit.cpp -- run-time specialised kernels (NVRTC) for the register-faithful
+// warp-shuffle exchange (LL_PATH_REGS_SHUFFLE).
+//
+// The paper lowers a conversion inside a compiler, so every register index of
+// the 2^|R| shuffle rounds is a constant and the uniform word permutations
+// (alpha, eps) are free register renames; only the lane-dependent parts
+// (beta / zeta selects, delta source lane) cost instructions.  A generic
+// kernel would have to apply alpha / eps as run-time register moves, so this
+// path generates CUDA source for the plan, compiles it for sm_100a with NVRTC
+// once per plan, and launches it through the driver API (entry points from
+// cudaGetDriverEntryPoint; no link-time libcuda dependency).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+
+#include "planner.hpp"
+
+namespace ll {
+
+namespace {
+
+typedef CUresult (*PFN_LoadData)(CUmodule*, const void*);
+typedef CUresult (*PFN_GetFunction)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*PFN_Launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
+                               unsigned, unsigned, CUstream, void**, void**);
+
+template <class F>
+F entry(const char* name) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(f);
+}
+
+// element-bit swap (a < b) of the thread's register file, compile-time
+// (same semantics as device_common.cuh apply_swap), emitted as source text
+void emit_swap(std::ostringstream& o, int W, int NW, int a, int b, const char* R) {
+  auto word_swap = [&](int A, int B) {
+    for (int i = 0; i < NW; ++i)
+      if (((i >> A) & 1) == 0 && ((i >> B) & 1) == 1) {
+        const int j = i ^ ((1 << A) | (1 << B));
+        o << "  { unsigned t_ = " << R << "[" << i << "]; " << R << "[" << i << "] = " << R << "[" << j
+          << "]; " << R << "[" << j << "] = t_; }\n";
+      }
+  };
+  auto sub_swap = [&](int B, unsigned lo, unsigned hi) {
+    for (int i = 0; i < NW; ++i)
+      if (((i >> B) & 1) == 0) {
+        const int j = i | (1 << B);
+        o << "  { unsigned x_ = " << R << "[" << i << "], y_ = " << R << "[" << j << "]; " << R << "["
+          << i << "] = __byte_perm(x_, y_, " << lo << "u); " << R << "[" << j
+          << "] = __byte_perm(x_, y_, " << hi << "u); }\n";
+      }
+  };
+  if (W == 4) {
+    word_swap(a, b);
+  } else if (W == 2) {
+    if (a == 0) sub_swap(b - 1, 0x5410u, 0x7632u);
+    else word_swap(a - 1, b - 1);
+  } else {
+    if (a == 0 && b == 1) {
+      for (int i = 0; i < NW; ++i)
+        o << "  " << R << "[" << i << "] = __byte_perm(" << R << "[" << i << "], 0u, " << 0x3120u << "u);\n";
+    } else if (a == 0) {
+      sub_swap(b - 2, 0x6240u, 0x7351u);
+    } else if (a == 1) {
+      sub_swap(b - 2, 0x5410u, 0x7632u);
+    } else {
+      word_swap(a - 2, b - 2);
+    }
+  }
+}
+
+// one direction of the exchange: D = exchange(S)
+void emit_dir(std::ostringstream& o, const ShuffleDir& d, int NW, const char* S, const char* D,
+              const char* pfx) {
+  o << "  {\n    unsigned T_[" << NW << "];\n";
+  for (int k = 0; k < NW; ++k) o << "    T_[" << k << "] = " << S << "[" << k << "];\n";
+  auto lane_xor = [&](const char* A, uint32_t any, const char* mask) {
+    for (int b = 0; (1 << b) < NW; ++b) {
+      if (!((any >> b) & 1)) continue;
+      o << "    { const bool q_ = (" << mask << " >> " << b << ") & 1;\n";
+      for (int k = 0; k < NW; ++k)
+        if (((k >> b) & 1) == 0) {
+          const int j = k | (1 << b);
+          o << "      { unsigned x_ = " << A << "[" << k << "], y_ = " << A << "[" << j << "]; " << A
+            << "[" << k << "] = q_ ? y_ : x_; " << A << "[" << j << "] = q_ ? x_ : y_; }\n";
+        }
+      o << "    }\n";
+    }
+  };
+  lane_xor("T_", d.beta_any, (std::string(pfx) + "b").c_str());
+  // every round reads the receiving lane itself: a register permutation
+  // inside each thread, no shuffle
+  bool local = true;
+  for (int k = 0; k < NW; ++k) local = local && d.gamma[k] == 0;
+  for (int c = 0; c < 5; ++c) local = local && d.delta[c] == (1u << c);
+  for (int k = 0; k < NW; ++k) {
+    if (local)
+      o << "    " << D << "[" << d.eps[k] << "] = T_[" << d.alpha[k] << "];\n";
+    else
+      o << "    " << D << "[" << d.eps[k] << "] = __shfl_sync(0xffffffffu, T_[" << d.alpha[k] << "], "
+        << (int)d.gamma[k] << " ^ " << pfx << "d);\n";
+  }
+  lane_xor(D, d.zeta_any, (std::string(pfx) + "z").c_str());
+  o << "  }\n";
+}
+
+std::string regs_shuffle_source(const RegsShufflePlan& p, int W) {
+  const int NW = p.nwords, NT = 32 << p.nw, TB = NW * 4;
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ") ll_regs_shfl(\n"
+    << "    const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,\n"
+    << "    long long n_tiles, long long tile_bytes, int reps, long long* cycles) {\n"
+    << "  const int tid = threadIdx.x, lane = tid & 31;\n"
+    << "  unsigned fb = 0, fz = 0, fd = 0, bb = 0, bz = 0, bd = 0;\n";
+  for (int c = 0; c < 5; ++c)
+    o << "  if (lane & " << (1 << c) << ") { fb ^= " << p.fwd.beta[c] << "u; fz ^= " << p.fwd.zeta[c]
+      << "u; fd ^= " << p.fwd.delta[c] << "u; bb ^= " << p.bwd.beta[c] << "u; bz ^= " << p.bwd.zeta[c]
+      << "u; bd ^= " << p.bwd.delta[c] << "u; }\n";
+  o << "  for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {\n"
+    << "  const unsigned char* sp = src + t * tile_bytes + (long long)tid * " << TB << ";\n"
+    << "  unsigned char* dp = dst + t * tile_bytes + (long long)tid * " << TB << ";\n"
+    << "  unsigned R[" << NW << "], Q[" << NW << "];\n";
+  if (TB >= 16) {
+    for (int u = 0; u < NW / 4; ++u)
+      o << "  { uint4 v_ = __ldg(reinterpret_cast<const uint4*>(sp) + " << u << "); R[" << 4 * u
+        << "] = v_.x; R[" << 4 * u + 1 << "] = v_.y; R[" << 4 * u + 2 << "] = v_.z; R[" << 4 * u + 3
+        << "] = v_.w; }\n";
+  } else {
+    for (int u = 0; u < NW; ++u)
+      o << "  R[" << u << "] = __ldg(reinterpret_cast<const unsigned*>(sp) + " << u << ");\n";
+  }
+  for (auto& s : p.swaps) emit_swap(o, W, NW, s.first, s.second, "R");
+  o << "  long long c0_ = 0;\n  if (cycles && tid == 0) c0_ = clock64();\n"
+    << "  for (int rep = 0; rep < reps; ++rep) {\n";
+  emit_dir(o, p.fwd, NW, "R", "Q", "f");
+  emit_dir(o, p.bwd, NW, "Q", "R", "b");
+  o << "  }\n  if (cycles && tid == 0 && t == blockIdx.x) cycles[blockIdx.x] = clock64() - c0_;\n";
+  emit_dir(o, p.fwd, NW, "R", "Q", "f");
+  if (TB >= 16) {
+    for (int u = 0; u < NW / 4; ++u)
+      o << "  reinterpret_cast<uint4*>(dp)[" << u << "] = make_uint4(Q[" << 4 * u << "], Q["
+        << 4 * u + 1 << "], Q[" << 4 * u + 2 << "], Q[" << 4 * u + 3 << "]);\n";
+  } else {
+    for (int u = 0; u < NW; ++u) o << "  reinterpret_cast<unsigned*>(dp)[" << u << "] = Q[" << u << "];\n";
+  }
+  o << "  }\n}\n";
+  return o.str();
+}
+
+struct JitEntry {
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+};
+std::mutex g_jit_mu;
+std::map<std::pair<int, std::string>, JitEntry> g_jit;
+
+cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_jit_mu);
+  auto key = std::make_pair(dev, src);
+  auto it = g_jit.find(key);
+  if (it != g_jit.end()) {
+    *fn = it->second.fn;
+    return cudaSuccess;
+  }
+  static PFN_LoadData load = entry<PFN_LoadData>("cuModuleLoadData");
+  static PFN_GetFunction getf = entry<PFN_GetFunction>("cuModuleGetFunction");
+  if (!load || !getf) {
+    *err = "driver entry points unavailable";
+    return cudaErrorNotSupported;
+  }
+  cudaFree(nullptr);  // make sure the runtime's primary context is current
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_regs_shfl.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    *err = "nvrtcCreateProgram failed";
+    return cudaErrorUnknown;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    *err = "NVRTC: " + log.substr(0, 400);
+    return cudaErrorUnknown;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::string cubin(n, '\0');
+  nvrtcGetCUBIN(prog, &cubin[0]);
+  nvrtcDestroyProgram(&prog);
+  JitEntry e;
+  if (load(&e.mod, cubin.data()) != CUDA_SUCCESS ||
+      getf(&e.fn, e.mod, "ll_regs_shfl") != CUDA_SUCCESS) {
+    *err = "cuModuleLoadData / cuModuleGetFunction failed";
+    return cudaErrorUnknown;
+  }
+  g_jit[key] = e;
+  *fn = e.fn;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+// Compile only (no device needed): NVRTC log / status for tests.
+bool regs_shuffle_compile_check(const RegsShufflePlan& p, int w, std::string* log, size_t* cubin_bytes) {
+  const std::string src = regs_shuffle_source(p, w);
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_regs_shfl.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    return false;
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device"};
+  const bool ok = nvrtcCompileProgram(prog, 3, opts) == NVRTC_SUCCESS;
+  size_t n = 0;
+  nvrtcGetProgramLogSize(prog, &n);
+  log->assign(n, '\0');
+  if (n) nvrtcGetProgramLog(prog, &(*log)[0]);
+  *cubin_bytes = 0;
+  if (ok) nvrtcGetCUBINSize(prog, cubin_bytes);
+  nvrtcDestroyProgram(&prog);
+  return ok;
+}
+
+std::string regs_shuffle_kernel_source(const RegsShufflePlan& p, int w) {
+  return regs_shuffle_source(p, w);
+}
+
+cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src, void* dst,
+                                int max_ctas, int reps, long long* cycles, cudaStream_t st,
+                                std::string* err) {
+  if (reps < 1 || w > 4) return cudaErrorInvalidValue;
+  CUfunction fn = nullptr;
+  cudaError_t e = get_kernel(regs_shuffle_source(p, w), &fn, err);
+  if (e != cudaSuccess) return e;
+  static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
+  if (!launch) return cudaErrorNotSupported;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = std::min<int64_t>(p.n_tiles, (int64_t)sms * 16);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+  if (grid <= 0) return cudaSuccess;
+  long long nt = p.n_tiles, tb = p.tile_bytes;
+  const void* s = src;
+  void* d = dst;
+  void* args[] = {(void*)&s, (void*)&d, (void*)&nt, (void*)&tb, (void*)&reps, (void*)&cycles};
+  if (launch(fn, (unsigned)grid, 1, 1, 32u << p.nw, 1, 1, 0, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    *err = "cuLaunchKernel failed";
+    return cudaErrorLaunchFailure;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ll

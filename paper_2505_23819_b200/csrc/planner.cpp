@@ -146,7 +146,8 @@ bool set_planner_knob(const std::string& name, int value) {
   if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule" &&
       name != "run_bytes" && name != "tile_order" && name != "host_chunk_mb" &&
       name != "host_slots" && name != "tma_run_bytes" && name != "tma_thread_bytes" &&
-      name != "tma_tile_bytes" && name != "tma_force_swizzle" && name != "regs_matrix")
+      name != "tma_tile_bytes" && name != "tma_force_swizzle" && name != "regs_matrix" &&
+      name != "regs_shuffle_max_rounds")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -1579,8 +1580,18 @@ bool plan_tma_store(ConvertPlan& P, const std::vector<u64>& X, std::ostringstrea
 // (generalised vectorisation) or stmatrix / ldmatrix rows when its
 // layout divided by the tile T = id^{reg,offset}_k x id^{thread,offset}_2
 // (left division P:354-362) exists -- checked on S^{-1} o L.
-bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vector<u64>& X,
-               std::ostringstream& js) {
+// Common frame of the register-faithful plans: both layouts are reg / lane /
+// warp / block with 5 lane bits, equal reg and warp bits and identical block
+// columns; tile vectors in A's (reg, lane, warp) index space; B's word must
+// hold elements A holds in registers (load-side prmt swaps).
+struct RegsFrame {
+  int w, lw, nr, nw, d, n, kw, LB, NW;
+  std::vector<std::pair<int, int>> swaps;
+  std::vector<u64> WB, Aw, Bw, Al, Bl, Awp, Bwp;
+};
+
+bool regs_frame(const ConvertPlan& P, const Layout& A, const Layout& B, const std::vector<u64>& X,
+                RegsFrame& f) {
   const int w = P.w;
   if (w > 4 || P.nA != P.nB) return false;
   auto dims_ok = [](const Layout& L) {
@@ -1635,6 +1646,21 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
   for (int u = 0; u < LB; ++u) { Aw.push_back(cur[kw + u]); Bw.push_back(X[kw + u]); }
   for (int b = 0; b < 5; ++b) { Al.push_back(e(nr + b)); Bl.push_back(X[nr + b]); }
   for (int b = 0; b < nw; ++b) { Awp.push_back(e(nr + 5 + b)); Bwp.push_back(X[nr + 5 + b]); }
+  f.w = w; f.lw = lw; f.nr = nr; f.nw = nw; f.d = d; f.n = n; f.kw = kw; f.LB = LB; f.NW = NW;
+  f.swaps = swaps;
+  f.WB = WB; f.Aw = Aw; f.Bw = Bw; f.Al = Al; f.Bl = Bl; f.Awp = Awp; f.Bwp = Bwp;
+  return true;
+}
+
+bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vector<u64>& X,
+               std::ostringstream& js) {
+  RegsFrame f;
+  if (!regs_frame(P, A, B, X, f)) return false;
+  const int w = f.w, lw = f.lw, nr = f.nr, nw = f.nw, d = f.d, n = f.n, kw = f.kw, LB = f.LB, NW = f.NW;
+  (void)nr;
+  auto e = [](int i) { return u64(1) << i; };
+  const auto& swaps = f.swaps;
+  const auto &WB = f.WB, &Aw = f.Aw, &Bw = f.Bw, &Al = f.Al, &Bl = f.Bl, &Awp = f.Awp, &Bwp = f.Bwp;
   auto pos = [](const std::vector<u64>& v, u64 x) {
     auto it = std::find(v.begin(), v.end(), x);
     return it == v.end() ? -1 : (int)(it - v.begin());
@@ -1836,6 +1862,58 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
   return true;
 }
 
+// Register-faithful warp-shuffle plan (LL_PATH_REGS_SHUFFLE): warp-local
+// pairs only ((B^{-1} o A)_warp = I): both directions of the paper's
+// exchange on the layouts' own registers and lanes.
+bool plan_regs_shuffle(ConvertPlan& P, const Layout& A, const Layout& B,
+                       const std::vector<u64>& X, std::ostringstream& js) {
+  RegsFrame f;
+  if (!regs_frame(P, A, B, X, f)) return false;
+  if (f.NW > LL_MAX_GRAN) return false;
+  for (int b = 0; b < f.nw; ++b)
+    if (f.Bwp[b] != f.Awp[b]) return false;
+  const u64 wmask = (u64(1) << (f.nr + 5)) - 1;  // (reg, lane) space of one warp
+  for (u64 v : f.Bw) if (v & ~wmask) return false;
+  for (u64 v : f.Bl) if (v & ~wmask) return false;
+  ShuffleCore fw = shuffle_core(f.Aw, f.Al, f.Bw, f.Bl, f.LB);
+  ShuffleCore bw = shuffle_core(f.Bw, f.Bl, f.Aw, f.Al, f.LB);
+  if (!fw.ok || !bw.ok) return false;
+  RegsShufflePlan& q = P.rsp;
+  q = RegsShufflePlan{};
+  q.nw = f.nw;
+  q.nwords = f.NW;
+  q.tile_bytes = int64_t(f.w) << f.d;
+  q.n_tiles = (int64_t(1) << (f.n - f.d)) * P.batch;
+  q.swaps = f.swaps;
+  auto fill = [&](const ShuffleCore& c, ShuffleDir& dd) {
+    for (int k = 0; k < c.rounds; ++k) {
+      int a = 0, e = 0;
+      for (int j = 0; j < f.LB; ++j)
+        if ((k >> j) & 1) { a ^= (int)c.alpha[j]; e ^= (int)c.epsm[j]; }
+      dd.alpha.push_back(a);
+      dd.eps.push_back(e);
+      dd.gamma.push_back(c.gamma[k]);
+    }
+    for (int b = 0; b < 5; ++b) { dd.beta[b] = c.beta[b]; dd.zeta[b] = c.zeta[b]; dd.delta[b] = c.delta[b]; }
+    dd.beta_any = c.beta_any;
+    dd.zeta_any = c.zeta_any;
+  };
+  fill(fw, q.fwd);
+  fill(bw, q.bwd);
+  P.nv = f.NW;
+  P.tile_bits = f.d;
+  // a register permutation (identical lanes) costs no shuffle round
+  P.shuffle_rounds = f.Al == f.Bl ? 0 : fw.rounds;
+  js << ",\"regs_shuffle\":{\"warps_log2\":" << f.nw << ",\"words_per_thread\":" << f.NW
+     << ",\"rounds\":" << fw.rounds << ",\"I\":" << vec_json(fw.I) << ",\"E\":" << vec_json(fw.E)
+     << ",\"F\":" << vec_json(fw.F) << ",\"G\":" << vec_json(fw.Gv) << ",\"R\":" << vec_json(fw.R)
+     << ",\"beta_lane\":" << u32_json(q.fwd.beta, 5) << ",\"zeta_lane\":" << u32_json(q.fwd.zeta, 5)
+     << ",\"delta_lane\":" << u32_json(q.fwd.delta, 5) << ",\"swaps\":" << f.swaps.size()
+     << ",\"exchange\":\"" << (f.Al == f.Bl ? "register permutation" : "warp shuffles") << "\""
+     << ",\"n_tiles\":" << q.n_tiles << "}";
+  return true;
+}
+
 std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B, int w,
                                                 int path_req, int64_t batch, int op) {
   if (!A.same_tensor(B)) throw Error(LL_ERR_SHAPE, "convert: source and destination layouts map to different tensors");
@@ -1911,6 +1989,31 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
                                       "bit permutation or a tile needs more than 5 TMA box dims");
     }
   }
+  if (path == LL_PATH_REGS_SHUFFLE) {
+    std::ostringstream js2;
+    if (plan_regs_shuffle(*P, A, B, X, js2)) {
+      js << js2.str();
+    } else {
+      throw Error(LL_ERR_UNSUPPORTED,
+                  "regs_shuffle path requested but the pair is not a warp-local register-faithful "
+                  "exchange ((B^-1 o A)_warp must be the identity, P:624)");
+    }
+  }
+  if (path == LL_PATH_REGS) {
+    // cost model (measured in-kernel on B200,
+    // profiles/r01/regs2): the paper's shuffle exchange beats the
+    // shared-memory round trip up to 4 rounds (26-30 vs 30-46 cycles) and
+    // loses from 8 rounds on (16 rounds: 166 vs 47; 64: 1100 vs 559); a
+    // warp-local pair with identical lanes is a register permutation
+    const int max_rounds = planner_knob("regs_shuffle_max_rounds", 4);
+    if (max_rounds > 0) {
+      std::ostringstream js2;
+      if (plan_regs_shuffle(*P, A, B, X, js2) && P->shuffle_rounds <= max_rounds) {
+        js << js2.str();
+        path = LL_PATH_REGS_SHUFFLE;
+      }
+    }
+  }
   if (path == LL_PATH_REGS) {
     std::ostringstream js2;
     if (plan_regs(*P, A, B, X, js2)) {
@@ -1927,7 +2030,8 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
   if (path == LL_PATH_GENERIC) fill_generic(*P, X);
   P->path = path;
   static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle",
-                                "smem_async", "smem_padded", "smem_tma", "regs", "smem_tma_store"};
+                                "smem_async", "smem_padded", "smem_tma", "regs", "smem_tma_store",
+                                "regs_shuffle"};
   js << ",\"path\":\"" << names[path] << "\"}";
   P->json = js.str();
   return P;

@@ -2,6 +2,8 @@
 // optimal swizzle (paper Sec. 5.4 / Appendix), gather plans, plan cache.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <memory>
 #include <string>
 #include <vector>
@@ -27,6 +29,26 @@ SwizzleResult optimal_swizzle(const std::vector<u64>& A_lane, const std::vector<
 // Lemma: wavefronts per instruction n * c, c from L_bank (A13).
 int lemma_wavefronts(const SwizzleResult& s, const std::vector<u64>& lanes, int elem_bytes);
 
+// Register-faithful warp-shuffle plan (LL_PATH_REGS_SHUFFLE): the paper's
+// exchange on the layouts' own registers and lanes, for both
+// directions (A -> B, and B -> A for loop-carried in-kernel timing).  Per
+// round k of 2^|R|: every lane l sends word alpha_k ^ beta(l) (after the
+// beta selects: T = R[. ^ beta(l)], send T[alpha_k]) to lane
+// gamma_k ^ delta(l), which stores it at eps_k ^ zeta(l).  Executed by a
+// kernel specialised for the plan at run time (NVRTC, jit.cpp): every
+// register index is a compile-time constant, as in the paper's compiler.
+struct ShuffleDir {
+  std::vector<int> alpha, eps, gamma;      // per round k
+  uint32_t beta[5] = {0}, zeta[5] = {0}, delta[5] = {0};
+  uint32_t beta_any = 0, zeta_any = 0;
+};
+struct RegsShufflePlan {
+  int nw = 0, nwords = 0;
+  int64_t tile_bytes = 0, n_tiles = 0;
+  std::vector<std::pair<int, int>> swaps;  // load-side element-bit swaps (A order -> B's words)
+  ShuffleDir fwd, bwd;
+};
+
 struct ConvertPlan {
   int path = LL_PATH_GENERIC;
   int w = 0;
@@ -43,6 +65,7 @@ struct ConvertPlan {
   TmaDesc td{};      // LL_PATH_SMEM_TMA (source box)
   TmaDesc td_dst{};  // LL_PATH_SMEM_TMA_STORE (destination box)
   RegsPlan rp{};     // LL_PATH_REGS
+  RegsShufflePlan rsp;  // LL_PATH_REGS_SHUFFLE
   int nv = 0, g = 0;
   int tile_bits = 0, r = 0, gw = 0;
   int pred_wf_ld = 0, pred_wf_st = 0;   // wavefronts per STS / LDS instruction
@@ -77,6 +100,13 @@ bool set_planner_knob(const std::string& name, int value);
 // path_req: ll_path value (AUTO lets the planner choose).  Throws ll::Error.
 std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layout& B, int w,
                                                     int path_req, int64_t batch, int op = 0);
+// jit.cpp: the NVRTC-specialised register-faithful shuffle kernel
+std::string regs_shuffle_kernel_source(const RegsShufflePlan& p, int w);
+bool regs_shuffle_compile_check(const RegsShufflePlan& p, int w, std::string* log, size_t* cubin_bytes);
+cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src, void* dst,
+                                int max_ctas, int reps, long long* cycles, cudaStream_t st,
+                                std::string* err);
+
 std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
                                                       int path_req, int64_t batch);
 

@@ -434,3 +434,42 @@ def test_tma_store_plan_conflict_free(name, c):
     assert tr == 4 * nr and tw == 4 * nw
     if name.startswith("cfg3"):
         assert d["diagonal_lanes"] >= 3   # a transpose needs the diagonals
+
+
+def test_regs_shuffle_plan_and_jit_compiles():
+    """Register-faithful warp-shuffle plan for the warp-aligned config-2 pair
+    (V = {j0}, |I| = 1, |G| = 4, |R| = 6 -> 64 rounds) and
+    the NVRTC compile of the kernel specialised for it (no device needed);
+    the non-warp-local config 2 is refused."""
+    c = configs.cfg2w(batch_bits=1)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    d = ll.plan_describe(A, B, 16, "regs_shuffle")["regs_shuffle"]
+    assert d["rounds"] == 64 and len(d["I"]) == 1 and len(d["G"]) == 4 and len(d["R"]) == 6
+    res = ll.jit_source(A, B, 16, compile=True)
+    assert res["compiled"] and res["cubin_bytes"] > 0
+    src = ll.jit_source(A, B, 16)
+    assert src.count("__shfl_sync") == 3 * 64     # fwd + bwd in the loop, one final fwd
+    c2 = configs.cfg2(batch_bits=1)
+    with pytest.raises(ll.LLError):
+        ll.plan_describe(ll.Layout.from_spec(c2["A"]), ll.Layout.from_spec(c2["B"]), 16, "regs_shuffle")
+
+
+def test_regs_cost_model_prefers_few_round_shuffles():
+    """The regs path's cost model (measured crossover, DESIGN 6b): a
+    warp-local pair with <= 4 shuffle rounds runs as the shuffle exchange, the
+    64-round warp-aligned config 2 stays on shared memory; knob 0 disables."""
+    c = configs.cfg2w(batch_bits=1)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    assert ll.plan_describe(A, B, 16, "regs")["path"] == "regs"          # 64 rounds
+    out = [("i", 6), ("j", 6)]
+    A2 = ll.Layout.from_spec(configs.spec([("reg", ["j0", "j1"]), ("lane", ["j2", "j3", "i0", "i1", "i2"]),
+                                           ("warp", ["i3", "i4"]), ("block", ["j4", "j5", "i5"])], out))
+    B2 = ll.Layout.from_spec(configs.spec([("reg", ["j0", "i0"]), ("lane", ["j2", "j3", "j1", "i1", "i2"]),
+                                           ("warp", ["i3", "i4"]), ("block", ["j4", "j5", "i5"])], out))
+    d = ll.plan_describe(A2, B2, 16, "regs")
+    assert d["path"] == "regs_shuffle" and d["regs_shuffle"]["rounds"] <= 4
+    try:
+        ll.tune("regs_shuffle_max_rounds", 0)
+        assert ll.plan_describe(A2, B2, 16, "regs")["path"] == "regs"
+    finally:
+        ll.tune("regs_shuffle_max_rounds", 4)

@@ -65,6 +65,21 @@ def cfg2(batch_bits=12):
     return dict(name="cfg2", A=A, B=B, elem_bytes=2)
 
 
+def cfg2w(batch_bits=12):
+    """SURVEY 8(a) a5, "cfg2 warp-aligned variant": the mma C fragment ->
+    a blocked-style layout that keeps the warps on [i5, i6] (8 fp16 per
+    thread along j, 16 x 2 threads, the remaining rows as register
+    repetitions), so (B^-1 o A)_warp = I and the paper's warp-shuffle
+    exchange applies; 64 rounds."""
+    out = [("b", batch_bits), ("i", 7), ("j", 7)]
+    blk = ("block", _rng("b", 0, batch_bits))
+    A = spec([("reg", ["j0", "i3", "j3", "j4", "j5", "j6", "i4"]),
+              ("lane", ["j1", "j2", "i0", "i1", "i2"]), ("warp", ["i5", "i6"]), blk], out)
+    B = spec([("reg", ["j0", "j1", "j2", "i1", "i2", "i3", "i4"]),
+              ("lane", ["j3", "j4", "j5", "j6", "i0"]), ("warp", ["i5", "i6"]), blk], out)
+    return dict(name="cfg2w", A=A, B=B, elem_bytes=2)
+
+
 # --- config 3: row-major -> column-major transpose, 2^n x 2^n bf16 -----------------
 
 def cfg3(n_bits=13, m_bits=None):
