@@ -18,16 +18,39 @@ namespace ll {
 
 // ------------------------------------------------------------------ PTX helpers
 
+// LL_LDG_HINT (build-time experiment): 0 = L1::no_allocate; 1 = + L2::256B
+// prefetch; 2 = + L2::evict_first; 3 = both.  LL_STG_HINT: 0 = .cs
+// (streaming); 1 = default (.wb); 2 = L2::evict_last ... (see the sweep).
+#ifndef LL_LDG_HINT
+#define LL_LDG_HINT 0
+#endif
+#ifndef LL_STG_HINT
+#define LL_STG_HINT 0
+#endif
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 v;
+#if LL_LDG_HINT == 1
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#elif LL_LDG_HINT == 2
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u32 {%0,%1,%2,%3}, [%4];"
+#elif LL_LDG_HINT == 3
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+#endif
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
 }
 
 __device__ __forceinline__ void stg_stream(void* p, uint4 v) {
+#if LL_STG_HINT == 1
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+#elif LL_STG_HINT == 2
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+#else
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+#endif
                "r"(v.z), "r"(v.w)
                : "memory");
 }
