@@ -526,8 +526,8 @@ ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_
     check_layout(src_layout, "ll_mxfp4_upcast");
     check_layout(dst_layout, "ll_mxfp4_upcast");
     if (!packed || !scales || !dst_bf16) return fail(LL_ERR_ARG, "ll_mxfp4_upcast: NULL buffer");
-    if ((reinterpret_cast<uintptr_t>(packed) | reinterpret_cast<uintptr_t>(dst_bf16)) & 15)
-      return fail(LL_ERR_ARG, "ll_mxfp4_upcast: buffers must be 16-byte aligned");
+    if ((reinterpret_cast<uintptr_t>(packed) & 15) || (reinterpret_cast<uintptr_t>(dst_bf16) & 31))
+      return fail(LL_ERR_ARG, "ll_mxfp4_upcast: packed must be 16-byte and dst_bf16 32-byte aligned");
     const int64_t batch = opts && opts->batch > 0 ? opts->batch : 1;
     if (batch != 1) return fail(LL_ERR_UNSUPPORTED, "ll_mxfp4_upcast: batch must be 1");
     auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, 1, LL_PATH_AUTO, 1, 1);

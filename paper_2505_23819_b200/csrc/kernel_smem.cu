@@ -4,6 +4,9 @@
 #ifndef LL_UP_PREFETCH
 #define LL_UP_PREFETCH 1  // upcast: load the next tile's scales with its data
 #endif
+#ifndef LL_UP_V8
+#define LL_UP_V8 1  // upcast stores: each lane writes its own 64 B as two 256-bit STG (sm_100)
+#endif
 #ifndef LL_UP_MINB
 #define LL_UP_MINB 2  // resident CTAs the upcast kernel is compiled for (sweep: 2 > 3 > 4 > 1)
 #endif
@@ -176,6 +179,52 @@ __global__ void __launch_bounds__(256, UP ? LL_UP_MINB : (G < 8 ? 1 : (NV >= 8 ?
       // vectors, the odd lane chunks 1 and 3.
       const int64_t dbyte = (int64_t)st_off - rg.dst_shift + dcur;
       const int64_t scur = sct_cur + sc_off;
+#if LL_UP_V8
+      // sm_100 256-bit stores: every lane writes whole 32-byte sectors of its
+      // own 64 output bytes, so no lane pairing is needed
+#pragma unroll
+      for (int u = 0; u < NV; ++u) {
+        const uint32_t pk = PKc[u];
+        uint8_t* op = dst + 4 * (dbyte + p.st_vec[u]);
+        uint32_t o8[2][8];
+        if ((fastc >> u) & 1u) {
+          const uint32_t plo = (pk << 7) & 0x80808080u, phi = (pk >> 1) & 0x7F7F7F7Fu;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t wq = Q[4 * u + q];
+            const uint32_t m = wq & 0x77777777u, mh = m >> 16, x = wq & 0x88888888u;
+            const uint32_t L01 = __byte_perm(kE2M1Lo0, kE2M1Lo1, m), H01 = __byte_perm(kE2M1Hi0, kE2M1Hi1, m);
+            const uint32_t L23 = __byte_perm(kE2M1Lo0, kE2M1Lo1, mh), H23 = __byte_perm(kE2M1Hi0, kE2M1Hi1, mh);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int e = 4 * q + k;
+              const uint32_t mag = __byte_perm(k < 2 ? L01 : L23, k < 2 ? H01 : H23, (k & 1) ? 0x7362 : 0x5140);
+              const uint32_t t = __byte_perm(x, 0u, 0x4440 | k) * 0x01001000u;  // bits 3,7 -> 15,31
+              const uint32_t v = mag | (t & 0x80008000u);
+              o8[q >> 1][4 * (q & 1) + k] = bf16x2_mul(v, __byte_perm(plo, phi, p.sc_sel[e]));
+            }
+          }
+        } else {
+          const uint8_t* scp = scales + scur + p.sc_vec[u];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t byte = (Q[4 * u + (e >> 2)] >> ((e & 3) * 8)) & 0xFFu;
+            const uint32_t sb = p.sc_nz <= 2 ? (pk >> (8 * p.sc_slot[e])) & 0xFFu
+                                             : (uint32_t)__ldg(scp + p.sc_e[e]);
+            const float sf = __uint_as_float(mx_scale_f32(sb));
+            const uint32_t lo = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte & 15u)), sf));
+            const uint32_t hi = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte >> 4)), sf));
+            o8[e >> 3][e & 7] = sb == 255u ? 0x7FC07FC0u : ((hi & 0xFFFF0000u) | (lo >> 16));
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(op + 32 * h),
+                       "r"(o8[h][0]), "r"(o8[h][1]), "r"(o8[h][2]), "r"(o8[h][3]), "r"(o8[h][4]),
+                       "r"(o8[h][5]), "r"(o8[h][6]), "r"(o8[h][7])
+                       : "memory");
+      }
+#else
       const bool odd = lane & 1;
       const uint32_t fpair = fastc & __shfl_xor_sync(0xFFFFFFFFu, fastc, 1);
 #pragma unroll
@@ -235,6 +284,7 @@ __global__ void __launch_bounds__(256, UP ? LL_UP_MINB : (G < 8 ? 1 : (NV >= 8 ?
             stg_stream(op + 16 * q, make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]));
         }
       }
+#endif
     } else {
       uint8_t* dp = dthr + dcur;
 #pragma unroll
