@@ -802,3 +802,29 @@ def test_regs_register_permutation_and_cost_model():
     assert "__shfl_sync" not in ll.jit_source(A_, B_, 16)
     src, dst = run_convert(c, path="regs", seed=8, batch=2)
     assert dst.tobytes() == expect_convert(c, src, 2).tobytes()
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_tiny_layouts(w):
+    """Degenerate sizes: 1 to 64 elements (less than one 16-byte vector, less
+    than a warp), a layout with no input bits at all, and the identity; every
+    AUTO plan (copy / generic) stays byte-exact."""
+    rng = random.Random(1100 + w)
+    for d in range(0, 7):
+        out = [("i", d // 2), ("j", d - d // 2)]
+        for _ in range(3):
+            dims = [("reg", rng.randint(0, d))]
+            dims.append(("lane", d - dims[0][1]))
+            specs = []
+            for _k in range(2):
+                cols = [1 << k for k in range(d)]
+                rng.shuffle(cols)
+                tmp = OLayout([], out, {})
+                bases, k = {}, 0
+                for n, b in dims:
+                    bases[n] = [tmp.unflatten(x) for x in cols[k:k + b]]
+                    k += b
+                specs.append({"in_dims": dims, "out_dims": out, "bases": bases})
+            c = {"A": specs[0], "B": specs[1], "elem_bytes": w}
+            src, dst = run_convert(c, seed=d + 17)
+            assert dst.tobytes() == expect_convert(c, src).tobytes(), (d, dims)
