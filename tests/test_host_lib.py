@@ -473,3 +473,14 @@ def test_regs_cost_model_prefers_few_round_shuffles():
         assert ll.plan_describe(A2, B2, 16, "regs")["path"] == "regs"
     finally:
         ll.tune("regs_shuffle_max_rounds", 4)
+
+
+def test_upcast_alignment_contract():
+    """ll_mxfp4_upcast writes 256-bit vectors: dst_bf16 must be 32-byte
+    aligned, packed 16-byte aligned -- checked before any device work."""
+    c = configs.cfg5(m_bits=8, kb_bits=7)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    for packed, dst in ((0x10000, 0x20010), (0x10008, 0x20000)):
+        with pytest.raises(ll.LLError) as e:
+            ll.mxfp4_upcast(packed, A, 0x30000, dst, B, stream=0)
+        assert e.value.name == "LL_ERR_ARG"

@@ -10,6 +10,9 @@
 //   r1w4_pair  lane pairs fill one 32-byte sector per store instruction (the
 //              upcast kernel's store pattern)
 //   r1w4_quad  lane quads fill 64 contiguous bytes per store instruction
+//   copy256    1 : 1 with sm_100 256-bit loads and stores (32 B per thread)
+//   r1w4_v8    read 16 B, write the thread's own 64 B as two 256-bit stores
+//              (the upcast kernel's store pattern since LL_UP_V8)
 // Prints one JSON line per case: GB/s = (read + write bytes) / time, best of
 // 20 launches over two rotating buffer sets larger than L2.
 #include <cstdint>
@@ -77,6 +80,33 @@ __global__ void k_r1w4_quad(const uint4* __restrict__ a, uint4* __restrict__ b, 
   }
 }
 
+struct alignas(32) u8x32 { uint32_t w[8]; };
+__device__ __forceinline__ u8x32 ldg256(const u8x32* p) {
+  u8x32 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]),
+                 "=r"(v.w[6]), "=r"(v.w[7]) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg256(u8x32* p, const u8x32& v) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]),
+                  "r"(v.w[6]), "r"(v.w[7]) : "memory");
+}
+__global__ void k_copy256(const u8x32* __restrict__ a, u8x32* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    stg256(b + i, ldg256(a + i));
+}
+__global__ void k_r1w4_v8(const uint4* __restrict__ a, u8x32* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 x = ldg_stream(a + i);
+    u8x32 v{{x.x, x.y, x.z, x.w, x.x ^ 1, x.y, x.z, x.w}};
+    stg256(b + 2 * i, v);
+    v.w[0] ^= 2;
+    stg256(b + 2 * i + 1, v);
+  }
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -114,6 +144,8 @@ int main() {
     run("r1w4_lane 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_lane<<<grid, threads>>>(a[s], b[s], nv); });
     run("r1w4_pair 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_pair<<<grid, threads>>>(a[s], b[s], nv); });
     run("r1w4_quad 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_quad<<<grid, threads>>>(a[s], b[s], nv); });
+    run("copy256 2GiB+2GiB", 2.0 * out_bytes, [&](int s) { k_copy256<<<grid, threads>>>((const u8x32*)a[s], (u8x32*)b[s], out_bytes / 32); });
+    run("r1w4_v8 512MiB->2GiB", 5.0 * in_bytes, [&](int s) { k_r1w4_v8<<<grid, threads>>>(a[s], (u8x32*)b[s], nv); });
   }
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) {
