@@ -1,0 +1,70 @@
+"""One small launch of every device path, each checked against the oracle --
+the workload for compute-sanitizer (memcheck / racecheck / synccheck):
+    compute-sanitizer --tool racecheck python scripts/sanitize_paths.py"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2505_23819_b200 as ll  # noqa: E402
+from oracle import convert as oconv  # noqa: E402
+from oracle.layout import Layout as OL  # noqa: E402
+from workloads import configs  # noqa: E402
+from workloads.values import indices_torch, values_torch  # noqa: E402
+
+NP = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}
+
+
+def conv(c, path, batch=1):
+    w = c["elem_bytes"]
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = (1 << A.in_bits) * batch
+    src = values_torch(n, 3, w, "cuda")
+    dst = torch.zeros_like(src)
+    ll.convert(src, A, dst, B, 8 * w, path=path, batch=batch)
+    torch.cuda.synchronize()
+    s = src.cpu().numpy().view(NP[w])
+    nA = A.in_bits
+    exp = np.concatenate([oconv.convert_np(s[b << nA:(b + 1) << nA], OL(**c["A"]), OL(**c["B"]))
+                          for b in range(batch)])
+    ok = dst.cpu().numpy().view(NP[w]).tobytes() == exp.tobytes()
+    print("%-10s %-16s %s" % (c["name"], path, "ok" if ok else "MISMATCH"), flush=True)
+    return ok
+
+
+def main():
+    ok = True
+    ok &= conv(configs.cfg2(batch_bits=2), "smem")
+    ok &= conv(configs.cfg3(n_bits=8), "smem")
+    ok &= conv(configs.cfg5(m_bits=8, kb_bits=8), "smem")
+    ok &= conv(configs.cfg2(batch_bits=2), "shuffle")
+    ok &= conv(configs.cfg2(batch_bits=2), "smem_async")
+    ok &= conv(configs.cfg3(n_bits=8), "smem_tma")
+    ok &= conv(configs.cfg5(m_bits=8, kb_bits=8), "smem_tma")
+    ok &= conv(configs.cfg3(n_bits=8), "smem_tma_store")
+    ok &= conv(configs.cfg1("mma"), "regs")
+    ok &= conv(configs.cfg2(batch_bits=1), "regs")
+    ok &= conv(configs.cfg2w(batch_bits=1), "regs_shuffle")
+    ok &= conv(configs.cfg2(batch_bits=1), "generic")
+    g = configs.cfg4(r_bits=3)
+    L = ll.Layout.from_spec(g["L"])
+    m = 1 << L.in_bits
+    for path in ("shuffle", "auto"):
+        gs = values_torch(m, 4, 4, "cuda")
+        gi = indices_torch(m, 5, 32, "cuda")
+        go = torch.empty_like(gs)
+        ll.gather(gs, gi, go, L, g["axis"], 32, path=path)
+        torch.cuda.synchronize()
+        exp = oconv.gather_np(gs.cpu().numpy().view(np.uint32), gi.cpu().numpy(), OL(**g["L"]), 2)
+        good = go.cpu().numpy().view(np.uint32).tobytes() == exp.tobytes()
+        print("%-10s %-16s %s" % ("cfg4", "gather " + path, "ok" if good else "MISMATCH"), flush=True)
+        ok &= good
+    print("ALL OK" if ok else "FAILURES")
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
