@@ -7,6 +7,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -408,6 +411,11 @@ __device__ __forceinline__ void lin_op(uint32_t (&T)[NW], int op, int a, int b) 
 
 // ------------------------------------------------------------- launch knobs
 int num_sms();
+
+// Resident CTAs per SM of `kernel` for (threads, dynamic smem, carveout),
+// computed once per key (thread-safe: several host threads may launch).  The
+// kernel's max dynamic smem (220 KB) and carveout (if != -1) are set first.
+int cached_occupancy(const void* kernel, int threads, size_t smem, int carveout);
 struct LaunchKnobs {
   int tpg, pipe, gather_tpt, carveout, pow2, stages, async_tpg, up_tpg, tma_tpg, tma_stages;
   LaunchKnobs();

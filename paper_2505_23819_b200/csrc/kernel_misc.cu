@@ -226,6 +226,23 @@ int num_sms() {
   return g_num_sms;
 }
 
+int cached_occupancy(const void* kernel, int threads, size_t smem, int carveout) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kernel, threads, smem, carveout, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (carveout != -1) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess) occ = 0;
+  cache[key] = occ;
+  return occ;
+}
+
 static int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;

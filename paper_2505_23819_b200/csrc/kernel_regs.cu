@@ -181,13 +181,7 @@ static cudaError_t launch_regs_t(const RegsPlan& p, const void* src, void* dst, 
   const int threads = 32 << p.nw;
   const size_t smem = (size_t)p.tile_bytes;
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-  static size_t attr_smem = 0;
-  if (smem > 48 * 1024 && attr_smem < smem) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_smem = smem;
-  }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
+  const int occ = cached_occupancy((const void*)k, threads, smem, -1);
   if (occ <= 0) return cudaErrorInvalidConfiguration;
   int64_t grid = std::min<int64_t>(p.n_tiles, (int64_t)occ * num_sms() * 8);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);

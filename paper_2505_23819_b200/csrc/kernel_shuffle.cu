@@ -84,8 +84,7 @@ static cudaError_t launch_shuffle_p(const ShufflePlan& p, const void* src, void*
   const int gpc = threads / 32;
   const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;
-  static int occ_cache = -1;
-  if (occ_cache < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, 0);
+  const int occ_cache = cached_occupancy((const void*)k, threads, 0, -1);
   const int tpg = knobs().tpg;
   int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)std::max(1, occ_cache) * num_sms() * gpc;
   if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);

@@ -303,16 +303,7 @@ static cudaError_t launch_smem_p(const SmemPlan& p, const void* src, void* dst, 
   const int threads = 256;
   const int gpc = (threads / 32) >> p.gw;
   const size_t smem = (size_t)gpc * 2 * p.tile_bytes;  // tile_bytes includes any padding
-  static int occ_cache = -1;
-  static size_t occ_smem = 0;
-  static int occ_carve = -2;
-  if (occ_cache < 0 || occ_smem != smem || occ_carve != knobs().carveout) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, knobs().carveout);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
-    occ_smem = smem;
-    occ_carve = knobs().carveout;
-  }
+  const int occ_cache = cached_occupancy((const void*)k, threads, smem, knobs().carveout);
   if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
   const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;

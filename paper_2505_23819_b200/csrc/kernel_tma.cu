@@ -386,13 +386,7 @@ static cudaError_t launch_tma_p(const SmemPlan& p, const TmaDesc& td, const void
   const int gpc = (threads / 32) >> p.gw;
   const size_t smem = (size_t)gpc * NS * p.tile_bytes + 1024;
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
-  static int occ_cache = -1;
-  static size_t occ_smem = 0;
-  if (occ_cache < 0 || occ_smem != smem) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
-    occ_smem = smem;
-  }
+  const int occ_cache = cached_occupancy((const void*)k, threads, smem, -1);
   if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
   const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;
@@ -425,13 +419,7 @@ static cudaError_t launch_tma_store_p(const SmemPlan& p, const TmaDesc& tds, con
   const int gpc = (threads / 32) >> p.gw;
   const size_t smem = (size_t)gpc * (NS + 2) * p.tile_bytes + 1024;
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
-  static int occ_cache = -1;
-  static size_t occ_smem = 0;
-  if (occ_cache < 0 || occ_smem != smem) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache, k, threads, smem);
-    occ_smem = smem;
-  }
+  const int occ_cache = cached_occupancy((const void*)k, threads, smem, -1);
   if (occ_cache <= 0) return cudaErrorInvalidConfiguration;
   const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;
