@@ -62,6 +62,20 @@ def main():
         good = go.cpu().numpy().view(np.uint32).tobytes() == exp.tobytes()
         print("%-10s %-16s %s" % ("cfg4", "gather " + path, "ok" if good else "MISMATCH"), flush=True)
         ok &= good
+    # fused mxfp4 upcast (NEXT 1) against oracle.mxfp4.upcast_np
+    from oracle import mxfp4 as omx
+    c = configs.cfg5(m_bits=8, kb_bits=7)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    packed = values_torch(n, 9, 1, "cuda")
+    sc = (indices_torch((1 << 8) * (1 << 3), 10, 16, "cuda") + 120).to(torch.uint8)
+    out = torch.empty(2 * n, dtype=torch.int16, device="cuda")
+    ll.mxfp4_upcast(packed, A, sc, out, B)
+    torch.cuda.synchronize()
+    exp = omx.upcast_np(packed.cpu().numpy(), OL(**c["A"]), sc.cpu().numpy(), OL(**c["B"]))
+    good = out.cpu().numpy().view(np.uint16).tobytes() == exp.tobytes()
+    print("%-10s %-16s %s" % ("cfg5", "mxfp4_upcast", "ok" if good else "MISMATCH"), flush=True)
+    ok &= good
     print("ALL OK" if ok else "FAILURES")
     sys.exit(0 if ok else 1)
 

@@ -828,3 +828,24 @@ def test_convert_tiny_layouts(w):
             c = {"A": specs[0], "B": specs[1], "elem_bytes": w}
             src, dst = run_convert(c, seed=d + 17)
             assert dst.tobytes() == expect_convert(c, src).tobytes(), (d, dims)
+
+
+@pytest.mark.parametrize("name,mk,path", [("cfg2", lambda: configs.cfg2(), "regs"),
+                                          ("cfg2w", lambda: configs.cfg2w(), "regs_shuffle")])
+def test_convert_regs_full_size_sampled(name, mk, path):
+    """Register-faithful paths at the BASELINE size (4096 tiles of 128x128
+    fp16): permutation property on the whole buffer + sampled outputs
+    computed one by one by the oracle."""
+    c = mk()
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src = values_torch(n, 23, 2, "cuda")
+    dst = torch.empty_like(src)
+    ll.convert(src, A, dst, B, 16, path=path)
+    torch.cuda.synchronize()
+    key = lambda t: t.view(torch.int16).to(torch.int32)  # noqa: E731
+    assert torch.equal(torch.sort(key(src))[0], torch.sort(key(dst))[0])
+    rng = np.random.default_rng(6)
+    h = np.concatenate([rng.integers(0, n, 100000), np.arange(4096), np.arange(n - 4096, n)])
+    exp = sampled_expected(c, _np(src, 2), h.astype(np.int64))
+    assert (_np(dst, 2)[h] == exp).all()
