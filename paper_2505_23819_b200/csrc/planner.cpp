@@ -7,6 +7,7 @@
 // tile (the "free mapping" of DESIGN.md), and the exchange between them goes
 // through shared memory laid out by the paper's optimal swizzle.
 #include "planner.hpp"
+#include "planner_internal.hpp"
 
 #include <algorithm>
 #include <array>
@@ -18,7 +19,7 @@
 
 namespace ll {
 
-namespace {
+namespace detail {
 
 int ilog2i(int x) {
   int r = 0;
@@ -48,7 +49,8 @@ std::string ivec_json(const std::vector<int>& v) {
   return o.str();
 }
 
-}  // namespace
+}  // namespace detail
+using namespace detail;
 
 // ------------------------------------------------------------ optimal swizzle
 SwizzleResult optimal_swizzle(const std::vector<u64>& A_lane, const std::vector<u64>& B_lane,
@@ -222,138 +224,137 @@ int64_t scale_contrib(const ConvertPlan& P, int k) {
   return pos >= 4 ? (int64_t(1) << (pos - 4)) : 0;                 // kb bit (32 fp4 = 16 bytes per scale)
 }
 
+}  // namespace
+
+namespace detail {
+
 // The paper's warp-shuffle exchange between two warp-local
 // thread layouts given by their word-level register vectors (Aw / Bw, word
 // order) and lane vectors (Al5 / Bl5): V is the word, I, E, F (ascending),
 // G = {e_i ^ f_i}, R completes span(I u G); round k sends
 // R[alpha(k) ^ beta(l)] to lane gamma(k) ^ delta(l), which stores it at word
 // eps(k) ^ zeta(l).  ok = false if the exchange is not expressible so.
-struct ShuffleCore {
-  bool ok = false;
-  int rounds = 0;
-  std::vector<u64> I, E, F, Gv, R, alpha, epsm;
-  std::vector<std::array<int, 3>> pre, post;
-  uint32_t beta[5] = {0}, zeta[5] = {0}, delta[5] = {0}, beta_any = 0, zeta_any = 0;
-  std::vector<uint8_t> gamma;
-};
-
 ShuffleCore shuffle_core(const std::vector<u64>& Aw, const std::vector<u64>& Al5,
                          const std::vector<u64>& Bw, const std::vector<u64>& Bl5, int LB) {
   ShuffleCore sc;
-    // I, E, F (ascending), G = {e_i ^ f_i}, R completes span(I u G)
-    std::vector<u64>& I = sc.I;
-    std::vector<u64>& E = sc.E;
-    std::vector<u64>& F = sc.F;
-    std::vector<u64>& Gv = sc.Gv;
-    std::vector<u64>& R = sc.R;
-    for (u64 x : Al5) if (std::find(Bl5.begin(), Bl5.end(), x) != Bl5.end()) I.push_back(x);
-    for (u64 x : Al5) if (std::find(I.begin(), I.end(), x) == I.end()) E.push_back(x);
-    for (u64 x : Bl5) if (std::find(I.begin(), I.end(), x) == I.end()) F.push_back(x);
-    std::sort(I.begin(), I.end());
-    std::sort(E.begin(), E.end());
-    std::sort(F.begin(), F.end());
-    for (size_t i = 0; i < E.size() && i < F.size(); ++i) Gv.push_back(E[i] ^ F[i]);
-    {
-      F2Basis bs;
-      for (u64 x : I) bs.add(x);
-      for (u64 x : Gv) bs.add(x);
-      std::vector<u64> units;
-      for (u64 x : Aw) units.push_back(x);
-      for (u64 x : Al5) units.push_back(x);
-      std::sort(units.begin(), units.end());
-      for (u64 x : units) if (bs.add(x)) R.push_back(x);
+  // I, E, F (ascending), G = {e_i ^ f_i}, R completes span(I u G)
+  std::vector<u64>& I = sc.I;
+  std::vector<u64>& E = sc.E;
+  std::vector<u64>& F = sc.F;
+  std::vector<u64>& Gv = sc.Gv;
+  std::vector<u64>& R = sc.R;
+  for (u64 x : Al5) if (std::find(Bl5.begin(), Bl5.end(), x) != Bl5.end()) I.push_back(x);
+  for (u64 x : Al5) if (std::find(I.begin(), I.end(), x) == I.end()) E.push_back(x);
+  for (u64 x : Bl5) if (std::find(I.begin(), I.end(), x) == I.end()) F.push_back(x);
+  std::sort(I.begin(), I.end());
+  std::sort(E.begin(), E.end());
+  std::sort(F.begin(), F.end());
+  for (size_t i = 0; i < E.size() && i < F.size(); ++i) Gv.push_back(E[i] ^ F[i]);
+  {
+    F2Basis bs;
+    for (u64 x : I) bs.add(x);
+    for (u64 x : Gv) bs.add(x);
+    std::vector<u64> units;
+    for (u64 x : Aw) units.push_back(x);
+    for (u64 x : Al5) units.push_back(x);
+    std::sort(units.begin(), units.end());
+    for (u64 x : units) if (bs.add(x)) R.push_back(x);
+  }
+  const int NWd = 1 << LB;
+  bool ok = E.size() == F.size() && (int)R.size() == LB && NWd <= LL_MAX_GRAN;
+  // decompose word-level vectors in the ld and st bases
+  auto decomp = [&](u64 x, const std::vector<u64>& wv, const std::vector<u64>& lv, int& word,
+                    int& lane) {
+    word = 0; lane = 0;
+    for (int b = 0; b < (int)wv.size(); ++b) if (x & wv[b]) word |= 1 << b;
+    for (int c = 0; c < 5; ++c) if (x & lv[c]) lane |= 1 << c;
+  };
+  std::vector<u64> span5;
+  if (ok) {
+    std::vector<u64> gen = I;
+    gen.insert(gen.end(), Gv.begin(), Gv.end());
+    span5.push_back(0);
+    for (u64 gvec : gen) {
+      size_t n0 = span5.size();
+      for (size_t i = 0; i < n0; ++i) span5.push_back(span5[i] ^ gvec);
     }
-    const int NWd = 1 << LB;
-    bool ok = E.size() == F.size() && (int)R.size() == LB && NWd <= LL_MAX_GRAN;
-    // decompose word-level vectors in the ld and st bases
-    auto decomp = [&](u64 x, const std::vector<u64>& wv, const std::vector<u64>& lv, int& word,
-                      int& lane) {
-      word = 0; lane = 0;
-      for (int b = 0; b < (int)wv.size(); ++b) if (x & wv[b]) word |= 1 << b;
-      for (int c = 0; c < 5; ++c) if (x & lv[c]) lane |= 1 << c;
-    };
-    std::vector<u64> span5;
-    if (ok) {
-      std::vector<u64> gen = I;
-      gen.insert(gen.end(), Gv.begin(), Gv.end());
-      span5.push_back(0);
-      for (u64 gvec : gen) {
-        size_t n0 = span5.size();
-        for (size_t i = 0; i < n0; ++i) span5.push_back(span5[i] ^ gvec);
+    ok = span5.size() == 32;
+  }
+  std::vector<int> ws(32 * NWd, -1), sl(32 * NWd, -1), wr(32 * NWd, -1);
+  for (int k = 0; ok && k < NWd; ++k) {
+    u64 Rk = 0;
+    for (int j = 0; j < LB; ++j) if ((k >> j) & 1) Rk ^= R[j];
+    for (u64 y : span5) {
+      const u64 x = Rk ^ y;
+      int aw, al, bw, bl;
+      decomp(x, Aw, Al5, aw, al);
+      decomp(x, Bw, Bl5, bw, bl);
+      if (ws[al * NWd + k] >= 0 || wr[bl * NWd + k] >= 0) { ok = false; break; }  // one send / recv per lane
+      ws[al * NWd + k] = aw;
+      sl[bl * NWd + k] = al;
+      wr[bl * NWd + k] = bw;
+    }
+  }
+  std::vector<u64>& alpha = sc.alpha;
+  std::vector<u64>& epsm = sc.epsm;
+  alpha.assign(LB, 0);
+  epsm.assign(LB, 0);
+  if (ok) {
+    // linear decomposition: ws(l,k) = alpha(k) ^ beta(l), etc. (checked)
+    for (int l = 0; l < 32 && ok; ++l)
+      for (int k = 0; k < NWd && ok; ++k) {
+        ok = ws[l * NWd + k] == (ws[k] ^ ws[l * NWd]) && sl[l * NWd + k] == (sl[k] ^ sl[l * NWd]) &&
+             wr[l * NWd + k] == (wr[k] ^ wr[l * NWd]);
       }
-      ok = span5.size() == 32;
+  }
+  std::vector<std::array<int, 3>>& pre = sc.pre;
+  std::vector<std::array<int, 3>>& post = sc.post;
+  if (ok) {
+    for (int j = 0; j < LB; ++j) { alpha[j] = (u64)ws[1 << j]; epsm[j] = (u64)wr[1 << j]; }
+    // eps^{-1}
+    std::vector<u64> einv(LB, 0);
+    for (int m = 0; m < NWd; ++m) {
+      int e = 0;
+      for (int j = 0; j < LB; ++j) if ((m >> j) & 1) e ^= (int)epsm[j];
+      for (int j = 0; j < LB; ++j) if (e == (1 << j)) einv[j] = (u64)m;
     }
-    std::vector<int> ws(32 * NWd, -1), sl(32 * NWd, -1), wr(32 * NWd, -1);
-    for (int k = 0; ok && k < NWd; ++k) {
-      u64 Rk = 0;
-      for (int j = 0; j < LB; ++j) if ((k >> j) & 1) Rk ^= R[j];
-      for (u64 y : span5) {
-        const u64 x = Rk ^ y;
-        int aw, al, bw, bl;
-        decomp(x, Aw, Al5, aw, al);
-        decomp(x, Bw, Bl5, bw, bl);
-        if (ws[al * NWd + k] >= 0 || wr[bl * NWd + k] >= 0) { ok = false; break; }  // one send / recv per lane
-        ws[al * NWd + k] = aw;
-        sl[bl * NWd + k] = al;
-        wr[bl * NWd + k] = bw;
+    ok = linop_factor(alpha, LB, pre) && linop_factor(einv, LB, post) &&
+         (int)pre.size() <= LL_MAX_LINOPS && (int)post.size() <= LL_MAX_LINOPS;
+    // verify the factorisations by applying them to index arrays
+    for (int pass = 0; ok && pass < 2; ++pass) {
+      const auto& ops = pass ? post : pre;
+      std::vector<int> T(NWd);
+      for (int k = 0; k < NWd; ++k) T[k] = k;
+      for (const auto& op : ops) {
+        std::vector<int> T2(NWd);
+        for (int k = 0; k < NWd; ++k) T2[k] = T[(int)linop_apply_index(op, (u64)k)];
+        T = T2;
+      }
+      for (int k = 0; k < NWd && ok; ++k) {
+        int want = 0;
+        for (int j = 0; j < LB; ++j) if ((k >> j) & 1) want ^= (int)(pass ? einv[j] : alpha[j]);
+        ok = T[k] == want;
       }
     }
-    std::vector<u64>& alpha = sc.alpha;
-    std::vector<u64>& epsm = sc.epsm;
-    alpha.assign(LB, 0);
-    epsm.assign(LB, 0);
-    if (ok) {
-      // linear decomposition: ws(l,k) = alpha(k) ^ beta(l), etc. (checked)
-      for (int l = 0; l < 32 && ok; ++l)
-        for (int k = 0; k < NWd && ok; ++k) {
-          ok = ws[l * NWd + k] == (ws[k] ^ ws[l * NWd]) && sl[l * NWd + k] == (sl[k] ^ sl[l * NWd]) &&
-               wr[l * NWd + k] == (wr[k] ^ wr[l * NWd]);
-        }
+  }
+  if (ok) {
+    for (int c = 0; c < 5; ++c) {
+      sc.beta[c] = (uint32_t)ws[(1 << c) * NWd];
+      sc.delta[c] = (uint32_t)sl[(1 << c) * NWd];
+      sc.zeta[c] = (uint32_t)wr[(1 << c) * NWd];
+      sc.beta_any |= sc.beta[c];
+      sc.zeta_any |= sc.zeta[c];
     }
-    std::vector<std::array<int, 3>>& pre = sc.pre;
-    std::vector<std::array<int, 3>>& post = sc.post;
-    if (ok) {
-      for (int j = 0; j < LB; ++j) { alpha[j] = (u64)ws[1 << j]; epsm[j] = (u64)wr[1 << j]; }
-      // eps^{-1}
-      std::vector<u64> einv(LB, 0);
-      for (int m = 0; m < NWd; ++m) {
-        int e = 0;
-        for (int j = 0; j < LB; ++j) if ((m >> j) & 1) e ^= (int)epsm[j];
-        for (int j = 0; j < LB; ++j) if (e == (1 << j)) einv[j] = (u64)m;
-      }
-      ok = linop_factor(alpha, LB, pre) && linop_factor(einv, LB, post) &&
-           (int)pre.size() <= LL_MAX_LINOPS && (int)post.size() <= LL_MAX_LINOPS;
-      // verify the factorisations by applying them to index arrays
-      for (int pass = 0; ok && pass < 2; ++pass) {
-        const auto& ops = pass ? post : pre;
-        std::vector<int> T(NWd);
-        for (int k = 0; k < NWd; ++k) T[k] = k;
-        for (const auto& op : ops) {
-          std::vector<int> T2(NWd);
-          for (int k = 0; k < NWd; ++k) T2[k] = T[(int)linop_apply_index(op, (u64)k)];
-          T = T2;
-        }
-        for (int k = 0; k < NWd && ok; ++k) {
-          int want = 0;
-          for (int j = 0; j < LB; ++j) if ((k >> j) & 1) want ^= (int)(pass ? einv[j] : alpha[j]);
-          ok = T[k] == want;
-        }
-      }
-    }
-    if (ok) {
-      for (int c = 0; c < 5; ++c) {
-        sc.beta[c] = (uint32_t)ws[(1 << c) * NWd];
-        sc.delta[c] = (uint32_t)sl[(1 << c) * NWd];
-        sc.zeta[c] = (uint32_t)wr[(1 << c) * NWd];
-        sc.beta_any |= sc.beta[c];
-        sc.zeta_any |= sc.zeta[c];
-      }
-      for (int k = 0; k < NWd; ++k) sc.gamma.push_back((uint8_t)sl[k]);
-    }
-    sc.ok = ok;
-    sc.rounds = NWd;
+    for (int k = 0; k < NWd; ++k) sc.gamma.push_back((uint8_t)sl[k]);
+  }
+  sc.ok = ok;
+  sc.rounds = NWd;
   return sc;
 }
+
+}  // namespace detail
+
+namespace {
 
 // Try to build the shared-memory tile plan; returns false if X is not a bit
 // permutation or the tile does not fit.
@@ -775,1142 +776,6 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
      << u32_json(sp.sr_thr, 5 + g) << ",\"sw_gran\":" << u32_json(sp.sw_gran, ngran)
      << ",\"sr_gran\":" << u32_json(sp.sr_gran, ngran) << "}"
      << ",\"tile_order_dst_bits\":" << ivec_json(torder) << sjs.str();
-  return true;
-}
-
-// Asynchronous-copy variant of the shared-memory path (LL_PATH_SMEM_ASYNC):
-// the source tile goes HBM -> shared memory with cp.async (16-byte chunks,
-// no registers, several tiles in flight per group), so the shared-memory
-// granule is the *source* 16-byte vector V = VS; the reading side holds
-// VS u VD in registers and permutes into destination vectors (prmt for the
-// sub-word bits, compile-time STG operand selection for the word bits).  The
-// swizzle S is the paper's construction for (writer, reader) with V = VS.
-bool plan_async(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js) {
-  const int n = P.nB, w = P.w;
-  if (P.nA != P.nB || n > 62 || w > 8) return false;
-  std::vector<int> sigma(n), sinv(n, -1);
-  for (int k = 0; k < n; ++k) {
-    if (popcount64(X[k]) != 1) return false;
-    sigma[k] = ctz64(X[k]);
-    if (sinv[sigma[k]] >= 0) return false;
-    sinv[sigma[k]] = k;
-  }
-  const int vb = ilog2i(16 / w);
-  if (n < vb + 5) return false;
-  auto contains = [](const std::vector<int>& v, int x) {
-    return std::find(v.begin(), v.end(), x) != v.end();
-  };
-  std::vector<int> VD, VS, CD, CS;
-  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
-  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
-  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
-  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
-  const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("thread_bytes", 64)) / w));
-  std::vector<int> need = VS;
-  for (int x : VD) if (!contains(need, x)) need.push_back(x);
-  if ((int)need.size() > r_max || (int)need.size() + 5 > n) return false;
-  int r = std::min(std::max((int)need.size(), r_pref), std::min(r_max, n - 5));
-  std::vector<int> T = VD;
-  for (auto* s : {&VS, &CD, &CS, &need})
-    for (int x : *s) if (!contains(T, x)) T.push_back(x);
-  for (int k = 0; (int)T.size() < r + 5 && k < n; ++k)
-    if (!contains(T, k)) T.push_back(k);
-  int g = (int)T.size() - r - 5;
-  if (g > 3) {
-    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
-    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
-  }
-  if (g < 0 || g > 3) return false;
-  std::sort(T.begin(), T.end());
-  // reader (store side): rho = VS (granule order), VD \ VS, extra (highest dst, not CD)
-  std::vector<int> rd_reg = VS;
-  for (int x : VD) if (!contains(rd_reg, x)) rd_reg.push_back(x);
-  {
-    std::vector<int> cand;
-    for (int x : T) if (!contains(rd_reg, x) && !contains(CD, x)) cand.push_back(x);
-    std::sort(cand.begin(), cand.end(), [](int a, int b) { return a > b; });
-    for (int x : cand) { if ((int)rd_reg.size() == r) break; rd_reg.push_back(x); }
-    if ((int)rd_reg.size() != r) return false;
-  }
-  std::vector<int> rd_lane, rd_warp;
-  {
-    for (int x : CD) if (!contains(rd_reg, x) && rd_lane.size() < 5) rd_lane.push_back(x);
-    std::vector<int> cand;
-    for (int x : T) if (!contains(rd_reg, x) && !contains(rd_lane, x)) cand.push_back(x);
-    std::sort(cand.begin(), cand.end());
-    for (int x : cand) (rd_lane.size() < 5 ? rd_lane : rd_warp).push_back(x);
-  }
-  // writer (cp.async): rho = VS + unroll (highest src, not CS); lanes lowest src
-  std::vector<int> wr_reg = VS;
-  {
-    std::vector<int> cand;
-    for (int x : T) if (!contains(wr_reg, x) && !contains(CS, x)) cand.push_back(x);
-    std::sort(cand.begin(), cand.end(), [&](int a, int b) { return sigma[a] > sigma[b]; });
-    for (int x : cand) { if ((int)wr_reg.size() == r) break; wr_reg.push_back(x); }
-    if ((int)wr_reg.size() != r) return false;
-  }
-  std::vector<int> wr_lane, wr_warp;
-  {
-    std::vector<int> cand;
-    for (int x : T) if (!contains(wr_reg, x)) cand.push_back(x);
-    std::sort(cand.begin(), cand.end(), [&](int a, int b) { return sigma[a] < sigma[b]; });
-    for (int x : cand) (wr_lane.size() < 5 ? wr_lane : wr_warp).push_back(x);
-  }
-  if (rd_lane.size() != 5 || wr_lane.size() != 5 || (int)rd_warp.size() != g ||
-      (int)wr_warp.size() != g)
-    return false;
-  // reader sub-word swaps (prmt): rho positions 0..nsub-1 must hold VD[0..nsub)
-  const int nsub = w >= 4 ? 0 : ilog2i(4 / w);
-  std::vector<int> order = rd_reg;
-  std::vector<std::pair<int, int>> swaps;
-  for (int t = 0; t < nsub; ++t) {
-    int s = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
-    if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
-  }
-  if ((int)swaps.size() > LL_MAX_SWAPS) return false;
-  auto wordbit = [&](int rho) { return w == 8 ? rho + 1 : rho - nsub; };
-  const int LB = w == 8 ? r + 1 : r - nsub;
-  std::vector<int> ssel;  // word bits forming a 16-byte store vector (2 word bits)
-  if (w == 8) ssel.push_back(0);
-  for (int t = (w == 8 ? 0 : nsub); t < vb; ++t) {
-    int pos = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
-    ssel.push_back(wordbit(pos));
-  }
-  if (ssel.size() != 2) return false;
-  std::vector<int> rest_rho;  // rho positions of the remaining word bits, ascending word bit
-  for (int wb = 0; wb < LB; ++wb) {
-    if (std::find(ssel.begin(), ssel.end(), wb) != ssel.end()) continue;
-    rest_rho.push_back(w == 8 ? wb - 1 : wb + nsub);
-  }
-  // swizzle: paper's construction, V = VS (source vector), writer A, reader B
-  const int d = (int)T.size();
-  auto loc = [&](int k) -> u64 {
-    return u64(1) << (std::find(T.begin(), T.end(), k) - T.begin());
-  };
-  std::vector<u64> Al, Bl, Vl;
-  for (int x : wr_lane) Al.push_back(loc(x));
-  for (int x : rd_lane) Bl.push_back(loc(x));
-  for (int x : VS) Vl.push_back(loc(x));
-  SwizzleResult sw = optimal_swizzle(Al, Bl, Vl, d, w);
-  std::vector<u64> Scols = sw.vect;
-  Scols.insert(Scols.end(), sw.bank.begin(), sw.bank.end());
-  Scols.insert(Scols.end(), sw.idx.begin(), sw.idx.end());
-  auto Sinv = f2_right_inverse(Scols, d);
-  const int lw = ilog2i(w);
-  for (int k : T)
-    if (sigma[k] + lw >= 31 || k + lw >= 31) return false;
-  auto boff = [&](int k) -> uint32_t { return (uint32_t)f2_apply(Sinv, loc(k)) << lw; };
-  SmemPlan& sp = P.sp;
-  sp = SmemPlan{};
-  sp.gw = g;
-  sp.tile_bytes = w << d;
-  sp.n_swaps = (int)swaps.size();
-  for (size_t i = 0; i < swaps.size(); ++i) {
-    sp.swap_a[i] = (int8_t)swaps[i].first;
-    sp.swap_b[i] = (int8_t)swaps[i].second;
-  }
-  sp.gsel_a = (int8_t)ssel[0];
-  sp.gsel_b = (int8_t)ssel[1];
-  for (int b = 0; b < 5; ++b) {
-    sp.ld_thr[b] = uint32_t(w) << sigma[wr_lane[b]];
-    sp.st_thr[b] = uint32_t(w) << rd_lane[b];
-    sp.sw_thr[b] = boff(wr_lane[b]);
-    sp.sr_thr[b] = boff(rd_lane[b]);
-  }
-  for (int b = 0; b < g; ++b) {
-    sp.ld_thr[5 + b] = uint32_t(w) << sigma[wr_warp[b]];
-    sp.st_thr[5 + b] = uint32_t(w) << rd_warp[b];
-    sp.sw_thr[5 + b] = boff(wr_warp[b]);
-    sp.sr_thr[5 + b] = boff(rd_warp[b]);
-  }
-  const int nvec = 1 << (r - vb);
-  if (nvec > LL_MAX_VEC || nvec > LL_MAX_GRAN) return false;
-  for (int u = 0; u < nvec; ++u) {
-    uint32_t lo = 0, wo = 0, ro = 0, so = 0;
-    for (int q = 0; q < r - vb; ++q) {
-      if ((u >> q) & 1) {
-        lo += uint32_t(w) << sigma[wr_reg[vb + q]];   // chunk u: source offset
-        wo ^= boff(wr_reg[vb + q]);                    //          smem offset
-        ro ^= boff(rd_reg[vb + q]);                    // granule u read offset
-        so += uint32_t(w) << order[rest_rho[q]];       // store vector u: dst offset
-      }
-    }
-    sp.ld_vec[u] = lo;
-    sp.sw_gran[u] = wo;
-    sp.sr_gran[u] = ro;
-    sp.st_vec[u] = so;
-  }
-  // tile map (dst order; top bits last)
-  std::vector<int> O;
-  for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
-  if ((int)O.size() > LL_MAX_OUTER) return false;
-  TileMap& tm = sp.tile;
-  tm.n_bits = (int)O.size();
-  tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
-  for (int k = 0; k < tm.n_tab; ++k)
-    for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
-      int64_t so = 0, dof = 0;
-      for (int q = 0; q < LL_TAB_BITS; ++q) {
-        const int bit = k * LL_TAB_BITS + q;
-        if (((v >> q) & 1) && bit < tm.n_bits) {
-          so += int64_t(w) << sigma[O[bit]];
-          dof += int64_t(w) << O[bit];
-        }
-      }
-      tm.tab[k][v].src = so;
-      tm.tab[k][v].dst = dof;
-    }
-  tm.batch_stride_src = int64_t(w) << P.nA;
-  tm.batch_stride_dst = int64_t(w) << P.nB;
-  tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
-  P.tile_bit_src.clear();
-  P.tile_bit_dst.clear();
-  for (int q = 0; q < tm.n_bits; ++q) {
-    P.tile_bit_src.push_back(sigma[O[q]]);
-    P.tile_bit_dst.push_back(O[q]);
-  }
-  P.nv = nvec;
-  P.g = 16;
-  P.tile_bits = d;
-  P.r = r;
-  P.gw = g;
-  P.pred_wf_ld = lemma_wavefronts(sw, Al, w);
-  P.pred_wf_st = lemma_wavefronts(sw, Bl, w);
-  auto srcpos = [&](const std::vector<int>& v) {
-    std::vector<int> o;
-    for (int x : v) o.push_back(sigma[x]);
-    return o;
-  };
-  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
-     << ",\"granule_bytes\":16,\"granule_dst_bits\":" << ivec_json(VS)
-     << ",\"vectors_per_thread\":" << nvec << ",\"swaps\":[";
-  for (size_t i = 0; i < swaps.size(); ++i)
-    js << (i ? "," : "") << "[" << swaps[i].first << "," << swaps[i].second << "]";
-  js << "],\"stg_sel\":" << ivec_json(ssel) << ",\"wr_reg_dst\":" << ivec_json(wr_reg)
-     << ",\"wr_reg_src\":" << ivec_json(srcpos(wr_reg)) << ",\"wr_lane_dst\":" << ivec_json(wr_lane)
-     << ",\"wr_lane_src\":" << ivec_json(srcpos(wr_lane)) << ",\"wr_warp_dst\":" << ivec_json(wr_warp)
-     << ",\"rd_reg\":" << ivec_json(rd_reg) << ",\"rd_rho_after_swaps\":" << ivec_json(order)
-     << ",\"rd_lane\":" << ivec_json(rd_lane) << ",\"rd_warp\":" << ivec_json(rd_warp)
-     << ",\"S_vect\":" << vec_json(sw.vect) << ",\"S_bank\":" << vec_json(sw.bank)
-     << ",\"S_idx\":" << vec_json(sw.idx) << ",\"H\":" << vec_json(sw.H) << ",\"C\":" << vec_json(sw.C)
-     << ",\"unavoidable\":" << (sw.unavoidable ? "true" : "false")
-     << ",\"pred_wavefronts_per_cp_async\":" << P.pred_wf_ld
-     << ",\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"n_tiles\":" << tm.n_tiles
-     << ",\"smem_bytes\":{\"sw_thr\":" << u32_json(sp.sw_thr, 5 + g) << ",\"sr_thr\":"
-     << u32_json(sp.sr_thr, 5 + g) << ",\"sw_gran\":" << u32_json(sp.sw_gran, nvec)
-     << ",\"sr_gran\":" << u32_json(sp.sr_gran, nvec) << "}";
-  return true;
-}
-
-// TMA-fed variant of the shared-memory path (LL_PATH_SMEM_TMA).  The source
-// tile is fetched by one cp.async.bulk.tensor per tile into a dense image
-// (tile bits in ascending source order) permuted by a hardware swizzle mode
-// m in {none, 32 B, 64 B, 128 B}: byte-address bits [4, 4+m) ^= [7, 7+m).
-// That map is Def. 5 with vec = 16 bytes, per_phase = 1 and
-// max_phase = 2^m on rows of 16 << m bytes (tests: test_oracle_swizzle.py),
-// i.e. a fixed member of the family the paper's construction searches; the
-// planner therefore cannot choose S, but chooses (a) the mode and (b) the
-// reader's lanes so that the reader's 16-byte granules are conflict-free
-// under it (wavefronts = 4 * 2^(rank(phase cols) - rank(bank projection)),
-// the lemma P:1083-1089 for 16-byte granules), and among conflict-free
-// choices the one with the longest coalesced destination runs.  The reader
-// holds VS u VD in registers and permutes into destination vectors exactly
-// as the cp.async path does.
-bool plan_tma(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js) {
-  const int n = P.nB, w = P.w;
-  if (P.nA != P.nB || n > 62 || w > 8) return false;
-  std::vector<int> sigma(n), sinv(n, -1);
-  for (int k = 0; k < n; ++k) {
-    if (popcount64(X[k]) != 1) return false;
-    sigma[k] = ctz64(X[k]);
-    if (sinv[sigma[k]] >= 0) return false;
-    sinv[sigma[k]] = k;
-  }
-  const int vb = ilog2i(16 / w);
-  const int lw = ilog2i(w);
-  if (n < vb + 5) return false;
-  auto contains = [](const std::vector<int>& v, int x) {
-    return std::find(v.begin(), v.end(), x) != v.end();
-  };
-  std::vector<int> VD, VS, CD, CS;
-  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
-  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("tma_run_bytes", 256)) / 16));
-  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
-  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
-  const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("tma_thread_bytes", 64)) / w));
-  std::vector<int> need = VS;
-  for (int x : VD) if (!contains(need, x)) need.push_back(x);
-  if ((int)need.size() > r_max || (int)need.size() + 5 > n) return false;
-  int r = std::min(std::max((int)need.size(), r_pref), std::min(r_max, n - 5));
-  // tile: the vectors and coalescing runs of both sides, then the lowest
-  // destination bits; at least tma_tile_bytes (several KB in flight per TMA)
-  const int tile_min = ilog2i(std::max(1024, planner_knob("tma_tile_bytes", 8192)) / w);
-  std::vector<int> T = VD;
-  for (auto* s : {&VS, &CD, &CS, &need})
-    for (int x : *s) if (!contains(T, x)) T.push_back(x);
-  for (int k = 0; (int)T.size() < std::max(r + 5, std::min(n, tile_min)) && k < n; ++k)
-    if (!contains(T, k)) T.push_back(k);
-  int g = (int)T.size() - r - 5;
-  if (g > 3) {
-    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
-    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
-  }
-  if (g < 0 || g > 3) return false;
-  std::sort(T.begin(), T.end());
-  const int d = (int)T.size();
-  // dense image: rank of the source bit among the tile's source bits
-  std::vector<int> Ts;
-  for (int k : T) Ts.push_back(sigma[k]);
-  std::sort(Ts.begin(), Ts.end());
-  auto dense = [&](int k) -> uint32_t {
-    return uint32_t(w) << (std::find(Ts.begin(), Ts.end(), sigma[k]) - Ts.begin());
-  };
-  for (int k : T)
-    if (sigma[k] + lw >= 40 || d + lw > 20) return false;
-  // reader registers: VS (granule order), VD \ VS, extra (highest dst, not CD)
-  std::vector<int> rd_reg = VS;
-  for (int x : VD) if (!contains(rd_reg, x)) rd_reg.push_back(x);
-  {
-    std::vector<int> cand;
-    for (int x : T) if (!contains(rd_reg, x) && !contains(CD, x)) cand.push_back(x);
-    std::sort(cand.begin(), cand.end(), [](int a, int b) { return a > b; });
-    for (int x : cand) { if ((int)rd_reg.size() == r) break; rd_reg.push_back(x); }
-    if ((int)rd_reg.size() != r) return false;
-  }
-  // TMA box dims for swizzle mode m: runs of consecutive source bits; the
-  // first run is split at the swizzle span (16 << m bytes), every box dim is
-  // at most 256 elements; <= 5 dims
-  auto make_desc = [&](int m, TmaDesc& td) -> bool {
-    td = TmaDesc{};
-    td.swizzle = m;
-    std::vector<std::pair<int, int>> runs;  // (first source bit, length)
-    for (int b : Ts) {
-      if (!runs.empty() && runs.back().first + runs.back().second == b) ++runs.back().second;
-      else runs.push_back({b, 1});
-    }
-    if (runs.empty() || runs[0].first != 0) return false;
-    const int span_bits = m ? ilog2i((16 << m) / w) : 8;
-    std::vector<std::pair<int, int>> dims;  // (shift, box bits)
-    for (size_t i = 0; i < runs.size(); ++i) {
-      int a = runs[i].first, len = runs[i].second;
-      if (i == 0 && m) {
-        if (len < span_bits) return false;
-        dims.push_back({a, span_bits});
-        a += span_bits;
-        len -= span_bits;
-      }
-      while (len > 0) {
-        const int piece = std::min(len, 8);
-        dims.push_back({a, piece});
-        a += piece;
-        len -= piece;
-      }
-    }
-    if (dims.size() > 5) return false;
-    if (!m && dims[0].second > 8) return false;
-    td.ndim = (int)dims.size();
-    for (int i = 0; i < td.ndim; ++i) {
-      td.shift[i] = dims[i].first;
-      td.box_bits[i] = dims[i].second;
-      td.size_bits[i] = i + 1 < td.ndim ? dims[i + 1].first - dims[i].first : 0;
-      if (i > 0 && (dims[i].first + lw) < 4) return false;  // strides: multiples of 16 B
-    }
-    return true;
-  };
-  auto swz = [](uint32_t a, int m) -> uint32_t {
-    return m ? a ^ (((a >> 7) & ((1u << m) - 1)) << 4) : a;
-  };
-  struct Choice {
-    int m = -1, wf = 1 << 30, run = -1;
-    std::vector<int> lane, warp;
-    TmaDesc td{};
-  } best;
-  const int force = planner_knob("tma_force_swizzle", -1);
-  for (int m = 0; m <= 3; ++m) {
-    if (force >= 0 && m != force) continue;
-    Choice c;
-    c.m = m;
-    if (!make_desc(m, c.td)) continue;
-    auto addr = [&](int k) { return swz(dense(k), m); };
-    std::vector<int> cand;
-    for (int x : T) if (!contains(rd_reg, x)) cand.push_back(x);
-    std::sort(cand.begin(), cand.end());
-    // phase lanes (lane bits 0-2 of a 16-byte access): independent bank
-    // projections (address bits 4-6), lowest destination bits first
-    std::vector<int> phase;
-    std::vector<u64> proj;
-    for (int x : cand) {
-      if (phase.size() == 3) break;
-      std::vector<u64> p2 = proj;
-      p2.push_back((addr(x) >> 4) & 7u);
-      if (f2_rank(p2) > f2_rank(proj)) { phase.push_back(x); proj = p2; }
-    }
-    for (int x : cand) {
-      if (phase.size() == 3) break;
-      if (!contains(phase, x)) phase.push_back(x);
-    }
-    c.lane = phase;
-    for (int x : cand) {
-      if (c.lane.size() == 5) break;
-      if (!contains(c.lane, x)) c.lane.push_back(x);
-    }
-    for (int x : cand) if (!contains(c.lane, x)) c.warp.push_back(x);
-    std::vector<u64> pc, pp;
-    for (int i = 0; i < 3; ++i) {
-      pc.push_back(addr(c.lane[i]));
-      pp.push_back((addr(c.lane[i]) >> 4) & 7u);
-    }
-    c.wf = 4 << (f2_rank(pc) - f2_rank(pp));
-    // destination run of one store instruction: 16 B x 2^(lane bits that
-    // extend the vector contiguously, in lane order)
-    std::vector<int> sl = c.lane;
-    int run = 0;
-    for (int q = 0;; ++q) {
-      if (!contains(sl, vb + q)) break;
-      ++run;
-    }
-    c.run = run;
-    if (c.wf < best.wf || (c.wf == best.wf && c.run > best.run)) best = c;
-  }
-  if (best.m < 0 || (int)best.warp.size() != g) return false;
-  const int m = best.m;
-  std::vector<int> rd_lane = best.lane, rd_warp = best.warp;
-  // reader sub-word swaps / store selection: as in plan_async
-  const int nsub = w >= 4 ? 0 : ilog2i(4 / w);
-  std::vector<int> order = rd_reg;
-  std::vector<std::pair<int, int>> swaps;
-  for (int t = 0; t < nsub; ++t) {
-    int s = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
-    if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
-  }
-  if ((int)swaps.size() > LL_MAX_SWAPS) return false;
-  auto wordbit = [&](int rho) { return w == 8 ? rho + 1 : rho - nsub; };
-  const int LB = w == 8 ? r + 1 : r - nsub;
-  std::vector<int> ssel;
-  if (w == 8) ssel.push_back(0);
-  for (int t = (w == 8 ? 0 : nsub); t < vb; ++t) {
-    int pos = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
-    ssel.push_back(wordbit(pos));
-  }
-  if (ssel.size() != 2) return false;
-  std::vector<int> rest_rho;
-  for (int wb = 0; wb < LB; ++wb) {
-    if (std::find(ssel.begin(), ssel.end(), wb) != ssel.end()) continue;
-    rest_rho.push_back(w == 8 ? wb - 1 : wb + nsub);
-  }
-  auto boff = [&](int k) -> uint32_t { return swz(dense(k), m); };
-  SmemPlan& sp = P.sp;
-  sp = SmemPlan{};
-  sp.gw = g;
-  sp.tile_bytes = w << d;
-  sp.n_swaps = (int)swaps.size();
-  for (size_t i = 0; i < swaps.size(); ++i) {
-    sp.swap_a[i] = (int8_t)swaps[i].first;
-    sp.swap_b[i] = (int8_t)swaps[i].second;
-  }
-  sp.gsel_a = (int8_t)ssel[0];
-  sp.gsel_b = (int8_t)ssel[1];
-  for (int b = 0; b < 5 + g; ++b) {
-    const int k = b < 5 ? rd_lane[b] : rd_warp[b - 5];
-    sp.st_thr[b] = uint32_t(w) << k;
-    sp.sr_thr[b] = boff(k);
-  }
-  const int nvec = 1 << (r - vb);
-  if (nvec > LL_MAX_VEC || nvec > LL_MAX_GRAN) return false;
-  for (int u = 0; u < nvec; ++u) {
-    uint32_t ro = 0, so = 0;
-    for (int q = 0; q < r - vb; ++q) {
-      if ((u >> q) & 1) {
-        ro ^= boff(rd_reg[vb + q]);
-        so += uint32_t(w) << order[rest_rho[q]];
-      }
-    }
-    sp.sr_gran[u] = ro;
-    sp.st_vec[u] = so;
-  }
-  std::vector<int> O;
-  for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
-  if ((int)O.size() > LL_MAX_OUTER) return false;
-  TileMap& tm = sp.tile;
-  tm.n_bits = (int)O.size();
-  tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
-  for (int k = 0; k < tm.n_tab; ++k)
-    for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
-      int64_t so = 0, dof = 0;
-      for (int q = 0; q < LL_TAB_BITS; ++q) {
-        const int bit = k * LL_TAB_BITS + q;
-        if (((v >> q) & 1) && bit < tm.n_bits) {
-          so += int64_t(w) << sigma[O[bit]];
-          dof += int64_t(w) << O[bit];
-        }
-      }
-      tm.tab[k][v].src = so;
-      tm.tab[k][v].dst = dof;
-    }
-  tm.batch_stride_src = int64_t(w) << P.nA;
-  tm.batch_stride_dst = int64_t(w) << P.nB;
-  tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
-  P.tile_bit_src.clear();
-  P.tile_bit_dst.clear();
-  for (int q = 0; q < tm.n_bits; ++q) {
-    P.tile_bit_src.push_back(sigma[O[q]]);
-    P.tile_bit_dst.push_back(O[q]);
-  }
-  P.td = best.td;
-  P.nv = nvec;
-  P.g = 16;
-  P.tile_bits = d;
-  P.r = r;
-  P.gw = g;
-  P.pred_wf_ld = 0;  // the TMA write has no bank conflicts to predict
-  P.pred_wf_st = best.wf;
-  std::vector<int> shifts, boxes;
-  for (int i = 0; i < P.td.ndim; ++i) {
-    shifts.push_back(P.td.shift[i]);
-    boxes.push_back(P.td.box_bits[i]);
-  }
-  static const char* mode_names[] = {"none", "32B", "64B", "128B"};
-  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
-     << ",\"granule_bytes\":16,\"granule_dst_bits\":" << ivec_json(VS)
-     << ",\"vectors_per_thread\":" << nvec << ",\"swaps\":[";
-  for (size_t i = 0; i < swaps.size(); ++i)
-    js << (i ? "," : "") << "[" << swaps[i].first << "," << swaps[i].second << "]";
-  js << "],\"stg_sel\":" << ivec_json(ssel) << ",\"rd_reg\":" << ivec_json(rd_reg)
-     << ",\"rd_rho_after_swaps\":" << ivec_json(order) << ",\"rd_lane\":" << ivec_json(rd_lane)
-     << ",\"rd_warp\":" << ivec_json(rd_warp) << ",\"tma\":{\"swizzle\":\"" << mode_names[m]
-     << "\",\"ndim\":" << P.td.ndim << ",\"dim_src_shift\":" << ivec_json(shifts)
-     << ",\"box_bits\":" << ivec_json(boxes) << ",\"store_run_bytes\":" << (16 << best.run)
-     << "},\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"n_tiles\":" << tm.n_tiles
-     << ",\"smem_bytes\":{\"sr_thr\":" << u32_json(sp.sr_thr, 5 + g)
-     << ",\"sr_gran\":" << u32_json(sp.sr_gran, nvec) << "}";
-  return true;
-}
-
-// TMA load + TMA store variant (LL_PATH_SMEM_TMA_STORE).  As plan_tma, but
-// the readers write their destination vectors into a second shared-memory
-// image (the destination tile, dense in destination-bit order, hardware
-// swizzle md) that one cp.async.bulk.tensor store sends to HBM.  The
-// readers' lanes are then free of global coalescing and must make BOTH the
-// 16-byte reads of the source image and the 16-byte writes of the
-// destination image conflict-free; when no set of single tile bits does,
-// XOR combinations are used (a lane bit then moves along a "diagonal" of the
-// tile -- the paper's swizzling idea applied to the thread layout).
-bool plan_tma_store(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js) {
-  const int n = P.nB, w = P.w;
-  if (P.nA != P.nB || n > 62 || w > 8) return false;
-  std::vector<int> sigma(n), sinv(n, -1);
-  for (int k = 0; k < n; ++k) {
-    if (popcount64(X[k]) != 1) return false;
-    sigma[k] = ctz64(X[k]);
-    if (sinv[sigma[k]] >= 0) return false;
-    sinv[sigma[k]] = k;
-  }
-  const int vb = ilog2i(16 / w);
-  const int lw = ilog2i(w);
-  if (n < vb + 5) return false;
-  auto contains = [](const std::vector<int>& v, int x) {
-    return std::find(v.begin(), v.end(), x) != v.end();
-  };
-  std::vector<int> VD, VS, CD, CS;
-  for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
-  const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("tma_run_bytes", 256)) / 16));
-  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
-  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
-  const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("tma_thread_bytes", 64)) / w));
-  std::vector<int> need = VS;
-  for (int x : VD) if (!contains(need, x)) need.push_back(x);
-  if ((int)need.size() > r_max || (int)need.size() + 5 > n) return false;
-  int r = std::min(std::max((int)need.size(), r_pref), std::min(r_max, n - 5));
-  const int tile_min = ilog2i(std::max(1024, planner_knob("tma_tile_bytes", 8192)) / w);
-  std::vector<int> T = VD;
-  for (auto* s : {&VS, &CD, &CS, &need})
-    for (int x : *s) if (!contains(T, x)) T.push_back(x);
-  for (int k = 0; (int)T.size() < std::max(r + 5, std::min(n, tile_min)) && k < n; ++k)
-    if (!contains(T, k)) T.push_back(k);
-  int g = (int)T.size() - r - 5;
-  if (g > 3) {
-    int r2 = std::min(r_max, (int)T.size() - 5 - 3);
-    if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
-  }
-  if (g < 0 || g > 3) return false;
-  std::sort(T.begin(), T.end());
-  const int d = (int)T.size();
-  if (d + lw > 20) return false;
-  std::vector<int> Ts;
-  for (int k : T) Ts.push_back(sigma[k]);
-  std::sort(Ts.begin(), Ts.end());
-  // dense images (byte offsets before the swizzle), linear in tile vectors
-  auto dense_s = [&](u64 v) -> uint32_t {
-    uint32_t o = 0;
-    for (int k = 0; k < n; ++k)
-      if ((v >> k) & 1) o ^= uint32_t(w) << (std::find(Ts.begin(), Ts.end(), sigma[k]) - Ts.begin());
-    return o;
-  };
-  auto dense_d = [&](u64 v) -> uint32_t {
-    uint32_t o = 0;
-    for (int k = 0; k < n; ++k)
-      if ((v >> k) & 1) o ^= uint32_t(w) << (std::find(T.begin(), T.end(), k) - T.begin());
-    return o;
-  };
-  auto swz = [](uint32_t a, int m) -> uint32_t {
-    return m ? a ^ (((a >> 7) & ((1u << m) - 1)) << 4) : a;
-  };
-  std::vector<int> rd_reg = VS;
-  for (int x : VD) if (!contains(rd_reg, x)) rd_reg.push_back(x);
-  {
-    std::vector<int> cand;
-    for (int x : T) if (!contains(rd_reg, x) && !contains(CD, x)) cand.push_back(x);
-    std::sort(cand.begin(), cand.end(), [](int a, int b) { return a > b; });
-    for (int x : cand) { if ((int)rd_reg.size() == r) break; rd_reg.push_back(x); }
-    if ((int)rd_reg.size() != r) return false;
-  }
-  auto make_desc = [&](const std::vector<int>& bits, int m, TmaDesc& td) -> bool {
-    td = TmaDesc{};
-    td.swizzle = m;
-    std::vector<std::pair<int, int>> runs;
-    for (int b : bits) {
-      if (!runs.empty() && runs.back().first + runs.back().second == b) ++runs.back().second;
-      else runs.push_back({b, 1});
-    }
-    if (runs.empty() || runs[0].first != 0) return false;
-    const int span_bits = m ? ilog2i((16 << m) / w) : 8;
-    std::vector<std::pair<int, int>> dims;
-    for (size_t i = 0; i < runs.size(); ++i) {
-      int a = runs[i].first, len = runs[i].second;
-      if (i == 0 && m) {
-        if (len < span_bits) return false;
-        dims.push_back({a, span_bits});
-        a += span_bits;
-        len -= span_bits;
-      }
-      while (len > 0) {
-        const int piece = std::min(len, 8);
-        dims.push_back({a, piece});
-        a += piece;
-        len -= piece;
-      }
-    }
-    if (dims.size() > 5) return false;
-    td.ndim = (int)dims.size();
-    for (int i = 0; i < td.ndim; ++i) {
-      td.shift[i] = dims[i].first;
-      td.box_bits[i] = dims[i].second;
-      td.size_bits[i] = i + 1 < td.ndim ? dims[i + 1].first - dims[i].first : 0;
-      if (i > 0 && (dims[i].first + lw) < 4) return false;
-    }
-    return true;
-  };
-  // candidate lane vectors: single non-register tile bits (lowest
-  // destination bit first), then their pairwise XORs
-  std::vector<u64> singles, cands;
-  for (int x : T) if (!contains(rd_reg, x)) singles.push_back(u64(1) << x);
-  cands = singles;
-  for (size_t i = 0; i < singles.size(); ++i)
-    for (size_t j = i + 1; j < singles.size(); ++j) cands.push_back(singles[i] | singles[j]);
-  struct Choice {
-    int ms = -1, md = -1, wf = 1 << 30, diag = 0;
-    std::vector<u64> thr;   // 5 lanes then g warps
-    TmaDesc tds{}, tdd{};
-  } best;
-  for (int ms = 0; ms <= 3; ++ms) {
-    for (int md = 0; md <= 3; ++md) {
-      Choice c;
-      c.ms = ms;
-      c.md = md;
-      if (!make_desc(Ts, ms, c.tds) || !make_desc(T, md, c.tdd)) continue;
-      auto ps = [&](u64 v) -> u64 { return (swz(dense_s(v), ms) >> 4) & 7u; };
-      auto pd = [&](u64 v) -> u64 { return (swz(dense_d(v), md) >> 4) & 7u; };
-      std::vector<u64> phase, prs, prd;
-      F2Basis span;
-      for (u64 v : cands) {
-        if (phase.size() == 3) break;
-        if (span.in_span(v)) continue;
-        std::vector<u64> a = prs, b = prd;
-        a.push_back(ps(v));
-        b.push_back(pd(v));
-        if (f2_rank(a) > f2_rank(prs) && f2_rank(b) > f2_rank(prd)) {
-          phase.push_back(v);
-          prs = a;
-          prd = b;
-          span.add(v);
-        }
-      }
-      for (u64 v : singles) {
-        if (phase.size() == 3) break;
-        if (span.add(v)) phase.push_back(v);
-      }
-      c.thr = phase;
-      for (u64 v : singles)
-        if (span.add(v)) c.thr.push_back(v);
-      if ((int)c.thr.size() != 5 + g) continue;
-      std::vector<u64> as, ad, qs, qd;
-      for (int i = 0; i < 3; ++i) {
-        as.push_back(swz(dense_s(c.thr[i]), ms));
-        ad.push_back(swz(dense_d(c.thr[i]), md));
-        qs.push_back(ps(c.thr[i]));
-        qd.push_back(pd(c.thr[i]));
-      }
-      c.wf = (4 << (f2_rank(as) - f2_rank(qs))) + (4 << (f2_rank(ad) - f2_rank(qd)));
-      for (u64 v : c.thr) c.diag += popcount64(v) > 1;
-      if (c.wf < best.wf || (c.wf == best.wf && c.diag < best.diag)) best = c;
-    }
-  }
-  if (best.ms < 0) return false;
-  const int nsub = w >= 4 ? 0 : ilog2i(4 / w);
-  std::vector<int> order = rd_reg;
-  std::vector<std::pair<int, int>> swaps;
-  for (int t = 0; t < nsub; ++t) {
-    int s = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
-    if (s != t) { swaps.push_back({t, s}); std::swap(order[t], order[s]); }
-  }
-  if ((int)swaps.size() > LL_MAX_SWAPS) return false;
-  auto wordbit = [&](int rho) { return w == 8 ? rho + 1 : rho - nsub; };
-  const int LB = w == 8 ? r + 1 : r - nsub;
-  std::vector<int> ssel;
-  if (w == 8) ssel.push_back(0);
-  for (int t = (w == 8 ? 0 : nsub); t < vb; ++t) {
-    int pos = (int)(std::find(order.begin(), order.end(), VD[t]) - order.begin());
-    ssel.push_back(wordbit(pos));
-  }
-  if (ssel.size() != 2) return false;
-  std::vector<int> rest_rho;
-  for (int wb = 0; wb < LB; ++wb) {
-    if (std::find(ssel.begin(), ssel.end(), wb) != ssel.end()) continue;
-    rest_rho.push_back(w == 8 ? wb - 1 : wb + nsub);
-  }
-  auto roff = [&](u64 v) -> uint32_t { return swz(dense_s(v), best.ms); };
-  auto woff = [&](u64 v) -> uint32_t { return swz(dense_d(v), best.md); };
-  SmemPlan& sp = P.sp;
-  sp = SmemPlan{};
-  sp.gw = g;
-  sp.tile_bytes = w << d;
-  sp.n_swaps = (int)swaps.size();
-  for (size_t i = 0; i < swaps.size(); ++i) {
-    sp.swap_a[i] = (int8_t)swaps[i].first;
-    sp.swap_b[i] = (int8_t)swaps[i].second;
-  }
-  sp.gsel_a = (int8_t)ssel[0];
-  sp.gsel_b = (int8_t)ssel[1];
-  for (int b = 0; b < 5 + g; ++b) {
-    sp.sr_thr[b] = roff(best.thr[b]);
-    sp.sw_thr[b] = woff(best.thr[b]);
-  }
-  const int nvec = 1 << (r - vb);
-  if (nvec > LL_MAX_VEC || nvec > LL_MAX_GRAN) return false;
-  for (int u = 0; u < nvec; ++u) {
-    uint32_t ro = 0, wo = 0;
-    for (int q = 0; q < r - vb; ++q) {
-      if ((u >> q) & 1) {
-        ro ^= roff(u64(1) << rd_reg[vb + q]);            // source granule u
-        wo ^= woff(u64(1) << order[rest_rho[q]]);        // destination vector u
-      }
-    }
-    sp.sr_gran[u] = ro;
-    sp.sw_gran[u] = wo;
-  }
-  std::vector<int> O;
-  for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
-  if ((int)O.size() > LL_MAX_OUTER) return false;
-  TileMap& tm = sp.tile;
-  tm.n_bits = (int)O.size();
-  tm.n_tab = (tm.n_bits + LL_TAB_BITS - 1) / LL_TAB_BITS;
-  for (int k = 0; k < tm.n_tab; ++k)
-    for (int v = 0; v < (1 << LL_TAB_BITS); ++v) {
-      int64_t so = 0, dof = 0;
-      for (int q = 0; q < LL_TAB_BITS; ++q) {
-        const int bit = k * LL_TAB_BITS + q;
-        if (((v >> q) & 1) && bit < tm.n_bits) {
-          so += int64_t(w) << sigma[O[bit]];
-          dof += int64_t(w) << O[bit];
-        }
-      }
-      tm.tab[k][v].src = so;
-      tm.tab[k][v].dst = dof;
-    }
-  tm.batch_stride_src = int64_t(w) << P.nA;
-  tm.batch_stride_dst = int64_t(w) << P.nB;
-  tm.n_tiles = (int64_t(1) << O.size()) * P.batch;
-  P.tile_bit_src.clear();
-  P.tile_bit_dst.clear();
-  for (int q = 0; q < tm.n_bits; ++q) {
-    P.tile_bit_src.push_back(sigma[O[q]]);
-    P.tile_bit_dst.push_back(O[q]);
-  }
-  P.td = best.tds;
-  P.td_dst = best.tdd;
-  P.nv = nvec;
-  P.g = 16;
-  P.tile_bits = d;
-  P.r = r;
-  P.gw = g;
-  std::vector<u64> as, ad, qs, qd;
-  for (int i = 0; i < 3; ++i) {
-    as.push_back(roff(best.thr[i]));
-    ad.push_back(woff(best.thr[i]));
-    qs.push_back((roff(best.thr[i]) >> 4) & 7u);
-    qd.push_back((woff(best.thr[i]) >> 4) & 7u);
-  }
-  P.pred_wf_st = 4 << (f2_rank(as) - f2_rank(qs));   // LDS of the source image
-  P.pred_wf_ld = 4 << (f2_rank(ad) - f2_rank(qd));   // STS of the destination image
-  static const char* mode_names[] = {"none", "32B", "64B", "128B"};
-  auto td_json = [&](const TmaDesc& t) {
-    std::vector<int> sh, bx;
-    for (int i = 0; i < t.ndim; ++i) { sh.push_back(t.shift[i]); bx.push_back(t.box_bits[i]); }
-    std::ostringstream o;
-    o << "{\"swizzle\":\"" << mode_names[t.swizzle] << "\",\"ndim\":" << t.ndim
-      << ",\"dim_shift\":" << ivec_json(sh) << ",\"box_bits\":" << ivec_json(bx) << "}";
-    return o.str();
-  };
-  js << ",\"tile_dst_bits\":" << ivec_json(T) << ",\"r\":" << r << ",\"group_warps_log2\":" << g
-     << ",\"granule_bytes\":16,\"vectors_per_thread\":" << nvec << ",\"rd_reg\":" << ivec_json(rd_reg)
-     << ",\"thread_vecs_dst_bits\":" << vec_json(best.thr) << ",\"diagonal_lanes\":" << best.diag
-     << ",\"tma\":{\"src\":" << td_json(best.tds) << ",\"dst\":" << td_json(best.tdd) << "}"
-     << ",\"pred_wavefronts_per_lds\":" << P.pred_wf_st << ",\"pred_wavefronts_per_sts\":" << P.pred_wf_ld
-     << ",\"n_tiles\":" << tm.n_tiles << ",\"smem_bytes\":{\"sr_thr\":" << u32_json(sp.sr_thr, 5 + g)
-     << ",\"sw_thr\":" << u32_json(sp.sw_thr, 5 + g) << ",\"sr_gran\":" << u32_json(sp.sr_gran, nvec)
-     << ",\"sw_gran\":" << u32_json(sp.sw_gran, nvec) << "}";
-  return true;
-}
-
-// Register-faithful plan (LL_PATH_REGS): the paper's in-kernel conversion.
-// Tile-local vectors live in A's (reg, lane, warp) index space: A's input bit
-// i is e_i, B's input bit k is X[k].  Shared memory S = the paper's optimal
-// swizzle for the two sides' bank-relevant thread vectors with S_vect =
-// [word bits, granule bits]; each side writes / reads either vectors
-// (generalised vectorisation) or stmatrix / ldmatrix rows when its
-// layout divided by the tile T = id^{reg,offset}_k x id^{thread,offset}_2
-// (left division P:354-362) exists -- checked on S^{-1} o L.
-// Common frame of the register-faithful plans: both layouts are reg / lane /
-// warp / block with 5 lane bits, equal reg and warp bits and identical block
-// columns; tile vectors in A's (reg, lane, warp) index space; B's word must
-// hold elements A holds in registers (load-side prmt swaps).
-struct RegsFrame {
-  int w, lw, nr, nw, d, n, kw, LB, NW;
-  std::vector<std::pair<int, int>> swaps;
-  std::vector<u64> WB, Aw, Bw, Al, Bl, Awp, Bwp;
-};
-
-bool regs_frame(const ConvertPlan& P, const Layout& A, const Layout& B, const std::vector<u64>& X,
-                RegsFrame& f) {
-  const int w = P.w;
-  if (w > 4 || P.nA != P.nB) return false;
-  auto dims_ok = [](const Layout& L) {
-    static const char* order[] = {"reg", "lane", "warp", "block"};
-    size_t k = 0;
-    for (auto& d : L.in) {
-      while (k < 4 && d.name != order[k]) ++k;
-      if (k == 4) return false;
-      ++k;
-    }
-    return true;
-  };
-  if (!dims_ok(A) || !dims_ok(B)) return false;
-  const int nr = A.in_size("reg"), nw = A.in_size("warp");
-  if (B.in_size("reg") != nr || B.in_size("warp") != nw || A.in_size("lane") != 5 ||
-      B.in_size("lane") != 5 || nw > 3)
-    return false;
-  const int d = nr + 5 + nw;
-  const int n = P.nB;
-  for (int k = d; k < n; ++k)
-    if (X[k] != (u64(1) << k)) return false;  // block bits: identical columns
-  const u64 tmask = (u64(1) << d) - 1;
-  for (int k = 0; k < d; ++k)
-    if (!X[k] || (X[k] & ~tmask)) return false;
-  {
-    std::vector<u64> xt(X.begin(), X.begin() + d);
-    if (f2_rank(xt) != d) return false;
-  }
-  const int lw = ilog2i(w);
-  const int kw = ilog2i(4 / w);             // element bits inside a 32-bit word
-  if (nr < kw) return false;
-  const int LB = nr - kw;                   // word-index bits
-  const int NW = 1 << LB;
-  if (NW > 64) return false;
-  auto e = [](int i) { return u64(1) << i; };
-  // word bits: B's word must hold the same elements as A's (prmt swaps on load)
-  // (any of A's register bits can be moved into the word by prmt / renames
-  // on load, the paper's register permutation P_reg)
-  std::vector<u64> WB(X.begin(), X.begin() + kw);
-  std::vector<std::pair<int, int>> swaps;
-  std::vector<u64> cur;  // A's register columns in register order after the swaps
-  for (int t = 0; t < nr; ++t) cur.push_back(e(t));
-  for (int t = 0; t < kw; ++t) {
-    auto it = std::find(cur.begin(), cur.end(), WB[t]);
-    if (it == cur.end()) return false;
-    int s = (int)(it - cur.begin());
-    if (s < t) return false;
-    if (s != t) { swaps.push_back({t, s}); std::swap(cur[t], cur[s]); }
-  }
-  // word-level columns, lanes, warps of both sides (tile vectors)
-  std::vector<u64> Aw, Bw, Al, Bl, Awp, Bwp;
-  for (int u = 0; u < LB; ++u) { Aw.push_back(cur[kw + u]); Bw.push_back(X[kw + u]); }
-  for (int b = 0; b < 5; ++b) { Al.push_back(e(nr + b)); Bl.push_back(X[nr + b]); }
-  for (int b = 0; b < nw; ++b) { Awp.push_back(e(nr + 5 + b)); Bwp.push_back(X[nr + 5 + b]); }
-  f.w = w; f.lw = lw; f.nr = nr; f.nw = nw; f.d = d; f.n = n; f.kw = kw; f.LB = LB; f.NW = NW;
-  f.swaps = swaps;
-  f.WB = WB; f.Aw = Aw; f.Bw = Bw; f.Al = Al; f.Bl = Bl; f.Awp = Awp; f.Bwp = Bwp;
-  return true;
-}
-
-bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vector<u64>& X,
-               std::ostringstream& js) {
-  RegsFrame f;
-  if (!regs_frame(P, A, B, X, f)) return false;
-  const int w = f.w, lw = f.lw, nr = f.nr, nw = f.nw, d = f.d, n = f.n, kw = f.kw, LB = f.LB, NW = f.NW;
-  (void)nr;
-  auto e = [](int i) { return u64(1) << i; };
-  const auto& swaps = f.swaps;
-  const auto &WB = f.WB, &Aw = f.Aw, &Bw = f.Bw, &Al = f.Al, &Bl = f.Bl, &Awp = f.Awp, &Bwp = f.Bwp;
-  auto pos = [](const std::vector<u64>& v, u64 x) {
-    auto it = std::find(v.begin(), v.end(), x);
-    return it == v.end() ? -1 : (int)(it - v.begin());
-  };
-  const bool allow_mat = planner_knob("regs_matrix", 1) != 0;
-  // candidate granule rows: (extra S_vect vectors beyond the word, side kinds)
-  struct Opt {
-    std::vector<u64> gv;     // granule vectors after the word bits (<= 2)
-    int wr_mat = 0, rd_mat = 0, wr_gw = 1, rd_gw = 1;
-    int wa = -1, wb = -1, ra = -1, rb = -1;
-    int cost = 1 << 30;
-  };
-  std::vector<Opt> opts;
-  auto side = [&](const std::vector<u64>& gv, const std::vector<u64>& W, const std::vector<u64>& L,
-                  int& mat, int& gw, int& a, int& b) {
-    // matrix: the granule rows are exactly the side's lanes 0, 1
-    if (allow_mat && gv.size() == 2 && L[0] == gv[0] && L[1] == gv[1]) {
-      mat = 1;
-      gw = std::min(4, NW);
-      a = LB > 0 ? 0 : -1;
-      b = LB > 1 ? 1 : -1;
-      return;
-    }
-    // vector: the longest prefix of gv the side holds as word bits
-    mat = 0;
-    int q = 0;
-    a = b = -1;
-    if (q < (int)gv.size() && pos(W, gv[0]) >= 0) { a = pos(W, gv[0]); ++q; }
-    if (q == 1 && q < (int)gv.size() && pos(W, gv[1]) >= 0) { b = pos(W, gv[1]); ++q; }
-    gw = 1 << q;
-  };
-  auto consider = [&](const std::vector<u64>& gv) {
-    Opt o;
-    o.gv = gv;
-    side(gv, Aw, Al, o.wr_mat, o.wr_gw, o.wa, o.wb);
-    side(gv, Bw, Bl, o.rd_mat, o.rd_gw, o.ra, o.rb);
-    o.cost = NW / o.wr_gw + NW / o.rd_gw;
-    opts.push_back(o);
-  };
-  {  // generalised vectorisation: word-level columns common to both sides
-    std::vector<u64> gv;
-    for (u64 x : Aw) if (pos(Bw, x) >= 0 && gv.size() < 2) gv.push_back(x);
-    consider(gv);
-  }
-  if (allow_mat) {
-    consider({Al[0], Al[1]});
-    consider({Bl[0], Bl[1]});
-  }
-  // options by cost (instructions per thread), matrix instructions first on
-  // ties (the paper's preference for hardware primitives); an option
-  // whose layouts turn out not divisible by the matrix tile under the
-  // constructed S is dropped for the next one
-  std::stable_sort(opts.begin(), opts.end(), [](const Opt& x, const Opt& y) {
-    if (x.cost != y.cost) return x.cost < y.cost;
-    return x.wr_mat + x.rd_mat > y.wr_mat + y.rd_mat;
-  });
-  SwizzleResult sw;
-  std::vector<u64> At, Bt, V;
-  Opt best;
-  auto build = [&](const Opt& o) -> bool {
-    best = o;
-    V = WB;  // S_vect: word bits (B's order), then the granule rows
-    for (u64 x : best.gv) V.push_back(x);
-    // bank-relevant thread vectors per side (phase order): lanes for vector
-    // accesses; the address providers (rows = lanes 2..4, then the matrix
-    // select word bits) for stmatrix / ldmatrix
-    auto thr_vecs = [&](int mat, const std::vector<u64>& W, const std::vector<u64>& L, int a, int b) {
-      std::vector<u64> t;
-      if (!mat) return L;
-      t = {L[2], L[3], L[4]};
-      if (a >= 0) t.push_back(W[a]);
-      if (b >= 0) t.push_back(W[b]);
-      while (t.size() < 5) t.push_back(L[2]);  // padding (dropped by the phase rule)
-      return t;
-    };
-    At = thr_vecs(best.wr_mat, Aw, Al, best.wa, best.wb);
-    Bt = thr_vecs(best.rd_mat, Bw, Bl, best.ra, best.rb);
-    sw = optimal_swizzle(At, Bt, V, d, w);
-    std::vector<u64> Scols = sw.vect;
-    Scols.insert(Scols.end(), sw.bank.begin(), sw.bank.end());
-    Scols.insert(Scols.end(), sw.idx.begin(), sw.idx.end());
-    if (f2_rank(Scols) != d) return false;
-    auto Sinv = f2_right_inverse(Scols, d);
-    if (d + lw > 31) return false;
-    auto boff = [&](u64 v) -> uint32_t { return (uint32_t)f2_apply(Sinv, v) << lw; };
-    // tile matching by left division of S^{-1} o L by the matrix tile: the
-    // word bits and lanes 0, 1 must be offset bits 0..k+1 and no other column
-    // may touch them
-    auto divisible = [&](const std::vector<u64>& W0, const std::vector<u64>& L,
-                         const std::vector<u64>& rest) {
-      const u64 low = (u64(1) << (kw + 2)) - 1;
-      for (int t = 0; t < kw; ++t)
-        if (f2_apply(Sinv, W0[t]) != e(t)) return false;
-      if (f2_apply(Sinv, L[0]) != e(kw) || f2_apply(Sinv, L[1]) != e(kw + 1)) return false;
-      for (u64 c : rest)
-        if (f2_apply(Sinv, c) & low) return false;
-      return true;
-    };
-    auto rest_of = [&](const std::vector<u64>& W, const std::vector<u64>& L, const std::vector<u64>& Wp) {
-      std::vector<u64> r(W);
-      r.insert(r.end(), L.begin() + 2, L.end());
-      r.insert(r.end(), Wp.begin(), Wp.end());
-      return r;
-    };
-    if (best.wr_mat && !divisible(WB, Al, rest_of(Aw, Al, Awp))) return false;
-    if (best.rd_mat && !divisible(WB, Bl, rest_of(Bw, Bl, Bwp))) return false;
-    RegsPlan& rp = P.rp;
-    rp = RegsPlan{};
-    rp.nw = nw;
-    rp.nwords = NW;
-    rp.tile_bytes = int64_t(w) << d;
-    rp.n_tiles = (int64_t(1) << (n - d)) * P.batch;
-    rp.wr_mat = best.wr_mat;
-    rp.rd_mat = best.rd_mat;
-    rp.wr_gw = best.wr_gw;
-    rp.rd_gw = best.rd_gw;
-    rp.n_swaps = (int)swaps.size();
-    for (size_t i = 0; i < swaps.size(); ++i) {
-      rp.swap_a[i] = (int8_t)swaps[i].first;
-      rp.swap_b[i] = (int8_t)swaps[i].second;
-    }
-    // canonical word order per side: the instruction's words at word bits 0
-    // (and 1), realised by transpositions (recorded for the kernel)
-    auto canon = [&](std::vector<u64> W, int a, int b, int gw, int& ns, int8_t* sa, int8_t* sb) {
-      ns = 0;
-      std::vector<u64> sel;
-      if (gw >= 2 && a >= 0) sel.push_back(W[a]);
-      if (gw >= 4 && b >= 0) sel.push_back(W[b]);
-      for (size_t t = 0; t < sel.size(); ++t) {
-        const int s2 = pos(W, sel[t]);
-        if (s2 != (int)t) {
-          sa[ns] = (int8_t)std::min<int>((int)t, s2);
-          sb[ns] = (int8_t)std::max<int>((int)t, s2);
-          ++ns;
-          std::swap(W[t], W[s2]);
-        }
-      }
-      return W;
-    };
-    const std::vector<u64> Awc = canon(Aw, best.wa, best.wb, best.wr_gw, rp.n_wsw, rp.wsw_a, rp.wsw_b);
-    const std::vector<u64> Bwc = canon(Bw, best.ra, best.rb, best.rd_gw, rp.n_rsw, rp.rsw_a, rp.rsw_b);
-    auto fill = [&](int mat, const std::vector<u64>& W, const std::vector<u64>& L,
-                    const std::vector<u64>& Wp, int a, int b, int gw, uint32_t* thr, uint32_t* inst) {
-      if (mat) {
-        // address provider lane p: rows = p bits 0..2 (the data lanes 2..4),
-        // matrix = p bits 3, 4 (the selected word bits)
-        thr[0] = boff(L[2]);
-        thr[1] = boff(L[3]);
-        thr[2] = boff(L[4]);
-        thr[3] = a >= 0 && gw >= 2 ? boff(W[a]) : 0;
-        thr[4] = b >= 0 && gw >= 4 ? boff(W[b]) : 0;
-      } else {
-        for (int q = 0; q < 5; ++q) thr[q] = boff(L[q]);
-      }
-      for (int q = 0; q < nw; ++q) thr[5 + q] = boff(Wp[q]);
-      // instruction j: the word bits other than the selected ones, ascending
-      const int ninst = NW / gw;
-      if (ninst > LL_REGS_MAX_INST) return false;
-      std::vector<int> other;
-      for (int u = 0; u < LB; ++u)
-        if (!(u == a && gw >= 2) && !(u == b && gw >= 4)) other.push_back(u);
-      for (int j = 0; j < ninst; ++j) {
-        uint32_t o = 0;
-        for (size_t q = 0; q < other.size(); ++q)
-          if ((j >> q) & 1) o ^= boff(W[other[q]]);
-        inst[j] = o;
-      }
-      return true;
-    };
-    if (!fill(rp.wr_mat, Awc, Al, Awp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.wr_gw, rp.sw_thr, rp.sw_inst))
-      return false;
-    if (!fill(rp.rd_mat, Bwc, Bl, Bwp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.rd_gw, rp.sr_thr, rp.sr_inst))
-      return false;
-    P.nv = NW;
-    P.tile_bits = d;
-    P.pred_wf_ld = lemma_wavefronts(sw, At, w);
-    P.pred_wf_st = lemma_wavefronts(sw, Bt, w);
-    return true;
-  };
-  bool ok = false;
-  for (auto& o : opts)
-    if ((ok = build(o))) break;
-  if (!ok) return false;
-  RegsPlan& rp = P.rp;
-  static const char* kinds[] = {"st.shared", "stmatrix", "ld.shared", "ldmatrix"};
-  js << ",\"regs\":{\"warps_log2\":" << nw << ",\"words_per_thread\":" << NW
-     << ",\"write\":\"" << kinds[rp.wr_mat] << "\",\"write_words\":" << rp.wr_gw
-     << ",\"read\":\"" << kinds[2 + rp.rd_mat] << "\",\"read_words\":" << rp.rd_gw
-     << ",\"write_instr_per_thread\":" << NW / rp.wr_gw
-     << ",\"read_instr_per_thread\":" << NW / rp.rd_gw << ",\"n_tiles\":" << rp.n_tiles
-     << ",\"swaps\":" << swaps.size() << ",\"sw_thr\":" << u32_json(rp.sw_thr, 5 + nw)
-     << ",\"sr_thr\":" << u32_json(rp.sr_thr, 5 + nw)
-     << ",\"sw_inst\":" << u32_json(rp.sw_inst, NW / rp.wr_gw)
-     << ",\"sr_inst\":" << u32_json(rp.sr_inst, NW / rp.rd_gw) << "},\"S_vect\":" << vec_json(sw.vect)
-     << ",\"S_bank\":" << vec_json(sw.bank) << ",\"S_idx\":" << vec_json(sw.idx)
-     << ",\"granule_bytes\":" << ((w << (int)V.size()))
-     << ",\"pred_wavefronts_per_sts\":" << P.pred_wf_ld
-     << ",\"pred_wavefronts_per_lds\":" << P.pred_wf_st;
-  return true;
-}
-
-// Register-faithful warp-shuffle plan (LL_PATH_REGS_SHUFFLE): warp-local
-// pairs only ((B^{-1} o A)_warp = I): both directions of the paper's
-// exchange on the layouts' own registers and lanes.
-bool plan_regs_shuffle(ConvertPlan& P, const Layout& A, const Layout& B,
-                       const std::vector<u64>& X, std::ostringstream& js) {
-  RegsFrame f;
-  if (!regs_frame(P, A, B, X, f)) return false;
-  if (f.NW > LL_MAX_GRAN) return false;
-  for (int b = 0; b < f.nw; ++b)
-    if (f.Bwp[b] != f.Awp[b]) return false;
-  const u64 wmask = (u64(1) << (f.nr + 5)) - 1;  // (reg, lane) space of one warp
-  for (u64 v : f.Bw) if (v & ~wmask) return false;
-  for (u64 v : f.Bl) if (v & ~wmask) return false;
-  ShuffleCore fw = shuffle_core(f.Aw, f.Al, f.Bw, f.Bl, f.LB);
-  ShuffleCore bw = shuffle_core(f.Bw, f.Bl, f.Aw, f.Al, f.LB);
-  if (!fw.ok || !bw.ok) return false;
-  RegsShufflePlan& q = P.rsp;
-  q = RegsShufflePlan{};
-  q.nw = f.nw;
-  q.nwords = f.NW;
-  q.tile_bytes = int64_t(f.w) << f.d;
-  q.n_tiles = (int64_t(1) << (f.n - f.d)) * P.batch;
-  q.swaps = f.swaps;
-  auto fill = [&](const ShuffleCore& c, ShuffleDir& dd) {
-    for (int k = 0; k < c.rounds; ++k) {
-      int a = 0, e = 0;
-      for (int j = 0; j < f.LB; ++j)
-        if ((k >> j) & 1) { a ^= (int)c.alpha[j]; e ^= (int)c.epsm[j]; }
-      dd.alpha.push_back(a);
-      dd.eps.push_back(e);
-      dd.gamma.push_back(c.gamma[k]);
-    }
-    for (int b = 0; b < 5; ++b) { dd.beta[b] = c.beta[b]; dd.zeta[b] = c.zeta[b]; dd.delta[b] = c.delta[b]; }
-    dd.beta_any = c.beta_any;
-    dd.zeta_any = c.zeta_any;
-  };
-  fill(fw, q.fwd);
-  fill(bw, q.bwd);
-  P.nv = f.NW;
-  P.tile_bits = f.d;
-  // a register permutation (identical lanes) costs no shuffle round
-  P.shuffle_rounds = f.Al == f.Bl ? 0 : fw.rounds;
-  js << ",\"regs_shuffle\":{\"warps_log2\":" << f.nw << ",\"words_per_thread\":" << f.NW
-     << ",\"rounds\":" << fw.rounds << ",\"I\":" << vec_json(fw.I) << ",\"E\":" << vec_json(fw.E)
-     << ",\"F\":" << vec_json(fw.F) << ",\"G\":" << vec_json(fw.Gv) << ",\"R\":" << vec_json(fw.R)
-     << ",\"beta_lane\":" << u32_json(q.fwd.beta, 5) << ",\"zeta_lane\":" << u32_json(q.fwd.zeta, 5)
-     << ",\"delta_lane\":" << u32_json(q.fwd.delta, 5) << ",\"swaps\":" << f.swaps.size()
-     << ",\"exchange\":\"" << (f.Al == f.Bl ? "register permutation" : "warp shuffles") << "\""
-     << ",\"n_tiles\":" << q.n_tiles << "}";
   return true;
 }
 
