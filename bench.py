@@ -464,10 +464,11 @@ def main():
                 cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "oracle",
                        "sample": "failed: %s" % ex}
         kernel = {"smem": "convert_smem_kernel", "generic": "convert_generic_kernel",
+                  "shuffle": "gather_shuffle_kernel" if cfg == "4" else "ll_shfl_hbm (NVRTC)",
                   "smem_noswizzle": "convert_smem_kernel", "smem_padded": "convert_smem_kernel",
                   "smem_async": "convert_async_kernel", "smem_tma": "convert_tma_kernel",
                   "regs": "convert_regs_kernel", "smem_tma_store": "convert_tma_store_kernel",
-                  "copy": "cudaMemcpyAsync", "shuffle": "gather_shuffle_kernel",
+                  "copy": "cudaMemcpyAsync",
                   "direct": "gather_direct_kernel"}.get(plan.get("path"), plan.get("path"))
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
@@ -486,7 +487,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic(cfg + ("_upcast" if args.upcast else "") +
-                                                {"smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas"}.get(
+                                                {"smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas",
+                                                 "shuffle": "" if cfg == "4" else "_shfl"}.get(
                                                     plan.get("path"), "")),
                          "peak_source": peak_src, "kernel": kernel,
                          "avg_launch_us": avg_launch_ms * 1000,

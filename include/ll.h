@@ -171,10 +171,14 @@ ll_status ll_gather(const void* src, const int32_t* idx, void* out, ll_layout la
 /* ------------------------------------------------------ extended control -- */
 
 typedef enum {
-  LL_PATH_AUTO = 0,      /* planner's choice (cost model)                          */
+  LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, SHUFFLE
+                            (plan-specialised kernel) when the planner's warp tile makes the
+                            exchange warp-local, else SMEM, else GENERIC               */
   LL_PATH_COPY = 1,      /* identity quotient: plain copy                          */
   LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle    */
-  LL_PATH_SHUFFLE = 3,   /* warp-local exchange with warp shuffles                 */
+  LL_PATH_SHUFFLE = 3,   /* warp-local exchange with warp shuffles; by default in a kernel
+                            specialised for the plan at run time (NVRTC; knob shuffle_jit=0:
+                            the generic kernel)                                      */
   LL_PATH_GENERIC = 4,   /* element-wise pull (any layouts; the slow baseline)     */
   LL_PATH_SMEM_NOSWIZZLE = 5, /* smem path with an unswizzled staging buffer (ablation) */
   LL_PATH_SMEM_ASYNC = 6, /* smem path fed by cp.async (source granules, multi-stage)  */
@@ -252,9 +256,10 @@ ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst
                                 ll_layout dst_layout, int elem_bits, int64_t batch, int reps,
                                 long long* cycles, ll_stream stream);
 
-/* The CUDA source of the run-time specialised LL_PATH_REGS_SHUFFLE kernel for
- * (src_layout, dst_layout) into buf (cap bytes, NUL-terminated; *need = the
- * size needed); compile != 0 instead compiles it with NVRTC for sm_100a (no
+/* The CUDA source of a run-time specialised kernel for (src_layout,
+ * dst_layout) into buf (cap bytes, NUL-terminated; *need = the size needed):
+ * the LL_PATH_REGS_SHUFFLE kernel, or with (compile & 2) the LL_PATH_SHUFFLE
+ * HBM kernel.  (compile & 1) instead compiles it with NVRTC for sm_100a (no
  * device needed) and returns {"compiled": true, "cubin_bytes": n}.
  * LL_ERR_UNSUPPORTED if the pair has no such plan or NVRTC fails. */
 ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int compile,

@@ -319,14 +319,16 @@ def convert_regs_timed(src, A, dst, B, elem_bits, reps=1, cycles=None, batch=1, 
                                           _stream_handle(stream)))
 
 
-def jit_source(A, B, elem_bits, compile=False):
-    """ll_jit_source: the NVRTC-specialised regs_shuffle kernel source (or,
-    with compile=True, the compile result as a dict)."""
+def jit_source(A, B, elem_bits, compile=False, kernel="regs_shuffle"):
+    """ll_jit_source: the NVRTC-specialised kernel source (kernel
+    "regs_shuffle" or "shuffle" = the HBM shuffle conversion), or with
+    compile=True the NVRTC compile result as a dict."""
+    mode = (1 if compile else 0) | (2 if kernel == "shuffle" else 0)
     need = ctypes.c_size_t()
-    _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), int(compile), None, 0,
+    _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), mode, None, 0,
                               ctypes.byref(need)))
     buf = ctypes.create_string_buffer(need.value)
-    _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), int(compile), buf, need.value,
+    _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), mode, buf, need.value,
                               ctypes.byref(need)))
     out = buf.value.decode()
     return json.loads(out) if compile else out

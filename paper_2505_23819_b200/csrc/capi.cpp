@@ -410,6 +410,19 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
     }
     case LL_PATH_SHUFFLE:
       ++g_launches;
+      if (ll::planner_knob("shuffle_jit", 1) && w <= 4) {
+        // the plan compiled into its own kernel (NVRTC, constant register indices)
+        std::string err;
+        cudaError_t e = ll::launch_shuffle_jit(*P, src, dst, max_ctas, st, rg, &err);
+        // NVRTC / module problems (nothing was launched): the generic shuffle kernel
+        if (e != cudaSuccess && !err.empty() && err.rfind("cuLaunchKernel", 0) != 0) {
+          cudaGetLastError();
+          return cuda_status(ll::launch_convert_shuffle(P->shp, w, P->nv, src, dst, max_ctas, st, rg),
+                             "ll_convert (shuffle kernel)");
+        }
+        if (e != cudaSuccess && !err.empty()) return fail(LL_ERR_CUDA, "ll_convert (shuffle): " + err);
+        return cuda_status(e, "ll_convert (specialised shuffle kernel)");
+      }
       return cuda_status(ll::launch_convert_shuffle(P->shp, w, P->nv, src, dst, max_ctas, st, rg),
                          "ll_convert (shuffle kernel)");
     case LL_PATH_SMEM_ASYNC:
@@ -492,12 +505,18 @@ ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bit
     check_layout(src_layout, "ll_jit_source");
     check_layout(dst_layout, "ll_jit_source");
     const int w = elem_bytes(elem_bits);
-    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_REGS_SHUFFLE, 1);
-    std::string out = ll::regs_shuffle_kernel_source(P->rsp, w);
-    if (compile) {
+    std::string out;
+    if (compile & 2) {  // the HBM shuffle conversion kernel (LL_PATH_SHUFFLE)
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_SHUFFLE, 1);
+      out = ll::shuffle_hbm_kernel_source(*P);
+    } else {
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_REGS_SHUFFLE, 1);
+      out = ll::regs_shuffle_kernel_source(P->rsp, w);
+    }
+    if (compile & 1) {
       std::string log;
       size_t cubin = 0;
-      const bool ok = ll::regs_shuffle_compile_check(P->rsp, w, &log, &cubin);
+      const bool ok = ll::nvrtc_compile_check(out, &log, &cubin);
       out = std::string("{\"compiled\":") + (ok ? "true" : "false") + ",\"cubin_bytes\":" +
             std::to_string(cubin) + "}";
       if (!ok) return fail(LL_ERR_UNSUPPORTED, "ll_jit_source: NVRTC failed: " + log.substr(0, 300));

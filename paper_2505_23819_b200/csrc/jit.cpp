@@ -157,6 +157,53 @@ std::string regs_shuffle_source(const RegsShufflePlan& p, int W) {
   return o.str();
 }
 
+// HBM -> HBM warp-shuffle conversion (LL_PATH_SHUFFLE) specialised for the
+// plan: the free-mapped warp tiles of plan_smem (load / store layouts), the
+// tile offsets from the plan's tables (kernel parameter, warp-uniform), and
+// the exchange with constant register indices.
+std::string shuffle_hbm_source(const ConvertPlan& P) {
+  const ShufflePlan& p = P.shp;
+  const int W = P.w, NV = P.nv, NW = NV * 4;
+  std::ostringstream o;
+  o << "struct TileTab { long long src, dst, sc; };\n"
+    << "struct TileMap { long long n_tiles; int n_bits; int n_tab; long long bss, bsd; TileTab tab["
+    << LL_MAX_TAB << "][" << (1 << LL_TAB_BITS) << "]; };\n"
+    << "extern \"C\" __global__ void __launch_bounds__(256) ll_shfl_hbm(\n"
+    << "    const __grid_constant__ TileMap tm, const unsigned char* __restrict__ src,\n"
+    << "    unsigned char* __restrict__ dst, long long n_groups, long long t0, long long t1,\n"
+    << "    long long src_shift, long long dst_shift) {\n"
+    << "  const int lane = threadIdx.x & 31;\n"
+    << "  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;\n"
+    << "  if (gid >= n_groups) return;\n"
+    << "  unsigned ld_off = 0, st_off = 0, fb = 0, fz = 0, fd = 0;\n";
+  for (int c = 0; c < 5; ++c)
+    o << "  if (lane & " << (1 << c) << ") { ld_off += " << p.ld_thr[c] << "u; st_off += " << p.st_thr[c]
+      << "u; fb ^= " << P.shd.beta[c] << "u; fz ^= " << P.shd.zeta[c] << "u; fd ^= " << P.shd.delta[c]
+      << "u; }\n";
+  o << "  const unsigned char* sthr = src + ld_off - src_shift;\n"
+    << "  unsigned char* dthr = dst + st_off - dst_shift;\n"
+    << "  const long long rmask = (1LL << tm.n_bits) - 1;\n"
+    << "  for (long long t = t0 + gid; t < t1; t += n_groups) {\n"
+    << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
+    << "    long long so = inst * tm.bss, dof = inst * tm.bsd;\n";
+  for (int k = 0; k < p.tile.n_tab; ++k)
+    o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
+      << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; }\n";
+  o << "    unsigned R[" << NW << "], Q[" << NW << "];\n";
+  for (int u = 0; u < NV; ++u)
+    o << "    asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(R["
+      << 4 * u << "]), \"=r\"(R[" << 4 * u + 1 << "]), \"=r\"(R[" << 4 * u + 2 << "]), \"=r\"(R["
+      << 4 * u + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
+  for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], "R");
+  emit_dir(o, P.shd, NW, "R", "Q", "f");
+  for (int u = 0; u < NV; ++u)
+    o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dof + "
+      << p.st_vec[u] << "), \"r\"(Q[" << 4 * u << "]), \"r\"(Q[" << 4 * u + 1 << "]), \"r\"(Q["
+      << 4 * u + 2 << "]), \"r\"(Q[" << 4 * u + 3 << "]) : \"memory\");\n";
+  o << "  }\n}\n";
+  return o.str();
+}
+
 struct JitEntry {
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
@@ -164,7 +211,8 @@ struct JitEntry {
 std::mutex g_jit_mu;
 std::map<std::pair<int, std::string>, JitEntry> g_jit;
 
-cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err) {
+cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
+                       const char* name = "ll_regs_shfl") {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_jit_mu);
@@ -182,7 +230,7 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err)
   }
   cudaFree(nullptr);  // make sure the runtime's primary context is current
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_regs_shfl.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     *err = "nvrtcCreateProgram failed";
     return cudaErrorUnknown;
   }
@@ -204,7 +252,7 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err)
   nvrtcDestroyProgram(&prog);
   JitEntry e;
   if (load(&e.mod, cubin.data()) != CUDA_SUCCESS ||
-      getf(&e.fn, e.mod, "ll_regs_shfl") != CUDA_SUCCESS) {
+      getf(&e.fn, e.mod, name) != CUDA_SUCCESS) {
     *err = "cuModuleLoadData / cuModuleGetFunction failed";
     return cudaErrorUnknown;
   }
@@ -216,10 +264,9 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err)
 }  // namespace
 
 // Compile only (no device needed): NVRTC log / status for tests.
-bool regs_shuffle_compile_check(const RegsShufflePlan& p, int w, std::string* log, size_t* cubin_bytes) {
-  const std::string src = regs_shuffle_source(p, w);
+bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin_bytes) {
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_regs_shfl.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return false;
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device"};
   const bool ok = nvrtcCompileProgram(prog, 3, opts) == NVRTC_SUCCESS;
@@ -266,5 +313,40 @@ cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src
   }
   return cudaGetLastError();
 }
+
+cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
+                               cudaStream_t st, const TileRange& rg, std::string* err) {
+  if (!P.shuffle_ok || P.w > 4) return cudaErrorInvalidValue;
+  CUfunction fn = nullptr;
+  cudaError_t e = get_kernel(shuffle_hbm_source(P), &fn, err, "ll_shfl_hbm");
+  if (e != cudaSuccess) return e;
+  static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
+  if (!launch) return cudaErrorNotSupported;
+  const int64_t n_tiles = rg.t1 - rg.t0;
+  if (n_tiles <= 0) return cudaSuccess;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tpg = planner_knob("shuffle_jit_tpg", 1);  // sweep: 1 > 2 > 4 > 8
+  int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)sms * 64;
+  if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * 8);
+  groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
+  const int64_t grid = (groups + 7) / 8;
+  long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
+  const void* s = src;
+  void* d = dst;
+  void* args[] = {(void*)&P.shp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
+                  (void*)&ss, (void*)&ds};
+  if (launch(fn, (unsigned)grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) != CUDA_SUCCESS) {
+    *err = "cuLaunchKernel failed";
+    return cudaErrorLaunchFailure;
+  }
+  return cudaGetLastError();
+}
+
+std::string shuffle_hbm_kernel_source(const ConvertPlan& P) { return shuffle_hbm_source(P); }
 
 }  // namespace ll

@@ -149,7 +149,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "run_bytes" && name != "tile_order" && name != "host_chunk_mb" &&
       name != "host_slots" && name != "tma_run_bytes" && name != "tma_thread_bytes" &&
       name != "tma_tile_bytes" && name != "tma_force_swizzle" && name != "regs_matrix" &&
-      name != "regs_shuffle_max_rounds")
+      name != "regs_shuffle_max_rounds" && name != "shuffle_jit" && name != "shuffle_jit_tpg" &&
+      name != "auto_shuffle")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -724,6 +725,18 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
         sh.post_op[i] = (int8_t)post[i][0]; sh.post_a[i] = (int8_t)post[i][1]; sh.post_b[i] = (int8_t)post[i][2];
       }
       for (int k = 0; k < NWd; ++k) sh.gamma[k] = sc.gamma[k];
+      P.shd = ShuffleDir{};
+      for (int k = 0; k < NWd; ++k) {
+        int a = 0, e = 0;
+        for (int j = 0; j < LB; ++j)
+          if ((k >> j) & 1) { a ^= (int)alpha[j]; e ^= (int)epsm[j]; }
+        P.shd.alpha.push_back(a);
+        P.shd.eps.push_back(e);
+        P.shd.gamma.push_back(sc.gamma[k]);
+      }
+      for (int c = 0; c < 5; ++c) { P.shd.beta[c] = sc.beta[c]; P.shd.zeta[c] = sc.zeta[c]; P.shd.delta[c] = sc.delta[c]; }
+      P.shd.beta_any = sc.beta_any;
+      P.shd.zeta_any = sc.zeta_any;
       P.shuffle_ok = true;
       P.shuffle_rounds = NWd;
     }
@@ -808,12 +821,29 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
      << ",\"batch\":" << batch << ",\"X\":" << vec_json(X) << ",\"identity\":"
      << (ident ? "true" : "false");
   int path = path_req;
-  if (path == LL_PATH_AUTO) path = ident ? LL_PATH_COPY : LL_PATH_SMEM;
+  bool planned = false;
+  if (path == LL_PATH_AUTO) {
+    path = ident ? LL_PATH_COPY : LL_PATH_SMEM;
+    // cost model: a warp-local exchange runs as the paper's warp shuffles in a
+    // kernel compiled for the plan (measured on B200: config 2 6601 vs 6517
+    // GB/s, config 5 6896 vs 6620 for the shared-memory path; the generic,
+    // uncompiled shuffle kernel loses, 5640 / 5542); otherwise shared memory
+    if (!ident && op == 0 && w <= 4 && planner_knob("auto_shuffle", 1) && planner_knob("shuffle_jit", 1)) {
+      auto trial = std::make_shared<ConvertPlan>(*P);
+      std::ostringstream js2;
+      if (plan_smem(*trial, X, true, js2, true) && trial->shuffle_ok) {
+        *P = *trial;
+        js << js2.str();
+        path = LL_PATH_SHUFFLE;
+        planned = true;
+      }
+    }
+  }
   if (path == LL_PATH_COPY && !ident)
     throw Error(LL_ERR_UNSUPPORTED, "copy path requested but the quotient is not the identity");
   if (path == LL_PATH_SMEM_PADDED) P->padded = true;
-  if (path == LL_PATH_SMEM || path == LL_PATH_SMEM_NOSWIZZLE || path == LL_PATH_SHUFFLE ||
-      path == LL_PATH_SMEM_PADDED) {
+  if (!planned && (path == LL_PATH_SMEM || path == LL_PATH_SMEM_NOSWIZZLE ||
+                   path == LL_PATH_SHUFFLE || path == LL_PATH_SMEM_PADDED)) {
     std::ostringstream js2;
     if (plan_smem(*P, X, path == LL_PATH_SMEM || path == LL_PATH_SHUFFLE, js2,
                   path == LL_PATH_SHUFFLE)) {

@@ -73,6 +73,7 @@ struct ConvertPlan {
   std::vector<int> tile_bit_src, tile_bit_dst;
   // shuffle path (warp tiles only)
   ShufflePlan shp{};
+  ShuffleDir shd;     // the same exchange per round, for the NVRTC-specialised kernel
   bool shuffle_ok = false;
   int shuffle_rounds = 0;
   // generic path
@@ -102,7 +103,10 @@ std::shared_ptr<const ConvertPlan> get_convert_plan(const Layout& A, const Layou
                                                     int path_req, int64_t batch, int op = 0);
 // jit.cpp: the NVRTC-specialised register-faithful shuffle kernel
 std::string regs_shuffle_kernel_source(const RegsShufflePlan& p, int w);
-bool regs_shuffle_compile_check(const RegsShufflePlan& p, int w, std::string* log, size_t* cubin_bytes);
+cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
+                               cudaStream_t st, const TileRange& rg, std::string* err);
+std::string shuffle_hbm_kernel_source(const ConvertPlan& P);
+bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin_bytes);
 cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src, void* dst,
                                 int max_ctas, int reps, long long* cycles, cudaStream_t st,
                                 std::string* err);

@@ -466,7 +466,7 @@ def test_convert_broadcast_layouts(w, za, zb, low):
         A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
         path = ll.plan_describe(A, B, 8 * w)["path"]
         if not low:
-            assert path == "smem", path
+            assert path in ("smem", "shuffle"), path
         src, dst = run_convert(c, seed=rng.randint(0, 999))
         assert dst.tobytes() == expect_convert(c, src).tobytes()
 

@@ -266,7 +266,7 @@ def test_broadcast_plans_stay_tiled():
         c = _bcast_pair(rng, 13, w, 1, 2)
         A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
         d = ll.plan_describe(A, B, 8 * w)
-        assert d["path"] == "smem"
+        assert d["path"] in ("smem", "shuffle")       # tiled (AUTO: shuffle if warp-local)
         X = d["X"]
         zd = [k for k, x in enumerate(X) if x == 0]
         assert len(zd) == 2 and d["tile_order_dst_bits"][:2] == zd
@@ -484,3 +484,15 @@ def test_upcast_alignment_contract():
         with pytest.raises(ll.LLError) as e:
             ll.mxfp4_upcast(packed, A, 0x30000, dst, B, stream=0)
         assert e.value.name == "LL_ERR_ARG"
+
+
+def test_shuffle_hbm_kernel_specialises_and_compiles():
+    """LL_PATH_SHUFFLE runs the plan compiled into its own kernel: the source
+    has one __shfl_sync per round with constant register indices, and NVRTC
+    compiles it for sm_100a (configs 2 and 5)."""
+    for c in (configs.cfg2(batch_bits=2), configs.cfg5(m_bits=8, kb_bits=8)):
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        d = ll.plan_describe(A, B, 8 * c["elem_bytes"], "shuffle")
+        src = ll.jit_source(A, B, 8 * c["elem_bytes"], kernel="shuffle")
+        assert src.count("__shfl_sync") == d["shuffle"]["rounds"]
+        assert ll.jit_source(A, B, 8 * c["elem_bytes"], compile=True, kernel="shuffle")["compiled"]
