@@ -463,7 +463,9 @@ def main():
             except Exception as ex:  # the baseline must never break the line
                 cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "oracle",
                        "sample": "failed: %s" % ex}
-        kernel = {"smem": "convert_smem_kernel", "generic": "convert_generic_kernel",
+        generic_smem = args.upcast or "smem_jit=0" in args.tune
+        kernel = {"smem": "convert_smem_kernel" if generic_smem else "ll_smem_hbm (NVRTC)",
+                  "generic": "convert_generic_kernel",
                   "shuffle": "gather_shuffle_kernel" if cfg == "4" else "ll_shfl_hbm (NVRTC)",
                   "smem_noswizzle": "convert_smem_kernel", "smem_padded": "convert_smem_kernel",
                   "smem_async": "convert_async_kernel", "smem_tma": "convert_tma_kernel",
@@ -487,7 +489,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic(cfg + ("_upcast" if args.upcast else "") +
-                                                {"smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas",
+                                                {"smem": "" if (args.upcast or "smem_jit=0" in args.tune) else "_jit", "smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas",
                                                  "shuffle": "" if cfg == "4" else "_shfl"}.get(
                                                     plan.get("path"), "")),
                          "peak_source": peak_src, "kernel": kernel,

@@ -171,11 +171,13 @@ ll_status ll_gather(const void* src, const int32_t* idx, void* out, ll_layout la
 /* ------------------------------------------------------ extended control -- */
 
 typedef enum {
-  LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, SHUFFLE
-                            (plan-specialised kernel) when the planner's warp tile makes the
-                            exchange warp-local, else SMEM, else GENERIC               */
+  LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, else SMEM
+                            (measured fastest once compiled per plan), else GENERIC     */
   LL_PATH_COPY = 1,      /* identity quotient: plain copy                          */
-  LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle    */
+  LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle; by default
+                            in a kernel specialised for the plan at run time (NVRTC, every
+                            offset and register index a constant; knob smem_jit=0: the
+                            generic kernel, which also serves the fused upcast)        */
   LL_PATH_SHUFFLE = 3,   /* warp-local exchange with warp shuffles; by default in a kernel
                             specialised for the plan at run time (NVRTC; knob shuffle_jit=0:
                             the generic kernel)                                      */

@@ -452,6 +452,16 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
       return cuda_status(ll::launch_convert_tma(P->sp, P->td, w, P->nv, src, dst, max_ctas, st, rg),
                          "ll_convert (TMA smem kernel)");
     case LL_PATH_SMEM:
+      if (ll::planner_knob("smem_jit", 1) && !P->sp.pad) {
+        ++g_launches;
+        std::string err;
+        cudaError_t e = ll::launch_smem_jit(*P, src, dst, max_ctas, st, rg, &err);
+        if (e == cudaSuccess || err.rfind("cuLaunchKernel", 0) == 0)
+          return cuda_status(e, "ll_convert (specialised smem kernel)");
+        cudaGetLastError();  // compile problem: the generic smem kernel below
+        --g_launches;
+      }
+      [[fallthrough]];
     case LL_PATH_SMEM_NOSWIZZLE:
     case LL_PATH_SMEM_PADDED:
       ++g_launches;
@@ -506,7 +516,10 @@ ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bit
     check_layout(dst_layout, "ll_jit_source");
     const int w = elem_bytes(elem_bits);
     std::string out;
-    if (compile & 2) {  // the HBM shuffle conversion kernel (LL_PATH_SHUFFLE)
+    if (compile & 4) {  // the HBM shared-memory conversion kernel (LL_PATH_SMEM)
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_SMEM, 1);
+      out = ll::smem_hbm_kernel_source(*P);
+    } else if (compile & 2) {  // the HBM shuffle conversion kernel (LL_PATH_SHUFFLE)
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_SHUFFLE, 1);
       out = ll::shuffle_hbm_kernel_source(*P);
     } else {

@@ -25,8 +25,15 @@ namespace ll {
 
 namespace {
 
+int ilog2i(int x) {
+  int r = 0;
+  while ((1 << (r + 1)) <= x) ++r;
+  return r;
+}
+
 typedef CUresult (*PFN_LoadData)(CUmodule*, const void*);
 typedef CUresult (*PFN_GetFunction)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
 typedef CUresult (*PFN_Launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                                unsigned, unsigned, CUstream, void**, void**);
 
@@ -60,7 +67,9 @@ void emit_swap(std::ostringstream& o, int W, int NW, int a, int b, const char* R
           << "] = __byte_perm(x_, y_, " << hi << "u); }\n";
       }
   };
-  if (W == 4) {
+  if (W == 8) {
+    word_swap(a + 1, b + 1);
+  } else if (W == 4) {
     word_swap(a, b);
   } else if (W == 2) {
     if (a == 0) sub_swap(b - 1, 0x5410u, 0x7632u);
@@ -201,6 +210,98 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
       << p.st_vec[u] << "), \"r\"(Q[" << 4 * u << "]), \"r\"(Q[" << 4 * u + 1 << "]), \"r\"(Q["
       << 4 * u + 2 << "]), \"r\"(Q[" << 4 * u + 3 << "]) : \"memory\");\n";
   o << "  }\n}\n";
+  return o.str();
+}
+
+int deposit_word_h(int j, int k, int LB, int A, int B) {
+  int idx = 0, q = 0;
+  for (int bit = 0; bit < LB; ++bit) {
+    if (bit == A) idx |= (k & 1) << bit;
+    else if (bit == B) idx |= ((k >> 1) & 1) << bit;
+    else { idx |= ((j >> q) & 1) << bit; ++q; }
+  }
+  return idx;
+}
+
+// HBM -> HBM shared-memory conversion (LL_PATH_SMEM) specialised for the
+// plan: the same schedule as convert_smem_kernel (software-pipelined loads,
+// swizzled STS, group barrier, LDS, streaming stores), with every offset,
+// granule operand and register permutation a compile-time constant.
+std::string smem_hbm_source(const ConvertPlan& P) {
+  const SmemPlan& p = P.sp;
+  const int W = P.w, NV = P.nv, NW = NV * 4, G = P.g, GWd = G / 4, NG = NV * 16 / G;
+  const int gw = p.gw, LB = ilog2i(NW);
+  const int minb = G < 8 ? 1 : (NV >= 8 ? 3 : 4);
+  std::ostringstream o;
+  o << "struct TileTab { long long src, dst, sc; };\n"
+    << "struct TileMap { long long n_tiles; int n_bits; int n_tab; long long bss, bsd; TileTab tab["
+    << LL_MAX_TAB << "][" << (1 << LL_TAB_BITS) << "]; };\n"
+    << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") ll_smem_hbm(\n"
+    << "    const __grid_constant__ TileMap tm, const unsigned char* __restrict__ src,\n"
+    << "    unsigned char* __restrict__ dst, long long n_groups, long long t0, long long t1,\n"
+    << "    long long src_shift, long long dst_shift) {\n"
+    << "  extern __shared__ __align__(16) unsigned char smem[];\n"
+    << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+    << "  const int group = warp >> " << gw << ";\n"
+    << "  const int tb = lane | ((warp & " << ((1 << gw) - 1) << ") << 5);\n"
+    << "  const long long gid = (long long)blockIdx.x * " << (8 >> gw) << " + group;\n"
+    << "  if (gid >= n_groups) return;\n"
+    << "  unsigned ld_off = 0, st_off = 0, swx = 0, srx = 0;\n";
+  for (int b = 0; b < 5 + gw; ++b)
+    o << "  if (tb & " << (1 << b) << ") { ld_off += " << p.ld_thr[b] << "u; st_off += " << p.st_thr[b]
+      << "u; swx ^= " << p.sw_thr[b] << "u; srx ^= " << p.sr_thr[b] << "u; }\n";
+  o << "  const unsigned char* sthr = src + ld_off - src_shift;\n"
+    << "  unsigned char* dthr = dst + st_off - dst_shift;\n"
+    << "  const long long rmask = (1LL << tm.n_bits) - 1;\n"
+    << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + group * "
+    << 2 * p.tile_bytes << "u;\n"
+    << "  unsigned buf = 0;\n  unsigned R[" << NW << "], Q[" << NW << "];\n"
+    << "  long long so = 0, dof = 0;\n"
+    << "  auto tile_off = [&](long long t) {\n"
+    << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
+    << "    so = inst * tm.bss; dof = inst * tm.bsd;\n";
+  for (int k = 0; k < p.tile.n_tab; ++k)
+    o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
+      << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; }\n";
+  o << "  };\n";
+  auto load = [&](const char* ind) {
+    for (int u = 0; u < NV; ++u)
+      o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(R["
+        << 4 * u << "]), \"=r\"(R[" << 4 * u + 1 << "]), \"=r\"(R[" << 4 * u + 2 << "]), \"=r\"(R["
+        << 4 * u + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
+  };
+  o << "  long long t = t0 + gid;\n  if (t < t1) { tile_off(t);\n";
+  load("    ");
+  o << "  }\n  for (; t < t1; t += n_groups) {\n    const long long dcur = dof;\n";
+  for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], "R");
+  const int ga = GWd >= 2 ? p.gsel_a : -1, gb = GWd >= 4 ? p.gsel_b : -1;
+  for (int j = 0; j < NG; ++j) {
+    o << "    asm volatile(\"st.shared.";
+    if (GWd == 4) o << "v4.b32 [%0], {%1,%2,%3,%4};\"";
+    else if (GWd == 2) o << "v2.b32 [%0], {%1,%2};\"";
+    else o << "b32 [%0], %1;\"";
+    o << " :: \"r\"(sbase + buf + (swx ^ " << p.sw_gran[j] << "u))";
+    for (int k = 0; k < GWd; ++k) o << ", \"r\"(R[" << deposit_word_h(j, k, LB, ga, gb) << "])";
+    o << " : \"memory\");\n";
+  }
+  o << "    { const long long tn = t + n_groups; if (tn < t1) { tile_off(tn);\n";
+  load("      ");
+  o << "    } }\n";
+  if (gw == 0) o << "    __syncwarp();\n";
+  else o << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(group + 1), \"r\"(" << (32 << gw) << ") : \"memory\");\n";
+  for (int j = 0; j < NG; ++j) {
+    o << "    asm volatile(\"ld.shared.";
+    if (GWd == 4) o << "v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q[" << 4 * j + 1
+                    << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "])";
+    else if (GWd == 2) o << "v2.b32 {%0,%1}, [%2];\" : \"=r\"(Q[" << 2 * j << "]), \"=r\"(Q[" << 2 * j + 1 << "])";
+    else o << "b32 %0, [%1];\" : \"=r\"(Q[" << j << "])";
+    o << " : \"r\"(sbase + buf + (srx ^ " << p.sr_gran[j] << "u)) : \"memory\");\n";
+  }
+  for (int u = 0; u < NV; ++u)
+    o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dcur + "
+      << p.st_vec[u] << "), \"r\"(Q[" << 4 * u << "]), \"r\"(Q[" << 4 * u + 1 << "]), \"r\"(Q["
+      << 4 * u + 2 << "]), \"r\"(Q[" << 4 * u + 3 << "]) : \"memory\");\n";
+  o << "    buf ^= " << p.tile_bytes << "u;\n  }\n}\n";
   return o.str();
 }
 
@@ -348,5 +449,44 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
 }
 
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P) { return shuffle_hbm_source(P); }
+std::string smem_hbm_kernel_source(const ConvertPlan& P) { return smem_hbm_source(P); }
+
+cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
+                            cudaStream_t st, const TileRange& rg, std::string* err) {
+  if (P.sp.pad || P.op != 0) return cudaErrorInvalidValue;
+  CUfunction fn = nullptr;
+  cudaError_t e = get_kernel(smem_hbm_source(P), &fn, err, "ll_smem_hbm");
+  if (e != cudaSuccess) return e;
+  static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
+  static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
+  if (!launch || !setattr) return cudaErrorNotSupported;
+  const int64_t n_tiles = rg.t1 - rg.t0;
+  if (n_tiles <= 0) return cudaSuccess;
+  const int gpc = 8 >> P.sp.gw;
+  const int smem = gpc * 2 * P.sp.tile_bytes;
+  if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
+  const int tpg = planner_knob("smem_jit_tpg", 1);  // sweep: 1 > 2 > 4
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)sms * 4 * gpc;
+  if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
+  groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
+  const int64_t grid = (groups + gpc - 1) / gpc;
+  long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
+  const void* s = src;
+  void* d = dst;
+  void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
+                  (void*)&ss, (void*)&ds};
+  if (launch(fn, (unsigned)grid, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    *err = "cuLaunchKernel failed";
+    return cudaErrorLaunchFailure;
+  }
+  return cudaGetLastError();
+}
 
 }  // namespace ll

@@ -150,7 +150,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "host_slots" && name != "tma_run_bytes" && name != "tma_thread_bytes" &&
       name != "tma_tile_bytes" && name != "tma_force_swizzle" && name != "regs_matrix" &&
       name != "regs_shuffle_max_rounds" && name != "shuffle_jit" && name != "shuffle_jit_tpg" &&
-      name != "auto_shuffle")
+      name != "auto_shuffle" && name != "smem_jit" && name != "smem_jit_tpg")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -824,11 +824,12 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
   bool planned = false;
   if (path == LL_PATH_AUTO) {
     path = ident ? LL_PATH_COPY : LL_PATH_SMEM;
-    // cost model: a warp-local exchange runs as the paper's warp shuffles in a
-    // kernel compiled for the plan (measured on B200: config 2 6601 vs 6517
-    // GB/s, config 5 6896 vs 6620 for the shared-memory path; the generic,
-    // uncompiled shuffle kernel loses, 5640 / 5542); otherwise shared memory
-    if (!ident && op == 0 && w <= 4 && planner_knob("auto_shuffle", 1) && planner_knob("shuffle_jit", 1)) {
+    // cost model (measured on B200, profiles/r01/shuffle_jit, smem_jit): with
+    // both exchanges compiled for the plan, the swizzled shared-memory path
+    // (config 2 6703 GB/s, config 5 6993) edges out the paper's warp shuffles
+    // (6601 / 6900), so AUTO takes shared memory; auto_shuffle=1 prefers
+    // shuffles whenever the planner's warp tile makes the exchange warp-local
+    if (!ident && op == 0 && w <= 4 && planner_knob("auto_shuffle", 0) && planner_knob("shuffle_jit", 1)) {
       auto trial = std::make_shared<ConvertPlan>(*P);
       std::ostringstream js2;
       if (plan_smem(*trial, X, true, js2, true) && trial->shuffle_ok) {

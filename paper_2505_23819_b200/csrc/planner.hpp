@@ -106,6 +106,9 @@ std::string regs_shuffle_kernel_source(const RegsShufflePlan& p, int w);
 cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
                                cudaStream_t st, const TileRange& rg, std::string* err);
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P);
+std::string smem_hbm_kernel_source(const ConvertPlan& P);
+cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
+                            cudaStream_t st, const TileRange& rg, std::string* err);
 bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin_bytes);
 cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src, void* dst,
                                 int max_ctas, int reps, long long* cycles, cudaStream_t st,

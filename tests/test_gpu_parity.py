@@ -849,3 +849,24 @@ def test_convert_regs_full_size_sampled(name, mk, path):
     h = np.concatenate([rng.integers(0, n, 100000), np.arange(4096), np.arange(n - 4096, n)])
     exp = sampled_expected(c, _np(src, 2), h.astype(np.int64))
     assert (_np(dst, 2)[h] == exp).all()
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_smem_generic_kernel(w):
+    """The generic (uncompiled) shared-memory kernel (knob smem_jit=0; the
+    default compiles the plan, covered by every other smem test): configs and
+    random pairs byte-exact against the oracle."""
+    rng = random.Random(1200 + w)
+    ll.tune("smem_jit", 0)
+    try:
+        cases = [rand_pair(rng, rng.randint(12, 16), w) for _ in range(8)]
+        if w == 2:
+            cases += [configs.cfg2(batch_bits=2), configs.cfg3(n_bits=9)]
+        if w == 1:
+            cases += [configs.cfg5(m_bits=9, kb_bits=8)]
+        for c in cases:
+            batch = rng.choice([1, 3])
+            src, dst = run_convert(c, path="smem", seed=rng.randint(0, 999), batch=batch)
+            assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
+    finally:
+        ll.tune("smem_jit", 1)
