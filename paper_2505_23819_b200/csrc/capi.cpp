@@ -6,6 +6,8 @@
 
 #include <atomic>
 #include <cstdlib>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -516,7 +518,10 @@ ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bit
     check_layout(dst_layout, "ll_jit_source");
     const int w = elem_bytes(elem_bits);
     std::string out;
-    if (compile & 4) {  // the HBM shared-memory conversion kernel (LL_PATH_SMEM)
+    if (compile & 8) {  // the fused mxfp4 upcast kernel (src / dst = the config-5 byte layouts)
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, 1, LL_PATH_AUTO, 1, 1);
+      out = ll::upcast_hbm_kernel_source(*P);
+    } else if (compile & 4) {  // the HBM shared-memory conversion kernel (LL_PATH_SMEM)
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_SMEM, 1);
       out = ll::smem_hbm_kernel_source(*P);
     } else if (compile & 2) {  // the HBM shuffle conversion kernel (LL_PATH_SHUFFLE)
@@ -565,6 +570,14 @@ ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_
     auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, 1, LL_PATH_AUTO, 1, 1);
     ll::TileRange rg{0, P->sp.tile.n_tiles, 0, 0};
     ++g_launches;
+    if (ll::planner_knob("upcast_jit", 0) && P->sp.sc_nz <= 2) {
+      std::string err;
+      cudaError_t e = ll::launch_upcast_jit(*P, packed, dst_bf16, scales, opts ? opts->max_ctas : 0,
+                                            reinterpret_cast<cudaStream_t>(stream), rg, &err);
+      if (e == cudaSuccess || err.rfind("cuLaunchKernel", 0) == 0)
+        return cuda_status(e, "ll_mxfp4_upcast (specialised kernel)");
+      cudaGetLastError();  // compile problem: the template kernel below
+    }
     return cuda_status(ll::launch_mxfp4_upcast(P->sp, P->nv, P->g, packed, dst_bf16, scales,
                                                opts ? opts->max_ctas : 0,
                                                reinterpret_cast<cudaStream_t>(stream), rg),

@@ -305,9 +305,146 @@ std::string smem_hbm_source(const ConvertPlan& P) {
   return o.str();
 }
 
+// The fused mxfp4 upcast (NEXT 1) compiled per plan: the smem schedule of
+// smem_hbm_source with the tile's scales loaded with the tile, and the store
+// stage decoding each 16-byte packed vector into 64 bytes of bf16 written as
+// two 256-bit stores (same arithmetic as the template kernel's UP path).
+std::string upcast_hbm_source(const ConvertPlan& P) {
+  const SmemPlan& p = P.sp;
+  const int NV = P.nv, NW = NV * 4, G = P.g, GWd = G / 4, NG = NV * 16 / G;
+  const int gw = p.gw, LB = ilog2i(NW);
+  std::ostringstream o;
+  o << "struct TileTab { long long src, dst, sc; };\n"
+    << "struct TileMap { long long n_tiles; int n_bits; int n_tab; long long bss, bsd; TileTab tab["
+    << LL_MAX_TAB << "][" << (1 << LL_TAB_BITS) << "]; };\n"
+    << "__device__ __forceinline__ unsigned mx_scale_f32(unsigned x) {\n"
+    << "  return x == 255u ? 0x7FC00000u : (x == 0u ? 0x00400000u : (x << 23)); }\n"
+    << "__device__ __forceinline__ unsigned e2m1_f32(unsigned n) {\n"
+    << "  const unsigned e = (n >> 1) & 3u, m = n & 1u;\n"
+    << "  const unsigned b = e ? (((e + 126u) << 23) | (m << 22)) : (m ? 0x3F000000u : 0u);\n"
+    << "  return b | ((n & 8u) << 28); }\n"
+    << "__device__ __forceinline__ unsigned bf16x2_mul(unsigned a, unsigned b) {\n"
+    << "  unsigned d; asm(\"mul.rn.bf16x2 %0, %1, %2;\" : \"=r\"(d) : \"r\"(a), \"r\"(b)); return d; }\n"
+    << "extern \"C\" __global__ void __launch_bounds__(256, 2) ll_upcast_hbm(\n"
+    << "    const __grid_constant__ TileMap tm, const unsigned char* __restrict__ src,\n"
+    << "    unsigned char* __restrict__ dst, long long n_groups, long long t0, long long t1,\n"
+    << "    long long src_shift, long long dst_shift, const unsigned char* __restrict__ scales) {\n"
+    << "  extern __shared__ __align__(16) unsigned char smem[];\n"
+    << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+    << "  const int group = warp >> " << gw << ";\n"
+    << "  const int tb = lane | ((warp & " << ((1 << gw) - 1) << ") << 5);\n"
+    << "  const long long gid = (long long)blockIdx.x * " << (8 >> gw) << " + group;\n"
+    << "  if (gid >= n_groups) return;\n"
+    << "  unsigned ld_off = 0, st_off = 0, swx = 0, srx = 0, sc_off = 0;\n";
+  for (int b = 0; b < 5 + gw; ++b)
+    o << "  if (tb & " << (1 << b) << ") { ld_off += " << p.ld_thr[b] << "u; st_off += " << p.st_thr[b]
+      << "u; swx ^= " << p.sw_thr[b] << "u; srx ^= " << p.sr_thr[b] << "u; sc_off += " << p.sc_thr[b]
+      << "u; }\n";
+  o << "  const unsigned char* sthr = src + ld_off - src_shift;\n"
+    << "  const long long dbase = (long long)st_off - dst_shift;\n"
+    << "  const long long rmask = (1LL << tm.n_bits) - 1;\n"
+    << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + group * "
+    << 2 * p.tile_bytes << "u;\n"
+    << "  unsigned buf = 0;\n  unsigned R[" << NW << "], Q[" << NW << "], PK[" << NV << "], fastm = 0;\n"
+    << "  long long so = 0, dof = 0, sct = 0;\n"
+    << "  auto tile_off = [&](long long t) {\n"
+    << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
+    << "    so = inst * tm.bss; dof = inst * tm.bsd; sct = 0;\n";
+  for (int k = 0; k < p.tile.n_tab; ++k)
+    o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
+      << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; sct += e.sc; }\n";
+  o << "  };\n";
+  auto load = [&](const char* ind) {
+    for (int u = 0; u < NV; ++u)
+      o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(R["
+        << 4 * u << "]), \"=r\"(R[" << 4 * u + 1 << "]), \"=r\"(R[" << 4 * u + 2 << "]), \"=r\"(R["
+        << 4 * u + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
+    o << ind << "fastm = 0;\n";
+    for (int u = 0; u < NV; ++u) {
+      o << ind << "{ const unsigned char* scp = scales + sct + sc_off + " << p.sc_vec[u] << ";\n"
+        << ind << "  const unsigned s0 = __ldg(scp), s1 = __ldg(scp + " << p.sc_c[0] << "), s2 = __ldg(scp + "
+        << p.sc_c[1] << "), s3 = __ldg(scp + " << p.sc_c[0] + p.sc_c[1] << ");\n"
+        << ind << "  PK[" << u << "] = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);\n"
+        << ind << "  fastm |= (unsigned)((s0 - 2u < 251u) & (s1 - 2u < 251u) & (s2 - 2u < 251u) & (s3 - 2u < 251u)) << "
+        << u << "; }\n";
+    }
+  };
+  o << "  long long t = t0 + gid;\n  if (t < t1) { tile_off(t);\n";
+  load("    ");
+  o << "  }\n  for (; t < t1; t += n_groups) {\n"
+    << "    const long long dcur = dof, scur = sct + sc_off;\n"
+    << "    unsigned PKc[" << NV << "];\n";
+  for (int u = 0; u < NV; ++u) o << "    PKc[" << u << "] = PK[" << u << "];\n";
+  o << "    const unsigned fastc = fastm;\n";
+  for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, 1, NW, p.swap_a[i], p.swap_b[i], "R");
+  const int ga = GWd >= 2 ? p.gsel_a : -1, gb = GWd >= 4 ? p.gsel_b : -1;
+  for (int j = 0; j < NG; ++j) {
+    o << "    asm volatile(\"st.shared.";
+    if (GWd == 4) o << "v4.b32 [%0], {%1,%2,%3,%4};\"";
+    else if (GWd == 2) o << "v2.b32 [%0], {%1,%2};\"";
+    else o << "b32 [%0], %1;\"";
+    o << " :: \"r\"(sbase + buf + (swx ^ " << p.sw_gran[j] << "u))";
+    for (int k = 0; k < GWd; ++k) o << ", \"r\"(R[" << deposit_word_h(j, k, LB, ga, gb) << "])";
+    o << " : \"memory\");\n";
+  }
+  o << "    { const long long tn = t + n_groups; if (tn < t1) { tile_off(tn);\n";
+  load("      ");
+  o << "    } }\n";
+  if (gw == 0) o << "    __syncwarp();\n";
+  else o << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(group + 1), \"r\"(" << (32 << gw) << ") : \"memory\");\n";
+  for (int j = 0; j < NG; ++j) {
+    o << "    asm volatile(\"ld.shared.";
+    if (GWd == 4) o << "v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q[" << 4 * j + 1
+                    << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "])";
+    else if (GWd == 2) o << "v2.b32 {%0,%1}, [%2];\" : \"=r\"(Q[" << 2 * j << "]), \"=r\"(Q[" << 2 * j + 1 << "])";
+    else o << "b32 %0, [%1];\" : \"=r\"(Q[" << j << "])";
+    o << " : \"r\"(sbase + buf + (srx ^ " << p.sr_gran[j] << "u)) : \"memory\");\n";
+  }
+  // decode + two 256-bit stores per packed vector
+  for (int u = 0; u < NV; ++u) {
+    o << "    { unsigned char* op = dst + 4 * (dbase + dcur + " << p.st_vec[u] << ");\n"
+      << "      unsigned o8[16]; const unsigned pk = PKc[" << u << "];\n"
+      << "      if ((fastc >> " << u << ") & 1u) {\n"
+      << "        const unsigned plo = (pk << 7) & 0x80808080u, phi = (pk >> 1) & 0x7F7F7F7Fu;\n";
+    for (int q = 0; q < 4; ++q) {
+      o << "        { const unsigned wq = Q[" << 4 * u + q << "];\n"
+        << "          const unsigned m = wq & 0x77777777u, mh = m >> 16, x = wq & 0x88888888u;\n"
+        << "          const unsigned L01 = __byte_perm(0xC0800000u, 0xC0804000u, m), H01 = __byte_perm(0x3F3F3F00u, 0x40404040u, m);\n"
+        << "          const unsigned L23 = __byte_perm(0xC0800000u, 0xC0804000u, mh), H23 = __byte_perm(0x3F3F3F00u, 0x40404040u, mh);\n";
+      for (int k = 0; k < 4; ++k) {
+        const int e = 4 * q + k;
+        o << "          { const unsigned mag = __byte_perm(" << (k < 2 ? "L01" : "L23") << ", "
+          << (k < 2 ? "H01" : "H23") << ", " << ((k & 1) ? 0x7362 : 0x5140) << ");\n"
+          << "            const unsigned tt = __byte_perm(x, 0u, " << (0x4440 | k) << ") * 0x01001000u;\n"
+          << "            o8[" << 4 * q + k << "] = bf16x2_mul(mag | (tt & 0x80008000u), __byte_perm(plo, phi, "
+          << p.sc_sel[e] << "u)); }\n";
+      }
+      o << "        }\n";
+    }
+    o << "      } else {\n";
+    for (int e = 0; e < 16; ++e)
+      o << "        { const unsigned byte = (Q[" << 4 * u + (e >> 2) << "] >> " << (e & 3) * 8
+        << ") & 0xFFu; const unsigned sb = (pk >> " << 8 * p.sc_slot[e]
+        << ") & 0xFFu; const float sf = __uint_as_float(mx_scale_f32(sb));\n"
+        << "          const unsigned lo = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte & 15u)), sf));\n"
+        << "          const unsigned hi = __float_as_uint(__fmul_rn(__uint_as_float(e2m1_f32(byte >> 4)), sf));\n"
+        << "          o8[" << e << "] = sb == 255u ? 0x7FC07FC0u : ((hi & 0xFFFF0000u) | (lo >> 16)); }\n";
+    o << "      }\n";
+    for (int h = 0; h < 2; ++h)
+      o << "      asm volatile(\"st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\" :: \"l\"(op + "
+        << 32 * h << "), \"r\"(o8[" << 8 * h << "]), \"r\"(o8[" << 8 * h + 1 << "]), \"r\"(o8[" << 8 * h + 2
+        << "]), \"r\"(o8[" << 8 * h + 3 << "]), \"r\"(o8[" << 8 * h + 4 << "]), \"r\"(o8[" << 8 * h + 5
+        << "]), \"r\"(o8[" << 8 * h + 6 << "]), \"r\"(o8[" << 8 * h + 7 << "]) : \"memory\");\n";
+    o << "    }\n";
+  }
+  o << "    buf ^= " << p.tile_bytes << "u;\n  }\n}\n";
+  return o.str();
+}
+
 struct JitEntry {
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
+  std::string error;   // non-empty: compiling / loading failed (not retried)
 };
 std::mutex g_jit_mu;
 std::map<std::pair<int, std::string>, JitEntry> g_jit;
@@ -320,21 +457,27 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
   auto key = std::make_pair(dev, src);
   auto it = g_jit.find(key);
   if (it != g_jit.end()) {
+    if (!it->second.error.empty()) {
+      *err = it->second.error;
+      return cudaErrorUnknown;
+    }
     *fn = it->second.fn;
     return cudaSuccess;
   }
+  auto failed = [&](const std::string& m) {
+    JitEntry bad;
+    bad.error = m;
+    g_jit[key] = bad;
+    *err = m;
+    return cudaErrorUnknown;
+  };
   static PFN_LoadData load = entry<PFN_LoadData>("cuModuleLoadData");
   static PFN_GetFunction getf = entry<PFN_GetFunction>("cuModuleGetFunction");
-  if (!load || !getf) {
-    *err = "driver entry points unavailable";
-    return cudaErrorNotSupported;
-  }
+  if (!load || !getf) return failed("driver entry points unavailable");
   cudaFree(nullptr);  // make sure the runtime's primary context is current
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
-    *err = "nvrtcCreateProgram failed";
-    return cudaErrorUnknown;
-  }
+  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    return failed("nvrtcCreateProgram failed");
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device"};
   nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
   if (r != NVRTC_SUCCESS) {
@@ -343,8 +486,7 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
     std::string log(n, '\0');
     nvrtcGetProgramLog(prog, &log[0]);
     nvrtcDestroyProgram(&prog);
-    *err = "NVRTC: " + log.substr(0, 400);
-    return cudaErrorUnknown;
+    return failed("NVRTC: " + log.substr(0, 400));
   }
   size_t n = 0;
   nvrtcGetCUBINSize(prog, &n);
@@ -352,11 +494,8 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
   nvrtcGetCUBIN(prog, &cubin[0]);
   nvrtcDestroyProgram(&prog);
   JitEntry e;
-  if (load(&e.mod, cubin.data()) != CUDA_SUCCESS ||
-      getf(&e.fn, e.mod, name) != CUDA_SUCCESS) {
-    *err = "cuModuleLoadData / cuModuleGetFunction failed";
-    return cudaErrorUnknown;
-  }
+  if (load(&e.mod, cubin.data()) != CUDA_SUCCESS || getf(&e.fn, e.mod, name) != CUDA_SUCCESS)
+    return failed("cuModuleLoadData / cuModuleGetFunction failed");
   g_jit[key] = e;
   *fn = e.fn;
   return cudaSuccess;
@@ -450,6 +589,58 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
 
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P) { return shuffle_hbm_source(P); }
 std::string smem_hbm_kernel_source(const ConvertPlan& P) { return smem_hbm_source(P); }
+std::string upcast_hbm_kernel_source(const ConvertPlan& P) { return upcast_hbm_source(P); }
+
+cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
+                              const uint8_t* scales, int max_ctas, cudaStream_t st,
+                              const TileRange& rg, std::string* err) {
+  if (P.op != 1 || P.sp.sc_nz > 2 || P.w != 1) return cudaErrorInvalidValue;
+  {
+    // the 256-bit stores need NVRTC >= 12.9 (the process may have loaded an
+    // older libnvrtc.so.12 first, e.g. PyTorch's bundled copy)
+    int major = 0, minor = 0;
+    nvrtcVersion(&major, &minor);
+    if (major < 12 || (major == 12 && minor < 9)) {
+      *err = "NVRTC " + std::to_string(major) + "." + std::to_string(minor) + " < 12.9";
+      return cudaErrorNotSupported;
+    }
+  }
+  CUfunction fn = nullptr;
+  cudaError_t e = get_kernel(upcast_hbm_source(P), &fn, err, "ll_upcast_hbm");
+  if (e != cudaSuccess) return e;
+  static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
+  static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
+  if (!launch || !setattr) return cudaErrorNotSupported;
+  const int64_t n_tiles = rg.t1 - rg.t0;
+  if (n_tiles <= 0) return cudaSuccess;
+  const int gpc = 8 >> P.sp.gw;
+  const int smem = gpc * 2 * P.sp.tile_bytes;
+  if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // persistent grid (the template kernel's sweep: 2 resident CTAs per SM)
+  const int tpg = planner_knob("upcast_jit_tpg", 0);
+  int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)sms * 2 * gpc;
+  if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
+  groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
+  const int64_t grid = (groups + gpc - 1) / gpc;
+  long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
+  const void* s = src;
+  void* d = dst;
+  const void* sc = scales;
+  void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
+                  (void*)&ss, (void*)&ds, (void*)&sc};
+  if (launch(fn, (unsigned)grid, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    *err = "cuLaunchKernel failed";
+    return cudaErrorLaunchFailure;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
                             cudaStream_t st, const TileRange& rg, std::string* err) {

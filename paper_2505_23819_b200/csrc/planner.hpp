@@ -107,6 +107,10 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
                                cudaStream_t st, const TileRange& rg, std::string* err);
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P);
 std::string smem_hbm_kernel_source(const ConvertPlan& P);
+std::string upcast_hbm_kernel_source(const ConvertPlan& P);
+cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
+                              const uint8_t* scales, int max_ctas, cudaStream_t st,
+                              const TileRange& rg, std::string* err);
 cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
                             cudaStream_t st, const TileRange& rg, std::string* err);
 bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin_bytes);

@@ -519,6 +519,18 @@ def test_mxfp4_upcast(mb, kb, dist):
     assert out.cpu().numpy().view(np.uint16).tobytes() == exp.tobytes()
 
 
+@pytest.mark.parametrize("jit", [0, 1])
+@pytest.mark.parametrize("dist", ["narrow", "uniform", "edges"])
+def test_mxfp4_upcast_kernels(dist, jit):
+    """Both upcast executors -- the template kernel and the one compiled for
+    the plan (knob upcast_jit) -- bit-exact on every scale distribution."""
+    ll.tune("upcast_jit", jit)
+    try:
+        test_mxfp4_upcast(9, 8, dist)
+    finally:
+        ll.tune("upcast_jit", 0)
+
+
 @pytest.mark.parametrize("dist", ["narrow", "uniform"])
 def test_mxfp4_upcast_full_size_sampled(dist):
     """Config 5 at the BASELINE size (packed [32768, 16384] u8 -> 2 GiB of
