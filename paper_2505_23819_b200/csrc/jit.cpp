@@ -231,7 +231,8 @@ std::string smem_hbm_source(const ConvertPlan& P) {
   const SmemPlan& p = P.sp;
   const int W = P.w, NV = P.nv, NW = NV * 4, G = P.g, GWd = G / 4, NG = NV * 16 / G;
   const int gw = p.gw, LB = ilog2i(NW);
-  const int minb = G < 8 ? 1 : (NV >= 8 ? 3 : 4);
+  const int minb_knob = planner_knob("smem_jit_minb", 0);
+  const int minb = minb_knob > 0 ? minb_knob : (G < 8 ? 1 : (NV >= 8 ? 3 : 4));
   std::ostringstream o;
   o << "struct TileTab { long long src, dst, sc; };\n"
     << "struct TileMap { long long n_tiles; int n_bits; int n_tab; long long bss, bsd; TileTab tab["
