@@ -14,10 +14,22 @@
 
 namespace ll {
 
-template <int G, bool MAT>
+// MAT: 0 = st/ld.shared vectors, 1 = stmatrix / ldmatrix, 2 = their .trans forms
+template <int G, int MAT>
 __device__ __forceinline__ void smem_put(uint32_t addr, const uint32_t* r) {
-  if constexpr (!MAT) {
+  if constexpr (MAT == 0) {
     sts<G * 4>(addr, r);
+  } else if constexpr (MAT == 2 && G == 4) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+                 : "memory");
+  } else if constexpr (MAT == 2 && G == 2) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x2.trans.shared.b16 [%0], {%1, %2};" ::"r"(addr), "r"(r[0]),
+                 "r"(r[1])
+                 : "memory");
+  } else if constexpr (MAT == 2) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x1.trans.shared.b16 [%0], {%1};" ::"r"(addr), "r"(r[0])
+                 : "memory");
   } else if constexpr (G == 4) {
     asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr),
                  "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
@@ -32,10 +44,22 @@ __device__ __forceinline__ void smem_put(uint32_t addr, const uint32_t* r) {
   }
 }
 
-template <int G, bool MAT>
+template <int G, int MAT>
 __device__ __forceinline__ void smem_get(uint32_t addr, uint32_t* r) {
-  if constexpr (!MAT) {
+  if constexpr (MAT == 0) {
     lds<G * 4>(addr, r);
+  } else if constexpr (MAT == 2 && G == 4) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr)
+                 : "memory");
+  } else if constexpr (MAT == 2 && G == 2) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1])
+                 : "r"(addr)
+                 : "memory");
+  } else if constexpr (MAT == 2) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x1.trans.shared.b16 {%0}, [%1];" : "=r"(r[0]) : "r"(addr) : "memory");
   } else if constexpr (G == 4) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -53,7 +77,7 @@ __device__ __forceinline__ void smem_get(uint32_t addr, uint32_t* r) {
 
 // all instructions of one side with compile-time operand selection: the GW
 // words of instruction j are R[deposit_word(j, k, LB, A, B)], k < GW
-template <int NW, int GW, bool MAT, bool PUT, int A, int B>
+template <int NW, int GW, int MAT, bool PUT, int A, int B>
 __device__ __forceinline__ void xfer_all(uint32_t (&R)[NW], uint32_t base, uint32_t tx,
                                          const uint32_t* inst) {
   constexpr int LB = ilog2(NW);
@@ -76,7 +100,7 @@ __device__ __forceinline__ void xfer_all(uint32_t (&R)[NW], uint32_t base, uint3
 // the exchange with fixed operand patterns (instruction words at word bits
 // 0, 1 -- the planner permuted the registers so); the side kinds are
 // dispatched once, outside the repetition loop
-template <int NW, int GWW, bool MW, int GWR, bool MR>
+template <int NW, int GWW, int MW, int GWR, int MR>
 __device__ __forceinline__ void exchange(uint32_t (&R)[NW], uint32_t (&Q)[NW], int reps,
                                          uint32_t sbase, uint32_t wx, uint32_t rx,
                                          const RegsPlan& p) {
@@ -90,20 +114,23 @@ __device__ __forceinline__ void exchange(uint32_t (&R)[NW], uint32_t (&Q)[NW], i
   }
 }
 
-template <int NW, int GWW, bool MW>
+template <int NW, int GWW, int MW>
 __device__ __forceinline__ void exchange_r(uint32_t (&R)[NW], uint32_t (&Q)[NW], int reps,
                                            uint32_t sbase, uint32_t wx, uint32_t rx,
                                            const RegsPlan& p) {
-  const int k = p.rd_gw * 2 + p.rd_mat;
-  if (k == 2) exchange<NW, GWW, MW, 1, false>(R, Q, reps, sbase, wx, rx, p);
-  else if (k == 3) exchange<NW, GWW, MW, 1, true>(R, Q, reps, sbase, wx, rx, p);
+  const int k = p.rd_gw * 4 + p.rd_mat;
+  if (k == 4) exchange<NW, GWW, MW, 1, 0>(R, Q, reps, sbase, wx, rx, p);
+  else if (k == 5) exchange<NW, GWW, MW, 1, 1>(R, Q, reps, sbase, wx, rx, p);
+  else if (k == 6) exchange<NW, GWW, MW, 1, 2>(R, Q, reps, sbase, wx, rx, p);
   if constexpr (NW >= 2) {
-    if (k == 4) exchange<NW, GWW, MW, 2, false>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 5) exchange<NW, GWW, MW, 2, true>(R, Q, reps, sbase, wx, rx, p);
+    if (k == 8) exchange<NW, GWW, MW, 2, 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 9) exchange<NW, GWW, MW, 2, 1>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 10) exchange<NW, GWW, MW, 2, 2>(R, Q, reps, sbase, wx, rx, p);
   }
   if constexpr (NW >= 4) {
-    if (k == 8) exchange<NW, GWW, MW, 4, false>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 9) exchange<NW, GWW, MW, 4, true>(R, Q, reps, sbase, wx, rx, p);
+    if (k == 16) exchange<NW, GWW, MW, 4, 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 17) exchange<NW, GWW, MW, 4, 1>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 18) exchange<NW, GWW, MW, 4, 2>(R, Q, reps, sbase, wx, rx, p);
   }
 }
 
@@ -111,16 +138,19 @@ template <int NW>
 __device__ __forceinline__ void exchange_w(uint32_t (&R)[NW], uint32_t (&Q)[NW], int reps,
                                            uint32_t sbase, uint32_t wx, uint32_t rx,
                                            const RegsPlan& p) {
-  const int k = p.wr_gw * 2 + p.wr_mat;
-  if (k == 2) exchange_r<NW, 1, false>(R, Q, reps, sbase, wx, rx, p);
-  else if (k == 3) exchange_r<NW, 1, true>(R, Q, reps, sbase, wx, rx, p);
+  const int k = p.wr_gw * 4 + p.wr_mat;
+  if (k == 4) exchange_r<NW, 1, 0>(R, Q, reps, sbase, wx, rx, p);
+  else if (k == 5) exchange_r<NW, 1, 1>(R, Q, reps, sbase, wx, rx, p);
+  else if (k == 6) exchange_r<NW, 1, 2>(R, Q, reps, sbase, wx, rx, p);
   if constexpr (NW >= 2) {
-    if (k == 4) exchange_r<NW, 2, false>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 5) exchange_r<NW, 2, true>(R, Q, reps, sbase, wx, rx, p);
+    if (k == 8) exchange_r<NW, 2, 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 9) exchange_r<NW, 2, 1>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 10) exchange_r<NW, 2, 2>(R, Q, reps, sbase, wx, rx, p);
   }
   if constexpr (NW >= 4) {
-    if (k == 8) exchange_r<NW, 4, false>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 9) exchange_r<NW, 4, true>(R, Q, reps, sbase, wx, rx, p);
+    if (k == 16) exchange_r<NW, 4, 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 17) exchange_r<NW, 4, 1>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 18) exchange_r<NW, 4, 2>(R, Q, reps, sbase, wx, rx, p);
   }
 }
 

@@ -14,8 +14,10 @@ namespace detail {
 // hold elements A holds in registers (load-side prmt swaps).
 struct RegsFrame {
   int w, lw, nr, nw, d, n, kw, LB, NW;
+  bool words_ok;        // B's word elements are among A's registers (swaps below)
   std::vector<std::pair<int, int>> swaps;
   std::vector<u64> WB, Aw, Bw, Al, Bl, Awp, Bwp;
+  std::vector<u64> Aw0;  // A's word-level columns without the swaps
 };
 
 bool regs_frame(const ConvertPlan& P, const Layout& A, const Layout& B, const std::vector<u64>& X,
@@ -62,12 +64,17 @@ bool regs_frame(const ConvertPlan& P, const Layout& A, const Layout& B, const st
   std::vector<std::pair<int, int>> swaps;
   std::vector<u64> cur;  // A's register columns in register order after the swaps
   for (int t = 0; t < nr; ++t) cur.push_back(e(t));
-  for (int t = 0; t < kw; ++t) {
+  const std::vector<u64> cur0 = cur;
+  bool words_ok = true;
+  for (int t = 0; t < kw && words_ok; ++t) {
     auto it = std::find(cur.begin(), cur.end(), WB[t]);
-    if (it == cur.end()) return false;
-    int s = (int)(it - cur.begin());
-    if (s < t) return false;
+    int s = it == cur.end() ? -1 : (int)(it - cur.begin());
+    if (s < t) { words_ok = false; break; }
     if (s != t) { swaps.push_back({t, s}); std::swap(cur[t], cur[s]); }
+  }
+  if (!words_ok) {  // only ldmatrix / stmatrix .trans options can serve (plan_regs)
+    swaps.clear();
+    cur = cur0;
   }
   // word-level columns, lanes, warps of both sides (tile vectors)
   std::vector<u64> Aw, Bw, Al, Bl, Awp, Bwp;
@@ -75,8 +82,10 @@ bool regs_frame(const ConvertPlan& P, const Layout& A, const Layout& B, const st
   for (int b = 0; b < 5; ++b) { Al.push_back(e(nr + b)); Bl.push_back(X[nr + b]); }
   for (int b = 0; b < nw; ++b) { Awp.push_back(e(nr + 5 + b)); Bwp.push_back(X[nr + 5 + b]); }
   f.w = w; f.lw = lw; f.nr = nr; f.nw = nw; f.d = d; f.n = n; f.kw = kw; f.LB = LB; f.NW = NW;
+  f.words_ok = words_ok;
   f.swaps = swaps;
   f.WB = WB; f.Aw = Aw; f.Bw = Bw; f.Al = Al; f.Bl = Bl; f.Awp = Awp; f.Bwp = Bwp;
+  for (int u = 0; u < LB; ++u) f.Aw0.push_back(cur0[kw + u]);
   return true;
 }
 
@@ -95,8 +104,11 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
   const int w = f.w, lw = f.lw, nr = f.nr, nw = f.nw, d = f.d, n = f.n, kw = f.kw, LB = f.LB, NW = f.NW;
   (void)nr;
   auto e = [](int i) { return u64(1) << i; };
-  const auto& swaps = f.swaps;
-  const auto &WB = f.WB, &Aw = f.Aw, &Bw = f.Bw, &Al = f.Al, &Bl = f.Bl, &Awp = f.Awp, &Bwp = f.Bwp;
+  const auto &WB = f.WB, &Bw = f.Bw, &Al = f.Al, &Bl = f.Bl, &Awp = f.Awp, &Bwp = f.Bwp;
+  // per option: with the load-side swaps (A's words = B's words) or without
+  // (the .trans options, where each side keeps its own words)
+  std::vector<std::pair<int, int>> swaps;
+  std::vector<u64> Aw;
   auto pos = [](const std::vector<u64>& v, u64 x) {
     auto it = std::find(v.begin(), v.end(), x);
     return it == v.end() ? -1 : (int)(it - v.begin());
@@ -105,7 +117,8 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
   // candidate granule rows: (extra S_vect vectors beyond the word, side kinds)
   struct Opt {
     std::vector<u64> gv;     // granule vectors after the word bits (<= 2)
-    int wr_mat = 0, rd_mat = 0, wr_gw = 1, rd_gw = 1;
+    std::vector<u64> svect;  // .trans options: the full S_vect (else WB + gv)
+    int wr_mat = 0, rd_mat = 0, wr_gw = 1, rd_gw = 1;   // mat: 0 vector, 1 matrix, 2 matrix.trans
     int wa = -1, wb = -1, ra = -1, rb = -1;
     int cost = 1 << 30;
   };
@@ -136,15 +149,58 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
     o.cost = NW / o.wr_gw + NW / o.rd_gw;
     opts.push_back(o);
   };
-  {  // generalised vectorisation: word-level columns common to both sides
-    std::vector<u64> gv;
-    for (u64 x : Aw) if (pos(Bw, x) >= 0 && gv.size() < 2) gv.push_back(x);
-    consider(gv);
+  if (f.words_ok) {
+    swaps = f.swaps;
+    Aw = f.Aw;
+    {  // generalised vectorisation: word-level columns common to both sides
+      std::vector<u64> gv;
+      for (u64 x : Aw) if (pos(Bw, x) >= 0 && gv.size() < 2) gv.push_back(x);
+      consider(gv);
+    }
+    if (allow_mat) {
+      consider({Al[0], Al[1]});
+      consider({Bl[0], Bl[1]});
+    }
   }
-  if (allow_mat) {
-    consider({Al[0], Al[1]});
-    consider({Bl[0], Bl[1]});
+  // ldmatrix / stmatrix .trans (b16): the 16-byte row is the side's lanes
+  // 2..4 (thread t holds rows 2(t%4), 2(t%4)+1 of column t/4), so each side
+  // keeps its own word and no load-side swap is needed -- the transposes
+  const size_t n_plain = opts.size();
+  if (w == 2 && allow_mat && planner_knob("regs_trans", 1)) {
+    const std::vector<u64> TA = {Al[2], Al[3], Al[4]}, TB = {Bl[2], Bl[3], Bl[4]};
+    const u64 a0 = e(0), b0 = X[0];  // each side's word element bit
+    auto side_t = [&](const std::vector<u64>& T, u64 w0, const std::vector<u64>& W,
+                      const std::vector<u64>& L, int& mat, int& gw, int& a, int& b) -> bool {
+      a = b = -1;
+      if (T == std::vector<u64>{L[2], L[3], L[4]}) {   // .trans too
+        mat = 2; gw = std::min(4, NW); a = LB > 0 ? 0 : -1; b = LB > 1 ? 1 : -1;
+        return true;
+      }
+      if (w0 != T[0]) return false;                    // the side's word must be the row's pair
+      if (T[1] == L[0] && T[2] == L[1]) {              // plain matrix
+        mat = 1; gw = std::min(4, NW); a = LB > 0 ? 0 : -1; b = LB > 1 ? 1 : -1;
+        return true;
+      }
+      mat = 0;
+      int q = 0;
+      if (pos(W, T[1]) >= 0) { a = pos(W, T[1]); ++q; }
+      if (q == 1 && pos(W, T[2]) >= 0) { b = pos(W, T[2]); ++q; }
+      gw = 1 << q;
+      return true;
+    };
+    for (int which = 0; which < 2; ++which) {
+      const std::vector<u64>& T = which ? TB : TA;
+      Opt o;
+      o.svect = T;
+      if (!side_t(T, a0, f.Aw0, Al, o.wr_mat, o.wr_gw, o.wa, o.wb)) continue;
+      if (!side_t(T, b0, Bw, Bl, o.rd_mat, o.rd_gw, o.ra, o.rb)) continue;
+      if (o.wr_mat != 2 && o.rd_mat != 2) continue;
+      o.cost = NW / o.wr_gw + NW / o.rd_gw;
+      opts.push_back(o);
+    }
   }
+  (void)n_plain;
+  if (opts.empty()) return false;
   // options by cost (instructions per thread), matrix instructions first on
   // ties (the paper's preference for hardware primitives); an option
   // whose layouts turn out not divisible by the matrix tile under the
@@ -158,22 +214,31 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
   Opt best;
   auto build = [&](const Opt& o) -> bool {
     best = o;
-    V = WB;  // S_vect: word bits (B's order), then the granule rows
-    for (u64 x : best.gv) V.push_back(x);
+    const bool own = !o.svect.empty();   // .trans option: no load-side swaps
+    swaps = own ? std::vector<std::pair<int, int>>{} : f.swaps;
+    Aw = own ? f.Aw0 : f.Aw;
+    const u64 wA = own ? e(0) : (WB.empty() ? 0 : WB[0]), wB = X[0];
+    if (own) {
+      V = o.svect;
+    } else {
+      V = WB;  // S_vect: word bits (B's order), then the granule rows
+      for (u64 x : best.gv) V.push_back(x);
+    }
     // bank-relevant thread vectors per side (phase order): lanes for vector
     // accesses; the address providers (rows = lanes 2..4, then the matrix
     // select word bits) for stmatrix / ldmatrix
-    auto thr_vecs = [&](int mat, const std::vector<u64>& W, const std::vector<u64>& L, int a, int b) {
+    auto thr_vecs = [&](int mat, const std::vector<u64>& W, const std::vector<u64>& L, int a, int b,
+                        u64 w0) {
       std::vector<u64> t;
       if (!mat) return L;
-      t = {L[2], L[3], L[4]};
+      t = mat == 2 ? std::vector<u64>{w0, L[0], L[1]} : std::vector<u64>{L[2], L[3], L[4]};
       if (a >= 0) t.push_back(W[a]);
       if (b >= 0) t.push_back(W[b]);
       while (t.size() < 5) t.push_back(L[2]);  // padding (dropped by the phase rule)
       return t;
     };
-    At = thr_vecs(best.wr_mat, Aw, Al, best.wa, best.wb);
-    Bt = thr_vecs(best.rd_mat, Bw, Bl, best.ra, best.rb);
+    At = thr_vecs(best.wr_mat, Aw, Al, best.wa, best.wb, wA);
+    Bt = thr_vecs(best.rd_mat, Bw, Bl, best.ra, best.rb, wB);
     sw = optimal_swizzle(At, Bt, V, d, w);
     std::vector<u64> Scols = sw.vect;
     Scols.insert(Scols.end(), sw.bank.begin(), sw.bank.end());
@@ -201,8 +266,28 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
       r.insert(r.end(), Wp.begin(), Wp.end());
       return r;
     };
-    if (best.wr_mat && !divisible(WB, Al, rest_of(Aw, Al, Awp))) return false;
-    if (best.rd_mat && !divisible(WB, Bl, rest_of(Bw, Bl, Bwp))) return false;
+    // .trans tile: the row's 8 elements are lanes 2..4 (offset bits 0..2); the
+    // word bit and lanes 0, 1 select rows, like every other column
+    auto divisible_t = [&](u64 w0, const std::vector<u64>& W, const std::vector<u64>& L,
+                           const std::vector<u64>& Wp) {
+      for (int t = 0; t < 3; ++t)
+        if (f2_apply(Sinv, L[2 + t]) != e(t)) return false;
+      std::vector<u64> rest(W);
+      rest.push_back(w0);
+      rest.push_back(L[0]);
+      rest.push_back(L[1]);
+      rest.insert(rest.end(), Wp.begin(), Wp.end());
+      for (u64 c : rest)
+        if (f2_apply(Sinv, c) & 7u) return false;
+      return true;
+    };
+    if (best.wr_mat == 1 && !divisible(own ? std::vector<u64>{wA} : WB, Al, rest_of(Aw, Al, Awp))) return false;
+    if (best.rd_mat == 1 && !divisible(own ? std::vector<u64>{wB} : WB, Bl, rest_of(Bw, Bl, Bwp))) return false;
+    if (best.wr_mat == 2 && !divisible_t(wA, Aw, Al, Awp)) return false;
+    if (best.rd_mat == 2 && !divisible_t(wB, Bw, Bl, Bwp)) return false;
+    // vector sides read / write whole words: their word must be offset bit 0
+    if (own && best.wr_mat == 0 && f2_apply(Sinv, wA) != 1) return false;
+    if (own && best.rd_mat == 0 && f2_apply(Sinv, wB) != 1) return false;
     RegsPlan& rp = P.rp;
     rp = RegsPlan{};
     rp.nw = nw;
@@ -239,13 +324,15 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
     const std::vector<u64> Awc = canon(Aw, best.wa, best.wb, best.wr_gw, rp.n_wsw, rp.wsw_a, rp.wsw_b);
     const std::vector<u64> Bwc = canon(Bw, best.ra, best.rb, best.rd_gw, rp.n_rsw, rp.rsw_a, rp.rsw_b);
     auto fill = [&](int mat, const std::vector<u64>& W, const std::vector<u64>& L,
-                    const std::vector<u64>& Wp, int a, int b, int gw, uint32_t* thr, uint32_t* inst) {
+                    const std::vector<u64>& Wp, int a, int b, int gw, uint32_t* thr, uint32_t* inst,
+                    u64 wrow0) {
       if (mat) {
-        // address provider lane p: rows = p bits 0..2 (the data lanes 2..4),
-        // matrix = p bits 3, 4 (the selected word bits)
-        thr[0] = boff(L[2]);
-        thr[1] = boff(L[3]);
-        thr[2] = boff(L[4]);
+        // address provider lane p: rows = p bits 0..2 (the data lanes 2..4;
+        // .trans: the word bit and lanes 0, 1), matrix = p bits 3, 4 (the
+        // selected word bits)
+        thr[0] = boff(mat == 2 ? wrow0 : L[2]);
+        thr[1] = boff(mat == 2 ? L[0] : L[3]);
+        thr[2] = boff(mat == 2 ? L[1] : L[4]);
         thr[3] = a >= 0 && gw >= 2 ? boff(W[a]) : 0;
         thr[4] = b >= 0 && gw >= 4 ? boff(W[b]) : 0;
       } else {
@@ -266,9 +353,9 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
       }
       return true;
     };
-    if (!fill(rp.wr_mat, Awc, Al, Awp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.wr_gw, rp.sw_thr, rp.sw_inst))
+    if (!fill(rp.wr_mat, Awc, Al, Awp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.wr_gw, rp.sw_thr, rp.sw_inst, wA))
       return false;
-    if (!fill(rp.rd_mat, Bwc, Bl, Bwp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.rd_gw, rp.sr_thr, rp.sr_inst))
+    if (!fill(rp.rd_mat, Bwc, Bl, Bwp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.rd_gw, rp.sr_thr, rp.sr_inst, wB))
       return false;
     P.nv = NW;
     P.tile_bits = d;
@@ -281,10 +368,10 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
     if ((ok = build(o))) break;
   if (!ok) return false;
   RegsPlan& rp = P.rp;
-  static const char* kinds[] = {"st.shared", "stmatrix", "ld.shared", "ldmatrix"};
+  static const char* kinds[] = {"st.shared", "stmatrix", "stmatrix.trans", "ld.shared", "ldmatrix", "ldmatrix.trans"};
   js << ",\"regs\":{\"warps_log2\":" << nw << ",\"words_per_thread\":" << NW
      << ",\"write\":\"" << kinds[rp.wr_mat] << "\",\"write_words\":" << rp.wr_gw
-     << ",\"read\":\"" << kinds[2 + rp.rd_mat] << "\",\"read_words\":" << rp.rd_gw
+     << ",\"read\":\"" << kinds[3 + rp.rd_mat] << "\",\"read_words\":" << rp.rd_gw
      << ",\"write_instr_per_thread\":" << NW / rp.wr_gw
      << ",\"read_instr_per_thread\":" << NW / rp.rd_gw << ",\"n_tiles\":" << rp.n_tiles
      << ",\"swaps\":" << swaps.size() << ",\"sw_thr\":" << u32_json(rp.sw_thr, 5 + nw)
@@ -304,7 +391,7 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
 bool plan_regs_shuffle(ConvertPlan& P, const Layout& A, const Layout& B,
                        const std::vector<u64>& X, std::ostringstream& js) {
   RegsFrame f;
-  if (!regs_frame(P, A, B, X, f)) return false;
+  if (!regs_frame(P, A, B, X, f) || !f.words_ok) return false;
   if (f.NW > LL_MAX_GRAN) return false;
   for (int b = 0; b < f.nw; ++b)
     if (f.Bwp[b] != f.Awp[b]) return false;

@@ -496,3 +496,41 @@ def test_shuffle_hbm_kernel_specialises_and_compiles():
         src = ll.jit_source(A, B, 8 * c["elem_bytes"], kernel="shuffle")
         assert src.count("__shfl_sync") == d["shuffle"]["rounds"]
         assert ll.jit_source(A, B, 8 * c["elem_bytes"], compile=True, kernel="shuffle")["compiled"]
+
+
+def test_regs_trans_tile_divides():
+    """The .trans lowering: on an mma-fragment / transposed-fragment pair the
+    planner writes with stmatrix.trans and reads with ldmatrix, and the
+    oracle's left division confirms the tiles on S^{-1} o L -- the .trans tile
+    (rows = word bit and lanes 0, 1; the 16-byte row = lanes 2..4) for A, the
+    plain tile for B; with .trans disabled the pair has no plan."""
+    from oracle.layout import left_divide as oldiv
+    import importlib.util
+    spec_ = importlib.util.spec_from_file_location("tgp", os.path.join(os.path.dirname(__file__), "test_gpu_parity.py"))
+    src = open(spec_.origin).read()
+    ns = {"OLayout": OLayout}
+    exec(src[src.index("def rand_trans_pair"):src.index("def test_convert_regs_trans_pairs")], ns)
+    c = ns["rand_trans_pair"](random.Random(3), 3)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    d = ll.plan_describe(A, B, 16, "regs")
+    assert (d["regs"]["write"], d["regs"]["read"]) == ("stmatrix.trans", "ldmatrix")
+    M = _regs_S_inverse_compose(d, c, "A")
+    # reorder A's input dims so the .trans tile is a left factor: lanes 2..4
+    # first (the row's elements), then the word bit and lanes 0, 1
+    cols = M.cols
+    r = 3
+    order = [r + 2, r + 3, r + 4, 0, r + 0, r + 1]
+    Mt = OLayout([("lane", 3), ("reg", 3)], [("offset", len(cols))],
+                 {"lane": [(cols[k],) for k in order[:3]], "reg": [(cols[k],) for k in order[3:]]})
+    T = OLayout([("lane", 3), ("reg", 0)], [("offset", 3)], {"lane": [(1,), (2,), (4,)], "reg": []})
+    oldiv(Mt, T)
+    MB = _regs_S_inverse_compose(d, c, "B")
+    Tb = OLayout([("reg", 1), ("lane", 2)], [("offset", 3)],
+                 {"reg": [(1,)], "lane": [(2,), (4,)]})
+    oldiv(MB, Tb)
+    try:
+        ll.tune("regs_trans", 0)
+        with pytest.raises(ll.LLError):
+            ll.plan_describe(A, B, 16, "regs")
+    finally:
+        ll.tune("regs_trans", 1)
