@@ -49,6 +49,15 @@ def main():
     ok &= conv(configs.cfg2(batch_bits=1), "regs")
     ok &= conv(configs.cfg2w(batch_bits=1), "regs_shuffle")
     ok &= conv(configs.cfg2(batch_bits=1), "generic")
+    # ldmatrix / stmatrix .trans (register-faithful transposed fragments)
+    import random
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_gpu_parity import rand_trans_pair  # noqa: E402
+    ok &= conv(dict(rand_trans_pair(random.Random(3), 3), name="trans"), "regs")
+    # the template smem kernel (the default compiles the plan)
+    ll.tune("smem_jit", 0)
+    ok &= conv(configs.cfg3(n_bits=8), "smem")
+    ll.tune("smem_jit", 1)
     g = configs.cfg4(r_bits=3)
     L = ll.Layout.from_spec(g["L"])
     m = 1 << L.in_bits
