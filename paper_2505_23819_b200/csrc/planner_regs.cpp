@@ -165,7 +165,6 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
   // ldmatrix / stmatrix .trans (b16): the 16-byte row is the side's lanes
   // 2..4 (thread t holds rows 2(t%4), 2(t%4)+1 of column t/4), so each side
   // keeps its own word and no load-side swap is needed -- the transposes
-  const size_t n_plain = opts.size();
   if (w == 2 && allow_mat && planner_knob("regs_trans", 1)) {
     const std::vector<u64> TA = {Al[2], Al[3], Al[4]}, TB = {Bl[2], Bl[3], Bl[4]};
     const u64 a0 = e(0), b0 = X[0];  // each side's word element bit
@@ -199,7 +198,6 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
       opts.push_back(o);
     }
   }
-  (void)n_plain;
   if (opts.empty()) return false;
   // options by cost (instructions per thread), matrix instructions first on
   // ties (the paper's preference for hardware primitives); an option
