@@ -463,8 +463,13 @@ def main():
             except Exception as ex:  # the baseline must never break the line
                 cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "oracle",
                        "sample": "failed: %s" % ex}
-        generic_smem = args.upcast or "smem_jit=0" in args.tune
-        kernel = {"smem": "convert_smem_kernel" if generic_smem else "ll_smem_hbm (NVRTC)",
+        generic_smem = "smem_jit=0" in args.tune
+        if args.upcast:
+            up_jit = "upcast_jit=0" not in args.tune
+            smem_kernel = "ll_upcast_hbm (NVRTC)" if up_jit else "convert_smem_kernel (upcast)"
+        else:
+            smem_kernel = "convert_smem_kernel" if generic_smem else "ll_smem_hbm (NVRTC)"
+        kernel = {"smem": smem_kernel,
                   "generic": "convert_generic_kernel",
                   "shuffle": "gather_shuffle_kernel" if cfg == "4" else "ll_shfl_hbm (NVRTC)",
                   "smem_noswizzle": "convert_smem_kernel", "smem_padded": "convert_smem_kernel",
@@ -489,7 +494,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic(cfg + ("_upcast" if args.upcast else "") +
-                                                {"smem": "" if (args.upcast or "smem_jit=0" in args.tune) else "_jit", "smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas",
+                                                {"smem": ("_jit" if "upcast_jit=0" not in args.tune else "") if args.upcast
+                                                 else ("" if "smem_jit=0" in args.tune else "_jit"), "smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas",
                                                  "shuffle": "" if cfg == "4" else "_shfl"}.get(
                                                     plan.get("path"), "")),
                          "peak_source": peak_src, "kernel": kernel,

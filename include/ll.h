@@ -240,8 +240,9 @@ ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout
  *             NaN.
  * The conversion runs on the smem path (LL_ERR_UNSUPPORTED otherwise); the
  * decode is fused into its store stage (2 GiB written for config 5, as
- * 256-bit sm_100 stores).  packed must be 16-byte and dst_bf16 32-byte
- * aligned (LL_ERR_ARG otherwise). */
+ * 256-bit sm_100 stores; by default in a kernel compiled for the plan with
+ * NVRTC, knob upcast_jit=0: the template kernel).  packed must be 16-byte and
+ * dst_bf16 32-byte aligned (LL_ERR_ARG otherwise). */
 ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_t* scales,
                           void* dst_bf16, ll_layout dst_layout, const ll_convert_options* opts,
                           ll_stream stream);

@@ -69,10 +69,12 @@ def build(force=False, verbose=False):
                 sys.stderr.write(log)
     if force or not os.path.exists(OUT) or _mtime(OUT) < max(_mtime(o) for o in objs):
         tmp = OUT + ".tmp"
-        # NVRTC (jit.cpp) from the toolkit, found through the rpath at run time
+        # NVRTC (jit.cpp): the toolkit's coexistence build (libnvrtc.alt, own soname and
+        # symbol versions), so an older libnvrtc.so.12 already loaded by PyTorch
+        # does not shadow it; found through the rpath at run time
         lib64 = os.path.join(CUDA, "lib64")
         cmd = [NVCC, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs,
-               "-L" + lib64, "-lnvrtc", "-Xlinker", "-rpath," + lib64,
+               "-L" + lib64, "-lnvrtc.alt", "-Xlinker", "-rpath," + lib64,
                "-Xlinker", "-soname,libll_b200.so"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

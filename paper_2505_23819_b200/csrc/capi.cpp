@@ -570,7 +570,7 @@ ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_
     auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, 1, LL_PATH_AUTO, 1, 1);
     ll::TileRange rg{0, P->sp.tile.n_tiles, 0, 0};
     ++g_launches;
-    if (ll::planner_knob("upcast_jit", 0) && P->sp.sc_nz <= 2) {
+    if (ll::planner_knob("upcast_jit", 1) && P->sp.sc_nz <= 2) {
       std::string err;
       cudaError_t e = ll::launch_upcast_jit(*P, packed, dst_bf16, scales, opts ? opts->max_ctas : 0,
                                             reinterpret_cast<cudaStream_t>(stream), rg, &err);

@@ -623,8 +623,8 @@ cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // persistent grid (the template kernel's sweep: 2 resident CTAs per SM)
-  const int tpg = planner_knob("upcast_jit_tpg", 0);
+  // tiles per group (sweep on B200: 4-8 -> 6.49-6.50 TB/s, persistent 5.81)
+  const int tpg = planner_knob("upcast_jit_tpg", 4);
   int64_t groups = tpg > 0 ? (n_tiles + tpg - 1) / tpg : (int64_t)sms * 2 * gpc;
   if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
   groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));

@@ -528,7 +528,7 @@ def test_mxfp4_upcast_kernels(dist, jit):
     try:
         test_mxfp4_upcast(9, 8, dist)
     finally:
-        ll.tune("upcast_jit", 0)
+        ll.tune("upcast_jit", 1)
 
 
 @pytest.mark.parametrize("dist", ["narrow", "uniform"])
