@@ -114,43 +114,43 @@ __device__ __forceinline__ void exchange(uint32_t (&R)[NW], uint32_t (&Q)[NW], i
   }
 }
 
-template <int NW, int GWW, int MW>
+template <int W, int NW, int GWW, int MW>
 __device__ __forceinline__ void exchange_r(uint32_t (&R)[NW], uint32_t (&Q)[NW], int reps,
                                            uint32_t sbase, uint32_t wx, uint32_t rx,
                                            const RegsPlan& p) {
   const int k = p.rd_gw * 4 + p.rd_mat;
   if (k == 4) exchange<NW, GWW, MW, 1, 0>(R, Q, reps, sbase, wx, rx, p);
   else if (k == 5) exchange<NW, GWW, MW, 1, 1>(R, Q, reps, sbase, wx, rx, p);
-  else if (k == 6) exchange<NW, GWW, MW, 1, 2>(R, Q, reps, sbase, wx, rx, p);
+  else if (W == 2 && k == 6) exchange<NW, GWW, MW, 1, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
   if constexpr (NW >= 2) {
     if (k == 8) exchange<NW, GWW, MW, 2, 0>(R, Q, reps, sbase, wx, rx, p);
     else if (k == 9) exchange<NW, GWW, MW, 2, 1>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 10) exchange<NW, GWW, MW, 2, 2>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 2 && k == 10) exchange<NW, GWW, MW, 2, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
   if constexpr (NW >= 4) {
     if (k == 16) exchange<NW, GWW, MW, 4, 0>(R, Q, reps, sbase, wx, rx, p);
     else if (k == 17) exchange<NW, GWW, MW, 4, 1>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 18) exchange<NW, GWW, MW, 4, 2>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 2 && k == 18) exchange<NW, GWW, MW, 4, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
 }
 
-template <int NW>
+template <int W, int NW>
 __device__ __forceinline__ void exchange_w(uint32_t (&R)[NW], uint32_t (&Q)[NW], int reps,
                                            uint32_t sbase, uint32_t wx, uint32_t rx,
                                            const RegsPlan& p) {
   const int k = p.wr_gw * 4 + p.wr_mat;
-  if (k == 4) exchange_r<NW, 1, 0>(R, Q, reps, sbase, wx, rx, p);
-  else if (k == 5) exchange_r<NW, 1, 1>(R, Q, reps, sbase, wx, rx, p);
-  else if (k == 6) exchange_r<NW, 1, 2>(R, Q, reps, sbase, wx, rx, p);
+  if (k == 4) exchange_r<W, NW, 1, 0>(R, Q, reps, sbase, wx, rx, p);
+  else if (k == 5) exchange_r<W, NW, 1, 1>(R, Q, reps, sbase, wx, rx, p);
+  else if (W == 2 && k == 6) exchange_r<W, NW, 1, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
   if constexpr (NW >= 2) {
-    if (k == 8) exchange_r<NW, 2, 0>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 9) exchange_r<NW, 2, 1>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 10) exchange_r<NW, 2, 2>(R, Q, reps, sbase, wx, rx, p);
+    if (k == 8) exchange_r<W, NW, 2, 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 9) exchange_r<W, NW, 2, 1>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 2 && k == 10) exchange_r<W, NW, 2, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
   if constexpr (NW >= 4) {
-    if (k == 16) exchange_r<NW, 4, 0>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 17) exchange_r<NW, 4, 1>(R, Q, reps, sbase, wx, rx, p);
-    else if (k == 18) exchange_r<NW, 4, 2>(R, Q, reps, sbase, wx, rx, p);
+    if (k == 16) exchange_r<W, NW, 4, 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (k == 17) exchange_r<W, NW, 4, 1>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 2 && k == 18) exchange_r<W, NW, 4, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
 }
 
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256) convert_regs_kernel(const __grid_constant
     uint32_t Q[NW];
     long long c0 = 0;
     if (cycles && tid == 0) c0 = clock64();
-    exchange_w<NW>(R, Q, reps, sbase, wx, rx, p);
+    exchange_w<W, NW>(R, Q, reps, sbase, wx, rx, p);
     if (cycles && tid == 0 && t == blockIdx.x) cycles[blockIdx.x] = clock64() - c0;
     for (int s = p.n_rsw - 1; s >= 0; --s) swap_word_bits<NW>(Q, p.rsw_a[s], p.rsw_b[s]);
     if constexpr (TB >= 16) {
