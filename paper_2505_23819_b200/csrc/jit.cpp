@@ -265,44 +265,68 @@ std::string smem_hbm_source(const ConvertPlan& P) {
     o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
       << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; }\n";
   o << "  };\n";
-  auto load = [&](const char* ind) {
+  auto load = [&](const char* ind, const std::string& R) {
     for (int u = 0; u < NV; ++u)
-      o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(R["
-        << 4 * u << "]), \"=r\"(R[" << 4 * u + 1 << "]), \"=r\"(R[" << 4 * u + 2 << "]), \"=r\"(R["
-        << 4 * u + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
+      o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(" << R << "["
+        << 4 * u << "]), \"=r\"(" << R << "[" << 4 * u + 1 << "]), \"=r\"(" << R << "[" << 4 * u + 2
+        << "]), \"=r\"(" << R << "[" << 4 * u + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
   };
-  o << "  long long t = t0 + gid;\n  if (t < t1) { tile_off(t);\n";
-  load("    ");
-  o << "  }\n  for (; t < t1; t += n_groups) {\n    const long long dcur = dof;\n";
-  for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], "R");
   const int ga = GWd >= 2 ? p.gsel_a : -1, gb = GWd >= 4 ? p.gsel_b : -1;
-  for (int j = 0; j < NG; ++j) {
-    o << "    asm volatile(\"st.shared.";
-    if (GWd == 4) o << "v4.b32 [%0], {%1,%2,%3,%4};\"";
-    else if (GWd == 2) o << "v2.b32 [%0], {%1,%2};\"";
-    else o << "b32 [%0], %1;\"";
-    o << " :: \"r\"(sbase + buf + (swx ^ " << p.sw_gran[j] << "u))";
-    for (int k = 0; k < GWd; ++k) o << ", \"r\"(R[" << deposit_word_h(j, k, LB, ga, gb) << "])";
-    o << " : \"memory\");\n";
+  // one tile: swaps, STS, prefetch of tile t + ahead * n_groups into the same
+  // registers, group barrier, LDS, streaming stores
+  auto body = [&](const std::string& R, const std::string& dv, int ahead) {
+    o << "    { const long long dcur = " << dv << ";\n";
+    for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], R.c_str());
+    for (int j = 0; j < NG; ++j) {
+      o << "    asm volatile(\"st.shared.";
+      if (GWd == 4) o << "v4.b32 [%0], {%1,%2,%3,%4};\"";
+      else if (GWd == 2) o << "v2.b32 [%0], {%1,%2};\"";
+      else o << "b32 [%0], %1;\"";
+      o << " :: \"r\"(sbase + buf + (swx ^ " << p.sw_gran[j] << "u))";
+      for (int k = 0; k < GWd; ++k) o << ", \"r\"(" << R << "[" << deposit_word_h(j, k, LB, ga, gb) << "])";
+      o << " : \"memory\");\n";
+    }
+    o << "    { const long long tn = t + " << ahead << " * n_groups; if (tn < t1) { tile_off(tn); "
+      << dv << " = dof;\n";
+    load("      ", R);
+    o << "    } }\n";
+    if (gw == 0) o << "    __syncwarp();\n";
+    else o << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(group + 1), \"r\"(" << (32 << gw) << ") : \"memory\");\n";
+    for (int j = 0; j < NG; ++j) {
+      o << "    asm volatile(\"ld.shared.";
+      if (GWd == 4) o << "v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q[" << 4 * j + 1
+                      << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "])";
+      else if (GWd == 2) o << "v2.b32 {%0,%1}, [%2];\" : \"=r\"(Q[" << 2 * j << "]), \"=r\"(Q[" << 2 * j + 1 << "])";
+      else o << "b32 %0, [%1];\" : \"=r\"(Q[" << j << "])";
+      o << " : \"r\"(sbase + buf + (srx ^ " << p.sr_gran[j] << "u)) : \"memory\");\n";
+    }
+    for (int u = 0; u < NV; ++u)
+      o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dcur + "
+        << p.st_vec[u] << "), \"r\"(Q[" << 4 * u << "]), \"r\"(Q[" << 4 * u + 1 << "]), \"r\"(Q["
+        << 4 * u + 2 << "]), \"r\"(Q[" << 4 * u + 3 << "]) : \"memory\");\n";
+    o << "    buf ^= " << p.tile_bytes << "u; }\n";
+  };
+  const int depth = std::max(1, std::min(2, planner_knob("smem_jit_depth", 1)));
+  o << "  long long t = t0 + gid;\n";
+  if (depth == 1) {
+    o << "  long long da = 0;\n  if (t < t1) { tile_off(t); da = dof;\n";
+    load("    ", "R");
+    o << "  }\n  for (; t < t1; t += n_groups) {\n";
+    body("R", "da", 1);
+    o << "  }\n}\n";
+  } else {
+    // two tiles in flight per group: registers Ra / Rb alternate
+    o << "  unsigned Ra[" << NW << "], Rb[" << NW << "];\n  long long da = 0, db = 0;\n"
+      << "  if (t < t1) { tile_off(t); da = dof;\n";
+    load("    ", "Ra");
+    o << "  }\n  if (t + n_groups < t1) { tile_off(t + n_groups); db = dof;\n";
+    load("    ", "Rb");
+    o << "  }\n  while (t < t1) {\n";
+    body("Ra", "da", 2);
+    o << "    t += n_groups;\n    if (t >= t1) break;\n";
+    body("Rb", "db", 2);
+    o << "    t += n_groups;\n  }\n}\n";
   }
-  o << "    { const long long tn = t + n_groups; if (tn < t1) { tile_off(tn);\n";
-  load("      ");
-  o << "    } }\n";
-  if (gw == 0) o << "    __syncwarp();\n";
-  else o << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(group + 1), \"r\"(" << (32 << gw) << ") : \"memory\");\n";
-  for (int j = 0; j < NG; ++j) {
-    o << "    asm volatile(\"ld.shared.";
-    if (GWd == 4) o << "v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q[" << 4 * j + 1
-                    << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "])";
-    else if (GWd == 2) o << "v2.b32 {%0,%1}, [%2];\" : \"=r\"(Q[" << 2 * j << "]), \"=r\"(Q[" << 2 * j + 1 << "])";
-    else o << "b32 %0, [%1];\" : \"=r\"(Q[" << j << "])";
-    o << " : \"r\"(sbase + buf + (srx ^ " << p.sr_gran[j] << "u)) : \"memory\");\n";
-  }
-  for (int u = 0; u < NV; ++u)
-    o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dcur + "
-      << p.st_vec[u] << "), \"r\"(Q[" << 4 * u << "]), \"r\"(Q[" << 4 * u + 1 << "]), \"r\"(Q["
-      << 4 * u + 2 << "]), \"r\"(Q[" << 4 * u + 3 << "]) : \"memory\");\n";
-  o << "    buf ^= " << p.tile_bytes << "u;\n  }\n}\n";
   return o.str();
 }
 
