@@ -496,6 +496,12 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
     *err = m;
     return cudaErrorUnknown;
   };
+  // test hook: make every compile fail (the template-kernel fallback path);
+  // not cached
+  if (planner_knob("jit_force_fail", 0)) {
+    *err = "jit_force_fail";
+    return cudaErrorUnknown;
+  }
   static PFN_LoadData load = entry<PFN_LoadData>("cuModuleLoadData");
   static PFN_GetFunction getf = entry<PFN_GetFunction>("cuModuleGetFunction");
   if (!load || !getf) return failed("driver entry points unavailable");

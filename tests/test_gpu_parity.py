@@ -925,3 +925,22 @@ def test_convert_regs_trans_pairs():
         src, dst = run_convert(c, path="regs", seed=rng.randint(0, 999), batch=batch)
         assert dst.tobytes() == expect_convert(c, src, batch).tobytes(), plan.get("regs")
     assert any("trans" in a or "trans" in b for a, b in kinds), kinds
+
+
+def test_jit_failure_falls_back_to_template_kernels():
+    """If NVRTC / module loading fails (forced by the jit_force_fail hook), the
+    smem, shuffle and upcast paths run their template kernels from the
+    library instead, byte-exact -- never a CPU path."""
+    rng = random.Random(1400)
+    ll.tune("jit_force_fail", 1)
+    try:
+        for w in (1, 2, 4):
+            c = rand_pair(rng, 14, w)
+            src, dst = run_convert(c, path="smem", seed=3, batch=2)
+            assert dst.tobytes() == expect_convert(c, src, 2).tobytes()
+        c = configs.cfg2(batch_bits=2)
+        src, dst = run_convert(c, path="shuffle", seed=4)
+        assert dst.tobytes() == expect_convert(c, src).tobytes()
+        test_mxfp4_upcast(8, 7, "narrow")
+    finally:
+        ll.tune("jit_force_fail", 0)
