@@ -34,6 +34,7 @@ int ilog2i(int x) {
 typedef CUresult (*PFN_LoadData)(CUmodule*, const void*);
 typedef CUresult (*PFN_GetFunction)(CUfunction*, CUmodule, const char*);
 typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+typedef CUresult (*PFN_LaunchEx)(const CUlaunchConfig*, CUfunction, void**, void**);
 typedef CUresult (*PFN_Launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                                unsigned, unsigned, CUstream, void**, void**);
 
@@ -307,11 +308,19 @@ std::string smem_hbm_source(const ConvertPlan& P) {
     o << "    buf ^= " << p.tile_bytes << "u; }\n";
   };
   const int depth = std::max(1, std::min(2, planner_knob("smem_jit_depth", 1)));
+  const bool pdl = planner_knob("pdl", 1) != 0;
+  // programmatic dependent launch: wait for the preceding grid (its writes
+  // visible) before the first global access; let the next grid launch once
+  // this CTA's first loads are issued (its CTAs then wait at their own
+  // griddepcontrol.wait), hiding launch latency and the tail wave
+  if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  long long t = t0 + gid;\n";
   if (depth == 1) {
     o << "  long long da = 0;\n  if (t < t1) { tile_off(t); da = dof;\n";
     load("    ", "R");
-    o << "  }\n  for (; t < t1; t += n_groups) {\n";
+    o << "  }\n";
+    if (pdl) o << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+    o << "  for (; t < t1; t += n_groups) {\n";
     body("R", "da", 1);
     o << "  }\n}\n";
   } else {
@@ -703,8 +712,26 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
   void* d = dst;
   void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
                   (void*)&ss, (void*)&ds};
-  if (launch(fn, (unsigned)grid, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr) !=
-      CUDA_SUCCESS) {
+  static PFN_LaunchEx launch_ex = entry<PFN_LaunchEx>("cuLaunchKernelEx");
+  CUresult r;
+  if (planner_knob("pdl", 1) && launch_ex) {
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg = {};
+    cfg.gridDimX = (unsigned)grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = 256;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)smem;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    r = launch_ex(&cfg, fn, args, nullptr);
+  } else {
+    r = launch(fn, (unsigned)grid, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr);
+  }
+  if (r != CUDA_SUCCESS) {
     *err = "cuLaunchKernel failed";
     return cudaErrorLaunchFailure;
   }

@@ -152,7 +152,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "regs_shuffle_max_rounds" && name != "shuffle_jit" && name != "shuffle_jit_tpg" &&
       name != "auto_shuffle" && name != "smem_jit" && name != "smem_jit_tpg" &&
       name != "upcast_jit" && name != "upcast_jit_tpg" && name != "smem_jit_minb" &&
-      name != "regs_trans" && name != "smem_jit_depth" && name != "jit_force_fail")
+      name != "regs_trans" && name != "smem_jit_depth" && name != "jit_force_fail" &&
+      name != "pdl")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
