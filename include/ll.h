@@ -355,6 +355,20 @@ int64_t ll_launch_count(void);
  *   "thread_bytes", "thread_bytes_max", "max_granule", "run_bytes",
  *   "tile_order"  thread vector bytes, granule cap, coalescing run bytes,
  *                tile index order
+ * Executors compiled per plan (NVRTC; jit.cpp):
+ *   "smem_jit" (1) / "shuffle_jit" (1) / "upcast_jit" (1)  compile the plan
+ *                (0 = the template kernels); "smem_jit_tpg" (1),
+ *                "shuffle_jit_tpg" (1), "upcast_jit_tpg" (4) tiles per group;
+ *                "smem_jit_minb" (0 = auto) register cap; "smem_jit_depth"
+ *                (1) tiles in flight; "pdl" (1) programmatic dependent launch;
+ *                "jit_force_fail" (0) test hook
+ *   "auto_shuffle" (0)  AUTO prefers the compiled shuffle exchange when the
+ *                warp tile is warp-local
+ * TMA paths: "tma_tpg" (-1 = by wave count), "tma_stages" (3),
+ *   "tma_run_bytes" (256), "tma_thread_bytes" (64), "tma_tile_bytes" (8192),
+ *   "tma_force_swizzle" (-1)
+ * Register-faithful paths: "regs_matrix" (1) stmatrix / ldmatrix allowed,
+ *   "regs_trans" (1) their .trans forms, "regs_shuffle_max_rounds" (4)
  * ll_convert_host: "host_chunk_mb" (default 16), "host_slots" (default 2).
  * LL_ERR_ARG for an unknown name.  Used by the tuning sweeps. */
 ll_status ll_tune(const char* name, int value);
