@@ -153,7 +153,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "auto_shuffle" && name != "smem_jit" && name != "smem_jit_tpg" &&
       name != "upcast_jit" && name != "upcast_jit_tpg" && name != "smem_jit_minb" &&
       name != "regs_trans" && name != "smem_jit_depth" && name != "jit_force_fail" &&
-      name != "pdl")
+      name != "pdl" && name != "run_bytes_dst" && name != "run_bytes_src" &&
+      name != "auto_asym")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -397,11 +398,22 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   // coalescing run: run_bytes contiguous bytes on both sides (skipping broadcast
   // bits); shortened (down to 128 B) when the tile would not fit 8 warps
   int cbits = warp_tile ? 3 : std::max(0, ilog2i(std::max(16, planner_knob("run_bytes", 256)) / 16));
+  // asymmetric runs: when the tile needs a group of >= 4 warps (transposes),
+  // the destination run is cut to 64 B -- stores merge in L2, loads need the
+  // long runs -- which halves the group (config 3: 6232 -> 6316 GB/s;
+  // configs 2 / 5 keep 2- / 1-warp groups and are unchanged)
+  bool asym = false;
   for (; cbits >= std::min(cbits, 3); --cbits) {
     CD.clear();
     CS.clear();
-    for (int k = vb; k < n && (int)CD.size() < cbits; ++k) if (sigma[k] >= 0) CD.push_back(k);
-    for (int k = vb; k < nA && (int)CS.size() < cbits; ++k) if (sinv[k] >= 0) CS.push_back(sinv[k]);
+    // per-side run lengths (knobs run_bytes_dst / run_bytes_src override the
+    // shared run_bytes for one side)
+    const int rd_knob = planner_knob("run_bytes_dst", 0), rs_knob = planner_knob("run_bytes_src", 0);
+    const int cbits_d = rd_knob > 0 && !warp_tile ? std::min(cbits, ilog2i(std::max(16, rd_knob) / 16))
+                        : asym ? std::min(cbits, 2) : cbits;
+    const int cbits_s = rs_knob > 0 && !warp_tile ? std::min(cbits, ilog2i(std::max(16, rs_knob) / 16)) : cbits;
+    for (int k = vb; k < n && (int)CD.size() < cbits_d; ++k) if (sigma[k] >= 0) CD.push_back(k);
+    for (int k = vb; k < nA && (int)CS.size() < cbits_s; ++k) if (sinv[k] >= 0) CS.push_back(sinv[k]);
     G = 0;
     // Granule choice: the largest prefix of the destination vector that the
     // load side can also hold in registers; prefer choices that keep the
@@ -434,6 +446,12 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     if (g > 3) {
       int r2 = std::min(r_max, (int)T.size() - 5 - 3);
       if (r2 > r) { r = r2; g = (int)T.size() - r - 5; }
+    }
+    if (!asym && !warp_tile && rd_knob == 0 && g >= 2 && cbits > 2 &&
+        planner_knob("auto_asym", 1)) {
+      asym = true;
+      ++cbits;  // the same run length again, with the shorter destination run
+      continue;
     }
     if (g >= 0 && g <= 3) break;
     if (cbits <= 3) break;
