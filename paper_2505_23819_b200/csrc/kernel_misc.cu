@@ -51,20 +51,21 @@ __global__ void __launch_bounds__(256) convert_generic_kernel(const __grid_const
 // Direct gather: each thread produces one 16-byte output vector; source
 // elements are read through L1 (the rows a warp gathers from are the rows it
 // covers, so L1 absorbs the reuse).  Works for any axis placement.
-template <int W>
+template <int W, bool V2 = false>
 __global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constant__ GatherPlan p,
                                                             const uint8_t* __restrict__ src,
                                                             const int32_t* __restrict__ idx,
                                                             uint8_t* __restrict__ out,
                                                             int* __restrict__ err) {
-  constexpr int NE = 16 / W;
+  constexpr int NE = (V2 ? 32 : 16) / W;   // elements per thread per iteration
   constexpr int VB = ilog2(NE);
   using T = typename std::conditional<W == 1, uint8_t,
             typename std::conditional<W == 2, uint16_t,
             typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
   const int64_t per_batch = int64_t(1) << (p.nbits - VB);
   const uint32_t amask = (1u << p.ax_bits) - 1;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n_vec;
+  const int64_t n_units = V2 ? (p.n_vec >> 1) : p.n_vec;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_units;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = v / per_batch;
     const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
@@ -85,7 +86,8 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constan
       for (int q = 0; q < NE; ++q) iv[q] = __ldg(ip + q);
     }
     union {
-      uint4 v4;
+      uint4 v4[NE * W / 16];
+      uint32_t w[NE * W / 4];
       T e[NE];
     } o;
     // axis coordinate of h0's elements and the "cleared" base
@@ -111,7 +113,16 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constan
       }
       o.e[e] = __ldg(s + hs);
     }
-    *reinterpret_cast<uint4*>(reinterpret_cast<T*>(out) + b * p.batch_stride + h0) = o.v4;
+    T* op = reinterpret_cast<T*>(out) + b * p.batch_stride + h0;
+    if constexpr (V2) {
+      // sm_100 256-bit store of the thread's 32 output bytes
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(op), "r"(o.w[0]),
+                   "r"(o.w[1]), "r"(o.w[2]), "r"(o.w[3]), "r"(o.w[4]), "r"(o.w[5]), "r"(o.w[6]),
+                   "r"(o.w[7])
+                   : "memory");
+    } else {
+      *reinterpret_cast<uint4*>(op) = o.v4[0];
+    }
   }
 }
 
@@ -259,7 +270,8 @@ LaunchKnobs::LaunchKnobs()
         gather_tpt(env_int("LL_GATHER_VPT", 0)), carveout(env_int("LL_CARVEOUT", -1)),
         pow2(env_int("LL_POW2", 0)), stages(env_int("LL_STAGES", 3)),
         async_tpg(env_int("LL_ASYNC_TPG", 8)), up_tpg(env_int("LL_UP_TPG", 0)),
-        tma_tpg(env_int("LL_TMA_TPG", -1)), tma_stages(env_int("LL_TMA_STAGES", 3)) {}
+        tma_tpg(env_int("LL_TMA_TPG", -1)), tma_stages(env_int("LL_TMA_STAGES", 3)),
+        gather_v8(env_int("LL_GATHER_V8", 0)) {}
 LaunchKnobs& knobs() {
   static LaunchKnobs k;
   return k;
@@ -277,6 +289,7 @@ int set_knob(const char* name, int value) {
   if (n == "up_tpg") { knobs().up_tpg = value; return 0; }
   if (n == "tma_tpg") { knobs().tma_tpg = value; return 0; }
   if (n == "tma_stages") { knobs().tma_stages = value; return 0; }
+  if (n == "gather_v8") { knobs().gather_v8 = value; return 0; }
   return -1;
 }
 
@@ -323,8 +336,22 @@ static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void
     gather_shuffle_kernel<W, false><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx,
                                                              (uint8_t*)out, err);
   else
-    gather_direct_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
-                                                     err);
+  {
+    // 32 bytes per thread (256-bit stores) when every batch holds an even
+    // number of 16-byte vectors (knob gather_v8)
+    const bool v2 = knobs().gather_v8 && (p.nbits - ilog2(16 / W)) >= 1 &&
+                    (reinterpret_cast<uintptr_t>(out) & 31) == 0;
+    if (v2) {
+      int64_t want2 = ((p.n_vec >> 1) + (int64_t)threads * vpt - 1) / ((int64_t)threads * vpt);
+      if (max_ctas > 0 && want2 > max_ctas) want2 = max_ctas;
+      const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>(want2, 0x7fffffff));
+      gather_direct_kernel<W, true><<<grid2, threads, 0, st>>>(p, (const uint8_t*)src, idx,
+                                                              (uint8_t*)out, err);
+    } else {
+      gather_direct_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
+                                                       err);
+    }
+  }
   return cudaGetLastError();
 }
 
