@@ -266,7 +266,12 @@ bool plan_tma(ConvertPlan& P, const std::vector<u64>& X, std::ostringstream& js)
   std::vector<int> VD, VS, CD, CS;
   for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
   const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("tma_run_bytes", 256)) / 16));
-  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
+  // destination run (knob tma_run_bytes_dst; the stores are merged in L2)
+  const int cbits_d = planner_knob("tma_run_bytes_dst", 0) > 0
+                          ? std::min(cbits, ilog2i(std::max(16, planner_knob("tma_run_bytes_dst", 0)) / 16))
+                          : cbits;
+  for (int k = vb; k < std::min(n, vb + cbits_d); ++k) CD.push_back(k);
+  for (int k = vb; k < std::min(n, vb + cbits); ++k) CS.push_back(sinv[k]);
   const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
   const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("tma_thread_bytes", 64)) / w));
   std::vector<int> need = VS;
@@ -545,7 +550,12 @@ bool plan_tma_store(ConvertPlan& P, const std::vector<u64>& X, std::ostringstrea
   std::vector<int> VD, VS, CD, CS;
   for (int k = 0; k < vb; ++k) { VD.push_back(k); VS.push_back(sinv[k]); }
   const int cbits = std::max(0, ilog2i(std::max(16, planner_knob("tma_run_bytes", 256)) / 16));
-  for (int k = vb; k < std::min(n, vb + cbits); ++k) { CD.push_back(k); CS.push_back(sinv[k]); }
+  // destination run (knob tma_run_bytes_dst; the stores are merged in L2)
+  const int cbits_d = planner_knob("tma_run_bytes_dst", 0) > 0
+                          ? std::min(cbits, ilog2i(std::max(16, planner_knob("tma_run_bytes_dst", 0)) / 16))
+                          : cbits;
+  for (int k = vb; k < std::min(n, vb + cbits_d); ++k) CD.push_back(k);
+  for (int k = vb; k < std::min(n, vb + cbits); ++k) CS.push_back(sinv[k]);
   const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
   const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("tma_thread_bytes", 64)) / w));
   std::vector<int> need = VS;
