@@ -360,7 +360,9 @@ int64_t ll_launch_count(void);
  *                (0 = the template kernels); "smem_jit_tpg" (1),
  *                "shuffle_jit_tpg" (1), "upcast_jit_tpg" (4) tiles per group;
  *                "smem_jit_minb" (0 = auto) register cap; "smem_jit_depth"
- *                (1) tiles in flight; "pdl" (1) programmatic dependent launch;
+ *                (1) tiles in flight; "smem_jit_single" (0) one staging
+ *                buffer per group when each group has one tile; "pdl" (1)
+ *                programmatic dependent launch;
  *                "jit_force_fail" (0) test hook
  *   "auto_shuffle" (0)  AUTO prefers the compiled shuffle exchange when the
  *                warp tile is warp-local

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -228,7 +230,11 @@ int deposit_word_h(int j, int k, int LB, int A, int B) {
 // plan: the same schedule as convert_smem_kernel (software-pipelined loads,
 // swizzled STS, group barrier, LDS, streaming stores), with every offset,
 // granule operand and register permutation a compile-time constant.
-std::string smem_hbm_source(const ConvertPlan& P) {
+//
+// single: every group converts exactly one tile (the launch has at least as
+// many groups as tiles), so the group needs one staging buffer instead of
+// two and no prefetch; half the shared memory per CTA.
+std::string smem_hbm_source(const ConvertPlan& P, bool single) {
   const SmemPlan& p = P.sp;
   const int W = P.w, NV = P.nv, NW = NV * 4, G = P.g, GWd = G / 4, NG = NV * 16 / G;
   const int gw = p.gw, LB = ilog2i(NW);
@@ -256,7 +262,7 @@ std::string smem_hbm_source(const ConvertPlan& P) {
     << "  unsigned char* dthr = dst + st_off - dst_shift;\n"
     << "  const long long rmask = (1LL << tm.n_bits) - 1;\n"
     << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + group * "
-    << 2 * p.tile_bytes << "u;\n"
+    << (single ? 1 : 2) * p.tile_bytes << "u;\n"
     << "  unsigned buf = 0;\n  unsigned R[" << NW << "], Q[" << NW << "];\n"
     << "  long long so = 0, dof = 0;\n"
     << "  auto tile_off = [&](long long t) {\n"
@@ -287,10 +293,12 @@ std::string smem_hbm_source(const ConvertPlan& P) {
       for (int k = 0; k < GWd; ++k) o << ", \"r\"(" << R << "[" << deposit_word_h(j, k, LB, ga, gb) << "])";
       o << " : \"memory\");\n";
     }
-    o << "    { const long long tn = t + " << ahead << " * n_groups; if (tn < t1) { tile_off(tn); "
-      << dv << " = dof;\n";
-    load("      ", R);
-    o << "    } }\n";
+    if (ahead > 0) {
+      o << "    { const long long tn = t + " << ahead << " * n_groups; if (tn < t1) { tile_off(tn); "
+        << dv << " = dof;\n";
+      load("      ", R);
+      o << "    } }\n";
+    }
     if (gw == 0) o << "    __syncwarp();\n";
     else o << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(group + 1), \"r\"(" << (32 << gw) << ") : \"memory\");\n";
     for (int j = 0; j < NG; ++j) {
@@ -315,7 +323,13 @@ std::string smem_hbm_source(const ConvertPlan& P) {
   // griddepcontrol.wait), hiding launch latency and the tail wave
   if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  long long t = t0 + gid;\n";
-  if (depth == 1) {
+  if (single) {
+    o << "  if (t >= t1) return;\n  tile_off(t);\n  long long da = dof;\n";
+    load("  ", "R");
+    if (pdl) o << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+    body("R", "da", 0);
+    o << "}\n";
+  } else if (depth == 1) {
     o << "  long long da = 0;\n  if (t < t1) { tile_off(t); da = dof;\n";
     load("    ", "R");
     o << "  }\n";
@@ -515,11 +529,26 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
   static PFN_GetFunction getf = entry<PFN_GetFunction>("cuModuleGetFunction");
   if (!load || !getf) return failed("driver entry points unavailable");
   cudaFree(nullptr);  // make sure the runtime's primary context is current
+  // LL_JIT_SOURCE_DIR: write each generated source there and name the
+  // program after it, so the line table (-lineinfo) points at a real file
+  // and `ncu --import-source on` can show the generated code.
+  std::string pname = "ll_jit.cu";
+  if (const char* dir = std::getenv("LL_JIT_SOURCE_DIR")) {
+    unsigned long long h = 1469598103934665603ull;
+    for (unsigned char c : src) h = (h ^ c) * 1099511628211ull;
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "/%s_%016llx.cu", name, h);
+    pname = std::string(dir) + buf;
+    if (FILE* f = std::fopen(pname.c_str(), "w")) {
+      std::fwrite(src.data(), 1, src.size(), f);
+      std::fclose(f);
+    }
+  }
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "ll_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+  if (nvrtcCreateProgram(&prog, src.c_str(), pname.c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return failed("nvrtcCreateProgram failed");
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device", "-lineinfo"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
@@ -628,7 +657,9 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
 }
 
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P) { return shuffle_hbm_source(P); }
-std::string smem_hbm_kernel_source(const ConvertPlan& P) { return smem_hbm_source(P); }
+std::string smem_hbm_kernel_source(const ConvertPlan& P) {
+  return smem_hbm_source(P, planner_knob("smem_jit_single", 0) != 0);
+}
 std::string upcast_hbm_kernel_source(const ConvertPlan& P) { return upcast_hbm_source(P); }
 
 cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
@@ -685,17 +716,12 @@ cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
 cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
                             cudaStream_t st, const TileRange& rg, std::string* err) {
   if (P.sp.pad || P.op != 0) return cudaErrorInvalidValue;
-  CUfunction fn = nullptr;
-  cudaError_t e = get_kernel(smem_hbm_source(P), &fn, err, "ll_smem_hbm");
-  if (e != cudaSuccess) return e;
   static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
   static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
   if (!launch || !setattr) return cudaErrorNotSupported;
   const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;
   const int gpc = 8 >> P.sp.gw;
-  const int smem = gpc * 2 * P.sp.tile_bytes;
-  if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
   const int tpg = planner_knob("smem_jit_tpg", 1);  // sweep: 1 > 2 > 4
   int sms = 148;
   {
@@ -707,6 +733,12 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
   if (max_ctas > 0) groups = std::min<int64_t>(groups, (int64_t)max_ctas * gpc);
   groups = std::max<int64_t>(1, std::min<int64_t>(groups, n_tiles));
   const int64_t grid = (groups + gpc - 1) / gpc;
+  const bool single = groups >= n_tiles && planner_knob("smem_jit_single", 0);
+  CUfunction fn = nullptr;
+  cudaError_t e = get_kernel(smem_hbm_source(P, single), &fn, err, "ll_smem_hbm");
+  if (e != cudaSuccess) return e;
+  const int smem = gpc * (single ? 1 : 2) * P.sp.tile_bytes;
+  if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   const void* s = src;
   void* d = dst;

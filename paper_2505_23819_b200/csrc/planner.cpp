@@ -152,7 +152,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "regs_shuffle_max_rounds" && name != "shuffle_jit" && name != "shuffle_jit_tpg" &&
       name != "auto_shuffle" && name != "smem_jit" && name != "smem_jit_tpg" &&
       name != "upcast_jit" && name != "upcast_jit_tpg" && name != "smem_jit_minb" &&
-      name != "regs_trans" && name != "smem_jit_depth" && name != "jit_force_fail" &&
+      name != "regs_trans" && name != "smem_jit_depth" && name != "smem_jit_single" && name != "jit_force_fail" &&
       name != "pdl" && name != "run_bytes_dst" && name != "run_bytes_src" &&
       name != "auto_asym" && name != "tma_run_bytes_dst")
     return false;

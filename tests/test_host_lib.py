@@ -498,6 +498,22 @@ def test_shuffle_hbm_kernel_specialises_and_compiles():
         assert ll.jit_source(A, B, 8 * c["elem_bytes"], compile=True, kernel="shuffle")["compiled"]
 
 
+def test_smem_hbm_single_buffer_variant_compiles():
+    """smem_jit_single: the compiled smem kernel with one staging buffer per
+    group (no prefetch) is a different source, and NVRTC compiles both."""
+    c = configs.cfg3(n_bits=9)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    two = ll.jit_source(A, B, 16, kernel="smem")
+    try:
+        ll.tune("smem_jit_single", 1)
+        one = ll.jit_source(A, B, 16, kernel="smem")
+        assert one != two and "n_groups; if (tn < t1)" not in one
+        assert ll.jit_source(A, B, 16, compile=True, kernel="smem")["compiled"]
+    finally:
+        ll.tune("smem_jit_single", 0)
+    assert "n_groups; if (tn < t1)" in two
+
+
 def test_regs_trans_tile_divides():
     """The .trans lowering: on an mma-fragment / transposed-fragment pair the
     planner writes with stmatrix.trans and reads with ldmatrix, and the
