@@ -348,6 +348,8 @@ int64_t ll_launch_count(void);
  *                default 0 = persistent)
  *   "gather_vpt" 16-byte output vectors per thread of the gather kernels
  *                (env LL_GATHER_VPT; 0 = per path: shuffle 4, direct 1)
+ *   "gather_shfl_u" warp-vectors whose loads the shuffle gather issues
+ *                before its first shuffle (1, 2 or 4; default 2)
  *   "carveout", "pow2", "stages", "async_tpg"  ablation knobs of the smem /
  *                cp.async kernels (env LL_CARVEOUT, LL_POW2, LL_STAGES,
  *                LL_ASYNC_TPG)

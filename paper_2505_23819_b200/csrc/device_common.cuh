@@ -417,7 +417,8 @@ int num_sms();
 // kernel's max dynamic smem (220 KB) and carveout (if != -1) are set first.
 int cached_occupancy(const void* kernel, int threads, size_t smem, int carveout);
 struct LaunchKnobs {
-  int tpg, pipe, gather_tpt, carveout, pow2, stages, async_tpg, up_tpg, tma_tpg, tma_stages, gather_v8;
+  int tpg, pipe, gather_tpt, carveout, pow2, stages, async_tpg, up_tpg, tma_tpg, tma_stages, gather_v8,
+      gather_shfl_u;
   LaunchKnobs();
 };
 LaunchKnobs& knobs();

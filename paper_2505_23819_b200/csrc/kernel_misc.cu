@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constan
 // matches.  Requires the axis to live in the warp's buffer bits (vb + 5).
 // ALLC: the axis covers every register bit (cand_mask = NE-1): all NE words
 // are shuffled from the source lane and a select tree picks the element.
-template <int W, bool ALLC>
+template <int W, bool ALLC, int U = 1>
 __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_constant__ GatherPlan p,
                                                              const uint8_t* __restrict__ src,
                                                              const int32_t* __restrict__ idx,
@@ -152,75 +152,93 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
   const int64_t n_wvec = p.n_vec >> 5;  // warps' worth of vectors
   const uint32_t clear32 = ~(uint32_t)p.axis_mask_buf;
   const int ybase = p.y_base;
-  for (int64_t wv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wv < n_wvec;
-       wv += nwarps_total) {
-    const int64_t v = (wv << 5) | lane;
-    const int64_t b = v / per_batch;
-    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
-    const uint8_t* sbase = src + (b * p.batch_stride) * W;
-    union {
-      uint4 v4;
-      T e[NE];
-      uint32_t w[4];
-    } sv, o;
-    sv.v4 = ldg_stream(sbase + h0 * W);
-    const int32_t* ip = idx + b * p.batch_stride + h0;
-    int32_t iv[NE];
-    if constexpr (NE >= 4) {
+  union V {
+    uint4 v4;
+    T e[NE];
+    uint32_t w[4];
+  };
+  // U warp-vectors per iteration: all their loads are issued before the
+  // first shuffle (U = 1: the plain loop)
+  for (int64_t wv0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wv0 < n_wvec;
+       wv0 += nwarps_total * U) {
+    V sv[U];
+    int32_t iv[U][NE];
+    int64_t vv[U];
 #pragma unroll
-      for (int q = 0; q < NE / 4; ++q) {
-        int4 t = __ldg(reinterpret_cast<const int4*>(ip) + q);
-        iv[4 * q] = t.x; iv[4 * q + 1] = t.y; iv[4 * q + 2] = t.z; iv[4 * q + 3] = t.w;
-      }
-    } else {
+    for (int u = 0; u < U; ++u) {
+      const int64_t wv = wv0 + (int64_t)u * nwarps_total;
+      vv[u] = -1;
+      if (wv >= n_wvec) continue;  // warp-uniform
+      const int64_t v = (wv << 5) | lane;
+      vv[u] = v;
+      const int64_t b = v / per_batch;
+      const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+      sv[u].v4 = ldg_stream(src + (b * p.batch_stride + h0) * W);
+      const int32_t* ip = idx + b * p.batch_stride + h0;
+      if constexpr (NE >= 4) {
 #pragma unroll
-      for (int q = 0; q < NE; ++q) iv[q] = __ldg(ip + q);
-    }
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      // only the warp-local bits (VB + 5) of h* matter here: 32-bit arithmetic
-      uint32_t i = (uint32_t)iv[e];
-      if (p.check && i > amask) atomicExch(err, 1);
-      i &= amask;
-      const uint32_t hl = (((uint32_t)lane << VB) | (uint32_t)e) & clear32;
-      const uint32_t hs = hl | (i << ybase);
-      const int src_lane = (int)((hs >> VB) & 31);
-      const int src_reg = (int)(hs & (NE - 1));
-      if constexpr (ALLC && W == 4) {
-        // four shuffles, then a 2-level select on the register index
-        const uint32_t g0 = __shfl_sync(0xffffffffu, sv.w[0], src_lane);
-        const uint32_t g1 = __shfl_sync(0xffffffffu, sv.w[1], src_lane);
-        const uint32_t g2 = __shfl_sync(0xffffffffu, sv.w[2], src_lane);
-        const uint32_t g3 = __shfl_sync(0xffffffffu, sv.w[3], src_lane);
-        const uint32_t lo = (src_reg & 1) ? g1 : g0;
-        const uint32_t hi = (src_reg & 1) ? g3 : g2;
-        o.e[e] = (T)((src_reg & 2) ? hi : lo);
-      } else {
-        T val = 0;
-        // candidate rounds: every register index the axis can select, i.e. the
-        // registers that agree with e outside cand_mask (2^|L_reg^axis| shuffles)
-#pragma unroll
-        for (int c = 0; c < NE; ++c) {
-          if (ALLC || ((c ^ e) & ~p.cand_mask) == 0) {
-            T got;
-            if constexpr (W == 8) {
-              uint32_t lo = __shfl_sync(0xffffffffu, sv.w[2 * c], src_lane);
-              uint32_t hi = __shfl_sync(0xffffffffu, sv.w[2 * c + 1], src_lane);
-              got = (T)(((uint64_t)hi << 32) | lo);
-            } else if constexpr (W == 4) {
-              got = (T)__shfl_sync(0xffffffffu, sv.w[c], src_lane);
-            } else {
-              // sub-word elements: shuffle the containing word, then extract
-              uint32_t wd = __shfl_sync(0xffffffffu, sv.w[(c * W) >> 2], src_lane);
-              got = (T)(wd >> (((c * W) & 3) * 8));
-            }
-            if (src_reg == c) val = got;
-          }
+        for (int q = 0; q < NE / 4; ++q) {
+          int4 t = __ldg(reinterpret_cast<const int4*>(ip) + q);
+          iv[u][4 * q] = t.x; iv[u][4 * q + 1] = t.y; iv[u][4 * q + 2] = t.z; iv[u][4 * q + 3] = t.w;
         }
-        o.e[e] = val;
+      } else {
+#pragma unroll
+        for (int q = 0; q < NE; ++q) iv[u][q] = __ldg(ip + q);
       }
     }
-    stg_stream(out + (b * p.batch_stride + h0) * W, o.v4);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (vv[u] < 0) continue;
+      const int64_t v = vv[u];
+      const int64_t b = v / per_batch;
+      const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+      V o;
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        // only the warp-local bits (VB + 5) of h* matter here: 32-bit arithmetic
+        uint32_t i = (uint32_t)iv[u][e];
+        if (p.check && i > amask) atomicExch(err, 1);
+        i &= amask;
+        const uint32_t hl = (((uint32_t)lane << VB) | (uint32_t)e) & clear32;
+        const uint32_t hs = hl | (i << ybase);
+        const int src_lane = (int)((hs >> VB) & 31);
+        const int src_reg = (int)(hs & (NE - 1));
+        if constexpr (ALLC && W == 4) {
+          // four shuffles, then a 2-level select on the register index
+          const uint32_t g0 = __shfl_sync(0xffffffffu, sv[u].w[0], src_lane);
+          const uint32_t g1 = __shfl_sync(0xffffffffu, sv[u].w[1], src_lane);
+          const uint32_t g2 = __shfl_sync(0xffffffffu, sv[u].w[2], src_lane);
+          const uint32_t g3 = __shfl_sync(0xffffffffu, sv[u].w[3], src_lane);
+          const uint32_t lo = (src_reg & 1) ? g1 : g0;
+          const uint32_t hi = (src_reg & 1) ? g3 : g2;
+          o.e[e] = (T)((src_reg & 2) ? hi : lo);
+        } else {
+          T val = 0;
+          // candidate rounds: every register index the axis can select, i.e. the
+          // registers that agree with e outside cand_mask (2^|L_reg^axis| shuffles)
+#pragma unroll
+          for (int c = 0; c < NE; ++c) {
+            if (ALLC || ((c ^ e) & ~p.cand_mask) == 0) {
+              T got;
+              if constexpr (W == 8) {
+                uint32_t lo = __shfl_sync(0xffffffffu, sv[u].w[2 * c], src_lane);
+                uint32_t hi = __shfl_sync(0xffffffffu, sv[u].w[2 * c + 1], src_lane);
+                got = (T)(((uint64_t)hi << 32) | lo);
+              } else if constexpr (W == 4) {
+                got = (T)__shfl_sync(0xffffffffu, sv[u].w[c], src_lane);
+              } else {
+                // sub-word elements: shuffle the containing word, then extract
+                uint32_t wd = __shfl_sync(0xffffffffu, sv[u].w[(c * W) >> 2], src_lane);
+                got = (T)(wd >> (((c * W) & 3) * 8));
+              }
+              if (src_reg == c) val = got;
+            }
+          }
+          o.e[e] = val;
+        }
+      }
+      stg_stream(out + (b * p.batch_stride + h0) * W, o.v4);
+    }
   }
 }
 
@@ -271,7 +289,7 @@ LaunchKnobs::LaunchKnobs()
         pow2(env_int("LL_POW2", 0)), stages(env_int("LL_STAGES", 3)),
         async_tpg(env_int("LL_ASYNC_TPG", 8)), up_tpg(env_int("LL_UP_TPG", 0)),
         tma_tpg(env_int("LL_TMA_TPG", -1)), tma_stages(env_int("LL_TMA_STAGES", 3)),
-        gather_v8(env_int("LL_GATHER_V8", 0)) {}
+        gather_v8(env_int("LL_GATHER_V8", 0)), gather_shfl_u(2) {}
 LaunchKnobs& knobs() {
   static LaunchKnobs k;
   return k;
@@ -290,6 +308,7 @@ int set_knob(const char* name, int value) {
   if (n == "tma_tpg") { knobs().tma_tpg = value; return 0; }
   if (n == "tma_stages") { knobs().tma_stages = value; return 0; }
   if (n == "gather_v8") { knobs().gather_v8 = value; return 0; }
+  if (n == "gather_shfl_u") { knobs().gather_shfl_u = value; return 0; }
   return -1;
 }
 
@@ -329,13 +348,17 @@ static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void
   if (max_ctas > 0 && want > max_ctas) want = max_ctas;
   int grid = (int)(want < 0x7fffffff ? want : 0x7fffffff);
   if (grid < 1) grid = 1;
-  if (shuffle && p.cand_mask == (16 / W) - 1)
-    gather_shuffle_kernel<W, true><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx,
-                                                            (uint8_t*)out, err);
-  else if (shuffle)
-    gather_shuffle_kernel<W, false><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx,
-                                                             (uint8_t*)out, err);
-  else
+  if (shuffle) {
+    // warp-vectors whose loads are in flight together (knob gather_shfl_u)
+    const int u = knobs().gather_shfl_u;
+    const bool allc = p.cand_mask == (16 / W) - 1;
+    auto go = [&](auto kern) {
+      kern<<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out, err);
+    };
+    if (u >= 4) allc ? go(gather_shuffle_kernel<W, true, 4>) : go(gather_shuffle_kernel<W, false, 4>);
+    else if (u == 2) allc ? go(gather_shuffle_kernel<W, true, 2>) : go(gather_shuffle_kernel<W, false, 2>);
+    else allc ? go(gather_shuffle_kernel<W, true, 1>) : go(gather_shuffle_kernel<W, false, 1>);
+  } else
   {
     // 32 bytes per thread (256-bit stores) when every batch holds an even
     // number of 16-byte vectors (knob gather_v8)

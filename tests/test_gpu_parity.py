@@ -361,6 +361,26 @@ def test_gather_other_widths(w):
         assert out.tobytes() == exp.tobytes(), (w, path)
 
 
+@pytest.mark.parametrize("u", [1, 4])
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_gather_shuffle_vectors_in_flight(w, u):
+    """Knob gather_shfl_u=u: the shuffle gather issues u warp-vectors'
+    loads before the first shuffle; same bytes, including a ragged last
+    iteration (warp-vectors not a multiple of u per grid stride)."""
+    try:
+        ll.tune("gather_shfl_u", u)
+        for r_bits, batch in ((0, 1), (3, 3)):
+            c = dict(configs.cfg4(r_bits=r_bits), elem_bytes=w)
+            src, idx, out = run_gather(c, "shuffle", batch=batch)
+            n = src.size // batch
+            for k in range(batch):
+                exp = oconv.gather_np(src[k * n:(k + 1) * n], idx[k * n:(k + 1) * n],
+                                      _olayout(c["L"]), c["axis"])
+                assert out[k * n:(k + 1) * n].tobytes() == exp.tobytes(), (w, r_bits, k)
+    finally:
+        ll.tune("gather_shfl_u", 2)
+
+
 def test_gather_full_size_sampled():
     c = configs.cfg4()
     w = 4
