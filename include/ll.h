@@ -294,6 +294,17 @@ ll_status ll_convert_shard(const void* src_slice, ll_layout src_layout, void* ds
 ll_status ll_shard_describe(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
                             int n_shards, int shard, int64_t* out4);
 
+/* Pitched shard (used by ll_convert_host for layouts that have no
+ * contiguous-on-both-sides split, e.g. a transpose): shard `shard` of
+ * `n_shards` (a power of two >= 2) is a contiguous slice of one buffer and,
+ * in the other, the elements whose index bits [r0, r0 + log2 n_shards) equal
+ * `shard` -- rows of elem_bytes << r0 bytes at a pitch of n_shards times
+ * that.  out6 = {side (0: src contiguous / dst pitched, 1: the reverse), r0,
+ * contiguous-side begin, end (bytes), pitched-side row bytes, pitch bytes}.
+ * LL_ERR_UNSUPPORTED when the plan's top tile bits do not allow it. */
+ll_status ll_shard_describe_2d(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
+                               int n_shards, int shard, int64_t* out6);
+
 /* Checksum of a device buffer (untimed; ours -- the
  * paper has no such step): the 64-bit sum, mod 2^64, over elements h of
  *     fmix( v_h + (index_base + h + 1) * 0x9E3779B97F4A7C15 )     (indexed)
@@ -314,12 +325,15 @@ ll_status ll_checksum(const void* buf, int64_t n_elems, int elem_bits, int index
 /* End-to-end conversion of HOST buffers: src_host/dst_host are host pointers
  * (pinned for full speed); the library pipelines host->device copies, the
  * conversion and device->host copies in chunks (~16 MiB: whole layout
- * instances, or shards of a single large instance) over a copy-in, a compute
+ * instances, or shards of a single large instance -- contiguous in both
+ * buffers, else contiguous in one and pitched in the other (ll_shard_describe_2d;
+ * the pitched side is then staged whole in its scratch buffer and copied
+ * with 2-D copies of >= 1 KiB rows)) over a copy-in, a compute
  * and a copy-out stream of its own, rotating 2 slots (knob: up to 4) of the caller's
  * device scratch buffers dev_src/dev_dst of scratch_bytes each (>= one
  * chunk).  Ordered after work already queued on `stream`; synchronous:
  * returns when dst_host is complete.  Knobs (ll_tune): "host_chunk_mb",
- * "host_slots". */
+ * "host_slots", "host_2d" (1: pitched shards allowed). */
 ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_host,
                           ll_layout dst_layout, int elem_bits, int64_t batch, void* dev_src,
                           void* dev_dst, size_t scratch_bytes, ll_stream stream);

@@ -380,7 +380,7 @@ HostPipe& host_pipe() {
 namespace {
 ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
                       int elem_bits, const ll_convert_options* opts, ll_stream stream,
-                      int n_shards, int shard) {
+                      int n_shards, int shard, const ll::TileRange* rg_in = nullptr) {
   check_layout(src_layout, "ll_convert");
   check_layout(dst_layout, "ll_convert");
   const int w = elem_bytes(elem_bits);
@@ -393,7 +393,9 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
   auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, path_req, batch);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ll::TileRange rg{0, 0, 0, 0};
-  if (n_shards > 1) {
+  if (rg_in) {
+    rg = *rg_in;
+  } else if (n_shards > 1) {
     rg = ll::shard_range(*P, n_shards, shard);
   } else if (P->path == LL_PATH_SMEM || P->path == LL_PATH_SMEM_NOSWIZZLE ||
              P->path == LL_PATH_SMEM_ASYNC || P->path == LL_PATH_SMEM_PADDED ||
@@ -628,6 +630,27 @@ ll_status ll_shard_describe(ll_layout src_layout, ll_layout dst_layout, int elem
   });
 }
 
+ll_status ll_shard_describe_2d(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
+                               int n_shards, int shard, int64_t* out6) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_shard_describe_2d");
+    check_layout(dst_layout, "ll_shard_describe_2d");
+    if (!out6) return fail(LL_ERR_ARG, "ll_shard_describe_2d: out is NULL");
+    const int w = elem_bytes(elem_bits);
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, path, 1);
+    int side = 0, r0 = 0;
+    auto rg = ll::shard_range_2d(*P, n_shards, shard, &side, &r0);
+    const int64_t slice = ((int64_t)w << (side == 0 ? P->nA : P->nB)) / n_shards;
+    out6[0] = side;
+    out6[1] = r0;
+    out6[2] = side == 0 ? rg.src_shift : rg.dst_shift;
+    out6[3] = out6[2] + slice;
+    out6[4] = (int64_t)w << r0;
+    out6[5] = ((int64_t)w << r0) * n_shards;
+    return LL_OK;
+  });
+}
+
 ll_status ll_convert(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
                      int elem_bits, ll_stream stream) {
   return ll_convert_ex(src, src_layout, dst, dst_layout, elem_bits, nullptr, stream);
@@ -707,6 +730,74 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
           break;
         } catch (const ll::Error&) {
         }
+      }
+    }
+    // a single instance that cannot be cut into slices contiguous in both
+    // buffers (a transpose): shards contiguous on one side and a pitched
+    // region of >= 1 KiB rows on the other, the pitched side staged whole in
+    // its scratch buffer and copied with cudaMemcpy2DAsync
+    if (batch == 1 && unit > cap && n_sh == 1 && ll::planner_knob("host_2d", 1)) {
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
+      int want = 2;
+      while ((unit / want) > cap && want < (1 << 12)) want *= 2;
+      for (int ns = want; ns > 1; ns /= 2) {
+        int side = 0, r0 = 0;
+        try {
+          ll::shard_range_2d(*P, ns, 0, &side, &r0);
+        } catch (const ll::Error&) {
+          continue;
+        }
+        const size_t whole = side == 0 ? db : sb;   // the pitched side
+        const size_t slice = (side == 0 ? sb : db) / ns;
+        const size_t width = (size_t)w << r0;
+        if (width < 1024 || scratch_bytes < whole || scratch_bytes < slice) continue;
+        const size_t pitch = width * ns, height = whole / pitch;
+        const int nslot = (int)std::max<size_t>(1, std::min<size_t>(max_slots, scratch_bytes / slice));
+        HostPipe& hp = host_pipe();
+        std::lock_guard<std::mutex> lk(hp.mu);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        cudaEventRecord(hp.start, st);
+        cudaStreamWaitEvent(hp.h2d, hp.start, 0);
+        cudaStreamWaitEvent(hp.comp, hp.start, 0);
+        cudaStreamWaitEvent(hp.d2h, hp.start, 0);
+        ll_status s = LL_OK;
+        for (int i = 0; i < ns && s == LL_OK; ++i) {
+          const int slot = i % nslot;
+          const ll::TileRange rg = ll::shard_range_2d(*P, ns, i, &side, &r0);
+          char* ds = (char*)dev_src + (side == 0 ? (size_t)slot * slice : 0);
+          char* dd = (char*)dev_dst + (side == 0 ? 0 : (size_t)slot * slice);
+          // the contiguous side's slot is reused every nslot chunks
+          if (side == 0 && i >= nslot) cudaStreamWaitEvent(hp.h2d, hp.ev_comp[slot], 0);
+          if (side == 0)
+            cudaMemcpyAsync(ds, (const char*)src_host + i * slice, slice, cudaMemcpyHostToDevice, hp.h2d);
+          else
+            cudaMemcpy2DAsync(ds + i * width, pitch, (const char*)src_host + i * width, pitch, width,
+                              height, cudaMemcpyHostToDevice, hp.h2d);
+          cudaEventRecord(hp.ev_h2d[slot], hp.h2d);
+          cudaStreamWaitEvent(hp.comp, hp.ev_h2d[slot], 0);
+          if (side == 1 && i >= nslot) cudaStreamWaitEvent(hp.comp, hp.ev_d2h[slot], 0);
+          ll_convert_options o{};
+          o.path = LL_PATH_AUTO;
+          s = guarded([&] {
+            return run_convert(ds, src_layout, dd, dst_layout, elem_bits, &o, (ll_stream)hp.comp,
+                               1, 0, &rg);
+          });
+          cudaEventRecord(hp.ev_comp[slot], hp.comp);
+          cudaStreamWaitEvent(hp.d2h, hp.ev_comp[slot], 0);
+          if (side == 0)
+            cudaMemcpy2DAsync((char*)dst_host + i * width, pitch, dd + i * width, pitch, width, height,
+                              cudaMemcpyDeviceToHost, hp.d2h);
+          else
+            cudaMemcpyAsync((char*)dst_host + i * slice, dd, slice, cudaMemcpyDeviceToHost, hp.d2h);
+          cudaEventRecord(hp.ev_d2h[slot], hp.d2h);
+        }
+        cudaEventRecord(hp.fin[0], hp.h2d);
+        cudaEventRecord(hp.fin[1], hp.comp);
+        cudaEventRecord(hp.fin[2], hp.d2h);
+        for (int k = 0; k < 3; ++k) cudaStreamWaitEvent(st, hp.fin[k], 0);
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (s != LL_OK) return s;
+        return cuda_status(e, "ll_convert_host");
       }
     }
     int64_t n_chunks, per_chunk = 1;

@@ -147,7 +147,7 @@ int planner_knob_version() {
 bool set_planner_knob(const std::string& name, int value) {
   if (name != "thread_bytes" && name != "thread_bytes_max" && name != "max_granule" &&
       name != "run_bytes" && name != "tile_order" && name != "host_chunk_mb" &&
-      name != "host_slots" && name != "tma_run_bytes" && name != "tma_thread_bytes" &&
+      name != "host_slots" && name != "host_2d" && name != "tma_run_bytes" && name != "tma_thread_bytes" &&
       name != "tma_tile_bytes" && name != "tma_force_swizzle" && name != "regs_matrix" &&
       name != "regs_shuffle_max_rounds" && name != "shuffle_jit" && name != "shuffle_jit_tpg" &&
       name != "auto_shuffle" && name != "smem_jit" && name != "smem_jit_tpg" &&
@@ -1044,6 +1044,44 @@ TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
   rg.src_shift = (int64_t)shard * ((w << P.nA) >> sb);
   rg.dst_shift = (int64_t)shard * ((w << P.nB) >> sb);
   return rg;
+}
+
+TileRange shard_range_2d(const ConvertPlan& P, int n_shards, int shard, int* side, int* r0) {
+  if (n_shards < 2 || (n_shards & (n_shards - 1)) || shard < 0 || shard >= n_shards)
+    throw Error(LL_ERR_ARG, "shard_2d: n_shards must be a power of two >= 2 and 0 <= shard < n_shards");
+  int sb = 0;
+  while ((1 << sb) < n_shards) ++sb;
+  if (P.batch != 1) throw Error(LL_ERR_UNSUPPORTED, "shard_2d: batch must be 1");
+  if (P.path != LL_PATH_SMEM && P.path != LL_PATH_SHUFFLE && P.path != LL_PATH_SMEM_NOSWIZZLE &&
+      P.path != LL_PATH_SMEM_ASYNC && P.path != LL_PATH_SMEM_PADDED && P.path != LL_PATH_SMEM_TMA &&
+      P.path != LL_PATH_SMEM_TMA_STORE)
+    throw Error(LL_ERR_UNSUPPORTED, "shard_2d: only tiled (smem / shuffle) plans are shardable");
+  const int nb = (int)P.tile_bit_src.size();
+  if (sb > nb) throw Error(LL_ERR_UNSUPPORTED, "shard_2d: more shards than tiles");
+  const int64_t w = P.w;
+  for (int s = 0; s < 2; ++s) {
+    const std::vector<int>& top = s == 0 ? P.tile_bit_src : P.tile_bit_dst;
+    const std::vector<int>& oth = s == 0 ? P.tile_bit_dst : P.tile_bit_src;
+    const int ntop = s == 0 ? P.nA : P.nB;
+    const int base = oth[nb - sb];
+    bool ok = true;
+    for (int j = 0; j < sb && ok; ++j)
+      ok = top[nb - sb + j] == ntop - sb + j && oth[nb - sb + j] == base + j;
+    if (!ok) continue;
+    *side = s;
+    *r0 = base;
+    TileRange rg{};
+    const int64_t per = (int64_t(1) << nb) >> sb;
+    rg.t0 = per * shard;
+    rg.t1 = per * (shard + 1);
+    const int64_t slice = (int64_t)shard * ((w << ntop) >> sb);
+    rg.src_shift = s == 0 ? slice : 0;
+    rg.dst_shift = s == 0 ? 0 : slice;
+    return rg;
+  }
+  throw Error(LL_ERR_UNSUPPORTED,
+              "shard_2d: the top tile bits are not the top bits of one side and a contiguous run "
+              "of the other's");
 }
 
 // ------------------------------------------------------------------ gather

@@ -93,6 +93,12 @@ struct GatherPlanHost {
 // last tile-index bits and mapped identically (so every shard is one
 // contiguous slice of each buffer).  Throws LL_ERR_UNSUPPORTED otherwise.
 TileRange shard_range(const ConvertPlan& P, int n_shards, int shard);
+// A shard that is a contiguous slice of one buffer and a pitched (2-D)
+// region of the other: the top log2(n_shards) tile bits are the top index
+// bits of side *side (0 = src, 1 = dst) and the contiguous run of index bits
+// [*r0, *r0 + log2(n_shards)) of the other side.  The contiguous side's
+// shift is its slice offset; the pitched side is addressed in place (shift 0).
+TileRange shard_range_2d(const ConvertPlan& P, int n_shards, int shard, int* side, int* r0);
 
 int planner_knob(const char* name, int dflt);
 int planner_knob_version();

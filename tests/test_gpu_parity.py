@@ -642,6 +642,29 @@ def test_convert_host_sharded_single_instance():
     assert dst_h.numpy().tobytes() == exp.tobytes()
 
 
+@pytest.mark.parametrize("host_2d", [1, 0])
+def test_convert_host_pitched_transpose(host_2d):
+    """A single 8 MiB transpose through ll_convert_host with 1 MiB chunks:
+    pitched shards (contiguous dst slices, 1 KiB src rows; host_2d=1) or the
+    whole instance at once (host_2d=0), both byte-exact."""
+    c = configs.cfg3(n_bits=11)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src_h = values_torch(n, 31, 2, "cpu").pin_memory()
+    dst_h = torch.zeros_like(src_h).pin_memory()
+    ds = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
+    dd = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
+    try:
+        ll.tune("host_chunk_mb", 1)
+        ll.tune("host_2d", host_2d)
+        ll.convert_host(src_h, A, dst_h, B, 16, 1, ds, dd, 2 * n)
+    finally:
+        ll.tune("host_chunk_mb", 16)
+        ll.tune("host_2d", 1)
+    exp = expect_convert(c, _np(src_h, 2))
+    assert _np(dst_h, 2).tobytes() == exp.tobytes()
+
+
 # ------------------------------------------------ register-faithful path (regs)
 
 def rand_faithful_pair(rng, w, match_lanes):

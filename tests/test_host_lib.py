@@ -550,3 +550,39 @@ def test_regs_trans_tile_divides():
             ll.plan_describe(A, B, 16, "regs")
     finally:
         ll.tune("regs_trans", 1)
+
+
+@pytest.mark.parametrize("n_bits,ns", [(9, 2), (9, 4), (10, 8)])
+def test_pitched_shards_partition_the_transpose(n_bits, ns):
+    """ll_shard_describe_2d on a transpose (no split is contiguous in both
+    buffers): shard s's contiguous slice of one side and pitched region of the
+    other hold exactly the same elements under the oracle's conversion
+    (plain definition), and the shards partition both buffers."""
+    import numpy as np
+    from oracle import convert as oconv
+    from workloads.values import values_np
+    c = configs.cfg3(n_bits=n_bits)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    with pytest.raises(ll.LLError):
+        ll.shard_describe(A, B, 16, ns, 0)
+    Ao, Bo = OLayout(**c["A"]), OLayout(**c["B"])
+    n = 1 << A.in_bits
+    src = values_np(n, 5, 2)
+    full = oconv.convert_np(src, Ao, Bo)
+    seen_c, seen_p = np.zeros(n, dtype=int), np.zeros(n, dtype=int)
+    for s in range(ns):
+        side, r0, b0, b1, row, pitch = ll.shard_describe_2d(A, B, 16, ns, s)
+        assert pitch == row * ns and b1 - b0 == 2 * n // ns
+        e = np.arange(n)
+        region = ((e >> r0) & (ns - 1)) == s               # pitched side, element indices
+        contig = (e >= b0 // 2) & (e < b1 // 2)            # contiguous side
+        # rows of `row` bytes at `pitch`, starting at s * row
+        assert region.nonzero()[0][0] * 2 == s * row
+        seen_c += contig
+        seen_p += region
+        src_mask, dst_mask = (contig, region) if side == 0 else (region, contig)
+        only = np.where(src_mask, src, 0).astype(src.dtype)
+        part = oconv.convert_np(only, Ao, Bo)
+        assert (part[dst_mask] == full[dst_mask]).all()
+        assert (part[~dst_mask] == 0).all()
+    assert (seen_c == 1).all() and (seen_p == 1).all()
