@@ -455,6 +455,38 @@ def main():
                "h2d_bytes_per_step": n * w, "d2h_bytes_per_step": n * w,
                "ms_per_step": e_ms, "api": "ll_convert_host (pinned host buffers, 16 MiB chunks, copy-in/compute/copy-out streams)"}
 
+    if cfg == "4" and args.e2e_steps > 0:
+        # the gather end to end: values and indices in, results out (host
+        # buffers, pinned), chunked by [128, 32] instances of the same layout
+        from workloads import configs as _cf
+        ct = _cf.cfg4(r_bits=0)
+        Lt = ll.Layout.from_spec(ct["L"])
+        nb = n >> Lt.in_bits
+        src_h = values_torch(n, 98, 4, "cpu").pin_memory()
+        idx_h = indices_torch(n, 97, 32, "cpu").pin_memory()
+        out_h = torch.empty_like(src_h).pin_memory()
+        scratch = 32 << 20
+        dbuf = [torch.empty(scratch, dtype=torch.uint8, device=dev) for _ in range(3)]
+        ll.gather_host(src_h, idx_h, out_h, Lt, ct["axis"], 32, nb, *dbuf, scratch)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            ll.gather_host(src_h, idx_h, out_h, Lt, ct["axis"], 32, nb, *dbuf, scratch, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * nbytes / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * n,
+               "ms_per_step": e_ms, "api": "ll_gather_host (pinned host buffers, 16 MiB chunks, copy-in/compute/copy-out streams)"}
+
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:

@@ -294,6 +294,17 @@ ll_status ll_convert_shard(const void* src_slice, ll_layout src_layout, void* ds
 ll_status ll_shard_describe(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int path,
                             int n_shards, int shard, int64_t* out4);
 
+/* End-to-end gather of HOST buffers (as ll_gather_ex with
+ * `batch` instances of `layout`): src_host (elem_bits values), idx_host
+ * (int32, one per output element) and out_host are host pointers (pinned for
+ * full speed), chunked by whole instances (~16 MiB, knob "host_chunk_mb")
+ * and pipelined like ll_convert_host over the caller's device scratch
+ * dev_src / dev_idx / dev_out of scratch_bytes each (>= one instance's
+ * max(elem_bytes, 4) * 2^in_bits bytes).  Synchronous. */
+ll_status ll_gather_host(const void* src_host, const int32_t* idx_host, void* out_host,
+                         ll_layout layout, int axis, int elem_bits, int64_t batch, void* dev_src,
+                         void* dev_idx, void* dev_out, size_t scratch_bytes, ll_stream stream);
+
 /* Pitched shard (used by ll_convert_host for layouts that have no
  * contiguous-on-both-sides split, e.g. a transpose): shard `shard` of
  * `n_shards` (a power of two >= 2) is a contiguous slice of one buffer and,

@@ -73,6 +73,8 @@ _lib.ll_convert_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_voi
                                   ctypes.c_void_p, ctypes.c_void_p]
 _lib.ll_shard_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+_lib.ll_gather_host.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                _VP, _VP, _VP, ctypes.c_size_t, _VP]
 _lib.ll_shard_describe_2d.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
 _lib.ll_left_divide.argtypes = [_VP, _VP, ctypes.POINTER(_VP)]
@@ -83,7 +85,7 @@ _lib.ll_convert_inkernel_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, cty
 _lib.ll_jit_source.argtypes = [_VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
 for _f in ("ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
-           "ll_convert_shard", "ll_shard_describe", "ll_shard_describe_2d", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
+           "ll_convert_shard", "ll_shard_describe", "ll_shard_describe_2d", "ll_gather_host", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
            "ll_gather_describe"):
@@ -368,6 +370,14 @@ def shard_describe(A, B, elem_bits, n_shards, shard, path="auto"):
                                   PATHS[path] if isinstance(path, str) else int(path),
                                   int(n_shards), int(shard), out))
     return tuple(out)
+
+
+def gather_host(src_host, idx_host, out_host, L, axis, elem_bits, batch, dev_src, dev_idx,
+                dev_out, scratch_bytes, stream=None):
+    """ll_gather_host: host buffers in, host buffer out (pipelined copies)."""
+    _check(_lib.ll_gather_host(_ptr(src_host), _ptr(idx_host), _ptr(out_host), L.handle, int(axis),
+                               int(elem_bits), int(batch), _ptr(dev_src), _ptr(dev_idx),
+                               _ptr(dev_out), int(scratch_bytes), _stream_handle(stream)))
 
 
 def shard_describe_2d(A, B, elem_bits, n_shards, shard, path="auto"):

@@ -886,4 +886,67 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
   });
 }
 
+ll_status ll_gather_host(const void* src_host, const int32_t* idx_host, void* out_host,
+                         ll_layout layout, int axis, int elem_bits, int64_t batch, void* dev_src,
+                         void* dev_idx, void* dev_out, size_t scratch_bytes, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(layout, "ll_gather_host");
+    const int w = elem_bytes(elem_bits);
+    if (!src_host || !idx_host || !out_host || !dev_src || !dev_idx || !dev_out)
+      return fail(LL_ERR_ARG, "ll_gather_host: NULL buffer");
+    if (batch < 1) batch = 1;
+    const int64_t n = int64_t(1) << layout->L.in_bits();  // elements per instance
+    const size_t ub = (size_t)std::max(w, 4) * n;       // the larger of value / index bytes
+    if (scratch_bytes < ub) return fail(LL_ERR_ARG, "ll_gather_host: scratch smaller than one instance");
+    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 16)) << 20;
+    const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 2)));
+    int64_t per_chunk = (int64_t)std::max<size_t>(1, target / ub);
+    per_chunk = std::min<int64_t>(std::min<int64_t>(per_chunk, (int64_t)(scratch_bytes / ub)), batch);
+    const int64_t n_chunks = (batch + per_chunk - 1) / per_chunk;
+    const size_t cs = (size_t)per_chunk * ub;
+    const int nslot = (int)std::max<size_t>(1, std::min<size_t>(max_slots, scratch_bytes / cs));
+    // the pipeline of ll_convert_host: values and indices in on the copy-in
+    // stream, the gather on the compute stream, results out on the copy-out
+    // stream; slot s is reused only after the chunk that last used it is done
+    HostPipe& hp = host_pipe();
+    std::lock_guard<std::mutex> lk(hp.mu);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaEventRecord(hp.start, st);
+    cudaStreamWaitEvent(hp.h2d, hp.start, 0);
+    cudaStreamWaitEvent(hp.comp, hp.start, 0);
+    cudaStreamWaitEvent(hp.d2h, hp.start, 0);
+    ll_status s = LL_OK;
+    for (int64_t i = 0; i < n_chunks && s == LL_OK; ++i) {
+      const int slot = (int)(i % nslot);
+      const int64_t b0 = i * per_chunk, nb = std::min<int64_t>(per_chunk, batch - b0);
+      char* ds = (char*)dev_src + (size_t)slot * cs;
+      char* di = (char*)dev_idx + (size_t)slot * cs;
+      char* dd = (char*)dev_out + (size_t)slot * cs;
+      if (i >= nslot) cudaStreamWaitEvent(hp.h2d, hp.ev_comp[slot], 0);
+      cudaMemcpyAsync(ds, (const char*)src_host + (size_t)b0 * n * w, (size_t)nb * n * w,
+                      cudaMemcpyHostToDevice, hp.h2d);
+      cudaMemcpyAsync(di, idx_host + b0 * n, (size_t)nb * n * 4, cudaMemcpyHostToDevice, hp.h2d);
+      cudaEventRecord(hp.ev_h2d[slot], hp.h2d);
+      cudaStreamWaitEvent(hp.comp, hp.ev_h2d[slot], 0);
+      if (i >= nslot) cudaStreamWaitEvent(hp.comp, hp.ev_d2h[slot], 0);
+      ll_convert_options o{};
+      o.path = LL_PATH_AUTO;
+      o.batch = nb;
+      s = ll_gather_ex(ds, (const int32_t*)di, dd, layout, axis, elem_bits, &o, (ll_stream)hp.comp);
+      cudaEventRecord(hp.ev_comp[slot], hp.comp);
+      cudaStreamWaitEvent(hp.d2h, hp.ev_comp[slot], 0);
+      cudaMemcpyAsync((char*)out_host + (size_t)b0 * n * w, dd, (size_t)nb * n * w,
+                      cudaMemcpyDeviceToHost, hp.d2h);
+      cudaEventRecord(hp.ev_d2h[slot], hp.d2h);
+    }
+    cudaEventRecord(hp.fin[0], hp.h2d);
+    cudaEventRecord(hp.fin[1], hp.comp);
+    cudaEventRecord(hp.fin[2], hp.d2h);
+    for (int k = 0; k < 3; ++k) cudaStreamWaitEvent(st, hp.fin[k], 0);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (s != LL_OK) return s;
+    return cuda_status(e, "ll_gather_host");
+  });
+}
+
 }  // extern "C"

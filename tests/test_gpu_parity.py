@@ -665,6 +665,30 @@ def test_convert_host_pitched_transpose(host_2d):
     assert _np(dst_h, 2).tobytes() == exp.tobytes()
 
 
+def test_gather_host_e2e():
+    """ll_gather_host: 300 [128, 32] instances (4.7 MiB of values) from pinned
+    host buffers in 1 MiB chunks (a ragged last chunk), byte-exact per
+    instance against the oracle."""
+    c = configs.cfg4(r_bits=0)
+    L = ll.Layout.from_spec(c["L"])
+    m = 1 << L.in_bits
+    batch = 300
+    src_h = values_torch(m * batch, 41, 4, "cpu").pin_memory()
+    idx_h = indices_torch(m * batch, 42, c["idx_limit"], "cpu").pin_memory()
+    out_h = torch.zeros_like(src_h).pin_memory()
+    scratch = 2 << 20
+    bufs = [torch.empty(scratch, dtype=torch.uint8, device="cuda") for _ in range(3)]
+    try:
+        ll.tune("host_chunk_mb", 1)
+        ll.gather_host(src_h, idx_h, out_h, L, c["axis"], 32, batch, *bufs, scratch)
+    finally:
+        ll.tune("host_chunk_mb", 16)
+    src, idx, out = _np(src_h, 4), idx_h.numpy(), _np(out_h, 4)
+    for b in range(batch):
+        exp = oconv.gather_np(src[b * m:(b + 1) * m], idx[b * m:(b + 1) * m], _olayout(c["L"]), c["axis"])
+        assert out[b * m:(b + 1) * m].tobytes() == exp.tobytes(), b
+
+
 # ------------------------------------------------ register-faithful path (regs)
 
 def rand_faithful_pair(rng, w, match_lanes):
