@@ -16,11 +16,13 @@ __global__ void __launch_bounds__(256) convert_generic_kernel(const __grid_const
   using T = typename std::conditional<W == 1, uint8_t,
             typename std::conditional<W == 2, uint16_t,
             typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
-  const int64_t per_batch = (p.nB >= VB) ? (int64_t(1) << (p.nB - VB)) : 1;
+  // vectors per instance: a power of two, so batch / offset are shift / mask
+  const int pb_shift = (p.nB >= VB) ? (p.nB - VB) : 0;
+  const int64_t pb_mask = (int64_t(1) << pb_shift) - 1;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n_vec;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = v / per_batch;
-    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    const int64_t b = v >> pb_shift;
+    const uint64_t h0 = (uint64_t)(v & pb_mask) << VB;
     uint64_t x0 = 0;
     for (int k = VB; k < p.nB; ++k)
       if ((h0 >> k) & 1) x0 ^= (uint64_t)p.x[k];
@@ -62,13 +64,15 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constan
   using T = typename std::conditional<W == 1, uint8_t,
             typename std::conditional<W == 2, uint16_t,
             typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
-  const int64_t per_batch = int64_t(1) << (p.nbits - VB);
+  // vectors per instance: a power of two, so batch / offset are shift / mask
+  const int pb_shift = p.nbits - VB;
+  const int64_t pb_mask = (int64_t(1) << pb_shift) - 1;
   const uint32_t amask = (1u << p.ax_bits) - 1;
   const int64_t n_units = V2 ? (p.n_vec >> 1) : p.n_vec;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_units;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = v / per_batch;
-    const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+    const int64_t b = v >> pb_shift;
+    const uint64_t h0 = (uint64_t)(v & pb_mask) << VB;
     const T* s = reinterpret_cast<const T*>(src) + b * p.batch_stride;
     const int32_t* ip = idx + b * p.batch_stride + h0;
     // warm L1 with this thread's own source vector while the indices load: for
@@ -146,7 +150,9 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
             typename std::conditional<W == 2, uint16_t,
             typename std::conditional<W == 4, uint32_t, uint64_t>::type>::type>::type;
   const int lane = threadIdx.x & 31;
-  const int64_t per_batch = int64_t(1) << (p.nbits - VB);
+  // vectors per instance: a power of two, so batch / offset are shift / mask
+  const int pb_shift = p.nbits - VB;
+  const int64_t pb_mask = (int64_t(1) << pb_shift) - 1;
   const uint32_t amask = (1u << p.ax_bits) - 1;
   const int64_t nwarps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_wvec = p.n_vec >> 5;  // warps' worth of vectors
@@ -171,8 +177,8 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
       if (wv >= n_wvec) continue;  // warp-uniform
       const int64_t v = (wv << 5) | lane;
       vv[u] = v;
-      const int64_t b = v / per_batch;
-      const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+      const int64_t b = v >> pb_shift;
+      const uint64_t h0 = (uint64_t)(v & pb_mask) << VB;
       sv[u].v4 = ldg_stream(src + (b * p.batch_stride + h0) * W);
       const int32_t* ip = idx + b * p.batch_stride + h0;
       if constexpr (NE >= 4) {
@@ -190,8 +196,8 @@ __global__ void __launch_bounds__(256) gather_shuffle_kernel(const __grid_consta
     for (int u = 0; u < U; ++u) {
       if (vv[u] < 0) continue;
       const int64_t v = vv[u];
-      const int64_t b = v / per_batch;
-      const uint64_t h0 = (uint64_t)(v - b * per_batch) << VB;
+      const int64_t b = v >> pb_shift;
+      const uint64_t h0 = (uint64_t)(v & pb_mask) << VB;
       V o;
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
