@@ -528,7 +528,7 @@ def main():
                          "traffic": ncu_traffic(cfg + ("_upcast" if args.upcast else "") +
                                                 {"smem": ("_jit" if "upcast_jit=0" not in args.tune else "") if args.upcast
                                                  else ("" if "smem_jit=0" in args.tune else "_jit"), "smem_tma": "_tma", "regs": "_regs", "smem_tma_store": "_tmas",
-                                                 "shuffle": "" if cfg == "4" else "_shfl"}.get(
+                                                 "shuffle": "_shfl"}.get(
                                                     plan.get("path"), "")),
                          "peak_source": peak_src, "kernel": kernel,
                          "avg_launch_us": avg_launch_ms * 1000,
