@@ -586,3 +586,17 @@ def test_pitched_shards_partition_the_transpose(n_bits, ns):
         assert (part[dst_mask] == full[dst_mask]).all()
         assert (part[~dst_mask] == 0).all()
     assert (seen_c == 1).all() and (seen_p == 1).all()
+
+
+def test_gather_host_argument_contract():
+    """ll_gather_host rejects NULL buffers and a scratch smaller than one
+    instance (max(elem, 4 B) x 2^in_bits) before any device work."""
+    c = configs.cfg4(r_bits=0)
+    L = ll.Layout.from_spec(c["L"])
+    m = 1 << L.in_bits
+    with pytest.raises(ll.LLError) as e:
+        ll.gather_host(0, 0x1000, 0x2000, L, c["axis"], 32, 1, 0x3000, 0x4000, 0x5000, 4 * m, stream=0)
+    assert e.value.name == "LL_ERR_ARG"
+    with pytest.raises(ll.LLError) as e:
+        ll.gather_host(0x1000, 0x2000, 0x3000, L, c["axis"], 32, 1, 0x4000, 0x5000, 0x6000, 4 * m - 16, stream=0)
+    assert e.value.name == "LL_ERR_ARG" and "scratch" in str(e.value)
