@@ -358,3 +358,33 @@ def test_from_flat_round_trip():
     A = layout_A()
     B = from_flat(A.in_dims, A.out_dims, A.cols)
     assert B == A
+
+
+def test_b8_matrix_tiles_measured_on_b200_are_linear_layouts():
+    """sm_100a's 8-bit ldmatrix / stmatrix forms are linear layouts (the
+    paper's claim for the 16-bit ones): the per-(lane, byte)
+    shared-memory offsets measured on the B200 by tools/b8_probe.cu
+    (profiles/r01/b8/b8_probe.json) equal apply() of the F2 layouts
+      ldmatrix.m16n16.x1.trans.b8: reg [16, 32, 8], lane [64, 128, 1, 2, 4]
+      stmatrix.m16n8.x1.trans.b8:  reg [16, 8],     lane [32, 64, 1, 2, 4]
+    at every one of the 256 / 128 bytes (the tiles the register-faithful path
+    would left-divide by; DESIGN 8b)."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                     "profiles", "r01", "b8", "b8_probe.json")
+    d = json.load(open(p))
+    ld = Layout([("reg", 3), ("lane", 5)], [("offset", 8)],
+                {"reg": [(16,), (32,), (8,)], "lane": [(64,), (128,), (1,), (2,), (4,)]})
+    got = d["ldmatrix.m16n16.x1.trans.b8"]
+    for lane in range(32):
+        for b in range(8):
+            assert ld.apply({"reg": b, "lane": lane}) == (got[lane][b],)
+    st = Layout([("reg", 2), ("lane", 5)], [("offset", 7)],
+                {"reg": [(16,), (8,)], "lane": [(32,), (64,), (1,), (2,), (4,)]})
+    mem = d["stmatrix.m16n8.x1.trans.b8"]
+    for lane in range(32):
+        for b in range(4):
+            (o,) = st.apply({"reg": b, "lane": lane})
+            assert mem[o] == (lane << 2) | b
+    assert sum(v != 255 for v in mem) == 128
