@@ -1,6 +1,6 @@
 #!/bin/bash
 # Shuffle gather: warp-vectors in flight per thread (gather_shfl_u) x vectors per thread.
-O=gpurun_out/gather_u; mkdir -p $O
+O=${O:-gpurun_out/gather_u}; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.txt 2>&1
 timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -q -k gather > $O/pytest.txt 2>&1
 B="--no-cpu-baseline --e2e-steps 0"
@@ -10,7 +10,7 @@ for rep in 1 2; do for u in 1 2 4; do for v in 2 4 8 16; do
 done; done; timeout 300 python bench.py --config 4 $B > $O/direct_r$rep.json 2>/dev/null; done
 python - > $O/summary.txt <<'PY'
 import json, glob, os
-for f in sorted(glob.glob("gpurun_out/gather_u/*.json")):
+for f in sorted(glob.glob(os.environ.get("O", "gpurun_out/gather_u") + "/*.json")):
     try:
         d = json.loads(open(f).read().strip().splitlines()[-1])
         print(os.path.basename(f), round(d["value"]), d["clocks"]["sm_mhz"], d["clocks"]["reasons"])
