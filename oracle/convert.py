@@ -127,3 +127,64 @@ def gather_np(src, idx, L, axis, h=None):
         raise ValueError("gather: index out of range")
     y = (apply_np(L.cols, h) & ~np.int64(mask)) | (ih << shift)
     return src[T[y]]
+
+
+# --- whole buffers at full size (chunked) --------------------------------------------
+#
+# The same definitions, evaluated over 2^26-2^29-element buffers in chunks
+# (GPU parity on the BASELINE sizes).  Two evaluation aids, both pinned
+# against the functions above in tests/test_oracle_convert.py:
+#   * apply_np_tab: the location of an index is the XOR of the locations of
+#     its parts ("the XOR of per-level locations"); the input bits are
+#     cut into groups of <= 16 bits, each group's 2^16 XOR-combinations are
+#     tabulated with apply_np, and a point is the XOR of its groups' entries;
+#   * preimage_table_bij_np: for a bijective layout the lowest preimage is the
+#     only preimage, so T is the inverse permutation, T[A(h)] = h (no sort).
+
+def _group_tables(cols, group_bits=16):
+    tabs = []
+    for g0 in range(0, len(cols), group_bits):
+        part = cols[g0:g0 + group_bits]
+        tabs.append((g0, len(part), apply_np(part, np.arange(1 << len(part), dtype=np.int64))))
+    return tabs
+
+
+def apply_np_tab(cols, h, tabs=None):
+    """apply_np(cols, h) as the XOR of per-group table entries."""
+    h = np.asarray(h, dtype=np.int64)
+    if tabs is None:
+        tabs = _group_tables(cols)
+    out = np.zeros_like(h)
+    for g0, nb, tab in tabs:
+        out ^= tab[(h >> g0) & ((1 << nb) - 1)]
+    return out
+
+
+def preimage_table_bij_np(A, chunk=1 << 22):
+    """T[x] = the preimage of x under a bijective A (in_bits == out_bits and
+    every x hit exactly once; ValueError otherwise)."""
+    n = A.in_bits
+    if n != A.out_bits:
+        raise ValueError("preimage_table_bij_np: layout is not square")
+    T = np.full(1 << n, -1, dtype=np.int64)
+    tabs = _group_tables(A.cols)
+    for h0 in range(0, 1 << n, chunk):
+        h = np.arange(h0, min(1 << n, h0 + chunk), dtype=np.int64)
+        T[apply_np_tab(A.cols, h, tabs)] = h
+    if (T < 0).any():
+        raise ValueError("preimage_table_bij_np: layout is not bijective")
+    return T
+
+
+def convert_np_chunks(src, A, B, chunk=1 << 22):
+    """Yields (h0, dst[h0:h0+chunk]) of ``convert_np(src, A, B)`` for a
+    bijective source layout A: dst[h_B] = src[T[B(h_B)]] chunk by chunk."""
+    src = np.asarray(src)
+    if src.shape[0] != (1 << A.in_bits):
+        raise ValueError("convert: src has the wrong size")
+    T = preimage_table_bij_np(A)
+    tabs = _group_tables(B.cols)
+    nB = 1 << B.in_bits
+    for h0 in range(0, nB, chunk):
+        h = np.arange(h0, min(nB, h0 + chunk), dtype=np.int64)
+        yield h0, src[T[apply_np_tab(B.cols, h, tabs)]]

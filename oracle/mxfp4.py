@@ -83,3 +83,28 @@ def upcast_np(packed, A, scales, B, h=None):
     out[0::2] = tab[sc, byte & 15]
     out[1::2] = tab[sc, byte >> 4]
     return out
+
+
+def upcast_np_chunks(packed, A, scales, B, chunk=1 << 22):
+    """Yields (h0, out[2*h0 : 2*(h0+chunk)]) of ``upcast_np`` over the whole
+    destination, chunk by chunk, for a bijective source layout A (the
+    evaluation aids of convert.convert_np_chunks; same definition)."""
+    kb_bits = B.out_dims[1][1]
+    row = 1 << (kb_bits - 4)
+    T = convert.preimage_table_bij_np(A)
+    tabs = convert._group_tables(B.cols)
+    tab = dequant_table()
+    packed = np.asarray(packed)
+    scales = np.asarray(scales)
+    nB = 1 << B.in_bits
+    for h0 in range(0, nB, chunk):
+        h = np.arange(h0, min(nB, h0 + chunk), dtype=np.int64)
+        x = convert.apply_np_tab(B.cols, h, tabs)
+        m = x >> kb_bits
+        kb = x & ((1 << kb_bits) - 1)
+        byte = packed[T[x]].astype(np.int64)
+        sc = scales[m * row + (kb >> 4)].astype(np.int64)
+        out = np.empty(2 * len(h), dtype=np.uint16)
+        out[0::2] = tab[sc, byte & 15]
+        out[1::2] = tab[sc, byte >> 4]
+        yield h0, out

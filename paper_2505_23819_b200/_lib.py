@@ -295,6 +295,35 @@ def _ptr(t):
     return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
 
 
+def _dev_arg(t, name, need_bytes, elem_bits=None):
+    """Argument checks for a torch tensor handed to a device entry point (the
+    C ABI takes bare pointers, so sizes are checked here): on CUDA,
+    contiguous, element width = elem_bits (when given), at least need_bytes
+    bytes.  Raw integer pointers are passed through unchecked."""
+    if not hasattr(t, "data_ptr"):
+        return
+    if not t.is_cuda:
+        raise LLError(1, "%s: tensor is not on a CUDA device" % name)
+    if not t.is_contiguous():
+        raise LLError(1, "%s: tensor is not contiguous" % name)
+    if elem_bits is not None and t.element_size() * 8 != int(elem_bits):
+        raise LLError(1, "%s: element size %d bits != elem_bits %d" % (
+            name, t.element_size() * 8, int(elem_bits)))
+    have = t.numel() * t.element_size()
+    if have < need_bytes:
+        raise LLError(1, "%s: %d bytes < %d needed" % (name, have, need_bytes))
+
+
+def _stream_for(stream, *tensors):
+    """The given stream, else the current stream of the first tensor's device."""
+    if stream is None:
+        for t in tensors:
+            if hasattr(t, "device") and getattr(t, "is_cuda", False):
+                import torch
+                return torch.cuda.current_stream(t.device).cuda_stream
+    return _stream_handle(stream)
+
+
 def _opts(path, batch, max_ctas):
     o = _Opts()
     o.path = PATHS[path] if isinstance(path, str) else int(path)
@@ -306,8 +335,11 @@ def _opts(path, batch, max_ctas):
 def convert(src, A, dst, B, elem_bits, path="auto", batch=1, max_ctas=0, stream=None):
     """ll_convert_ex on device tensors (or raw device pointers as ints)."""
     o = _opts(path, batch, max_ctas)
+    wb = int(elem_bits) // 8
+    _dev_arg(src, "convert src", (wb << A.in_bits) * int(batch), elem_bits)
+    _dev_arg(dst, "convert dst", (wb << B.in_bits) * int(batch), elem_bits)
     _check(_lib.ll_convert_ex(_ptr(src), A.handle, _ptr(dst), B.handle, int(elem_bits),
-                              ctypes.byref(o), _stream_handle(stream)))
+                              ctypes.byref(o), _stream_for(stream, src, dst)))
 
 
 def convert_regs_timed(src, A, dst, B, elem_bits, reps=1, cycles=None, batch=1, stream=None,
@@ -343,22 +375,31 @@ def convert_shard(src_slice, A, dst_slice, B, elem_bits, n_shards, shard, path="
                   max_ctas=0, stream=None):
     """ll_convert_shard: convert this rank's slice."""
     o = _opts(path, 1, max_ctas)
+    wb = int(elem_bits) // 8
+    if int(n_shards) >= 1:
+        _dev_arg(src_slice, "convert_shard src", (wb << A.in_bits) // int(n_shards), elem_bits)
+        _dev_arg(dst_slice, "convert_shard dst", (wb << B.in_bits) // int(n_shards), elem_bits)
     _check(_lib.ll_convert_shard(_ptr(src_slice), A.handle, _ptr(dst_slice), B.handle,
                                  int(elem_bits), int(n_shards), int(shard), ctypes.byref(o),
-                                 _stream_handle(stream)))
+                                 _stream_for(stream, src_slice, dst_slice)))
 
 
 def mxfp4_upcast(packed, A, scales, dst_bf16, B, max_ctas=0, stream=None):
     """ll_mxfp4_upcast: packed E2M1 bytes (layout A) + E8M0 scales [M][K/32]
     -> bf16, two per byte of B (fused with the conversion)."""
     o = _opts("auto", 1, max_ctas)
+    _dev_arg(packed, "mxfp4_upcast packed", 1 << A.in_bits)
+    _dev_arg(scales, "mxfp4_upcast scales", (1 << A.in_bits) // 16)
+    _dev_arg(dst_bf16, "mxfp4_upcast dst_bf16", 4 << B.in_bits)
     _check(_lib.ll_mxfp4_upcast(_ptr(packed), A.handle, _ptr(scales), _ptr(dst_bf16), B.handle,
-                                ctypes.byref(o), _stream_handle(stream)))
+                                ctypes.byref(o), _stream_for(stream, packed, dst_bf16)))
 
 
 def checksum(buf, n_elems, elem_bits, result, indexed=True, index_base=0, stream=None):
     """ll_checksum into the device uint64 `result` (a 1-element int64 tensor or
     a device pointer); enqueued on `stream`, no synchronisation."""
+    _dev_arg(buf, "checksum buf", int(n_elems) * int(elem_bits) // 8)
+    _dev_arg(result, "checksum result", 8)
     _check(_lib.ll_checksum(_ptr(buf), int(n_elems), int(elem_bits), 1 if indexed else 0,
                             int(index_base), _ptr(result), _stream_handle(stream)))
 
@@ -391,8 +432,12 @@ def shard_describe_2d(A, B, elem_bits, n_shards, shard, path="auto"):
 
 def gather(src, idx, out, L, axis, elem_bits, path="auto", batch=1, max_ctas=0, stream=None):
     o = _opts(path, batch, max_ctas)
+    n = (1 << L.in_bits) * int(batch)
+    _dev_arg(src, "gather src", n * (int(elem_bits) // 8), elem_bits)
+    _dev_arg(idx, "gather idx", n * 4, 32)
+    _dev_arg(out, "gather out", n * (int(elem_bits) // 8), elem_bits)
     _check(_lib.ll_gather_ex(_ptr(src), _ptr(idx), _ptr(out), L.handle, int(axis),
-                             int(elem_bits), ctypes.byref(o), _stream_handle(stream)))
+                             int(elem_bits), ctypes.byref(o), _stream_for(stream, src, idx, out)))
 
 
 def convert_host(src_host, A, dst_host, B, elem_bits, batch, dev_src, dev_dst, scratch_bytes,

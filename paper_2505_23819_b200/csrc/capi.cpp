@@ -100,7 +100,8 @@ ll_status ll_layout_create(int n_in, const char* const* in_names, const int* in_
     std::set<std::string> seen;
     int tin = 0, tout = 0;
     for (int i = 0; i < n_in; ++i) {
-      if (!in_names[i] || in_bits[i] < 0) return fail(LL_ERR_ARG, "ll_layout_create: bad input dim");
+      if (!in_names[i] || in_bits[i] < 0 || in_bits[i] > 62)
+        return fail(LL_ERR_ARG, "ll_layout_create: bad input dim (bits must be in [0, 62])");
       if (!seen.insert(in_names[i]).second)
         return fail(LL_ERR_ARG, std::string("ll_layout_create: duplicate input dim '") + in_names[i] + "'");
       L.in.push_back({in_names[i], in_bits[i]});
@@ -108,7 +109,8 @@ ll_status ll_layout_create(int n_in, const char* const* in_names, const int* in_
     }
     seen.clear();
     for (int i = 0; i < n_out; ++i) {
-      if (!out_names[i] || out_bits[i] < 0) return fail(LL_ERR_ARG, "ll_layout_create: bad output dim");
+      if (!out_names[i] || out_bits[i] < 0 || out_bits[i] > 62)
+        return fail(LL_ERR_ARG, "ll_layout_create: bad output dim (bits must be in [0, 62])");
       if (!seen.insert(out_names[i]).second)
         return fail(LL_ERR_ARG, std::string("ll_layout_create: duplicate output dim '") + out_names[i] + "'");
       L.out.push_back({out_names[i], out_bits[i]});
@@ -420,7 +422,6 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
         cudaError_t e = ll::launch_shuffle_jit(*P, src, dst, max_ctas, st, rg, &err);
         // NVRTC / module problems (nothing was launched): the generic shuffle kernel
         if (e != cudaSuccess && !err.empty() && err.rfind("cuLaunchKernel", 0) != 0) {
-          cudaGetLastError();
           return cuda_status(ll::launch_convert_shuffle(P->shp, w, P->nv, src, dst, max_ctas, st, rg),
                              "ll_convert (shuffle kernel)");
         }
@@ -462,7 +463,8 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
         cudaError_t e = ll::launch_smem_jit(*P, src, dst, max_ctas, st, rg, &err);
         if (e == cudaSuccess || err.rfind("cuLaunchKernel", 0) == 0)
           return cuda_status(e, "ll_convert (specialised smem kernel)");
-        cudaGetLastError();  // compile problem: the generic smem kernel below
+        // compile / module problem, nothing launched (a successful launch
+        // returns cudaSuccess): the generic smem kernel below
         --g_launches;
       }
       [[fallthrough]];
@@ -578,7 +580,7 @@ ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_
                                             reinterpret_cast<cudaStream_t>(stream), rg, &err);
       if (e == cudaSuccess || err.rfind("cuLaunchKernel", 0) == 0)
         return cuda_status(e, "ll_mxfp4_upcast (specialised kernel)");
-      cudaGetLastError();  // compile problem: the template kernel below
+      // compile / module problem, nothing launched: the template kernel below
     }
     return cuda_status(ll::launch_mxfp4_upcast(P->sp, P->nv, P->g, packed, dst_bf16, scales,
                                                opts ? opts->max_ctas : 0,

@@ -620,7 +620,7 @@ cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src
     *err = "cuLaunchKernel failed";
     return cudaErrorLaunchFailure;
   }
-  return cudaGetLastError();
+  return cudaSuccess;  // launched by the driver API: no runtime error state to read
 }
 
 cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
@@ -653,7 +653,7 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
     *err = "cuLaunchKernel failed";
     return cudaErrorLaunchFailure;
   }
-  return cudaGetLastError();
+  return cudaSuccess;  // launched by the driver API: no runtime error state to read
 }
 
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P) { return shuffle_hbm_source(P); }
@@ -710,7 +710,7 @@ cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
     *err = "cuLaunchKernel failed";
     return cudaErrorLaunchFailure;
   }
-  return cudaGetLastError();
+  return cudaSuccess;  // launched by the driver API: no runtime error state to read
 }
 
 cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
@@ -767,7 +767,7 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
     *err = "cuLaunchKernel failed";
     return cudaErrorLaunchFailure;
   }
-  return cudaGetLastError();
+  return cudaSuccess;  // launched by the driver API: no runtime error state to read
 }
 
 }  // namespace ll

@@ -600,3 +600,40 @@ def test_gather_host_argument_contract():
     with pytest.raises(ll.LLError) as e:
         ll.gather_host(0x1000, 0x2000, 0x3000, L, c["axis"], 32, 1, 0x4000, 0x5000, 0x6000, 4 * m - 16, stream=0)
     assert e.value.name == "LL_ERR_ARG" and "scratch" in str(e.value)
+
+
+def test_binding_rejects_bad_tensor_arguments():
+    """The C ABI takes bare pointers, so the binding checks torch tensors
+    first (device, contiguity, element width, size) -- all before any launch,
+    so this runs without a GPU."""
+    import torch
+    import paper_2505_23819_b200 as ll
+    from workloads import configs
+    c = configs.cfg2(batch_bits=0)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src = torch.zeros(n, dtype=torch.int16)
+    with pytest.raises(ll.LLError, match="not on a CUDA device"):
+        ll.convert(src, A, torch.zeros(n, dtype=torch.int16), B, 16)
+
+    class FakeCuda:
+        """Duck-typed stand-in for a CUDA tensor (is_cuda only)."""
+        def __init__(self, n, esize, contiguous=True):
+            self.n, self.esize, self.contiguous = n, esize, contiguous
+            self.is_cuda = True
+        def data_ptr(self): return 1 << 20
+        def is_contiguous(self): return self.contiguous
+        def element_size(self): return self.esize
+        def numel(self): return self.n
+
+    with pytest.raises(ll.LLError, match="bytes <"):
+        ll.convert(FakeCuda(n, 2), A, FakeCuda(n - 8, 2), B, 16)
+    with pytest.raises(ll.LLError, match="element size"):
+        ll.convert(FakeCuda(n, 4), A, FakeCuda(n, 2), B, 16)
+    with pytest.raises(ll.LLError, match="not contiguous"):
+        ll.convert(FakeCuda(n, 2, False), A, FakeCuda(n, 2), B, 16)
+    with pytest.raises(ll.LLError, match="gather idx"):
+        g = configs.cfg4(r_bits=0)
+        L = ll.Layout.from_spec(g["L"])
+        m = 1 << L.in_bits
+        ll.gather(FakeCuda(m, 4), FakeCuda(m, 2), FakeCuda(m, 4), L, 2, 32)

@@ -187,3 +187,42 @@ def test_contiguity_tab_micro_load_store(k, w, bits):
     t0 = 5 - t1
     L = blocked([9, kb], R=[r0, r1], T=[t0, t1], W=[9 - r0 - t0, 0], order=[1, 0])
     assert contig.vector_bits(L, w) == bits
+
+
+# --- chunked whole-buffer evaluation (full-size GPU parity) ------------------------
+
+def test_apply_np_tab_equals_apply_np_and_f2_apply():
+    import random
+    from oracle import convert as oc
+    from oracle import f2 as of2
+    rng = random.Random(5)
+    for n in (3, 16, 17, 29, 35):
+        cols = [rng.getrandbits(40) for _ in range(n)]
+        h = np.array([rng.getrandbits(n) for _ in range(2000)], dtype=np.int64)
+        a = oc.apply_np_tab(cols, h)
+        assert (a == oc.apply_np(cols, h)).all()
+        assert all(int(a[i]) == of2.apply(cols, int(h[i])) for i in range(0, 2000, 97))
+
+
+def test_preimage_table_bij_equals_lowest_preimage_and_rejects_non_bijective():
+    from oracle import convert as oc
+    from oracle.layout import Layout
+    from workloads import configs
+    for c in (configs.cfg2(batch_bits=2), configs.cfg3(n_bits=7), configs.cfg5(m_bits=8, kb_bits=7)):
+        A = Layout(**c["A"])
+        assert (oc.preimage_table_bij_np(A, chunk=1 << 10) == oc.preimage_table_np(A)).all()
+    bc = Layout([("reg", 2)], [("i", 2)], {"reg": [(1,), (1,)]})
+    with pytest.raises(ValueError):
+        oc.preimage_table_bij_np(bc)
+
+
+def test_convert_np_chunks_concatenate_to_convert_np():
+    from oracle import convert as oc
+    from oracle.layout import Layout
+    from workloads import configs
+    from workloads.values import values_np
+    for c in (configs.cfg2(batch_bits=2), configs.cfg3(n_bits=7), configs.cfg5(m_bits=8, kb_bits=7)):
+        A, B = Layout(**c["A"]), Layout(**c["B"])
+        src = values_np(1 << A.in_bits, 3, c["elem_bytes"])
+        parts = [d for _, d in oc.convert_np_chunks(src, A, B, chunk=1 << 11)]
+        assert np.concatenate(parts).tobytes() == oc.convert_np(src, A, B).tobytes()
