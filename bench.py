@@ -407,7 +407,6 @@ def ncu_probe(args):
             else:
                 ll.convert(s, A, d, B, 8 * w, path=args.path)
         torch.cuda.synchronize()
-        del s, d
         torch.cuda.empty_cache()
 
 

@@ -222,9 +222,42 @@ typedef struct {
 ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_layout dst_layout,
                         int elem_bits, const ll_convert_options* opts, ll_stream stream);
 
-/* Same with gather options (path: AUTO, SHUFFLE, SMEM or GENERIC; batch). */
+/* Same with gather options (path, batch).  Paths:
+ *   LL_PATH_AUTO     the direct kernel (measured fastest on B200)
+ *   LL_PATH_SHUFFLE  warp-shuffle gather: the axis vectors L^{-1} e_axis lie in
+ *                    one warp's registers and lanes (L_warp^axis =
+ *                    L_block^axis = 0, in the coalesced mapping: within the low
+ *                    log2(16 / elem_bytes) + 9 buffer bits); 2^|L_reg^axis|
+ *                    candidate shuffles per output (reading A19); compiled per
+ *                    plan (NVRTC)
+ *   LL_PATH_SMEM     shared-memory gather: the axis inside an aligned unit of
+ *                    <= 64 KiB (L_block^axis = 0); one cp.async.bulk per unit,
+ *                    one ld.shared per output; compiled per plan
+ *   LL_PATH_GENERIC  direct: source elements read through L1, any layout
+ * LL_ERR_UNSUPPORTED when the requested path does not apply.  A compile or
+ * module failure of a compiled kernel falls back to the direct kernel. */
 ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout layout, int axis,
                        int elem_bits, const ll_convert_options* opts, ll_stream stream);
+
+/* The CUDA source of the compiled gather kernel for (layout, axis, path =
+ * LL_PATH_SHUFFLE or LL_PATH_SMEM) into buf (as ll_jit_source); mode bit 1 =
+ * the in-kernel timed variant, bit 0 = compile it with NVRTC for sm_100a
+ * instead (no device needed) and return {"compiled": true, "cubin_bytes": n}.
+ * LL_ERR_UNSUPPORTED if the path does not apply or NVRTC fails. */
+ll_status ll_gather_jit_source(ll_layout layout, int axis, int elem_bits, int path, int mode,
+                               char* buf, size_t cap, size_t* need);
+
+/* In-kernel timing of the gather exchange (the paper's fig:micro-gather
+ * setting: one CTA): one CTA gathers the first unit of the buffers
+ * (shuffle: one warp unit = 2^warp_unit_bits elements; smem: one CTA unit),
+ * with the exchange -- idx -> source (lane, register) -> shuffles + select, or
+ * idx -> ld.shared -- repeated `reps` times on data already in registers /
+ * shared memory; thread 0 writes the clock64 cycles of the repeated section
+ * to cycles[0] (device pointer).  out receives the gather of that unit.
+ * path = LL_PATH_SHUFFLE or LL_PATH_SMEM; errors as ll_gather_ex. */
+ll_status ll_gather_timed(const void* src, const int32_t* idx, void* out, ll_layout layout,
+                          int axis, int elem_bits, int path, int reps, long long* cycles,
+                          ll_stream stream);
 
 /* Fused mxfp4 dequantisation with the layout conversion (
  * "Software Emulation" / "Data Shuffling"; OCP MX):

@@ -84,7 +84,12 @@ _lib.ll_convert_inkernel_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, cty
                                            ctypes.c_int, ctypes.c_int, _VP, _VP]
 _lib.ll_jit_source.argtypes = [_VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
-for _f in ("ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+_lib.ll_gather_jit_source.argtypes = [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_char_p, ctypes.c_size_t,
+                                      ctypes.POINTER(ctypes.c_size_t)]
+_lib.ll_gather_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_int, _VP, _VP]
+for _f in ("ll_gather_jit_source", "ll_gather_timed", "ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_shard_describe_2d", "ll_gather_host", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
@@ -298,15 +303,15 @@ def _ptr(t):
 def _dev_arg(t, name, need_bytes, elem_bits=None):
     """Argument checks for a torch tensor handed to a device entry point (the
     C ABI takes bare pointers, so sizes are checked here): on CUDA,
-    contiguous, element width = elem_bits (when given), at least need_bytes
-    bytes.  Raw integer pointers are passed through unchecked."""
+    contiguous, element width = elem_bits or a raw byte view (uint8), at
+    least need_bytes bytes.  Raw integer pointers are passed through unchecked."""
     if not hasattr(t, "data_ptr"):
         return
     if not t.is_cuda:
         raise LLError(1, "%s: tensor is not on a CUDA device" % name)
     if not t.is_contiguous():
         raise LLError(1, "%s: tensor is not contiguous" % name)
-    if elem_bits is not None and t.element_size() * 8 != int(elem_bits):
+    if elem_bits is not None and t.element_size() not in (1, int(elem_bits) // 8):
         raise LLError(1, "%s: element size %d bits != elem_bits %d" % (
             name, t.element_size() * 8, int(elem_bits)))
     have = t.numel() * t.element_size()
@@ -464,3 +469,26 @@ def plan_describe(A, B, elem_bits, path="auto"):
 def gather_describe(L, axis, elem_bits, path="auto"):
     return _describe(_lib.ll_gather_describe, L.handle, int(axis), int(elem_bits),
                      PATHS[path] if isinstance(path, str) else int(path))
+
+
+def gather_jit_source(L, axis, elem_bits, path="shuffle", compile=False, timed=False):
+    """ll_gather_jit_source: the compiled gather kernel's CUDA source (or,
+    compile=True, the NVRTC result as a dict)."""
+    mode = (1 if compile else 0) | (2 if timed else 0)
+    p = PATHS[path] if isinstance(path, str) else int(path)
+    need = ctypes.c_size_t()
+    _check(_lib.ll_gather_jit_source(L.handle, int(axis), int(elem_bits), p, mode, None, 0,
+                                     ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(_lib.ll_gather_jit_source(L.handle, int(axis), int(elem_bits), p, mode, buf,
+                                     need.value, ctypes.byref(need)))
+    out = buf.value.decode()
+    return json.loads(out) if compile else out
+
+
+def gather_timed(src, idx, out, L, axis, elem_bits, path, reps, cycles, stream=None):
+    """ll_gather_timed: one CTA, the gather exchange repeated `reps` times
+    in-kernel; clock64 cycles into cycles[0] (int64 device tensor)."""
+    _check(_lib.ll_gather_timed(_ptr(src), _ptr(idx), _ptr(out), L.handle, int(axis),
+                                int(elem_bits), PATHS[path] if isinstance(path, str) else int(path),
+                                int(reps), _ptr(cycles), _stream_for(stream, src, idx, out)))

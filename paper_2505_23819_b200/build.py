@@ -21,7 +21,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernel_smem.cu", "kernel_async.cu", "kernel_tma.cu", "kernel_regs.cu", "kernel_shuffle.cu", "kernel_misc.cu"]
-CPP_SOURCES = ["core.cpp", "planner.cpp", "planner_tma.cpp", "planner_regs.cpp", "capi.cpp", "jit.cpp"]
+CPP_SOURCES = ["core.cpp", "planner.cpp", "planner_tma.cpp", "planner_regs.cpp", "capi.cpp", "jit.cpp", "gather.cpp"]
 HEADERS = ["core.hpp", "plan.hpp", "planner.hpp", "planner_internal.hpp", "kernels.hpp", "device_common.cuh"]
 
 

@@ -553,6 +553,55 @@ ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bit
   });
 }
 
+ll_status ll_gather_jit_source(ll_layout layout, int axis, int elem_bits, int path, int mode,
+                              char* buf, size_t cap, size_t* need) {
+  return guarded([&]() -> ll_status {
+    check_layout(layout, "ll_gather_jit_source");
+    const int w = elem_bytes(elem_bits);
+    if (path != LL_PATH_SHUFFLE && path != LL_PATH_SMEM)
+      return fail(LL_ERR_ARG, "ll_gather_jit_source: path must be SHUFFLE or SMEM");
+    auto P = ll::get_gather_plan(layout->L, axis, w, path, 1);
+    const int timed = (mode & 2) ? 1 : 0;
+    std::string out = path == LL_PATH_SHUFFLE ? ll::gather_shfl_source(*P, timed)
+                                              : ll::gather_smem_source(*P, timed);
+    if (mode & 1) {
+      std::string log;
+      size_t cubin = 0;
+      const bool ok = ll::nvrtc_compile_check(out, &log, &cubin);
+      out = std::string("{\"compiled\":") + (ok ? "true" : "false") + ",\"cubin_bytes\":" +
+            std::to_string(cubin) + "}";
+      if (!ok) return fail(LL_ERR_UNSUPPORTED, "ll_gather_jit_source: NVRTC failed: " + log.substr(0, 600));
+    }
+    if (need) *need = out.size() + 1;
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, out.size());
+      std::memcpy(buf, out.data(), n);
+      buf[n] = 0;
+    }
+    return LL_OK;
+  });
+}
+
+ll_status ll_gather_timed(const void* src, const int32_t* idx, void* out, ll_layout layout,
+                          int axis, int elem_bits, int path, int reps, long long* cycles,
+                          ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(layout, "ll_gather_timed");
+    const int w = elem_bytes(elem_bits);
+    if (!src || !idx || !out) return fail(LL_ERR_ARG, "ll_gather_timed: NULL buffer");
+    if (reps < 1) return fail(LL_ERR_ARG, "ll_gather_timed: reps < 1");
+    if (path != LL_PATH_SHUFFLE && path != LL_PATH_SMEM)
+      return fail(LL_ERR_ARG, "ll_gather_timed: path must be SHUFFLE or SMEM");
+    auto P = ll::get_gather_plan(layout->L, axis, w, path, 1);
+    std::string err;
+    ++g_launches;
+    cudaError_t e = ll::launch_gather_jit(*P, src, idx, out, nullptr, 1,
+                                          reinterpret_cast<cudaStream_t>(stream), &err, reps, cycles);
+    if (e != cudaSuccess) return fail(LL_ERR_CUDA, "ll_gather_timed: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+    return LL_OK;
+  });
+}
+
 ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst,
                                 ll_layout dst_layout, int elem_bits, int64_t batch, int reps,
                                 long long* cycles, ll_stream stream) {
@@ -682,9 +731,23 @@ ll_status ll_gather_ex(const void* src, const int32_t* idx, void* out, ll_layout
       gp.check = 1;
     }
     ++g_launches;
-    ll_status s = cuda_status(
-        ll::launch_gather(gp, w, P->path == LL_PATH_SHUFFLE, src, idx, out, derr, max_ctas, st),
-        "ll_gather");
+    ll_status s = LL_OK;
+    bool done = false;
+    if (P->path == LL_PATH_SHUFFLE || P->path == LL_PATH_SMEM) {
+      // compiled per plan (gather.cpp); a compile / module failure (nothing
+      // launched) falls back to the direct kernel, which takes any layout
+      ll::GatherPlanHost hp = *P;
+      hp.gp.check = check ? 1 : 0;
+      std::string err;
+      cudaError_t e = ll::launch_gather_jit(hp, src, idx, out, derr, max_ctas, st, &err);
+      if (e == cudaSuccess || err == "cuLaunchKernel failed") {
+        s = e == cudaSuccess ? LL_OK : fail(LL_ERR_CUDA, "ll_gather (compiled kernel): " + err);
+        done = true;
+      }
+    }
+    if (!done)
+      s = cuda_status(ll::launch_gather(gp, w, false, src, idx, out, derr, max_ctas, st),
+                      "ll_gather");
     if (check) {
       int h = 0;
       cudaMemcpyAsync(&h, derr, sizeof(int), cudaMemcpyDeviceToHost, st);

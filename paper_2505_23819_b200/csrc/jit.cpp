@@ -572,6 +572,31 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
 
 }  // namespace
 
+// Compile (cached per source) and fetch a kernel of a generated source; the
+// gather kernels (gather.cpp) use these too.
+cudaError_t jit_kernel(const std::string& src, const char* name, void** fn, std::string* err) {
+  CUfunction f = nullptr;
+  cudaError_t e = get_kernel(src, &f, err, name);
+  *fn = (void*)f;
+  return e;
+}
+
+cudaError_t jit_launch(void* fn, unsigned grid, unsigned block, unsigned smem, cudaStream_t st,
+                       void** args, std::string* err) {
+  static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
+  static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
+  if (!launch || !setattr) {
+    *err = "driver entry points unavailable";
+    return cudaErrorNotSupported;
+  }
+  if (smem > 48 * 1024) setattr((CUfunction)fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+  if (launch((CUfunction)fn, grid, 1, 1, block, 1, 1, smem, (CUstream)st, args, nullptr) != CUDA_SUCCESS) {
+    *err = "cuLaunchKernel failed";
+    return cudaErrorLaunchFailure;
+  }
+  return cudaSuccess;
+}
+
 // Compile only (no device needed): NVRTC log / status for tests.
 bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin_bytes) {
   nvrtcProgram prog;

@@ -1093,55 +1093,7 @@ std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis,
     auto it = g_gcache.find(k);
     if (it != g_gcache.end()) return it->second;
   }
-  if (axis < 0 || axis >= (int)L.out.size()) throw Error(LL_ERR_ARG, "gather: axis out of range");
-  const int n = L.in_bits();
-  if (n != L.out_bits() || !L.surjective())
-    throw Error(LL_ERR_UNSUPPORTED, "gather: the layout must be a bijection (no broadcasting)");
-  auto P = std::make_shared<GatherPlanHost>();
-  P->w = w;
-  GatherPlan& g = P->gp;
-  g = GatherPlan{};
-  const int vb = ilog2i(16 / w);
-  if (n < vb) throw Error(LL_ERR_UNSUPPORTED, "gather: tensor smaller than one 16-byte vector");
-  g.nbits = n;
-  g.batch_stride = int64_t(1) << n;
-  g.ax_shift = L.out_shift(axis);
-  g.ax_bits = L.out[axis].bits;
-  if (g.ax_bits > 31) throw Error(LL_ERR_UNSUPPORTED, "gather: axis too long");
-  for (int k = 0; k < n; ++k) g.L[k] = (int64_t)L.cols[k];
-  auto Linv = f2_right_inverse(L.cols, L.out_bits());
-  bool contig = true;
-  int64_t amask = 0;
-  for (int k = 0; k < g.ax_bits; ++k) {
-    g.Y[k] = (int64_t)Linv[g.ax_shift + k];
-    amask |= g.Y[k];
-    if (g.Y[k] != (int64_t(1) << (ctz64(Linv[g.ax_shift]) + k))) contig = false;
-  }
-  g.y_contig = contig ? 1 : 0;
-  g.y_base = g.ax_bits ? ctz64(Linv[g.ax_shift]) : 0;
-  g.axis_mask_buf = amask;
-  g.vb = vb;
-  g.cand_mask = (int32_t)(amask & ((1 << vb) - 1));
-  g.n_vec = (int64_t(1) << (n - vb)) * batch;
-  const bool shuffle_ok = contig && n >= vb + 5 && (g.y_base + g.ax_bits) <= vb + 5;
-  int path = path_req;
-  // AUTO: the direct (L1) gather -- measured faster than the warp-shuffle
-  // gather on B200 for HBM-resident data (profiles/r01/SUMMARY.md); the
-  // paper's shuffle gather is LL_PATH_SHUFFLE.
-  if (path == LL_PATH_AUTO) path = LL_PATH_GENERIC;
-  if (path == LL_PATH_SHUFFLE && !shuffle_ok)
-    throw Error(LL_ERR_UNSUPPORTED, "gather: shuffle path needs the axis inside one warp's registers and lanes (L_warp^axis = 0, P:722)");
-  if (path != LL_PATH_SHUFFLE && path != LL_PATH_GENERIC)
-    throw Error(LL_ERR_UNSUPPORTED, "gather: path must be auto, shuffle or generic");
-  P->path = path;
-  std::ostringstream js;
-  js << "{\"path\":\"" << (path == LL_PATH_SHUFFLE ? "shuffle" : "direct") << "\",\"nbits\":" << n
-     << ",\"elem_bytes\":" << w << ",\"axis_bits\":" << g.ax_bits << ",\"Y\":[";
-  for (int k = 0; k < g.ax_bits; ++k) js << (k ? "," : "") << g.Y[k];
-  js << "],\"y_contig\":" << g.y_contig << ",\"cand_mask\":" << g.cand_mask
-     << ",\"candidate_shuffles\":" << (1 << popcount64((u64)g.cand_mask)) << ",\"batch\":" << batch
-     << "}";
-  P->json = js.str();
+  auto P = build_gather_plan(L, axis, w, path_req, batch);
   std::lock_guard<std::mutex> lk(g_mu);
   if (g_gcache.size() >= kMaxCached) g_gcache.clear();
   g_gcache[k] = P;

@@ -81,12 +81,41 @@ struct ConvertPlan {
   std::string json;
 };
 
+// Gather plan.  out[h] = src[h ^ Y(a(h) ^ idx[h])]: a(h) = the
+// axis coordinate of L(h) (XOR of acol over h's bits), Y = the buffer vectors
+// of the axis bits (L^{-1} e_axis_k).  Every Y lies in the low unit_bits
+// buffer bits, so a gather never leaves an aligned unit of 2^unit_bits
+// elements.  Paths:
+//   LL_PATH_SHUFFLE  the unit fits one warp's registers (free mapping: lane l
+//                    holds 16-byte vectors l, l + 32, ...): 2^|Y_reg| candidate
+//                    shuffles per output (reading A19), compiled per plan;
+//   LL_PATH_SMEM     the unit fits a CTA's shared memory: one bulk copy
+//                    (cp.async.bulk) per unit, then LDS per output, compiled
+//                    per plan (the paper's "legacy" gather);
+//   LL_PATH_GENERIC  direct: source elements read through L1 (any layout).
 struct GatherPlanHost {
-  int path = LL_PATH_GENERIC;  // LL_PATH_SHUFFLE or LL_PATH_GENERIC (direct)
+  int path = LL_PATH_GENERIC;
   int w = 0;
   GatherPlan gp{};
+  int n = 0, vb = 0;
+  int unit_bits = 0;                // top buffer bit of span(Y) + 1
+  int warp_bits = 0, cta_bits = 0;  // unit of the shuffle / smem kernel (>= unit_bits)
+  int64_t batch = 1;
+  std::vector<u64> Y;               // per axis bit
+  std::vector<uint32_t> acol;       // per buffer bit
+  bool shuffle_ok = false, smem_ok = false;
+  bool paper_criterion = false;     // L_warp^axis = L_block^axis = 0 by the labels (A20)
   std::string json;
 };
+
+// gather.cpp
+std::shared_ptr<GatherPlanHost> build_gather_plan(const Layout& L, int axis, int w, int path_req,
+                                                  int64_t batch);
+std::string gather_shfl_source(const GatherPlanHost& P, int timed);
+std::string gather_smem_source(const GatherPlanHost& P, int timed);
+cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const int32_t* idx,
+                              void* out, int* err_flag, int max_ctas, cudaStream_t st,
+                              std::string* err, int reps = 0, long long* cycles = nullptr);
 
 // Shard `shard` of `n_shards` (a power of two) of a smem / shuffle / copy
 // plan: the top log2(n_shards) bits of the src and dst indices must be the
@@ -123,6 +152,11 @@ bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin
 cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src, void* dst,
                                 int max_ctas, int reps, long long* cycles, cudaStream_t st,
                                 std::string* err);
+
+// jit.cpp: compile (cached) / launch a generated kernel (driver API)
+cudaError_t jit_kernel(const std::string& src, const char* name, void** fn, std::string* err);
+cudaError_t jit_launch(void* fn, unsigned grid, unsigned block, unsigned smem, cudaStream_t st,
+                       void** args, std::string* err);
 
 std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
                                                       int path_req, int64_t batch);

@@ -1,0 +1,12 @@
+#!/bin/bash
+# Round 2: gather generalisation (compiled shuffle / smem gathers) -- tests,
+# bench per path, one-CTA in-kernel study; plus the whole GPU suite.
+O=gpurun_out/r02b
+mkdir -p $O
+timeout 600 python -m pytest tests -m gpu -q -x -k gather > $O/pytest_gather.txt 2>&1
+B="--no-cpu-baseline --e2e-steps 0 --also '' --ncu off --steps 200"
+for p in auto shuffle smem; do eval timeout 300 python bench.py --config 4 --path $p $B > $O/bench_cfg4_$p.json 2> $O/bench_cfg4_$p.err; done
+for p in auto smem; do eval timeout 300 python bench.py --config 4full --path $p $B > $O/bench_cfg4full_$p.json 2> $O/bench_cfg4full_$p.err; done
+timeout 300 python scripts/gather_inkernel.py > $O/gather_inkernel.json 2> $O/gather_inkernel.err
+timeout 1500 python -m pytest tests -m gpu -q --durations=10 > $O/pytest_gpu.txt 2>&1
+echo done > $O/done.txt

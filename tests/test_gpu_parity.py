@@ -406,6 +406,115 @@ def test_gather_full_size_whole_buffer(variant):
     assert _np(out, w).tobytes() == exp.tobytes()
 
 
+def rand_gather_layout(rng, w, n, a, region, mix):
+    """A bijective distributed layout over n bits whose axis (the middle
+    output dim, 2^a long) has all its preimage vectors L^{-1} e_axis inside
+    the low `region` buffer bits; mix: random invertible column operations
+    inside / outside the region (non-unit axis vectors, y_contig = 0)."""
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    x = rng.randint(1, 3)
+    out = [("p", x), ("q", a), ("t", n - a - x)]
+    flat_axis = [n - a - x + k for k in range(a)]          # bit positions of q in the flat index
+    pos = rng.sample(range(region), a)
+    cols = [None] * n
+    for k, p_ in enumerate(pos):
+        cols[p_] = 1 << flat_axis[k]
+    rest = [b for b in range(n) if b not in flat_axis]
+    rng.shuffle(rest)
+    for p_ in range(n):
+        if cols[p_] is None:
+            cols[p_] = 1 << rest.pop()
+    if mix:
+        for _ in range(3 * n):
+            i, j = rng.sample(range(n), 2)
+            if (i < region) == (j < region):
+                cols[i] ^= cols[j]
+    r = rng.randint(max(0, vb - 1), vb + 2)
+    nw = rng.randint(0, min(3, n - r - 5))
+    dims = [("reg", r), ("lane", 5), ("warp", nw), ("block", n - r - 5 - nw)]
+    tmp = OLayout([], out, {})
+    bases, k = {}, 0
+    for nm, b in dims:
+        bases[nm] = [tmp.unflatten(c) for c in cols[k:k + b]]
+        k += b
+    return {"L": {"in_dims": dims, "out_dims": out, "bases": bases}, "axis": 1, "elem_bytes": w,
+            "idx_limit": 1 << a}
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_gather_random_layouts_every_path(w):
+    """P:719-727 on random distributed layouts with the axis bits placed
+    anywhere inside a region (inside a warp's registers and lanes, inside a
+    CTA unit, or anywhere), with unit and mixed (non-unit) axis vectors:
+    every applicable path -- shuffle, smem, direct -- byte-exact against the
+    oracle."""
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    rng = random.Random(900 + w)
+    ran = {"shuffle": 0, "smem": 0, "generic": 0}
+    for case in range(18):
+        n = rng.randint(vb + 9, vb + 12)
+        kind = case % 3
+        region = [rng.randint(vb + 3, vb + 9), rng.randint(vb + 6, min(n, vb + 12)), n][kind]
+        a = rng.randint(1, min(6, region))
+        c = rand_gather_layout(rng, w, n, a, region, mix=case % 2 == 1)
+        L = ll.Layout.from_spec(c["L"])
+        for path in ("shuffle", "smem", "generic"):
+            try:
+                ll.gather_describe(L, 1, 8 * w, path)
+            except ll.LLError:
+                assert path != "generic"
+                continue
+            batch = 1 + case % 2 * 2
+            src, idx, out = run_gather(c, path, seed=case * 7 + w, batch=batch)
+            m = src.size // batch
+            for b in range(batch):
+                exp = oconv.gather_np(src[b * m:(b + 1) * m], idx[b * m:(b + 1) * m],
+                                      _olayout(c["L"]), 1)
+                assert out[b * m:(b + 1) * m].tobytes() == exp.tobytes(), (w, case, path, b)
+            ran[path] += 1
+    assert ran["shuffle"] >= 4 and ran["smem"] >= 6 and ran["generic"] == 18, ran
+
+
+@pytest.mark.parametrize("path", ["shuffle", "smem"])
+@pytest.mark.parametrize("variant", ["tile", "full"])
+def test_gather_compiled_paths_configs(path, variant):
+    """Config 4 (tile axis) and its full-axis variant at reduced rows on the
+    compiled gather paths, where they apply (the full 4096 axis does not fit a
+    warp: shuffle is rejected)."""
+    c = configs.cfg4(r_bits=4, variant=variant)
+    L = ll.Layout.from_spec(c["L"])
+    try:
+        ll.gather_describe(L, c["axis"], 32, path)
+    except ll.LLError:
+        assert (path, variant) == ("shuffle", "full")
+        return
+    src, idx, out = run_gather(c, path)
+    exp = oconv.gather_np(src, idx, _olayout(c["L"]), c["axis"])
+    assert out.tobytes() == exp.tobytes()
+
+
+@pytest.mark.parametrize("path", ["shuffle", "smem"])
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_gather_timed_one_cta(path, w):
+    """ll_gather_timed (the one-CTA in-kernel study): the first unit of the
+    output equals the oracle's gather after `reps` repeated exchanges, and the
+    cycle count is positive."""
+    c = dict(configs.cfg4(r_bits=3), elem_bytes=w)
+    L = ll.Layout.from_spec(c["L"])
+    d = ll.gather_describe(L, c["axis"], 8 * w, path)
+    ub = d["warp_unit_bits"] if path == "shuffle" else d["cta_unit_bits"]
+    n = 1 << L.in_bits
+    src = values_torch(n, 31, w, "cuda")
+    idx = indices_torch(n, 32, 32, "cuda")
+    out = torch.zeros_like(src)
+    cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ll.gather_timed(src, idx, out, L, c["axis"], 8 * w, path, 5, cyc)
+    torch.cuda.synchronize()
+    exp = oconv.gather_np(_np(src, w), idx.cpu().numpy(), _olayout(c["L"]), c["axis"])
+    assert _np(out, w)[:1 << ub].tobytes() == exp[:1 << ub].tobytes()
+    assert int(cyc.item()) > 0
+
+
 def test_gather_out_of_range_check(monkeypatch):
     monkeypatch.setenv("LL_GATHER_CHECK", "1")
     c = configs.cfg4(r_bits=0)

@@ -629,7 +629,7 @@ def test_binding_rejects_bad_tensor_arguments():
     with pytest.raises(ll.LLError, match="bytes <"):
         ll.convert(FakeCuda(n, 2), A, FakeCuda(n - 8, 2), B, 16)
     with pytest.raises(ll.LLError, match="element size"):
-        ll.convert(FakeCuda(n, 4), A, FakeCuda(n, 2), B, 16)
+        ll.convert(FakeCuda(n, 4), A, FakeCuda(n, 2), B, 16)  # 32-bit elements for 16-bit data
     with pytest.raises(ll.LLError, match="not contiguous"):
         ll.convert(FakeCuda(n, 2, False), A, FakeCuda(n, 2), B, 16)
     with pytest.raises(ll.LLError, match="gather idx"):
@@ -637,3 +637,30 @@ def test_binding_rejects_bad_tensor_arguments():
         L = ll.Layout.from_spec(g["L"])
         m = 1 << L.in_bits
         ll.gather(FakeCuda(m, 4), FakeCuda(m, 2), FakeCuda(m, 4), L, 2, 32)
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_gather_kernels_compile_for_random_layouts(w):
+    """The per-plan gather kernels (shuffle and smem, plain and in-kernel
+    timed) compile with NVRTC for sm_100a on random layouts (no device);
+    path eligibility follows the unit of the axis vectors (A20)."""
+    from tests.test_gpu_parity import rand_gather_layout
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    rng = random.Random(40 + w)
+    seen = set()
+    for case in range(4):
+        n = rng.randint(vb + 9, vb + 11)
+        region = [vb + 4, vb + 7, n, vb + 9][case]
+        c = rand_gather_layout(rng, w, n, rng.randint(1, 4), region, mix=case % 2 == 1)
+        L = ll.Layout.from_spec(c["L"])
+        for path in ("shuffle", "smem"):
+            try:
+                d = ll.gather_describe(L, 1, 8 * w, path)
+            except ll.LLError:
+                continue
+            assert d["path"] == path and d["unit_bits"] <= n
+            for timed in (False, True):
+                r = ll.gather_jit_source(L, 1, 8 * w, path, compile=True, timed=timed)
+                assert r["compiled"] and r["cubin_bytes"] > 0
+            seen.add(path)
+    assert seen == {"shuffle", "smem"}
