@@ -82,7 +82,16 @@ std::shared_ptr<GatherPlanHost> build_gather_plan(const Layout& L, int axis, int
     if (g.Y[k] != (int64_t(1) << (ctz64(Linv[g.ax_shift]) + k))) contig = false;
   }
   for (int b = 0; b < n; ++b) P->acol.push_back((uint32_t)(L.cols[b] >> g.ax_shift) & mask);
-  g.y_contig = contig ? 1 : 0;
+  // the direct kernel's field insert h* = (h & ~M) | (idx << y_base) needs
+  // a(h) to be exactly that field: contiguous unit Y and no other column
+  // with an axis component
+  bool onehot = contig;
+  for (int b = 0; b < n && onehot; ++b) {
+    const int y0 = g.ax_bits ? ctz64(Linv[g.ax_shift]) : 0;
+    const bool in_field = b >= y0 && b < y0 + g.ax_bits;
+    onehot = P->acol[b] == (in_field ? (1u << (b - y0)) : 0u);
+  }
+  g.y_contig = onehot ? 1 : 0;
   g.y_base = g.ax_bits ? ctz64(Linv[g.ax_shift]) : 0;
   g.axis_mask_buf = amask;
   g.vb = vb;
@@ -175,8 +184,11 @@ void emit_idx_load(std::ostringstream& o, int NE, const std::string& dst, const 
 // axis bit
 std::string hstar_expr(const GatherPlanHost& P, const std::string& hl, const std::string& d) {
   std::ostringstream e;
-  if (P.gp.y_contig) {
-    e << "((" << hl << " & ~" << (uint32_t)P.gp.axis_mask_buf << "u) | (" << d << " << " << P.gp.y_base << "))";
+  bool contig = !P.Y.empty();
+  for (size_t k = 0; k < P.Y.size(); ++k) contig = contig && P.Y[k] == (P.Y[0] << k) && P.Y[0] && !(P.Y[0] & (P.Y[0] - 1));
+  if (contig) {
+    // Y_k = 1 << (y0 + k): Y(d) = d << y0
+    e << "(" << hl << " ^ (" << d << " << " << ctz64(P.Y[0]) << "))";
   } else {
     e << "(" << hl;
     for (size_t k = 0; k < P.Y.size(); ++k)
@@ -437,7 +449,9 @@ cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const in
     grid = (int)std::max<long long>(1, std::min<long long>(n_units, (long long)sms * per_sm));
   }
   if (timed) {
-    n_units = std::min<long long>(n_units, 1);
+    // one CTA: 8 warp units (one per warp) for the shuffle gather, one CTA
+    // unit for the shared-memory gather
+    n_units = std::min<long long>(n_units, shfl ? 8 : 1);
     grid = 1;
   }
   if (max_ctas > 0) grid = std::min(grid, max_ctas);

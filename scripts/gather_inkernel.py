@@ -59,8 +59,10 @@ def main():
             except ll.LLError as e:
                 res.append({"K": 1 << k_bits, "path": path, "unsupported": str(e)[:120]})
                 continue
+            # one CTA of 8 warps: 8 warp units (shuffle) or one CTA unit (smem)
             ub = d["warp_unit_bits"] if path == "shuffle" else d["cta_unit_bits"]
-            warps = 1 if path == "shuffle" else 8
+            elems = (8 << ub) if path == "shuffle" else (1 << ub)
+            warps = 8
             out = torch.zeros_like(src)
             cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
             best = None
@@ -72,13 +74,13 @@ def main():
                     vals.append(int(cyc.item()))
                 vals.sort()
                 best = (best or []) + [(r, vals[len(vals) // 2])]
-            ok = out.cpu().numpy().view(np.uint32)[:1 << ub].tobytes() == exp[:1 << ub].tobytes()
+            ok = out.cpu().numpy().view(np.uint32)[:elems].tobytes() == exp[:elems].tobytes()
             # cycles per repetition from the slope between reps and 2 reps (drops fixed costs)
             (r1, c1), (r2, c2) = best
             per_rep = (c2 - c1) / (r2 - r1)
-            res.append({"K": 1 << k_bits, "path": path, "unit_elems": 1 << ub, "warps": warps,
+            res.append({"K": 1 << k_bits, "path": path, "elems_per_rep": elems, "warps": warps,
                         "cycles_per_rep": per_rep,
-                        "warp_cycles_per_elem": per_rep * warps / (1 << ub),
+                        "warp_cycles_per_elem": per_rep * warps / elems,
                         "candidate_shuffles": d["candidate_shuffles"] if path == "shuffle" else None,
                         "paper_criterion": d["paper_criterion"], "parity_ok": ok})
     print(json.dumps({"reps": reps, "results": res}, indent=1))
