@@ -223,16 +223,19 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
                         int elem_bits, const ll_convert_options* opts, ll_stream stream);
 
 /* Same with gather options (path, batch).  Paths:
- *   LL_PATH_AUTO     the direct kernel (measured fastest on B200)
+ *   LL_PATH_AUTO     measured on B200: the direct kernel when the
+ *                    axis stays inside one warp's 16-byte vectors and lanes,
+ *                    else the shared-memory gather where it applies, else direct
  *   LL_PATH_SHUFFLE  warp-shuffle gather: the axis vectors L^{-1} e_axis lie in
  *                    one warp's registers and lanes (L_warp^axis =
  *                    L_block^axis = 0, in the coalesced mapping: within the low
  *                    log2(16 / elem_bytes) + 9 buffer bits); 2^|L_reg^axis|
  *                    candidate shuffles per output (reading A19); compiled per
  *                    plan (NVRTC)
- *   LL_PATH_SMEM     shared-memory gather: the axis inside an aligned unit of
- *                    <= 64 KiB (L_block^axis = 0); one cp.async.bulk per unit,
- *                    one ld.shared per output; compiled per plan
+ *   LL_PATH_SMEM     shared-memory gather: the axis inside an aligned unit
+ *                    whose source + indices fit 96 KiB (L_block^axis = 0);
+ *                    two cp.async.bulk (source, indices) per unit into a
+ *                    2-stage ring, one ld.shared per output; compiled per plan
  *   LL_PATH_GENERIC  direct: source elements read through L1, any layout
  * LL_ERR_UNSUPPORTED when the requested path does not apply.  A compile or
  * module failure of a compiled kernel falls back to the direct kernel. */

@@ -33,7 +33,7 @@ using detail::ilog2i;
 namespace {
 
 constexpr int kMaxWarpVec = 16;          // 16-byte vectors per lane per warp unit
-constexpr int kSmemUnitMax = 64 * 1024;  // bytes per stage of the smem gather
+constexpr int kSmemUnitMax = 96 * 1024;  // bytes per stage (source + indices) of the smem gather
 
 int top_bit(u64 x) { return x ? 63 - __builtin_clzll(x) : -1; }
 
@@ -100,9 +100,9 @@ std::shared_ptr<GatherPlanHost> build_gather_plan(const Layout& L, int axis, int
   // the unit closed under the gather, and the two unit-local executors
   P->unit_bits = top_bit((u64)amask) + 1;
   P->warp_bits = std::max(P->unit_bits, vb + 5);
-  P->cta_bits = std::max(P->unit_bits, vb + 8);
+  P->cta_bits = std::max(P->unit_bits, vb + 8 + std::max(0, planner_knob("gather_cta_extra", 0)));
   P->shuffle_ok = n >= P->warp_bits && P->warp_bits - vb - 5 <= ilog2i(kMaxWarpVec) && w <= 8;
-  P->smem_ok = n >= P->cta_bits && (int64_t(w) << P->cta_bits) <= kSmemUnitMax;
+  P->smem_ok = n >= P->cta_bits && (int64_t(w + 4) << P->cta_bits) <= kSmemUnitMax;
   // the paper's criterion by the labels: no warp or block bit moves the axis
   {
     bool ok = true;
@@ -115,10 +115,12 @@ std::shared_ptr<GatherPlanHost> build_gather_plan(const Layout& L, int axis, int
     P->paper_criterion = ok;
   }
   int path = path_req;
-  // AUTO: the direct (L1) gather -- measured fastest on B200 for HBM-resident
-  // data; the paper's shuffle gather and the shared-memory
-  // gather are LL_PATH_SHUFFLE / LL_PATH_SMEM
-  if (path == LL_PATH_AUTO) path = LL_PATH_GENERIC;
+  // AUTO (measured on B200): the direct (L1) gather when the
+  // unit is warp-local (config 4: 6464 vs 6297 smem, 6061 shuffle GB/s), the
+  // shared-memory gather for longer axes (full 4096 axis: 6080 vs 4662 direct)
+  if (path == LL_PATH_AUTO)
+    path = P->unit_bits <= vb + 5 || !P->smem_ok || !planner_knob("gather_auto_smem", 1) ? LL_PATH_GENERIC
+                                                                                      : LL_PATH_SMEM;
   if (path == LL_PATH_SHUFFLE && !P->shuffle_ok)
     throw Error(LL_ERR_UNSUPPORTED,
                 "gather: shuffle path needs the axis inside one warp's registers and lanes "
@@ -126,7 +128,7 @@ std::shared_ptr<GatherPlanHost> build_gather_plan(const Layout& L, int axis, int
                 " buffer bits; P:722 L_warp^axis = 0)");
   if (path == LL_PATH_SMEM && !P->smem_ok)
     throw Error(LL_ERR_UNSUPPORTED,
-                "gather: smem path needs the axis inside one CTA's unit of <= 64 KiB "
+                "gather: smem path needs the axis inside one CTA's unit of <= 96 KiB of source + indices "
                 "(L_block^axis = 0, reading A20)");
   if (path != LL_PATH_SHUFFLE && path != LL_PATH_SMEM && path != LL_PATH_GENERIC)
     throw Error(LL_ERR_UNSUPPORTED, "gather: path must be auto, shuffle, smem or generic");
@@ -213,7 +215,8 @@ std::string gather_shfl_source(const GatherPlanHost& P, int timed) {
   const int NV = 1 << (WU - vb - 5);
   const int NS = NV * NE;                 // element slots per lane
   const int NWD = NV * 4;                 // 32-bit words per lane
-  const int MU = timed ? 1 : std::max(1, std::min(4 / NV, 64 / (NV * NE)));
+  const int mu_knob = planner_knob("gather_shfl_mu", 0);
+  const int MU = timed ? 1 : mu_knob > 0 ? mu_knob : std::max(1, std::min(4 / NV, 64 / (NV * NE)));
   const uint32_t mask = (uint32_t)((1ull << P.gp.ax_bits) - 1);
   std::vector<u64> yslot;
   for (u64 y : P.Y) yslot.push_back((y & (u64)(NE - 1)) | ((y >> (vb + 5)) << vb));
@@ -321,15 +324,24 @@ std::string gather_shfl_source(const GatherPlanHost& P, int timed) {
   return o.str();
 }
 
-// Shared-memory gather: a CTA unit of 2^CU elements (CU = cta_bits) is copied
-// into shared memory by one cp.async.bulk (1-D TMA, mbarrier complete_tx) into
-// a 2-stage ring; each thread then takes its NVT 16-byte output vectors of the
-// unit: idx vectors from global memory (coalesced), one LDS per output
-// element at h* (in-unit), streaming 16-byte stores.
+// Shared-memory gather: a CTA unit of 2^CU elements (CU = cta_bits) and its
+// 2^CU indices are copied into shared memory by two cp.async.bulk (1-D TMA,
+// one mbarrier with complete_tx) into a 2-stage ring; each thread then takes
+// its NVT 16-byte output vectors of the unit: indices by ld.shared (16-byte,
+// conflict-free), one ld.shared per output element at h* (in-unit),
+// streaming 16-byte stores.  No thread issues a global load.
+//
+// timed: the one-CTA in-kernel study from REGISTERS (the paper's setting:
+// the tensor is distributed over the threads): every repetition stores the
+// thread's vectors of the unit to shared memory, synchronises, gathers with
+// ld.shared and synchronises again -- the legacy staging round trip the
+// shuffle gather avoids.
 std::string gather_smem_source(const GatherPlanHost& P, int timed) {
   const int W = P.w, NE = 16 / W, vb = P.vb, CU = P.cta_bits;
   const int NVT = 1 << (CU - vb - 8);
-  const uint32_t UB = (uint32_t)W << CU;
+  const uint32_t UB = (uint32_t)W << CU;       // source bytes per unit
+  const uint32_t IB = 4u << CU;                // index bytes per unit
+  const uint32_t SB = UB + IB;                 // stage bytes
   const uint32_t mask = (uint32_t)((1ull << P.gp.ax_bits) - 1);
   auto aconst = [&](int e, int j) {   // axis contribution of element bits and vector-index bits >= 8
     uint32_t a = 0;
@@ -344,10 +356,9 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
   if (timed) o << ", int reps, long long* cycles";
   o << ") {\n"
     << "  extern __shared__ __align__(128) unsigned char smem[];\n"
-    << "  typedef " << kElemT[W] << " T;\n"
     << "  const int tid = threadIdx.x;\n"
     << "  const unsigned sb = (unsigned)__cvta_generic_to_shared(smem);\n"
-    << "  const unsigned bar0 = sb + " << 2 * UB << "u;\n"
+    << "  const unsigned bar0 = sb + " << 2 * SB << "u;\n"
     << "  unsigned a_tid = 0;\n";
   for (int c = 0; c < 8; ++c)
     if (P.acol[vb + c]) o << "  if (tid & " << (1 << c) << ") a_tid ^= " << P.acol[vb + c] << "u;\n";
@@ -358,12 +369,13 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
     << "  }\n"
     << "  __syncthreads();\n"
     << "  auto issue = [&](long long t, int s) {\n"
-    << "    const unsigned bar = bar0 + 8u * s;\n"
-    << "    asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(bar), \"r\"(" << UB
+    << "    const unsigned bar = bar0 + 8u * s, st = sb + " << SB << "u * s;\n"
+    << "    asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(bar), \"r\"(" << SB
     << "u) : \"memory\");\n"
     << "    asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\" "
-       ":: \"r\"(sb + " << UB << "u * s), \"l\"(src + (t << " << CU << ") * " << W << "), \"r\"(" << UB
-    << "u), \"r\"(bar) : \"memory\");\n"
+       ":: \"r\"(st), \"l\"(src + (t << " << CU << ") * " << W << "), \"r\"(" << UB << "u), \"r\"(bar) : \"memory\");\n"
+    << "    asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\" "
+       ":: \"r\"(st + " << UB << "u), \"l\"(idx + (t << " << CU << ")), \"r\"(" << IB << "u), \"r\"(bar) : \"memory\");\n"
     << "  };\n"
     << "  const long long g0 = blockIdx.x, gs = gridDim.x;\n"
     << "  if (tid == 0) { if (g0 < n_units) issue(g0, 0); if (g0 + gs < n_units) issue(g0 + gs, 1); }\n"
@@ -372,18 +384,38 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
     << "    const int s = k & 1;\n"
     << "    const unsigned ph = (unsigned)(k >> 1) & 1u;\n"
     << "    asm volatile(\"{\\n.reg .pred p;\\nLL_GW_%=:\\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\\n@!p bra LL_GW_%=;\\n}\\n\" :: \"r\"(bar0 + 8u * s), \"r\"(ph) : \"memory\");\n"
-    << "    const unsigned su = sb + " << UB << "u * s;\n"
+    << "    const unsigned su = sb + " << SB << "u * s, si = su + " << UB << "u;\n"
     << "    const long long base = t << " << CU << ";\n";
   emit_unit_axis(o, P, CU, "t");
   o << "    int I[" << NVT << "][" << NE << "];\n";
-  for (int j = 0; j < NVT; ++j) {
-    std::ostringstream dst, ptr;
-    dst << "(&I[" << j << "][0])";
-    ptr << "idx + base + (((long long)tid + " << (j << 8) << ") << " << vb << ")";
-    emit_idx_load(o, NE, dst.str(), ptr.str());
+  for (int j = 0; j < NVT; ++j)
+    for (int q = 0; q < NE; q += (NE >= 4 ? 4 : 2)) {
+      if (NE >= 4)
+        o << "    asm volatile(\"ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(I[" << j << "][" << q
+          << "]), \"=r\"(I[" << j << "][" << q + 1 << "]), \"=r\"(I[" << j << "][" << q + 2 << "]), \"=r\"(I["
+          << j << "][" << q + 3 << "]) : \"r\"(si + ((((unsigned)tid + " << (j << 8) << "u) << " << vb << ") + "
+          << q << "u) * 4u));\n";
+      else
+        o << "    asm volatile(\"ld.shared.v2.u32 {%0,%1}, [%2];\" : \"=r\"(I[" << j << "][" << q
+          << "]), \"=r\"(I[" << j << "][" << q + 1 << "]) : \"r\"(si + ((((unsigned)tid + " << (j << 8)
+          << "u) << " << vb << ") + " << q << "u) * 4u));\n";
+    }
+  if (timed) {
+    // registers-resident input: the thread's own vectors of the unit
+    o << "    unsigned RV[" << NVT << "][4];\n";
+    for (int j = 0; j < NVT; ++j)
+      o << "    asm volatile(\"ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(RV[" << j << "][0]), \"=r\"(RV["
+        << j << "][1]), \"=r\"(RV[" << j << "][2]), \"=r\"(RV[" << j << "][3]) : \"r\"(su + (((unsigned)tid + "
+        << (j << 8) << "u) << 4)));\n";
+    o << "    __syncthreads();\n"
+      << "    long long c0 = clock64(); unsigned acc = 0;\n    for (int rep = 0; rep < reps; ++rep) {\n"
+      << "    unsigned z_; asm volatile(\"mov.b32 %0, 0;\" : \"=r\"(z_));\n";
+    for (int j = 0; j < NVT; ++j)
+      o << "    asm volatile(\"st.shared.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"r\"(su + (((unsigned)tid + " << (j << 8)
+        << "u) << 4)), \"r\"(RV[" << j << "][0] ^ z_), \"r\"(RV[" << j << "][1]), \"r\"(RV[" << j << "][2]), \"r\"(RV["
+        << j << "][3]) : \"memory\");\n";
+    o << "    __syncthreads();\n";
   }
-  if (timed) o << "    long long c0 = clock64(); unsigned acc = 0;\n    for (int rep = 0; rep < reps; ++rep) {\n"
-               << "    unsigned z_; asm volatile(\"mov.b32 %0, 0;\" : \"=r\"(z_));\n";
   for (int j = 0; j < NVT; ++j) {
     o << "    { unsigned O[4] = {0, 0, 0, 0};\n";
     for (int e = 0; e < NE; ++e) {
@@ -411,7 +443,7 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
       << "    }\n";
   }
   if (timed)
-    o << "    }\n    long long c1 = clock64();\n"
+    o << "    __syncthreads();\n    }\n    long long c1 = clock64();\n"
       << "    if (tid == 0 && cycles) cycles[blockIdx.x] = c1 - c0;\n"
       << "    if (acc == 0x9e3779b9u && reps < 0) err[1] = 1;\n";
   o << "    __syncthreads();   // every thread is done with stage s\n"
@@ -440,11 +472,12 @@ cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const in
   unsigned smem = 0;
   if (shfl) {
     const int NV = 1 << (P.warp_bits - P.vb - 5);
-    const int MU = std::max(1, std::min(4 / NV, 64 / (NV * (16 / P.w))));
+    const int mu_knob = planner_knob("gather_shfl_mu", 0);
+    const int MU = mu_knob > 0 ? mu_knob : std::max(1, std::min(4 / NV, 64 / (NV * (16 / P.w))));
     const long long warps = (n_units + MU - 1) / MU;
     grid = (int)std::max<long long>(1, std::min<long long>((warps + 7) / 8, (long long)sms * 8));
   } else {
-    smem = 2u * ((unsigned)P.w << P.cta_bits) + 16u;
+    smem = 2u * ((unsigned)(P.w + 4) << P.cta_bits) + 16u;
     const int per_sm = std::max(1, std::min(8, (int)((200u * 1024u) / smem)));
     grid = (int)std::max<long long>(1, std::min<long long>(n_units, (long long)sms * per_sm));
   }

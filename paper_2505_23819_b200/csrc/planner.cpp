@@ -154,7 +154,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "upcast_jit" && name != "upcast_jit_tpg" && name != "smem_jit_minb" &&
       name != "regs_trans" && name != "smem_jit_depth" && name != "smem_jit_single" && name != "jit_force_fail" &&
       name != "pdl" && name != "run_bytes_dst" && name != "run_bytes_src" &&
-      name != "auto_asym" && name != "tma_run_bytes_dst")
+      name != "auto_asym" && name != "tma_run_bytes_dst" && name != "gather_shfl_mu" &&
+      name != "gather_cta_extra" && name != "gather_auto_smem")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;

@@ -223,7 +223,8 @@ def test_gather_plan_config4():
     assert ll.gather_describe(L, c["axis"], 32)["path"] == "direct"     # AUTO: measured fastest
     cf = configs.cfg4(variant="full")
     Lf = ll.Layout.from_spec(cf["L"])
-    assert ll.gather_describe(Lf, cf["axis"], 32)["path"] == "direct"
+    df = ll.gather_describe(Lf, cf["axis"], 32)
+    assert df["path"] == "smem" and df["unit_bits"] == 12              # AUTO: the 16 KiB row in smem
     with pytest.raises(ll.LLError):
         ll.gather_describe(Lf, cf["axis"], 32, "shuffle")
 
