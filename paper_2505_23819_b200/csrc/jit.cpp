@@ -272,11 +272,30 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
     o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
       << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; }\n";
   o << "  };\n";
+  // 256-bit accesses where a thread's vectors u, u + 1 are contiguous (knob vec32)
+  bool ld32 = NV >= 2, st32 = NV >= 2;
+  for (int u = 0; u + 1 < NV; u += 2) {
+    ld32 = ld32 && p.ld_vec[u + 1] == p.ld_vec[u] + 16;
+    st32 = st32 && p.st_vec[u + 1] == p.st_vec[u] + 16;
+  }
+  const bool noload = planner_knob("smem_jit_noload", 0) != 0;   // test hook: no global loads
   auto load = [&](const char* ind, const std::string& R) {
-    for (int u = 0; u < NV; ++u)
+    if (noload) {
+      for (int i = 0; i < NW; ++i)
+        o << ind << R << "[" << i << "] = (unsigned)so * 2654435761u + tb * " << 4 * NW + 1 << "u + " << i << "u;\n";
+      return;
+    }
+    for (int u = 0; u < NV; u += ld32 ? 2 : 1) {
+      if (ld32) {
+        o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\" : ";
+        for (int q = 0; q < 8; ++q) o << (q ? ", " : "") << "\"=r\"(" << R << "[" << 4 * u + q << "])";
+        o << " : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
+        continue;
+      }
       o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(" << R << "["
         << 4 * u << "]), \"=r\"(" << R << "[" << 4 * u + 1 << "]), \"=r\"(" << R << "[" << 4 * u + 2
         << "]), \"=r\"(" << R << "[" << 4 * u + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
+    }
   };
   const int ga = GWd >= 2 ? p.gsel_a : -1, gb = GWd >= 4 ? p.gsel_b : -1;
   // one tile: swaps, STS, prefetch of tile t + ahead * n_groups into the same
@@ -309,10 +328,18 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
       else o << "b32 %0, [%1];\" : \"=r\"(Q[" << j << "])";
       o << " : \"r\"(sbase + buf + (srx ^ " << p.sr_gran[j] << "u)) : \"memory\");\n";
     }
-    for (int u = 0; u < NV; ++u)
+    for (int u = 0; u < NV; u += st32 ? 2 : 1) {
+      if (st32) {
+        o << "    asm volatile(\"st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\" :: \"l\"(dthr + dcur + "
+          << p.st_vec[u] << ")";
+        for (int q = 0; q < 8; ++q) o << ", \"r\"(Q[" << 4 * u + q << "])";
+        o << " : \"memory\");\n";
+        continue;
+      }
       o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dcur + "
         << p.st_vec[u] << "), \"r\"(Q[" << 4 * u << "]), \"r\"(Q[" << 4 * u + 1 << "]), \"r\"(Q["
         << 4 * u + 2 << "]), \"r\"(Q[" << 4 * u + 3 << "]) : \"memory\");\n";
+    }
     o << "    buf ^= " << p.tile_bytes << "u; }\n";
   };
   const int depth = std::max(1, std::min(2, planner_knob("smem_jit_depth", 1)));

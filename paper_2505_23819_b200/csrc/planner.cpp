@@ -155,7 +155,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "regs_trans" && name != "smem_jit_depth" && name != "smem_jit_single" && name != "jit_force_fail" &&
       name != "pdl" && name != "run_bytes_dst" && name != "run_bytes_src" &&
       name != "auto_asym" && name != "tma_run_bytes_dst" && name != "gather_shfl_mu" &&
-      name != "gather_cta_extra" && name != "gather_auto_smem")
+      name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
+      name != "smem_jit_noload")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -498,6 +499,40 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   if (ld_lane.size() != 5 || st_lane.size() != 5 || (int)ld_warp.size() != g ||
       (int)st_warp.size() != g)
     return false;
+  // 32-byte thread vectors (knob vec32; sm_100 256-bit LDG / STG): the first
+  // register bit above the 16-byte vector becomes the next buffer bit, so a
+  // thread's vectors u and u ^ 1 are contiguous -- on the load side the source
+  // bit vb, on the store side the destination bit vb.  The bit trades places
+  // with a register bit the granule does not need; lanes and warps are
+  // re-sorted (lowest buffer bits first, the coalescing order).
+  if (planner_knob("vec32", 0) && r > vb) {
+    auto to32 = [&](std::vector<int>& reg, std::vector<int>& lane, std::vector<int>& warp, int bit,
+                    const std::vector<int>& keep, auto key) {
+      if (bit < 0 || !contains(T, bit)) return false;
+      auto it = std::find(reg.begin(), reg.end(), bit);
+      if (it == reg.end()) {
+        int x = -1;
+        for (int q = (int)reg.size() - 1; q >= vb; --q)
+          if (!contains(keep, reg[q])) { x = q; break; }
+        if (x < 0) return false;
+        std::vector<int>* side = contains(lane, bit) ? &lane : &warp;
+        *std::find(side->begin(), side->end(), bit) = reg[x];
+        reg.erase(reg.begin() + x);
+        std::vector<int> tw = lane;
+        tw.insert(tw.end(), warp.begin(), warp.end());
+        std::sort(tw.begin(), tw.end(), [&](int a, int b) { return key(a) < key(b); });
+        lane.assign(tw.begin(), tw.begin() + 5);
+        warp.assign(tw.begin() + 5, tw.end());
+      } else {
+        reg.erase(it);
+      }
+      reg.insert(reg.begin() + vb, bit);
+      return true;
+    };
+    std::vector<int> keep_ld = need, keep_st = VD;
+    to32(ld_reg, ld_lane, ld_warp, sinv[vb], keep_ld, [&](int k) { return sigma[k]; });
+    if (sigma[vb] >= 0) to32(st_reg, st_lane, st_warp, vb, keep_st, [&](int k) { return k; });
+  }
   // ---- sub-word register-bit swaps on the load side (prmt): the first sw
   // positions of rho must hold V's sub-word bits; V's word-level bits are
   // then picked at compile time by the STS operand selection (gsel).

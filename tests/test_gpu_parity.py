@@ -124,6 +124,27 @@ def test_convert_random_pairs(w):
         assert dst.tobytes() == expect_convert(c, src).tobytes()
 
 
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_vec32(w):
+    """Knob vec32: 32-byte thread vectors (sm_100 256-bit LDG / STG) on the
+    compiled smem kernel -- random pairs and the config families, byte-exact."""
+    ll.tune("vec32", 1)
+    try:
+        rng = random.Random(350 + w)
+        for _ in range(10):
+            c = rand_pair(rng, rng.randint(12, 16), w)
+            src, dst = run_convert(c, seed=rng.randint(0, 1000))
+            assert dst.tobytes() == expect_convert(c, src).tobytes()
+        for name, mk in CASES:
+            c = mk()
+            if c["elem_bytes"] != w and not (w == 2 and c["elem_bytes"] == 2):
+                continue
+            src, dst = run_convert(c)
+            assert dst.tobytes() == expect_convert(c, src).tobytes(), name
+    finally:
+        ll.tune("vec32", 0)
+
+
 @pytest.mark.parametrize("w", [1, 2, 4])
 def test_convert_random_pairs_shuffle(w):
     rng = random.Random(500 + w)
