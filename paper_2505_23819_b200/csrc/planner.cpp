@@ -156,7 +156,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "pdl" && name != "run_bytes_dst" && name != "run_bytes_src" &&
       name != "auto_asym" && name != "tma_run_bytes_dst" && name != "gather_shfl_mu" &&
       name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
-      name != "smem_jit_noload")
+      name != "smem_jit_noload" && name != "smem_jit_nostore")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
