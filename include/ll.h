@@ -135,6 +135,24 @@ ll_status ll_reshape(ll_layout l, int n_out, const char* const* out_names, const
 ll_status ll_expand_dims(ll_layout l, int axis, const char* name, ll_layout* out);
 ll_status ll_broadcast(ll_layout l, int axis, int bits, ll_layout* out);
 ll_status ll_join(ll_layout l, const char* name, ll_layout* out);
+/* Sliced layout: output dim `axis` removed (the layout of a
+ * reduction's result along it).  The matrix loses that dim's rows; columns
+ * that only reached it become zero (broadcast), and the result is still
+ * surjective.  LL_ERR_ARG for a bad axis.  Caller owns *out. */
+ll_status ll_slice(ll_layout l, int axis, ll_layout* out);
+/* Blocked layout (Appendix proposition): a tensor of rank dims,
+ * shape_bits[i] = log2 of dim i; R / T / W = log2 registers / threads /
+ * warps per dim with R[i] + T[i] + W[i] = shape_bits[i]; order[0] = the
+ * fastest dim.  Input dims reg, lane, warp; output dims dim0..dim{rank-1}.
+ * LL_ERR_SHAPE if the sizes do not add up, LL_ERR_ARG for a bad order. */
+ll_status ll_blocked(int rank, const int* shape_bits, const int* R, const int* T, const int* W,
+                     const int* order, ll_layout* out);
+/* mma.sync register / thread tiles (Appendix proposition, reading
+ * A8): operand 0 = lhs (A fragment), 1 = rhs (B fragment), 2 = output
+ * (accumulator, m16n8); bitwidth 8, 16 or 32.  Input dims reg, lane; output
+ * dims dim0 (rows) and dim1 (columns).  Combine with ll_product for warps /
+ * repetitions and ll_slice for sliced mma layouts. */
+ll_status ll_mma_tile(int operand, int bitwidth, ll_layout* out);
 ll_status ll_split(ll_layout l, ll_layout* out);
 
 /* Apply to one point ("w = Av"): in_coords[n_in] -> out_coords[n_out].

@@ -92,3 +92,14 @@ def split(L):
         bases[n] = [tuple(v[:-1]) for k, v in enumerate(vs) if not (n == n0 and k == k0)]
     in_dims = [(n, b - 1) if n == n0 else (n, b) for n, b in L.in_dims]
     return Layout(in_dims, L.out_dims[:-1], bases)
+
+
+def slice_(L, axis):
+    """Sliced layout: "Removing a dimension is a linear map" --
+    the output dim ``axis`` is dropped from every basis vector, so the matrix
+    loses that dim's rows; columns that only reached it become
+    zero."""
+    out = [d for i, d in enumerate(L.out_dims) if i != axis]
+    bases = {n: [tuple(c for i, c in enumerate(v) if i != axis) for v in vs]
+             for n, vs in L.bases.items()}
+    return Layout(L.in_dims, out, bases)

@@ -68,6 +68,10 @@ _lib.ll_expand_dims.argtypes = [_VP, ctypes.c_int, ctypes.c_char_p, ctypes.POINT
 _lib.ll_broadcast.argtypes = [_VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_VP)]
 _lib.ll_join.argtypes = [_VP, ctypes.c_char_p, ctypes.POINTER(_VP)]
 _lib.ll_split.argtypes = [_VP, ctypes.POINTER(_VP)]
+_lib.ll_slice.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(_VP)]
+_IP = ctypes.POINTER(ctypes.c_int)
+_lib.ll_blocked.argtypes = [ctypes.c_int, _IP, _IP, _IP, _IP, _IP, ctypes.POINTER(_VP)]
+_lib.ll_mma_tile.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(_VP)]
 _lib.ll_convert_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_void_p, ctypes.c_void_p]
@@ -89,7 +93,7 @@ _lib.ll_gather_jit_source.argtypes = [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_
                                       ctypes.POINTER(ctypes.c_size_t)]
 _lib.ll_gather_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_int, _VP, _VP]
-for _f in ("ll_gather_jit_source", "ll_gather_timed", "ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+for _f in ("ll_slice", "ll_blocked", "ll_mma_tile", "ll_gather_jit_source", "ll_gather_timed", "ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_shard_describe_2d", "ll_gather_host", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
@@ -284,6 +288,31 @@ def join(layout, name):
 def split(layout):
     h = ctypes.c_void_p()
     _check(_lib.ll_split(layout.handle, ctypes.byref(h)))
+    return _wrap(h)
+
+
+def slice_layout(layout, axis):
+    """ll_slice: sliced layout, output dim `axis` removed."""
+    h = ctypes.c_void_p()
+    _check(_lib.ll_slice(layout.handle, int(axis), ctypes.byref(h)))
+    return _wrap(h)
+
+
+def blocked(shape_bits, R, T, W, order):
+    """ll_blocked: blocked layout; order[0] = fastest dim."""
+    n = len(shape_bits)
+    arr = lambda v: (ctypes.c_int * max(1, n))(*[int(x) for x in v])  # noqa: E731
+    h = ctypes.c_void_p()
+    _check(_lib.ll_blocked(n, arr(shape_bits), arr(R), arr(T), arr(W), arr(order), ctypes.byref(h)))
+    return _wrap(h)
+
+
+def mma_tile(operand, bitwidth):
+    """ll_mma_tile: mma.sync fragment tile (P:1031-1047, reading A8);
+    operand "lhs", "rhs" or "out"."""
+    op = {"lhs": 0, "rhs": 1, "out": 2}[operand] if isinstance(operand, str) else int(operand)
+    h = ctypes.c_void_p()
+    _check(_lib.ll_mma_tile(op, int(bitwidth), ctypes.byref(h)))
     return _wrap(h)
 
 

@@ -251,6 +251,34 @@ ll_status ll_expand_dims(ll_layout l, int axis, const char* name, ll_layout* out
   });
 }
 
+ll_status ll_slice(ll_layout l, int axis, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(l, "ll_slice");
+    if (!out) return fail(LL_ERR_ARG, "ll_slice: NULL argument");
+    *out = wrap(ll::shape_slice(l->L, axis));
+    return LL_OK;
+  });
+}
+
+ll_status ll_blocked(int rank, const int* shape_bits, const int* R, const int* T, const int* W,
+                     const int* order, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    if (!out || rank <= 0 || rank > 16 || !shape_bits || !R || !T || !W || !order)
+      return fail(LL_ERR_ARG, "ll_blocked: bad argument");
+    auto v = [&](const int* a) { return std::vector<int>(a, a + rank); };
+    *out = wrap(ll::make_blocked(v(shape_bits), v(R), v(T), v(W), v(order)));
+    return LL_OK;
+  });
+}
+
+ll_status ll_mma_tile(int operand, int bitwidth, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    if (!out) return fail(LL_ERR_ARG, "ll_mma_tile: NULL argument");
+    *out = wrap(ll::make_mma_tile(operand, bitwidth));
+    return LL_OK;
+  });
+}
+
 ll_status ll_broadcast(ll_layout l, int axis, int bits, ll_layout* out) {
   return guarded([&]() -> ll_status {
     check_layout(l, "ll_broadcast");
@@ -466,6 +494,13 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
         // compile / module problem, nothing launched (a successful launch
         // returns cudaSuccess): the generic smem kernel below
         --g_launches;
+      }
+      if (P->jit_only) {
+        // broadcast-dedup plans exist only as compiled kernels: element-wise pull
+        if (n_shards > 1) return fail(LL_ERR_UNSUPPORTED, "ll_convert_shard: this plan needs the compiled smem kernel");
+        ++g_launches;
+        return cuda_status(ll::launch_convert_generic(P->gp, w, src, dst, max_ctas, st),
+                           "ll_convert (generic kernel, broadcast plan)");
       }
       [[fallthrough]];
     case LL_PATH_SMEM_NOSWIZZLE:

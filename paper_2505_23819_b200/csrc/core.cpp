@@ -404,4 +404,105 @@ Layout shape_split(const Layout& l) {
   return o;
 }
 
+// Sliced layouts: removing the output dim `axis` (the result of a
+// reduction along it) is a linear map; the matrix loses that dim's rows, so
+// columns that only reached it become zero (broadcast) -- still surjective.
+Layout shape_slice(const Layout& l, int axis) {
+  if (axis < 0 || axis >= (int)l.out.size()) throw Error(LL_ERR_ARG, "slice: axis out of range");
+  Layout o;
+  o.in = l.in;
+  o.out = l.out;
+  o.out.erase(o.out.begin() + axis);
+  for (u64 c : l.cols) {
+    auto x = l.unflatten(c);
+    x.erase(x.begin() + axis);
+    o.cols.push_back(o.flatten(x));
+  }
+  return o;
+}
+
+namespace {
+// Product of identity tiles id^{in,out}_k in order (Appendix notation,
+// P:1005): each factor maps the next k bits of input dim `in` onto the next k
+// bits of output dim `out` (a shared label's earlier factors are the low bits,
+// Definition "Product").
+struct TileBuilder {
+  std::vector<std::string> in_names;
+  std::vector<std::vector<std::pair<int, int>>> in_cols;  // per input dim: (out dim, out bit)
+  std::vector<int> out_used;
+  explicit TileBuilder(int n_out) : out_used(n_out, 0) {}
+  void id(const std::string& in, int out, int k) {
+    auto it = std::find(in_names.begin(), in_names.end(), in);
+    size_t d = it - in_names.begin();
+    if (it == in_names.end()) {
+      in_names.push_back(in);
+      in_cols.emplace_back();
+    }
+    for (int i = 0; i < k; ++i) in_cols[d].push_back({out, out_used[out]++});
+  }
+  Layout build(const std::vector<std::string>& order, const std::vector<int>& out_bits) {
+    Layout L;
+    for (size_t o = 0; o < out_bits.size(); ++o) L.out.push_back({"dim" + std::to_string(o), out_bits[o]});
+    for (const std::string& nm : order) {
+      auto it = std::find(in_names.begin(), in_names.end(), nm);
+      const int d = it == in_names.end() ? -1 : (int)(it - in_names.begin());
+      const int bits = d < 0 ? 0 : (int)in_cols[d].size();
+      L.in.push_back({nm, bits});
+      for (int i = 0; i < bits; ++i) {
+        std::vector<int64_t> x(out_bits.size(), 0);
+        x[in_cols[d][i].first] = int64_t(1) << in_cols[d][i].second;
+        L.cols.push_back(L.flatten(x));
+      }
+    }
+    return L;
+  }
+};
+}  // namespace
+
+// Blocked layouts (Appendix proposition):
+// sigma_o^{-1} o (id_R^o x id_T^o x id_W^o), id_R^o = id^{reg,o_1}_{r_{o_1}} x
+// ... x id^{reg,o_l}_{r_{o_l}}; order[0] = the fastest dim.
+Layout make_blocked(const std::vector<int>& shape_bits, const std::vector<int>& R,
+                    const std::vector<int>& T, const std::vector<int>& W,
+                    const std::vector<int>& order) {
+  const size_t rank = shape_bits.size();
+  if (rank == 0 || R.size() != rank || T.size() != rank || W.size() != rank || order.size() != rank)
+    throw Error(LL_ERR_ARG, "blocked: R, T, W, order must have one entry per dim");
+  std::vector<int> seen(rank, 0);
+  for (int o : order) {
+    if (o < 0 || o >= (int)rank || seen[o]++) throw Error(LL_ERR_ARG, "blocked: order must be a permutation");
+  }
+  for (size_t i = 0; i < rank; ++i)
+    if (R[i] < 0 || T[i] < 0 || W[i] < 0 || R[i] + T[i] + W[i] != shape_bits[i])
+      throw Error(LL_ERR_SHAPE, "blocked: R_i + T_i + W_i must equal d_i (P:1012)");
+  TileBuilder tb((int)rank);
+  for (int o : order) tb.id("reg", o, R[o]);
+  for (int o : order) tb.id("lane", o, T[o]);
+  for (int o : order) tb.id("warp", o, W[o]);
+  return tb.build({"reg", "lane", "warp"}, shape_bits);
+}
+
+// mma tiles (Appendix proposition): lhs / output
+// id^{reg,1}_{log2(32/b)} x id^{thread,1}_2 x id^{thread,0}_3 x id^{reg,0}_1 x
+// id^{reg,1}_1; rhs id^{reg,0}_{log2(32/b)} x id^{thread,0}_2 x id^{thread,1}_3 x
+// id^{reg,0}_1 (reading A8: the printed trailing id^{reg,1}_1 contradicts the
+// PTX m16n8k16 B fragment); output = the first four factors of the b = 16 lhs
+// tile (the m16n8 accumulator fragment).  operand 0 = lhs, 1 = rhs, 2 = out.
+Layout make_mma_tile(int operand, int bitwidth) {
+  if (bitwidth != 8 && bitwidth != 16 && bitwidth != 32) throw Error(LL_ERR_ARG, "mma: bitwidth must be 8, 16 or 32");
+  int kreg = 0;
+  while ((32 / bitwidth) > (1 << kreg)) ++kreg;
+  TileBuilder tb(2);
+  if (operand == 0) {
+    tb.id("reg", 1, kreg); tb.id("lane", 1, 2); tb.id("lane", 0, 3); tb.id("reg", 0, 1); tb.id("reg", 1, 1);
+  } else if (operand == 1) {
+    tb.id("reg", 0, kreg); tb.id("lane", 0, 2); tb.id("lane", 1, 3); tb.id("reg", 0, 1);
+  } else if (operand == 2) {
+    tb.id("reg", 1, 1); tb.id("lane", 1, 2); tb.id("lane", 0, 3); tb.id("reg", 0, 1);
+  } else {
+    throw Error(LL_ERR_ARG, "mma: operand must be 0 (lhs), 1 (rhs) or 2 (out)");
+  }
+  return tb.build({"reg", "lane"}, {tb.out_used[0], tb.out_used[1]});
+}
+
 }  // namespace ll

@@ -115,4 +115,9 @@ Layout shape_expand_dims(const Layout& l, int axis, const std::string& name);
 Layout shape_broadcast(const Layout& l, int axis, int bits);
 Layout shape_join(const Layout& l, const std::string& name);
 Layout shape_split(const Layout& l);
+Layout shape_slice(const Layout& l, int axis);
+Layout make_blocked(const std::vector<int>& shape_bits, const std::vector<int>& R,
+                    const std::vector<int>& T, const std::vector<int>& W,
+                    const std::vector<int>& order);
+Layout make_mma_tile(int operand, int bitwidth);
 }  // namespace ll

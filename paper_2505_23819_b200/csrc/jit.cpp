@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -226,6 +227,43 @@ int deposit_word_h(int j, int k, int LB, int A, int B) {
   return idx;
 }
 
+// One 32-bit word from 4 bytes (word expression, byte index), with prmt:
+// a copy, one __byte_perm of two words, or two + a merge.
+std::string pack_bytes(const std::vector<std::pair<std::string, int>>& b) {
+  if (b[0].first == b[1].first && b[0].first == b[2].first && b[0].first == b[3].first &&
+      b[0].second == 0 && b[1].second == 1 && b[2].second == 2 && b[3].second == 3)
+    return b[0].first;
+  std::vector<std::string> words;
+  for (auto& x : b)
+    if (std::find(words.begin(), words.end(), x.first) == words.end()) words.push_back(x.first);
+  auto sel2 = [&](const std::string& w0, int i0, int i1, int i2, int i3) {
+    // selector over (w0, w1): index < 4 from w0, else w1
+    unsigned sel = 0;
+    const int ii[4] = {i0, i1, i2, i3};
+    for (int k = 0; k < 4; ++k) sel |= (unsigned)(ii[k] & 7) << (4 * k);
+    (void)w0;
+    return sel;
+  };
+  if (words.size() <= 2) {
+    const std::string& w0 = words[0];
+    const std::string& w1 = words.size() > 1 ? words[1] : words[0];
+    int ii[4];
+    for (int k = 0; k < 4; ++k) ii[k] = (b[k].first == w0 ? 0 : 4) + b[k].second;
+    std::ostringstream e;
+    e << "__byte_perm(" << w0 << ", " << w1 << ", " << sel2(w0, ii[0], ii[1], ii[2], ii[3]) << "u)";
+    return e.str();
+  }
+  // two halves, then merge: t0 = [b0 b1 . .], t1 = [b2 b3 . .]
+  auto half = [&](int k0) {
+    const std::string& a = b[k0].first;
+    const std::string& c = b[k0 + 1].first;
+    std::ostringstream e;
+    e << "__byte_perm(" << a << ", " << c << ", " << sel2(a, b[k0].second, 4 + b[k0 + 1].second, 0, 0) << "u)";
+    return e.str();
+  };
+  return "__byte_perm(" + half(0) + ", " + half(2) + ", 0x5410u)";
+}
+
 // HBM -> HBM shared-memory conversion (LL_PATH_SMEM) specialised for the
 // plan: the same schedule as convert_smem_kernel (software-pipelined loads,
 // swizzled STS, group barrier, LDS, streaming stores), with every offset,
@@ -286,6 +324,39 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
         o << ind << R << "[" << i << "] = (unsigned)so * 2654435761u + tb * " << 4 * NW + 1 << "u + " << i << "u;\n";
       return;
     }
+    if (P.ld_span > 0) {
+      // broadcast dedup: a virtual vector's elements come from 2^ld_span
+      // physical vectors (source copy bits inside them are dropped)
+      const int C = 1 << P.ld_span, NEl = 16 / W, vbl = ilog2i(NEl);
+      std::vector<char> ref(C, 0);     // physical vectors holding virtual elements
+      for (int e = 0; e < NEl; ++e) {
+        int ph = 0;
+        for (int b = 0; b < vbl; ++b) if ((e >> b) & 1) ph |= 1 << P.src_phys[b];
+        ref[ph >> vbl] = 1;
+      }
+      for (int u = 0; u < NV; ++u) {
+        o << ind << "{ unsigned PL[" << 4 * C << "];\n";
+        for (int c = 0; c < C; ++c)
+          if (ref[c])
+            o << ind << "  asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(PL["
+              << 4 * c << "]), \"=r\"(PL[" << 4 * c + 1 << "]), \"=r\"(PL[" << 4 * c + 2 << "]), \"=r\"(PL["
+              << 4 * c + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] + 16u * c << "));\n";
+        auto src_byte = [&](int byte) {   // byte of the virtual vector -> (word, byte) of PL
+          const int e = byte / W, eb = byte % W;
+          int ph = 0;
+          for (int b = 0; b < vbl; ++b) if ((e >> b) & 1) ph |= 1 << P.src_phys[b];
+          const int pbyte = (ph & (NEl - 1)) * W + eb + 16 * (ph >> vbl);
+          return std::make_pair("PL[" + std::to_string(pbyte >> 2) + "]", pbyte & 3);
+        };
+        for (int q = 0; q < 4; ++q) {
+          std::vector<std::pair<std::string, int>> bs;
+          for (int k = 0; k < 4; ++k) bs.push_back(src_byte(4 * q + k));
+          o << ind << "  " << R << "[" << 4 * u + q << "] = " << pack_bytes(bs) << ";\n";
+        }
+        o << ind << "}\n";
+      }
+      return;
+    }
     for (int u = 0; u < NV; u += ld32 ? 2 : 1) {
       if (ld32) {
         o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\" : ";
@@ -334,7 +405,36 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
       for (int i = 0; i < NW; ++i) o << " x_ ^= Q[" << i << "];";
       o << " if (x_ == 0x9e3779b9u && dcur < 0) dthr[0] = 1; }\n";
     }
-    for (int u = 0; u < NV && !nostore; u += st32 ? 2 : 1) {
+    if (!nostore && (P.st_span > 0 || P.copy_off.size() > 1)) {
+      // broadcast dedup: each virtual vector becomes 2^st_span physical
+      // vectors (destination copy bits inside them duplicated in registers),
+      // each stored at every copy offset
+      const int C = 1 << P.st_span, NEl = 16 / W, vbl = ilog2i(NEl);
+      for (int u = 0; u < NV; ++u) {
+        for (int c = 0; c < C; ++c) {
+          std::string wexpr[4];
+          for (int q = 0; q < 4; ++q) {
+            std::vector<std::pair<std::string, int>> bs;
+            for (int k = 0; k < 4; ++k) {
+              const int pbyte = 4 * q + k, pe = (c << vbl) | (pbyte / W);
+              int e = 0;   // virtual element: the bits at the virtual vector's physical positions
+              for (int b = 0; b < vbl; ++b) if ((pe >> P.dst_phys[b]) & 1) e |= 1 << b;
+              const int vbyte = e * W + pbyte % W;
+              bs.push_back(std::make_pair("Q[" + std::to_string(4 * u + (vbyte >> 2)) + "]", vbyte & 3));
+            }
+            wexpr[q] = pack_bytes(bs);
+          }
+          o << "    { const unsigned S0 = " << wexpr[0] << ", S1 = " << wexpr[1] << ", S2 = " << wexpr[2]
+            << ", S3 = " << wexpr[3] << ";\n";
+          const std::vector<uint32_t> offs = P.copy_off.empty() ? std::vector<uint32_t>{0u} : P.copy_off;
+          for (uint32_t co : offs)
+            o << "      asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dcur + "
+              << p.st_vec[u] + 16u * c + co << "u), \"r\"(S0), \"r\"(S1), \"r\"(S2), \"r\"(S3) : \"memory\");\n";
+          o << "    }\n";
+        }
+      }
+    }
+    for (int u = 0; u < NV && !nostore && !(P.st_span > 0 || P.copy_off.size() > 1); u += st32 ? 2 : 1) {
       if (st32) {
         o << "    asm volatile(\"st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\" :: \"l\"(dthr + dcur + "
           << p.st_vec[u] << ")";

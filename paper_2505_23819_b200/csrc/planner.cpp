@@ -156,7 +156,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "pdl" && name != "run_bytes_dst" && name != "run_bytes_src" &&
       name != "auto_asym" && name != "tma_run_bytes_dst" && name != "gather_shfl_mu" &&
       name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
-      name != "smem_jit_noload" && name != "smem_jit_nostore")
+      name != "smem_jit_noload" && name != "smem_jit_nostore" && name != "bcast_dedup")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -367,7 +367,13 @@ namespace {
 // permutation or the tile does not fit.
 bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ostringstream& js,
                bool warp_tile = false) {
-  const int n = P.nB, nA = P.nA, w = P.w;
+  // virtual index spaces (broadcast dedup, build_convert_plan): X is over
+  // the destination bits that are not copies and the source bits that are
+  // read; SP / DP give their physical buffer positions (identity otherwise)
+  const bool virt = !P.dst_phys.empty();
+  const int n = virt ? (int)P.dst_phys.size() : P.nB, nA = virt ? (int)P.src_phys.size() : P.nA, w = P.w;
+  auto SP = [&](int p) { return virt ? P.src_phys[p] : p; };
+  auto DP = [&](int k) { return virt ? P.dst_phys[k] : k; };
   if (n > 62 || nA > 62) return false;
   // sigma: dst bit -> src bit; -1 for destination broadcast bits (zero columns
   // of X: the min-weight quotient makes every copy read the same source,
@@ -393,7 +399,8 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     VD.push_back(k);
     VS.push_back(sinv[k]);
   }
-  const int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
+  int r_max = ilog2i(std::max(16, std::min(128, planner_knob("thread_bytes_max", 128))) / w);
+  if (P.r_cap > 0) r_max = std::min(r_max, P.r_cap);
   const int r_pref = std::min(r_max, ilog2i(std::max(16, planner_knob("thread_bytes", 64)) / w));
   int G = 0, gbits = 0, r = 0, g = -1;
   std::vector<int> V, need, T;
@@ -591,7 +598,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   sp = SmemPlan{};
   const int lw = ilog2i(w);
   for (int k : T)
-    if (sigma[k] + lw >= 31 || k + lw >= 31) return false;  // 32-bit in-tile byte offsets
+    if (SP(sigma[k]) + lw >= 31 || DP(k) + lw >= 31) return false;  // 32-bit in-tile byte offsets
   sp.gw = g;
   sp.tile_bytes = w << d;
   if (P.padded) {
@@ -607,14 +614,14 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   sp.gsel_b = gsel.size() > 1 ? (int8_t)gsel[1] : (int8_t)-1;
   auto boff = [&](int k) -> uint32_t { return (uint32_t)off(k) << lw; };
   for (int b = 0; b < 5; ++b) {
-    sp.ld_thr[b] = uint32_t(w) << sigma[ld_lane[b]];
-    sp.st_thr[b] = uint32_t(w) << st_lane[b];
+    sp.ld_thr[b] = uint32_t(w) << SP(sigma[ld_lane[b]]);
+    sp.st_thr[b] = uint32_t(w) << DP(st_lane[b]);
     sp.sw_thr[b] = boff(ld_lane[b]);
     sp.sr_thr[b] = boff(st_lane[b]);
   }
   for (int b = 0; b < g; ++b) {
-    sp.ld_thr[5 + b] = uint32_t(w) << sigma[ld_warp[b]];
-    sp.st_thr[5 + b] = uint32_t(w) << st_warp[b];
+    sp.ld_thr[5 + b] = uint32_t(w) << SP(sigma[ld_warp[b]]);
+    sp.st_thr[5 + b] = uint32_t(w) << DP(st_warp[b]);
     sp.sw_thr[5 + b] = boff(ld_warp[b]);
     sp.sr_thr[5 + b] = boff(st_warp[b]);
   }
@@ -623,7 +630,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   for (int u = 0; u < nvec; ++u) {
     uint32_t lo = 0, so = 0;
     for (int q = 0; q < r - vb; ++q)
-      if ((u >> q) & 1) { lo += uint32_t(w) << sigma[ld_reg[vb + q]]; so += uint32_t(w) << st_reg[vb + q]; }
+      if ((u >> q) & 1) { lo += uint32_t(w) << SP(sigma[ld_reg[vb + q]]); so += uint32_t(w) << DP(st_reg[vb + q]); }
     sp.ld_vec[u] = lo;
     sp.st_vec[u] = so;
   }
@@ -713,8 +720,8 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       for (int q = 0; q < LL_TAB_BITS; ++q) {
         const int bit = k * LL_TAB_BITS + q;
         if (((v >> q) & 1) && bit < tm.n_bits) {
-          if (sigma[torder[bit]] >= 0) so += int64_t(w) << sigma[torder[bit]];
-          dof += int64_t(w) << torder[bit];
+          if (sigma[torder[bit]] >= 0) so += int64_t(w) << SP(sigma[torder[bit]]);
+          dof += int64_t(w) << DP(torder[bit]);
           if (P.op == 1) sc += scale_contrib(P, torder[bit]);
         }
       }
@@ -729,8 +736,8 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   P.tile_bit_src.clear();
   P.tile_bit_dst.clear();
   for (int q = 0; q < tm.n_bits; ++q) {
-    P.tile_bit_src.push_back(sigma[torder[q]]);
-    P.tile_bit_dst.push_back(torder[q]);
+    P.tile_bit_src.push_back(sigma[torder[q]] >= 0 ? SP(sigma[torder[q]]) : -1);
+    P.tile_bit_dst.push_back(DP(torder[q]));
   }
   P.nv = nvec;
   P.g = G;
@@ -745,7 +752,7 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
   // ---- warp-shuffle exchange, warp tiles only (g == 0), word payload
   P.shuffle_ok = false;
   std::ostringstream sjs;
-  if (g == 0 && w <= 4 && swizzle) {
+  if (g == 0 && w <= 4 && swizzle && !virt) {
     // word-level coordinates: tile-local unit vectors of the word bits / lanes
     std::vector<u64> Aw, Al5, Bw, Bl5;
     for (int b = 0; b < LB; ++b) Aw.push_back(loc(order[b + nsub]));
@@ -893,6 +900,85 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
         *P = *trial;
         js << js2.str();
         path = LL_PATH_SHUFFLE;
+        planned = true;
+      }
+    }
+  }
+  // broadcast dedup (SMEM / AUTO): zero columns of X (destination copies) and
+  // source bits X never reads are removed from the index spaces the tile plan
+  // works in, so each distinct element crosses shared memory once; copies
+  // are made in registers (inside a 16-byte vector) or by extra stores
+  // (above it), unread source copies are dropped in registers after the load
+  if (!ident && op == 0 && (path == LL_PATH_AUTO || path == LL_PATH_SMEM) &&
+      planner_knob("bcast_dedup", 1)) {
+    const int vb = ilog2i(16 / w);
+    std::vector<int> srcbit(P->nB, -1);
+    std::vector<char> read(P->nA, 0);
+    bool perm = true;
+    for (int k = 0; k < P->nB && perm; ++k) {
+      if (!X[k]) continue;
+      perm = popcount64(X[k]) == 1;
+      if (perm) { srcbit[k] = ctz64(X[k]); perm = !read[srcbit[k]]; read[srcbit[k]] = 1; }
+    }
+    int zd = 0, zs = 0;
+    for (int k = 0; k < P->nB; ++k) zd += srcbit[k] < 0;
+    for (int p = 0; p < P->nA; ++p) zs += !read[p];
+    if (perm && (zd || zs)) {
+      auto trial = std::make_shared<ConvertPlan>(*P);
+      std::vector<int> svirt(P->nA, -1);
+      for (int p = 0; p < P->nA; ++p)
+        if (read[p]) { svirt[p] = (int)trial->src_phys.size(); trial->src_phys.push_back(p); }
+      std::vector<u64> Xv;
+      for (int k = 0; k < P->nB; ++k)
+        if (srcbit[k] >= 0) { trial->dst_phys.push_back(k); Xv.push_back(u64(1) << svirt[srcbit[k]]); }
+      const int nv = (int)Xv.size();
+      bool ok = nv >= vb + 5;
+      if (ok) {
+        trial->ld_span = std::max(0, trial->src_phys[vb - 1] + 1 - vb);
+        trial->st_span = std::max(0, trial->dst_phys[vb - 1] + 1 - vb);
+        std::vector<int> high;   // destination copy bits above the virtual vector's range
+        for (int k = trial->dst_phys[vb - 1] + 1; k < P->nB; ++k) if (srcbit[k] < 0) high.push_back(k);
+        // loads: only the physical vectors holding virtual elements (chunks
+        // of copies are skipped); stores: every physical vector of the range
+        int ld_chunks = 0;
+        {
+          std::vector<char> ref(size_t(1) << trial->ld_span, 0);
+          for (int e = 0; e < (1 << vb); ++e) {
+            int ph = 0;
+            for (int b = 0; b < vb; ++b) if ((e >> b) & 1) ph |= 1 << trial->src_phys[b];
+            ref[ph >> vb] = 1;
+          }
+          for (char r : ref) ld_chunks += r;
+        }
+        trial->ld_chunks = ld_chunks;
+        ok = trial->ld_span <= 6 && trial->st_span <= 6 && high.size() <= 4 && ld_chunks <= 16;
+        for (int j = 0; ok && j < (1 << high.size()); ++j) {
+          int64_t off = 0;
+          for (size_t q = 0; q < high.size(); ++q) if ((j >> q) & 1) off += int64_t(w) << high[q];
+          ok = off < (int64_t(1) << 31);
+          trial->copy_off.push_back((uint32_t)off);
+        }
+      }
+      std::ostringstream js2;
+      // sparse sources (many copy bits inside the vectors) take fewer vectors
+      // per thread: at most 16 physical 16-byte loads per thread and tile
+      bool fit = false;
+      for (int rc = 0; ok && !fit && rc >= 0; ) {
+        trial->r_cap = rc;
+        js2.str("");
+        fit = plan_smem(*trial, Xv, true, js2) && trial->nv * trial->ld_chunks <= 16 &&
+              (trial->nv << trial->st_span) * (int)std::max<size_t>(1, trial->copy_off.size()) <= 256;
+        if (!fit) rc = rc == 0 ? trial->r - 1 : rc - 1;
+        if (rc > 0 && rc < vb) rc = -1;
+      }
+      if (ok && fit) {
+        trial->jit_only = true;
+        *P = *trial;
+        fill_generic(*P, X);    // fallback when the plan cannot be compiled
+        js << js2.str() << ",\"bcast_dedup\":{\"src_phys\":" << ivec_json(P->src_phys)
+           << ",\"dst_phys\":" << ivec_json(P->dst_phys) << ",\"ld_span\":" << P->ld_span
+           << ",\"st_span\":" << P->st_span << ",\"copies\":" << P->copy_off.size() << "}";
+        path = LL_PATH_SMEM;
         planned = true;
       }
     }

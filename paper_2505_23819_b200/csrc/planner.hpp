@@ -76,6 +76,19 @@ struct ConvertPlan {
   ShuffleDir shd;     // the same exchange per round, for the NVRTC-specialised kernel
   bool shuffle_ok = false;
   int shuffle_rounds = 0;
+  // broadcast dedup on the smem path:
+  // the plan runs over virtual index spaces without the destination copy
+  // bits and the unread source copy bits; src_phys / dst_phys map a virtual
+  // bit to its buffer bit (empty: identity).  A virtual 16-byte vector spans
+  // 2^ld_span / 2^st_span physical 16-byte vectors (copy bits inside it:
+  // compacted / duplicated in registers), copy_off = byte offsets of the
+  // destination copies above it (every destination vector stored at each).
+  // Executed by the plan-compiled kernel only (jit_only; fallback: generic).
+  std::vector<int> src_phys, dst_phys;
+  int ld_span = 0, st_span = 0, ld_chunks = 1;
+  int r_cap = 0;   // cap on the thread's register bits in plan_smem (0: none)
+  std::vector<uint32_t> copy_off;
+  bool jit_only = false;
   // generic path
   GenericPlan gp{};
   std::string json;

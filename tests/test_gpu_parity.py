@@ -627,6 +627,89 @@ def test_convert_broadcast_layouts(w, za, zb, low):
         assert dst.tobytes() == expect_convert(c, src).tobytes()
 
 
+def reg_bcast_pair(rng, d, w, za, zb):
+    """Distributed layouts over a d-bit tensor whose REGISTER bits carry
+    zero columns ("registers 4-7 map to the same tensor elements
+    as registers 0-3"): za / zb zero columns placed among A's / B's register
+    bits, inside or above the 16-byte vector."""
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    out = [("i", d // 2), ("j", d - d // 2)]
+    tmp = OLayout([], out, {})
+    specs = []
+    for z in (za, zb):
+        r = vb + 1 + z
+        n = d + z
+        rest = n - r - 5
+        nw = min(rest, 2)
+        names = [("reg", r), ("lane", 5), ("warp", nw), ("block", rest - nw)]
+        cols = [1 << k for k in range(d)]
+        rng.shuffle(cols)
+        regc = cols[:vb + 1] + [0] * z
+        rng.shuffle(regc)
+        allc = regc + cols[vb + 1:]
+        bases, k = {}, 0
+        for nme, b in names:
+            bases[nme] = [tmp.unflatten(x) for x in allc[k:k + b]]
+            k += b
+        specs.append({"in_dims": names, "out_dims": out, "bases": bases})
+    return {"A": specs[0], "B": specs[1], "elem_bytes": w}
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+@pytest.mark.parametrize("za,zb", [(1, 0), (0, 1), (1, 1), (2, 0), (0, 2), (2, 1)])
+def test_convert_register_broadcast(w, za, zb):
+    """Zero columns in register bits stay on the swizzled smem path (broadcast
+    dedup, P:607-610): each distinct element crosses shared memory once;
+    source copies are dropped after the load, destination copies are made in
+    registers or by extra stores.  Byte-exact against the oracle (lowest
+    preimage), and equal to the naive plan (knob bcast_dedup=0)."""
+    rng = random.Random(1300 + 17 * w + 5 * za + zb)
+    dedup = 0
+    for _ in range(5):
+        c = reg_bcast_pair(rng, rng.randint(12, 15), w, za, zb)
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        d = ll.plan_describe(A, B, 8 * w)
+        dedup += d["path"] == "smem" and "bcast_dedup" in d
+        seed = rng.randint(0, 999)
+        src, dst = run_convert(c, seed=seed)
+        assert dst.tobytes() == expect_convert(c, src).tobytes()
+        ll.tune("bcast_dedup", 0)
+        try:
+            _, dst0 = run_convert(c, seed=seed)
+        finally:
+            ll.tune("bcast_dedup", 1)
+        assert dst0.tobytes() == dst.tobytes()
+    assert dedup >= (3 if w > 1 else 2), dedup
+
+
+@pytest.mark.parametrize("fam", ["blocked", "mma"])
+def test_convert_sliced_layouts(fam):
+    """Sliced layouts from blocked / mma parents over [512, 32]
+    (4 warps, 8 CTAs), sliced along dim 1 with ll_slice: sliced<blocked> ->
+    sliced<mma> and back, batched, byte-exact; the broadcast-dedup smem plan."""
+    from oracle import shapeops
+    from workloads.configs import spec as mkspec
+    out = [("i", 9), ("j", 5)]
+    pb = OLayout(**mkspec([("reg", ["j0", "j1", "j2", "i0"]), ("lane", ["j3", "j4", "i1", "i2", "i3"]),
+                           ("warp", ["i4", "i5"]), ("block", ["i6", "i7", "i8"])], out))
+    pm = OLayout(**mkspec([("reg", ["j0", "i3", "j3", "j4"]), ("lane", ["j1", "j2", "i0", "i1", "i2"]),
+                           ("warp", ["i4", "i5"]), ("block", ["i6", "i7", "i8"])], out))
+
+    def to_spec(L):
+        return {"in_dims": L.in_dims, "out_dims": L.out_dims, "bases": {k: list(v) for k, v in L.bases.items()}}
+    sb, sm = shapeops.slice_(pb, 1), shapeops.slice_(pm, 1)
+    # the ABI's ll_slice agrees with the oracle's
+    for par, sl in ((pb, sb), (pm, sm)):
+        got = ll.slice_layout(ll.Layout.from_spec(to_spec(par)), 1).spec()["bases"]
+        assert got == {k: [tuple(x) for x in v] for k, v in to_spec(sl)["bases"].items()}
+    A, B = (sb, sm) if fam == "blocked" else (sm, sb)
+    c = {"A": to_spec(A), "B": to_spec(B), "elem_bytes": 2}
+    d = ll.plan_describe(ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"]), 16)
+    assert d["path"] == "smem" and "bcast_dedup" in d, d["path"]
+    src, dst = run_convert(c, batch=64, seed=5)
+    assert dst.tobytes() == expect_convert(c, src, 64).tobytes()
+
+
 @pytest.mark.parametrize("mb,nb", [(6, 6), (7, 9), (10, 8)])
 def test_fp8_transpose_paths(mb, nb):
     """fig:matrix-size workload: fp8 transposes through the three

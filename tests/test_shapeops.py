@@ -150,3 +150,59 @@ def test_config5_packed_layout_from_shape_ops_reading_A22():
     # same through the C ABI
     Q = ll.split(ll.reshape(ll.Layout(**spec), [("m", 7), ("kb", 6), ("nib", 1)]))
     assert from_ll(Q) == P
+
+
+# --- sliced layouts and the layout constructors --------
+
+def _blocked_cases():
+    from oracle.constructors import blocked
+    return [
+        (blocked([4, 5], [0, 3], [2, 2], [2, 0], [1, 0]), 1),
+        (blocked([4, 5], [0, 3], [2, 2], [2, 0], [1, 0]), 0),
+        (blocked([3, 4, 2], [1, 1, 1], [1, 3, 1], [1, 0, 0], [2, 1, 0]), 1),
+    ]
+
+
+def test_oracle_slice_removes_rows_and_keeps_surjectivity():
+    """the slice removes the dim's rows; columns become zero exactly
+    where the layout reached only that dim; the result is surjective (and, for
+    these one-hot blocked layouts, has as many zero columns as the dim had
+    bits)."""
+    from oracle import shapeops
+    for L, ax in _blocked_cases():
+        S = shapeops.slice_(L, ax)
+        dbits = L.out_dims[ax][1]
+        assert S.out_bits == L.out_bits - dbits
+        assert S.is_surjective()
+        zero = [c for c in S.cols if c == 0]
+        assert len(zero) == dbits
+        # every hardware index holds the reduction-result index of its element:
+        # the coordinates of L(h) other than `ax` (brute force over all h)
+        for h in range(1 << L.in_bits):
+            full = L.unflatten(L.apply_flat(h))
+            assert S.unflatten(S.apply_flat(h)) == tuple(c for i, c in enumerate(full) if i != ax)
+
+
+def test_ll_slice_blocked_mma_match_oracle():
+    """C ABI constructors (ll_blocked, ll_mma_tile, ll_slice) agree with the
+    oracle's (written separately from the paper)."""
+    import paper_2505_23819_b200 as ll
+    from oracle import shapeops
+    from oracle.constructors import blocked, mma_tile
+
+    def same(a_ll, b_or):
+        sp = a_ll.spec()
+        return (sp["in_dims"] == b_or.in_dims and sp["out_dims"] == b_or.out_dims and
+                all(list(map(tuple, sp["bases"][n])) == list(b_or.bases[n]) for n, _ in b_or.in_dims))
+
+    for args in (([4, 5], [0, 3], [2, 2], [2, 0], [1, 0]), ([3, 4, 2], [1, 1, 1], [1, 3, 1], [1, 0, 0], [2, 1, 0]),
+                 ([7, 7], [0, 3], [2, 3], [5, 1], [1, 0])):
+        B_ll, B_or = ll.blocked(*args), blocked(*args)
+        assert same(B_ll, B_or), args
+        for ax in range(len(args[0])):
+            assert same(ll.slice_layout(B_ll, ax), shapeops.slice_(B_or, ax))
+    for op in ("lhs", "rhs", "out"):
+        for b in (8, 16, 32):
+            assert same(ll.mma_tile(op, b), mma_tile(op, b)), (op, b)
+    with pytest.raises(ll.LLError):
+        ll.blocked([4], [1], [1], [1], [0])          # 1 + 1 + 1 != 4
