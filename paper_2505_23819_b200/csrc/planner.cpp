@@ -971,6 +971,13 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
         if (!fit) rc = rc == 0 ? trial->r - 1 : rc - 1;
         if (rc > 0 && rc < vb) rc = -1;
       }
+      // AUTO keeps the dedup plan where it measured as fast as the alternatives
+      // (profiles/r02/bcast_smem_counts.json: copies above or inside short
+      // vector spans, enough tiles for every SM); sparse sliced layouts (long
+      // spans, few tiles) ran 2-10x slower than the element-wise kernel
+      if (ok && fit && path_req == LL_PATH_AUTO &&
+          (trial->ld_span > 2 || trial->st_span > 2 || trial->sp.tile.n_tiles < 148))
+        fit = false;
       if (ok && fit) {
         trial->jit_only = true;
         *P = *trial;

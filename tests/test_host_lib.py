@@ -260,17 +260,31 @@ def test_async_plan_swizzle_conflict_free(name, c):
 
 def test_broadcast_plans_stay_tiled():
     """Replicated warps / blocks (zero columns at high bits) keep the smem
-    path; the destination broadcast bits become the lowest tile-index bits."""
+    path.  Default (broadcast dedup): the plan works in the index
+    space without the copy bits and stores every destination vector at the
+    2^|copies| copy offsets (one exchange per distinct element).  Naive
+    (knob bcast_dedup=0): the copy bits become the lowest tile-index bits
+    (the exchange re-runs per copy)."""
     from tests.test_gpu_parity import _bcast_pair   # layout generator only
     rng = random.Random(11)
     for w in (1, 2, 4):
         c = _bcast_pair(rng, 13, w, 1, 2)
         A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
         d = ll.plan_describe(A, B, 8 * w)
-        assert d["path"] in ("smem", "shuffle")       # tiled (AUTO: shuffle if warp-local)
+        assert d["path"] == "smem"
         X = d["X"]
         zd = [k for k, x in enumerate(X) if x == 0]
-        assert len(zd) == 2 and d["tile_order_dst_bits"][:2] == zd
+        assert len(zd) == 2
+        bd = d["bcast_dedup"]
+        assert bd["copies"] == 4 and not set(zd) & set(bd["dst_phys"])
+        assert sorted(bd["dst_phys"] + zd) == list(range(len(X)))
+        ll.tune("bcast_dedup", 0)
+        try:
+            d0 = ll.plan_describe(A, B, 8 * w)
+        finally:
+            ll.tune("bcast_dedup", 1)
+        assert d0["path"] in ("smem", "shuffle") and "bcast_dedup" not in d0
+        assert d0["tile_order_dst_bits"][:2] == zd
 
 
 def _reader_wavefronts(d, side="r"):
