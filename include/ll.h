@@ -189,8 +189,10 @@ ll_status ll_gather(const void* src, const int32_t* idx, void* out, ll_layout la
 /* ------------------------------------------------------ extended control -- */
 
 typedef enum {
-  LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, else SMEM
-                            (measured fastest once compiled per plan), else GENERIC     */
+  LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, REGPERM when
+                            only the low <= 64 bytes of each chunk are permuted, else SMEM
+                            (measured fastest once compiled per plan; broadcast layouts: the
+                            dedup plan where measured fast), else GENERIC                */
   LL_PATH_COPY = 1,      /* identity quotient: plain copy                          */
   LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle; by default
                             in a kernel specialised for the plan at run time (NVRTC, every
@@ -226,7 +228,14 @@ typedef enum {
   LL_PATH_REGS_SHUFFLE = 11 /* register-faithful warp-shuffle exchange for warp-local
                             pairs ((B^-1 o A)_warp = I), in a kernel specialised for the
                             plan at run time (NVRTC: every register index a compile-time
-                            constant); LL_ERR_UNSUPPORTED otherwise. */
+                            constant); LL_ERR_UNSUPPORTED otherwise. */,
+  LL_PATH_REGPERM = 12   /* no exchange between threads (the quotient is the
+                            identity outside registers): X = A^{-1} o B permutes only the low
+                            q bits of the buffer index (2^q elements <= 64 bytes) and is the
+                            identity above, so every thread loads its 2^q-element chunk,
+                            permutes it in registers (renames / prmt, compiled per plan) and
+                            stores it -- no shared memory, no shuffles.  AUTO takes it
+                            whenever it applies; LL_ERR_UNSUPPORTED otherwise. */
 } ll_path;
 
 typedef struct {

@@ -105,7 +105,7 @@ STATUS = {0: "LL_OK", 1: "LL_ERR_ARG", 2: "LL_ERR_SHAPE", 3: "LL_ERR_LABEL",
           7: "LL_ERR_UNSUPPORTED", 8: "LL_ERR_CUDA", 9: "LL_ERR_OOM"}
 PATHS = {"auto": 0, "copy": 1, "smem": 2, "shuffle": 3, "generic": 4, "smem_noswizzle": 5,
          "smem_async": 6, "smem_padded": 7, "smem_tma": 8,
-         "regs": 9, "smem_tma_store": 10, "regs_shuffle": 11}
+         "regs": 9, "smem_tma_store": 10, "regs_shuffle": 11, "regperm": 12}
 
 
 class LLError(RuntimeError):
@@ -394,7 +394,7 @@ def jit_source(A, B, elem_bits, compile=False, kernel="regs_shuffle"):
     "regs_shuffle" or "shuffle" = the HBM shuffle conversion), or with
     compile=True the NVRTC compile result as a dict."""
     mode = (1 if compile else 0) | (2 if kernel == "shuffle" else 0) | (4 if kernel == "smem" else 0) \
-        | (8 if kernel == "upcast" else 0)
+        | (8 if kernel == "upcast" else 0) | (16 if kernel == "regperm" else 0)
     need = ctypes.c_size_t()
     _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), mode, None, 0,
                               ctypes.byref(need)))

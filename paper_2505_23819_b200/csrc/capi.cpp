@@ -436,6 +436,24 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
   }
   const size_t dst_bytes = (size_t)w << P->nB;
   switch (P->path) {
+    case LL_PATH_REGPERM: {
+      if (!rg_in && n_shards <= 1) {
+        rg.t0 = 0;
+        rg.t1 = ((int64_t(1) << P->nB) >> P->rp_bits) * batch;
+      }
+      ++g_launches;
+      std::string err;
+      cudaError_t e = ll::launch_regperm_jit(*P, src, dst, max_ctas, st, rg, &err);
+      if (e != cudaSuccess && err != "cuLaunchKernel failed") {
+        // compile / module problem, nothing launched: element-wise pull
+        if (n_shards > 1) return fail(LL_ERR_UNSUPPORTED, "ll_convert_shard: regperm kernel unavailable: " + err);
+        ll::GenericPlan gp = P->gp;
+        return cuda_status(ll::launch_convert_generic(gp, w, src, dst, max_ctas, st),
+                           "ll_convert (generic kernel, regperm fallback)");
+      }
+      if (e != cudaSuccess) return fail(LL_ERR_CUDA, "ll_convert (regperm): " + err);
+      return LL_OK;
+    }
     case LL_PATH_COPY: {
       ++g_launches;
       const size_t bytes = n_shards > 1 ? dst_bytes / n_shards : dst_bytes * batch;
@@ -557,7 +575,10 @@ ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bit
     check_layout(dst_layout, "ll_jit_source");
     const int w = elem_bytes(elem_bits);
     std::string out;
-    if (compile & 8) {  // the fused mxfp4 upcast kernel (src / dst = the config-5 byte layouts)
+    if (compile & 16) {  // the register-permutation kernel (LL_PATH_REGPERM)
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_REGPERM, 1);
+      out = ll::regperm_kernel_source(*P);
+    } else if (compile & 8) {  // the fused mxfp4 upcast kernel (src / dst = the config-5 byte layouts)
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, 1, LL_PATH_AUTO, 1, 1);
       out = ll::upcast_hbm_kernel_source(*P);
     } else if (compile & 4) {  // the HBM shared-memory conversion kernel (LL_PATH_SMEM)

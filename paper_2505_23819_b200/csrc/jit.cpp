@@ -814,6 +814,78 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
   return cudaSuccess;  // launched by the driver API: no runtime error state to read
 }
 
+// Register permutation (LL_PATH_REGPERM): thread c loads chunk c (2^rp_bits
+// elements, contiguous in both buffers: 16-byte or 256-bit accesses),
+// rebuilds it in destination order with renames / prmt (compile time) and
+// stores it.  No shared memory, no shuffles.
+std::string regperm_kernel_source(const ConvertPlan& P) {
+  const int W = P.w, CB = W << P.rp_bits, NW = CB / 4;
+  const bool v8 = CB >= 32;
+  const int step = v8 ? 32 : 16;
+  std::ostringstream o;
+  o << "extern \"C\" __global__ void __launch_bounds__(256) ll_regperm(\n"
+    << "    const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, long long t0,\n"
+    << "    long long t1, long long src_shift, long long dst_shift) {\n"
+    << "  for (long long c = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; c < t1;\n"
+    << "       c += (long long)gridDim.x * blockDim.x) {\n"
+    << "    const unsigned char* s = src + c * " << CB << " - src_shift;\n"
+    << "    unsigned char* d = dst + c * " << CB << " - dst_shift;\n"
+    << "    unsigned R[" << NW << "];\n";
+  for (int off = 0; off < CB; off += step) {
+    const int k = off / 4, nw = step / 4;
+    o << "    asm volatile(\"ld.global.nc.L1::no_allocate.v" << nw << ".u32 {";
+    for (int q = 0; q < nw; ++q) o << (q ? "," : "") << "%" << q;
+    o << "}, [%" << nw << "];\" : ";
+    for (int q = 0; q < nw; ++q) o << (q ? ", " : "") << "\"=r\"(R[" << k + q << "])";
+    o << " : \"l\"(s + " << off << "));\n";
+  }
+  std::vector<std::string> Q(NW);
+  for (int q = 0; q < NW; ++q) {
+    std::vector<std::pair<std::string, int>> bs;
+    for (int b = 0; b < 4; ++b) {
+      const int byte = 4 * q + b, e = byte / W, eb = byte % W;
+      const int sbyte = P.rp_src[e] * W + eb;
+      bs.push_back(std::make_pair("R[" + std::to_string(sbyte >> 2) + "]", sbyte & 3));
+    }
+    Q[q] = pack_bytes(bs);
+  }
+  for (int q = 0; q < NW; ++q) o << "    const unsigned Q" << q << " = " << Q[q] << ";\n";
+  for (int off = 0; off < CB; off += step) {
+    const int k = off / 4, nw = step / 4;
+    o << "    asm volatile(\"st.global.cs.v" << nw << ".b32 [%0], {";
+    for (int q = 0; q < nw; ++q) o << (q ? "," : "") << "%" << q + 1;
+    o << "};\" :: \"l\"(d + " << off << ")";
+    for (int q = 0; q < nw; ++q) o << ", \"r\"(Q" << k + q << ")";
+    o << " : \"memory\");\n";
+  }
+  o << "  }\n}\n";
+  return o.str();
+}
+
+cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
+                               cudaStream_t st, const TileRange& rg, std::string* err) {
+  CUfunction fn = nullptr;
+  cudaError_t e = get_kernel(regperm_kernel_source(P), &fn, err, "ll_regperm");
+  if (e != cudaSuccess) return e;
+  const int64_t n = rg.t1 - rg.t0;
+  if (n <= 0) return cudaSuccess;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+  grid = std::max<int64_t>(1, grid);
+  long long t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
+  const void* s = src;
+  void* d = dst;
+  void* args[] = {(void*)&s, (void*)&d, (void*)&t0, (void*)&t1, (void*)&ss, (void*)&ds};
+  void* f = (void*)fn;
+  return jit_launch(f, (unsigned)grid, 256, 0, st, args, err);
+}
+
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P) { return shuffle_hbm_source(P); }
 std::string smem_hbm_kernel_source(const ConvertPlan& P) {
   return smem_hbm_source(P, planner_knob("smem_jit_single", 0) != 0);

@@ -156,7 +156,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "pdl" && name != "run_bytes_dst" && name != "run_bytes_src" &&
       name != "auto_asym" && name != "tma_run_bytes_dst" && name != "gather_shfl_mu" &&
       name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
-      name != "smem_jit_noload" && name != "smem_jit_nostore" && name != "bcast_dedup")
+      name != "smem_jit_noload" && name != "smem_jit_nostore" && name != "bcast_dedup" &&
+      name != "auto_regperm")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -886,6 +887,32 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
      << (ident ? "true" : "false");
   int path = path_req;
   bool planned = false;
+  // register permutation: X is the identity above the low q
+  // bits and permutes them among themselves -> each thread permutes its own
+  // chunk, no exchange.  Chunk = max(q, 16-byte vector) <= 64 bytes.
+  if (!ident && op == 0 && (path == LL_PATH_AUTO || path == LL_PATH_REGPERM) && P->nA == P->nB &&
+      planner_knob("auto_regperm", 1) | (path == LL_PATH_REGPERM)) {
+    int q = P->nB;
+    while (q > 0 && X[q - 1] == (u64(1) << (q - 1))) --q;
+    const int vb = ilog2i(16 / w);
+    const int cb = std::max(q, vb);
+    bool ok = (int64_t(w) << cb) <= 64 && cb <= P->nB;
+    for (int k = 0; ok && k < q; ++k) ok = popcount64(X[k]) == 1 && X[k] < (u64(1) << q);
+    if (ok) {
+      P->rp_bits = cb;
+      for (int e = 0; e < (1 << cb); ++e) {
+        u64 x = 0;
+        for (int k = 0; k < cb; ++k) if ((e >> k) & 1) x ^= X[k];
+        P->rp_src.push_back((int)x);
+      }
+      js << ",\"regperm\":{\"chunk_bits\":" << cb << ",\"chunk_bytes\":" << (w << cb) << "}";
+      path = LL_PATH_REGPERM;
+      planned = true;
+    } else if (path == LL_PATH_REGPERM) {
+      throw Error(LL_ERR_UNSUPPORTED, "regperm path requested but the quotient moves data between "
+                                      "chunks of <= 64 bytes (an exchange is needed)");
+    }
+  }
   if (path == LL_PATH_AUTO) {
     path = ident ? LL_PATH_COPY : LL_PATH_SMEM;
     // cost model (measured on B200, profiles/r01/shuffle_jit, smem_jit): with
@@ -1073,11 +1100,11 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
   }
   if (op == 1 && path != LL_PATH_SMEM)
     throw Error(LL_ERR_UNSUPPORTED, "mxfp4 upcast: the layouts are not a tileable bit permutation");
-  if (path == LL_PATH_GENERIC) fill_generic(*P, X);
+  if (path == LL_PATH_GENERIC || path == LL_PATH_REGPERM) fill_generic(*P, X);
   P->path = path;
   static const char* names[] = {"auto", "copy", "smem", "shuffle", "generic", "smem_noswizzle",
                                 "smem_async", "smem_padded", "smem_tma", "regs", "smem_tma_store",
-                                "regs_shuffle"};
+                                "regs_shuffle", "regperm"};
   js << ",\"path\":\"" << names[path] << "\"}";
   P->json = js.str();
   return P;
@@ -1150,6 +1177,16 @@ TileRange shard_range(const ConvertPlan& P, int n_shards, int shard) {
   if (P.path == LL_PATH_COPY) {
     rg.t0 = (int64_t)shard;
     rg.t1 = (int64_t)shard + 1;
+    rg.src_shift = (int64_t)shard * ((w << P.nA) >> sb);
+    rg.dst_shift = (int64_t)shard * ((w << P.nB) >> sb);
+    return rg;
+  }
+  if (P.path == LL_PATH_REGPERM) {
+    // chunks are contiguous in both buffers: shard = a contiguous chunk range
+    const int64_t chunks = (int64_t(1) << P.nB) >> P.rp_bits;
+    if ((int64_t)n_shards > chunks) throw Error(LL_ERR_UNSUPPORTED, "shard: more shards than chunks");
+    rg.t0 = chunks / n_shards * shard;
+    rg.t1 = chunks / n_shards * (shard + 1);
     rg.src_shift = (int64_t)shard * ((w << P.nA) >> sb);
     rg.dst_shift = (int64_t)shard * ((w << P.nB) >> sb);
     return rg;

@@ -87,6 +87,10 @@ struct ConvertPlan {
   std::vector<int> src_phys, dst_phys;
   int ld_span = 0, st_span = 0, ld_chunks = 1;
   int r_cap = 0;   // cap on the thread's register bits in plan_smem (0: none)
+  // register permutation (LL_PATH_REGPERM): chunks of 2^rp_bits elements,
+  // destination element e of a chunk = source element rp_src[e]
+  int rp_bits = 0;
+  std::vector<int> rp_src;
   std::vector<uint32_t> copy_off;
   bool jit_only = false;
   // generic path
@@ -159,6 +163,9 @@ std::string upcast_hbm_kernel_source(const ConvertPlan& P);
 cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
                               const uint8_t* scales, int max_ctas, cudaStream_t st,
                               const TileRange& rg, std::string* err);
+std::string regperm_kernel_source(const ConvertPlan& P);
+cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
+                               cudaStream_t st, const TileRange& rg, std::string* err);
 cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
                             cudaStream_t st, const TileRange& rg, std::string* err);
 bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin_bytes);

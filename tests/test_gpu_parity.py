@@ -145,6 +145,85 @@ def test_convert_vec32(w):
         ll.tune("vec32", 0)
 
 
+def perm_pair(rng, d, w, r, which):
+    """A random distributed layout A and B = A with its `which` columns
+    ("reg" or "lane") permuted: the pair differs only in register order (no
+    exchange between threads) or only in lane order (warp-local,
+    P:624)."""
+    names = [("reg", r), ("lane", 5)]
+    rest = d - r - 5
+    nw = min(rest, rng.randint(0, 2))
+    names += [("warp", nw), ("block", rest - nw)]
+    out = [("i", d // 2), ("j", d - d // 2)]
+    tmp = OLayout([], out, {})
+    cols = [1 << k for k in range(d)]
+    rng.shuffle(cols)
+    bases, k = {}, 0
+    for n, b in names:
+        bases[n] = [tmp.unflatten(x) for x in cols[k:k + b]]
+        k += b
+    A = {"in_dims": names, "out_dims": out, "bases": bases}
+    bb = dict(bases)
+    p = list(bb[which])
+    while p == bases[which]:
+        rng.shuffle(p)
+    bb[which] = p
+    return {"A": A, "B": {"in_dims": names, "out_dims": out, "bases": bb}, "elem_bytes": w}
+
+
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_register_permutation_pairs(w):
+    """Pairs that differ only in register order take LL_PATH_REGPERM under
+    AUTO (no STS / LDS, no shuffles) whenever the permuted chunk is <= 64
+    bytes; byte-exact, also batched and sharded."""
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    rng = random.Random(1500 + w)
+    took = 0
+    for case in range(8):
+        r = rng.randint(2, max(2, vb + (6 - vb if w == 1 else 2)))
+        c = perm_pair(rng, rng.randint(12, 15), w, r, "reg")
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        d = ll.plan_describe(A, B, 8 * w)
+        if (w << max(r, vb)) <= 64:
+            assert d["path"] == "regperm", (r, d["path"])
+        took += d["path"] == "regperm"
+        batch = 1 + 2 * (case % 2)
+        src, dst = run_convert(c, seed=case, batch=batch)
+        assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
+        if d["path"] == "regperm":
+            n = 1 << A.in_bits
+            full = values_torch(n, 77, w, "cuda")
+            parts = []
+            for s_ in range(4):
+                s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, 4, s_)
+                dl = torch.empty(d1 - d0, dtype=torch.uint8, device="cuda")
+                ll.convert_shard(full.view(torch.uint8)[s0:s1].clone(), A, dl, B, 8 * w, 4, s_)
+                parts.append(dl)
+            torch.cuda.synchronize()
+            got = torch.cat(parts).cpu().numpy().view(_NP[w])
+            assert got.tobytes() == expect_convert(c, _np(full, w)).tobytes()
+    assert took >= 4
+
+
+@pytest.mark.parametrize("w", [1, 2, 4])
+def test_convert_lane_permutation_pairs(w):
+    """Pairs that differ only in lane order (warp-local): AUTO, the
+    warp-shuffle exchange and the smem exchange all byte-exact."""
+    vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
+    rng = random.Random(1600 + w)
+    for case in range(6):
+        c = perm_pair(rng, rng.randint(12, 15), w, vb, "lane")
+        for path in ("auto", "shuffle", "smem"):
+            A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+            try:
+                ll.plan_describe(A, B, 8 * w, path)
+            except ll.LLError:
+                assert path == "shuffle"
+                continue
+            src, dst = run_convert(c, path=path, seed=case)
+            assert dst.tobytes() == expect_convert(c, src).tobytes(), (case, path)
+
+
 @pytest.mark.parametrize("w", [1, 2, 4])
 def test_convert_random_pairs_shuffle(w):
     rng = random.Random(500 + w)
