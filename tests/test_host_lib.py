@@ -270,7 +270,7 @@ def test_broadcast_plans_stay_tiled():
     for w in (1, 2, 4):
         c = _bcast_pair(rng, 13, w, 1, 2)
         A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
-        d = ll.plan_describe(A, B, 8 * w)
+        d = ll.plan_describe(A, B, 8 * w, path="smem")
         assert d["path"] == "smem"
         X = d["X"]
         zd = [k for k, x in enumerate(X) if x == 0]
@@ -280,7 +280,7 @@ def test_broadcast_plans_stay_tiled():
         assert sorted(bd["dst_phys"] + zd) == list(range(len(X)))
         ll.tune("bcast_dedup", 0)
         try:
-            d0 = ll.plan_describe(A, B, 8 * w)
+            d0 = ll.plan_describe(A, B, 8 * w, path="smem")
         finally:
             ll.tune("bcast_dedup", 1)
         assert d0["path"] in ("smem", "shuffle") and "bcast_dedup" not in d0
