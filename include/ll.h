@@ -325,7 +325,9 @@ ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst
 /* The CUDA source of a run-time specialised kernel for (src_layout,
  * dst_layout) into buf (cap bytes, NUL-terminated; *need = the size needed):
  * the LL_PATH_REGS_SHUFFLE kernel, or with (compile & 2) the LL_PATH_SHUFFLE
- * HBM kernel.  (compile & 1) instead compiles it with NVRTC for sm_100a (no
+ * HBM kernel, (compile & 4) the LL_PATH_SMEM kernel, (& 8) the fused mxfp4
+ * upcast, (& 16) the LL_PATH_REGPERM kernel, (& 32 / & 64) the warp-
+ * specialised TMA kernels of LL_PATH_SMEM_TMA / LL_PATH_SMEM_TMA_STORE.  (compile & 1) instead compiles it with NVRTC for sm_100a (no
  * device needed) and returns {"compiled": true, "cubin_bytes": n}.
  * LL_ERR_UNSUPPORTED if the pair has no such plan or NVRTC fails. */
 ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bits, int compile,

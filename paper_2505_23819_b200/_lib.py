@@ -391,10 +391,13 @@ def convert_regs_timed(src, A, dst, B, elem_bits, reps=1, cycles=None, batch=1, 
 
 def jit_source(A, B, elem_bits, compile=False, kernel="regs_shuffle"):
     """ll_jit_source: the NVRTC-specialised kernel source (kernel
-    "regs_shuffle" or "shuffle" = the HBM shuffle conversion), or with
+    "regs_shuffle" or "shuffle" = the HBM shuffle conversion, "smem",
+    "upcast", "regperm", "tma" / "tma_store" = the warp-specialised TMA
+    kernels), or with
     compile=True the NVRTC compile result as a dict."""
     mode = (1 if compile else 0) | (2 if kernel == "shuffle" else 0) | (4 if kernel == "smem" else 0) \
-        | (8 if kernel == "upcast" else 0) | (16 if kernel == "regperm" else 0)
+        | (8 if kernel == "upcast" else 0) | (16 if kernel == "regperm" else 0) \
+        | (32 if kernel == "tma" else 0) | (64 if kernel == "tma_store" else 0)
     need = ctypes.c_size_t()
     _check(_lib.ll_jit_source(A.handle, B.handle, int(elem_bits), mode, None, 0,
                               ctypes.byref(need)))

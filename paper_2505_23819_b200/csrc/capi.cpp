@@ -494,14 +494,22 @@ ll_status run_convert(const void* src, ll_layout src_layout, void* dst, ll_layou
       return cuda_status(ll::launch_convert_regs(P->rp, w, src, dst, max_ctas, 1, nullptr, st),
                          "ll_convert (register-faithful kernel)");
     case LL_PATH_SMEM_TMA_STORE:
+    case LL_PATH_SMEM_TMA:
       ++g_launches;
+      if (ll::planner_knob("tma_jit", 1)) {
+        // warp-specialised TMA kernel compiled for the plan (NVRTC)
+        std::string err;
+        cudaError_t e = ll::launch_tma_jit(*P, P->path == LL_PATH_SMEM_TMA_STORE, src, dst, max_ctas, st, rg, &err);
+        if (e == cudaSuccess || err.rfind("cuLaunchKernel", 0) == 0)
+          return cuda_status(e, "ll_convert (specialised TMA kernel)");
+        // compile / module / shape problem, nothing launched: the template kernels below
+      }
+      if (P->path == LL_PATH_SMEM_TMA)
+        return cuda_status(ll::launch_convert_tma(P->sp, P->td, w, P->nv, src, dst, max_ctas, st, rg),
+                           "ll_convert (TMA smem kernel)");
       return cuda_status(ll::launch_convert_tma_store(P->sp, P->td, P->td_dst, w, P->nv, src, dst,
                                                       max_ctas, st, rg),
                          "ll_convert (TMA load/store kernel)");
-    case LL_PATH_SMEM_TMA:
-      ++g_launches;
-      return cuda_status(ll::launch_convert_tma(P->sp, P->td, w, P->nv, src, dst, max_ctas, st, rg),
-                         "ll_convert (TMA smem kernel)");
     case LL_PATH_SMEM:
       if (ll::planner_knob("smem_jit", 1) && !P->sp.pad) {
         ++g_launches;
@@ -575,7 +583,13 @@ ll_status ll_jit_source(ll_layout src_layout, ll_layout dst_layout, int elem_bit
     check_layout(dst_layout, "ll_jit_source");
     const int w = elem_bytes(elem_bits);
     std::string out;
-    if (compile & 16) {  // the register-permutation kernel (LL_PATH_REGPERM)
+    if (compile & 96) {  // the compiled TMA kernels (32: LL_PATH_SMEM_TMA, 64: _TMA_STORE)
+      const bool store = (compile & 64) != 0;
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w,
+                                    store ? LL_PATH_SMEM_TMA_STORE : LL_PATH_SMEM_TMA, 1);
+      out = ll::tma_hbm_kernel_source(*P, store);
+      if (out.empty()) return fail(LL_ERR_UNSUPPORTED, "ll_jit_source: the TMA tile does not fit two stages");
+    } else if (compile & 16) {  // the register-permutation kernel (LL_PATH_REGPERM)
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_REGPERM, 1);
       out = ll::regperm_kernel_source(*P);
     } else if (compile & 8) {  // the fused mxfp4 upcast kernel (src / dst = the config-5 byte layouts)

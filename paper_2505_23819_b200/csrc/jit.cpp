@@ -16,12 +16,14 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <sstream>
 #include <string>
 
+#include "kernels.hpp"
 #include "planner.hpp"
 
 namespace ll {
@@ -998,6 +1000,286 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
     return cudaErrorLaunchFailure;
   }
   return cudaSuccess;  // launched by the driver API: no runtime error state to read
+}
+
+// ------------------------------------------------------------------------
+// TMA-fed conversion compiled per plan (LL_PATH_SMEM_TMA / _TMA_STORE,
+// knob tma_jit).  Warp-specialised and persistent: one producer warp per CTA
+// (one elected lane) streams the CTA's source tiles into an NS-stage ring
+// with cp.async.bulk.tensor (one box per tile, mbarrier complete_tx); K
+// consumer groups of 2^gw warps each own one slot per stage, wait on the
+// slot's full barrier, read their 16-byte granules (the planner's
+// conflict-free reader lanes), release the slot on its empty barrier (one
+// arrival per warp) and then either store their destination vectors with
+// st.global.cs (tma_store = false) or write them into one of two
+// destination images and let one lane store the image with a TMA tensor
+// store (tma_store = true).  Every offset, permutation, box coordinate
+// shift and stage count is a compile-time constant.
+std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) {
+  const SmemPlan& p = P.sp;
+  const int W = P.w, NV = P.nv, NW = NV * 4, gw = p.gw, LB = ilog2i(NW), lw = ilog2i(W);
+  const int NC = K << gw;   // consumer warps
+  const TmaDesc& ts = P.td;
+  const TmaDesc& tq = P.td_dst;
+  const uint32_t TB = (uint32_t)p.tile_bytes;
+  const int ga = p.gsel_a, gb = p.gsel_b;
+  const bool pdl = planner_knob("pdl", 1) != 0;
+  std::ostringstream o;
+  o << "struct TileTab { long long src, dst, sc; };\n"
+    << "struct TileMap { long long n_tiles; int n_bits; int n_tab; long long bss, bsd; TileTab tab["
+    << LL_MAX_TAB << "][" << (1 << LL_TAB_BITS) << "]; };\n"
+    << "struct __align__(64) TMap { unsigned long long v[16]; };\n"
+    << "__device__ __forceinline__ void mwait(unsigned b, unsigned ph) {\n"
+    << "  asm volatile(\"{\\n.reg .pred p;\\nW_%=:\\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\\n@!p bra W_%=;\\n}\\n\" :: \"r\"(b), \"r\"(ph) : \"memory\");\n}\n"
+    << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (NC + 1) << ", 1) ll_tma_hbm(\n"
+    << "    const __grid_constant__ TileMap tm, const __grid_constant__ TMap tsrc,\n"
+    << "    const __grid_constant__ TMap tdst, unsigned char* __restrict__ dst,\n"
+    << "    long long t0, long long t1, long long src_shift, long long dst_shift) {\n"
+    << "  extern __shared__ __align__(16) unsigned char smem[];\n"
+    << "  __shared__ __align__(8) unsigned long long bars[" << 2 * NS * K << "];\n"
+    << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+    << "  const unsigned sb = (((unsigned)__cvta_generic_to_shared(smem)) + 1023u) & ~1023u;\n"
+    << "  const unsigned full0 = (unsigned)__cvta_generic_to_shared(bars), empty0 = full0 + "
+    << 8 * NS * K << "u;\n"
+    << "  if (threadIdx.x == 0) {\n"
+    << "    for (int i = 0; i < " << NS * K << "; ++i) {\n"
+    << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(full0 + 8 * i) : \"memory\");\n"
+    << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << (1 << gw)
+    << ";\" :: \"r\"(empty0 + 8 * i) : \"memory\");\n"
+    << "    }\n"
+    << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+    << "  }\n"
+    << "  __syncthreads();\n";
+  if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  o << "  const long long rmask = (1LL << tm.n_bits) - 1;\n"
+    << "  auto tile_off = [&](long long t, long long& so, long long& dof) {\n"
+    << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
+    << "    so = inst * tm.bss; dof = inst * tm.bsd;\n";
+  for (int k = 0; k < p.tile.n_tab; ++k)
+    o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
+      << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; }\n";
+  o << "  };\n";
+  // box coordinates of a tile origin (element offset e) in a TmaDesc view
+  auto coords = [&](const TmaDesc& td, const char* e) {
+    std::ostringstream c;
+    for (int i = 0; i < td.ndim; ++i) {
+      c << (i ? ", " : "") << "(int)((" << e << " >> " << td.shift[i] << ")";
+      if (i + 1 < td.ndim) c << " & " << ((1LL << td.size_bits[i]) - 1) << "LL";
+      c << ")";
+    }
+    return c.str();
+  };
+  auto regs = [&](int nd, int first) {
+    std::ostringstream c;
+    c << "{";
+    for (int i = 0; i < nd; ++i) c << (i ? ", " : "") << "%" << first + i;
+    c << "}";
+    return c.str();
+  };
+  // producer: the last warp, one lane
+  o << "  if (warp == " << NC << ") {\n"
+    << "    if (lane == 0) {\n"
+    << "      int s = 0; unsigned ph = 0;\n"
+    << "      for (long long base = t0 + (long long)blockIdx.x * " << K << "; base < t1; base += (long long)gridDim.x * "
+    << K << ") {\n";
+  for (int g = 0; g < K; ++g) {
+    o << "        { const long long t = base + " << g << "; if (t < t1) {\n"
+      << "          const unsigned fb = full0 + 8u * (s * " << K << " + " << g << "), eb = empty0 + 8u * (s * " << K
+      << " + " << g << ");\n"
+      << "          mwait(eb, ph ^ 1u);\n"   // first pass: the preceding phase counts as complete
+      << "          long long so, dof; tile_off(t, so, dof);\n"
+      << "          const long long e = (so - src_shift) >> " << lw << ";\n"
+      << "          asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(fb), \"r\"("
+      << TB << "u) : \"memory\");\n"
+      << "          asm volatile(\"cp.async.bulk.tensor." << ts.ndim
+      << "d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, " << regs(ts.ndim, 2) << "], [%"
+      << 2 + ts.ndim << "];\" :: \"r\"(sb + (unsigned)(s * " << K << " + " << g << ") * " << TB
+      << "u), \"l\"(&tsrc), ";
+    {
+      // each coordinate as its own operand
+      for (int i = 0; i < ts.ndim; ++i) {
+        o << "\"r\"((int)((e >> " << ts.shift[i] << ")";
+        if (i + 1 < ts.ndim) o << " & " << ((1LL << ts.size_bits[i]) - 1) << "LL";
+        o << ")), ";
+      }
+    }
+    o << "\"r\"(fb) : \"memory\");\n"
+      << "        } }\n";
+  }
+  o << "        if (++s == " << NS << ") { s = 0; ph ^= 1u; }\n";
+  if (pdl) o << "        if (base == t0 + (long long)blockIdx.x * " << K << ") asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  o << "      }\n"
+    << "    }\n"
+    << "    return;\n"
+    << "  }\n";
+  (void)coords;
+  // consumers
+  o << "  const int g = warp >> " << gw << ";\n"
+    << "  const int tb = lane | ((warp & " << ((1 << gw) - 1) << ") << 5);\n"
+    << "  unsigned st_off = 0, srx = 0, swx = 0;\n";
+  for (int b = 0; b < 5 + gw; ++b)
+    o << "  if (tb & " << (1 << b) << ") { st_off += " << p.st_thr[b] << "u; srx ^= " << p.sr_thr[b]
+      << "u; swx ^= " << p.sw_thr[b] << "u; }\n";
+  o << "  unsigned char* dthr = dst + st_off - dst_shift;\n"
+    << "  (void)dthr; (void)swx;\n";
+  if (tma_store)
+    o << "  const unsigned db0 = sb + " << NS * K << "u * " << TB << "u + (unsigned)g * " << 2 * TB << "u;\n"
+      << "  unsigned it = 0;\n";
+  o << "  int s = 0; unsigned ph = 0;\n"
+    << "  for (long long t = t0 + (long long)blockIdx.x * " << K << " + g; t < t1; t += (long long)gridDim.x * " << K
+    << ") {\n"
+    << "    const unsigned slot = (unsigned)(s * " << K << ") + (unsigned)g;\n"
+    << "    mwait(full0 + 8u * slot, ph);\n"
+    << "    unsigned Q[" << NW << "];\n"
+    << "    const unsigned rb = sb + slot * " << TB << "u;\n";
+  for (int j = 0; j < NV; ++j)
+    o << "    asm volatile(\"ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q["
+      << 4 * j + 1 << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "]) : \"r\"(rb + (srx ^ "
+      << p.sr_gran[j] << "u)) : \"memory\");\n";
+  o << "    __syncwarp();\n"
+    << "    if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(empty0 + 8u * slot) : \"memory\");\n"
+    << "    if (++s == " << NS << ") { s = 0; ph ^= 1u; }\n";
+  for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], "Q");
+  o << "    long long so, dof; tile_off(t, so, dof);\n";
+  if (!tma_store) {
+    for (int u = 0; u < NV; ++u) {
+      o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dof + " << p.st_vec[u] << ")";
+      for (int k = 0; k < 4; ++k) o << ", \"r\"(Q[" << deposit_word_h(u, k, LB, ga, gb) << "])";
+      o << " : \"memory\");\n";
+    }
+  } else {
+    const std::string gbar = gw == 0 ? std::string("__syncwarp();")
+                                     : "asm volatile(\"bar.sync %0, %1;\" :: \"r\"(g + 1), \"r\"(" +
+                                           std::to_string(32 << gw) + ") : \"memory\");";
+    o << "    const unsigned db = db0 + (it & 1u) * " << TB << "u;\n"
+      << "    if (tb == 0) asm volatile(\"cp.async.bulk.wait_group.read 1;\" ::: \"memory\");\n"
+      << "    " << gbar << "\n";
+    for (int j = 0; j < NV; ++j) {
+      o << "    asm volatile(\"st.shared.v4.b32 [%0], {%1,%2,%3,%4};\" :: \"r\"(db + (swx ^ " << p.sw_gran[j] << "u))";
+      for (int k = 0; k < 4; ++k) o << ", \"r\"(Q[" << deposit_word_h(j, k, LB, ga, gb) << "])";
+      o << " : \"memory\");\n";
+    }
+    o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+      << "    " << gbar << "\n"
+      << "    if (tb == 0) {\n"
+      << "      const long long e = (dof - dst_shift) >> " << lw << ";\n"
+      << "      asm volatile(\"cp.async.bulk.tensor." << tq.ndim << "d.global.shared::cta.bulk_group [%0, "
+      << regs(tq.ndim, 1) << "], [%" << 1 + tq.ndim << "];\" :: \"l\"(&tdst), ";
+    for (int i = 0; i < tq.ndim; ++i) {
+      o << "\"r\"((int)((e >> " << tq.shift[i] << ")";
+      if (i + 1 < tq.ndim) o << " & " << ((1LL << tq.size_bits[i]) - 1) << "LL";
+      o << ")), ";
+    }
+    o << "\"r\"(db) : \"memory\");\n"
+      << "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
+      << "    }\n"
+      << "    ++it;\n";
+  }
+  o << "  }\n";
+  if (tma_store) o << "  if (tb == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
+  o << "}\n";
+  return o.str();
+}
+
+namespace {
+// stages / groups of the compiled TMA kernel: K consumer groups (8 consumer
+// warps by default), as many stages as fit the CTA's shared memory at
+// tmaj_cps CTAs per SM (knobs tmaj_k, tmaj_stages, tmaj_cps)
+bool tma_jit_shape(const ConvertPlan& P, bool tma_store, int* ns, int* k, int* cps, size_t* smem) {
+  const int gw = P.sp.gw;
+  int K = planner_knob("tmaj_k", 0);
+  if (K <= 0) K = std::max(1, 8 >> gw);
+  if ((K << gw) > 16) return false;
+  const int c = std::max(1, std::min(4, planner_knob("tmaj_cps", 1)));
+  const size_t tb = (size_t)P.sp.tile_bytes;
+  const size_t budget = (size_t)(227 * 1024) / c - 1024 - 1024;   // per CTA: alignment slack, reserved
+  const size_t fixed = tma_store ? 2 * K * tb : 0;
+  if (budget <= fixed) return false;
+  int n = (int)((budget - fixed) / (K * tb));
+  const int want = planner_knob("tmaj_stages", 0);
+  if (want > 0) n = std::min(n, want);
+  n = std::min(n, 16);
+  if (n < 2) return false;
+  *ns = n;
+  *k = K;
+  *cps = c;
+  *smem = (size_t)n * K * tb + fixed + 1024;
+  return true;
+}
+}  // namespace
+
+std::string tma_hbm_kernel_source(const ConvertPlan& P, bool tma_store) {
+  int ns, k, cps;
+  size_t smem;
+  if (!tma_jit_shape(P, tma_store, &ns, &k, &cps, &smem)) return std::string();
+  return tma_hbm_source(P, tma_store, ns, k);
+}
+
+cudaError_t launch_tma_jit(const ConvertPlan& P, bool tma_store, const void* src, void* dst, int max_ctas,
+                           cudaStream_t st, const TileRange& rg, std::string* err) {
+  static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
+  static PFN_LaunchEx launch_ex = entry<PFN_LaunchEx>("cuLaunchKernelEx");
+  static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
+  if (!launch || !setattr) return cudaErrorNotSupported;
+  const int64_t n_tiles = rg.t1 - rg.t0;
+  if (n_tiles <= 0) return cudaSuccess;
+  int ns, K, cps;
+  size_t smem;
+  if (!tma_jit_shape(P, tma_store, &ns, &K, &cps, &smem)) {
+    *err = "tma_jit: tile does not fit two stages";
+    return cudaErrorInvalidConfiguration;
+  }
+  // tensor maps over the launch's slices (as the template kernels)
+  alignas(64) unsigned char ms[128], md[128];
+  std::memset(md, 0, sizeof md);
+  const int64_t slice_elems = n_tiles * (int64_t(P.sp.tile_bytes) / P.w);
+  cudaError_t e = encode_tma_map(ms, P.td, P.w, src, slice_elems);
+  if (e == cudaSuccess && tma_store) e = encode_tma_map(md, P.td_dst, P.w, dst, slice_elems);
+  if (e != cudaSuccess) {
+    *err = "tma_jit: tensor map encoding failed";
+    return e;
+  }
+  CUfunction fn = nullptr;
+  e = get_kernel(tma_hbm_source(P, tma_store, ns, K), &fn, err, "ll_tma_hbm");
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = std::min<int64_t>((n_tiles + K - 1) / K, (int64_t)sms * cps);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+  grid = std::max<int64_t>(1, grid);
+  if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+  long long t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
+  void* d = dst;
+  void* args[] = {(void*)&P.sp.tile, (void*)ms, (void*)md, (void*)&d, (void*)&t0, (void*)&t1,
+                  (void*)&ss, (void*)&ds};
+  const unsigned threads = 32u * ((unsigned)(K << P.sp.gw) + 1u);
+  CUresult r;
+  if (planner_knob("pdl", 1) && launch_ex) {
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg = {};
+    cfg.gridDimX = (unsigned)grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = threads;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)smem;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    r = launch_ex(&cfg, fn, args, nullptr);
+  } else {
+    r = launch(fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr);
+  }
+  if (r != CUDA_SUCCESS) {
+    *err = "cuLaunchKernel failed";
+    return cudaErrorLaunchFailure;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace ll

@@ -484,6 +484,11 @@ static cudaError_t launch_tma_w(const SmemPlan& p, const TmaDesc& td, int nv, co
   return cudaErrorNotSupported;
 }
 
+// The plan-compiled TMA kernels (jit.cpp) encode their maps here too.
+cudaError_t encode_tma_map(void* tm, const TmaDesc& td, int w, const void* base, int64_t slice_elems) {
+  return encode_src_map(reinterpret_cast<CUtensorMap*>(tm), td, w, base, slice_elems);
+}
+
 cudaError_t launch_convert_tma(const SmemPlan& p, const TmaDesc& td, int w, int nv,
                                const void* src, void* dst, int max_ctas, cudaStream_t st,
                                const TileRange& rg) {

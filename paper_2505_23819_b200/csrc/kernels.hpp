@@ -20,6 +20,8 @@ cudaError_t launch_convert_tma(const SmemPlan& p, const TmaDesc& td, int w, int 
 cudaError_t launch_convert_tma_store(const SmemPlan& p, const TmaDesc& tds, const TmaDesc& tdd,
                                      int w, int nv, const void* src, void* dst, int max_ctas,
                                      cudaStream_t st, const TileRange& rg);
+// Tensor map (128-byte CUtensorMap at tm) of a TmaDesc view of base[0, slice_elems).
+cudaError_t encode_tma_map(void* tm, const TmaDesc& td, int w, const void* base, int64_t slice_elems);
 cudaError_t launch_convert_regs(const RegsPlan& p, int w, const void* src, void* dst,
                                 int max_ctas, int reps, long long* cycles, cudaStream_t st);
 cudaError_t launch_convert_generic(const GenericPlan& p, int w, const void* src, void* dst,

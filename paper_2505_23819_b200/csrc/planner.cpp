@@ -157,7 +157,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "auto_asym" && name != "tma_run_bytes_dst" && name != "gather_shfl_mu" &&
       name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
       name != "smem_jit_noload" && name != "smem_jit_nostore" && name != "bcast_dedup" &&
-      name != "auto_regperm")
+      name != "auto_regperm" && name != "tma_jit" && name != "tmaj_k" && name != "tmaj_stages" &&
+      name != "tmaj_cps")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;

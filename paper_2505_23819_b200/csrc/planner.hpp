@@ -168,6 +168,10 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
                                cudaStream_t st, const TileRange& rg, std::string* err);
 cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
                             cudaStream_t st, const TileRange& rg, std::string* err);
+// the warp-specialised TMA kernels compiled per plan (LL_PATH_SMEM_TMA[_STORE])
+std::string tma_hbm_kernel_source(const ConvertPlan& P, bool tma_store);
+cudaError_t launch_tma_jit(const ConvertPlan& P, bool tma_store, const void* src, void* dst, int max_ctas,
+                           cudaStream_t st, const TileRange& rg, std::string* err);
 bool nvrtc_compile_check(const std::string& src, std::string* log, size_t* cubin_bytes);
 cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src, void* dst,
                                 int max_ctas, int reps, long long* cycles, cudaStream_t st,

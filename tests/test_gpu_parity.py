@@ -308,6 +308,32 @@ def test_convert_random_pairs_tma_store(w):
     assert done >= 6, (done, tried)
 
 
+@pytest.mark.parametrize("path", ["smem_tma", "smem_tma_store"])
+@pytest.mark.parametrize("knobs", [{"tma_jit": 0}, {"tmaj_stages": 2}, {"tmaj_k": 1, "tmaj_stages": 3},
+                                   {"tmaj_cps": 2}, {"pdl": 0}])
+def test_convert_tma_kernel_variants(path, knobs):
+    """The warp-specialised TMA kernels compiled per plan (default) under
+    ring depths that wrap many times, one consumer group per CTA, two CTAs
+    per SM, no PDL, and the template kernels (tma_jit=0); configs 2 / 3 / 5
+    at small sizes, a ragged batch, and a CTA cap (many tiles per CTA)."""
+    cases = [(configs.cfg2(batch_bits=0), 5, 0), (configs.cfg3(n_bits=9), 1, 3),
+             (configs.cfg5(m_bits=9, kb_bits=9), 1, 2), (configs.cfg3(n_bits=9, m_bits=8), 2, 0)]
+    for k, v in knobs.items():
+        ll.tune(k, v)
+    try:
+        for c, batch, max_ctas in cases:
+            w = c["elem_bytes"]
+            A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+            src = values_torch((1 << A.in_bits) * batch, 61, w, "cuda")
+            dst = torch.zeros((1 << B.in_bits) * batch, dtype=src.dtype, device="cuda")
+            ll.convert(src, A, dst, B, 8 * w, path=path, batch=batch, max_ctas=max_ctas)
+            torch.cuda.synchronize()
+            assert _np(dst, w).tobytes() == expect_convert(c, _np(src, w), batch).tobytes(), (path, knobs)
+    finally:
+        for k in knobs:
+            ll.tune(k, {"tma_jit": 1, "pdl": 1}.get(k, 0))
+
+
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
 def test_convert_tma_each_swizzle_mode(swz):
     """Every hardware swizzle mode (the Def. 5 instances) executed on the

@@ -513,6 +513,34 @@ def test_shuffle_hbm_kernel_specialises_and_compiles():
         assert ll.jit_source(A, B, 8 * c["elem_bytes"], compile=True, kernel="shuffle")["compiled"]
 
 
+def test_tma_kernels_specialise_and_compile():
+    """LL_PATH_SMEM_TMA / _TMA_STORE compiled per plan: one producer warp
+    (cp.async.bulk.tensor with mbarrier complete_tx), 8 consumer warps, a
+    full / empty mbarrier per ring slot, the store variant's TMA tensor store
+    from the destination image; NVRTC compiles every variant for sm_100a."""
+    for c in (configs.cfg2(batch_bits=2), configs.cfg3(n_bits=9), configs.cfg5(m_bits=9, kb_bits=9)):
+        A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+        eb = 8 * c["elem_bytes"]
+        for kern, path in (("tma", "smem_tma"), ("tma_store", "smem_tma_store")):
+            d = ll.plan_describe(A, B, eb, path)
+            src = ll.jit_source(A, B, eb, kernel=kern)
+            nc = 8 >> d["group_warps_log2"] << d["group_warps_log2"]
+            assert "__launch_bounds__(%d, 1)" % (32 * (nc + 1)) in src
+            assert "mbarrier::complete_tx::bytes" in src
+            assert ("global.shared::cta.bulk_group" in src) == (kern == "tma_store")
+            assert ("st.global.cs" in src) == (kern == "tma")
+            assert src.count("ld.shared.v4") == d["vectors_per_thread"]
+            assert ll.jit_source(A, B, eb, compile=True, kernel=kern)["compiled"]
+            for knob, v in (("tmaj_stages", 2), ("tmaj_k", 1 if d["group_warps_log2"] < 3 else 0)):
+                if not v:
+                    continue
+                ll.tune(knob, v)
+                try:
+                    assert ll.jit_source(A, B, eb, kernel=kern) != src
+                finally:
+                    ll.tune(knob, 0)
+
+
 def test_smem_hbm_single_buffer_variant_compiles():
     """smem_jit_single: the compiled smem kernel with one staging buffer per
     group (no prefetch) is a different source, and NVRTC compiles both."""
