@@ -49,7 +49,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "convert_layout effective GB/s vs 8 TB/s HBM peak; smem bank conflicts/request"
-CONFIGS = ["1", "2", "3", "4", "4full", "5"]
+CONFIGS = ["1", "2", "3", "4", "4full", "5", "6"]
 
 
 def parse(argv=None):
@@ -104,6 +104,10 @@ def workload(cfg):
     elif cfg == "4full":
         c = configs.cfg4(variant="full")
         desc = "cfg4 full-axis variant: tl.gather along the 4096-long axis of [4096,4096] fp32, int32 idx in [0,4096)"
+    elif cfg == "6":
+        c = configs.cfg6()
+        desc = ("cfg6: HBM pre-shuffle of a bf16 [8192,8192] operand, row-major -> mma m16n8k16 "
+                "B-fragment order, 16 B per thread (P:558-563, reading A25)")
     else:
         c = configs.cfg5()
         desc = "cfg5: mxfp4 packed [32768,16384] u8, blocked -> packed mma A-fragment (reading A22)"
@@ -123,7 +127,7 @@ def algorithmic_bytes(cfg, c):
     return total_elems(c["A"]) * c["elem_bytes"] + total_elems(c["B"]) * c["elem_bytes"]
 
 
-DTYPE = {"1": "fp16", "2": "fp16", "3": "bf16", "4": "fp32", "4full": "fp32", "5": "u8"}
+DTYPE = {"1": "fp16", "2": "fp16", "3": "bf16", "4": "fp32", "4full": "fp32", "5": "u8", "6": "bf16"}
 
 
 # ------------------------------------------------------------------- clocks
@@ -319,6 +323,8 @@ def cpu_baseline(cfg, c, budget_s=12.0):
                 "host_cpus": cores, "seconds": round(dt, 2)}
     if cfg == "2":
         cs = configs.cfg2(batch_bits=4)
+    elif cfg == "6":
+        cs = configs.cfg6(n_bits=10, k_bits=10)
     else:
         cs = configs.cfg3(n_bits=10)
     A, B = OL(**cs["A"]), OL(**cs["B"])

@@ -14,4 +14,10 @@ for c in 3 2 5; do
   done
   eval timeout 300 python bench.py --config $c $B > $O/bench_c${c}_auto.json 2> $O/bench_c${c}_auto.err
 done
+
+# config 6 (pre-shuffle): parity + default line and path sweep
+timeout 900 python -m pytest tests -m gpu -q -k "cfg6" > $O/pytest_cfg6.txt 2>&1
+for p in auto smem shuffle smem_tma smem_tma_store; do
+  eval timeout 300 python bench.py --config 6 --path $p $B > $O/bench_c6_$p.json 2> $O/bench_c6_$p.err
+done
 echo done > $O/done.txt

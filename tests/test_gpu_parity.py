@@ -68,6 +68,8 @@ CASES = [
     ("cfg3_rect", lambda: configs.cfg3(n_bits=9, m_bits=7)),
     ("cfg5_small", lambda: configs.cfg5(m_bits=8, kb_bits=7)),
     ("cfg5_mid", lambda: configs.cfg5(m_bits=9, kb_bits=9)),
+    ("cfg6_small", lambda: configs.cfg6(n_bits=7, k_bits=7)),
+    ("cfg6_rect", lambda: configs.cfg6(n_bits=6, k_bits=9)),
 ]
 
 
@@ -421,7 +423,8 @@ def test_convert_roundtrip_on_device():
 
 _FULL = {}
 FULL_CONFIGS = {"cfg2": lambda: configs.cfg2(), "cfg3": lambda: configs.cfg3(),
-                "cfg5": lambda: configs.cfg5(), "cfg2w": lambda: configs.cfg2w()}
+                "cfg5": lambda: configs.cfg5(), "cfg2w": lambda: configs.cfg2w(),
+                "cfg6": lambda: configs.cfg6()}
 
 
 def full_expected(name):
@@ -441,7 +444,7 @@ def full_expected(name):
 
 
 @pytest.mark.parametrize("path", ["auto", "smem_tma", "smem_tma_store"])
-@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg5"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg5", "cfg6"])
 def test_convert_full_size_whole_buffer(name, path):
     c, src, exp = full_expected(name)
     w = c["elem_bytes"]

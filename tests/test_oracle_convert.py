@@ -118,6 +118,36 @@ def test_config2_is_ptx_formula_permutation():
     assert (dst[di] == src[si]).all()
 
 
+def _cfg6_dst_index(n, k, n_bits, k_bits):
+    """Pre-shuffled bf16 operand (reading A25) from the PTX ISA's m16n8k16
+    B fragment (.bf16): element b_i of a thread sits at row (k) = 2*tig +
+    (i & 1) + 8*(i >> 1), column (n) = groupID, lane = 4*groupID + tig; k-tiles
+    k4, k5 are registers 4..15, warps step n by 8, blocks cover (k >> 6) then
+    (n >> 5)."""
+    kk = k & 15
+    i = (kk & 1) | ((kk >> 3) << 1)
+    tig = (kk >> 1) & 3
+    lane = (n & 7) * 4 + tig
+    reg = i | (((k >> 4) & 3) << 2)
+    warp = (n >> 3) & 3
+    blk = (k >> 6) | ((n >> 5) << (k_bits - 6))
+    return reg | (lane << 4) | (warp << 9) | (blk << 11)
+
+
+def test_config6_preshuffle_is_ptx_fragment_order():
+    """Config 6 (the bf16 pre-shuffle) computed without F2: index
+    formula of the PTX B fragment."""
+    for nb, kb in ((6, 7), (7, 6)):
+        c = configs.cfg6(n_bits=nb, k_bits=kb)
+        A, B = L_from_spec(c["A"]), L_from_spec(c["B"])
+        src = values_np(1 << (nb + kb), 6, 2)
+        dst = convert.convert_np(src, A, B)
+        n, k = np.meshgrid(np.arange(1 << nb), np.arange(1 << kb), indexing="ij")
+        di = np.vectorize(_cfg6_dst_index)(n, k, nb, kb).ravel()
+        assert sorted(di.tolist()) == list(range(1 << (nb + kb)))
+        assert (dst[di] == src[(n * (1 << kb) + k).ravel()]).all()
+
+
 def test_convert_np_sampled_equals_full():
     c = configs.cfg5(m_bits=8, kb_bits=7)
     A, B = L_from_spec(c["A"]), L_from_spec(c["B"])

@@ -120,5 +120,22 @@ def cfg5(m_bits=15, kb_bits=14):
     return dict(name="cfg5", A=A, B=B, elem_bytes=1)
 
 
+# --- pre-shuffle: bf16 operand -> fragment order ------
+
+def cfg6(n_bits=13, k_bits=13):
+    """Reading A25: the HBM pre-shuffle of a bf16 [N, K] operand.
+    A = row-major memory layout (k fastest).  B = the bf16 mma m16n8k16
+    B-operand fragment (reg [k0, k3], lane [k1, k2, n0, n1, n2], reading A8)
+    with two more k-tiles as register bits (k4, k5: 8 bf16 = 16 B per thread,
+    so a consumer loads its fragments with one 128-bit load), 4 warps along n
+    (n3, n4), blocks over the rest -- the destination buffer in
+    hardware-index order."""
+    out = [("n", n_bits), ("k", k_bits)]
+    B = spec([("reg", ["k0", "k3", "k4", "k5"]), ("lane", ["k1", "k2", "n0", "n1", "n2"]),
+              ("warp", ["n3", "n4"]), ("block", _rng("k", 6, k_bits) + _rng("n", 5, n_bits))], out)
+    A = spec([("offset", _rng("k", 0, k_bits) + _rng("n", 0, n_bits))], out)
+    return dict(name="cfg6", A=A, B=B, elem_bytes=2)
+
+
 def total_elems(spec_):
     return 1 << sum(b for _, b in spec_["in_dims"])
