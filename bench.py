@@ -380,7 +380,7 @@ NCU_METRICS = [
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
 ]
-OUR_KERNELS = "regex:(ll_smem|ll_shfl|ll_upcast|ll_regs|convert_.*kernel|gather_.*kernel)"
+OUR_KERNELS = "regex:(ll_smem|ll_shfl|ll_upcast|ll_regs|ll_regperm|ll_tma|ll_gather|convert_.*kernel|gather_.*kernel)"
 
 
 def ncu_probe(args):
@@ -813,11 +813,18 @@ def main():
 def kernel_name(plan, cfg, args):
     if args.upcast:
         return "ll_upcast_hbm (NVRTC)"
+    tuned = dict(kv.split("=") for kv in args.tune)
+    tma_jit = tuned.get("tma_jit", "1") != "0"
+    if is_gather(cfg):
+        return {"smem": "ll_gather_smem (NVRTC)", "shuffle": "ll_gather_shfl (NVRTC)",
+                "generic": "gather_direct_kernel", "direct": "gather_direct_kernel"}.get(
+                    plan.get("path"), plan.get("path"))
     return {"smem": "ll_smem_hbm (NVRTC)", "generic": "convert_generic_kernel",
-            "shuffle": "gather_shuffle_kernel" if is_gather(cfg) else "ll_shfl_hbm (NVRTC)",
-            "smem_tma": "convert_tma_kernel", "regs": "convert_regs_kernel",
-            "smem_tma_store": "convert_tma_store_kernel", "copy": "cudaMemcpyAsync",
-            "direct": "gather_direct_kernel"}.get(plan.get("path"), plan.get("path"))
+            "shuffle": "ll_shfl_hbm (NVRTC)", "regperm": "ll_regperm (NVRTC)",
+            "smem_tma": "ll_tma_hbm (NVRTC)" if tma_jit else "convert_tma_kernel",
+            "regs": "convert_regs_kernel",
+            "smem_tma_store": "ll_tma_hbm (NVRTC)" if tma_jit else "convert_tma_store_kernel",
+            "copy": "cudaMemcpyAsync"}.get(plan.get("path"), plan.get("path"))
 
 
 def run_e2e(ll, b, args, dev, world, rank, scaling, barrier, coll_dev):

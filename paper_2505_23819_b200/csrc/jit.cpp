@@ -824,41 +824,52 @@ std::string regperm_kernel_source(const ConvertPlan& P) {
   const int W = P.w, CB = W << P.rp_bits, NW = CB / 4;
   const bool v8 = CB >= 32;
   const int step = v8 ? 32 : 16;
+  // U chunks per thread and iteration, all loads issued first: >= 64 bytes
+  // in flight per thread (one 32-byte chunk alone ran at 0.89 of the smem
+  // path, profiles/r02/classify)
+  const int U = std::max(1, planner_knob("regperm_u", std::max(1, 64 / CB)));
   std::ostringstream o;
   o << "extern \"C\" __global__ void __launch_bounds__(256) ll_regperm(\n"
     << "    const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, long long t0,\n"
     << "    long long t1, long long src_shift, long long dst_shift) {\n"
-    << "  for (long long c = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; c < t1;\n"
-    << "       c += (long long)gridDim.x * blockDim.x) {\n"
-    << "    const unsigned char* s = src + c * " << CB << " - src_shift;\n"
-    << "    unsigned char* d = dst + c * " << CB << " - dst_shift;\n"
-    << "    unsigned R[" << NW << "];\n";
-  for (int off = 0; off < CB; off += step) {
-    const int k = off / 4, nw = step / 4;
-    o << "    asm volatile(\"ld.global.nc.L1::no_allocate.v" << nw << ".u32 {";
-    for (int q = 0; q < nw; ++q) o << (q ? "," : "") << "%" << q;
-    o << "}, [%" << nw << "];\" : ";
-    for (int q = 0; q < nw; ++q) o << (q ? ", " : "") << "\"=r\"(R[" << k + q << "])";
-    o << " : \"l\"(s + " << off << "));\n";
-  }
-  std::vector<std::string> Q(NW);
-  for (int q = 0; q < NW; ++q) {
-    std::vector<std::pair<std::string, int>> bs;
-    for (int b = 0; b < 4; ++b) {
-      const int byte = 4 * q + b, e = byte / W, eb = byte % W;
-      const int sbyte = P.rp_src[e] * W + eb;
-      bs.push_back(std::make_pair("R[" + std::to_string(sbyte >> 2) + "]", sbyte & 3));
+    << "  for (long long c0 = t0 + (long long)blockIdx.x * " << U << " * blockDim.x + threadIdx.x; c0 < t1;\n"
+    << "       c0 += (long long)gridDim.x * " << U << " * blockDim.x) {\n"
+    << "    unsigned R[" << U << "][" << NW << "];\n";
+  for (int u = 0; u < U; ++u) {
+    o << "    { const long long c = c0 + " << u << "LL * blockDim.x; if (c < t1) {\n"
+      << "      const unsigned char* s = src + c * " << CB << " - src_shift;\n";
+    for (int off = 0; off < CB; off += step) {
+      const int k = off / 4, nw = step / 4;
+      o << "      asm volatile(\"ld.global.nc.L1::no_allocate.v" << nw << ".u32 {";
+      for (int q = 0; q < nw; ++q) o << (q ? "," : "") << "%" << q;
+      o << "}, [%" << nw << "];\" : ";
+      for (int q = 0; q < nw; ++q) o << (q ? ", " : "") << "\"=r\"(R[" << u << "][" << k + q << "])";
+      o << " : \"l\"(s + " << off << "));\n";
     }
-    Q[q] = pack_bytes(bs);
+    o << "    } }\n";
   }
-  for (int q = 0; q < NW; ++q) o << "    const unsigned Q" << q << " = " << Q[q] << ";\n";
-  for (int off = 0; off < CB; off += step) {
-    const int k = off / 4, nw = step / 4;
-    o << "    asm volatile(\"st.global.cs.v" << nw << ".b32 [%0], {";
-    for (int q = 0; q < nw; ++q) o << (q ? "," : "") << "%" << q + 1;
-    o << "};\" :: \"l\"(d + " << off << ")";
-    for (int q = 0; q < nw; ++q) o << ", \"r\"(Q" << k + q << ")";
-    o << " : \"memory\");\n";
+  for (int u = 0; u < U; ++u) {
+    o << "    { const long long c = c0 + " << u << "LL * blockDim.x; if (c < t1) {\n"
+      << "      unsigned char* d = dst + c * " << CB << " - dst_shift;\n";
+    const std::string Ru = "R[" + std::to_string(u) + "]";
+    for (int q = 0; q < NW; ++q) {
+      std::vector<std::pair<std::string, int>> bs;
+      for (int b = 0; b < 4; ++b) {
+        const int byte = 4 * q + b, e = byte / W, eb = byte % W;
+        const int sbyte = P.rp_src[e] * W + eb;
+        bs.push_back(std::make_pair(Ru + "[" + std::to_string(sbyte >> 2) + "]", sbyte & 3));
+      }
+      o << "      const unsigned Q" << q << " = " << pack_bytes(bs) << ";\n";
+    }
+    for (int off = 0; off < CB; off += step) {
+      const int k = off / 4, nw = step / 4;
+      o << "      asm volatile(\"st.global.cs.v" << nw << ".b32 [%0], {";
+      for (int q = 0; q < nw; ++q) o << (q ? "," : "") << "%" << q + 1;
+      o << "};\" :: \"l\"(d + " << off << ")";
+      for (int q = 0; q < nw; ++q) o << ", \"r\"(Q" << k + q << ")";
+      o << " : \"memory\");\n";
+    }
+    o << "    } }\n";
   }
   o << "  }\n}\n";
   return o.str();
@@ -877,7 +888,8 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+  const int U = std::max(1, planner_knob("regperm_u", std::max(1, 64 / (P.w << P.rp_bits))));
+  int64_t grid = std::min<int64_t>((n + 256 * U - 1) / (256 * U), (int64_t)sms * 8);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
   grid = std::max<int64_t>(1, grid);
   long long t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;

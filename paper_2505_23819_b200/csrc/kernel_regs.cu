@@ -14,11 +14,25 @@
 
 namespace ll {
 
-// MAT: 0 = st/ld.shared vectors, 1 = stmatrix / ldmatrix, 2 = their .trans forms
+// MAT: 0 = st/ld.shared vectors, 1 = stmatrix / ldmatrix, 2 = their .trans
+// forms, 3 = the sm_100a 8-bit forms stmatrix.m16n8.trans.b8 /
+// ldmatrix.m16n16.trans.b8 (G = words per thread: 1 / 2 / 4 matrices for the
+// store, 2 / 4 words = x1 / x2 for the load)
 template <int G, int MAT>
 __device__ __forceinline__ void smem_put(uint32_t addr, const uint32_t* r) {
   if constexpr (MAT == 0) {
     sts<G * 4>(addr, r);
+  } else if constexpr (MAT == 3 && G == 4) {
+    asm volatile("stmatrix.sync.aligned.m16n8.x4.trans.shared.b8 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+                 : "memory");
+  } else if constexpr (MAT == 3 && G == 2) {
+    asm volatile("stmatrix.sync.aligned.m16n8.x2.trans.shared.b8 [%0], {%1, %2};" ::"r"(addr), "r"(r[0]),
+                 "r"(r[1])
+                 : "memory");
+  } else if constexpr (MAT == 3) {
+    asm volatile("stmatrix.sync.aligned.m16n8.x1.trans.shared.b8 [%0], {%1};" ::"r"(addr), "r"(r[0])
+                 : "memory");
   } else if constexpr (MAT == 2 && G == 4) {
     asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr),
                  "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
@@ -48,6 +62,18 @@ template <int G, int MAT>
 __device__ __forceinline__ void smem_get(uint32_t addr, uint32_t* r) {
   if constexpr (MAT == 0) {
     lds<G * 4>(addr, r);
+  } else if constexpr (MAT == 3 && G == 4) {
+    asm volatile("ldmatrix.sync.aligned.m16n16.x2.trans.shared.b8 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr)
+                 : "memory");
+  } else if constexpr (MAT == 3 && G == 2) {
+    asm volatile("ldmatrix.sync.aligned.m16n16.x1.trans.shared.b8 {%0, %1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1])
+                 : "r"(addr)
+                 : "memory");
+  } else if constexpr (MAT == 3) {
+    static_assert(G != 1, "ldmatrix.b8 returns at least two words");
   } else if constexpr (MAT == 2 && G == 4) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -126,11 +152,13 @@ __device__ __forceinline__ void exchange_r(uint32_t (&R)[NW], uint32_t (&Q)[NW],
     if (k == 8) exchange<NW, GWW, MW, 2, 0>(R, Q, reps, sbase, wx, rx, p);
     else if (k == 9) exchange<NW, GWW, MW, 2, 1>(R, Q, reps, sbase, wx, rx, p);
     else if (W == 2 && k == 10) exchange<NW, GWW, MW, 2, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 1 && k == 11) exchange<NW, GWW, MW, 2, W == 1 ? 3 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
   if constexpr (NW >= 4) {
     if (k == 16) exchange<NW, GWW, MW, 4, 0>(R, Q, reps, sbase, wx, rx, p);
     else if (k == 17) exchange<NW, GWW, MW, 4, 1>(R, Q, reps, sbase, wx, rx, p);
     else if (W == 2 && k == 18) exchange<NW, GWW, MW, 4, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 1 && k == 19) exchange<NW, GWW, MW, 4, W == 1 ? 3 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
 }
 
@@ -142,15 +170,18 @@ __device__ __forceinline__ void exchange_w(uint32_t (&R)[NW], uint32_t (&Q)[NW],
   if (k == 4) exchange_r<W, NW, 1, 0>(R, Q, reps, sbase, wx, rx, p);
   else if (k == 5) exchange_r<W, NW, 1, 1>(R, Q, reps, sbase, wx, rx, p);
   else if (W == 2 && k == 6) exchange_r<W, NW, 1, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
+  else if (W == 1 && k == 7) exchange_r<W, NW, 1, W == 1 ? 3 : 0>(R, Q, reps, sbase, wx, rx, p);
   if constexpr (NW >= 2) {
     if (k == 8) exchange_r<W, NW, 2, 0>(R, Q, reps, sbase, wx, rx, p);
     else if (k == 9) exchange_r<W, NW, 2, 1>(R, Q, reps, sbase, wx, rx, p);
     else if (W == 2 && k == 10) exchange_r<W, NW, 2, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 1 && k == 11) exchange_r<W, NW, 2, W == 1 ? 3 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
   if constexpr (NW >= 4) {
     if (k == 16) exchange_r<W, NW, 4, 0>(R, Q, reps, sbase, wx, rx, p);
     else if (k == 17) exchange_r<W, NW, 4, 1>(R, Q, reps, sbase, wx, rx, p);
     else if (W == 2 && k == 18) exchange_r<W, NW, 4, W == 2 ? 2 : 0>(R, Q, reps, sbase, wx, rx, p);
+    else if (W == 1 && k == 19) exchange_r<W, NW, 4, W == 1 ? 3 : 0>(R, Q, reps, sbase, wx, rx, p);
   }
 }
 

@@ -198,6 +198,66 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
       opts.push_back(o);
     }
   }
+  // sm_100a 8-bit matrix tiles (w = 1; measured on the B200, tools/b8_probe.cu,
+  // pinned in test_b8_matrix_tiles_measured_on_b200_are_linear_layouts):
+  //   stmatrix.m16n8.x{1,2,4}.trans.b8: word bytes (e0, e1) -> (row 1, col 8),
+  //     lanes 0..4 -> (row 2, row 4, col 1, 2, 4); 8 rows of 16 B per matrix,
+  //     row r of matrix m addressed by lane 8m + r
+  //   ldmatrix.m16n16.x{1,2}.trans.b8: two words per matrix; bytes (e0, e1)
+  //     -> (row 1, row 2), word 1 -> col 8, lanes -> (row 4, row 8, col 1,
+  //     2, 4); 16 rows of 16 B, row r of matrix m addressed by lane 16m + r
+  // The tile's 16-byte row (the smem granule S_vect) is the side's lanes
+  // 2..4 plus element bit 1 (store) or an instruction word bit (load); left
+  // division of S^{-1} o L by the tile is checked
+  // below.  Either side may instead use vectors whose word bytes are the
+  // row's first two vectors (the other side's transposition).
+  if (w == 1 && planner_knob("regs_b8", 1)) {
+    const std::vector<u64> RA = {Al[2], Al[3], Al[4], e(1)};
+    auto vec_side = [&](const std::vector<u64>& row, u64 e0, u64 e1, const std::vector<u64>& W,
+                        int& gw, int& a, int& b) -> bool {
+      a = b = -1;
+      if (e0 != row[0] || e1 != row[1]) return false;
+      int q = 0;
+      if (pos(W, row[2]) >= 0) { a = pos(W, row[2]); ++q; }
+      if (q == 1 && pos(W, row[3]) >= 0) { b = pos(W, row[3]); ++q; }
+      gw = 1 << q;
+      return true;
+    };
+    // A writes with stmatrix.b8
+    {
+      Opt o;
+      o.svect = RA;
+      o.wr_mat = 3;
+      o.wr_gw = std::min(4, NW);
+      o.wa = LB > 0 ? 0 : -1;
+      o.wb = LB > 1 ? 1 : -1;
+      bool ok = false;
+      for (int u = 0; u < LB && !ok; ++u) {
+        if (NW < 2 || !(Bl[2] == RA[0] && Bl[3] == RA[1] && Bl[4] == RA[2] && Bw[u] == RA[3])) continue;
+        o.rd_mat = 3; o.rd_gw = std::min(4, NW); o.ra = u; o.rb = -1;
+        for (int v = 0; v < LB && o.rd_gw == 4; ++v) if (v != u) { o.rb = v; break; }
+        ok = true;
+      }
+      if (!ok) ok = vec_side(RA, X[0], X[1], Bw, o.rd_gw, o.ra, o.rb);
+      if (ok) {
+        o.cost = NW / o.wr_gw + NW / o.rd_gw;
+        opts.push_back(o);
+      }
+    }
+    // B reads with ldmatrix.b8 (column-8 word bit u), A writes vectors
+    for (int u = 0; u < LB && NW >= 2; ++u) {
+      Opt o;
+      o.svect = {Bl[2], Bl[3], Bl[4], Bw[u]};
+      o.rd_mat = 3;
+      o.rd_gw = std::min(4, NW);
+      o.ra = u;
+      o.rb = -1;
+      for (int v = 0; v < LB && o.rd_gw == 4; ++v) if (v != u) { o.rb = v; break; }
+      if (!vec_side(o.svect, e(0), e(1), f.Aw0, o.wr_gw, o.wa, o.wb)) continue;
+      o.cost = NW / o.wr_gw + NW / o.rd_gw;
+      opts.push_back(o);
+    }
+  }
   if (opts.empty()) return false;
   // options by cost (instructions per thread), matrix instructions first on
   // ties (the paper's preference for hardware primitives); an option
@@ -226,17 +286,25 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
     // accesses; the address providers (rows = lanes 2..4, then the matrix
     // select word bits) for stmatrix / ldmatrix
     auto thr_vecs = [&](int mat, const std::vector<u64>& W, const std::vector<u64>& L, int a, int b,
-                        u64 w0) {
+                        u64 w0, bool ld) {
       std::vector<u64> t;
       if (!mat) return L;
+      if (mat == 3) {
+        // b8 address providers: rows (element bits, lanes 0, 1), then the matrix selects
+        t = ld ? std::vector<u64>{w0, X[1], L[0], L[1]} : std::vector<u64>{w0, L[0], L[1]};
+        if (!ld && a >= 0) t.push_back(W[a]);
+        if (b >= 0) t.push_back(W[b]);
+        while (t.size() < 5) t.push_back(L[2]);
+        return t;
+      }
       t = mat == 2 ? std::vector<u64>{w0, L[0], L[1]} : std::vector<u64>{L[2], L[3], L[4]};
       if (a >= 0) t.push_back(W[a]);
       if (b >= 0) t.push_back(W[b]);
       while (t.size() < 5) t.push_back(L[2]);  // padding (dropped by the phase rule)
       return t;
     };
-    At = thr_vecs(best.wr_mat, Aw, Al, best.wa, best.wb, wA);
-    Bt = thr_vecs(best.rd_mat, Bw, Bl, best.ra, best.rb, wB);
+    At = thr_vecs(best.wr_mat, Aw, Al, best.wa, best.wb, wA, false);
+    Bt = thr_vecs(best.rd_mat, Bw, Bl, best.ra, best.rb, wB, true);
     sw = optimal_swizzle(At, Bt, V, d, w);
     std::vector<u64> Scols = sw.vect;
     Scols.insert(Scols.end(), sw.bank.begin(), sw.bank.end());
@@ -283,9 +351,54 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
     if (best.rd_mat == 1 && !divisible(own ? std::vector<u64>{wB} : WB, Bl, rest_of(Bw, Bl, Bwp))) return false;
     if (best.wr_mat == 2 && !divisible_t(wA, Aw, Al, Awp)) return false;
     if (best.rd_mat == 2 && !divisible_t(wB, Bw, Bl, Bwp)) return false;
+    if (w == 1 && (best.wr_mat == 3 || best.rd_mat == 3)) {
+      // b8 tiles: the row vectors are offset bits 0..3 and no other column of
+      // the side touches them; vector sides: bytes, then the granule's words,
+      // at the low offset bits, nothing else below the granule
+      auto b8_ok = [&](int mat, const std::vector<u64>& row, const std::vector<u64>& others) {
+        for (int t = 0; t < 4; ++t)
+          if (mat == 3 && f2_apply(Sinv, row[t]) != e(t)) return false;
+        for (u64 c : others)
+          if (f2_apply(Sinv, c) & 15u) return false;
+        return true;
+      };
+      auto vec_ok = [&](u64 e0, u64 e1, const std::vector<u64>& W, int a, int b, int gw,
+                        const std::vector<u64>& L, const std::vector<u64>& Wp) {
+        std::vector<u64> gran = {e0, e1};
+        if (gw >= 2) gran.push_back(W[a]);
+        if (gw >= 4) gran.push_back(W[b]);
+        for (size_t t = 0; t < gran.size(); ++t)
+          if (f2_apply(Sinv, gran[t]) != e((int)t)) return false;
+        const u64 low = (u64(1) << gran.size()) - 1;
+        std::vector<u64> rest(L);
+        rest.insert(rest.end(), Wp.begin(), Wp.end());
+        for (int u = 0; u < (int)W.size(); ++u)
+          if (!(gw >= 2 && u == a) && !(gw >= 4 && u == b)) rest.push_back(W[u]);
+        for (u64 c : rest)
+          if (f2_apply(Sinv, c) & low) return false;
+        return true;
+      };
+      const std::vector<u64>& row = best.svect;
+      if (best.wr_mat == 3) {
+        std::vector<u64> oth = {e(0), Al[0], Al[1]};
+        oth.insert(oth.end(), Aw.begin(), Aw.end());
+        oth.insert(oth.end(), Awp.begin(), Awp.end());
+        if (!b8_ok(3, row, oth)) return false;
+      } else if (!vec_ok(e(0), e(1), Aw, best.wa, best.wb, best.wr_gw, Al, Awp)) {
+        return false;
+      }
+      if (best.rd_mat == 3) {
+        std::vector<u64> oth = {X[0], X[1], Bl[0], Bl[1]};
+        for (int u = 0; u < LB; ++u) if (u != best.ra) oth.push_back(Bw[u]);
+        oth.insert(oth.end(), Bwp.begin(), Bwp.end());
+        if (!b8_ok(3, row, oth)) return false;
+      } else if (!vec_ok(X[0], X[1], Bw, best.ra, best.rb, best.rd_gw, Bl, Bwp)) {
+        return false;
+      }
+    }
     // vector sides read / write whole words: their word must be offset bit 0
-    if (own && best.wr_mat == 0 && f2_apply(Sinv, wA) != 1) return false;
-    if (own && best.rd_mat == 0 && f2_apply(Sinv, wB) != 1) return false;
+    if (own && w == 2 && best.wr_mat == 0 && f2_apply(Sinv, wA) != 1) return false;
+    if (own && w == 2 && best.rd_mat == 0 && f2_apply(Sinv, wB) != 1) return false;
     RegsPlan& rp = P.rp;
     rp = RegsPlan{};
     rp.nw = nw;
@@ -323,8 +436,24 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
     const std::vector<u64> Bwc = canon(Bw, best.ra, best.rb, best.rd_gw, rp.n_rsw, rp.rsw_a, rp.rsw_b);
     auto fill = [&](int mat, const std::vector<u64>& W, const std::vector<u64>& L,
                     const std::vector<u64>& Wp, int a, int b, int gw, uint32_t* thr, uint32_t* inst,
-                    u64 wrow0) {
-      if (mat) {
+                    u64 wrow0, bool ld) {
+      if (mat == 3) {
+        // b8: address provider lane p; store: p bits 0..2 = rows (e0, lanes
+        // 0, 1), bits 3, 4 = matrix (words a, b); load: p bits 0..3 = rows
+        // (e0, e1, lanes 0, 1), bit 4 = matrix (word b)
+        thr[0] = boff(wrow0);
+        if (ld) {
+          thr[1] = boff(X[1]);
+          thr[2] = boff(L[0]);
+          thr[3] = boff(L[1]);
+          thr[4] = b >= 0 && gw >= 4 ? boff(W[b]) : 0;
+        } else {
+          thr[1] = boff(L[0]);
+          thr[2] = boff(L[1]);
+          thr[3] = a >= 0 && gw >= 2 ? boff(W[a]) : 0;
+          thr[4] = b >= 0 && gw >= 4 ? boff(W[b]) : 0;
+        }
+      } else if (mat) {
         // address provider lane p: rows = p bits 0..2 (the data lanes 2..4;
         // .trans: the word bit and lanes 0, 1), matrix = p bits 3, 4 (the
         // selected word bits)
@@ -351,9 +480,9 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
       }
       return true;
     };
-    if (!fill(rp.wr_mat, Awc, Al, Awp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.wr_gw, rp.sw_thr, rp.sw_inst, wA))
+    if (!fill(rp.wr_mat, Awc, Al, Awp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.wr_gw, rp.sw_thr, rp.sw_inst, wA, false))
       return false;
-    if (!fill(rp.rd_mat, Bwc, Bl, Bwp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.rd_gw, rp.sr_thr, rp.sr_inst, wB))
+    if (!fill(rp.rd_mat, Bwc, Bl, Bwp, LB > 0 ? 0 : -1, LB > 1 ? 1 : -1, rp.rd_gw, rp.sr_thr, rp.sr_inst, wB, true))
       return false;
     P.nv = NW;
     P.tile_bits = d;
@@ -366,15 +495,20 @@ bool plan_regs(ConvertPlan& P, const Layout& A, const Layout& B, const std::vect
     if ((ok = build(o))) break;
   if (!ok) return false;
   RegsPlan& rp = P.rp;
-  static const char* kinds[] = {"st.shared", "stmatrix", "stmatrix.trans", "ld.shared", "ldmatrix", "ldmatrix.trans"};
+  static const char* kinds[] = {"st.shared", "stmatrix", "stmatrix.trans", "stmatrix.m16n8.trans.b8",
+                                "ld.shared", "ldmatrix", "ldmatrix.trans", "ldmatrix.m16n16.trans.b8"};
   js << ",\"regs\":{\"warps_log2\":" << nw << ",\"words_per_thread\":" << NW
      << ",\"write\":\"" << kinds[rp.wr_mat] << "\",\"write_words\":" << rp.wr_gw
-     << ",\"read\":\"" << kinds[3 + rp.rd_mat] << "\",\"read_words\":" << rp.rd_gw
+     << ",\"read\":\"" << kinds[4 + rp.rd_mat] << "\",\"read_words\":" << rp.rd_gw
      << ",\"write_instr_per_thread\":" << NW / rp.wr_gw
      << ",\"read_instr_per_thread\":" << NW / rp.rd_gw << ",\"n_tiles\":" << rp.n_tiles
      << ",\"swaps\":" << swaps.size() << ",\"sw_thr\":" << u32_json(rp.sw_thr, 5 + nw)
      << ",\"sr_thr\":" << u32_json(rp.sr_thr, 5 + nw)
-     << ",\"sw_inst\":" << u32_json(rp.sw_inst, NW / rp.wr_gw)
+     << ",\"wsw\":[";
+  for (int i = 0; i < rp.n_wsw; ++i) js << (i ? "," : "") << "[" << int(rp.wsw_a[i]) << "," << int(rp.wsw_b[i]) << "]";
+  js << "],\"rsw\":[";
+  for (int i = 0; i < rp.n_rsw; ++i) js << (i ? "," : "") << "[" << int(rp.rsw_a[i]) << "," << int(rp.rsw_b[i]) << "]";
+  js << "],\"sw_inst\":" << u32_json(rp.sw_inst, NW / rp.wr_gw)
      << ",\"sr_inst\":" << u32_json(rp.sr_inst, NW / rp.rd_gw) << "},\"S_vect\":" << vec_json(sw.vect)
      << ",\"S_bank\":" << vec_json(sw.bank) << ",\"S_idx\":" << vec_json(sw.idx)
      << ",\"granule_bytes\":" << ((w << (int)V.size()))

@@ -147,6 +147,73 @@ def test_convert_vec32(w):
         ll.tune("vec32", 0)
 
 
+def b8_pair(rng, kind, nr=3, nw=1, nb=2):
+    """fp8 pairs the sm_100a 8-bit matrix tiles serve (the tiles
+    measured in test_b8_matrix_tiles_measured_on_b200_are_linear_layouts):
+    kind "both": B's lanes 2..4 and its first word bit hold A's lanes 2..4 and
+    A's byte bit 1 (stmatrix.b8 writes, ldmatrix.b8 reads); "st_vec": B's
+    bytes are A's lanes 2, 3 (stmatrix.b8 writes, vector reads); "ld_vec":
+    A's bytes are B's lanes 2, 3 (vector writes, ldmatrix.b8 reads).  One
+    tensor dim of nr + 5 + nw + nb bits; blocks identical."""
+    d = nr + 5 + nw
+    bits = list(range(d))
+    rng.shuffle(bits)
+    blk = list(range(d, d + nb))
+
+    def mk(reg, lane, warp):
+        return {"in_dims": [("reg", nr), ("lane", 5), ("warp", nw), ("block", nb)],
+                "out_dims": [("t", d + nb)],
+                "bases": {"reg": [(1 << b,) for b in reg], "lane": [(1 << b,) for b in lane],
+                          "warp": [(1 << b,) for b in warp], "block": [(1 << b,) for b in blk]}}
+
+    if kind == "ld_vec":
+        Br, Bl, Bw = bits[:nr], bits[nr:nr + 5], bits[nr + 5:]
+        fixed = [Bl[2], Bl[3], Bl[4]] + ([Br[2]] if nr >= 4 else [])
+        rest = [b for b in bits if b not in fixed]
+        rng.shuffle(rest)
+        a = fixed + rest
+        return {"A": mk(a[:nr], a[nr:nr + 5], a[nr + 5:]), "B": mk(Br, Bl, Bw), "elem_bytes": 1}
+    Ar, Al, Aw = bits[:nr], bits[nr:nr + 5], bits[nr + 5:]
+    if kind == "both":
+        rest = [b for b in bits if b not in (Al[2], Al[3], Al[4], Ar[1])]
+        rng.shuffle(rest)
+        Br = [rest[0], rest[1]] + rest[2:2 + nr - 3]
+        Br.insert(rng.randint(2, nr - 1), Ar[1])      # any of B's word bits
+        r2 = rest[2 + nr - 3:]
+        Bl, Bw = [r2[0], r2[1], Al[2], Al[3], Al[4]], r2[2:]
+    else:
+        fixed = [Al[2], Al[3], Al[4], Ar[1]][:max(2, min(4, nr))]
+        rest = [b for b in bits if b not in fixed]
+        rng.shuffle(rest)
+        b = fixed + rest
+        Br, Bl, Bw = b[:nr], b[nr:nr + 5], b[nr + 5:]
+    return {"A": mk(Ar, Al, Aw), "B": mk(Br, Bl, Bw), "elem_bytes": 1}
+
+
+@pytest.mark.parametrize("kind", ["both", "st_vec", "ld_vec"])
+def test_convert_regs_b8_tiles(kind):
+    """Register-faithful fp8 conversions lowered with stmatrix.m16n8.trans.b8
+    / ldmatrix.m16n16.trans.b8 (x1 / x2 / x4 by words per thread), against
+    the oracle; with the b8 tiles off the same pairs have no regs plan or a
+    vector one."""
+    rng = random.Random({"both": 81, "st_vec": 82, "ld_vec": 83}[kind])
+    done = 0
+    for nr, nw in ((3, 0), (3, 1), (4, 1), (4, 2), (5, 1)):
+        for _ in range(3):
+            c = b8_pair(rng, kind, nr=nr, nw=nw)
+            A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+            try:
+                d = ll.plan_describe(A, B, 8, "regs")
+            except ll.LLError:
+                continue
+            assert "b8" in d["regs"]["write"] + d["regs"]["read"], d["regs"]
+            for batch in (1, 3):
+                src, dst = run_convert(c, path="regs", batch=batch, seed=rng.randint(0, 99))
+                assert dst.tobytes() == expect_convert(c, src, batch).tobytes(), (kind, nr, nw, d["regs"])
+            done += 1
+    assert done >= 6
+
+
 def perm_pair(rng, d, w, r, which):
     """A random distributed layout A and B = A with its `which` columns
     ("reg" or "lane") permuted: the pair differs only in register order (no

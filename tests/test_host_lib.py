@@ -541,6 +541,114 @@ def test_tma_kernels_specialise_and_compile():
                     ll.tune(knob, 0)
 
 
+def _regs_b8_emulate(d, c):
+    """Byte addresses of every element on both sides of a register-faithful
+    plan, from the plan's per-thread / per-instruction offsets and the
+    instruction semantics: vectors (st/ld.shared), and the sm_100a 8-bit
+    tiles as measured on the B200 (test_b8_matrix_tiles_measured_on_b200_are_
+    linear_layouts): stmatrix.m16n8.trans.b8 byte b of lane l -> row (b & 1)
+    | (l & 3) << 1 of the matrix's 8 rows (addressed by lanes 8m + row), col
+    8 (b >> 1) + (l >> 2); ldmatrix.m16n16.trans.b8 byte b of word k -> row
+    (b | (l & 3) << 2) (lanes 16m + row), col 8 (k & 1) + (l >> 2), matrix
+    k >> 1."""
+    from oracle.layout import Layout as OL
+    r = d["regs"]
+    nw = r["warps_log2"]
+    NW = r["words_per_thread"]
+    LB = NW.bit_length() - 1
+
+    def dep(j, k, a, b):
+        idx, q = 0, 0
+        for bit in range(LB):
+            if bit == a:
+                idx |= (k & 1) << bit
+            elif bit == b:
+                idx |= ((k >> 1) & 1) << bit
+            else:
+                idx |= ((j >> q) & 1) << bit
+                q += 1
+        return idx
+
+    def swapbits(i, a, b):
+        x, y = (i >> a) & 1, (i >> b) & 1
+        return i ^ ((x ^ y) << a) ^ ((x ^ y) << b)
+
+    def side(L, thr, inst, kind, gw, sw, load):
+        addr = {}
+        a, b = (0 if gw >= 2 else -1), (1 if gw >= 4 else -1)
+        for t in range(32 << nw):
+            lane, warp = t & 31, t >> 5
+
+            def tx(tt):
+                o = 0
+                for q in range(5 + nw):
+                    if (tt >> q) & 1:
+                        o ^= thr[q]
+                return o
+            for j in range(NW // gw):
+                for k in range(gw):
+                    wi = dep(j, k, a, b)          # word index after the transpositions
+                    w0 = wi
+                    for sa, sb in reversed(sw):
+                        w0 = swapbits(w0, sa, sb)
+                    for byte in range(4):
+                        if "b8" not in kind:
+                            ad = (tx(t) ^ inst[j]) + 4 * k + byte
+                        elif not load:       # stmatrix.m16n8.trans.b8, matrix k
+                            row = (byte & 1) | ((lane & 3) << 1)
+                            p = (warp << 5) | (8 * k + row)
+                            ad = (tx(p) ^ inst[j]) + 8 * (byte >> 1) + (lane >> 2)
+                        else:                # ldmatrix.m16n16.trans.b8, word k
+                            row = byte | ((lane & 3) << 2)
+                            p = (warp << 5) | (16 * (k >> 1) + row)
+                            ad = (tx(p) ^ inst[j]) + 8 * (k & 1) + (lane >> 2)
+                        x = L.apply({"reg": 4 * w0 + byte, "lane": lane, "warp": warp, "block": 0})
+                        addr[x] = ad
+        return addr
+
+    A, B = OL(**c["A"]), OL(**c["B"])
+    wr = side(A, r["sw_thr"], r["sw_inst"], r["write"], r["write_words"], r["wsw"], False)
+    rd = side(B, r["sr_thr"], r["sr_inst"], r["read"], r["read_words"], r["rsw"], True)
+    return wr, rd
+
+
+def test_regs_b8_plans_match_the_measured_tiles():
+    """The register-faithful planner's 8-bit matrix options (stmatrix /
+    ldmatrix .trans.b8, left division by the measured tiles):
+    emulating the plan's addresses with the measured instruction semantics,
+    every element is written once and read back from the address it was
+    written to; without the tiles (knob regs_b8=0) the 'both' pairs have no
+    plan at all."""
+    from tests.test_gpu_parity import b8_pair
+    rng = random.Random(5)
+    seen = set()
+    for kind in ("both", "st_vec", "ld_vec"):
+        for nr, nw in ((3, 0), (3, 1), (4, 1), (4, 2), (5, 1)):
+            c = b8_pair(rng, kind, nr=nr, nw=nw, nb=0)
+            A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+            try:
+                d = ll.plan_describe(A, B, 8, "regs")
+            except ll.LLError:
+                continue
+            seen.add((kind, d["regs"]["write"], d["regs"]["read"], d["regs"]["read_words"]))
+            wr, rd = _regs_b8_emulate(d, c)
+            n = 1 << (nr + 5 + nw)
+            assert len(wr) == n and len(set(wr.values())) == n
+            assert wr == rd, (kind, nr, nw)
+            if kind == "both":
+                ll.tune("regs_b8", 0)
+                try:
+                    with pytest.raises(ll.LLError):
+                        ll.plan_describe(A, B, 8, "regs")
+                finally:
+                    ll.tune("regs_b8", 1)
+    kinds = {(w, r) for _, w, r, _ in seen}
+    assert ("stmatrix.m16n8.trans.b8", "ldmatrix.m16n16.trans.b8") in kinds
+    assert ("stmatrix.m16n8.trans.b8", "ld.shared") in kinds
+    assert ("st.shared", "ldmatrix.m16n16.trans.b8") in kinds
+    assert {rw for _, _, _, rw in seen} >= {2, 4}
+
+
 def test_smem_hbm_single_buffer_variant_compiles():
     """smem_jit_single: the compiled smem kernel with one staging buffer per
     group (no prefetch) is a different source, and NVRTC compiles both."""
