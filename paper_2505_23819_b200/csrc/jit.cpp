@@ -1148,9 +1148,16 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
     o << "    asm volatile(\"ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q["
       << 4 * j + 1 << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "]) : \"r\"(rb + (srx ^ "
       << p.sr_gran[j] << "u)) : \"memory\");\n";
-  o << "    __syncwarp();\n"
-    << "    if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(empty0 + 8u * slot) : \"memory\");\n"
-    << "    if (++s == " << NS << ") { s = 0; ph ^= 1u; }\n";
+  // release the slot: every lane's LDS done (the results are in registers),
+  // then one arrival per warp; knob tmaj_fence adds a generic -> async proxy
+  // fence, tmaj_late releases only after the tile's stores were issued
+  const bool fence = planner_knob("tmaj_fence", 0) != 0, late = planner_knob("tmaj_late", 0) != 0;
+  auto release = [&]() {
+    if (fence) o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+    o << "    __syncwarp();\n"
+      << "    if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(empty0 + 8u * slot) : \"memory\");\n";
+  };
+  if (!late) release();
   for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], "Q");
   o << "    long long so, dof; tile_off(t, so, dof);\n";
   if (!tma_store) {
@@ -1187,6 +1194,8 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
       << "    }\n"
       << "    ++it;\n";
   }
+  if (late) release();
+  o << "    if (++s == " << NS << ") { s = 0; ph ^= 1u; }\n";
   o << "  }\n";
   if (tma_store) o << "  if (tb == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
   o << "}\n";

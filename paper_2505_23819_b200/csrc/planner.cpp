@@ -158,7 +158,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
       name != "smem_jit_noload" && name != "smem_jit_nostore" && name != "bcast_dedup" &&
       name != "auto_regperm" && name != "tma_jit" && name != "tmaj_k" && name != "tmaj_stages" &&
-      name != "tmaj_cps" && name != "regs_b8" && name != "regperm_u")
+      name != "tmaj_cps" && name != "regs_b8" && name != "regperm_u" && name != "tmaj_fence" && name != "tmaj_late")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
