@@ -446,7 +446,10 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
     o << "    __syncthreads();\n    }\n    long long c1 = clock64();\n"
       << "    if (tid == 0 && cycles) cycles[blockIdx.x] = c1 - c0;\n"
       << "    if (acc == 0x9e3779b9u && reps < 0) err[1] = 1;\n";
-  o << "    __syncthreads();   // every thread is done with stage s\n"
+  // every thread is done with stage s; its generic-proxy reads ordered
+  // before the async-proxy refill (fence.proxy.async, as the TMA kernels)
+  o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+    << "    __syncthreads();   // every thread is done with stage s\n"
     << "    if (tid == 0 && t + 2 * gs < n_units) issue(t + 2 * gs, s);\n"
     << "  }\n}\n";
   return o.str();

@@ -1148,10 +1148,13 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
     o << "    asm volatile(\"ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q["
       << 4 * j + 1 << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "]) : \"r\"(rb + (srx ^ "
       << p.sr_gran[j] << "u)) : \"memory\");\n";
-  // release the slot: every lane's LDS done (the results are in registers),
-  // then one arrival per warp; knob tmaj_fence adds a generic -> async proxy
-  // fence, tmaj_late releases only after the tile's stores were issued
-  const bool fence = planner_knob("tmaj_fence", 0) != 0, late = planner_knob("tmaj_late", 0) != 0;
+  // release the slot: the warp's generic-proxy reads (LDS) are ordered
+  // before the producer's next async-proxy write (TMA) into it by
+  // fence.proxy.async, then one arrival per warp.  Without the fence the
+  // refill overwrote slots still being read (full-size mismatches on configs
+  // 2 / 3 / 5, scripts/tma_diag.py, profiles/r02/diag); knob tmaj_late
+  // releases only after the tile's stores were issued
+  const bool fence = planner_knob("tmaj_fence", 1) != 0, late = planner_knob("tmaj_late", 0) != 0;
   auto release = [&]() {
     if (fence) o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
     o << "    __syncwarp();\n"

@@ -208,7 +208,9 @@ __global__ void __launch_bounds__(256) convert_tma_kernel(const __grid_constant_
   for (int64_t t = t_first; t < rg.t1; t += n_groups) {
     mbar_wait(bar0 + 8 * stage, (phase >> stage) & 1u);
     phase ^= 1u << stage;
-    // every reader of the group is done with the stage read last iteration
+    // every reader of the group is done with the stage read last iteration;
+    // their generic-proxy reads ordered before the leader's TMA refill
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     group_sync(gw, group);
     issue(t + (NS - 1) * n_groups, stage == 0 ? NS - 1 : stage - 1);
     uint32_t Q[NW];
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(256) convert_tma_store_kernel(
     mbar_wait(bar0 + 8 * stage, (phase >> stage) & 1u);
     phase ^= 1u << stage;
     if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     group_sync(gw, group);
     issue(t + (NS - 1) * n_groups, stage == 0 ? NS - 1 : stage - 1);
     uint32_t Q[NW];

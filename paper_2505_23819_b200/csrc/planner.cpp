@@ -158,7 +158,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
       name != "smem_jit_noload" && name != "smem_jit_nostore" && name != "bcast_dedup" &&
       name != "auto_regperm" && name != "tma_jit" && name != "tmaj_k" && name != "tmaj_stages" &&
-      name != "tmaj_cps" && name != "regs_b8" && name != "regperm_u" && name != "tmaj_fence" && name != "tmaj_late")
+      name != "tmaj_cps" && name != "regs_b8" && name != "regperm_u" && name != "tmaj_fence" && name != "tmaj_late" &&
+      name != "auto_small_granule_shuffle")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -1026,6 +1027,21 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
     std::ostringstream js2;
     if (plan_smem(*P, X, path == LL_PATH_SMEM || path == LL_PATH_SHUFFLE, js2,
                   path == LL_PATH_SHUFFLE)) {
+      // AUTO with a small shared-memory granule (<= 4 bytes: NV * 16 / G
+      // STS + LDS per thread and tile) takes the warp-shuffle exchange when
+      // the pair is warp-local on the planner's warp tile (config 6, the
+      // pre-shuffle: smem 5293 vs shuffles 6470 GB/s, profiles/r02/s2b;
+      // 16-byte granules keep smem: configs 2 / 5, 6700 / 6986 vs 6595 / 6900)
+      if (path_req == LL_PATH_AUTO && path == LL_PATH_SMEM && P->g <= 4 && op == 0 && w <= 4 &&
+          planner_knob("shuffle_jit", 1) && planner_knob("auto_small_granule_shuffle", 1)) {
+        auto trial = std::make_shared<ConvertPlan>(*P);
+        std::ostringstream js3;
+        if (plan_smem(*trial, X, true, js3, true) && trial->shuffle_ok) {
+          *P = *trial;
+          js2.str(js3.str());
+          path = LL_PATH_SHUFFLE;
+        }
+      }
       js << js2.str();
       if (path == LL_PATH_SHUFFLE && !P->shuffle_ok)
         throw Error(LL_ERR_UNSUPPORTED,

@@ -12,8 +12,8 @@ import paper_2505_23819_b200 as ll  # noqa: E402
 from workloads import configs  # noqa: E402
 from workloads.values import values_torch  # noqa: E402
 
-VARIANTS = [{}, {"tmaj_stages": 3}, {"tmaj_stages": 2}, {"tmaj_fence": 1}, {"tmaj_late": 1}, {"pdl": 0},
-            {"tmaj_cps": 2}, {"tmaj_k": 1}]
+VARIANTS = [{}, {"tmaj_fence": 0}, {"tmaj_fence": 0, "tmaj_late": 1}, {"tmaj_stages": 2}, {"pdl": 0},
+            {"tmaj_cps": 2}, {"tmaj_k": 1}, {"tma_jit": 0}]
 
 
 def main():
@@ -40,7 +40,7 @@ def main():
                                 "first": bad[:4].tolist(),
                                 "zeros_in_bad": int((dst[bad] == 0).sum().item()) if bad.numel() else 0})
                 for k in v:
-                    ll.tune(k, {"pdl": 1}.get(k, 0))
+                    ll.tune(k, {"pdl": 1, "tmaj_fence": 1, "tma_jit": 1}.get(k, 0))
                 out.append({"cfg": name, "path": path, "knobs": v, "runs": res, "tile_elems": tile_elems})
                 print(json.dumps(out[-1]), flush=True)
 
