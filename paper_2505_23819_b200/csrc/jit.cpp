@@ -822,7 +822,7 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
 // stores it.  No shared memory, no shuffles.
 std::string regperm_kernel_source(const ConvertPlan& P) {
   const int W = P.w, CB = W << P.rp_bits, NW = CB / 4;
-  const bool v8 = CB >= 32;
+  const bool v8 = CB >= 32 && planner_knob("regperm_v8", 1);   // 256-bit accesses
   const int step = v8 ? 32 : 16;
   // U chunks per thread and iteration, all loads issued first: >= 64 bytes
   // in flight per thread (one 32-byte chunk alone ran at 0.89 of the smem
@@ -831,8 +831,10 @@ std::string regperm_kernel_source(const ConvertPlan& P) {
   std::ostringstream o;
   o << "extern \"C\" __global__ void __launch_bounds__(256) ll_regperm(\n"
     << "    const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, long long t0,\n"
-    << "    long long t1, long long src_shift, long long dst_shift) {\n"
-    << "  for (long long c0 = t0 + (long long)blockIdx.x * " << U << " * blockDim.x + threadIdx.x; c0 < t1;\n"
+    << "    long long t1, long long src_shift, long long dst_shift) {\n";
+  const bool pdl = planner_knob("pdl", 1) != 0;
+  if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  o << "  for (long long c0 = t0 + (long long)blockIdx.x * " << U << " * blockDim.x + threadIdx.x; c0 < t1;\n"
     << "       c0 += (long long)gridDim.x * " << U << " * blockDim.x) {\n"
     << "    unsigned R[" << U << "][" << NW << "];\n";
   for (int u = 0; u < U; ++u) {
@@ -848,6 +850,7 @@ std::string regperm_kernel_source(const ConvertPlan& P) {
     }
     o << "    } }\n";
   }
+  if (pdl) o << "    asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   for (int u = 0; u < U; ++u) {
     o << "    { const long long c = c0 + " << u << "LL * blockDim.x; if (c < t1) {\n"
       << "      unsigned char* d = dst + c * " << CB << " - dst_shift;\n";
@@ -889,13 +892,36 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int U = std::max(1, planner_knob("regperm_u", std::max(1, 64 / (P.w << P.rp_bits))));
-  int64_t grid = std::min<int64_t>((n + 256 * U - 1) / (256 * U), (int64_t)sms * 8);
+  // knob regperm_waves: CTAs per SM of a grid-stride launch (0: one pass,
+  // every thread U chunks)
+  const int waves = planner_knob("regperm_waves", 8);
+  int64_t grid = (n + 256 * U - 1) / (256 * U);
+  if (waves > 0) grid = std::min<int64_t>(grid, (int64_t)sms * waves);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
-  grid = std::max<int64_t>(1, grid);
+  grid = std::max<int64_t>(1, std::min<int64_t>(grid, 0x7fffffff));
   long long t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   const void* s = src;
   void* d = dst;
   void* args[] = {(void*)&s, (void*)&d, (void*)&t0, (void*)&t1, (void*)&ss, (void*)&ds};
+  static PFN_LaunchEx launch_ex = entry<PFN_LaunchEx>("cuLaunchKernelEx");
+  if (planner_knob("pdl", 1) && launch_ex) {
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg = {};
+    cfg.gridDimX = (unsigned)grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = 256;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (launch_ex(&cfg, fn, args, nullptr) != CUDA_SUCCESS) {
+      *err = "cuLaunchKernel failed";
+      return cudaErrorLaunchFailure;
+    }
+    return cudaSuccess;
+  }
   void* f = (void*)fn;
   return jit_launch(f, (unsigned)grid, 256, 0, st, args, err);
 }
