@@ -827,7 +827,7 @@ std::string regperm_kernel_source(const ConvertPlan& P) {
   // U chunks per thread and iteration, all loads issued first: >= 64 bytes
   // in flight per thread (one 32-byte chunk alone ran at 0.89 of the smem
   // path, profiles/r02/classify)
-  const int U = std::max(1, planner_knob("regperm_u", std::max(1, 64 / CB)));
+  const int U = planner_knob("regperm_u", 0) > 0 ? planner_knob("regperm_u", 0) : std::max(1, 64 / CB);
   std::ostringstream o;
   o << "extern \"C\" __global__ void __launch_bounds__(256) ll_regperm(\n"
     << "    const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, long long t0,\n"
@@ -891,7 +891,8 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int U = std::max(1, planner_knob("regperm_u", std::max(1, 64 / (P.w << P.rp_bits))));
+  const int U = planner_knob("regperm_u", 0) > 0 ? planner_knob("regperm_u", 0)
+                                                 : std::max(1, 64 / (P.w << P.rp_bits));
   // knob regperm_waves: CTAs per SM of a grid-stride launch (0: one pass,
   // every thread U chunks)
   const int waves = planner_knob("regperm_waves", 8);
