@@ -1234,8 +1234,8 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
 
 namespace {
 // stages / groups of the compiled TMA kernel: K consumer groups (8 consumer
-// warps by default), as many stages as fit the CTA's shared memory at
-// tmaj_cps CTAs per SM (knobs tmaj_k, tmaj_stages, tmaj_cps)
+// warps by default), 3 stages (or knob tmaj_stages, capped by what fits the
+// CTA's shared memory at tmaj_cps CTAs per SM; knobs tmaj_k, tmaj_cps)
 bool tma_jit_shape(const ConvertPlan& P, bool tma_store, int* ns, int* k, int* cps, size_t* smem) {
   const int gw = P.sp.gw;
   int K = planner_knob("tmaj_k", 0);
@@ -1247,8 +1247,11 @@ bool tma_jit_shape(const ConvertPlan& P, bool tma_store, int* ns, int* k, int* c
   const size_t fixed = tma_store ? 2 * K * tb : 0;
   if (budget <= fixed) return false;
   int n = (int)((budget - fixed) / (K * tb));
-  const int want = planner_knob("tmaj_stages", 0);
-  if (want > 0) n = std::min(n, want);
+  // default 3 stages (sweep over 2 / 3 / 4 / 6 stages x 1 / 2 CTAs per SM,
+  // profiles/r02/s2d: 3 stages at one CTA per SM best or within 2 % on
+  // configs 2 / 3 / 5 / 6; deeper rings lost up to 10 %)
+  const int want = planner_knob("tmaj_stages", 0) > 0 ? planner_knob("tmaj_stages", 0) : 3;
+  n = std::min(n, want);
   n = std::min(n, 16);
   if (n < 2) return false;
   *ns = n;
