@@ -893,9 +893,10 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
   }
   const int U = planner_knob("regperm_u", 0) > 0 ? planner_knob("regperm_u", 0)
                                                  : std::max(1, 64 / (P.w << P.rp_bits));
-  // knob regperm_waves: CTAs per SM of a grid-stride launch (0: one pass,
-  // every thread U chunks)
-  const int waves = planner_knob("regperm_waves", 8);
+  // knob regperm_waves: CTAs per SM of a grid-stride launch; 0 (default):
+  // one pass, every thread U chunks (profiles/r02/s2e/regperm_sweep.jsonl:
+  // 6804-6814 vs 6235 GB/s with 8 CTAs per SM striding, w = 4)
+  const int waves = planner_knob("regperm_waves", 0);
   int64_t grid = (n + 256 * U - 1) / (256 * U);
   if (waves > 0) grid = std::min<int64_t>(grid, (int64_t)sms * waves);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
@@ -1302,8 +1303,15 @@ cudaError_t launch_tma_jit(const ConvertPlan& P, bool tma_store, const void* src
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  int64_t grid = std::min<int64_t>((n_tiles + K - 1) / K, (int64_t)sms * cps);
+  // persistent (one CTA per SM x tmaj_cps) or, knob tmaj_tpc > 0, tmaj_tpc
+  // tiles per consumer group and CTA in as many waves as that takes (the
+  // next launch's CTAs then fill SMs while this one drains, PDL)
+  const int tpc = planner_knob("tmaj_tpc", 0);
+  int64_t grid = (n_tiles + K - 1) / K;
+  if (tpc > 0) grid = (grid + tpc - 1) / tpc;
+  else grid = std::min<int64_t>(grid, (int64_t)sms * cps);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+  grid = std::min<int64_t>(grid, 0x7fffffff);
   grid = std::max<int64_t>(1, grid);
   if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   long long t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
