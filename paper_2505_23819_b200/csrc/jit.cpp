@@ -822,7 +822,9 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
 // stores it.  No shared memory, no shuffles.
 std::string regperm_kernel_source(const ConvertPlan& P) {
   const int W = P.w, CB = W << P.rp_bits, NW = CB / 4;
-  const bool v8 = CB >= 32 && planner_knob("regperm_v8", 1);   // 256-bit accesses
+  // 256-bit accesses only on request (knob regperm_v8): 128-bit ran 1.7 %
+  // faster for 1-byte elements, equal for 4-byte (profiles/r02/s2f)
+  const bool v8 = CB >= 32 && planner_knob("regperm_v8", 0);
   const int step = v8 ? 32 : 16;
   // U chunks per thread and iteration, all loads issued first: >= 64 bytes
   // in flight per thread (one 32-byte chunk alone ran at 0.89 of the smem
@@ -1235,31 +1237,34 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
 
 namespace {
 // stages / groups of the compiled TMA kernel: K consumer groups (8 consumer
-// warps by default), 3 stages (or knob tmaj_stages, capped by what fits the
-// CTA's shared memory at tmaj_cps CTAs per SM; knobs tmaj_k, tmaj_cps)
+// warps by default) and tmaj_stages ring stages (default 2), sized for
+// tmaj_cps CTAs per SM (default 2; fewer when the tiles do not fit, e.g. the
+// 32 KB tiles of the config-3 store variant)
 bool tma_jit_shape(const ConvertPlan& P, bool tma_store, int* ns, int* k, int* cps, size_t* smem) {
   const int gw = P.sp.gw;
   int K = planner_knob("tmaj_k", 0);
   if (K <= 0) K = std::max(1, 8 >> gw);
   if ((K << gw) > 16) return false;
-  const int c = std::max(1, std::min(4, planner_knob("tmaj_cps", 1)));
   const size_t tb = (size_t)P.sp.tile_bytes;
-  const size_t budget = (size_t)(227 * 1024) / c - 1024 - 1024;   // per CTA: alignment slack, reserved
   const size_t fixed = tma_store ? 2 * K * tb : 0;
-  if (budget <= fixed) return false;
-  int n = (int)((budget - fixed) / (K * tb));
-  // default 3 stages (sweep over 2 / 3 / 4 / 6 stages x 1 / 2 CTAs per SM,
-  // profiles/r02/s2d: 3 stages at one CTA per SM best or within 2 % on
-  // configs 2 / 3 / 5 / 6; deeper rings lost up to 10 %)
-  const int want = planner_knob("tmaj_stages", 0) > 0 ? planner_knob("tmaj_stages", 0) : 3;
-  n = std::min(n, want);
-  n = std::min(n, 16);
-  if (n < 2) return false;
-  *ns = n;
-  *k = K;
-  *cps = c;
-  *smem = (size_t)n * K * tb + fixed + 1024;
-  return true;
+  // default 2 stages with the non-persistent launch (tmaj_tpc = 2 tiles per
+  // group and CTA; profiles/r02/s2f: config 5 6952 GB/s vs 6692 for the
+  // best persistent shape, 3 stages at one CTA per SM, profiles/r02/s2d;
+  // deeper rings lost up to 10 % there)
+  const int want = std::min(16, planner_knob("tmaj_stages", 0) > 0 ? planner_knob("tmaj_stages", 0) : 2);
+  for (int c = std::max(1, std::min(4, planner_knob("tmaj_cps", 0) > 0 ? planner_knob("tmaj_cps", 0) : 2));
+       c >= 1; --c) {
+    const size_t budget = (size_t)(227 * 1024) / c - 1024 - 1024;   // per CTA: alignment slack, reserved
+    if (budget <= fixed) continue;
+    const int n = std::min(want, (int)((budget - fixed) / (K * tb)));
+    if (n < 2) continue;
+    *ns = n;
+    *k = K;
+    *cps = c;
+    *smem = (size_t)n * K * tb + fixed + 1024;
+    return true;
+  }
+  return false;
 }
 }  // namespace
 
@@ -1303,10 +1308,11 @@ cudaError_t launch_tma_jit(const ConvertPlan& P, bool tma_store, const void* src
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // persistent (one CTA per SM x tmaj_cps) or, knob tmaj_tpc > 0, tmaj_tpc
-  // tiles per consumer group and CTA in as many waves as that takes (the
-  // next launch's CTAs then fill SMs while this one drains, PDL)
-  const int tpc = planner_knob("tmaj_tpc", 0);
+  // tmaj_tpc (default 2) tiles per consumer group and CTA in as many waves
+  // as that takes -- several CTAs per SM, and the next launch's CTAs fill
+  // SMs while this one drains (PDL); tmaj_tpc < 0: persistent, tmaj_cps
+  // CTAs per SM (the persistent grid's drain cost 4-7 %, profiles/r02/s2d)
+  const int tpc = planner_knob("tmaj_tpc", 0) != 0 ? planner_knob("tmaj_tpc", 0) : 2;
   int64_t grid = (n_tiles + K - 1) / K;
   if (tpc > 0) grid = (grid + tpc - 1) / tpc;
   else grid = std::min<int64_t>(grid, (int64_t)sms * cps);

@@ -15,7 +15,7 @@ from scripts.classify_bench import timeit  # noqa: E402
 from tests.test_gpu_parity import perm_pair  # noqa: E402
 from workloads.values import values_torch  # noqa: E402
 
-VARIANTS = [{}, {"regperm_waves": 8}, {"regperm_waves": 4}, {"regperm_waves": 16}, {"regperm_v8": 0},
+VARIANTS = [{}, {"regperm_waves": 8}, {"regperm_waves": 4}, {"regperm_waves": 16}, {"regperm_v8": 1},
             {"pdl": 0}, {"regperm_u": 1}, {"regperm_u": 2}, {"regperm_u": 4}]
 
 
@@ -38,7 +38,7 @@ def main():
             ms = timeit(lambda i: ll.convert(sets[i % 2][0], A, sets[i % 2][1], B, 8 * w, path="regperm"))
             row["regperm " + json.dumps(v)] = round(2 * n * w / (ms * 1e-3) / 1e9)
             for k in v:
-                ll.tune(k, {"pdl": 1, "regperm_waves": 0, "regperm_v8": 1}.get(k, 0))
+                ll.tune(k, {"pdl": 1, "regperm_waves": 0, "regperm_v8": 0}.get(k, 0))
         print(json.dumps(row), flush=True)
         del sets
         torch.cuda.empty_cache()

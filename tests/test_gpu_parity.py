@@ -378,13 +378,14 @@ def test_convert_random_pairs_tma_store(w):
 
 
 @pytest.mark.parametrize("path", ["smem_tma", "smem_tma_store"])
-@pytest.mark.parametrize("knobs", [{"tma_jit": 0}, {"tmaj_stages": 2}, {"tmaj_k": 1, "tmaj_stages": 3},
-                                   {"tmaj_cps": 2}, {"pdl": 0}])
+@pytest.mark.parametrize("knobs", [{"tma_jit": 0}, {"tmaj_tpc": -1}, {"tmaj_tpc": -1, "tmaj_stages": 3},
+                                   {"tmaj_k": 1, "tmaj_stages": 3}, {"tmaj_tpc": 1}, {"pdl": 0}])
 def test_convert_tma_kernel_variants(path, knobs):
-    """The warp-specialised TMA kernels compiled per plan (default) under
-    ring depths that wrap many times, one consumer group per CTA, two CTAs
-    per SM, no PDL, and the template kernels (tma_jit=0); configs 2 / 3 / 5
-    at small sizes, a ragged batch, and a CTA cap (many tiles per CTA)."""
+    """The warp-specialised TMA kernels compiled per plan (default: 2-stage
+    ring, 2 tiles per group and CTA) persistent (rings that wrap many
+    times), one consumer group per CTA, one tile per CTA, no PDL, and the
+    template kernels (tma_jit=0); configs 2 / 3 / 5 at small sizes, a ragged
+    batch, and a CTA cap (many tiles per CTA)."""
     cases = [(configs.cfg2(batch_bits=0), 5, 0), (configs.cfg3(n_bits=9), 1, 3),
              (configs.cfg5(m_bits=9, kb_bits=9), 1, 2), (configs.cfg3(n_bits=9, m_bits=8), 2, 0)]
     for k, v in knobs.items():

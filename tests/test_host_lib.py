@@ -531,7 +531,7 @@ def test_tma_kernels_specialise_and_compile():
             assert ("st.global.cs" in src) == (kern == "tma")
             assert src.count("ld.shared.v4") == d["vectors_per_thread"]
             assert ll.jit_source(A, B, eb, compile=True, kernel=kern)["compiled"]
-            for knob, v in (("tmaj_stages", 2), ("tmaj_k", 1 if d["group_warps_log2"] < 3 else 0)):
+            for knob, v in (("tmaj_stages", 3), ("tmaj_k", 1 if d["group_warps_log2"] < 3 else 0)):
                 if not v:
                     continue
                 ll.tune(knob, v)
