@@ -1057,7 +1057,7 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
 // destination images and let one lane store the image with a TMA tensor
 // store (tma_store = true).  Every offset, permutation, box coordinate
 // shift and stage count is a compile-time constant.
-std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) {
+std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K, int NI) {
   const SmemPlan& p = P.sp;
   const int W = P.w, NV = P.nv, NW = NV * 4, gw = p.gw, LB = ilog2i(NW), lw = ilog2i(W);
   const int NC = K << gw;   // consumer warps
@@ -1165,7 +1165,7 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
   o << "  unsigned char* dthr = dst + st_off - dst_shift;\n"
     << "  (void)dthr; (void)swx;\n";
   if (tma_store)
-    o << "  const unsigned db0 = sb + " << NS * K << "u * " << TB << "u + (unsigned)g * " << 2 * TB << "u;\n"
+    o << "  const unsigned db0 = sb + " << NS * K << "u * " << TB << "u + (unsigned)g * " << NI * TB << "u;\n"
       << "  unsigned it = 0;\n";
   o << "  int s = 0; unsigned ph = 0;\n"
     << "  for (long long t = t0 + (long long)blockIdx.x * " << K << " + g; t < t1; t += (long long)gridDim.x * " << K
@@ -1203,8 +1203,8 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
     const std::string gbar = gw == 0 ? std::string("__syncwarp();")
                                      : "asm volatile(\"bar.sync %0, %1;\" :: \"r\"(g + 1), \"r\"(" +
                                            std::to_string(32 << gw) + ") : \"memory\");";
-    o << "    const unsigned db = db0 + (it & 1u) * " << TB << "u;\n"
-      << "    if (tb == 0) asm volatile(\"cp.async.bulk.wait_group.read 1;\" ::: \"memory\");\n"
+    o << "    const unsigned db = db0 + (it % " << NI << "u) * " << TB << "u;\n"
+      << "    if (tb == 0) asm volatile(\"cp.async.bulk.wait_group.read " << NI - 1 << ";\" ::: \"memory\");\n"
       << "    " << gbar << "\n";
     for (int j = 0; j < NV; ++j) {
       o << "    asm volatile(\"st.shared.v4.b32 [%0], {%1,%2,%3,%4};\" :: \"r\"(db + (swx ^ " << p.sw_gran[j] << "u))";
@@ -1237,42 +1237,49 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K) 
 
 namespace {
 // stages / groups of the compiled TMA kernel: K consumer groups (8 consumer
-// warps by default) and tmaj_stages ring stages (default 2), sized for
-// tmaj_cps CTAs per SM (default 2; fewer when the tiles do not fit, e.g. the
-// 32 KB tiles of the config-3 store variant)
-bool tma_jit_shape(const ConvertPlan& P, bool tma_store, int* ns, int* k, int* cps, size_t* smem) {
+// warps by default), tmaj_stages ring stages (default 2) and, for the store
+// variant, two destination images per group (one when two do not fit),
+// sized for tmaj_cps CTAs per SM (default 2; fewer when the tiles do not
+// fit, e.g. the 32 KB tiles of config 3)
+bool tma_jit_shape(const ConvertPlan& P, bool tma_store, int* ns, int* k, int* cps, size_t* smem,
+                   int* ni) {
   const int gw = P.sp.gw;
   int K = planner_knob("tmaj_k", 0);
   if (K <= 0) K = std::max(1, 8 >> gw);
   if ((K << gw) > 16) return false;
   const size_t tb = (size_t)P.sp.tile_bytes;
-  const size_t fixed = tma_store ? 2 * K * tb : 0;
   // default 2 stages with the non-persistent launch (tmaj_tpc = 2 tiles per
   // group and CTA; profiles/r02/s2f: config 5 6952 GB/s vs 6692 for the
   // best persistent shape, 3 stages at one CTA per SM, profiles/r02/s2d;
   // deeper rings lost up to 10 % there)
   const int want = std::min(16, planner_knob("tmaj_stages", 0) > 0 ? planner_knob("tmaj_stages", 0) : 2);
+  const int img_knob = planner_knob("tmaj_images", 0);
   for (int c = std::max(1, std::min(4, planner_knob("tmaj_cps", 0) > 0 ? planner_knob("tmaj_cps", 0) : 2));
        c >= 1; --c) {
-    const size_t budget = (size_t)(227 * 1024) / c - 1024 - 1024;   // per CTA: alignment slack, reserved
-    if (budget <= fixed) continue;
-    const int n = std::min(want, (int)((budget - fixed) / (K * tb)));
-    if (n < 2) continue;
-    *ns = n;
-    *k = K;
-    *cps = c;
-    *smem = (size_t)n * K * tb + fixed + 1024;
-    return true;
+    for (int im = tma_store ? (img_knob > 0 ? std::min(2, img_knob) : 2) : 0;
+         im >= (tma_store ? (img_knob > 0 ? std::min(2, img_knob) : 1) : 0); --im) {
+      const size_t budget = (size_t)(227 * 1024) / c - 1024 - 1024;   // per CTA: alignment slack, reserved
+      const size_t fixed = (size_t)im * K * tb;
+      if (budget <= fixed) continue;
+      const int n = std::min(want, (int)((budget - fixed) / (K * tb)));
+      if (n < 2) continue;
+      *ns = n;
+      *k = K;
+      *cps = c;
+      *ni = std::max(1, im);
+      *smem = (size_t)n * K * tb + fixed + 1024;
+      return true;
+    }
   }
   return false;
 }
 }  // namespace
 
 std::string tma_hbm_kernel_source(const ConvertPlan& P, bool tma_store) {
-  int ns, k, cps;
+  int ns, k, cps, ni;
   size_t smem;
-  if (!tma_jit_shape(P, tma_store, &ns, &k, &cps, &smem)) return std::string();
-  return tma_hbm_source(P, tma_store, ns, k);
+  if (!tma_jit_shape(P, tma_store, &ns, &k, &cps, &smem, &ni)) return std::string();
+  return tma_hbm_source(P, tma_store, ns, k, ni);
 }
 
 cudaError_t launch_tma_jit(const ConvertPlan& P, bool tma_store, const void* src, void* dst, int max_ctas,
@@ -1283,9 +1290,9 @@ cudaError_t launch_tma_jit(const ConvertPlan& P, bool tma_store, const void* src
   if (!launch || !setattr) return cudaErrorNotSupported;
   const int64_t n_tiles = rg.t1 - rg.t0;
   if (n_tiles <= 0) return cudaSuccess;
-  int ns, K, cps;
+  int ns, K, cps, ni;
   size_t smem;
-  if (!tma_jit_shape(P, tma_store, &ns, &K, &cps, &smem)) {
+  if (!tma_jit_shape(P, tma_store, &ns, &K, &cps, &smem, &ni)) {
     *err = "tma_jit: tile does not fit two stages";
     return cudaErrorInvalidConfiguration;
   }
@@ -1300,7 +1307,7 @@ cudaError_t launch_tma_jit(const ConvertPlan& P, bool tma_store, const void* src
     return e;
   }
   CUfunction fn = nullptr;
-  e = get_kernel(tma_hbm_source(P, tma_store, ns, K), &fn, err, "ll_tma_hbm");
+  e = get_kernel(tma_hbm_source(P, tma_store, ns, K, ni), &fn, err, "ll_tma_hbm");
   if (e != cudaSuccess) return e;
   int sms = 148;
   {

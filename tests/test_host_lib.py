@@ -531,14 +531,16 @@ def test_tma_kernels_specialise_and_compile():
             assert ("st.global.cs" in src) == (kern == "tma")
             assert src.count("ld.shared.v4") == d["vectors_per_thread"]
             assert ll.jit_source(A, B, eb, compile=True, kernel=kern)["compiled"]
-            for knob, v in (("tmaj_stages", 3), ("tmaj_k", 1 if d["group_warps_log2"] < 3 else 0)):
-                if not v:
+            for knobs in ({"tmaj_stages": 3, "tmaj_cps": 1}, {"tmaj_k": 1 if d["group_warps_log2"] < 3 else 0}):
+                if not all(knobs.values()):
                     continue
-                ll.tune(knob, v)
+                for knob, v in knobs.items():
+                    ll.tune(knob, v)
                 try:
                     assert ll.jit_source(A, B, eb, kernel=kern) != src
                 finally:
-                    ll.tune(knob, 0)
+                    for knob in knobs:
+                        ll.tune(knob, 0)
 
 
 def _regs_b8_emulate(d, c):
