@@ -192,7 +192,9 @@ typedef enum {
   LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, REGPERM when
                             only the low <= 64 bytes of each chunk are permuted, else SMEM
                             (measured fastest once compiled per plan; broadcast layouts: the
-                            dedup plan where measured fast), else GENERIC                */
+                            dedup plan where measured fast) -- SHUFFLE instead when the smem
+                            plan's granule is <= 4 bytes and the pair is warp-local --,
+                            else GENERIC                                              */
   LL_PATH_COPY = 1,      /* identity quotient: plain copy                          */
   LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle; by default
                             in a kernel specialised for the plan at run time (NVRTC, every
@@ -209,12 +211,20 @@ typedef enum {
                             hardware-swizzled image: the 32/64/128-byte swizzle modes are
                             Def. 5 instances; the planner picks the mode and the
                             reader's lanes so the reads are conflict-free.
+                            By default a warp-specialised kernel compiled per plan (NVRTC):
+                            one producer warp issues the boxes into an mbarrier ring,
+                            8 consumer warps read, release the slot (fence.proxy.async +
+                            mbarrier arrive) and store; knobs tma_jit (0: the template
+                            kernel), tmaj_stages, tmaj_tpc (tiles per group and CTA; < 0:
+                            persistent), tmaj_cps, tmaj_k, tmaj_images.
                             LL_ERR_UNSUPPORTED when the source tile needs > 5 box dims. */
   LL_PATH_REGS = 9,      /* register-faithful: threads are the layouts' own lanes / warps (one
                             CTA per block index, each thread's registers contiguous in the
                             buffers), exchange registers -> smem (optimal swizzle) -> registers
                             with stmatrix / ldmatrix where the layout is divisible by their tile
-                            (P:588-591), else vectorised st/ld.shared.  Needs reg/lane/warp/block
+                            (b16 plain and .trans; for 1-byte elements the sm_100a
+                            stmatrix.m16n8.trans.b8 / ldmatrix.m16n16.trans.b8 tiles, knob
+                            regs_b8), else vectorised st/ld.shared.  Needs reg/lane/warp/block
                             layouts with equal lane (5) and warp (<= 3) bits, identical block
                             columns and elements of <= 4 bytes; else LL_ERR_UNSUPPORTED.
                             Cost model: a warp-local pair whose shuffle exchange needs <= 4
