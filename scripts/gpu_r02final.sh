@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round 2 consolidated run on the committed head: smoke, GPU suite, the default
+# bench line, its ncu launch list, one ncu --set full capture of the dominant
+# kernel, the reference arm, cfg4full / upcast / cfg6 lines, knob A/B on cfg5.
+O=gpurun_out/r02final
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > $O/smoke.txt 2>&1
+timeout 1800 python -m pytest tests -m gpu -q --durations=10 > $O/pytest_gpu.txt 2>&1
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
+  python bench.py --steps 2 --warmup 3 --ncu off > $O/bench_under_ncu.log 2>&1
+export LL_JIT_SOURCE_DIR=$PWD/$O
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ll_smem_hbm -c 1 -o $O/cfg5_smem_full \
+  python bench.py --steps 2 --warmup 1 --reps 1 --ncu off --no-cpu-baseline --e2e-steps 0 --also '' > $O/ncu_full.log 2>&1
+unset LL_JIT_SOURCE_DIR
+timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_reference.json 2> $O/bench_reference.err
+B="--no-cpu-baseline --also '' --steps 300"
+eval timeout 600 python bench.py --config 4full $B > $O/bench_cfg4full.json 2> $O/bench_cfg4full.err
+eval timeout 600 python bench.py --config 6 $B > $O/bench_cfg6.json 2> $O/bench_cfg6.err
+eval timeout 600 python bench.py --config 5 --upcast $B > $O/bench_upcast.json 2> $O/bench_upcast.err
+timeout 900 python scripts/ab_knobs.py 5 ';vec32=1;smem_jit_tpg=2;smem_jit_single=1;smem_jit_minb=3;pdl=0' 5 > $O/ab_knobs_cfg5.jsonl 2> $O/ab_knobs_cfg5.err
+echo done > $O/done.txt
