@@ -1101,16 +1101,6 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K, 
     o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
       << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; }\n";
   o << "  };\n";
-  // box coordinates of a tile origin (element offset e) in a TmaDesc view
-  auto coords = [&](const TmaDesc& td, const char* e) {
-    std::ostringstream c;
-    for (int i = 0; i < td.ndim; ++i) {
-      c << (i ? ", " : "") << "(int)((" << e << " >> " << td.shift[i] << ")";
-      if (i + 1 < td.ndim) c << " & " << ((1LL << td.size_bits[i]) - 1) << "LL";
-      c << ")";
-    }
-    return c.str();
-  };
   auto regs = [&](int nd, int first) {
     std::ostringstream c;
     c << "{";
@@ -1154,7 +1144,6 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K, 
     << "    }\n"
     << "    return;\n"
     << "  }\n";
-  (void)coords;
   // consumers
   o << "  const int g = warp >> " << gw << ";\n"
     << "  const int tb = lane | ((warp & " << ((1 << gw) - 1) << ") << 5);\n"
