@@ -54,6 +54,21 @@ def main():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from test_gpu_parity import rand_trans_pair  # noqa: E402
     ok &= conv(dict(rand_trans_pair(random.Random(3), 3), name="trans"), "regs")
+    # round 2: compiled TMA kernels (non-persistent default and persistent
+    # rings), register permutation, small-granule shuffle (config 6), the
+    # b8 matrix tiles, broadcast dedup
+    ok &= conv(configs.cfg2(batch_bits=2), "smem_tma")
+    ok &= conv(configs.cfg2(batch_bits=2), "smem_tma_store")
+    ll.tune("tmaj_tpc", -1)
+    ok &= conv(configs.cfg5(m_bits=9, kb_bits=8), "smem_tma")
+    ok &= conv(configs.cfg5(m_bits=9, kb_bits=8), "smem_tma_store")
+    ll.tune("tmaj_tpc", 0)
+    ok &= conv(configs.cfg6(n_bits=7, k_bits=7), "auto")
+    from test_gpu_parity import perm_pair, b8_pair, _bcast_pair  # noqa: E402
+    ok &= conv(dict(perm_pair(random.Random(5), 14, 2, 4, "reg"), name="regperm"), "regperm")
+    for kind in ("both", "st_vec", "ld_vec"):
+        ok &= conv(dict(b8_pair(random.Random(6), kind, nr=4, nw=1), name="b8_" + kind), "regs")
+    ok &= conv(dict(_bcast_pair(random.Random(7), 13, 2, 0, 2), name="bcast"), "smem")
     # the template smem kernel (the default compiles the plan)
     ll.tune("smem_jit", 0)
     ok &= conv(configs.cfg3(n_bits=8), "smem")
@@ -61,7 +76,7 @@ def main():
     g = configs.cfg4(r_bits=3)
     L = ll.Layout.from_spec(g["L"])
     m = 1 << L.in_bits
-    for path in ("shuffle", "auto"):
+    for path in ("shuffle", "smem", "auto"):
         gs = values_torch(m, 4, 4, "cuda")
         gi = indices_torch(m, 5, 32, "cuda")
         go = torch.empty_like(gs)
