@@ -1183,7 +1183,21 @@ std::string tma_hbm_source(const ConvertPlan& P, bool tma_store, int NS, int K, 
   for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], "Q");
   o << "    long long so, dof; tile_off(t, so, dof);\n";
   if (!tma_store) {
-    for (int u = 0; u < NV; ++u) {
+    // 256-bit stores where a thread's destination vectors u, u + 1 are
+    // adjacent: the TMA swizzle modes often force reader lanes whose 16-byte
+    // vectors leave 16-byte gaps between lanes (config 2: 16-byte runs),
+    // which one 32-byte store per pair closes (knob tmaj_v8)
+    bool st32 = NV >= 2 && planner_knob("tmaj_v8", 1) != 0;
+    for (int u = 0; st32 && u + 1 < NV; u += 2) st32 = p.st_vec[u + 1] == p.st_vec[u] + 16;
+    for (int u = 0; u < NV; u += st32 ? 2 : 1) {
+      if (st32) {
+        o << "    asm volatile(\"st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\" :: \"l\"(dthr + dof + "
+          << p.st_vec[u] << ")";
+        for (int q = 0; q < 2; ++q)
+          for (int k = 0; k < 4; ++k) o << ", \"r\"(Q[" << deposit_word_h(u + q, k, LB, ga, gb) << "])";
+        o << " : \"memory\");\n";
+        continue;
+      }
       o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dof + " << p.st_vec[u] << ")";
       for (int k = 0; k < 4; ++k) o << ", \"r\"(Q[" << deposit_word_h(u, k, LB, ga, gb) << "])";
       o << " : \"memory\");\n";

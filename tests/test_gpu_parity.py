@@ -380,7 +380,7 @@ def test_convert_random_pairs_tma_store(w):
 @pytest.mark.parametrize("path", ["smem_tma", "smem_tma_store"])
 @pytest.mark.parametrize("knobs", [{"tma_jit": 0}, {"tmaj_tpc": -1}, {"tmaj_tpc": -1, "tmaj_stages": 3},
                                    {"tmaj_k": 1, "tmaj_stages": 3}, {"tmaj_tpc": 1}, {"tmaj_images": 1},
-                                   {"pdl": 0}])
+                                   {"tmaj_v8": 0}, {"pdl": 0}])
 def test_convert_tma_kernel_variants(path, knobs):
     """The warp-specialised TMA kernels compiled per plan (default: 2-stage
     ring, 2 tiles per group and CTA) persistent (rings that wrap many
@@ -402,7 +402,7 @@ def test_convert_tma_kernel_variants(path, knobs):
             assert _np(dst, w).tobytes() == expect_convert(c, _np(src, w), batch).tobytes(), (path, knobs)
     finally:
         for k in knobs:
-            ll.tune(k, {"tma_jit": 1, "pdl": 1}.get(k, 0))
+            ll.tune(k, {"tma_jit": 1, "pdl": 1, "tmaj_v8": 1}.get(k, 0))
 
 
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
