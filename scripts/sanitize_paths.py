@@ -23,7 +23,7 @@ def conv(c, path, batch=1):
     A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
     n = (1 << A.in_bits) * batch
     src = values_torch(n, 3, w, "cuda")
-    dst = torch.zeros_like(src)
+    dst = torch.zeros((1 << B.in_bits) * batch, dtype=src.dtype, device="cuda")
     ll.convert(src, A, dst, B, 8 * w, path=path, batch=batch)
     torch.cuda.synchronize()
     s = src.cpu().numpy().view(NP[w])
