@@ -478,18 +478,21 @@ cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const in
     const int mu_knob = planner_knob("gather_shfl_mu", 0);
     const int MU = mu_knob > 0 ? mu_knob : std::max(1, std::min(4 / NV, 64 / (NV * (16 / P.w))));
     const long long warps = (n_units + MU - 1) / MU;
-    // knob gather_shfl_waves: CTAs per SM of the grid-stride launch (default
-    // 8); < 0: one pass (every warp MU units)
-    const int waves = planner_knob("gather_shfl_waves", 8);
+    // knob gather_shfl_waves: CTAs per SM of a grid-stride launch; < 0
+    // (default): one pass, every warp MU units (config 4: 6460 vs 6084 GB/s
+    // striding over 8 CTAs per SM, profiles/r02/s2l)
+    const int waves = planner_knob("gather_shfl_waves", -1);
     long long g = (warps + 7) / 8;
     if (waves > 0) g = std::min<long long>(g, (long long)sms * waves);
     grid = (int)std::max<long long>(1, std::min<long long>(g, 0x7fffffff));
   } else {
     smem = 2u * ((unsigned)(P.w + 4) << P.cta_bits) + 16u;
     const int per_sm = std::max(1, std::min(8, (int)((200u * 1024u) / smem)));
-    // knob gather_smem_upc: units per CTA (grid = units / upc, several waves);
-    // 0 (default): persistent, every resident CTA slot striding over the units
-    const int upc = planner_knob("gather_smem_upc", 0);
+    // knob gather_smem_upc: units per CTA (grid = units / upc, several
+    // waves; default 1: config 4full 6464 vs 6132 GB/s for the persistent
+    // grid, profiles/r02/s2l); 0: persistent, every resident CTA slot
+    // striding over the units
+    const int upc = planner_knob("gather_smem_upc", 1);
     const long long g = upc > 0 ? (n_units + upc - 1) / upc : std::min<long long>(n_units, (long long)sms * per_sm);
     grid = (int)std::max<long long>(1, std::min<long long>(g, 0x7fffffff));
   }

@@ -14,10 +14,10 @@ from scripts.classify_bench import timeit  # noqa: E402
 from workloads import configs  # noqa: E402
 from workloads.values import indices_torch, values_torch  # noqa: E402
 
-VARIANTS = [("auto", {}), ("generic", {}), ("smem", {}), ("smem", {"gather_smem_upc": 1}),
+VARIANTS = [("auto", {}), ("generic", {}), ("smem", {}), ("smem", {"gather_smem_upc": 0}),
             ("smem", {"gather_smem_upc": 2}), ("smem", {"gather_smem_upc": 4}), ("shuffle", {}),
-            ("shuffle", {"gather_shfl_waves": -1}), ("shuffle", {"gather_shfl_waves": 16})]
-DEFAULTS = {"gather_smem_upc": 0, "gather_shfl_waves": 8}
+            ("shuffle", {"gather_shfl_waves": 8}), ("shuffle", {"gather_shfl_waves": 16})]
+DEFAULTS = {"gather_smem_upc": 1, "gather_shfl_waves": -1}
 
 
 def main():

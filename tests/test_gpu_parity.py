@@ -691,6 +691,31 @@ def test_gather_compiled_paths_configs(path, variant):
     assert out.tobytes() == exp.tobytes()
 
 
+@pytest.mark.parametrize("path,knobs", [("smem", {"gather_smem_upc": 0}), ("smem", {"gather_smem_upc": 3}),
+                                         ("shuffle", {"gather_shfl_waves": 8}), ("shuffle", {"gather_shfl_waves": 1})])
+def test_gather_launch_shapes(path, knobs):
+    """The compiled gathers' launch shapes (one pass by default; persistent /
+    several units per CTA / grid-stride) on config 4 and its full-axis
+    variant, byte-exact."""
+    defaults = {"gather_smem_upc": 1, "gather_shfl_waves": -1}
+    for k, v in knobs.items():
+        ll.tune(k, v)
+    try:
+        for variant in ("tile", "full"):
+            c = configs.cfg4(r_bits=5, variant=variant)
+            L = ll.Layout.from_spec(c["L"])
+            try:
+                ll.gather_describe(L, c["axis"], 32, path)
+            except ll.LLError:
+                continue
+            src, idx, out = run_gather(c, path)
+            exp = oconv.gather_np(src, idx, _olayout(c["L"]), c["axis"])
+            assert out.tobytes() == exp.tobytes(), (path, knobs, variant)
+    finally:
+        for k in knobs:
+            ll.tune(k, defaults[k])
+
+
 @pytest.mark.parametrize("path", ["shuffle", "smem"])
 @pytest.mark.parametrize("w", [1, 2, 4, 8])
 def test_gather_timed_one_cta(path, w):
