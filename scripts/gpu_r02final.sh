@@ -2,7 +2,7 @@
 # Round 2 consolidated run on the committed head: smoke, GPU suite, the default
 # bench line, its ncu launch list, one ncu --set full capture of the dominant
 # kernel, the reference arm, cfg4full / upcast / cfg6 lines, knob A/B on cfg5.
-O=gpurun_out/r02final
+O=gpurun_out/${FINAL_TAG:-r02final}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > $O/smoke.txt 2>&1
@@ -19,5 +19,7 @@ B="--no-cpu-baseline --also '' --steps 300"
 eval timeout 600 python bench.py --config 4full $B > $O/bench_cfg4full.json 2> $O/bench_cfg4full.err
 eval timeout 600 python bench.py --config 6 $B > $O/bench_cfg6.json 2> $O/bench_cfg6.err
 eval timeout 600 python bench.py --config 5 --upcast $B > $O/bench_upcast.json 2> $O/bench_upcast.err
-timeout 900 python scripts/ab_knobs.py 5 ';vec32=1;smem_jit_tpg=2;smem_jit_single=1;smem_jit_minb=3;pdl=0' 5 > $O/ab_knobs_cfg5.jsonl 2> $O/ab_knobs_cfg5.err
+timeout 900 python scripts/ab_paths.py 3 > $O/ab_paths.jsonl 2> $O/ab_paths.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_timed.csv \
+  python bench.py --steps 20 --warmup 3 --ncu off --no-cpu-baseline --e2e-steps 0 --also '' --reps 2 > $O/bench_timed_under_ncu.log 2>&1
 echo done > $O/done.txt
