@@ -320,6 +320,7 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
   }
   const bool noload = planner_knob("smem_jit_noload", 0) != 0;   // test hook: no global loads
   const bool nostore = planner_knob("smem_jit_nostore", 0) != 0; // test hook: no global stores
+  const bool noxchg = planner_knob("smem_jit_noxchg", 0) != 0;   // test hook: no exchange
   auto load = [&](const char* ind, const std::string& R) {
     if (noload) {
       for (int i = 0; i < NW; ++i)
@@ -377,7 +378,11 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
   auto body = [&](const std::string& R, const std::string& dv, int ahead) {
     o << "    { const long long dcur = " << dv << ";\n";
     for (int i = 0; i < p.n_swaps; ++i) emit_swap(o, W, NW, p.swap_a[i], p.swap_b[i], R.c_str());
-    for (int j = 0; j < NG; ++j) {
+    // test hook (knob smem_jit_noxchg): no shared-memory exchange at all --
+    // the loaded words are stored as they are, so the kernel keeps exactly
+    // the global access pattern of the plan (the pattern's own ceiling)
+    if (noxchg) for (int i = 0; i < NW; ++i) o << "    Q[" << i << "] = " << R << "[" << i << "];\n";
+    for (int j = 0; j < NG && !noxchg; ++j) {
       o << "    asm volatile(\"st.shared.";
       if (GWd == 4) o << "v4.b32 [%0], {%1,%2,%3,%4};\"";
       else if (GWd == 2) o << "v2.b32 [%0], {%1,%2};\"";
@@ -392,9 +397,10 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
       load("      ", R);
       o << "    } }\n";
     }
-    if (gw == 0) o << "    __syncwarp();\n";
+    if (noxchg) {
+    } else if (gw == 0) o << "    __syncwarp();\n";
     else o << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(group + 1), \"r\"(" << (32 << gw) << ") : \"memory\");\n";
-    for (int j = 0; j < NG; ++j) {
+    for (int j = 0; j < NG && !noxchg; ++j) {
       o << "    asm volatile(\"ld.shared.";
       if (GWd == 4) o << "v4.b32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(Q[" << 4 * j << "]), \"=r\"(Q[" << 4 * j + 1
                       << "]), \"=r\"(Q[" << 4 * j + 2 << "]), \"=r\"(Q[" << 4 * j + 3 << "])";

@@ -157,6 +157,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "auto_asym" && name != "tma_run_bytes_dst" && name != "gather_shfl_mu" &&
       name != "gather_cta_extra" && name != "gather_auto_smem" && name != "vec32" &&
       name != "smem_jit_noload" && name != "smem_jit_nostore" && name != "bcast_dedup" &&
+      name != "smem_jit_noxchg" &&
       name != "auto_regperm" && name != "tma_jit" && name != "tmaj_k" && name != "tmaj_stages" &&
       name != "tmaj_cps" && name != "regs_b8" && name != "regperm_u" && name != "tmaj_fence" && name != "tmaj_late" &&
       name != "auto_small_granule_shuffle" && name != "regperm_v8" && name != "regperm_waves" && name != "tmaj_tpc" && name != "tmaj_images" && name != "tmaj_v8" &&
