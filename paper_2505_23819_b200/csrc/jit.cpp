@@ -913,6 +913,12 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
   const void* s = src;
   void* d = dst;
   void* args[] = {(void*)&s, (void*)&d, (void*)&t0, (void*)&t1, (void*)&ss, (void*)&ds};
+  // knob regperm_occ: CTAs per SM (occupancy capped through dynamic shared
+  // memory the kernel does not use; 0 = no cap)
+  const int occ = planner_knob("regperm_occ", 0);
+  unsigned smem = occ > 0 ? (unsigned)std::min(227 * 1024, 228 * 1024 / occ - 1024) : 0u;
+  static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
+  if (smem > 48 * 1024 && setattr) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   static PFN_LaunchEx launch_ex = entry<PFN_LaunchEx>("cuLaunchKernelEx");
   if (planner_knob("pdl", 1) && launch_ex) {
     CUlaunchAttribute attr[1];
@@ -923,6 +929,7 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
     cfg.gridDimY = cfg.gridDimZ = 1;
     cfg.blockDimX = 256;
     cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = smem;
     cfg.hStream = (CUstream)st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -933,7 +940,7 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
     return cudaSuccess;
   }
   void* f = (void*)fn;
-  return jit_launch(f, (unsigned)grid, 256, 0, st, args, err);
+  return jit_launch(f, (unsigned)grid, 256, smem, st, args, err);
 }
 
 std::string shuffle_hbm_kernel_source(const ConvertPlan& P) { return shuffle_hbm_source(P); }

@@ -15,13 +15,13 @@ from scripts.classify_bench import timeit  # noqa: E402
 from tests.test_gpu_parity import perm_pair  # noqa: E402
 from workloads.values import values_torch  # noqa: E402
 
-VARIANTS = [{}, {"regperm_waves": 8}, {"regperm_waves": 4}, {"regperm_waves": 16}, {"regperm_v8": 1},
-            {"pdl": 0}, {"regperm_u": 1}, {"regperm_u": 2}, {"regperm_u": 4}]
+VARIANTS = [{}, {"regperm_occ": 2}, {"regperm_occ": 3}, {"regperm_occ": 4}, {"regperm_occ": 6},
+            {"regperm_u": 2}, {"regperm_u": 8}, {"regperm_occ": 4, "regperm_u": 2}]
 
 
 def main():
     d = 26
-    for w, r in ((4, 3), (4, 2), (2, 4), (1, 5)):
+    for w, r in ((4, 3), (4, 2), (2, 3), (1, 4), (1, 5)):
         rng = random.Random(7 + w)
         c = perm_pair(rng, d, w, r, "reg")
         A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
@@ -38,7 +38,7 @@ def main():
             ms = timeit(lambda i: ll.convert(sets[i % 2][0], A, sets[i % 2][1], B, 8 * w, path="regperm"))
             row["regperm " + json.dumps(v)] = round(2 * n * w / (ms * 1e-3) / 1e9)
             for k in v:
-                ll.tune(k, {"pdl": 1, "regperm_waves": 0, "regperm_v8": 0}.get(k, 0))
+                ll.tune(k, {"pdl": 1, "regperm_waves": 0, "regperm_v8": 0, "regperm_occ": 0}.get(k, 0))
         print(json.dumps(row), flush=True)
         del sets
         torch.cuda.empty_cache()
