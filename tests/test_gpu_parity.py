@@ -234,6 +234,8 @@ def perm_pair(rng, d, w, r, which):
     A = {"in_dims": names, "out_dims": out, "bases": bases}
     bb = dict(bases)
     p = list(bb[which])
+    if len(p) < 2:
+        raise ValueError("perm_pair: %s needs at least two columns to permute" % which)
     while p == bases[which]:
         rng.shuffle(p)
     bb[which] = p
