@@ -190,7 +190,8 @@ ll_status ll_gather(const void* src, const int32_t* idx, void* out, ll_layout la
 
 typedef enum {
   LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, REGPERM when
-                            only the low <= 64 bytes of each chunk are permuted, else SMEM
+                            only the low <= 64 bytes of each chunk are permuted (and the smem
+                            plan's granule is < 8 bytes), else SMEM
                             (measured fastest once compiled per plan; broadcast layouts: the
                             dedup plan where measured fast) -- SHUFFLE instead when the smem
                             plan's granule is <= 4 bytes and the pair is warp-local --,
@@ -245,7 +246,9 @@ typedef enum {
                             identity above, so every thread loads its 2^q-element chunk,
                             permutes it in registers (renames / prmt, compiled per plan) and
                             stores it -- no shared memory, no shuffles.  AUTO takes it
-                            whenever it applies; LL_ERR_UNSUPPORTED otherwise. */
+                            unless the smem plan exchanges >= 8-byte granules (measured
+                            1-3 % faster there; knob auto_regperm: 2 = always, 0 = never);
+                            LL_ERR_UNSUPPORTED when it does not apply. */
 } ll_path;
 
 typedef struct {

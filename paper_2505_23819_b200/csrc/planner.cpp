@@ -902,6 +902,16 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
     const int cb = std::max(q, vb);
     bool ok = (int64_t(w) << cb) <= 64 && cb <= P->nB;
     for (int k = 0; ok && k < q; ++k) ok = popcount64(X[k]) == 1 && X[k] < (u64(1) << q);
+    // AUTO (knob auto_regperm = 1): the register permutation unless the smem
+    // plan exchanges granules of >= 8 bytes -- measured on register-only
+    // pairs (profiles/r02/s2f classify, s2q): smem ahead by 0.7-2.6 % there
+    // (6464-6915 vs 6323-6819 GB/s), the register permutation ahead by 15-19 %
+    // where the smem plan falls back to 4-byte granules; 2 = always
+    if (ok && path == LL_PATH_AUTO && planner_knob("auto_regperm", 1) == 1) {
+      auto trial = std::make_shared<ConvertPlan>(*P);
+      std::ostringstream js2;
+      if (plan_smem(*trial, X, true, js2) && trial->g >= 8) ok = false;
+    }
     if (ok) {
       P->rp_bits = cb;
       for (int e = 0; e < (1 << cb); ++e) {

@@ -244,9 +244,10 @@ def perm_pair(rng, d, w, r, which):
 
 @pytest.mark.parametrize("w", [1, 2, 4, 8])
 def test_convert_register_permutation_pairs(w):
-    """Pairs that differ only in register order take LL_PATH_REGPERM under
-    AUTO (no STS / LDS, no shuffles) whenever the permuted chunk is <= 64
-    bytes; byte-exact, also batched and sharded."""
+    """Pairs that differ only in register order: LL_PATH_REGPERM (no STS /
+    LDS, no shuffles) applies whenever the permuted chunk is <= 64 bytes, and
+    AUTO takes it unless the smem plan exchanges >= 8-byte granules (the
+    measured rule); both byte-exact, also batched and sharded."""
     vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
     rng = random.Random(1500 + w)
     took = 0
@@ -256,23 +257,30 @@ def test_convert_register_permutation_pairs(w):
         A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
         d = ll.plan_describe(A, B, 8 * w)
         if (w << max(r, vb)) <= 64:
-            assert d["path"] == "regperm", (r, d["path"])
-        took += d["path"] == "regperm"
+            g = ll.plan_describe(A, B, 8 * w, "smem")["granule_bytes"]
+            assert d["path"] == ("smem" if g >= 8 else "regperm"), (r, g, d["path"])
         batch = 1 + 2 * (case % 2)
         src, dst = run_convert(c, seed=case, batch=batch)
         assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
-        if d["path"] == "regperm":
-            n = 1 << A.in_bits
-            full = values_torch(n, 77, w, "cuda")
-            parts = []
-            for s_ in range(4):
-                s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, 4, s_)
-                dl = torch.empty(d1 - d0, dtype=torch.uint8, device="cuda")
-                ll.convert_shard(full.view(torch.uint8)[s0:s1].clone(), A, dl, B, 8 * w, 4, s_)
-                parts.append(dl)
-            torch.cuda.synchronize()
-            got = torch.cat(parts).cpu().numpy().view(_NP[w])
-            assert got.tobytes() == expect_convert(c, _np(full, w)).tobytes()
+        try:
+            ll.plan_describe(A, B, 8 * w, "regperm")
+        except ll.LLError:
+            assert (w << max(r, vb)) > 64
+            continue
+        took += 1
+        src, dst = run_convert(c, path="regperm", seed=case + 10, batch=batch)
+        assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
+        n = 1 << A.in_bits
+        full = values_torch(n, 77, w, "cuda")
+        parts = []
+        for s_ in range(4):
+            s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, 4, s_, "regperm")
+            dl = torch.empty(d1 - d0, dtype=torch.uint8, device="cuda")
+            ll.convert_shard(full.view(torch.uint8)[s0:s1].clone(), A, dl, B, 8 * w, 4, s_, path="regperm")
+            parts.append(dl)
+        torch.cuda.synchronize()
+        got = torch.cat(parts).cpu().numpy().view(_NP[w])
+        assert got.tobytes() == expect_convert(c, _np(full, w)).tobytes()
     assert took >= 4
 
 
