@@ -56,6 +56,8 @@ def main():
         vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
         rng = random.Random(7 + w)
         for which, r in (("reg", vb), ("reg", vb + 1), ("reg", vb + 2), ("lane", vb)):
+            if which == "reg" and r < 2:
+                continue          # a single register bit has no permutation
             c = perm_pair(rng, d, w, r, which)
             A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
             n = 1 << d
