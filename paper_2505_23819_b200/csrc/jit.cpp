@@ -828,9 +828,13 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
 // stores it.  No shared memory, no shuffles.
 std::string regperm_kernel_source(const ConvertPlan& P) {
   const int W = P.w, CB = W << P.rp_bits, NW = CB / 4;
-  // 256-bit accesses only on request (knob regperm_v8): 128-bit ran 1.7 %
-  // faster for 1-byte elements, equal for 4-byte (profiles/r02/s2f)
-  const bool v8 = CB >= 32 && planner_knob("regperm_v8", 0);
+  // 256-bit accesses for 64-byte chunks (lanes 64 B apart: 128-bit accesses
+  // would leave every instruction half of each sector, 5157-5541 vs
+  // 6376-6846 GB/s, profiles/r02/s2r vs s2f); 128-bit for 32-byte chunks
+  // (1.7 % faster for 1-byte elements, equal for 4-byte); knob regperm_v8:
+  // 1 = always (>= 32-byte chunks), 0 = never
+  const int v8k = planner_knob("regperm_v8", -1);
+  const bool v8 = CB >= 32 && (v8k < 0 ? CB >= 64 : v8k != 0);
   const int step = v8 ? 32 : 16;
   // U chunks per thread and iteration, all loads issued first: >= 64 bytes
   // in flight per thread (one 32-byte chunk alone ran at 0.89 of the smem

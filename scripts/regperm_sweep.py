@@ -38,7 +38,7 @@ def main():
             ms = timeit(lambda i: ll.convert(sets[i % 2][0], A, sets[i % 2][1], B, 8 * w, path="regperm"))
             row["regperm " + json.dumps(v)] = round(2 * n * w / (ms * 1e-3) / 1e9)
             for k in v:
-                ll.tune(k, {"pdl": 1, "regperm_waves": 0, "regperm_v8": 0, "regperm_occ": 0}.get(k, 0))
+                ll.tune(k, {"pdl": 1, "regperm_waves": 0, "regperm_v8": -1, "regperm_occ": 0}.get(k, 0))
         print(json.dumps(row), flush=True)
         del sets
         torch.cuda.empty_cache()
