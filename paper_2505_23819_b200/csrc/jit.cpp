@@ -53,6 +53,36 @@ F entry(const char* name) {
   return reinterpret_cast<F>(f);
 }
 
+// global load / store instructions of the compiled smem kernel; knobs
+// ld_hint / st_hint select the cache qualifiers (ablation of the streaming
+// hints): ld 0 = .nc.L1::no_allocate, 1 = + .L2::256B prefetch, 2 = + L2
+// evict_first policy, 3 = .cs.nc; st 0 = .cs, 1 = plain (write-back),
+// 2 = L2 evict_first policy, 3 = .L1::no_allocate, 4 = L2 evict_last policy.
+// Each returns the asm text from the opcode to the end: "op.vN.T {...}, [%a];"
+std::string ldg_asm(const std::string& vt, const std::string& regs, int a) {
+  const int h = planner_knob("ld_hint", 0);
+  const std::string addr = "[%" + std::to_string(a) + "]";
+  switch (h) {
+    case 1: return "ld.global.nc.L1::no_allocate.L2::256B." + vt + " " + regs + ", " + addr + ";";
+    case 2: return "{ .reg .b64 p_; createpolicy.fractional.L2::evict_first.b64 p_, 1.0; "
+                   "ld.global.nc.L1::no_allocate.L2::cache_hint." + vt + " " + regs + ", " + addr + ", p_; }";
+    case 3: return "ld.global.cs.nc." + vt + " " + regs + ", " + addr + ";";
+    default: return "ld.global.nc.L1::no_allocate." + vt + " " + regs + ", " + addr + ";";
+  }
+}
+std::string stg_asm(const std::string& vt, const std::string& regs) {
+  const int h = planner_knob("st_hint", 0);
+  switch (h) {
+    case 1: return "st.global." + vt + " [%0], " + regs + ";";
+    case 2: return "{ .reg .b64 p_; createpolicy.fractional.L2::evict_first.b64 p_, 1.0; "
+                   "st.global.L2::cache_hint." + vt + " [%0], " + regs + ", p_; }";
+    case 3: return "st.global.L1::no_allocate." + vt + " [%0], " + regs + ";";
+    case 4: return "{ .reg .b64 p_; createpolicy.fractional.L2::evict_last.b64 p_, 1.0; "
+                   "st.global.L2::cache_hint." + vt + " [%0], " + regs + ", p_; }";
+    default: return "st.global.cs." + vt + " [%0], " + regs + ";";
+  }
+}
+
 // element-bit swap (a < b) of the thread's register file, compile-time
 // (same semantics as device_common.cuh apply_swap), emitted as source text
 void emit_swap(std::ostringstream& o, int W, int NW, int a, int b, const char* R) {
@@ -341,7 +371,7 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
         o << ind << "{ unsigned PL[" << 4 * C << "];\n";
         for (int c = 0; c < C; ++c)
           if (ref[c])
-            o << ind << "  asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(PL["
+            o << ind << "  asm volatile(\"" << ldg_asm("v4.u32", "{%0,%1,%2,%3}", 4) << "\" : \"=r\"(PL["
               << 4 * c << "]), \"=r\"(PL[" << 4 * c + 1 << "]), \"=r\"(PL[" << 4 * c + 2 << "]), \"=r\"(PL["
               << 4 * c + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] + 16u * c << "));\n";
         auto src_byte = [&](int byte) {   // byte of the virtual vector -> (word, byte) of PL
@@ -362,12 +392,12 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
     }
     for (int u = 0; u < NV; u += ld32 ? 2 : 1) {
       if (ld32) {
-        o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\" : ";
+        o << ind << "asm volatile(\"" << ldg_asm("v8.u32", "{%0,%1,%2,%3,%4,%5,%6,%7}", 8) << "\" : ";
         for (int q = 0; q < 8; ++q) o << (q ? ", " : "") << "\"=r\"(" << R << "[" << 4 * u + q << "])";
         o << " : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
         continue;
       }
-      o << ind << "asm volatile(\"ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\" : \"=r\"(" << R << "["
+      o << ind << "asm volatile(\"" << ldg_asm("v4.u32", "{%0,%1,%2,%3}", 4) << "\" : \"=r\"(" << R << "["
         << 4 * u << "]), \"=r\"(" << R << "[" << 4 * u + 1 << "]), \"=r\"(" << R << "[" << 4 * u + 2
         << "]), \"=r\"(" << R << "[" << 4 * u + 3 << "]) : \"l\"(sthr + so + " << p.ld_vec[u] << "));\n";
     }
@@ -436,7 +466,7 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
             << ", S3 = " << wexpr[3] << ";\n";
           const std::vector<uint32_t> offs = P.copy_off.empty() ? std::vector<uint32_t>{0u} : P.copy_off;
           for (uint32_t co : offs)
-            o << "      asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dcur + "
+            o << "      asm volatile(\"" << stg_asm("v4.u32", "{%1,%2,%3,%4}") << "\" :: \"l\"(dthr + dcur + "
               << p.st_vec[u] + 16u * c + co << "u), \"r\"(S0), \"r\"(S1), \"r\"(S2), \"r\"(S3) : \"memory\");\n";
           o << "    }\n";
         }
@@ -444,13 +474,13 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
     }
     for (int u = 0; u < NV && !nostore && !(P.st_span > 0 || P.copy_off.size() > 1); u += st32 ? 2 : 1) {
       if (st32) {
-        o << "    asm volatile(\"st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\" :: \"l\"(dthr + dcur + "
+        o << "    asm volatile(\"" << stg_asm("v8.b32", "{%1,%2,%3,%4,%5,%6,%7,%8}") << "\" :: \"l\"(dthr + dcur + "
           << p.st_vec[u] << ")";
         for (int q = 0; q < 8; ++q) o << ", \"r\"(Q[" << 4 * u + q << "])";
         o << " : \"memory\");\n";
         continue;
       }
-      o << "    asm volatile(\"st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\" :: \"l\"(dthr + dcur + "
+      o << "    asm volatile(\"" << stg_asm("v4.u32", "{%1,%2,%3,%4}") << "\" :: \"l\"(dthr + dcur + "
         << p.st_vec[u] << "), \"r\"(Q[" << 4 * u << "]), \"r\"(Q[" << 4 * u + 1 << "]), \"r\"(Q["
         << 4 * u + 2 << "]), \"r\"(Q[" << 4 * u + 3 << "]) : \"memory\");\n";
     }

@@ -161,7 +161,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "auto_regperm" && name != "tma_jit" && name != "tmaj_k" && name != "tmaj_stages" &&
       name != "tmaj_cps" && name != "regs_b8" && name != "regperm_u" && name != "tmaj_fence" && name != "tmaj_late" &&
       name != "auto_small_granule_shuffle" && name != "regperm_v8" && name != "regperm_waves" && name != "tmaj_tpc" && name != "tmaj_images" && name != "tmaj_v8" &&
-      name != "gather_shfl_waves" && name != "gather_smem_upc" && name != "regperm_occ")
+      name != "gather_shfl_waves" && name != "gather_smem_upc" && name != "regperm_occ" &&
+      name != "ld_hint" && name != "st_hint")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
