@@ -688,10 +688,11 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
       sp.sc_sel[e] = (uint32_t)(slot | (4 + slot) << 4 | slot << 8 | (4 + slot) << 12);
     }
   }
-  // ---- tile map: outer dst bits in the planner's tile order.  Order 2
-  // (default) interleaves "next lowest destination bit" and "next lowest
-  // source bit", so the tiles in flight at the same time form a 2-D block
-  // that is contiguous in both buffers (DRAM locality for transposes).
+  // ---- tile map: outer dst bits in the planner's tile order.  Order 0
+  // (default): destination order, so consecutive tiles complete destination
+  // runs and lines (measured best on every config); 1: source order; 2:
+  // "next lowest destination bit" and "next lowest source bit" interleaved
+  // (the tiles in flight form a 2-D block contiguous in both buffers).
   std::vector<int> O;
   for (int k = 0; k < n; ++k) if (!contains(T, k)) O.push_back(k);
   if ((int)O.size() > LL_MAX_OUTER) return false;
@@ -708,6 +709,15 @@ bool plan_smem(ConvertPlan& P, const std::vector<u64>& X, bool swizzle, std::ost
     torder.insert(torder.end(), by_dst.begin(), by_dst.end());
   } else if (order_knob == 1) {
     torder.insert(torder.end(), by_src.begin(), by_src.end());
+  } else if (order_knob >= 10 && order_knob < 30) {
+    // sweep: the k lowest bits of one buffer's order (10 + k: destination,
+    // 20 + k: source), then the other buffer's order
+    const int k = order_knob % 10;
+    const auto& first = order_knob < 20 ? by_dst : by_src;
+    const auto& second = order_knob < 20 ? by_src : by_dst;
+    for (int i = 0; i < (int)first.size() && i < k; ++i) torder.push_back(first[i]);
+    for (int x : second) if (!contains(torder, x)) torder.push_back(x);
+    for (int x : first) if (!contains(torder, x)) torder.push_back(x);
   } else {
     size_t i = 0, j = 0;
     while (torder.size() < O.size()) {
