@@ -40,6 +40,7 @@ typedef CUresult (*PFN_LoadData)(CUmodule*, const void*);
 typedef CUresult (*PFN_GetFunction)(CUfunction*, CUmodule, const char*);
 typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
 typedef CUresult (*PFN_LaunchEx)(const CUlaunchConfig*, CUfunction, void**, void**);
+typedef CUresult (*PFN_Occupancy)(int*, CUfunction, int, size_t);
 typedef CUresult (*PFN_Launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                                unsigned, unsigned, CUstream, void**, void**);
 
@@ -317,7 +318,7 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
     << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") ll_smem_hbm(\n"
     << "    const __grid_constant__ TileMap tm, const unsigned char* __restrict__ src,\n"
     << "    unsigned char* __restrict__ dst, long long n_groups, long long t0, long long t1,\n"
-    << "    long long src_shift, long long dst_shift) {\n"
+    << "    long long src_shift, long long dst_shift, long long pf_ctas) {\n"
     << "  extern __shared__ __align__(16) unsigned char smem[];\n"
     << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
     << "  const int group = warp >> " << gw << ";\n"
@@ -492,6 +493,22 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
   // visible) before the first global access; let the next grid launch once
   // this CTA's first loads are issued (its CTAs then wait at their own
   // griddepcontrol.wait), hiding launch latency and the tail wave
+  // L2 prefetch of the first tile's source lines before the wait (knob
+  // pdl_prefetch): a CTA that PDL makes resident during the preceding grid's
+  // tail starts pulling its source into L2 then, so the DRAM pipe stays full
+  // across the launch boundary.  Only the first wave (blockIdx < pf_ctas =
+  // SMs x resident CTAs) can be early; later CTAs skip it (2: every CTA
+  // prefetches, the A/B variant).  Safe whatever the
+  // preceding grid writes: L2 is the device's point of coherence (its writes
+  // land in the same lines), and nothing enters L1 before the wait.
+  if (pdl && P.ld_span == 0 && !noload && planner_knob("pdl_prefetch", 0)) {
+    o << "  { const long long tp = t0 + gid; if (tp < t1"
+      << (planner_knob("pdl_prefetch", 0) == 2 ? "" : " && blockIdx.x < pf_ctas") << ") { tile_off(tp);\n";
+    for (int u = 0; u < NV; ++u)
+      o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
+        << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
+    o << "  } }\n";
+  }
   if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  long long t = t0 + gid;\n";
   if (single) {
@@ -1061,10 +1078,25 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
   const int smem = gpc * (single ? 1 : 2) * P.sp.tile_bytes;
   if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
+  // the first wave: CTAs that can be resident at once (pdl_prefetch)
+  long long pf = 0;
+  if (planner_knob("pdl_prefetch", 0)) {
+    static PFN_Occupancy occ = entry<PFN_Occupancy>("cuOccupancyMaxActiveBlocksPerMultiprocessor");
+    static std::mutex occ_mu;
+    static std::map<std::pair<CUfunction, int>, int> occ_cache;
+    std::lock_guard<std::mutex> lk(occ_mu);
+    auto it = occ_cache.find(std::make_pair(fn, smem));
+    if (it == occ_cache.end()) {
+      int per_sm = 0;
+      if (!occ || occ(&per_sm, fn, 256, (size_t)smem) != CUDA_SUCCESS) per_sm = 1;
+      it = occ_cache.emplace(std::make_pair(fn, smem), std::max(1, per_sm)).first;
+    }
+    pf = (long long)it->second * sms;
+  }
   const void* s = src;
   void* d = dst;
   void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
-                  (void*)&ss, (void*)&ds};
+                  (void*)&ss, (void*)&ds, (void*)&pf};
   static PFN_LaunchEx launch_ex = entry<PFN_LaunchEx>("cuLaunchKernelEx");
   CUresult r;
   if (planner_knob("pdl", 1) && launch_ex) {

@@ -1,0 +1,13 @@
+#!/bin/bash
+# PDL L2 prefetch (knob pdl_prefetch): interleaved A/B on configs 2 / 3 / 5 / 6,
+# the strong-scaling shard projection with and without it, and the parity
+# tests of the smem-kernel knobs.
+O=gpurun_out/r02s3e
+mkdir -p $O
+timeout 600 python -m pytest tests -m gpu -q -x -k "hint_and_order" > $O/pytest_knobs.txt 2>&1
+for c in 3 2 5 6; do
+  timeout 600 python scripts/ab_knobs.py $c ";pdl_prefetch=1" 7 >> $O/ab_prefetch.jsonl 2>> $O/ab.err
+done
+timeout 600 python scripts/shard_projection.py "" > $O/proj_base.jsonl 2>> $O/ab.err
+timeout 600 python scripts/shard_projection.py "pdl_prefetch=1" > $O/proj_prefetch.jsonl 2>> $O/ab.err
+echo done > $O/done.txt

@@ -44,6 +44,10 @@ def timeit(fn, steps=50, reps=5):
 
 
 def main():
+    # optional knobs: python scripts/shard_projection.py k=v,k=v
+    for kv in (sys.argv[1].split(",") if len(sys.argv) > 1 and sys.argv[1] else []):
+        k, v = kv.split("=")
+        ll.tune(k, int(v))
     c = configs.cfg5()
     A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
     total = 2 << A.in_bits   # bytes moved by the whole job (1 B read + 1 B written per element)

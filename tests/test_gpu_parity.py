@@ -415,6 +415,34 @@ def test_convert_tma_kernel_variants(path, knobs):
             ll.tune(k, {"tma_jit": 1, "pdl": 1, "tmaj_v8": 1}.get(k, 0))
 
 
+@pytest.mark.parametrize("knobs", [{"ld_hint": 1}, {"ld_hint": 2}, {"ld_hint": 3}, {"st_hint": 1},
+                                   {"st_hint": 2}, {"st_hint": 3}, {"st_hint": 4}, {"tile_order": 1},
+                                   {"tile_order": 2}, {"tile_order": 12}, {"tile_order": 23},
+                                   {"pdl_prefetch": 1}, {"pdl_prefetch": 2}, {"pdl_prefetch": 1, "smem_jit_tpg": 0}])
+def test_convert_smem_kernel_hint_and_order_knobs(knobs):
+    """The compiled smem kernel under the cache-hint ablation (ld_hint /
+    st_hint change only the global instructions' qualifiers) and the tile
+    orders (a different tile -> CTA assignment): configs 2 / 3 / 5 at small
+    sizes with a ragged batch and a CTA cap, byte-exact."""
+    cases = [(configs.cfg2(batch_bits=0), 3, 0), (configs.cfg3(n_bits=9), 1, 3),
+             (configs.cfg5(m_bits=9, kb_bits=9), 2, 0)]
+    for k, v in knobs.items():
+        ll.tune(k, v)
+    try:
+        for c, batch, max_ctas in cases:
+            w = c["elem_bytes"]
+            A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+            assert ll.plan_describe(A, B, 8 * w)["path"] == "smem"
+            src = values_torch((1 << A.in_bits) * batch, 67, w, "cuda")
+            dst = torch.zeros((1 << B.in_bits) * batch, dtype=src.dtype, device="cuda")
+            ll.convert(src, A, dst, B, 8 * w, batch=batch, max_ctas=max_ctas)
+            torch.cuda.synchronize()
+            assert _np(dst, w).tobytes() == expect_convert(c, _np(src, w), batch).tobytes(), knobs
+    finally:
+        for k in knobs:
+            ll.tune(k, {"smem_jit_tpg": 1}.get(k, 0))
+
+
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
 def test_convert_tma_each_swizzle_mode(swz):
     """Every hardware swizzle mode (the Def. 5 instances) executed on the
