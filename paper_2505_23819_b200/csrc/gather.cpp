@@ -240,6 +240,11 @@ std::string gather_shfl_source(const GatherPlanHost& P, int timed) {
     << "  unsigned a_lane = 0;\n";
   for (int c = 0; c < 5; ++c)
     if (P.acol[vb + c]) o << "  if (lane & " << (1 << c) << ") a_lane ^= " << P.acol[vb + c] << "u;\n";
+  // programmatic dependent launch (knob gather_pdl): wait for the preceding
+  // grid before the first global access, let the next one launch at once
+  if (!timed && planner_knob("gather_pdl", 0))
+    o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
+      << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   o << "  for (long long t0 = gw * " << MU << "; t0 < n_units; t0 += tw * " << MU << ") {\n"
     << "    unsigned V[" << MU << "][" << NWD << "]; int I[" << MU << "][" << NS << "];\n";
   for (int m = 0; m < MU; ++m) {
@@ -377,8 +382,11 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
     << "    asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\" "
        ":: \"r\"(st + " << UB << "u), \"l\"(idx + (t << " << CU << ")), \"r\"(" << IB << "u), \"r\"(bar) : \"memory\");\n"
     << "  };\n"
-    << "  const long long g0 = blockIdx.x, gs = gridDim.x;\n"
-    << "  if (tid == 0) { if (g0 < n_units) issue(g0, 0); if (g0 + gs < n_units) issue(g0 + gs, 1); }\n"
+    << "  const long long g0 = blockIdx.x, gs = gridDim.x;\n";
+  if (!timed && planner_knob("gather_pdl", 0))   // programmatic dependent launch (knob gather_pdl)
+    o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
+      << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  o << "  if (tid == 0) { if (g0 < n_units) issue(g0, 0); if (g0 + gs < n_units) issue(g0 + gs, 1); }\n"
     << "  int k = 0;\n"
     << "  for (long long t = g0; t < n_units; t += gs, ++k) {\n"
     << "    const int s = k & 1;\n"
@@ -510,7 +518,8 @@ cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const in
   void* d = out;
   void* args[] = {(void*)&s, (void*)&ix, (void*)&d, (void*)&nu, (void*)&ef, (void*)&check,
                   (void*)&reps, (void*)&cycles};
-  return jit_launch(fn, (unsigned)grid, 256, smem, st, args, err);
+  return jit_launch(fn, (unsigned)grid, 256, smem, st, args, err,
+                    !timed && planner_knob("gather_pdl", 0) != 0);
 }
 
 }  // namespace ll

@@ -501,9 +501,9 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
   // prefetches, the A/B variant).  Safe whatever the
   // preceding grid writes: L2 is the device's point of coherence (its writes
   // land in the same lines), and nothing enters L1 before the wait.
-  if (pdl && P.ld_span == 0 && !noload && planner_knob("pdl_prefetch", 0)) {
+  if (pdl && P.ld_span == 0 && !noload && planner_knob("pdl_prefetch", 1)) {
     o << "  { const long long tp = t0 + gid; if (tp < t1"
-      << (planner_knob("pdl_prefetch", 0) == 2 ? "" : " && blockIdx.x < pf_ctas") << ") { tile_off(tp);\n";
+      << (planner_knob("pdl_prefetch", 1) == 2 ? "" : " && blockIdx.x < pf_ctas") << ") { tile_off(tp);\n";
     for (int u = 0; u < NV; ++u)
       o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
         << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
@@ -770,14 +770,35 @@ cudaError_t jit_kernel(const std::string& src, const char* name, void** fn, std:
 }
 
 cudaError_t jit_launch(void* fn, unsigned grid, unsigned block, unsigned smem, cudaStream_t st,
-                       void** args, std::string* err) {
+                       void** args, std::string* err, bool pdl) {
   static PFN_Launch launch = entry<PFN_Launch>("cuLaunchKernel");
+  static PFN_LaunchEx launch_ex = entry<PFN_LaunchEx>("cuLaunchKernelEx");
   static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
   if (!launch || !setattr) {
     *err = "driver entry points unavailable";
     return cudaErrorNotSupported;
   }
   if (smem > 48 * 1024) setattr((CUfunction)fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+  if (pdl && launch_ex) {
+    // programmatic dependent launch: the kernel itself waits (griddepcontrol.wait)
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg = {};
+    cfg.gridDimX = grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = block;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = smem;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (launch_ex(&cfg, (CUfunction)fn, args, nullptr) != CUDA_SUCCESS) {
+      *err = "cuLaunchKernel failed";
+      return cudaErrorLaunchFailure;
+    }
+    return cudaSuccess;
+  }
   if (launch((CUfunction)fn, grid, 1, 1, block, 1, 1, smem, (CUstream)st, args, nullptr) != CUDA_SUCCESS) {
     *err = "cuLaunchKernel failed";
     return cudaErrorLaunchFailure;
@@ -1080,7 +1101,7 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   // the first wave: CTAs that can be resident at once (pdl_prefetch)
   long long pf = 0;
-  if (planner_knob("pdl_prefetch", 0)) {
+  if (planner_knob("pdl_prefetch", 1)) {
     static PFN_Occupancy occ = entry<PFN_Occupancy>("cuOccupancyMaxActiveBlocksPerMultiprocessor");
     static std::mutex occ_mu;
     static std::map<std::pair<CUfunction, int>, int> occ_cache;

@@ -3,6 +3,8 @@
 
 namespace ll {
 
+int planner_knob(const char* name, int dflt);   // planner.cpp
+
 // ------------------------------------------------------------ generic kernel
 
 // dst[h] = src[X h]: each thread writes one 16-byte destination vector; the
@@ -69,6 +71,10 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(const __grid_constan
   const int64_t pb_mask = (int64_t(1) << pb_shift) - 1;
   const uint32_t amask = (1u << p.ax_bits) - 1;
   const int64_t n_units = V2 ? (p.n_vec >> 1) : p.n_vec;
+  // programmatic dependent launch (knob gather_pdl; a no-op otherwise):
+  // wait for the preceding grid, let the next one launch at once
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_units;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = v >> pb_shift;
@@ -370,15 +376,29 @@ static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void
     // number of 16-byte vectors (knob gather_v8)
     const bool v2 = knobs().gather_v8 && (p.nbits - ilog2(16 / W)) >= 1 &&
                     (reinterpret_cast<uintptr_t>(out) & 31) == 0;
+    auto go = [&](auto kern, int g) {
+      if (planner_knob("gather_pdl", 0)) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)g);
+        cfg.blockDim = dim3(threads);
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, p, (const uint8_t*)src, idx, (uint8_t*)out, err);
+      } else {
+        kern<<<g, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out, err);
+      }
+    };
     if (v2) {
       int64_t want2 = ((p.n_vec >> 1) + (int64_t)threads * vpt - 1) / ((int64_t)threads * vpt);
       if (max_ctas > 0 && want2 > max_ctas) want2 = max_ctas;
       const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>(want2, 0x7fffffff));
-      gather_direct_kernel<W, true><<<grid2, threads, 0, st>>>(p, (const uint8_t*)src, idx,
-                                                              (uint8_t*)out, err);
+      go(gather_direct_kernel<W, true>, grid2);
     } else {
-      gather_direct_kernel<W><<<grid, threads, 0, st>>>(p, (const uint8_t*)src, idx, (uint8_t*)out,
-                                                       err);
+      go(gather_direct_kernel<W, false>, grid);
     }
   }
   return cudaGetLastError();

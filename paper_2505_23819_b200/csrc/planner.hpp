@@ -180,7 +180,7 @@ cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src
 // jit.cpp: compile (cached) / launch a generated kernel (driver API)
 cudaError_t jit_kernel(const std::string& src, const char* name, void** fn, std::string* err);
 cudaError_t jit_launch(void* fn, unsigned grid, unsigned block, unsigned smem, cudaStream_t st,
-                       void** args, std::string* err);
+                       void** args, std::string* err, bool pdl = false);
 
 std::shared_ptr<const GatherPlanHost> get_gather_plan(const Layout& L, int axis, int w,
                                                       int path_req, int64_t batch);

@@ -17,7 +17,9 @@ from workloads.values import indices_torch, values_torch  # noqa: E402
 VARIANTS = [("auto", {}), ("generic", {}), ("smem", {}), ("smem", {"gather_smem_upc": 0}),
             ("smem", {"gather_smem_upc": 2}), ("smem", {"gather_smem_upc": 4}), ("shuffle", {}),
             ("shuffle", {"gather_shfl_waves": 8}), ("shuffle", {"gather_shfl_waves": 16})]
-DEFAULTS = {"gather_smem_upc": 1, "gather_shfl_waves": -1}
+DEFAULTS = {"gather_smem_upc": 1, "gather_shfl_waves": -1, "gather_pdl": 0}
+if len(sys.argv) > 1 and sys.argv[1] == "pdl":   # programmatic dependent launch A/B
+    VARIANTS = [(p, kn) for p in ("auto", "generic", "smem", "shuffle") for kn in ({}, {"gather_pdl": 1})]
 
 
 def main():
@@ -28,7 +30,7 @@ def main():
         sets = [(values_torch(n, 4 + k, w, "cuda"), indices_torch(n, 5 + k, c["idx_limit"], "cuda"),
                  torch.empty(n, dtype=values_torch(1, 0, w, "cpu").dtype, device="cuda")) for k in range(2)]
         res = {}
-        for _ in range(3):
+        for _ in range(5 if len(sys.argv) > 1 else 3):
             for p, kn in VARIANTS:
                 try:
                     ll.gather_describe(L, c["axis"], 8 * w, p)

@@ -418,7 +418,7 @@ def test_convert_tma_kernel_variants(path, knobs):
 @pytest.mark.parametrize("knobs", [{"ld_hint": 1}, {"ld_hint": 2}, {"ld_hint": 3}, {"st_hint": 1},
                                    {"st_hint": 2}, {"st_hint": 3}, {"st_hint": 4}, {"tile_order": 1},
                                    {"tile_order": 2}, {"tile_order": 12}, {"tile_order": 23},
-                                   {"pdl_prefetch": 1}, {"pdl_prefetch": 2}, {"pdl_prefetch": 1, "smem_jit_tpg": 0}])
+                                   {"pdl_prefetch": 0}, {"pdl_prefetch": 2}, {"smem_jit_tpg": 0}])
 def test_convert_smem_kernel_hint_and_order_knobs(knobs):
     """The compiled smem kernel under the cache-hint ablation (ld_hint /
     st_hint change only the global instructions' qualifiers) and the tile
@@ -440,7 +440,7 @@ def test_convert_smem_kernel_hint_and_order_knobs(knobs):
             assert _np(dst, w).tobytes() == expect_convert(c, _np(src, w), batch).tobytes(), knobs
     finally:
         for k in knobs:
-            ll.tune(k, {"smem_jit_tpg": 1}.get(k, 0))
+            ll.tune(k, {"smem_jit_tpg": 1, "pdl_prefetch": 1}.get(k, 0))
 
 
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
