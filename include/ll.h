@@ -263,9 +263,8 @@ ll_status ll_convert_ex(const void* src, ll_layout src_layout, void* dst, ll_lay
                         int elem_bits, const ll_convert_options* opts, ll_stream stream);
 
 /* Same with gather options (path, batch).  Paths:
- *   LL_PATH_AUTO     measured on B200: the direct kernel when the
- *                    axis stays inside one warp's 16-byte vectors and lanes,
- *                    else the shared-memory gather where it applies, else direct
+ *   LL_PATH_AUTO     measured on B200: the shared-memory gather
+ *                    where it applies (the axis unit fits a CTA), else direct
  *   LL_PATH_SHUFFLE  warp-shuffle gather: the axis vectors L^{-1} e_axis lie in
  *                    one warp's registers and lanes (L_warp^axis =
  *                    L_block^axis = 0, in the coalesced mapping: within the low

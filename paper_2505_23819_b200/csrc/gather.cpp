@@ -115,12 +115,16 @@ std::shared_ptr<GatherPlanHost> build_gather_plan(const Layout& L, int axis, int
     P->paper_criterion = ok;
   }
   int path = path_req;
-  // AUTO (measured on B200): the direct (L1) gather when the
-  // unit is warp-local (config 4: 6464 vs 6297 smem, 6061 shuffle GB/s), the
-  // shared-memory gather for longer axes (full 4096 axis: 6080 vs 4662 direct)
-  if (path == LL_PATH_AUTO)
-    path = P->unit_bits <= vb + 5 || !P->smem_ok || !planner_knob("gather_auto_smem", 1) ? LL_PATH_GENERIC
-                                                                                      : LL_PATH_SMEM;
+  // AUTO (measured on B200): the shared-memory gather whenever
+  // the unit fits a CTA -- one-pass launches with PDL: config 4 6688 vs 6459
+  // direct / 6580 shuffle GB/s, the full 4096 axis 6551 vs 4750 direct
+  // (profiles/r02/s3g) -- else the direct (L1) gather.  Knob
+  // gather_auto_smem: 2 = the round-1 rule (direct for warp-local units),
+  // 0 = always direct.
+  if (path == LL_PATH_AUTO) {
+    const int ak = planner_knob("gather_auto_smem", 1);
+    path = !P->smem_ok || ak == 0 || (ak == 2 && P->unit_bits <= vb + 5) ? LL_PATH_GENERIC : LL_PATH_SMEM;
+  }
   if (path == LL_PATH_SHUFFLE && !P->shuffle_ok)
     throw Error(LL_ERR_UNSUPPORTED,
                 "gather: shuffle path needs the axis inside one warp's registers and lanes "
@@ -242,7 +246,7 @@ std::string gather_shfl_source(const GatherPlanHost& P, int timed) {
     if (P.acol[vb + c]) o << "  if (lane & " << (1 << c) << ") a_lane ^= " << P.acol[vb + c] << "u;\n";
   // programmatic dependent launch (knob gather_pdl): wait for the preceding
   // grid before the first global access, let the next one launch at once
-  if (!timed && planner_knob("gather_pdl", 0))
+  if (!timed && planner_knob("gather_pdl", 1))
     o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
       << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   o << "  for (long long t0 = gw * " << MU << "; t0 < n_units; t0 += tw * " << MU << ") {\n"
@@ -383,7 +387,7 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
        ":: \"r\"(st + " << UB << "u), \"l\"(idx + (t << " << CU << ")), \"r\"(" << IB << "u), \"r\"(bar) : \"memory\");\n"
     << "  };\n"
     << "  const long long g0 = blockIdx.x, gs = gridDim.x;\n";
-  if (!timed && planner_knob("gather_pdl", 0))   // programmatic dependent launch (knob gather_pdl)
+  if (!timed && planner_knob("gather_pdl", 1))   // programmatic dependent launch (knob gather_pdl)
     o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
       << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   o << "  if (tid == 0) { if (g0 < n_units) issue(g0, 0); if (g0 + gs < n_units) issue(g0 + gs, 1); }\n"
@@ -519,7 +523,7 @@ cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const in
   void* args[] = {(void*)&s, (void*)&ix, (void*)&d, (void*)&nu, (void*)&ef, (void*)&check,
                   (void*)&reps, (void*)&cycles};
   return jit_launch(fn, (unsigned)grid, 256, smem, st, args, err,
-                    !timed && planner_knob("gather_pdl", 0) != 0);
+                    !timed && planner_knob("gather_pdl", 1) != 0);
 }
 
 }  // namespace ll

@@ -84,6 +84,23 @@ std::string stg_asm(const std::string& vt, const std::string& regs) {
   }
 }
 
+// CTAs of a launch that can be resident at once (SMs x occupancy of fn):
+// the first wave, the only CTAs PDL can start during the preceding grid
+long long first_wave_ctas(CUfunction fn, int block, int smem, int sms) {
+  static PFN_Occupancy occ = entry<PFN_Occupancy>("cuOccupancyMaxActiveBlocksPerMultiprocessor");
+  static std::mutex occ_mu;
+  static std::map<std::pair<CUfunction, int>, int> occ_cache;
+  std::lock_guard<std::mutex> lk(occ_mu);
+  auto key = std::make_pair(fn, smem * 2048 + block);
+  auto it = occ_cache.find(key);
+  if (it == occ_cache.end()) {
+    int per_sm = 0;
+    if (!occ || occ(&per_sm, fn, block, (size_t)smem) != CUDA_SUCCESS) per_sm = 1;
+    it = occ_cache.emplace(key, std::max(1, per_sm)).first;
+  }
+  return (long long)it->second * sms;
+}
+
 // element-bit swap (a < b) of the thread's register file, compile-time
 // (same semantics as device_common.cuh apply_swap), emitted as source text
 void emit_swap(std::ostringstream& o, int W, int NW, int a, int b, const char* R) {
@@ -217,7 +234,7 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
     << "extern \"C\" __global__ void __launch_bounds__(256) ll_shfl_hbm(\n"
     << "    const __grid_constant__ TileMap tm, const unsigned char* __restrict__ src,\n"
     << "    unsigned char* __restrict__ dst, long long n_groups, long long t0, long long t1,\n"
-    << "    long long src_shift, long long dst_shift) {\n"
+    << "    long long src_shift, long long dst_shift, long long pf_ctas) {\n"
     << "  const int lane = threadIdx.x & 31;\n"
     << "  const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;\n"
     << "  if (gid >= n_groups) return;\n"
@@ -228,8 +245,26 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
       << "u; }\n";
   o << "  const unsigned char* sthr = src + ld_off - src_shift;\n"
     << "  unsigned char* dthr = dst + st_off - dst_shift;\n"
-    << "  const long long rmask = (1LL << tm.n_bits) - 1;\n"
-    << "  for (long long t = t0 + gid; t < t1; t += n_groups) {\n"
+    << "  const long long rmask = (1LL << tm.n_bits) - 1;\n";
+  // programmatic dependent launch (knob shuffle_pdl) with the first wave's
+  // L2 prefetch of its first tile (as the smem kernel, pdl_prefetch)
+  if (planner_knob("shuffle_pdl", 0)) {
+    if (planner_knob("pdl_prefetch", 1)) {
+      o << "  { const long long t = t0 + gid; if (t < t1 && blockIdx.x < pf_ctas) {\n"
+        << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
+        << "    long long so = inst * tm.bss;\n";
+      for (int k = 0; k < p.tile.n_tab; ++k)
+        o << "    so += tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
+          << ((1 << LL_TAB_BITS) - 1) << ")].src;\n";
+      for (int u = 0; u < NV; ++u)
+        o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
+          << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
+      o << "  } }\n";
+    }
+    o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
+      << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  }
+  o << "  for (long long t = t0 + gid; t < t1; t += n_groups) {\n"
     << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
     << "    long long so = inst * tm.bss, dof = inst * tm.bsd;\n";
   for (int k = 0; k < p.tile.n_tab; ++k)
@@ -881,13 +916,11 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   const void* s = src;
   void* d = dst;
+  const bool pdl = planner_knob("shuffle_pdl", 0) != 0;
+  long long pf = pdl && planner_knob("pdl_prefetch", 1) ? first_wave_ctas(fn, 256, 0, sms) : 0;
   void* args[] = {(void*)&P.shp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
-                  (void*)&ss, (void*)&ds};
-  if (launch(fn, (unsigned)grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) != CUDA_SUCCESS) {
-    *err = "cuLaunchKernel failed";
-    return cudaErrorLaunchFailure;
-  }
-  return cudaSuccess;  // launched by the driver API: no runtime error state to read
+                  (void*)&ss, (void*)&ds, (void*)&pf};
+  return jit_launch((void*)fn, (unsigned)grid, 256, 0, st, args, err, pdl);
 }
 
 // Register permutation (LL_PATH_REGPERM): thread c loads chunk c (2^rp_bits
@@ -911,8 +944,20 @@ std::string regperm_kernel_source(const ConvertPlan& P) {
   std::ostringstream o;
   o << "extern \"C\" __global__ void __launch_bounds__(256) ll_regperm(\n"
     << "    const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, long long t0,\n"
-    << "    long long t1, long long src_shift, long long dst_shift) {\n";
+    << "    long long t1, long long src_shift, long long dst_shift, long long pf_ctas) {\n";
   const bool pdl = planner_knob("pdl", 1) != 0;
+  // the first wave's L2 prefetch of its first chunks before the wait (knob
+  // pdl_prefetch, as the smem kernel): one prefetch per 128-byte line
+  if (pdl && planner_knob("pdl_prefetch", 1)) {
+    o << "  if (blockIdx.x < pf_ctas) {\n";
+    for (int u = 0; u < U; ++u)
+      for (int off = 0; off < CB; off += 128)
+        o << "    { const long long c = t0 + (long long)blockIdx.x * " << U << " * blockDim.x + threadIdx.x + "
+          << u << "LL * blockDim.x; const unsigned char* a_ = src + c * " << CB << " + " << off
+          << " - src_shift; if (c < t1 && (((unsigned long long)a_) & 127ull) == 0) "
+          << "asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
+    o << "  }\n";
+  }
   if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  for (long long c0 = t0 + (long long)blockIdx.x * " << U << " * blockDim.x + threadIdx.x; c0 < t1;\n"
     << "       c0 += (long long)gridDim.x * " << U << " * blockDim.x) {\n"
@@ -984,11 +1029,13 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
   long long t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   const void* s = src;
   void* d = dst;
-  void* args[] = {(void*)&s, (void*)&d, (void*)&t0, (void*)&t1, (void*)&ss, (void*)&ds};
   // knob regperm_occ: CTAs per SM (occupancy capped through dynamic shared
   // memory the kernel does not use; 0 = no cap)
   const int occ = planner_knob("regperm_occ", 0);
   unsigned smem = occ > 0 ? (unsigned)std::min(227 * 1024, 228 * 1024 / occ - 1024) : 0u;
+  long long pf = planner_knob("pdl", 1) && planner_knob("pdl_prefetch", 1)
+                     ? first_wave_ctas(fn, 256, (int)smem, sms) : 0;
+  void* args[] = {(void*)&s, (void*)&d, (void*)&t0, (void*)&t1, (void*)&ss, (void*)&ds, (void*)&pf};
   static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
   if (smem > 48 * 1024 && setattr) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   static PFN_LaunchEx launch_ex = entry<PFN_LaunchEx>("cuLaunchKernelEx");
@@ -1100,20 +1147,7 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
   if (smem > 48 * 1024) setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   // the first wave: CTAs that can be resident at once (pdl_prefetch)
-  long long pf = 0;
-  if (planner_knob("pdl_prefetch", 1)) {
-    static PFN_Occupancy occ = entry<PFN_Occupancy>("cuOccupancyMaxActiveBlocksPerMultiprocessor");
-    static std::mutex occ_mu;
-    static std::map<std::pair<CUfunction, int>, int> occ_cache;
-    std::lock_guard<std::mutex> lk(occ_mu);
-    auto it = occ_cache.find(std::make_pair(fn, smem));
-    if (it == occ_cache.end()) {
-      int per_sm = 0;
-      if (!occ || occ(&per_sm, fn, 256, (size_t)smem) != CUDA_SUCCESS) per_sm = 1;
-      it = occ_cache.emplace(std::make_pair(fn, smem), std::max(1, per_sm)).first;
-    }
-    pf = (long long)it->second * sms;
-  }
+  long long pf = planner_knob("pdl_prefetch", 1) ? first_wave_ctas(fn, 256, smem, sms) : 0;
   const void* s = src;
   void* d = dst;
   void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,

@@ -377,7 +377,7 @@ static cudaError_t launch_gather_t(const GatherPlan& p, bool shuffle, const void
     const bool v2 = knobs().gather_v8 && (p.nbits - ilog2(16 / W)) >= 1 &&
                     (reinterpret_cast<uintptr_t>(out) & 31) == 0;
     auto go = [&](auto kern, int g) {
-      if (planner_knob("gather_pdl", 0)) {
+      if (planner_knob("gather_pdl", 1)) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)g);
         cfg.blockDim = dim3(threads);

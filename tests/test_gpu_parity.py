@@ -443,6 +443,34 @@ def test_convert_smem_kernel_hint_and_order_knobs(knobs):
             ll.tune(k, {"smem_jit_tpg": 1, "pdl_prefetch": 1}.get(k, 0))
 
 
+@pytest.mark.parametrize("knobs", [{"shuffle_pdl": 1}, {"shuffle_pdl": 1, "pdl_prefetch": 0},
+                                   {"shuffle_pdl": 1, "pdl_prefetch": 2}])
+def test_convert_shuffle_kernel_pdl(knobs):
+    """The compiled HBM shuffle kernel launched with programmatic dependent
+    launch (griddepcontrol.wait first) and the first wave's L2 prefetch:
+    back-to-back launches where each reads what the previous one wrote
+    (src -> tmp -> back), byte-exact; configs 6 and 2 at small sizes."""
+    cases = [(configs.cfg6(n_bits=9, k_bits=9), 1), (configs.cfg2(batch_bits=2), 3)]
+    for k, v in knobs.items():
+        ll.tune(k, v)
+    try:
+        for c, batch in cases:
+            w = c["elem_bytes"]
+            A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+            src = values_torch((1 << A.in_bits) * batch, 71, w, "cuda")
+            mid = torch.zeros((1 << B.in_bits) * batch, dtype=src.dtype, device="cuda")
+            back = torch.zeros_like(src)
+            for _ in range(3):
+                ll.convert(src, A, mid, B, 8 * w, path="shuffle", batch=batch)
+                ll.convert(mid, B, back, A, 8 * w, path="shuffle", batch=batch)
+            torch.cuda.synchronize()
+            assert _np(mid, w).tobytes() == expect_convert(c, _np(src, w), batch).tobytes(), knobs
+            assert _np(back, w).tobytes() == _np(src, w).tobytes(), knobs
+    finally:
+        for k in knobs:
+            ll.tune(k, {"pdl_prefetch": 1}.get(k, 0))
+
+
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
 def test_convert_tma_each_swizzle_mode(swz):
     """Every hardware swizzle mode (the Def. 5 instances) executed on the

@@ -220,7 +220,7 @@ def test_gather_plan_config4():
     L = ll.Layout.from_spec(c["L"])
     d = ll.gather_describe(L, c["axis"], 32, "shuffle")
     assert d["path"] == "shuffle" and d["candidate_shuffles"] == 4      # reading A19: 2^|L_reg^axis|
-    assert ll.gather_describe(L, c["axis"], 32)["path"] == "direct"     # AUTO: measured fastest
+    assert ll.gather_describe(L, c["axis"], 32)["path"] == "smem"       # AUTO: measured fastest
     cf = configs.cfg4(variant="full")
     Lf = ll.Layout.from_spec(cf["L"])
     df = ll.gather_describe(Lf, cf["axis"], 32)
