@@ -246,9 +246,10 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
   o << "  const unsigned char* sthr = src + ld_off - src_shift;\n"
     << "  unsigned char* dthr = dst + st_off - dst_shift;\n"
     << "  const long long rmask = (1LL << tm.n_bits) - 1;\n";
-  // programmatic dependent launch (knob shuffle_pdl) with the first wave's
-  // L2 prefetch of its first tile (as the smem kernel, pdl_prefetch)
-  if (planner_knob("shuffle_pdl", 0)) {
+  // programmatic dependent launch (knob shuffle_pdl; config 6: 6601 -> 6793
+  // GB/s, profiles/r02/s3h) with the first wave's L2 prefetch of its first
+  // tile (as the smem kernel, pdl_prefetch)
+  if (planner_knob("shuffle_pdl", 1)) {
     if (planner_knob("pdl_prefetch", 1)) {
       o << "  { const long long t = t0 + gid; if (t < t1 && blockIdx.x < pf_ctas) {\n"
         << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
@@ -916,7 +917,7 @@ cudaError_t launch_shuffle_jit(const ConvertPlan& P, const void* src, void* dst,
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   const void* s = src;
   void* d = dst;
-  const bool pdl = planner_knob("shuffle_pdl", 0) != 0;
+  const bool pdl = planner_knob("shuffle_pdl", 1) != 0;
   long long pf = pdl && planner_knob("pdl_prefetch", 1) ? first_wave_ctas(fn, 256, 0, sms) : 0;
   void* args[] = {(void*)&P.shp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
                   (void*)&ss, (void*)&ds, (void*)&pf};
@@ -947,8 +948,10 @@ std::string regperm_kernel_source(const ConvertPlan& P) {
     << "    long long t1, long long src_shift, long long dst_shift, long long pf_ctas) {\n";
   const bool pdl = planner_knob("pdl", 1) != 0;
   // the first wave's L2 prefetch of its first chunks before the wait (knob
-  // pdl_prefetch, as the smem kernel): one prefetch per 128-byte line
-  if (pdl && planner_knob("pdl_prefetch", 1)) {
+  // regperm_prefetch, as the smem kernel's pdl_prefetch): one prefetch per
+  // 128-byte line.  Off by default: measured 0.8-1.2 % slower at every
+  // element width (profiles/r02/s3h/ab_regperm.jsonl)
+  if (pdl && planner_knob("regperm_prefetch", 0)) {
     o << "  if (blockIdx.x < pf_ctas) {\n";
     for (int u = 0; u < U; ++u)
       for (int off = 0; off < CB; off += 128)
@@ -1033,7 +1036,7 @@ cudaError_t launch_regperm_jit(const ConvertPlan& P, const void* src, void* dst,
   // memory the kernel does not use; 0 = no cap)
   const int occ = planner_knob("regperm_occ", 0);
   unsigned smem = occ > 0 ? (unsigned)std::min(227 * 1024, 228 * 1024 / occ - 1024) : 0u;
-  long long pf = planner_knob("pdl", 1) && planner_knob("pdl_prefetch", 1)
+  long long pf = planner_knob("pdl", 1) && planner_knob("regperm_prefetch", 0)
                      ? first_wave_ctas(fn, 256, (int)smem, sms) : 0;
   void* args[] = {(void*)&s, (void*)&d, (void*)&t0, (void*)&t1, (void*)&ss, (void*)&ds, (void*)&pf};
   static PFN_FuncSetAttribute setattr = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");

@@ -163,7 +163,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "auto_small_granule_shuffle" && name != "regperm_v8" && name != "regperm_waves" && name != "tmaj_tpc" && name != "tmaj_images" && name != "tmaj_v8" &&
       name != "gather_shfl_waves" && name != "gather_smem_upc" && name != "regperm_occ" &&
       name != "ld_hint" && name != "st_hint" && name != "pdl_prefetch" && name != "gather_pdl" &&
-      name != "shuffle_pdl")
+      name != "shuffle_pdl" && name != "regperm_prefetch")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;

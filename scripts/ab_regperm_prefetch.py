@@ -1,4 +1,4 @@
-"""Interleaved A/B of the first-wave PDL prefetch (knob pdl_prefetch) on the
+"""Interleaved A/B of the first-wave PDL prefetch (knob regperm_prefetch; pdl_prefetch before session 3's split) on the
 register-permutation kernel: register-only pairs of 2^26 elements at every
 element width (AUTO = regperm for them), median over rounds."""
 import importlib.util
@@ -31,10 +31,10 @@ def main():
         res = {}
         for _ in range(5):
             for pf in (1, 0):
-                ll.tune("pdl_prefetch", pf)
+                ll.tune("regperm_prefetch", pf)
                 ms = timeit(lambda i: ll.convert(sets[i % 2][0], A, sets[i % 2][1], B, 8 * w, path="regperm"))
-                res.setdefault("pdl_prefetch=%d" % pf, []).append(2 * n * w / (ms * 1e-3) / 1e9)
-        ll.tune("pdl_prefetch", 1)
+                res.setdefault("regperm_prefetch=%d" % pf, []).append(2 * n * w / (ms * 1e-3) / 1e9)
+        ll.tune("regperm_prefetch", 0)
         print(json.dumps({"elem_bytes": w, "reg_bits": r, "auto_path": ll.plan_describe(A, B, 8 * w)["path"],
                           "gbps_median": {k: round(statistics.median(v)) for k, v in res.items()},
                           "gbps_all": {k: [round(x) for x in v] for k, v in res.items()}}), flush=True)

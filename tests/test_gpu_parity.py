@@ -443,8 +443,24 @@ def test_convert_smem_kernel_hint_and_order_knobs(knobs):
             ll.tune(k, {"smem_jit_tpg": 1, "pdl_prefetch": 1}.get(k, 0))
 
 
-@pytest.mark.parametrize("knobs", [{"shuffle_pdl": 1}, {"shuffle_pdl": 1, "pdl_prefetch": 0},
-                                   {"shuffle_pdl": 1, "pdl_prefetch": 2}])
+@pytest.mark.parametrize("w", [1, 2, 4, 8])
+def test_convert_register_permutation_prefetch(w):
+    """The register-permutation kernel with the first wave's L2 prefetch
+    before griddepcontrol.wait (knob regperm_prefetch, off by default),
+    ragged batches, byte-exact."""
+    rng = random.Random(1600 + w)
+    ll.tune("regperm_prefetch", 1)
+    try:
+        for case in range(3):
+            c = perm_pair(rng, rng.randint(12, 15), w, 2 + case % 2, "reg")
+            batch = 1 + 2 * (case % 2)
+            src, dst = run_convert(c, path="regperm", seed=case + 30, batch=batch)
+            assert dst.tobytes() == expect_convert(c, src, batch).tobytes(), (w, case)
+    finally:
+        ll.tune("regperm_prefetch", 0)
+
+
+@pytest.mark.parametrize("knobs", [{}, {"shuffle_pdl": 0}, {"pdl_prefetch": 0}, {"pdl_prefetch": 2}])
 def test_convert_shuffle_kernel_pdl(knobs):
     """The compiled HBM shuffle kernel launched with programmatic dependent
     launch (griddepcontrol.wait first) and the first wave's L2 prefetch:
@@ -468,7 +484,7 @@ def test_convert_shuffle_kernel_pdl(knobs):
             assert _np(back, w).tobytes() == _np(src, w).tobytes(), knobs
     finally:
         for k in knobs:
-            ll.tune(k, {"pdl_prefetch": 1}.get(k, 0))
+            ll.tune(k, {"pdl_prefetch": 1, "shuffle_pdl": 1}.get(k, 0))
 
 
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
