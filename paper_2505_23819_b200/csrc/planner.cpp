@@ -163,7 +163,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "auto_small_granule_shuffle" && name != "regperm_v8" && name != "regperm_waves" && name != "tmaj_tpc" && name != "tmaj_images" && name != "tmaj_v8" &&
       name != "gather_shfl_waves" && name != "gather_smem_upc" && name != "regperm_occ" &&
       name != "ld_hint" && name != "st_hint" && name != "pdl_prefetch" && name != "gather_pdl" &&
-      name != "shuffle_pdl" && name != "regperm_prefetch")
+      name != "shuffle_pdl" && name != "regperm_prefetch" &&
+      name != "auto_regperm_shuffle")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;
@@ -919,10 +920,22 @@ std::shared_ptr<ConvertPlan> build_convert_plan(const Layout& A, const Layout& B
     // pairs (profiles/r02/s2f classify, s2q): smem ahead by 0.7-2.6 % there
     // (6464-6915 vs 6323-6819 GB/s), the register permutation ahead by 15-19 %
     // where the smem plan falls back to 4-byte granules; 2 = always
+    // With PDL on the compiled shuffle kernel (session 3) the warp-shuffle
+    // exchange ties or beats the register permutation wherever it applies
+    // (w <= 4: 6671 vs 6371 GB/s for 1-byte elements with 6 register bits,
+    // 6685-6847 vs 6684-6845 otherwise, profiles/r02/s3i/classify_rows.jsonl),
+    // so AUTO leaves those pairs to the small-granule shuffle rule below
+    // (knob auto_regperm_shuffle = 0: keep the register permutation)
     if (ok && path == LL_PATH_AUTO && planner_knob("auto_regperm", 1) == 1) {
       auto trial = std::make_shared<ConvertPlan>(*P);
       std::ostringstream js2;
       if (plan_smem(*trial, X, true, js2) && trial->g >= 8) ok = false;
+      if (ok && w <= 4 && planner_knob("auto_regperm_shuffle", 1) && planner_knob("shuffle_jit", 1) &&
+          planner_knob("auto_small_granule_shuffle", 1)) {
+        auto strial = std::make_shared<ConvertPlan>(*P);
+        std::ostringstream js3;
+        if (plan_smem(*strial, X, true, js3, true) && strial->shuffle_ok && strial->g <= 4) ok = false;
+      }
     }
     if (ok) {
       P->rp_bits = cb;

@@ -245,9 +245,10 @@ def perm_pair(rng, d, w, r, which):
 @pytest.mark.parametrize("w", [1, 2, 4, 8])
 def test_convert_register_permutation_pairs(w):
     """Pairs that differ only in register order: LL_PATH_REGPERM (no STS /
-    LDS, no shuffles) applies whenever the permuted chunk is <= 64 bytes, and
-    AUTO takes it unless the smem plan exchanges >= 8-byte granules (the
-    measured rule); both byte-exact, also batched and sharded."""
+    LDS, no shuffles) applies whenever the permuted chunk is <= 64 bytes;
+    AUTO takes the smem plan when it exchanges >= 8-byte granules, else the
+    warp-shuffle exchange where it applies (w <= 4), else the permutation
+    (the measured rule); all byte-exact, also batched and sharded."""
     vb = {1: 4, 2: 3, 4: 2, 8: 1}[w]
     rng = random.Random(1500 + w)
     took = 0
@@ -258,7 +259,12 @@ def test_convert_register_permutation_pairs(w):
         d = ll.plan_describe(A, B, 8 * w)
         if (w << max(r, vb)) <= 64:
             g = ll.plan_describe(A, B, 8 * w, "smem")["granule_bytes"]
-            assert d["path"] == ("smem" if g >= 8 else "regperm"), (r, g, d["path"])
+            try:
+                shfl = w <= 4 and ll.plan_describe(A, B, 8 * w, "shuffle")["granule_bytes"] <= 4
+            except ll.LLError:
+                shfl = False
+            want = "smem" if g >= 8 else ("shuffle" if shfl else "regperm")
+            assert d["path"] == want, (r, g, d["path"])
         batch = 1 + 2 * (case % 2)
         src, dst = run_convert(c, seed=case, batch=batch)
         assert dst.tobytes() == expect_convert(c, src, batch).tobytes()
