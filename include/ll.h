@@ -189,13 +189,13 @@ ll_status ll_gather(const void* src, const int32_t* idx, void* out, ll_layout la
 /* ------------------------------------------------------ extended control -- */
 
 typedef enum {
-  LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the identity, REGPERM when
-                            only the low <= 64 bytes of each chunk are permuted (and the smem
-                            plan's granule is < 8 bytes), else SMEM
+  LL_PATH_AUTO = 0,      /* planner's choice (cost model): COPY for the
+                            identity; SMEM when its plan exchanges >= 8-byte granules
                             (measured fastest once compiled per plan; broadcast layouts: the
-                            dedup plan where measured fast) -- SHUFFLE instead when the smem
-                            plan's granule is <= 4 bytes and the pair is warp-local --,
-                            else GENERIC                                              */
+                            dedup plan where measured fast); SHUFFLE when the smem plan's
+                            granule is <= 4 bytes and the pair is warp-local (elements of
+                            <= 4 bytes); else REGPERM when only the low <= 64 bytes of each
+                            chunk are permuted; else SMEM; else GENERIC             */
   LL_PATH_COPY = 1,      /* identity quotient: plain copy                          */
   LL_PATH_SMEM = 2,      /* tile through shared memory with the optimal swizzle; by default
                             in a kernel specialised for the plan at run time (NVRTC, every
