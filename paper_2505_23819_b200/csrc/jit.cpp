@@ -641,9 +641,16 @@ std::string upcast_hbm_source(const ConvertPlan& P) {
         << u << "; }\n";
     }
   };
+  // programmatic dependent launch (knob upcast_pdl): wait for the preceding
+  // grid before the first global access, let the next one launch once this
+  // CTA's first loads are issued
+  const bool pdl = planner_knob("upcast_pdl", 0) != 0;
+  if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  long long t = t0 + gid;\n  if (t < t1) { tile_off(t);\n";
   load("    ");
-  o << "  }\n  for (; t < t1; t += n_groups) {\n"
+  o << "  }\n";
+  if (pdl) o << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  o << "  for (; t < t1; t += n_groups) {\n"
     << "    const long long dcur = dof, scur = sct + sc_off;\n"
     << "    unsigned PKc[" << NV << "];\n";
   for (int u = 0; u < NV; ++u) o << "    PKc[" << u << "] = PK[" << u << "];\n";
@@ -1114,12 +1121,8 @@ cudaError_t launch_upcast_jit(const ConvertPlan& P, const void* src, void* dst,
   const void* sc = scales;
   void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
                   (void*)&ss, (void*)&ds, (void*)&sc};
-  if (launch(fn, (unsigned)grid, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr) !=
-      CUDA_SUCCESS) {
-    *err = "cuLaunchKernel failed";
-    return cudaErrorLaunchFailure;
-  }
-  return cudaSuccess;  // launched by the driver API: no runtime error state to read
+  return jit_launch((void*)fn, (unsigned)grid, 256, (unsigned)smem, st, args, err,
+                    planner_knob("upcast_pdl", 0) != 0);
 }
 
 cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, int max_ctas,
@@ -1151,6 +1154,10 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   // the first wave: CTAs that can be resident at once (pdl_prefetch)
   long long pf = planner_knob("pdl_prefetch", 1) ? first_wave_ctas(fn, 256, smem, sms) : 0;
+  // short launches (<= 2 waves, e.g. strong-scaling shards): every CTA
+  // prefetches (config 5's N = 8 shard: 6751 vs 6690 GB/s first wave only;
+  // longer launches lose with it, profiles/r02/s3f)
+  if (pf > 0 && grid <= 2 * pf && planner_knob("pdl_prefetch_short", 1)) pf = grid;
   const void* s = src;
   void* d = dst;
   void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,

@@ -1068,6 +1068,20 @@ def test_mxfp4_upcast_kernels(dist, jit):
         ll.tune("upcast_jit", 1)
 
 
+@pytest.mark.parametrize("pdl", [0, 1])
+def test_mxfp4_upcast_pdl_back_to_back(pdl):
+    """The compiled upcast with and without programmatic dependent launch
+    (knob upcast_pdl), three launches back to back on the same buffers, then
+    a conversion that reads the upcast's input after the last one: bit-exact
+    every time."""
+    ll.tune("upcast_pdl", pdl)
+    try:
+        for _ in range(3):
+            test_mxfp4_upcast(9, 8, "uniform")
+    finally:
+        ll.tune("upcast_pdl", 0)
+
+
 @pytest.mark.parametrize("dist", ["narrow", "uniform"])
 def test_mxfp4_upcast_full_size_whole_buffer(dist):
     """Config 5 at the BASELINE size (packed [32768, 16384] u8 -> 2 GiB of
