@@ -1071,9 +1071,9 @@ def test_mxfp4_upcast_kernels(dist, jit):
 @pytest.mark.parametrize("pdl", [0, 1])
 def test_mxfp4_upcast_pdl_back_to_back(pdl):
     """The compiled upcast with and without programmatic dependent launch
-    (knob upcast_pdl), three launches back to back on the same buffers, then
-    a conversion that reads the upcast's input after the last one: bit-exact
-    every time."""
+    (knob upcast_pdl), three rounds of input generation + upcast back to back
+    (each launch follows the kernels that wrote its inputs): bit-exact every
+    time."""
     ll.tune("upcast_pdl", pdl)
     try:
         for _ in range(3):
