@@ -1154,10 +1154,11 @@ cudaError_t launch_smem_jit(const ConvertPlan& P, const void* src, void* dst, in
   long long ng = groups, t0 = rg.t0, t1 = rg.t1, ss = rg.src_shift, ds = rg.dst_shift;
   // the first wave: CTAs that can be resident at once (pdl_prefetch)
   long long pf = planner_knob("pdl_prefetch", 1) ? first_wave_ctas(fn, 256, smem, sms) : 0;
-  // short launches (<= 2 waves, e.g. strong-scaling shards): every CTA
-  // prefetches (config 5's N = 8 shard: 6751 vs 6690 GB/s first wave only;
-  // longer launches lose with it, profiles/r02/s3f)
-  if (pf > 0 && grid <= 2 * pf && planner_knob("pdl_prefetch_short", 1)) pf = grid;
+  // knob pdl_prefetch_short: every CTA prefetches in launches of <= 2 waves
+  // (strong-scaling shards).  Off: config 5's N = 8 shard measured 6751 vs
+  // 6690 GB/s in one run (profiles/r02/s3f) and 6603 vs 6689 in the next
+  // (s3k) -- inside the run-to-run spread
+  if (pf > 0 && grid <= 2 * pf && planner_knob("pdl_prefetch_short", 0)) pf = grid;
   const void* s = src;
   void* d = dst;
   void* args[] = {(void*)&P.sp.tile, (void*)&s, (void*)&d, (void*)&ng, (void*)&t0, (void*)&t1,
