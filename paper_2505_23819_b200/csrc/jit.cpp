@@ -371,10 +371,23 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
     << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + group * "
     << (single ? 1 : 2) * p.tile_bytes << "u;\n"
     << "  unsigned buf = 0;\n  unsigned R[" << NW << "], Q[" << NW << "];\n"
-    << "  long long so = 0, dof = 0;\n"
-    << "  auto tile_off = [&](long long t) {\n"
-    << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
-    << "    so = inst * tm.bss; dof = inst * tm.bsd;\n";
+    << "  long long so = 0, dof = 0;\n";
+  // knob tile_xor = L (sweep): the tile -> CTA order XORs L bits of the tile
+  // index (from bit tile_xor_skip up) into its top L bits, so consecutive
+  // tiles of a column walk also hop across the outer dimension ("diagonal"
+  // order against DRAM channel camping of power-of-two strides).  A
+  // bijection on each instance's tiles; only for full-range launches (a
+  // shard's tile range is not closed under it).
+  const int txl = std::max(0, std::min(planner_knob("tile_xor", 0), p.tile.n_bits / 2));
+  const int txs = std::max(0, planner_knob("tile_xor_skip", 1));
+  const bool twist = txl > 0 && txs + txl <= p.tile.n_bits - txl;
+  if (twist) o << "  const bool twist = t0 == 0 && t1 == tm.n_tiles;\n";
+  o << "  auto tile_off = [&](long long t) {\n"
+    << "    const long long inst = t >> tm.n_bits;\n"
+    << "    long long r = t & rmask;\n";
+  if (twist)
+    o << "    if (twist) r ^= ((r >> " << txs << ") & " << ((1 << txl) - 1) << "LL) << " << p.tile.n_bits - txl << ";\n";
+  o << "    so = inst * tm.bss; dof = inst * tm.bsd;\n";
   for (int k = 0; k < p.tile.n_tab; ++k)
     o << "    { const TileTab& e = tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
       << ((1 << LL_TAB_BITS) - 1) << ")]; so += e.src; dof += e.dst; }\n";

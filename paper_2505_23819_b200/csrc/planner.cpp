@@ -164,7 +164,8 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "gather_shfl_waves" && name != "gather_smem_upc" && name != "regperm_occ" &&
       name != "ld_hint" && name != "st_hint" && name != "pdl_prefetch" && name != "gather_pdl" &&
       name != "shuffle_pdl" && name != "regperm_prefetch" &&
-      name != "auto_regperm_shuffle" && name != "pdl_prefetch_short" && name != "upcast_pdl")
+      name != "auto_regperm_shuffle" && name != "pdl_prefetch_short" && name != "upcast_pdl" &&
+      name != "tile_xor" && name != "tile_xor_skip")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;

@@ -424,7 +424,8 @@ def test_convert_tma_kernel_variants(path, knobs):
 @pytest.mark.parametrize("knobs", [{"ld_hint": 1}, {"ld_hint": 2}, {"ld_hint": 3}, {"st_hint": 1},
                                    {"st_hint": 2}, {"st_hint": 3}, {"st_hint": 4}, {"tile_order": 1},
                                    {"tile_order": 2}, {"tile_order": 12}, {"tile_order": 23},
-                                   {"pdl_prefetch": 0}, {"pdl_prefetch": 2}, {"smem_jit_tpg": 0}])
+                                   {"pdl_prefetch": 0}, {"pdl_prefetch": 2}, {"smem_jit_tpg": 0},
+                                   {"tile_xor": 2}, {"tile_xor": 6}, {"tile_xor": 4, "tile_xor_skip": 0}])
 def test_convert_smem_kernel_hint_and_order_knobs(knobs):
     """The compiled smem kernel under the cache-hint ablation (ld_hint /
     st_hint change only the global instructions' qualifiers) and the tile
