@@ -447,7 +447,30 @@ def test_convert_smem_kernel_hint_and_order_knobs(knobs):
             assert _np(dst, w).tobytes() == expect_convert(c, _np(src, w), batch).tobytes(), knobs
     finally:
         for k in knobs:
-            ll.tune(k, {"smem_jit_tpg": 1, "pdl_prefetch": 1}.get(k, 0))
+            ll.tune(k, {"smem_jit_tpg": 1, "pdl_prefetch": 1, "tile_xor_skip": 1}.get(k, 0))
+
+
+def test_convert_shard_with_tile_xor():
+    """The diagonal tile order (knob tile_xor) applies to full-range launches
+    only: sharded conversions (ll_convert_shard) stay inside their slices."""
+    c = configs.cfg3(n_bits=10, m_bits=10)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    w = c["elem_bytes"]
+    full = values_torch(1 << A.in_bits, 77, w, "cuda")
+    exp = expect_convert(c, _np(full, w))
+    ll.tune("tile_xor", 4)
+    try:
+        assert ll.plan_describe(A, B, 8 * w)["path"] == "smem"
+        parts = []
+        for r in range(4):
+            s0, s1, d0, d1 = ll.shard_describe(A, B, 8 * w, 4, r)
+            dl = torch.zeros(d1 - d0, dtype=torch.uint8, device="cuda")
+            ll.convert_shard(full.view(torch.uint8)[s0:s1].clone(), A, dl, B, 8 * w, 4, r)
+            torch.cuda.synchronize()
+            parts.append((d0, dl.cpu().numpy().tobytes()))
+        assert b"".join(b for _, b in sorted(parts)) == exp.tobytes()
+    finally:
+        ll.tune("tile_xor", 0)
 
 
 @pytest.mark.parametrize("w", [1, 2, 4, 8])
