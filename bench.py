@@ -67,6 +67,8 @@ def parse(argv=None):
                          "workload")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-scratch-mb", type=int, default=64,
+                    help="device staging per side for ll_convert_host (2 slots of its 32 MiB chunks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--also", default="2,3,4",
                     help="extra configs timed in the same run (N = 1; '' = none)")
@@ -918,14 +920,15 @@ def run_e2e(ll, b, args, dev, world, rank, scaling, barrier, coll_dev):
         shardable = True
     except ll.LLError:
         shardable = False
-    scratch = min(n * w, 32 << 20) if (nb > 1 or shardable) else n * w
+    scratch = min(n * w, args.e2e_scratch_mb << 20) if (nb > 1 or shardable) else n * w
     ds = torch.empty(scratch, dtype=torch.uint8, device=dev)
     dd = torch.empty(scratch, dtype=torch.uint8, device=dev)
     ms = timed(lambda: ll.convert_host(src_h, At, dst_h, Bt, 8 * w, nb, ds, dd, scratch,
                                        stream=stream))
     return {"value": world * b.nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": n * w, "d2h_bytes_per_step": n * w, "ms_per_step": ms,
-            "api": "ll_convert_host (pinned host buffers, 16 MiB chunks, copy-in/compute/copy-out streams)"}
+            "api": "ll_convert_host (pinned host buffers, %d MiB device staging per side, 32 MiB chunks, "
+                   "ramped first / last chunks, copy-in/compute/copy-out streams)" % (scratch >> 20)}
 
 
 def multigpu_max(x, coll_dev):

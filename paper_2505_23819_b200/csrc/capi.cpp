@@ -847,7 +847,7 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     const size_t sb = (size_t)w << src_layout->L.in_bits();
     const size_t db = (size_t)w << dst_layout->L.in_bits();
     const size_t unit = sb > db ? sb : db;
-    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 16)) << 20;
+    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 32)) << 20;
     const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 2)));
     // chunking: whole layout instances (batch elements), or -- for a single
     // large instance -- shards (contiguous slices of both buffers)
@@ -970,6 +970,35 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     cudaStreamWaitEvent(hp.h2d, hp.start, 0);
     cudaStreamWaitEvent(hp.comp, hp.start, 0);
     cudaStreamWaitEvent(hp.d2h, hp.start, 0);
+    // shard chunks: (n_shards, shard) per chunk.  Ramp (knob host_ramp = R
+    // levels): the first and the last shard are cut into pieces of 1/2^R ..
+    // 1/2 of a chunk, so the pipeline fills and drains on small copies (only
+    // one direction of the link is busy then) while the steady state keeps
+    // large chunks (per-chunk overhead ~20 us)
+    std::vector<std::pair<int, int>> sched;
+    if (n_sh > 1) {
+      int R = std::max(0, std::min(4, ll::planner_knob("host_ramp", 2)));
+      auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
+      while (R > 0 && n_sh >= 2) {
+        try {
+          ll::shard_range(*P, n_sh << R, 0);
+          break;
+        } catch (const ll::Error&) {
+          --R;
+        }
+      }
+      if (R > 0 && n_sh >= 2) {
+        const int fin = n_sh << R;
+        sched.push_back({fin, 0});
+        for (int L = R; L >= 1; --L) sched.push_back({n_sh << L, 1});
+        for (int k = 1; k + 1 < n_sh; ++k) sched.push_back({n_sh, k});
+        for (int L = 1; L <= R; ++L) sched.push_back({n_sh << L, (n_sh << L) - 2});
+        sched.push_back({fin, fin - 1});
+      } else {
+        for (int k = 0; k < n_sh; ++k) sched.push_back({n_sh, k});
+      }
+      n_chunks = (int64_t)sched.size();
+    }
     ll_status s = LL_OK;
     for (int64_t i = 0; i < n_chunks && s == LL_OK; ++i) {
       const int slot = (int)(i % nslot);
@@ -978,10 +1007,11 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
       size_t in_off, in_len, out_off, out_len;
       int64_t nb = 1;
       if (n_sh > 1) {
-        in_off = i * cs_src;
-        in_len = cs_src;
-        out_off = i * cs_dst;
-        out_len = cs_dst;
+        const int nsh = sched[i].first, idx = sched[i].second;
+        in_len = sb / nsh;
+        in_off = (size_t)idx * in_len;
+        out_len = db / nsh;
+        out_off = (size_t)idx * out_len;
       } else {
         const int64_t b0 = i * per_chunk;
         nb = std::min<int64_t>(per_chunk, batch - b0);
@@ -996,8 +1026,8 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
       cudaStreamWaitEvent(hp.comp, hp.ev_h2d[slot], 0);
       if (i >= nslot) cudaStreamWaitEvent(hp.comp, hp.ev_d2h[slot], 0);
       if (n_sh > 1) {
-        s = ll_convert_shard(ds, src_layout, dd, dst_layout, elem_bits, n_sh, (int)i, nullptr,
-                             (ll_stream)hp.comp);
+        s = ll_convert_shard(ds, src_layout, dd, dst_layout, elem_bits, sched[i].first, sched[i].second,
+                             nullptr, (ll_stream)hp.comp);
       } else {
         ll_convert_options o{};
         o.path = LL_PATH_AUTO;

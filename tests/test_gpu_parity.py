@@ -1172,8 +1172,11 @@ def test_checksum_full_size_conversion_properties():
     assert parts == r[2]
 
 
-def test_convert_host_sharded_single_instance():
-    """One large instance (8 MiB) chunked by shards through ll_convert_host."""
+@pytest.mark.parametrize("ramp,chunk_mb", [(2, 32), (0, 32), (2, 1), (4, 1), (3, 2)])
+def test_convert_host_sharded_single_instance(ramp, chunk_mb):
+    """One large instance (8 MiB) chunked by shards through ll_convert_host,
+    uniform chunks (host_ramp 0) or a ramped schedule whose first and last
+    chunks are cut into 1/2^R .. 1/2 pieces, 1-32 MiB chunks."""
     c = configs.cfg5(m_bits=12, kb_bits=11)
     A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
     n = 1 << A.in_bits
@@ -1182,7 +1185,13 @@ def test_convert_host_sharded_single_instance():
     scratch = 4 << 20
     ds = torch.empty(scratch, dtype=torch.uint8, device="cuda")
     dd = torch.empty(scratch, dtype=torch.uint8, device="cuda")
-    ll.convert_host(src_h, A, dst_h, B, 8, 1, ds, dd, scratch)
+    ll.tune("host_ramp", ramp)
+    ll.tune("host_chunk_mb", chunk_mb)
+    try:
+        ll.convert_host(src_h, A, dst_h, B, 8, 1, ds, dd, scratch)
+    finally:
+        ll.tune("host_ramp", 2)
+        ll.tune("host_chunk_mb", 32)
     exp = expect_convert(c, src_h.numpy())
     assert dst_h.numpy().tobytes() == exp.tobytes()
 
@@ -1204,7 +1213,7 @@ def test_convert_host_pitched_transpose(host_2d):
         ll.tune("host_2d", host_2d)
         ll.convert_host(src_h, A, dst_h, B, 16, 1, ds, dd, 2 * n)
     finally:
-        ll.tune("host_chunk_mb", 16)
+        ll.tune("host_chunk_mb", 32)
         ll.tune("host_2d", 1)
     exp = expect_convert(c, _np(src_h, 2))
     assert _np(dst_h, 2).tobytes() == exp.tobytes()
