@@ -421,8 +421,8 @@ ll_status ll_checksum(const void* buf, int64_t n_elems, int elem_bits, int index
  * device scratch buffers dev_src/dev_dst of scratch_bytes each (>= one
  * chunk).  Ordered after work already queued on `stream`; synchronous:
  * returns when dst_host is complete.  Knobs (ll_tune): "host_chunk_mb",
- * "host_slots", "host_2d" (1: pitched shards allowed), "host_ramp" (2: the
- * first and last shard chunks cut into 1/4 and 1/2 pieces). */
+ * "host_slots", "host_2d" (1: pitched shards allowed), "host_ramp" (0; R > 0:
+ * the first and last shard chunks cut into 1/2^R .. 1/2 pieces). */
 ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_host,
                           ll_layout dst_layout, int elem_bits, int64_t batch, void* dev_src,
                           void* dev_dst, size_t scratch_bytes, ll_stream stream);
@@ -477,7 +477,7 @@ int64_t ll_launch_count(void);
  * Register-faithful paths: "regs_matrix" (1) stmatrix / ldmatrix allowed,
  *   "regs_trans" (1) their .trans forms, "regs_shuffle_max_rounds" (4)
  * ll_convert_host: "host_chunk_mb" (default 32; ll_gather_host 16), "host_slots"
- *   (default 2), "host_ramp" (default 2).
+ *   (default 2), "host_ramp" (default 0).
  * LL_ERR_ARG for an unknown name.  Used by the tuning sweeps. */
 ll_status ll_tune(const char* name, int value);
 

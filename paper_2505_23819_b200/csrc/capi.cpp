@@ -971,13 +971,13 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     cudaStreamWaitEvent(hp.comp, hp.start, 0);
     cudaStreamWaitEvent(hp.d2h, hp.start, 0);
     // shard chunks: (n_shards, shard) per chunk.  Ramp (knob host_ramp = R
-    // levels): the first and the last shard are cut into pieces of 1/2^R ..
-    // 1/2 of a chunk, so the pipeline fills and drains on small copies (only
-    // one direction of the link is busy then) while the steady state keeps
-    // large chunks (per-chunk overhead ~20 us)
+    // levels, default 0): the first and the last shard cut into pieces of
+    // 1/2^R .. 1/2 of a chunk, so the pipeline would fill and drain on small
+    // copies -- measured no faster on config 5 (92.6 vs 92.8 GB/s,
+    // profiles/r02/s3o), kept as a knob
     std::vector<std::pair<int, int>> sched;
     if (n_sh > 1) {
-      int R = std::max(0, std::min(4, ll::planner_knob("host_ramp", 2)));
+      int R = std::max(0, std::min(4, ll::planner_knob("host_ramp", 0)));
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
       while (R > 0 && n_sh >= 2) {
         try {

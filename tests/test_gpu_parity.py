@@ -1190,7 +1190,7 @@ def test_convert_host_sharded_single_instance(ramp, chunk_mb):
     try:
         ll.convert_host(src_h, A, dst_h, B, 8, 1, ds, dd, scratch)
     finally:
-        ll.tune("host_ramp", 2)
+        ll.tune("host_ramp", 0)
         ll.tune("host_chunk_mb", 32)
     exp = expect_convert(c, src_h.numpy())
     assert dst_h.numpy().tobytes() == exp.tobytes()
