@@ -69,6 +69,19 @@ def main():
     for kind in ("both", "st_vec", "ld_vec"):
         ok &= conv(dict(b8_pair(random.Random(6), kind, nr=4, nw=1), name="b8_" + kind), "regs")
     ok &= conv(dict(_bcast_pair(random.Random(7), 13, 2, 0, 2), name="bcast"), "smem")
+    # session 3: PDL prologue prefetch in every CTA, the diagonal tile order,
+    # the register permutation's prefetch, the direct gather (AUTO is the
+    # smem gather now), the upcast with PDL (defaults cover the first-wave
+    # prefetch and the shuffle / gather PDL)
+    ll.tune("pdl_prefetch", 2)
+    ok &= conv(configs.cfg3(n_bits=8), "smem")
+    ll.tune("pdl_prefetch", 1)
+    ll.tune("tile_xor", 3)
+    ok &= conv(configs.cfg3(n_bits=8), "smem")
+    ll.tune("tile_xor", 0)
+    ll.tune("regperm_prefetch", 1)
+    ok &= conv(dict(perm_pair(random.Random(5), 14, 2, 4, "reg"), name="regperm_pf"), "regperm")
+    ll.tune("regperm_prefetch", 0)
     # the template smem kernel (the default compiles the plan)
     ll.tune("smem_jit", 0)
     ok &= conv(configs.cfg3(n_bits=8), "smem")
@@ -76,7 +89,7 @@ def main():
     g = configs.cfg4(r_bits=3)
     L = ll.Layout.from_spec(g["L"])
     m = 1 << L.in_bits
-    for path in ("shuffle", "smem", "auto"):
+    for path in ("shuffle", "smem", "auto", "generic"):
         gs = values_torch(m, 4, 4, "cuda")
         gi = indices_torch(m, 5, 32, "cuda")
         go = torch.empty_like(gs)
@@ -93,13 +106,16 @@ def main():
     n = 1 << A.in_bits
     packed = values_torch(n, 9, 1, "cuda")
     sc = (indices_torch((1 << 8) * (1 << 3), 10, 16, "cuda") + 120).to(torch.uint8)
-    out = torch.empty(2 * n, dtype=torch.int16, device="cuda")
-    ll.mxfp4_upcast(packed, A, sc, out, B)
-    torch.cuda.synchronize()
     exp = omx.upcast_np(packed.cpu().numpy(), OL(**c["A"]), sc.cpu().numpy(), OL(**c["B"]))
-    good = out.cpu().numpy().view(np.uint16).tobytes() == exp.tobytes()
-    print("%-10s %-16s %s" % ("cfg5", "mxfp4_upcast", "ok" if good else "MISMATCH"), flush=True)
-    ok &= good
+    for pdl in (0, 1):
+        ll.tune("upcast_pdl", pdl)
+        out = torch.empty(2 * n, dtype=torch.int16, device="cuda")
+        ll.mxfp4_upcast(packed, A, sc, out, B)
+        torch.cuda.synchronize()
+        good = out.cpu().numpy().view(np.uint16).tobytes() == exp.tobytes()
+        print("%-10s %-16s %s" % ("cfg5", "mxfp4_upcast" + " pdl" * pdl, "ok" if good else "MISMATCH"), flush=True)
+        ok &= good
+    ll.tune("upcast_pdl", 0)
     print("ALL OK" if ok else "FAILURES")
     sys.exit(0 if ok else 1)
 
