@@ -474,6 +474,15 @@ int64_t ll_launch_count(void);
  * TMA paths: "tma_tpg" (-1 = by wave count), "tma_stages" (3),
  *   "tma_run_bytes" (256), "tma_thread_bytes" (64), "tma_tile_bytes" (8192),
  *   "tma_force_swizzle" (-1)
+ * Session-3 knobs: "pdl_prefetch" (1: the first wave of the
+ *   compiled smem kernel prefetches its first tile's source into L2 before
+ *   griddepcontrol.wait; 2: every CTA; 0: off), "pdl_prefetch_short" (0),
+ *   "shuffle_pdl" (1) / "gather_pdl" (1) / "upcast_pdl" (0) programmatic
+ *   dependent launch of those kernels, "regperm_prefetch" (0),
+ *   "auto_regperm_shuffle" (1: AUTO takes the warp-shuffle exchange over the
+ *   register permutation where it applies), "ld_hint" / "st_hint" (0: global
+ *   cache-qualifier ablation), "tile_xor" (0) / "tile_xor_skip" (1) diagonal
+ *   tile order, "gather_auto_smem" (1: AUTO smem gather wherever it fits)
  * Register-faithful paths: "regs_matrix" (1) stmatrix / ldmatrix allowed,
  *   "regs_trans" (1) their .trans forms, "regs_shuffle_max_rounds" (4)
  * ll_convert_host: "host_chunk_mb" (default 32; ll_gather_host 16), "host_slots"
