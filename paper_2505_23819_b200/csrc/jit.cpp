@@ -551,12 +551,18 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
   // preceding grid writes: L2 is the device's point of coherence (its writes
   // land in the same lines), and nothing enters L1 before the wait.
   if (pdl && P.ld_span == 0 && !noload && planner_knob("pdl_prefetch", 1)) {
-    o << "  { const long long tp = t0 + gid; if (tp < t1"
-      << (planner_knob("pdl_prefetch", 1) == 2 ? "" : " && blockIdx.x < pf_ctas") << ") { tile_off(tp);\n";
-    for (int u = 0; u < NV; ++u)
-      o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
-        << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
-    o << "  } }\n";
+    // knob pdl_prefetch_waves = K: a first-wave CTA also prefetches the first
+    // tiles of the CTAs that replace it in waves 2..K (one-pass launches:
+    // tile + k * pf_ctas * groups per CTA)
+    const int pfk = std::max(1, std::min(4, planner_knob("pdl_prefetch_waves", 1)));
+    for (int k = 0; k < pfk; ++k) {
+      o << "  { const long long tp = t0 + gid + " << k << "LL * pf_ctas * " << (8 >> gw) << "; if (tp < t1"
+        << (planner_knob("pdl_prefetch", 1) == 2 ? "" : " && blockIdx.x < pf_ctas") << ") { tile_off(tp);\n";
+      for (int u = 0; u < NV; ++u)
+        o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
+          << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
+      o << "  } }\n";
+    }
   }
   if (pdl) o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  long long t = t0 + gid;\n";
