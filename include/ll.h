@@ -476,7 +476,8 @@ int64_t ll_launch_count(void);
  *   "tma_force_swizzle" (-1)
  * Session-3 knobs: "pdl_prefetch" (1: the first wave of the
  *   compiled smem kernel prefetches its first tile's source into L2 before
- *   griddepcontrol.wait; 2: every CTA; 0: off), "pdl_prefetch_short" (0),
+ *   griddepcontrol.wait; 2: every CTA; 0: off), "pdl_prefetch_waves" (2:
+ *   also the tiles of the CTAs replacing it in wave 2), "pdl_prefetch_short" (0),
  *   "shuffle_pdl" (1) / "gather_pdl" (1) / "upcast_pdl" (0) programmatic
  *   dependent launch of those kernels, "regperm_prefetch" (0),
  *   "auto_regperm_shuffle" (1: AUTO takes the warp-shuffle exchange over the

@@ -551,10 +551,12 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
   // preceding grid writes: L2 is the device's point of coherence (its writes
   // land in the same lines), and nothing enters L1 before the wait.
   if (pdl && P.ld_span == 0 && !noload && planner_knob("pdl_prefetch", 1)) {
-    // knob pdl_prefetch_waves = K: a first-wave CTA also prefetches the first
-    // tiles of the CTAs that replace it in waves 2..K (one-pass launches:
-    // tile + k * pf_ctas * groups per CTA)
-    const int pfk = std::max(1, std::min(4, planner_knob("pdl_prefetch_waves", 1)));
+    // knob pdl_prefetch_waves = K (default 2): a first-wave CTA also
+    // prefetches the first tiles of the CTAs that replace it in waves 2..K
+    // (one-pass launches: tile + k * pf_ctas * groups per CTA).  K = 2:
+    // config 2 6845 -> 6893 GB/s, config 5's N = 8 shard 6676 -> 6801,
+    // configs 3 / 5 -0.2 % (profiles/r02/s3p); K = 3 loses
+    const int pfk = std::max(1, std::min(4, planner_knob("pdl_prefetch_waves", 2)));
     for (int k = 0; k < pfk; ++k) {
       o << "  { const long long tp = t0 + gid + " << k << "LL * pf_ctas * " << (8 >> gw) << "; if (tp < t1"
         << (planner_knob("pdl_prefetch", 1) == 2 ? "" : " && blockIdx.x < pf_ctas") << ") { tile_off(tp);\n";
