@@ -427,6 +427,19 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
                           ll_layout dst_layout, int elem_bits, int64_t batch, void* dev_src,
                           void* dev_dst, size_t scratch_bytes, ll_stream stream);
 
+/* End-to-end conversion of ONE RANK'S SHARD from host buffers (SURVEY 8(e):
+ * the multi-GPU path with its host copies): src_host holds this shard's
+ * source slice and dst_host receives its destination slice -- the byte
+ * ranges ll_shard_describe(n_shards, shard) reports, as contiguous host
+ * buffers (pinned for full speed).  The slice is cut into k sub-shards
+ * (shards n_shards*k, shard*k .. shard*k+k-1; chunks of ~host_chunk_mb)
+ * pipelined like ll_convert_host through the caller's device scratch
+ * dev_src / dev_dst of scratch_bytes each (>= one chunk).  LL_ERR_UNSUPPORTED
+ * when the plan is not shardable; synchronous. */
+ll_status ll_convert_host_shard(const void* src_host, ll_layout src_layout, void* dst_host,
+                                ll_layout dst_layout, int elem_bits, int n_shards, int shard,
+                                void* dev_src, void* dev_dst, size_t scratch_bytes, ll_stream stream);
+
 /* JSON description of the plan the planner builds for (src, dst, elem_bits)
  * with the given path request: path, tile bits, thread mapping, granule,
  * swizzle bases, predicted wavefronts, shuffle sets.  Writes at most cap bytes

@@ -10,13 +10,13 @@ PyTorch fallback: if the shared library is missing the import fails loudly.
     ll.convert(src, A, dst, B, elem_bits=16)      # device tensors (torch)
 """
 
-from ._lib import (LLError, Layout, broadcast, checksum, compose, convert, convert_host, convert_regs_timed,
+from ._lib import (LLError, Layout, broadcast, checksum, compose, convert, convert_host, convert_host_shard, convert_regs_timed,
                    convert_shard, jit_source, left_divide,
                    expand_dims, join, mxfp4_upcast, reshape, shard_describe, shard_describe_2d, gather_host, split, transpose, gather, gather_describe,
                    invert, launch_count, lib_path, plan_describe, product, tune, version, PATHS,
                    gather_jit_source, gather_timed, slice_layout, blocked, mma_tile)
 
-__all__ = ["LLError", "Layout", "broadcast", "checksum", "compose", "convert", "convert_host",
+__all__ = ["LLError", "Layout", "broadcast", "checksum", "compose", "convert", "convert_host", "convert_host_shard",
            "convert_regs_timed", "convert_shard", "jit_source", "left_divide",
            "expand_dims", "join", "mxfp4_upcast", "reshape", "split", "transpose",
            "shard_describe", "shard_describe_2d", "gather_host", "gather", "gather_describe",

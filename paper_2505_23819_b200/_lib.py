@@ -51,6 +51,9 @@ _lib.ll_gather_ex.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
 _lib.ll_convert_host.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
                                  ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+_lib.ll_convert_host_shard.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
 _lib.ll_plan_describe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_char_p, ctypes.c_size_t,
                                   ctypes.POINTER(ctypes.c_size_t)]
@@ -96,7 +99,7 @@ _lib.ll_gather_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int,
 for _f in ("ll_slice", "ll_blocked", "ll_mma_tile", "ll_gather_jit_source", "ll_gather_timed", "ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_shard_describe_2d", "ll_gather_host", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
-           "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_plan_describe",
+           "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_convert_host_shard", "ll_plan_describe",
            "ll_gather_describe"):
     getattr(_lib, _f).restype = ctypes.c_int
 
@@ -483,6 +486,14 @@ def convert_host(src_host, A, dst_host, B, elem_bits, batch, dev_src, dev_dst, s
     _check(_lib.ll_convert_host(_ptr(src_host), A.handle, _ptr(dst_host), B.handle,
                                 int(elem_bits), int(batch), _ptr(dev_src), _ptr(dev_dst),
                                 int(scratch_bytes), _stream_handle(stream)))
+
+
+def convert_host_shard(src_host, A, dst_host, B, elem_bits, n_shards, shard, dev_src, dev_dst,
+                       scratch_bytes, stream=None):
+    """ll_convert_host_shard: one rank's shard from host slices (pipelined)."""
+    _check(_lib.ll_convert_host_shard(_ptr(src_host), A.handle, _ptr(dst_host), B.handle,
+                                      int(elem_bits), int(n_shards), int(shard), _ptr(dev_src),
+                                      _ptr(dev_dst), int(scratch_bytes), _stream_handle(stream)))
 
 
 def _describe(fn, *args):

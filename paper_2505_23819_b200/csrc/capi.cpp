@@ -1051,6 +1051,81 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
   });
 }
 
+ll_status ll_convert_host_shard(const void* src_host, ll_layout src_layout, void* dst_host,
+                                ll_layout dst_layout, int elem_bits, int n_shards, int shard,
+                                void* dev_src, void* dev_dst, size_t scratch_bytes, ll_stream stream) {
+  return guarded([&]() -> ll_status {
+    check_layout(src_layout, "ll_convert_host_shard");
+    check_layout(dst_layout, "ll_convert_host_shard");
+    const int w = elem_bytes(elem_bits);
+    if (!src_host || !dst_host || !dev_src || !dev_dst)
+      return fail(LL_ERR_ARG, "ll_convert_host_shard: NULL buffer");
+    if (n_shards < 1 || (n_shards & (n_shards - 1)) || shard < 0 || shard >= n_shards)
+      return fail(LL_ERR_ARG, "ll_convert_host_shard: n_shards must be a power of two, 0 <= shard < n_shards");
+    auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
+    ll::shard_range(*P, n_shards, shard);   // throws if not shardable
+    const size_t sb = (size_t)w << src_layout->L.in_bits(), db = (size_t)w << dst_layout->L.in_bits();
+    const size_t slice = std::max(sb, db) / (size_t)n_shards;
+    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 32)) << 20;
+    const size_t cap = std::max<size_t>(1, std::min(target, scratch_bytes));
+    // k sub-shards per shard: the smallest power of two whose chunks fit
+    int k = 1;
+    while (slice / k > cap && k < (1 << 12)) k *= 2;
+    while (k > 1) {
+      try {
+        ll::shard_range(*P, n_shards * k, shard * k);
+        break;
+      } catch (const ll::Error&) {
+        k /= 2;
+      }
+    }
+    const size_t cs = slice / k;
+    if (scratch_bytes < cs) return fail(LL_ERR_ARG, "ll_convert_host_shard: scratch smaller than one chunk");
+    const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 2)));
+    const int nslot = (int)std::max<size_t>(1, std::min<size_t>(max_slots, scratch_bytes / cs));
+    const size_t in_len = sb / ((size_t)n_shards * k), out_len = db / ((size_t)n_shards * k);
+    // the sub-shards must tile the shard's slices in order on both sides
+    for (int j = 0; j < k; ++j) {
+      const ll::TileRange rg = ll::shard_range(*P, n_shards * k, shard * k + j);
+      const int64_t q = (int64_t)shard * k + j;
+      if (rg.src_shift != q * (int64_t)in_len || rg.dst_shift != q * (int64_t)out_len)
+        return fail(LL_ERR_UNSUPPORTED, "ll_convert_host_shard: sub-shards are not contiguous in order");
+    }
+    // the pipeline of ll_convert_host over this shard's k sub-shards
+    HostPipe& hp = host_pipe();
+    std::lock_guard<std::mutex> lk(hp.mu);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaEventRecord(hp.start, st);
+    cudaStreamWaitEvent(hp.h2d, hp.start, 0);
+    cudaStreamWaitEvent(hp.comp, hp.start, 0);
+    cudaStreamWaitEvent(hp.d2h, hp.start, 0);
+    ll_status s = LL_OK;
+    for (int j = 0; j < k && s == LL_OK; ++j) {
+      const int slot = j % nslot;
+      char* ds = (char*)dev_src + (size_t)slot * cs;
+      char* dd = (char*)dev_dst + (size_t)slot * cs;
+      if (j >= nslot) cudaStreamWaitEvent(hp.h2d, hp.ev_comp[slot], 0);
+      cudaMemcpyAsync(ds, (const char*)src_host + (size_t)j * in_len, in_len, cudaMemcpyHostToDevice, hp.h2d);
+      cudaEventRecord(hp.ev_h2d[slot], hp.h2d);
+      cudaStreamWaitEvent(hp.comp, hp.ev_h2d[slot], 0);
+      if (j >= nslot) cudaStreamWaitEvent(hp.comp, hp.ev_d2h[slot], 0);
+      s = ll_convert_shard(ds, src_layout, dd, dst_layout, elem_bits, n_shards * k, shard * k + j, nullptr,
+                           (ll_stream)hp.comp);
+      cudaEventRecord(hp.ev_comp[slot], hp.comp);
+      cudaStreamWaitEvent(hp.d2h, hp.ev_comp[slot], 0);
+      cudaMemcpyAsync((char*)dst_host + (size_t)j * out_len, dd, out_len, cudaMemcpyDeviceToHost, hp.d2h);
+      cudaEventRecord(hp.ev_d2h[slot], hp.d2h);
+    }
+    cudaEventRecord(hp.fin[0], hp.h2d);
+    cudaEventRecord(hp.fin[1], hp.comp);
+    cudaEventRecord(hp.fin[2], hp.d2h);
+    for (int q = 0; q < 3; ++q) cudaStreamWaitEvent(st, hp.fin[q], 0);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (s != LL_OK) return s;
+    return cuda_status(e, "ll_convert_host_shard");
+  });
+}
+
 ll_status ll_gather_host(const void* src_host, const int32_t* idx_host, void* out_host,
                          ll_layout layout, int axis, int elem_bits, int64_t batch, void* dev_src,
                          void* dev_idx, void* dev_out, size_t scratch_bytes, ll_stream stream) {

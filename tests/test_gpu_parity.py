@@ -1197,6 +1197,33 @@ def test_convert_host_sharded_single_instance(ramp, chunk_mb):
     assert dst_h.numpy().tobytes() == exp.tobytes()
 
 
+@pytest.mark.parametrize("n_shards,chunk_mb", [(2, 1), (4, 32), (8, 1)])
+def test_convert_host_shard(n_shards, chunk_mb):
+    """ll_convert_host_shard: every rank's shard from its host slices, cut
+    into sub-shards and pipelined; the slices reassemble to the oracle's
+    whole destination (config 5 family, 8 MiB)."""
+    c = configs.cfg5(m_bits=12, kb_bits=11)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src = values_torch(n, 29, 1, "cpu")
+    exp = expect_convert(c, src.numpy())
+    scratch = 2 << 20
+    ds = torch.empty(scratch, dtype=torch.uint8, device="cuda")
+    dd = torch.empty(scratch, dtype=torch.uint8, device="cuda")
+    ll.tune("host_chunk_mb", chunk_mb)
+    try:
+        parts = []
+        for r in range(n_shards):
+            s0, s1, d0, d1 = ll.shard_describe(A, B, 8, n_shards, r)
+            src_h = src[s0:s1].clone().pin_memory()
+            dst_h = torch.zeros(d1 - d0, dtype=torch.uint8).pin_memory()
+            ll.convert_host_shard(src_h, A, dst_h, B, 8, n_shards, r, ds, dd, scratch)
+            parts.append((d0, dst_h.numpy().tobytes()))
+    finally:
+        ll.tune("host_chunk_mb", 32)
+    assert b"".join(b for _, b in sorted(parts)) == exp.tobytes()
+
+
 @pytest.mark.parametrize("host_2d", [1, 0])
 def test_convert_host_pitched_transpose(host_2d):
     """A single 8 MiB transpose through ll_convert_host with 1 MiB chunks:
