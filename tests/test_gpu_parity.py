@@ -454,7 +454,7 @@ def test_convert_smem_kernel_hint_and_order_knobs(knobs):
 def test_convert_shard_with_tile_xor():
     """The diagonal tile order (knob tile_xor) applies to full-range launches
     only: sharded conversions (ll_convert_shard) stay inside their slices."""
-    c = configs.cfg3(n_bits=10, m_bits=10)
+    c = configs.cfg5(m_bits=11, kb_bits=10)   # shardable (config 3 is not: a transpose)
     A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
     w = c["elem_bytes"]
     full = values_torch(1 << A.in_bits, 77, w, "cuda")
