@@ -351,6 +351,21 @@ def _dev_arg(t, name, need_bytes, elem_bits=None):
         raise LLError(1, "%s: %d bytes < %d needed" % (name, have, need_bytes))
 
 
+def _host_arg(t, name, need_bytes):
+    """Argument checks for a host buffer (torch CPU tensor; pinned for full
+    speed): on the host, contiguous, at least need_bytes bytes.  Raw integer
+    pointers are passed through unchecked."""
+    if not hasattr(t, "data_ptr"):
+        return
+    if getattr(t, "is_cuda", False):
+        raise LLError(1, "%s: expected a host (CPU) tensor" % name)
+    if not t.is_contiguous():
+        raise LLError(1, "%s: tensor is not contiguous" % name)
+    have = t.numel() * t.element_size()
+    if have < need_bytes:
+        raise LLError(1, "%s: %d bytes < %d needed" % (name, have, need_bytes))
+
+
 def _stream_for(stream, *tensors):
     """The given stream, else the current stream of the first tensor's device."""
     if stream is None:
@@ -456,6 +471,12 @@ def shard_describe(A, B, elem_bits, n_shards, shard, path="auto"):
 def gather_host(src_host, idx_host, out_host, L, axis, elem_bits, batch, dev_src, dev_idx,
                 dev_out, scratch_bytes, stream=None):
     """ll_gather_host: host buffers in, host buffer out (pipelined copies)."""
+    wb, n = int(elem_bits) // 8, (1 << L.in_bits) * int(batch)
+    _host_arg(src_host, "gather_host src_host", wb * n)
+    _host_arg(idx_host, "gather_host idx_host", 4 * n)
+    _host_arg(out_host, "gather_host out_host", wb * n)
+    for t, nm in ((dev_src, "dev_src"), (dev_idx, "dev_idx"), (dev_out, "dev_out")):
+        _dev_arg(t, "gather_host " + nm, int(scratch_bytes))
     _check(_lib.ll_gather_host(_ptr(src_host), _ptr(idx_host), _ptr(out_host), L.handle, int(axis),
                                int(elem_bits), int(batch), _ptr(dev_src), _ptr(dev_idx),
                                _ptr(dev_out), int(scratch_bytes), _stream_handle(stream)))
@@ -483,6 +504,11 @@ def gather(src, idx, out, L, axis, elem_bits, path="auto", batch=1, max_ctas=0, 
 def convert_host(src_host, A, dst_host, B, elem_bits, batch, dev_src, dev_dst, scratch_bytes,
                  stream=None):
     """ll_convert_host: host buffers in, host buffers out (pipelined copies)."""
+    wb, nb = int(elem_bits) // 8, max(1, int(batch))
+    _host_arg(src_host, "convert_host src_host", (wb << A.in_bits) * nb)
+    _host_arg(dst_host, "convert_host dst_host", (wb << B.in_bits) * nb)
+    _dev_arg(dev_src, "convert_host dev_src", int(scratch_bytes))
+    _dev_arg(dev_dst, "convert_host dev_dst", int(scratch_bytes))
     _check(_lib.ll_convert_host(_ptr(src_host), A.handle, _ptr(dst_host), B.handle,
                                 int(elem_bits), int(batch), _ptr(dev_src), _ptr(dev_dst),
                                 int(scratch_bytes), _stream_handle(stream)))
@@ -491,6 +517,11 @@ def convert_host(src_host, A, dst_host, B, elem_bits, batch, dev_src, dev_dst, s
 def convert_host_shard(src_host, A, dst_host, B, elem_bits, n_shards, shard, dev_src, dev_dst,
                        scratch_bytes, stream=None):
     """ll_convert_host_shard: one rank's shard from host slices (pipelined)."""
+    wb, ns = int(elem_bits) // 8, max(1, int(n_shards))
+    _host_arg(src_host, "convert_host_shard src_host", (wb << A.in_bits) // ns)
+    _host_arg(dst_host, "convert_host_shard dst_host", (wb << B.in_bits) // ns)
+    _dev_arg(dev_src, "convert_host_shard dev_src", int(scratch_bytes))
+    _dev_arg(dev_dst, "convert_host_shard dev_dst", int(scratch_bytes))
     _check(_lib.ll_convert_host_shard(_ptr(src_host), A.handle, _ptr(dst_host), B.handle,
                                       int(elem_bits), int(n_shards), int(shard), _ptr(dev_src),
                                       _ptr(dev_dst), int(scratch_bytes), _stream_handle(stream)))

@@ -755,6 +755,33 @@ def test_gather_host_argument_contract():
     assert e.value.name == "LL_ERR_ARG" and "scratch" in str(e.value)
 
 
+def test_binding_rejects_bad_host_buffer_arguments():
+    """The host-buffer entry points (ll_convert_host, ll_convert_host_shard,
+    ll_gather_host) check their torch arguments before the C call: host
+    buffers on the host and large enough, staging buffers on the device and
+    at least scratch_bytes (runs without a GPU)."""
+    import torch
+    import paper_2505_23819_b200 as ll
+    from workloads import configs
+    c = configs.cfg5(m_bits=8, kb_bits=8)
+    A, B = ll.Layout.from_spec(c["A"]), ll.Layout.from_spec(c["B"])
+    n = 1 << A.in_bits
+    src, dst = torch.zeros(n, dtype=torch.uint8), torch.zeros(n, dtype=torch.uint8)
+    with pytest.raises(ll.LLError, match="not on a CUDA device"):
+        ll.convert_host(src, A, dst, B, 8, 1, torch.zeros(64, dtype=torch.uint8),
+                        torch.zeros(64, dtype=torch.uint8), 64)
+    with pytest.raises(ll.LLError, match="dst_host: .* bytes <"):
+        ll.convert_host(src, A, dst[:-1], B, 8, 1, 0x1000, 0x2000, 64)
+    with pytest.raises(ll.LLError, match="src_host: .* bytes <"):
+        ll.convert_host_shard(src[: n // 4 - 1], A, dst, B, 8, 4, 1, 0x1000, 0x2000, 64)
+    g = configs.cfg4(r_bits=0)
+    L = ll.Layout.from_spec(g["L"])
+    m = 1 << L.in_bits
+    with pytest.raises(ll.LLError, match="idx_host: .* bytes <"):
+        ll.gather_host(torch.zeros(m, dtype=torch.float32), torch.zeros(m - 1, dtype=torch.int32),
+                       torch.zeros(m, dtype=torch.float32), L, g["axis"], 32, 1, 0x1000, 0x2000, 0x3000, 64)
+
+
 def test_binding_rejects_bad_tensor_arguments():
     """The C ABI takes bare pointers, so the binding checks torch tensors
     first (device, contiguity, element width, size) -- all before any launch,
