@@ -67,6 +67,8 @@ def parse(argv=None):
                          "workload")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-gather-scratch-mb", type=int, default=32,
+                    help="device staging per buffer for ll_gather_host")
     ap.add_argument("--e2e-scratch-mb", type=int, default=64,
                     help="device staging per side for ll_convert_host (2 slots of its 32 MiB chunks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -863,13 +865,14 @@ def run_e2e(ll, b, args, dev, world, rank, scaling, barrier, coll_dev):
         src_h = values_torch(n, 98, 4, "cpu").pin_memory()
         idx_h = indices_torch(n, 97, ct["idx_limit"], "cpu").pin_memory()
         out_h = torch.empty_like(src_h).pin_memory()
-        scratch = 32 << 20
+        scratch = args.e2e_gather_scratch_mb << 20
         dbuf = [torch.empty(scratch, dtype=torch.uint8, device=dev) for _ in range(3)]
         ms = timed(lambda: ll.gather_host(src_h, idx_h, out_h, Lt, ct["axis"], 32, nb, *dbuf,
                                           scratch, stream=stream))
         return {"value": world * b.nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": ms,
-                "api": "ll_gather_host (pinned host buffers, 16 MiB chunks, copy-in/compute/copy-out streams)"}
+                "api": "ll_gather_host (pinned host buffers, %d MiB device staging per buffer, copy-in/"
+                       "compute/copy-out streams)" % (scratch >> 20)}
     w = c["elem_bytes"]
     if b.upcast:
         # packed bytes + scales in, 2 GiB of bf16 out (copies, then the fused kernel)
