@@ -932,8 +932,8 @@ def run_e2e(ll, b, args, dev, world, rank, scaling, barrier, coll_dev):
                                        stream=stream))
     return {"value": world * b.nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": n * w, "d2h_bytes_per_step": n * w, "ms_per_step": ms,
-            "api": "ll_convert_host (pinned host buffers, %d MiB device staging per side, 32 MiB chunks, "
-                   "copy-in/compute/copy-out streams)" % (scratch >> 20)}
+            "api": "ll_convert_host (pinned host buffers, %d MiB device staging per side, 16-32 MiB "
+                   "chunks, copy-in/compute/copy-out streams)" % (scratch >> 20)}
 
 
 def multigpu_max(x, coll_dev):

@@ -412,7 +412,7 @@ ll_status ll_checksum(const void* buf, int64_t n_elems, int elem_bits, int index
 
 /* End-to-end conversion of HOST buffers: src_host/dst_host are host pointers
  * (pinned for full speed); the library pipelines host->device copies, the
- * conversion and device->host copies in chunks (~16 MiB: whole layout
+ * conversion and device->host copies in chunks (16-32 MiB: whole layout
  * instances, or shards of a single large instance -- contiguous in both
  * buffers, else contiguous in one and pitched in the other (ll_shard_describe_2d;
  * the pitched side is then staged whole in its scratch buffer and copied
@@ -499,7 +499,8 @@ int64_t ll_launch_count(void);
  *   tile order, "gather_auto_smem" (1: AUTO smem gather wherever it fits)
  * Register-faithful paths: "regs_matrix" (1) stmatrix / ldmatrix allowed,
  *   "regs_trans" (1) their .trans forms, "regs_shuffle_max_rounds" (4)
- * ll_convert_host: "host_chunk_mb" (default 32; ll_gather_host 16), "host_slots"
+ * ll_convert_host: "host_chunk_mb" (default: 32 for shards of one instance, 16
+ *   for whole instances and pitched shards; ll_gather_host 16), "host_slots"
  *   (default 2), "host_ramp" (default 0).
  * LL_ERR_ARG for an unknown name.  Used by the tuning sweeps. */
 ll_status ll_tune(const char* name, int value);

@@ -847,12 +847,17 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     const size_t sb = (size_t)w << src_layout->L.in_bits();
     const size_t db = (size_t)w << dst_layout->L.in_bits();
     const size_t unit = sb > db ? sb : db;
-    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 32)) << 20;
+    // chunk target (knob host_chunk_mb; default by chunk kind, measured:
+    // shards of one large instance 32 MiB -- config 5 92.8 vs 91.6 GB/s at
+    // 16 --, whole batched instances 16 MiB -- config 2 85 vs 81 at 32)
+    const int chunk_knob = ll::planner_knob("host_chunk_mb", 0);
+    const size_t target_sh = (size_t)(chunk_knob > 0 ? chunk_knob : 32) << 20;
+    const size_t target = (size_t)(chunk_knob > 0 ? chunk_knob : 16) << 20;
     const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 2)));
     // chunking: whole layout instances (batch elements), or -- for a single
     // large instance -- shards (contiguous slices of both buffers)
     // (a chunk must also fit one slot of the caller's scratch)
-    const size_t cap = std::max<size_t>(1, std::min(target, scratch_bytes));
+    const size_t cap = std::max<size_t>(1, std::min(target_sh, scratch_bytes));
     int n_sh = 1;
     if (batch == 1 && unit > cap) {
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
@@ -871,10 +876,12 @@ ll_status ll_convert_host(const void* src_host, ll_layout src_layout, void* dst_
     // buffers (a transpose): shards contiguous on one side and a pitched
     // region of >= 1 KiB rows on the other, the pitched side staged whole in
     // its scratch buffer and copied with cudaMemcpy2DAsync
-    if (batch == 1 && unit > cap && n_sh == 1 && ll::planner_knob("host_2d", 1)) {
+    // (pitched shards keep the 16 MiB target: config 3 85 vs 79 GB/s at 32)
+    const size_t cap2d = std::max<size_t>(1, std::min(target, scratch_bytes));
+    if (batch == 1 && unit > cap2d && n_sh == 1 && ll::planner_knob("host_2d", 1)) {
       auto P = ll::get_convert_plan(src_layout->L, dst_layout->L, w, LL_PATH_AUTO, 1);
       int want = 2;
-      while ((unit / want) > cap && want < (1 << 12)) want *= 2;
+      while ((unit / want) > cap2d && want < (1 << 12)) want *= 2;
       for (int ns = want; ns > 1; ns /= 2) {
         int side = 0, r0 = 0;
         try {
@@ -1066,7 +1073,8 @@ ll_status ll_convert_host_shard(const void* src_host, ll_layout src_layout, void
     ll::shard_range(*P, n_shards, shard);   // throws if not shardable
     const size_t sb = (size_t)w << src_layout->L.in_bits(), db = (size_t)w << dst_layout->L.in_bits();
     const size_t slice = std::max(sb, db) / (size_t)n_shards;
-    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 32)) << 20;
+    const int chunk_knob = ll::planner_knob("host_chunk_mb", 0);   // <= 0: the default
+    const size_t target = (size_t)(chunk_knob > 0 ? chunk_knob : 32) << 20;
     const size_t cap = std::max<size_t>(1, std::min(target, scratch_bytes));
     // k sub-shards per shard: the smallest power of two whose chunks fit
     int k = 1;
@@ -1138,7 +1146,8 @@ ll_status ll_gather_host(const void* src_host, const int32_t* idx_host, void* ou
     const int64_t n = int64_t(1) << layout->L.in_bits();  // elements per instance
     const size_t ub = (size_t)std::max(w, 4) * n;       // the larger of value / index bytes
     if (scratch_bytes < ub) return fail(LL_ERR_ARG, "ll_gather_host: scratch smaller than one instance");
-    const size_t target = (size_t)std::max(1, ll::planner_knob("host_chunk_mb", 16)) << 20;
+    const int chunk_knob = ll::planner_knob("host_chunk_mb", 0);   // <= 0: the default
+    const size_t target = (size_t)(chunk_knob > 0 ? chunk_knob : 16) << 20;
     const int max_slots = std::max(1, std::min(HostPipe::kSlots, ll::planner_knob("host_slots", 2)));
     int64_t per_chunk = (int64_t)std::max<size_t>(1, target / ub);
     per_chunk = std::min<int64_t>(std::min<int64_t>(per_chunk, (int64_t)(scratch_bytes / ub)), batch);

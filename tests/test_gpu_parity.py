@@ -1192,7 +1192,7 @@ def test_convert_host_sharded_single_instance(ramp, chunk_mb):
         ll.convert_host(src_h, A, dst_h, B, 8, 1, ds, dd, scratch)
     finally:
         ll.tune("host_ramp", 0)
-        ll.tune("host_chunk_mb", 32)
+        ll.tune("host_chunk_mb", 0)
     exp = expect_convert(c, src_h.numpy())
     assert dst_h.numpy().tobytes() == exp.tobytes()
 
@@ -1220,7 +1220,7 @@ def test_convert_host_shard(n_shards, chunk_mb):
             ll.convert_host_shard(src_h, A, dst_h, B, 8, n_shards, r, ds, dd, scratch)
             parts.append((d0, dst_h.numpy().tobytes()))
     finally:
-        ll.tune("host_chunk_mb", 32)
+        ll.tune("host_chunk_mb", 0)
     assert b"".join(b for _, b in sorted(parts)) == exp.tobytes()
 
 
@@ -1241,7 +1241,7 @@ def test_convert_host_pitched_transpose(host_2d):
         ll.tune("host_2d", host_2d)
         ll.convert_host(src_h, A, dst_h, B, 16, 1, ds, dd, 2 * n)
     finally:
-        ll.tune("host_chunk_mb", 32)
+        ll.tune("host_chunk_mb", 0)
         ll.tune("host_2d", 1)
     exp = expect_convert(c, _np(src_h, 2))
     assert _np(dst_h, 2).tobytes() == exp.tobytes()
@@ -1264,7 +1264,7 @@ def test_gather_host_e2e():
         ll.tune("host_chunk_mb", 1)
         ll.gather_host(src_h, idx_h, out_h, L, c["axis"], 32, batch, *bufs, scratch)
     finally:
-        ll.tune("host_chunk_mb", 16)
+        ll.tune("host_chunk_mb", 0)
     src, idx, out = _np(src_h, 4), idx_h.numpy(), _np(out_h, 4)
     for b in range(batch):
         exp = oconv.gather_np(src[b * m:(b + 1) * m], idx[b * m:(b + 1) * m], _olayout(c["L"]), c["axis"])
