@@ -301,6 +301,16 @@ ll_status ll_gather_timed(const void* src, const int32_t* idx, void* out, ll_lay
                           int axis, int elem_bits, int path, int reps, long long* cycles,
                           ll_stream stream);
 
+/* The scale layout of the mxfp4 upcast:
+ * S = P o dst_layout, where dst_layout maps a destination byte's hardware
+ * index to its packed-tensor coordinate (m, kb) and P : (m, kb) -> (m, g =
+ * kb >> 4) is the projection onto the E8M0 scale tensor [M][K/32] (one scale
+ * per 16 packed bytes = 32 fp4 values) -- a linear layout whose columns for
+ * kb bits 0-3 are zero (the broadcast of one scale over its 16 bytes).  The
+ * upcast reads scales[flatten(S(h))] for destination byte h.  Caller owns
+ * *out; LL_ERR_SHAPE unless dst_layout has two output dims and >= 4 kb bits. */
+ll_status ll_mxfp4_scale_layout(ll_layout dst_layout, ll_layout* out);
+
 /* Fused mxfp4 dequantisation with the layout conversion (
  * "Software Emulation" / "Data Shuffling"; OCP MX):
  *   packed    u8 buffer in layout src_layout over (m, kb): byte (m, kb) holds

@@ -14,11 +14,11 @@ from ._lib import (LLError, Layout, broadcast, checksum, compose, convert, conve
                    convert_shard, jit_source, left_divide,
                    expand_dims, join, mxfp4_upcast, reshape, shard_describe, shard_describe_2d, gather_host, split, transpose, gather, gather_describe,
                    invert, launch_count, lib_path, plan_describe, product, tune, version, PATHS,
-                   gather_jit_source, gather_timed, slice_layout, blocked, mma_tile)
+                   gather_jit_source, gather_timed, slice_layout, blocked, mma_tile, mxfp4_scale_layout)
 
 __all__ = ["LLError", "Layout", "broadcast", "checksum", "compose", "convert", "convert_host", "convert_host_shard",
            "convert_regs_timed", "convert_shard", "jit_source", "left_divide",
            "expand_dims", "join", "mxfp4_upcast", "reshape", "split", "transpose",
            "shard_describe", "shard_describe_2d", "gather_host", "gather", "gather_describe",
            "invert", "launch_count", "lib_path", "plan_describe", "product", "tune", "version",
-           "PATHS", "gather_jit_source", "gather_timed", "slice_layout", "blocked", "mma_tile"]
+           "PATHS", "gather_jit_source", "gather_timed", "slice_layout", "blocked", "mma_tile", "mxfp4_scale_layout"]

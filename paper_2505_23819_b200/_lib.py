@@ -72,6 +72,7 @@ _lib.ll_broadcast.argtypes = [_VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_V
 _lib.ll_join.argtypes = [_VP, ctypes.c_char_p, ctypes.POINTER(_VP)]
 _lib.ll_split.argtypes = [_VP, ctypes.POINTER(_VP)]
 _lib.ll_slice.argtypes = [_VP, ctypes.c_int, ctypes.POINTER(_VP)]
+_lib.ll_mxfp4_scale_layout.argtypes = [_VP, ctypes.POINTER(_VP)]
 _IP = ctypes.POINTER(ctypes.c_int)
 _lib.ll_blocked.argtypes = [ctypes.c_int, _IP, _IP, _IP, _IP, _IP, ctypes.POINTER(_VP)]
 _lib.ll_mma_tile.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(_VP)]
@@ -96,7 +97,7 @@ _lib.ll_gather_jit_source.argtypes = [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_
                                       ctypes.POINTER(ctypes.c_size_t)]
 _lib.ll_gather_timed.argtypes = [_VP, _VP, _VP, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_int, _VP, _VP]
-for _f in ("ll_slice", "ll_blocked", "ll_mma_tile", "ll_gather_jit_source", "ll_gather_timed", "ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
+for _f in ("ll_mxfp4_scale_layout", "ll_slice", "ll_blocked", "ll_mma_tile", "ll_gather_jit_source", "ll_gather_timed", "ll_jit_source", "ll_left_divide", "ll_convert_regs_timed", "ll_convert_inkernel_timed", "ll_mxfp4_upcast", "ll_checksum", "ll_transpose", "ll_reshape", "ll_expand_dims", "ll_broadcast", "ll_join", "ll_split",
            "ll_convert_shard", "ll_shard_describe", "ll_shard_describe_2d", "ll_gather_host", "ll_tune", "ll_layout_create", "ll_layout_destroy", "ll_layout_info", "ll_layout_get",
            "ll_compose", "ll_invert", "ll_product", "ll_apply", "ll_layout_props", "ll_convert",
            "ll_convert_ex", "ll_gather", "ll_gather_ex", "ll_convert_host", "ll_convert_host_shard", "ll_plan_describe",
@@ -298,6 +299,14 @@ def slice_layout(layout, axis):
     """ll_slice: sliced layout, output dim `axis` removed."""
     h = ctypes.c_void_p()
     _check(_lib.ll_slice(layout.handle, int(axis), ctypes.byref(h)))
+    return _wrap(h)
+
+
+def mxfp4_scale_layout(dst_layout):
+    """ll_mxfp4_scale_layout: the upcast's scale layout S = (m, kb -> m, kb >> 4)
+    o dst_layout (zero columns for kb bits 0-3)."""
+    h = ctypes.c_void_p()
+    _check(_lib.ll_mxfp4_scale_layout(dst_layout.handle, ctypes.byref(h)))
     return _wrap(h)
 
 

@@ -679,6 +679,26 @@ ll_status ll_convert_regs_timed(const void* src, ll_layout src_layout, void* dst
                                    LL_PATH_REGS, reps, cycles, stream);
 }
 
+ll_status ll_mxfp4_scale_layout(ll_layout dst_layout, ll_layout* out) {
+  return guarded([&]() -> ll_status {
+    check_layout(dst_layout, "ll_mxfp4_scale_layout");
+    if (!out) return fail(LL_ERR_ARG, "ll_mxfp4_scale_layout: NULL argument");
+    const ll::Layout& B = dst_layout->L;
+    if (B.out.size() != 2 || B.out[1].bits < 4)
+      return fail(LL_ERR_SHAPE, "ll_mxfp4_scale_layout: the layout must map to [m, kb] with >= 4 kb bits");
+    // the projection (m, kb) -> (m, kb >> 4): one E8M0 scale per 16 packed
+    // bytes (32 fp4 values) along K; kb bits 0-3 become zero columns
+    const int kbb = B.out[1].bits;
+    const ll::u64 kmask = (ll::u64(1) << kbb) - 1;
+    ll::Layout S;
+    S.in = B.in;
+    S.out = {ll::Dim{B.out[0].name, B.out[0].bits}, ll::Dim{"g", kbb - 4}};
+    for (ll::u64 c : B.cols) S.cols.push_back(((c >> kbb) << (kbb - 4)) | ((c & kmask) >> 4));
+    *out = wrap(std::move(S));
+    return LL_OK;
+  });
+}
+
 ll_status ll_mxfp4_upcast(const void* packed, ll_layout src_layout, const uint8_t* scales,
                           void* dst_bf16, ll_layout dst_layout, const ll_convert_options* opts,
                           ll_stream stream) {

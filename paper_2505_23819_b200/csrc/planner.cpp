@@ -231,7 +231,9 @@ u64 linop_apply_index(const std::array<int, 3>& op, u64 k) {
 }
 
 // mxfp4 upcast: scale-index contribution of destination (byte-layout) index
-// bit k, for scales stored row-major [M][K/32] = [M][KB/16]
+// bit k, for scales stored row-major [M][K/32] = [M][KB/16] -- column k of
+// the scale layout S = (m, kb -> m, kb >> 4) o B (ll_mxfp4_scale_layout),
+// flattened; zero for the kb bits 0-3 (one scale per 16 bytes)
 int64_t scale_contrib(const ConvertPlan& P, int k) {
   const u64 c = P.dst_cols[k];
   if (!c) return 0;

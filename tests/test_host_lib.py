@@ -844,3 +844,46 @@ def test_gather_kernels_compile_for_random_layouts(w):
                 assert r["compiled"] and r["cubin_bytes"] > 0
             seen.add(path)
     assert seen == {"shuffle", "smem"}
+
+
+def test_mxfp4_scale_layout_matches_the_oracle_scale_index():
+    """ll_mxfp4_scale_layout (the scale layout with zero
+    columns): S(h), flattened row-major over [M][K/32], equals the scale index
+    the oracle's upcast uses for destination byte h (m * K/32 + (kb >> 4),
+    oracle/mxfp4.upcast_np, pinned to transformers' MXFP4 dequantisation), on
+    config 5's destination layout; kb bits 0-3 are zero columns."""
+    import numpy as np
+    import paper_2505_23819_b200 as ll
+    from oracle import convert as oconv
+    from oracle.layout import Layout as OL
+    from workloads import configs
+    c = configs.cfg5(m_bits=9, kb_bits=8)
+    B = ll.Layout.from_spec(c["B"])
+    S = ll.mxfp4_scale_layout(B)
+    sp = S.spec()
+    assert [tuple(d) for d in sp["out_dims"]] == [("m", 9), ("g", 4)]
+    Bo = OL(**c["B"])
+    kbb = 8
+    rng = np.random.default_rng(5)
+    hs = rng.integers(0, 1 << B.in_bits, 300)
+    x = oconv.apply_np(Bo.cols, hs)
+    want = (x >> kbb) * (1 << (kbb - 4)) + ((x & ((1 << kbb) - 1)) >> 4)
+    names = [d[0] for d in sp["in_dims"]]
+    sizes = [d[1] for d in sp["in_dims"]]
+    for h, wv in zip(hs, want):
+        coords, r = [], int(h)
+        for b in sizes:
+            coords.append(r & ((1 << b) - 1))
+            r >>= b
+        m, g = S.apply(coords)
+        assert m * 16 + g == wv, (h, names)
+    # the broadcast: destination bits whose packed coordinate is a kb bit < 4
+    # map to nothing in the scale tensor
+    Bcols = Bo.cols
+    for k, col in enumerate(Bcols):
+        coords, r = [], 1 << k
+        for b in sizes:
+            coords.append(r & ((1 << b) - 1))
+            r >>= b
+        zero = col < 16   # kb bits 0-3 (kb is the fastest dim)
+        assert (S.apply(coords) == (0, 0)) == zero, k
