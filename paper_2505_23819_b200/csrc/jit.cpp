@@ -251,16 +251,21 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
   // tile (as the smem kernel, pdl_prefetch)
   if (planner_knob("shuffle_pdl", 1)) {
     if (planner_knob("pdl_prefetch", 1)) {
-      o << "  { const long long t = t0 + gid; if (t < t1 && blockIdx.x < pf_ctas) {\n"
-        << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
-        << "    long long so = inst * tm.bss;\n";
-      for (int k = 0; k < p.tile.n_tab; ++k)
-        o << "    so += tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
-          << ((1 << LL_TAB_BITS) - 1) << ")].src;\n";
-      for (int u = 0; u < NV; ++u)
-        o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
-          << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
-      o << "  } }\n";
+      // knob shuffle_prefetch_waves = K: also the tiles of the warps that
+      // replace this one in waves 2..K (8 warps per CTA)
+      const int pfk = std::max(1, std::min(4, planner_knob("shuffle_prefetch_waves", 1)));
+      for (int kw = 0; kw < pfk; ++kw) {
+        o << "  { const long long t = t0 + gid + " << kw << "LL * pf_ctas * 8; if (t < t1 && blockIdx.x < pf_ctas) {\n"
+          << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
+          << "    long long so = inst * tm.bss;\n";
+        for (int k = 0; k < p.tile.n_tab; ++k)
+          o << "    so += tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
+            << ((1 << LL_TAB_BITS) - 1) << ")].src;\n";
+        for (int u = 0; u < NV; ++u)
+          o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
+            << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
+        o << "  } }\n";
+      }
     }
     o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
       << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
