@@ -500,7 +500,8 @@ int64_t ll_launch_count(void);
  * Session-3 knobs: "pdl_prefetch" (1: the first wave of the
  *   compiled smem kernel prefetches its first tile's source into L2 before
  *   griddepcontrol.wait; 2: every CTA; 0: off), "pdl_prefetch_waves" (2:
- *   also the tiles of the CTAs replacing it in wave 2), "pdl_prefetch_short" (0),
+ *   also the tiles of the CTAs replacing it in wave 2; "shuffle_prefetch_waves" (3)
+ *   the same for the shuffle kernel), "pdl_prefetch_short" (0),
  *   "shuffle_pdl" (1) / "gather_pdl" (1) / "upcast_pdl" (0) programmatic
  *   dependent launch of those kernels, "regperm_prefetch" (0),
  *   "auto_regperm_shuffle" (1: AUTO takes the warp-shuffle exchange over the

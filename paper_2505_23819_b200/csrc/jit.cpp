@@ -251,9 +251,10 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
   // tile (as the smem kernel, pdl_prefetch)
   if (planner_knob("shuffle_pdl", 1)) {
     if (planner_knob("pdl_prefetch", 1)) {
-      // knob shuffle_prefetch_waves = K: also the tiles of the warps that
-      // replace this one in waves 2..K (8 warps per CTA)
-      const int pfk = std::max(1, std::min(4, planner_knob("shuffle_prefetch_waves", 1)));
+      // knob shuffle_prefetch_waves = K (default 3): also the tiles of the
+      // warps that replace this one in waves 2..K (8 warps per CTA); config
+      // 6: 6765 -> 6795 (K = 2) -> 6819 GB/s (K = 3), profiles/r02/s3y
+      const int pfk = std::max(1, std::min(4, planner_knob("shuffle_prefetch_waves", 3)));
       for (int kw = 0; kw < pfk; ++kw) {
         o << "  { const long long t = t0 + gid + " << kw << "LL * pf_ctas * 8; if (t < t1 && blockIdx.x < pf_ctas) {\n"
           << "    const long long inst = t >> tm.n_bits, r = t & rmask;\n"
