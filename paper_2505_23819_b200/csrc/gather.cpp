@@ -363,6 +363,7 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
     << "    const unsigned char* __restrict__ src, const int* __restrict__ idx,\n"
     << "    unsigned char* __restrict__ out, long long n_units, int* err, int check";
   if (timed) o << ", int reps, long long* cycles";
+  else o << ", long long pf_ctas";
   o << ") {\n"
     << "  extern __shared__ __align__(128) unsigned char smem[];\n"
     << "  const int tid = threadIdx.x;\n"
@@ -387,6 +388,20 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
        ":: \"r\"(st + " << UB << "u), \"l\"(idx + (t << " << CU << ")), \"r\"(" << IB << "u), \"r\"(bar) : \"memory\");\n"
     << "  };\n"
     << "  const long long g0 = blockIdx.x, gs = gridDim.x;\n";
+  // first-wave L2 prefetch of the units of this CTA and the CTAs replacing
+  // it in waves 2..K (knob gather_prefetch_waves; one bulk prefetch per
+  // unit's source and indices) before the PDL wait, as the smem conversion
+  const int gpk = std::max(0, std::min(4, planner_knob("gather_prefetch_waves", 0)));
+  if (!timed && planner_knob("gather_pdl", 1) && gpk > 0) {
+    o << "  if (tid == 0 && blockIdx.x < pf_ctas) {\n";
+    for (int k = 0; k < gpk; ++k)
+      o << "    { const long long t = g0 + " << k << "LL * pf_ctas; if (t < n_units) {\n"
+        << "      asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(src + (t << " << CU << ") * " << W
+        << "), \"r\"(" << UB << "u) : \"memory\");\n"
+        << "      asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(idx + (t << " << CU
+        << ")), \"r\"(" << IB << "u) : \"memory\"); } }\n";
+    o << "  }\n";
+  }
   if (!timed && planner_knob("gather_pdl", 1))   // programmatic dependent launch (knob gather_pdl)
     o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
       << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
@@ -520,8 +535,15 @@ cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const in
   const void* s = src;
   const int32_t* ix = idx;
   void* d = out;
-  void* args[] = {(void*)&s, (void*)&ix, (void*)&d, (void*)&nu, (void*)&ef, (void*)&check,
-                  (void*)&reps, (void*)&cycles};
+  long long pf = 0;
+  if (!shfl && !timed && planner_knob("gather_prefetch_waves", 0) > 0)
+    pf = jit_first_wave_ctas(fn, 256, (int)smem);
+  void* args_t[] = {(void*)&s, (void*)&ix, (void*)&d, (void*)&nu, (void*)&ef, (void*)&check,
+                    (void*)&reps, (void*)&cycles};
+  // the non-timed smem gather takes pf_ctas after check (the shuffle gather
+  // reads the first six only)
+  void* args_s[] = {(void*)&s, (void*)&ix, (void*)&d, (void*)&nu, (void*)&ef, (void*)&check, (void*)&pf};
+  void** args = (!shfl && !timed) ? args_s : args_t;
   return jit_launch(fn, (unsigned)grid, 256, smem, st, args, err,
                     !timed && planner_knob("gather_pdl", 1) != 0);
 }

@@ -88,6 +88,9 @@ std::string stg_asm(const std::string& vt, const std::string& regs) {
 // the first wave, the only CTAs PDL can start during the preceding grid
 long long first_wave_ctas(CUfunction fn, int block, int smem, int sms) {
   static PFN_Occupancy occ = entry<PFN_Occupancy>("cuOccupancyMaxActiveBlocksPerMultiprocessor");
+  static PFN_FuncSetAttribute setattr_ = entry<PFN_FuncSetAttribute>("cuFuncSetAttribute");
+  // the occupancy query needs the kernel's dynamic shared-memory limit raised first
+  if (smem > 48 * 1024 && setattr_) setattr_(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
   static std::mutex occ_mu;
   static std::map<std::pair<CUfunction, int>, int> occ_cache;
   std::lock_guard<std::mutex> lk(occ_mu);
@@ -829,6 +832,14 @@ cudaError_t get_kernel(const std::string& src, CUfunction* fn, std::string* err,
 }
 
 }  // namespace
+
+// First-wave CTA count of a compiled kernel (for gather.cpp's prefetch).
+long long jit_first_wave_ctas(void* fn, int block, int smem) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return first_wave_ctas((CUfunction)fn, block, smem, sms);
+}
 
 // Compile (cached per source) and fetch a kernel of a generated source; the
 // gather kernels (gather.cpp) use these too.

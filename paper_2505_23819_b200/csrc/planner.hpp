@@ -179,6 +179,7 @@ cudaError_t launch_regs_shuffle(const RegsShufflePlan& p, int w, const void* src
 
 // jit.cpp: compile (cached) / launch a generated kernel (driver API)
 cudaError_t jit_kernel(const std::string& src, const char* name, void** fn, std::string* err);
+long long jit_first_wave_ctas(void* fn, int block, int smem);
 cudaError_t jit_launch(void* fn, unsigned grid, unsigned block, unsigned smem, cudaStream_t st,
                        void** args, std::string* err, bool pdl = false);
 
