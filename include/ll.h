@@ -502,7 +502,8 @@ int64_t ll_launch_count(void);
  *   griddepcontrol.wait; 2: every CTA; 0: off), "pdl_prefetch_waves" (2:
  *   also the tiles of the CTAs replacing it in wave 2; "shuffle_prefetch_waves" (3)
  *   the same for the shuffle kernel), "pdl_prefetch_short" (0),
- *   "shuffle_pdl" (1) / "gather_pdl" (1) / "upcast_pdl" (0) programmatic
+ *   "gather_prefetch_waves" (1: the smem gather's first wave bulk-prefetches its
+ *   units), "shuffle_pdl" (1) / "gather_pdl" (1) / "upcast_pdl" (0) programmatic
  *   dependent launch of those kernels, "regperm_prefetch" (0),
  *   "auto_regperm_shuffle" (1: AUTO takes the warp-shuffle exchange over the
  *   register permutation where it applies), "ld_hint" / "st_hint" (0: global

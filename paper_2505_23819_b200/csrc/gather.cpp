@@ -389,9 +389,11 @@ std::string gather_smem_source(const GatherPlanHost& P, int timed) {
     << "  };\n"
     << "  const long long g0 = blockIdx.x, gs = gridDim.x;\n";
   // first-wave L2 prefetch of the units of this CTA and the CTAs replacing
-  // it in waves 2..K (knob gather_prefetch_waves; one bulk prefetch per
-  // unit's source and indices) before the PDL wait, as the smem conversion
-  const int gpk = std::max(0, std::min(4, planner_knob("gather_prefetch_waves", 0)));
+  // it in waves 2..K (knob gather_prefetch_waves, default 1; one bulk
+  // prefetch per unit's source and indices) before the PDL wait, as the smem
+  // conversion: config 4 6689 -> 6770 GB/s, the full axis 6550 -> 6853
+  // (profiles/r02/s3z; K = 2, 3 lose part of it)
+  const int gpk = std::max(0, std::min(4, planner_knob("gather_prefetch_waves", 1)));
   if (!timed && planner_knob("gather_pdl", 1) && gpk > 0) {
     o << "  if (tid == 0 && blockIdx.x < pf_ctas) {\n";
     for (int k = 0; k < gpk; ++k)
@@ -536,7 +538,7 @@ cudaError_t launch_gather_jit(const GatherPlanHost& P, const void* src, const in
   const int32_t* ix = idx;
   void* d = out;
   long long pf = 0;
-  if (!shfl && !timed && planner_knob("gather_prefetch_waves", 0) > 0)
+  if (!shfl && !timed && planner_knob("gather_prefetch_waves", 1) > 0)
     pf = jit_first_wave_ctas(fn, 256, (int)smem);
   void* args_t[] = {(void*)&s, (void*)&ix, (void*)&d, (void*)&nu, (void*)&ef, (void*)&check,
                     (void*)&reps, (void*)&cycles};

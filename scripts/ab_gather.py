@@ -17,11 +17,11 @@ from workloads.values import indices_torch, values_torch  # noqa: E402
 VARIANTS = [("auto", {}), ("generic", {}), ("smem", {}), ("smem", {"gather_smem_upc": 0}),
             ("smem", {"gather_smem_upc": 2}), ("smem", {"gather_smem_upc": 4}), ("shuffle", {}),
             ("shuffle", {"gather_shfl_waves": 8}), ("shuffle", {"gather_shfl_waves": 16})]
-DEFAULTS = {"gather_smem_upc": 1, "gather_shfl_waves": -1, "gather_pdl": 1, "gather_prefetch_waves": 0}
+DEFAULTS = {"gather_smem_upc": 1, "gather_shfl_waves": -1, "gather_pdl": 1, "gather_prefetch_waves": 1}
 if len(sys.argv) > 1 and sys.argv[1] == "pdl":   # programmatic dependent launch A/B
     VARIANTS = [(p, kn) for p in ("auto", "generic", "smem", "shuffle") for kn in ({}, {"gather_pdl": 0})]
 if len(sys.argv) > 1 and sys.argv[1] == "prefetch":   # smem gather: first-wave bulk prefetch
-    VARIANTS = [("smem", kn) for kn in ({}, {"gather_prefetch_waves": 1}, {"gather_prefetch_waves": 2},
+    VARIANTS = [("smem", kn) for kn in ({}, {"gather_prefetch_waves": 0}, {"gather_prefetch_waves": 2},
                                         {"gather_prefetch_waves": 3})]
 
 

@@ -807,13 +807,13 @@ def test_gather_compiled_paths_configs(path, variant):
 
 @pytest.mark.parametrize("path,knobs", [("smem", {"gather_smem_upc": 0}), ("smem", {"gather_smem_upc": 3}),
                                          ("shuffle", {"gather_shfl_waves": 8}), ("shuffle", {"gather_shfl_waves": 1}),
-                                         ("smem", {"gather_prefetch_waves": 2}), ("smem", {"gather_prefetch_waves": 4}),
+                                         ("smem", {"gather_prefetch_waves": 0}), ("smem", {"gather_prefetch_waves": 4}),
                                          ("smem", {"gather_prefetch_waves": 2, "gather_smem_upc": 0})])
 def test_gather_launch_shapes(path, knobs):
     """The compiled gathers' launch shapes (one pass by default; persistent /
     several units per CTA / grid-stride) on config 4 and its full-axis
     variant, byte-exact."""
-    defaults = {"gather_smem_upc": 1, "gather_shfl_waves": -1, "gather_prefetch_waves": 0}
+    defaults = {"gather_smem_upc": 1, "gather_shfl_waves": -1, "gather_prefetch_waves": 1}
     for k, v in knobs.items():
         ll.tune(k, v)
     try:
