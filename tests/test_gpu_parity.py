@@ -426,7 +426,7 @@ def test_convert_tma_kernel_variants(path, knobs):
                                    {"tile_order": 2}, {"tile_order": 12}, {"tile_order": 23},
                                    {"pdl_prefetch": 0}, {"pdl_prefetch": 2}, {"smem_jit_tpg": 0},
                                    {"tile_xor": 2}, {"tile_xor": 6}, {"tile_xor": 4, "tile_xor_skip": 0},
-                                   {"pdl_prefetch_waves": 3}, {"pdl_prefetch_waves": 1}])
+                                   {"pdl_prefetch_waves": 3}, {"pdl_prefetch_waves": 1}, {"pdl_prefetch_bulk": 1}])
 def test_convert_smem_kernel_hint_and_order_knobs(knobs):
     """The compiled smem kernel under the cache-hint ablation (ld_hint /
     st_hint change only the global instructions' qualifiers) and the tile
