@@ -265,9 +265,12 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
         for (int k = 0; k < p.tile.n_tab; ++k)
           o << "    so += tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
             << ((1 << LL_TAB_BITS) - 1) << ")].src;\n";
+        const bool sbulk = planner_knob("shuffle_prefetch_bulk", 0) != 0;   // as pdl_prefetch_bulk
         for (int u = 0; u < NV; ++u)
           o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
-            << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(a_)); }\n";
+            << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\""
+            << (sbulk ? "cp.async.bulk.prefetch.L2.global [%0], 128;" : "prefetch.global.L2 [%0];")
+            << "\" :: \"l\"(a_)); }\n";
         o << "  } }\n";
       }
     }
@@ -569,9 +572,12 @@ std::string smem_hbm_source(const ConvertPlan& P, bool single) {
     for (int k = 0; k < pfk; ++k) {
       o << "  { const long long tp = t0 + gid + " << k << "LL * pf_ctas * " << (8 >> gw) << "; if (tp < t1"
         << (planner_knob("pdl_prefetch", 1) == 2 ? "" : " && blockIdx.x < pf_ctas") << ") { tile_off(tp);\n";
-      // knob pdl_prefetch_bulk: the same lines through the bulk-copy engine
-      // (cp.async.bulk.prefetch.L2, 128 B) instead of prefetch.global.L2
-      const bool bulk = planner_knob("pdl_prefetch_bulk", 0) != 0;
+      // knob pdl_prefetch_bulk (default 1): the same lines through the
+      // bulk-copy engine (cp.async.bulk.prefetch.L2, 128 B) instead of
+      // prefetch.global.L2 -- config 3 6270 -> 6464 GB/s, config 2 6889 ->
+      // 6914, config 5 unchanged, config 5's N = 8 shard 6936
+      // (profiles/r02/s3aa)
+      const bool bulk = planner_knob("pdl_prefetch_bulk", 1) != 0;
       for (int u = 0; u < NV; ++u)
         o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
           << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\""

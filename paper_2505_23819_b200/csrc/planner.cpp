@@ -165,7 +165,7 @@ bool set_planner_knob(const std::string& name, int value) {
       name != "ld_hint" && name != "st_hint" && name != "pdl_prefetch" && name != "gather_pdl" &&
       name != "shuffle_pdl" && name != "regperm_prefetch" &&
       name != "auto_regperm_shuffle" && name != "pdl_prefetch_short" && name != "upcast_pdl" &&
-      name != "tile_xor" && name != "tile_xor_skip" && name != "host_ramp" && name != "pdl_prefetch_waves" && name != "shuffle_prefetch_waves" && name != "gather_prefetch_waves" && name != "pdl_prefetch_bulk")
+      name != "tile_xor" && name != "tile_xor_skip" && name != "host_ramp" && name != "pdl_prefetch_waves" && name != "shuffle_prefetch_waves" && name != "gather_prefetch_waves" && name != "pdl_prefetch_bulk" && name != "shuffle_prefetch_bulk")
     return false;
   std::lock_guard<std::mutex> lk(g_knob_mu);
   g_knobs[name] = value;

@@ -426,7 +426,7 @@ def test_convert_tma_kernel_variants(path, knobs):
                                    {"tile_order": 2}, {"tile_order": 12}, {"tile_order": 23},
                                    {"pdl_prefetch": 0}, {"pdl_prefetch": 2}, {"smem_jit_tpg": 0},
                                    {"tile_xor": 2}, {"tile_xor": 6}, {"tile_xor": 4, "tile_xor_skip": 0},
-                                   {"pdl_prefetch_waves": 3}, {"pdl_prefetch_waves": 1}, {"pdl_prefetch_bulk": 1}])
+                                   {"pdl_prefetch_waves": 3}, {"pdl_prefetch_waves": 1}, {"pdl_prefetch_bulk": 0}])
 def test_convert_smem_kernel_hint_and_order_knobs(knobs):
     """The compiled smem kernel under the cache-hint ablation (ld_hint /
     st_hint change only the global instructions' qualifiers) and the tile
@@ -448,7 +448,7 @@ def test_convert_smem_kernel_hint_and_order_knobs(knobs):
             assert _np(dst, w).tobytes() == expect_convert(c, _np(src, w), batch).tobytes(), knobs
     finally:
         for k in knobs:
-            ll.tune(k, {"smem_jit_tpg": 1, "pdl_prefetch": 1, "tile_xor_skip": 1, "pdl_prefetch_waves": 2}.get(k, 0))
+            ll.tune(k, {"smem_jit_tpg": 1, "pdl_prefetch": 1, "tile_xor_skip": 1, "pdl_prefetch_waves": 2, "pdl_prefetch_bulk": 1}.get(k, 0))
 
 
 def test_convert_shard_with_tile_xor():
@@ -492,7 +492,8 @@ def test_convert_register_permutation_prefetch(w):
 
 
 @pytest.mark.parametrize("knobs", [{}, {"shuffle_pdl": 0}, {"pdl_prefetch": 0}, {"pdl_prefetch": 2},
-                                   {"shuffle_prefetch_waves": 2}, {"shuffle_prefetch_waves": 1}, {"shuffle_prefetch_waves": 4}])
+                                   {"shuffle_prefetch_waves": 2}, {"shuffle_prefetch_waves": 1}, {"shuffle_prefetch_waves": 4},
+                                   {"shuffle_prefetch_bulk": 1}])
 def test_convert_shuffle_kernel_pdl(knobs):
     """The compiled HBM shuffle kernel launched with programmatic dependent
     launch (griddepcontrol.wait first) and the first wave's L2 prefetch:
