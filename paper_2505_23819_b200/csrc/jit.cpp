@@ -265,7 +265,7 @@ std::string shuffle_hbm_source(const ConvertPlan& P) {
         for (int k = 0; k < p.tile.n_tab; ++k)
           o << "    so += tm.tab[" << k << "][(int)((r >> " << k * LL_TAB_BITS << ") & "
             << ((1 << LL_TAB_BITS) - 1) << ")].src;\n";
-        const bool sbulk = planner_knob("shuffle_prefetch_bulk", 0) != 0;   // as pdl_prefetch_bulk
+        const bool sbulk = planner_knob("shuffle_prefetch_bulk", 1) != 0;   // as pdl_prefetch_bulk (config 6: 6818 -> 6929, s3bb)
         for (int u = 0; u < NV; ++u)
           o << "    { const unsigned char* a_ = sthr + so + " << p.ld_vec[u]
             << "u; if ((((unsigned long long)a_) & 127ull) == 0) asm volatile(\""

@@ -22,7 +22,7 @@ from workloads.values import values_torch  # noqa: E402
 # the knobs' defaults (planner.cpp / jit.cpp)
 DEFAULTS = {"vec32": 0, "smem_jit_minb": 0, "smem_jit_tpg": 1, "pdl": 1, "smem_jit_single": 0,
             "smem_jit_depth": 1, "run_bytes": 256, "thread_bytes": 64, "tile_order": 0, "auto_asym": 1,
-            "ld_hint": 0, "st_hint": 0, "run_bytes_dst": 0, "run_bytes_src": 0, "tmaj_tpc": 2, "pdl_prefetch": 1, "shuffle_pdl": 1, "tile_xor": 0, "tile_xor_skip": 1, "pdl_prefetch_waves": 2, "max_granule": 16, "shuffle_prefetch_waves": 3, "pdl_prefetch_bulk": 1, "shuffle_prefetch_bulk": 0}
+            "ld_hint": 0, "st_hint": 0, "run_bytes_dst": 0, "run_bytes_src": 0, "tmaj_tpc": 2, "pdl_prefetch": 1, "shuffle_pdl": 1, "tile_xor": 0, "tile_xor_skip": 1, "pdl_prefetch_waves": 2, "max_granule": 16, "shuffle_prefetch_waves": 3, "pdl_prefetch_bulk": 1, "shuffle_prefetch_bulk": 1}
 
 
 def main():

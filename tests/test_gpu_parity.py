@@ -493,7 +493,7 @@ def test_convert_register_permutation_prefetch(w):
 
 @pytest.mark.parametrize("knobs", [{}, {"shuffle_pdl": 0}, {"pdl_prefetch": 0}, {"pdl_prefetch": 2},
                                    {"shuffle_prefetch_waves": 2}, {"shuffle_prefetch_waves": 1}, {"shuffle_prefetch_waves": 4},
-                                   {"shuffle_prefetch_bulk": 1}])
+                                   {"shuffle_prefetch_bulk": 0}])
 def test_convert_shuffle_kernel_pdl(knobs):
     """The compiled HBM shuffle kernel launched with programmatic dependent
     launch (griddepcontrol.wait first) and the first wave's L2 prefetch:
@@ -517,7 +517,7 @@ def test_convert_shuffle_kernel_pdl(knobs):
             assert _np(back, w).tobytes() == _np(src, w).tobytes(), knobs
     finally:
         for k in knobs:
-            ll.tune(k, {"pdl_prefetch": 1, "shuffle_pdl": 1, "shuffle_prefetch_waves": 3}.get(k, 0))
+            ll.tune(k, {"pdl_prefetch": 1, "shuffle_pdl": 1, "shuffle_prefetch_waves": 3, "shuffle_prefetch_bulk": 1}.get(k, 0))
 
 
 @pytest.mark.parametrize("swz", [0, 1, 2, 3])
